@@ -198,7 +198,7 @@ def test_new_ops_definitions():
     assert qmin[0, 1, 1] == q[:2, 2:, 2:].min() and qmax[0, 1, 1] == q[:2, 2:, 2:].max()
     assert O.threshold_count(q, 0.5, 2, 10.0) == 3  # regions (0,0,0),(0,0,1),(0,1,0)
     g = O.gradient_magnitude(q, 0.5)
-    assert g[1, 1, 1] == 0.0  # axis-0 boundary layer
+    assert g[1, 1, 1] == pytest.approx(0.5 * np.sqrt(8**2 + 2**2))  # D0 = 0 (axis 0 has 2 layers)
     q2 = np.arange(16, dtype=np.int32).reshape(4, 4)
     g2 = O.gradient_magnitude(q2, 0.5)
     assert g2[1, 1] == pytest.approx(0.5 * np.sqrt(8**2 + 2**2))
