@@ -1,0 +1,118 @@
+"""Regional statistics, threshold counts and gradient magnitude (SURVEY §8(a) N2–N5).
+
+Not in the reference (SPEC.md:340 lists regional statistics as a non-goal;
+PAPER.md:51,165-168 motivates them).  Definitions, pinned by the oracle
+(oracle/hsz_oracle.py: region_stats, region_minmax, threshold_count,
+gradient_magnitude):
+
+* regions tile the grid like ``grid.partition`` (origin-aligned, edge regions
+  shrunk, row-major region order); the extent is clipped to the grid;
+* per region exact S1 = sum(q), S2 = sum(q^2) (int128), qmin, qmax;
+  mean_r = S1/size*2eps, var_r = (size*S2 - S1^2)/(size(size-1))*(2eps)^2
+  (NaN below two points); min_r = qmin*2eps, max_r = qmax*2eps;
+* threshold count = #regions with min_r < tau <= max_r;
+* gradient magnitude = eps*sqrt(sum_k D_k^2) with D_k the integer central
+  differences of fields._axis_central_diff.
+
+One K-REG pass computes every per-region integer; one small kernel
+finalises the floats and the count.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .. import _lib, device as devmod
+from ..compressors import CompressedStream
+from ..stages import Stage, _check_stage, count_stage_work
+
+
+@dataclass(frozen=True)
+class RegionStats:
+    region: tuple
+    grid: tuple          # regions per axis
+    s1: np.ndarray       # int64
+    s2: np.ndarray       # Python ints (object) — exact int128
+    qmin: np.ndarray     # int32
+    qmax: np.ndarray     # int32
+    size: np.ndarray     # int64
+    mean: np.ndarray     # float64
+    var: np.ndarray      # float64
+    vmin: np.ndarray     # float64 = qmin * 2eps
+    vmax: np.ndarray     # float64 = qmax * 2eps
+    threshold: float | None = None
+    crossing_count: int | None = None
+
+
+def _region_tuple(region, nd):
+    return (int(region),) * nd if np.isscalar(region) else tuple(int(r) for r in region)
+
+
+def region_reduce_device(q_dev, eps: float, region, tau: float = float("nan")):
+    """Device-side per-region reduction + finalisation; returns CUDA tensors."""
+    t = _lib.torch()
+    nd = q_dev.dim()
+    reg = _region_tuple(region, nd)
+    grid, s1, s2lo, s2hi, qmin, qmax, size = devmod.region_reduce(q_dev, reg)
+    nr = s1.numel()
+    dev = _lib.device()
+    mean = t.empty(nr, dtype=t.float64, device=dev)
+    var = t.empty(nr, dtype=t.float64, device=dev)
+    fmin = t.empty(nr, dtype=t.float64, device=dev)
+    fmax = t.empty(nr, dtype=t.float64, device=dev)
+    count = t.zeros(1, dtype=t.int64, device=dev)
+    _lib.call("hszg_region_finalize", _lib.ptr(s1), _lib.ptr(s2lo), _lib.ptr(s2hi), _lib.ptr(qmin), _lib.ptr(qmax),
+              _lib.ptr(size), nr, 2.0 * eps, float(tau), _lib.ptr(mean), _lib.ptr(var), _lib.ptr(fmin),
+              _lib.ptr(fmax), _lib.ptr(count), _lib.stream_handle())
+    return dict(grid=grid, region=tuple(min(r, n) for r, n in zip(reg, q_dev.shape)), s1=s1, s2lo=s2lo, s2hi=s2hi,
+                qmin=qmin, qmax=qmax, size=size, mean=mean, var=var, vmin=fmin, vmax=fmax, count=count)
+
+
+def _quantized(c: CompressedStream, stage: Stage):
+    stage = Stage(stage)
+    if stage not in (Stage.DECORRELATED, Stage.QUANTIZED):
+        raise ValueError("regional statistics run on stage 2 or 3 integers")
+    _check_stage(c, stage)
+    count_stage_work(c, stage)
+    t = _lib.torch()
+    return c.device().reconstruct(t.int32)
+
+
+def region_stats(c: CompressedStream, region, stage: Stage = Stage.QUANTIZED,
+                 tau: float | None = None) -> RegionStats:
+    """Per-region mean/variance/min/max (N2, N3) and optionally the tau crossing count (N4)."""
+    q = _quantized(c, stage)
+    r = region_reduce_device(q, c.eps, region, float("nan") if tau is None else tau)
+    g = r["grid"]
+    s2 = [(int(h) << 64) | (int(l) & 0xFFFFFFFFFFFFFFFF) for h, l in zip(r["s2hi"].cpu().numpy(),
+                                                                         r["s2lo"].cpu().numpy())]
+    return RegionStats(
+        region=r["region"], grid=g,
+        s1=r["s1"].cpu().numpy().reshape(g),
+        s2=np.array(s2, dtype=object).reshape(g),
+        qmin=r["qmin"].cpu().numpy().reshape(g), qmax=r["qmax"].cpu().numpy().reshape(g),
+        size=r["size"].cpu().numpy().reshape(g),
+        mean=r["mean"].cpu().numpy().reshape(g), var=r["var"].cpu().numpy().reshape(g),
+        vmin=r["vmin"].cpu().numpy().reshape(g), vmax=r["vmax"].cpu().numpy().reshape(g),
+        threshold=tau, crossing_count=None if tau is None else int(r["count"].item()),
+    )
+
+
+def region_minmax(c: CompressedStream, region, stage: Stage = Stage.QUANTIZED):
+    """N3: (qmin, qmax, min_r, max_r) arrays shaped like the region grid."""
+    s = region_stats(c, region, stage)
+    return s.qmin, s.qmax, s.vmin, s.vmax
+
+
+def threshold_count(c: CompressedStream, region, tau: float, stage: Stage = Stage.QUANTIZED) -> int:
+    """N4: number of regions with min_r < tau <= max_r."""
+    return region_stats(c, region, stage, tau).crossing_count
+
+
+def gradient_magnitude(c: CompressedStream, stage: Stage = Stage.QUANTIZED, out: str = "numpy", out_dtype=None):
+    """N5: eps * sqrt(sum_k D_k^2) on the integer central differences."""
+    from .fields import compute_field_op
+
+    return compute_field_op(c, "gradient_magnitude", stage, out, out_dtype).components[0]

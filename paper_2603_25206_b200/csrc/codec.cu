@@ -1,0 +1,432 @@
+// codec.cu — chunk-stream validation, decode (stage 2) and encode (K-DEC / K-ENC).
+//
+// Byte layout of a chunk (reference _kernels/_fallback.py:1-8): byte 0 = bit
+// width b; if b > 0, ceil(count/8) sign bytes (bit j set = element j
+// negative, LSB-first) then the magnitudes packed LSB-first at b bits each,
+// zero-padded to a byte.  An all-zero chunk is the single byte 0.
+#include <cstdio>
+#include <cstring>
+#include "tile.cuh"
+#include "lookback.cuh"
+
+namespace hszg {
+
+// ---------------------------------------------------------------------------
+// per-chunk checks, in the order of the reference loop (_bitpack.pyx:106-140)
+
+enum { DEC_OK = 0, DEC_OFFSET = 1, DEC_BITWIDTH = 2, DEC_TRUNC = 3, DEC_MAG = 4, DEC_NEGZERO = 5 };
+
+__device__ __forceinline__ uint32_t gbyte(const uint8_t* p, uint64_t i) { return p[i]; }
+
+// full check of one chunk read straight from global memory; returns DEC_* and the element
+__device__ int check_chunk(const uint8_t* payload, uint64_t len, uint64_t off, int64_t count,
+                           int64_t* elem, int* bw_out) {
+    *elem = -1;
+    if (off >= len) return DEC_OFFSET;
+    const int bw = (int)gbyte(payload, off);
+    *bw_out = bw;
+    if (bw > 32) return DEC_BITWIDTH;
+    if (bw == 0) return DEC_OK;
+    const uint64_t sign_pos = off + 1;
+    const uint64_t mag_pos = sign_pos + (uint64_t)((count + 7) / 8);
+    const uint64_t end = mag_pos + (uint64_t)((count * bw + 7) / 8);
+    if (end > len) return DEC_TRUNC;
+    uint64_t acc = 0;
+    int nbits = 0;
+    uint64_t pos = mag_pos;
+    const uint64_t mask = (bw == 64) ? ~0ull : ((1ull << bw) - 1);
+    for (int64_t j = 0; j < count; j++) {
+        while (nbits < bw) {
+            acc |= (uint64_t)gbyte(payload, pos) << nbits;
+            pos++;
+            nbits += 8;
+        }
+        const uint64_t mag = acc & mask;
+        acc >>= bw;
+        nbits -= bw;
+        if (mag > 2147483647ull) { *elem = j; return DEC_MAG; }
+        const int neg = (gbyte(payload, sign_pos + (j >> 3)) >> (j & 7)) & 1;
+        if (neg && mag == 0) { *elem = j; return DEC_NEGZERO; }
+    }
+    return DEC_OK;
+}
+
+struct GeoSpans {
+    SegGeo sg;
+    __device__ __forceinline__ ChunkLoc get(int64_t c) const { return locate_chunk(sg, c); }
+};
+struct ArrSpans {
+    const int64_t* st;
+    const int64_t* en;
+    __device__ __forceinline__ ChunkLoc get(int64_t c) const {
+        ChunkLoc L;
+        L.start = st[c];
+        int64_t cnt = en[c] - st[c];
+        L.count = (int32_t)(cnt < 0 ? 0 : cnt);
+        L.seg = 0;
+        L.j = 0;
+        return L;
+    }
+};
+
+struct ValidateOut {
+    unsigned long long first_bad;   // min failing chunk (ULLONG_MAX = none)
+    unsigned long long noncanonical;
+    int max_bw;
+    int pad;
+};
+
+template <class Spans>
+__global__ void k_validate(Spans spans, int64_t n_chunks, const uint8_t* payload, uint64_t len,
+                           const uint64_t* offsets, ValidateOut* out) {
+    int local_max = 0;
+    unsigned long long nonc = 0;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n_chunks;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const ChunkLoc L = spans.get(c);
+        const uint64_t off = offsets[c];
+        int64_t elem;
+        int bw = 0;
+        const int r = check_chunk(payload, len, off, L.count, &elem, &bw);
+        if (r != DEC_OK) {
+            atomicMin(&out->first_bad, (unsigned long long)c);
+            continue;
+        }
+        local_max = max(local_max, bw);
+        if (L.count > kChunkCap) nonc++;
+        const uint64_t next = off + (uint64_t)chunk_bytes(L.count, bw);
+        if (c + 1 < n_chunks) {
+            if (offsets[c + 1] != next) nonc++;
+        }
+    }
+    // warp-aggregate to keep atomics cheap
+    for (int d = 16; d > 0; d >>= 1) {
+        local_max = max(local_max, __shfl_down_sync(0xffffffffu, local_max, d));
+        nonc += __shfl_down_sync(0xffffffffu, nonc, d);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (local_max) atomicMax(&out->max_bw, local_max);
+        if (nonc) atomicAdd(&out->noncanonical, nonc);
+    }
+}
+
+template <class Spans>
+__global__ void k_diagnose(Spans spans, const uint8_t* payload, uint64_t len, const uint64_t* offsets,
+                           int64_t c, int64_t* res) {
+    const ChunkLoc L = spans.get(c);
+    int64_t elem;
+    int bw = 0;
+    const uint64_t off = offsets[c];
+    res[0] = check_chunk(payload, len, off, L.count, &elem, &bw);
+    res[1] = elem;
+    res[2] = off < len ? (int64_t)payload[off] : -1;
+}
+
+// ---------------------------------------------------------------------------
+// stage-2 decode
+
+// canonical index: staged tiles, coalesced int32 stores
+__global__ void __launch_bounds__(TILE_CHUNKS) k_decode_tiles(SegGeo sg, const uint8_t* payload, uint64_t len,
+                                                             const uint64_t* offsets, int32_t* out) {
+    TileCtx t = tile_stage(sg, payload, len, offsets, blockIdx.x);
+    const int64_t c = t.c0 + threadIdx.x;
+    if (c < t.c1) {
+        const ChunkLoc L = locate_chunk(sg, c);
+        const int local = (int)(L.start - t.e0);
+        int32_t* vals = t.vals;
+        decode_chunk_words(t.words, (uint32_t)(offsets[c] - t.base), L.count,
+                           [&](int j, int32_t v) { vals[pad_idx(local + j)] = v; });
+    }
+    __syncthreads();
+    const int n = (int)(t.e1 - t.e0);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[t.e0 + i] = t.vals[pad_idx(i)];
+}
+
+// general path (non-canonical index or spans wider than 32): thread per chunk from global memory
+template <class Spans>
+__global__ void k_decode_direct(Spans spans, int64_t n_chunks, const uint8_t* payload, const uint64_t* offsets,
+                                int32_t* out) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n_chunks;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const ChunkLoc L = spans.get(c);
+        const uint64_t off = offsets[c];
+        const int bw = payload[off];
+        if (bw == 0) {
+            for (int j = 0; j < L.count; j++) out[L.start + j] = 0;
+            continue;
+        }
+        const uint64_t sign_pos = off + 1;
+        uint64_t bitpos = (sign_pos + (uint64_t)((L.count + 7) / 8)) * 8;
+        const uint64_t mask = bw == 32 ? 0xffffffffull : ((1ull << bw) - 1);
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(payload);
+        for (int j = 0; j < L.count; j++) {
+            const uint64_t wi = bitpos >> 5;
+            const uint32_t sh = (uint32_t)(bitpos & 31);
+            const uint32_t mag = __funnelshift_r(__ldg(w + wi), __ldg(w + wi + 1), sh) & (uint32_t)mask;
+            bitpos += bw;
+            const int neg = (payload[sign_pos + (j >> 3)] >> (j & 7)) & 1;
+            out[L.start + j] = neg ? -(int32_t)mag : (int32_t)mag;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// encode: per-chunk bit widths and byte sizes, exclusive scan, pack
+
+template <class Spans>
+__global__ void k_encode_sizes(Spans spans, int64_t n_chunks, const int32_t* vals, uint64_t* sizes,
+                               uint8_t* bws, unsigned long long* bad) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n_chunks;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const ChunkLoc L = spans.get(c);
+        uint32_t maxmag = 0;
+        bool neg_min = false;
+        for (int j = 0; j < L.count; j++) {
+            const int32_t v = vals[L.start + j];
+            if (v == INT32_MIN) neg_min = true;
+            const uint32_t m = v < 0 ? (uint32_t)(-(int64_t)v) : (uint32_t)v;
+            maxmag = m > maxmag ? m : maxmag;
+        }
+        if (neg_min) atomicMin(bad, (unsigned long long)c);
+        const int bw = maxmag ? 32 - __clz(maxmag) : 0;
+        bws[c] = (uint8_t)bw;
+        sizes[c] = (uint64_t)chunk_bytes(L.count, bw);
+    }
+}
+
+template <class Spans>
+__global__ void k_encode_pack(Spans spans, int64_t n_chunks, const int32_t* vals, const uint64_t* offsets,
+                              const uint8_t* bws, uint8_t* payload) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n_chunks;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const ChunkLoc L = spans.get(c);
+        const int bw = bws[c];
+        uint64_t pos = offsets[c];
+        payload[pos++] = (uint8_t)bw;
+        if (bw == 0) continue;
+        const int64_t sb = (L.count + 7) / 8;
+        for (int64_t k = 0; k < sb; k++) {
+            uint32_t byte = 0;
+            for (int b = 0; b < 8; b++) {
+                const int64_t j = k * 8 + b;
+                if (j < L.count && vals[L.start + j] < 0) byte |= 1u << b;
+            }
+            payload[pos + k] = (uint8_t)byte;
+        }
+        pos += sb;
+        uint64_t acc = 0;
+        int nbits = 0;
+        for (int j = 0; j < L.count; j++) {
+            const int32_t v = vals[L.start + j];
+            const uint64_t mag = v < 0 ? (uint64_t)(-(int64_t)v) : (uint64_t)v;
+            acc |= mag << nbits;
+            nbits += bw;
+            while (nbits >= 8) {
+                payload[pos++] = (uint8_t)(acc & 0xff);
+                acc >>= 8;
+                nbits -= 8;
+            }
+        }
+        if (nbits > 0) payload[pos++] = (uint8_t)(acc & 0xff);
+    }
+}
+
+}  // namespace hszg
+
+using namespace hszg;
+
+// ---------------------------------------------------------------------------
+// host helpers
+
+static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int hszg_set_cuda_error(HszgErr* err, cudaError_t e, const char* where) {
+    if (err) {
+        err->status = HSZG_CUDA;
+        snprintf(err->message, sizeof(err->message), "%s: %s", where, cudaGetErrorString(e));
+    }
+    return HSZG_CUDA;
+}
+
+#define HSZG_CHECK_LAUNCH(where)                                  \
+    do {                                                          \
+        cudaError_t _e = cudaGetLastError();                      \
+        if (_e != cudaSuccess) return hszg_set_cuda_error(err, _e, where); \
+    } while (0)
+
+static void set_decode_error(HszgErr* err, int kind, int64_t chunk, int64_t elem, int64_t bwv) {
+    err->status = HSZG_CORRUPT;
+    err->detail = kind;
+    err->chunk = chunk;
+    err->element = elem;
+    err->value = bwv;
+    switch (kind) {
+        case DEC_OFFSET: snprintf(err->message, sizeof(err->message), "chunk offset past end of payload"); break;
+        case DEC_BITWIDTH: snprintf(err->message, sizeof(err->message), "chunk bitwidth %lld exceeds 32", (long long)bwv); break;
+        case DEC_TRUNC: snprintf(err->message, sizeof(err->message), "truncated chunk payload"); break;
+        case DEC_MAG: snprintf(err->message, sizeof(err->message), "chunk magnitude exceeds int32 range"); break;
+        default: snprintf(err->message, sizeof(err->message), "negative zero in chunk"); break;
+    }
+}
+
+// workspace layout for validation: ValidateOut (32 B) + diag (3 x int64)
+template <class Spans>
+static int validate_impl(Spans spans, int64_t n_chunks, const uint8_t* payload, uint64_t len,
+                         const uint64_t* offsets, void* ws, size_t ws_bytes, cudaStream_t st, HszgErr* err,
+                         int* canonical, int* max_bw) {
+    if (ws_bytes < 64) {
+        err->status = HSZG_INVALID_ARG;
+        snprintf(err->message, sizeof(err->message), "workspace too small for validation");
+        return HSZG_INVALID_ARG;
+    }
+    ValidateOut* vo = reinterpret_cast<ValidateOut*>(ws);
+    int64_t* diag = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(ws) + 32);
+    ValidateOut init = {~0ull, 0ull, 0, 0};
+    cudaMemcpyAsync(vo, &init, sizeof(init), cudaMemcpyHostToDevice, st);
+    if (n_chunks > 0) {
+        k_validate<Spans><<<grid_for(n_chunks, 256, 148 * 64), 256, 0, st>>>(spans, n_chunks, payload, len,
+                                                                           offsets, vo);
+        HSZG_CHECK_LAUNCH("validate");
+    }
+    ValidateOut h;
+    cudaMemcpyAsync(&h, vo, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return hszg_set_cuda_error(err, e, "validate sync");
+    *canonical = h.noncanonical == 0;
+    *max_bw = h.max_bw;
+    if (h.first_bad != ~0ull) {
+        const int64_t c = (int64_t)h.first_bad;
+        k_diagnose<Spans><<<1, 1, 0, st>>>(spans, payload, len, offsets, c, diag);
+        int64_t r[3];
+        cudaMemcpyAsync(r, diag, sizeof(r), cudaMemcpyDeviceToHost, st);
+        e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return hszg_set_cuda_error(err, e, "diagnose sync");
+        set_decode_error(err, (int)r[0], c, r[1], r[2]);
+        return HSZG_CORRUPT;
+    }
+    return HSZG_OK;
+}
+
+extern "C" int hszg_validate(const HszgGeom* g, HszgStream* s, void* ws, size_t ws_bytes, void* stream,
+                             HszgErr* err) {
+    err->status = HSZG_OK;
+    GeoSpans sp{make_seggeo(*g)};
+    int canonical = 0, max_bw = 0;
+    int r = validate_impl(sp, g->n_chunks, s->payload, s->payload_len, s->offsets, ws, ws_bytes,
+                          as_stream(stream), err, &canonical, &max_bw);
+    s->canonical = canonical;
+    s->max_bitwidth = max_bw;
+    return r;
+}
+
+int hszg_launch_decode(const HszgGeom* g, const HszgStream* s, int32_t* out, cudaStream_t st, HszgErr* err) {
+    const SegGeo sg = make_seggeo(*g);
+    if (g->n_chunks == 0) return HSZG_OK;
+    if (s->canonical) {
+        const int64_t tiles = (g->n_chunks + TILE_CHUNKS - 1) / TILE_CHUNKS;
+        const size_t smem = tile_smem_bytes(s->max_bitwidth);
+        k_decode_tiles<<<(unsigned)tiles, TILE_CHUNKS, smem, st>>>(sg, s->payload, s->payload_len, s->offsets, out);
+    } else {
+        GeoSpans sp{sg};
+        k_decode_direct<GeoSpans><<<grid_for(g->n_chunks, 256, 148 * 64), 256, 0, st>>>(sp, g->n_chunks, s->payload,
+                                                                                      s->offsets, out);
+    }
+    HSZG_CHECK_LAUNCH("decode");
+    return HSZG_OK;
+}
+
+extern "C" int hszg_decode(const HszgGeom* g, const HszgStream* s, int32_t* out, void* stream, HszgErr* err) {
+    err->status = HSZG_OK;
+    return hszg_launch_decode(g, s, out, as_stream(stream), err);
+}
+
+extern "C" int hszg_decode_spans(const uint8_t* payload, uint64_t len, const int64_t* starts, const int64_t* ends,
+                                 const uint64_t* offsets, int64_t n_chunks, int32_t* out, void* ws,
+                                 size_t ws_bytes, void* stream, HszgErr* err) {
+    err->status = HSZG_OK;
+    cudaStream_t st = as_stream(stream);
+    ArrSpans sp{starts, ends};
+    int canonical = 0, max_bw = 0;
+    int r = validate_impl(sp, n_chunks, payload, len, offsets, ws, ws_bytes, st, err, &canonical, &max_bw);
+    if (r != HSZG_OK) return r;
+    if (n_chunks == 0) return HSZG_OK;
+    k_decode_direct<ArrSpans><<<grid_for(n_chunks, 256, 148 * 64), 256, 0, st>>>(sp, n_chunks, payload, offsets, out);
+    HSZG_CHECK_LAUNCH("decode_spans");
+    return HSZG_OK;
+}
+
+// ---- encode ---------------------------------------------------------------
+
+template <class Spans>
+static int encode_sizes_impl(Spans sp, int64_t n_chunks, const int32_t* vals, uint64_t* offsets, uint8_t* bws,
+                             uint64_t* total_host, void* ws, size_t ws_bytes, cudaStream_t st, HszgErr* err) {
+    // workspace: [bad u64][total u64][scan state]
+    const size_t need = 16 + lookback_ws_bytes(n_chunks);
+    if (ws_bytes < need) {
+        err->status = HSZG_INVALID_ARG;
+        snprintf(err->message, sizeof(err->message), "workspace too small for encode (%zu < %zu)", ws_bytes, need);
+        return HSZG_INVALID_ARG;
+    }
+    unsigned long long* bad = reinterpret_cast<unsigned long long*>(ws);
+    uint64_t* total = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(ws) + 8);
+    void* scan_ws = reinterpret_cast<char*>(ws) + 16;
+    const unsigned long long none = ~0ull;
+    cudaMemcpyAsync(bad, &none, 8, cudaMemcpyHostToDevice, st);
+    if (n_chunks > 0) {
+        // sizes are written into `offsets`, then scanned in place (exclusive)
+        k_encode_sizes<Spans><<<grid_for(n_chunks, 256, 148 * 64), 256, 0, st>>>(sp, n_chunks, vals, offsets, bws, bad);
+        HSZG_CHECK_LAUNCH("encode_sizes");
+        int r = exclusive_scan_u64(offsets, offsets, n_chunks, total, scan_ws, st);
+        if (r) return hszg_set_cuda_error(err, cudaGetLastError(), "encode scan");
+    } else {
+        cudaMemsetAsync(total, 0, 8, st);
+    }
+    uint64_t h[2];
+    cudaMemcpyAsync(h, ws, 16, cudaMemcpyDeviceToHost, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return hszg_set_cuda_error(err, e, "encode sync");
+    if (h[0] != ~0ull) {
+        err->status = HSZG_VALUE;
+        err->chunk = (int64_t)h[0];
+        snprintf(err->message, sizeof(err->message), "value -2**31 has no sign-magnitude representation");
+        return HSZG_VALUE;
+    }
+    *total_host = h[1];
+    return HSZG_OK;
+}
+
+extern "C" int hszg_encode_spans_sizes(const int32_t* values, const int64_t* starts, const int64_t* ends,
+                                       int64_t n_chunks, uint64_t* offsets, uint8_t* bitwidths,
+                                       uint64_t* total_host, void* ws, size_t ws_bytes, void* stream, HszgErr* err) {
+    err->status = HSZG_OK;
+    return encode_sizes_impl(ArrSpans{starts, ends}, n_chunks, values, offsets, bitwidths, total_host, ws, ws_bytes,
+                             as_stream(stream), err);
+}
+
+extern "C" int hszg_encode_spans_pack(const int32_t* values, const int64_t* starts, const int64_t* ends,
+                                      int64_t n_chunks, const uint64_t* offsets, const uint8_t* bitwidths,
+                                      uint8_t* payload, void* stream, HszgErr* err) {
+    err->status = HSZG_OK;
+    if (n_chunks == 0) return HSZG_OK;
+    k_encode_pack<ArrSpans><<<grid_for(n_chunks, 256, 148 * 64), 256, 0, as_stream(stream)>>>(
+        ArrSpans{starts, ends}, n_chunks, values, offsets, bitwidths, payload);
+    HSZG_CHECK_LAUNCH("encode_pack");
+    return HSZG_OK;
+}
+
+extern "C" int hszg_encode_sizes(const HszgGeom* g, const int32_t* p, uint64_t* offsets, uint8_t* bitwidths,
+                                 uint64_t* total_host, void* ws, size_t ws_bytes, void* stream, HszgErr* err) {
+    err->status = HSZG_OK;
+    return encode_sizes_impl(GeoSpans{make_seggeo(*g)}, g->n_chunks, p, offsets, bitwidths, total_host, ws, ws_bytes,
+                             as_stream(stream), err);
+}
+
+extern "C" int hszg_encode_pack(const HszgGeom* g, const int32_t* p, const uint64_t* offsets,
+                                const uint8_t* bitwidths, uint8_t* payload, void* stream, HszgErr* err) {
+    err->status = HSZG_OK;
+    if (g->n_chunks == 0) return HSZG_OK;
+    k_encode_pack<GeoSpans><<<grid_for(g->n_chunks, 256, 148 * 64), 256, 0, as_stream(stream)>>>(
+        GeoSpans{make_seggeo(*g)}, g->n_chunks, p, offsets, bitwidths, payload);
+    HSZG_CHECK_LAUNCH("encode_pack");
+    return HSZG_OK;
+}

@@ -1,0 +1,612 @@
+// ops.cu — homomorphic statistics (K-STAT), regional reductions (K-REG) and
+// integer finite-difference stencils (K-STEN).
+//
+// Exactness: integer sums are accumulated in int128 per thread and reduced
+// deterministically (per-CTA partials + one finalize CTA); the host finishes
+// with the reference's own Python-int expressions (analytics/stats.py:58-62,
+// 69-77, 92, 118, 130-138), so scalars are bit-identical.  Stencil outputs
+// reproduce the reference's fp64 rounding sequence exactly (int stencil, one
+// multiply by eps or 2*eps — analytics/fields.py:67-80 — or, in the float
+// domain, fields.py:83-93 operation by operation), then round to the output
+// type.
+#include <cstdio>
+#include "tile.cuh"
+
+namespace hszg {
+
+constexpr int RED_THREADS = 256;
+
+// ---- per-chunk accumulators for the fused stream reductions -----------------
+
+// mode 1/2: sum over the row-major box of w * p with w = (N0-i0)(N1-i1)(N2-i2)
+// (stats.py:88 for HSZP, the separable Lorenzo weights of stats.py:95-112)
+struct WeightedChunk {
+    int64_t N0, N1, N2;
+    int64_t w0, i1, i2;
+    i128 csum;
+    __device__ __forceinline__ void begin(const SegGeo& sg, const ChunkLoc& L, const int32_t*) {
+        N0 = sg.n[0]; N1 = sg.n[1]; N2 = sg.n[2];
+        const int64_t plane = N1 * N2;
+        const int64_t i0 = L.start / plane;
+        const int64_t rem = L.start - i0 * plane;
+        i1 = rem / N2;
+        i2 = rem - i1 * N2;
+        w0 = N0 - i0;
+        csum = 0;
+    }
+    __device__ __forceinline__ void take(Acc&, int, int32_t v) {
+        const int64_t w12 = (N1 - i1) * (N2 - i2);
+        csum += (i128)w12 * (i128)v;
+        if (++i2 == N2) {
+            i2 = 0;
+            ++i1;   // chunks never cross planes (segments are planes / rows / 1-D blocks)
+        }
+    }
+    __device__ __forceinline__ void end(Acc& a, int count) {
+        a.s1 += csum * (i128)w0;
+        a.count += count;
+    }
+};
+
+// mode 3: q = p + M_b in stream order (HSZX*): sum, sum of squares, min, max
+struct MetaChunk {
+    int32_t m;
+    __device__ __forceinline__ void begin(const SegGeo&, const ChunkLoc& L, const int32_t* meta) { m = __ldg(meta + L.seg); }
+    __device__ __forceinline__ void take(Acc& a, int, int32_t v) {
+        const int32_t q = v + m;
+        a.s1 += q;
+        a.s2 += (i128)((int64_t)q * (int64_t)q);
+        a.vmin = min(a.vmin, q);
+        a.vmax = max(a.vmax, q);
+    }
+    __device__ __forceinline__ void end(Acc& a, int count) { a.count += count; }
+};
+
+template <class CA>
+__global__ void __launch_bounds__(TILE_CHUNKS) k_reduce_tiles(SegGeo sg, const uint8_t* payload, uint64_t len,
+                                                             const uint64_t* offsets, const int32_t* meta,
+                                                             HszgSums* partials) {
+    TileCtx t = tile_stage(sg, payload, len, offsets, blockIdx.x);
+    Acc a;
+    a.init();
+    const int64_t c = t.c0 + threadIdx.x;
+    if (c < t.c1) {
+        const ChunkLoc L = locate_chunk(sg, c);
+        CA ca;
+        ca.begin(sg, L, meta);
+        decode_chunk_words(t.words, (uint32_t)(offsets[c] - t.base), L.count,
+                           [&](int j, int32_t v) { ca.take(a, j, v); });
+        ca.end(a, L.count);
+    }
+    block_reduce(a);
+    if (threadIdx.x == 0) store_sums(partials + blockIdx.x, a);
+}
+
+// same reduction over an already-decoded stream-order array (non-canonical containers)
+template <class CA>
+__global__ void k_reduce_chunks_array(SegGeo sg, const int32_t* p, const int32_t* meta, HszgSums* partials) {
+    Acc a;
+    a.init();
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < sg.n_chunks;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const ChunkLoc L = locate_chunk(sg, c);
+        CA ca;
+        ca.begin(sg, L, meta);
+        for (int j = 0; j < L.count; j++) ca.take(a, j, p[L.start + j]);
+        ca.end(a, L.count);
+    }
+    block_reduce(a);
+    if (threadIdx.x == 0) store_sums(partials + blockIdx.x, a);
+}
+
+// mode 4: sum(M_b * S_b) over the metadata (stats.py:69-77)
+__global__ void k_reduce_meta(SegGeo sg, const int32_t* meta, HszgSums* partials) {
+    Acc a;
+    a.init();
+    const int64_t nb = sg.G[0] * sg.G[1] * sg.G[2];
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b2 = b % sg.G[2];
+        const int64_t r = b / sg.G[2];
+        const int64_t b1 = r % sg.G[1];
+        const int64_t b0 = r / sg.G[1];
+        const int64_t size = seg_ext(sg, 0, b0) * seg_ext(sg, 1, b1) * seg_ext(sg, 2, b2);
+        a.s1 += (i128)size * (i128)meta[b];
+        a.count += size;
+    }
+    block_reduce(a);
+    if (threadIdx.x == 0) store_sums(partials + blockIdx.x, a);
+}
+
+// mode 0 over int32 arrays: sum, sum of squares, min, max
+__global__ void k_reduce_i32(const int32_t* src, int64_t n, HszgSums* partials) {
+    Acc a;
+    a.init();
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t s1 = 0;
+    const bool aligned = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+    int64_t head = 0;
+    if (aligned) {
+        const int4* v4 = reinterpret_cast<const int4*>(src);
+        const int64_t n4 = n >> 2;
+        for (int64_t i = tid; i < n4; i += stride) {
+            const int4 v = __ldg(v4 + i);
+            s1 += (int64_t)v.x + v.y + v.z + v.w;
+            a.s2 += (i128)((int64_t)v.x * v.x + (int64_t)v.y * v.y) + (i128)((int64_t)v.z * v.z + (int64_t)v.w * v.w);
+            a.vmin = min(a.vmin, min(min(v.x, v.y), min(v.z, v.w)));
+            a.vmax = max(a.vmax, max(max(v.x, v.y), max(v.z, v.w)));
+        }
+        head = n4 << 2;
+    }
+    for (int64_t i = head + tid; i < n; i += stride) {
+        const int32_t v = src[i];
+        s1 += v;
+        a.s2 += (i128)((int64_t)v * v);
+        a.vmin = min(a.vmin, v);
+        a.vmax = max(a.vmax, v);
+    }
+    a.s1 += s1;   // per-thread int64 partial: <= n/(4*threads) terms of |v| <= 2^31, far from overflow
+    block_reduce(a);
+    if (threadIdx.x == 0) {
+        a.count = blockIdx.x ? 0 : n;
+        store_sums(partials + blockIdx.x, a);
+    }
+}
+
+// stage-4 float sums: f1 = sum(fl(q*s)), f2 = sum((fl(q*s) - mean)^2)
+__global__ void k_reduce_f64(const int32_t* q, int64_t n, double s, const double* mean, HszgSums* partials) {
+    Acc a;
+    a.init();
+    const double mu = mean ? *mean : 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double d = __dmul_rn((double)q[i], s);
+        a.f1 = __dadd_rn(a.f1, d);
+        if (mean) {
+            const double e = __dsub_rn(d, mu);
+            a.f2 = __dadd_rn(a.f2, __dmul_rn(e, e));
+        }
+    }
+    block_reduce(a);
+    if (threadIdx.x == 0) {
+        a.count = blockIdx.x ? 0 : n;
+        store_sums(partials + blockIdx.x, a);
+    }
+}
+
+__global__ void k_reduce_dot(const int32_t* x, const int32_t* y, int64_t n, HszgSums* partials) {
+    Acc a;
+    a.init();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        a.s1 += (i128)((int64_t)x[i] * (int64_t)y[i]);
+    block_reduce(a);
+    if (threadIdx.x == 0) {
+        a.count = blockIdx.x ? 0 : n;
+        store_sums(partials + blockIdx.x, a);
+    }
+}
+
+__global__ void k_finalize(const HszgSums* partials, int64_t nparts, HszgSums* out) {
+    Acc a;
+    a.init();
+    // fixed per-thread striding + fixed tree: deterministic float sums too
+    for (int64_t i = threadIdx.x; i < nparts; i += blockDim.x) a.merge(load_sums(partials + i));
+    block_reduce(a);
+    if (threadIdx.x == 0) store_sums(out, a);
+}
+
+// ---- regional reductions (N2-N4) --------------------------------------------------
+
+__global__ void k_region_reduce(const int32_t* q, int64_t n0, int64_t n1, int64_t n2, int64_t R0, int64_t R1,
+                                int64_t R2, int64_t g1, int64_t g2, int64_t* s1, uint64_t* s2lo, int64_t* s2hi,
+                                int32_t* qmin, int32_t* qmax, int64_t* size) {
+    const int64_t r = blockIdx.x;
+    const int64_t r2 = r % g2;
+    const int64_t rr = r / g2;
+    const int64_t r1 = rr % g1;
+    const int64_t r0 = rr / g1;
+    const int64_t z0 = r0 * R0, y0 = r1 * R1, x0 = r2 * R2;
+    const int e0 = (int)((z0 + R0 <= n0 ? R0 : n0 - z0));
+    const int e1 = (int)((y0 + R1 <= n1 ? R1 : n1 - y0));
+    const int e2 = (int)((x0 + R2 <= n2 ? R2 : n2 - x0));
+    const int tot = e0 * e1 * e2;
+    Acc a;
+    a.init();
+    for (int i = threadIdx.x; i < tot; i += blockDim.x) {
+        const int zy = i / e2;
+        const int x = i - zy * e2;
+        const int z = zy / e1;
+        const int y = zy - z * e1;
+        const int32_t v = __ldg(q + ((z0 + z) * n1 + (y0 + y)) * n2 + x0 + x);
+        a.s1 += v;
+        a.s2 += (i128)((int64_t)v * v);
+        a.vmin = min(a.vmin, v);
+        a.vmax = max(a.vmax, v);
+    }
+    block_reduce(a);
+    if (threadIdx.x == 0) {
+        s1[r] = (int64_t)a.s1;
+        s2lo[r] = (uint64_t)a.s2;
+        s2hi[r] = (int64_t)(a.s2 >> 64);
+        qmin[r] = a.vmin;
+        qmax[r] = a.vmax;
+        size[r] = tot;
+    }
+}
+
+__global__ void k_region_finalize(const int64_t* s1, const uint64_t* s2lo, const int64_t* s2hi, const int32_t* qmin,
+                                  const int32_t* qmax, const int64_t* size, int64_t nr, double two_eps, double tau,
+                                  double* mean, double* var, double* fmin, double* fmax, unsigned long long* count) {
+    unsigned long long cnt = 0;
+    const double s2e = __dmul_rn(two_eps, two_eps);
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nr; r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t n = size[r];
+        mean[r] = __dmul_rn(__ddiv_rn((double)s1[r], (double)n), two_eps);
+        if (n < 2) {
+            var[r] = __longlong_as_double(0x7ff8000000000000ll);
+        } else {
+            const i128 S2 = (i128)(((u128)(uint64_t)s2hi[r] << 64) | s2lo[r]);
+            const i128 num = (i128)n * S2 - (i128)s1[r] * (i128)s1[r];
+            const double numd = (num >= 0 && num < ((i128)1 << 63)) ? (double)(int64_t)num
+                              : __dadd_rn(__dmul_rn((double)(int64_t)(num >> 64), 18446744073709551616.0),
+                                          __ull2double_rn((uint64_t)num));
+            var[r] = __dmul_rn(__ddiv_rn(numd, (double)(n * (n - 1))), s2e);
+        }
+        const double lo = __dmul_rn((double)qmin[r], two_eps), hi = __dmul_rn((double)qmax[r], two_eps);
+        fmin[r] = lo;
+        fmax[r] = hi;
+        if (lo < tau && tau <= hi) cnt++;
+    }
+    for (int d = 16; d > 0; d >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, d);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(count, cnt);
+}
+
+// float64 input sums: f1 = sum(x), f2 = sum((x-mean)^2)
+__global__ void k_reduce_flt(const double* x, int64_t n, const double* mean, HszgSums* partials) {
+    Acc a;
+    a.init();
+    const double mu = mean ? *mean : 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double d = __ldg(x + i);
+        a.f1 = __dadd_rn(a.f1, d);
+        if (mean) {
+            const double e = __dsub_rn(d, mu);
+            a.f2 = __dadd_rn(a.f2, __dmul_rn(e, e));
+        }
+    }
+    block_reduce(a);
+    if (threadIdx.x == 0) {
+        a.count = blockIdx.x ? 0 : n;
+        store_sums(partials + blockIdx.x, a);
+    }
+}
+
+// ---- stencils -----------------------------------------------------------------------
+
+struct StencilArgs {
+    int op;
+    int nd;             // original dimensionality
+    int ncomp;
+    int float_domain;   // 0: int32 q (stage 2/3), 1: int32 q read as fl(q*2eps) (stage 4), 2: float64 input grids
+    int out_type;
+    int64_t n[3];       // box dims (leading 1s for 1-D / 2-D)
+    const void* q[3];
+    double eps[3];
+    double two_eps[3];
+    void* out[3];
+};
+
+__device__ __forceinline__ void put(const StencilArgs& A, int k, int64_t i, double v) {
+    if (A.out_type == HSZG_F32) reinterpret_cast<float*>(A.out[k])[i] = __double2float_rn(v);
+    else reinterpret_cast<double*>(A.out[k])[i] = v;
+}
+
+__device__ __forceinline__ int32_t qv(const StencilArgs& A, int c, int64_t i) {
+    return __ldg(reinterpret_cast<const int32_t*>(A.q[c]) + i);
+}
+// float-domain value of component c at i: the stage-4 float fl(q*2eps) or a float64 input
+__device__ __forceinline__ double fv(const StencilArgs& A, int c, int64_t i) {
+    if (A.float_domain == 2) return __ldg(reinterpret_cast<const double*>(A.q[c]) + i);
+    return __dmul_rn((double)qv(A, c, i), A.two_eps[c]);
+}
+
+// derivative of component c along original axis k at box position (i0,i1,i2), linear i
+__device__ __forceinline__ double deriv(const StencilArgs& A, int c, int k, const int64_t* idx, int64_t i,
+                                        int64_t* dint) {
+    const int a = 3 - A.nd + k;
+    const int64_t s = a == 2 ? 1 : (a == 1 ? A.n[2] : A.n[1] * A.n[2]);
+    if (idx[a] == 0 || idx[a] == A.n[a] - 1) {
+        if (dint) *dint = 0;
+        return 0.0;
+    }
+    if (A.float_domain) return __ddiv_rn(__dsub_rn(fv(A, c, i + s), fv(A, c, i - s)), 2.0);   // fields.py:85
+    const int64_t d = (int64_t)qv(A, c, i + s) - (int64_t)qv(A, c, i - s);                    // fields.py:43
+    if (dint) *dint = d;
+    return __dmul_rn((double)d, A.eps[c]);                   // fields.py:70
+}
+
+__global__ void k_stencil(StencilArgs A) {
+    const int64_t i2 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i2 >= A.n[2]) return;
+    const int64_t i1 = blockIdx.y;
+    const int64_t i0 = blockIdx.z;
+    const int64_t idx[3] = {i0, i1, i2};
+    const int64_t i = (i0 * A.n[1] + i1) * A.n[2] + i2;
+    switch (A.op) {
+        case HSZG_OP_DERIV:
+            for (int k = 0; k < A.nd; k++) put(A, k, i, deriv(A, 0, k, idx, i, nullptr));
+            break;
+        case HSZG_OP_LAPLACIAN: {
+            bool interior = true;
+            for (int k = 0; k < A.nd; k++) {
+                const int a = 3 - A.nd + k;
+                interior &= idx[a] > 0 && idx[a] < A.n[a] - 1;
+            }
+            if (!interior) {
+                put(A, 0, i, 0.0);
+                break;
+            }
+            if (A.float_domain) {
+                // fields.py:47-60 on float64 values: acc = (-2*nd)*v; acc = acc + lo + hi per axis
+                double acc = __dmul_rn((double)(-2 * A.nd), fv(A, 0, i));
+                for (int k = 0; k < A.nd; k++) {
+                    const int a = 3 - A.nd + k;
+                    const int64_t st = a == 2 ? 1 : (a == 1 ? A.n[2] : A.n[1] * A.n[2]);
+                    acc = __dadd_rn(acc, fv(A, 0, i - st));
+                    acc = __dadd_rn(acc, fv(A, 0, i + st));
+                }
+                put(A, 0, i, acc);
+            } else {
+                int64_t acc = -2 * (int64_t)A.nd * qv(A, 0, i);
+                for (int k = 0; k < A.nd; k++) {
+                    const int a = 3 - A.nd + k;
+                    const int64_t st = a == 2 ? 1 : (a == 1 ? A.n[2] : A.n[1] * A.n[2]);
+                    acc += (int64_t)qv(A, 0, i - st) + (int64_t)qv(A, 0, i + st);
+                }
+                put(A, 0, i, __dmul_rn((double)acc, A.two_eps[0]));   // fields.py:79
+            }
+            break;
+        }
+        case HSZG_OP_GRADMAG: {
+            if (A.float_domain) {
+                double s = 0.0;
+                for (int k = 0; k < A.nd; k++) {
+                    const double d = deriv(A, 0, k, idx, i, nullptr);
+                    s = __dadd_rn(s, __dmul_rn(d, d));
+                }
+                put(A, 0, i, __dsqrt_rn(s));
+            } else {
+                u128 s = 0;
+                for (int k = 0; k < A.nd; k++) {
+                    int64_t d;
+                    deriv(A, 0, k, idx, i, &d);
+                    const uint64_t ad = (uint64_t)(d < 0 ? -d : d);
+                    s += (u128)ad * ad;
+                }
+                double sd;
+                if ((uint64_t)(s >> 64) == 0) sd = __ull2double_rn((uint64_t)s);
+                else sd = __dadd_rn(__dmul_rn(__ull2double_rn((uint64_t)(s >> 64)), 18446744073709551616.0),
+                                    __ull2double_rn((uint64_t)s));
+                put(A, 0, i, __dmul_rn(__dsqrt_rn(sd), A.eps[0]));
+            }
+            break;
+        }
+        case HSZG_OP_DIVERGENCE: {
+            double acc = deriv(A, 0, 0, idx, i, nullptr);        // fields.py:219-221
+            for (int k = 1; k < A.ncomp; k++) acc = __dadd_rn(acc, deriv(A, k, k, idx, i, nullptr));
+            put(A, 0, i, acc);
+            break;
+        }
+        case HSZG_OP_CURL: {
+            if (A.ncomp == 2) {                                     // fields.py:228-231
+                put(A, 0, i, __dsub_rn(deriv(A, 0, 1, idx, i, nullptr), deriv(A, 1, 0, idx, i, nullptr)));
+            } else {                                                // fields.py:232-236
+                put(A, 0, i, __dsub_rn(deriv(A, 2, 1, idx, i, nullptr), deriv(A, 1, 2, idx, i, nullptr)));
+                put(A, 1, i, __dsub_rn(deriv(A, 0, 2, idx, i, nullptr), deriv(A, 2, 0, idx, i, nullptr)));
+                put(A, 2, i, __dsub_rn(deriv(A, 1, 0, idx, i, nullptr), deriv(A, 0, 1, idx, i, nullptr)));
+            }
+            break;
+        }
+        default:
+            break;
+    }
+}
+
+}  // namespace hszg
+
+using namespace hszg;
+
+int hszg_set_cuda_error(HszgErr* err, cudaError_t e, const char* where);
+int hszg_launch_decode(const HszgGeom* g, const HszgStream* s, int32_t* out, cudaStream_t st, HszgErr* err);
+
+static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+static const int kMaxParts = 148 * 16;
+
+size_t hszg_reduce_ws_bytes(int64_t tiles) {
+    const int64_t parts = tiles > kMaxParts ? tiles : kMaxParts;
+    return (size_t)(parts + 1) * sizeof(HszgSums) + 256;
+}
+
+static int finalize(HszgSums* partials, int64_t nparts, HszgSums* out, cudaStream_t st) {
+    k_finalize<<<1, 1024, 0, st>>>(partials, nparts, out);
+    return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
+}
+
+extern "C" int hszg_reduce_stream(const HszgGeom* g, const HszgStream* s, int mode, HszgSums* out_dev, void* ws,
+                                  size_t ws_bytes, void* stream, HszgErr* err) {
+    err->status = HSZG_OK;
+    cudaStream_t st = as_stream(stream);
+    const SegGeo sg = make_seggeo(*g);
+    HszgSums* partials = reinterpret_cast<HszgSums*>(ws);
+    if (mode == 4) {
+        if (!s->metadata) {
+            err->status = HSZG_INVALID_ARG;
+            snprintf(err->message, sizeof(err->message), "stream has no block-mean metadata");
+            return HSZG_INVALID_ARG;
+        }
+        const int64_t nb = sg.G[0] * sg.G[1] * sg.G[2];
+        const int grid = grid_for(nb, RED_THREADS, kMaxParts);
+        k_reduce_meta<<<grid, RED_THREADS, 0, st>>>(sg, s->metadata, partials);
+        return finalize(partials, grid, out_dev, st);
+    }
+    if (mode < 1 || mode > 3) {
+        err->status = HSZG_INVALID_ARG;
+        snprintf(err->message, sizeof(err->message), "unknown reduction mode %d", mode);
+        return HSZG_INVALID_ARG;
+    }
+    const int64_t tiles = (g->n_chunks + TILE_CHUNKS - 1) / TILE_CHUNKS;
+    if (g->n_chunks == 0) {
+        HszgSums z = {};
+        cudaMemcpyAsync(out_dev, &z, sizeof(z), cudaMemcpyHostToDevice, st);
+        return HSZG_OK;
+    }
+    if (s->canonical) {
+        if (ws_bytes < hszg_reduce_ws_bytes(tiles)) {
+            err->status = HSZG_INVALID_ARG;
+            snprintf(err->message, sizeof(err->message), "workspace too small for reduction");
+            return HSZG_INVALID_ARG;
+        }
+        const size_t smem = tile_smem_bytes(s->max_bitwidth);
+        if (mode == 3)
+            k_reduce_tiles<MetaChunk><<<(unsigned)tiles, TILE_CHUNKS, smem, st>>>(sg, s->payload, s->payload_len,
+                                                                                s->offsets, s->metadata, partials);
+        else
+            k_reduce_tiles<WeightedChunk><<<(unsigned)tiles, TILE_CHUNKS, smem, st>>>(
+                sg, s->payload, s->payload_len, s->offsets, s->metadata, partials);
+        if (cudaGetLastError() != cudaSuccess) return hszg_set_cuda_error(err, cudaGetLastError(), "reduce tiles");
+        return finalize(partials, tiles, out_dev, st);
+    }
+    // non-canonical: decode into the workspace tail, then reduce per chunk
+    const size_t head = hszg_reduce_ws_bytes(kMaxParts);
+    if (ws_bytes < head + (size_t)g->n * 4) {
+        err->status = HSZG_INVALID_ARG;
+        snprintf(err->message, sizeof(err->message), "workspace too small for reduction");
+        return HSZG_INVALID_ARG;
+    }
+    int32_t* p = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ws) + head);
+    int r = hszg_launch_decode(g, s, p, st, err);
+    if (r) return r;
+    const int grid = grid_for(g->n_chunks, RED_THREADS, kMaxParts);
+    if (mode == 3) k_reduce_chunks_array<MetaChunk><<<grid, RED_THREADS, 0, st>>>(sg, p, s->metadata, partials);
+    else k_reduce_chunks_array<WeightedChunk><<<grid, RED_THREADS, 0, st>>>(sg, p, s->metadata, partials);
+    return finalize(partials, grid, out_dev, st);
+}
+
+extern "C" int hszg_reduce_array(const HszgGeom* g, const int32_t* p, const int32_t* metadata, int mode,
+                                 HszgSums* out_dev, void* ws, size_t ws_bytes, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    const SegGeo sg = make_seggeo(*g);
+    if (ws_bytes < hszg_reduce_ws_bytes(0)) return HSZG_INVALID_ARG;
+    HszgSums* partials = reinterpret_cast<HszgSums*>(ws);
+    const int grid = grid_for(g->n_chunks, RED_THREADS, kMaxParts);
+    if (mode == 3) k_reduce_chunks_array<MetaChunk><<<grid, RED_THREADS, 0, st>>>(sg, p, metadata, partials);
+    else if (mode == 1 || mode == 2)
+        k_reduce_chunks_array<WeightedChunk><<<grid, RED_THREADS, 0, st>>>(sg, p, metadata, partials);
+    else return HSZG_INVALID_ARG;
+    return finalize(partials, grid, out_dev, st);
+}
+
+extern "C" int hszg_reduce_i32(const int32_t* src, int64_t n, HszgSums* out_dev, void* ws, size_t ws_bytes,
+                               void* stream) {
+    cudaStream_t st = as_stream(stream);
+    if (ws_bytes < hszg_reduce_ws_bytes(0)) return HSZG_INVALID_ARG;
+    HszgSums* partials = reinterpret_cast<HszgSums*>(ws);
+    const int grid = grid_for(n / 4 + 1, RED_THREADS * 8, kMaxParts);
+    k_reduce_i32<<<grid, RED_THREADS, 0, st>>>(src, n, partials);
+    return finalize(partials, grid, out_dev, st);
+}
+
+extern "C" int hszg_reduce_f64(const int32_t* q, int64_t n, double scale, const double* mean_dev, HszgSums* out_dev,
+                               void* ws, size_t ws_bytes, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    if (ws_bytes < hszg_reduce_ws_bytes(0)) return HSZG_INVALID_ARG;
+    HszgSums* partials = reinterpret_cast<HszgSums*>(ws);
+    const int grid = grid_for(n, RED_THREADS * 8, kMaxParts);
+    k_reduce_f64<<<grid, RED_THREADS, 0, st>>>(q, n, scale, mean_dev, partials);
+    return finalize(partials, grid, out_dev, st);
+}
+
+extern "C" int hszg_reduce_dot(const int32_t* a, const int32_t* b, int64_t n, HszgSums* out_dev, void* ws,
+                               size_t ws_bytes, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    if (ws_bytes < hszg_reduce_ws_bytes(0)) return HSZG_INVALID_ARG;
+    HszgSums* partials = reinterpret_cast<HszgSums*>(ws);
+    const int grid = grid_for(n, RED_THREADS * 8, kMaxParts);
+    k_reduce_dot<<<grid, RED_THREADS, 0, st>>>(a, b, n, partials);
+    return finalize(partials, grid, out_dev, st);
+}
+
+static void box3(int32_t ndims, const int64_t* dims, int64_t* n) {
+    n[0] = n[1] = n[2] = 1;
+    for (int k = 0; k < ndims; k++) n[3 - ndims + k] = dims[k];
+}
+
+extern "C" int hszg_region_reduce(const int32_t* q, int32_t ndims, const int64_t* dims, const int64_t* region,
+                                  int64_t* s1, uint64_t* s2_lo, int64_t* s2_hi, int32_t* qmin, int32_t* qmax,
+                                  int64_t* size, void* stream) {
+    if (ndims < 1 || ndims > 3) return HSZG_INVALID_ARG;
+    int64_t n[3], R[3] = {1, 1, 1};
+    box3(ndims, dims, n);
+    for (int k = 0; k < ndims; k++) {
+        const int64_t r = region[k] < dims[k] ? region[k] : dims[k];
+        if (r < 1) return HSZG_INVALID_ARG;
+        R[3 - ndims + k] = r;
+    }
+    const int64_t g0 = (n[0] + R[0] - 1) / R[0], g1 = (n[1] + R[1] - 1) / R[1], g2 = (n[2] + R[2] - 1) / R[2];
+    const int64_t nr = g0 * g1 * g2;
+    if (nr == 0) return HSZG_OK;
+    const int64_t rs = R[0] * R[1] * R[2];
+    const int threads = rs >= 1024 ? 256 : (rs >= 256 ? 128 : 64);
+    k_region_reduce<<<(unsigned)nr, threads, 0, as_stream(stream)>>>(q, n[0], n[1], n[2], R[0], R[1], R[2], g1, g2,
+                                                                     s1, s2_lo, s2_hi, qmin, qmax, size);
+    return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
+}
+
+extern "C" int hszg_stencil(int op, int32_t ndims, const int64_t* dims, int32_t ncomp, const void* const* q,
+                            const double* eps, int float_domain, int32_t out_type, void* const* out, void* stream) {
+    if (ndims < 1 || ndims > 3 || ncomp < 1 || ncomp > 3) return HSZG_INVALID_ARG;
+    if (out_type != HSZG_F32 && out_type != HSZG_F64) return HSZG_INVALID_ARG;
+    StencilArgs A = {};
+    A.op = op;
+    A.nd = ndims;
+    A.ncomp = ncomp;
+    A.float_domain = float_domain;
+    A.out_type = out_type;
+    box3(ndims, dims, A.n);
+    for (int c = 0; c < ncomp; c++) {
+        A.q[c] = q[c];
+        A.eps[c] = eps[c];
+        A.two_eps[c] = 2.0 * eps[c];
+    }
+    int nout = 1;
+    if (op == HSZG_OP_DERIV) nout = ndims;
+    if (op == HSZG_OP_CURL) nout = ncomp == 2 ? 1 : 3;
+    for (int k = 0; k < nout; k++) A.out[k] = out[k];
+    if (A.n[1] > 65535 || A.n[0] > 65535) return HSZG_INVALID_ARG;
+    dim3 grid((unsigned)((A.n[2] + 255) / 256), (unsigned)A.n[1], (unsigned)A.n[0]);
+    if (A.n[0] * A.n[1] * A.n[2] == 0) return HSZG_OK;
+    k_stencil<<<grid, 256, 0, as_stream(stream)>>>(A);
+    return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
+}
+
+extern "C" int hszg_region_finalize(const int64_t* s1, const uint64_t* s2_lo, const int64_t* s2_hi, const int32_t* qmin,
+                                    const int32_t* qmax, const int64_t* size, int64_t n_regions, double two_eps,
+                                    double tau, double* mean, double* var, double* fmin, double* fmax,
+                                    unsigned long long* count_dev, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    cudaMemsetAsync(count_dev, 0, 8, st);
+    if (n_regions <= 0) return HSZG_OK;
+    k_region_finalize<<<grid_for(n_regions, 256, 148 * 8), 256, 0, st>>>(s1, s2_lo, s2_hi, qmin, qmax, size, n_regions,
+                                                                         two_eps, tau, mean, var, fmin, fmax, count_dev);
+    return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
+}
+
+extern "C" int hszg_reduce_flt(const double* x, int64_t n, const double* mean_dev, HszgSums* out_dev, void* ws,
+                               size_t ws_bytes, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    if (ws_bytes < hszg_reduce_ws_bytes(0)) return HSZG_INVALID_ARG;
+    HszgSums* partials = reinterpret_cast<HszgSums*>(ws);
+    const int grid = grid_for(n, RED_THREADS * 8, kMaxParts);
+    k_reduce_flt<<<grid, RED_THREADS, 0, st>>>(x, n, mean_dev, partials);
+    return finalize(partials, grid, out_dev, st);
+}

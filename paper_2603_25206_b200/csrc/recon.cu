@@ -1,0 +1,549 @@
+// recon.cu — stage 3 (prediction reversion, K-REC-*) and stage 4 (K-DEQ epilogue).
+//
+// Reference: recorrelate (compressors.py:201-226) and the stage-4 dequantize
+// q.astype(float64) * (2.0*eps) (stages.py:88).
+//   HSZX    : q = p + M_b, stream order == row-major          -> k_tile_stream<add_meta>
+//   HSZX_ND : q = p + M_b scattered block-contiguous -> row-major -> k_tile_blocks (smem transpose)
+//   HSZP    : q = inclusive cumsum of p over the flat stream  -> k_tile_scan (decoupled look-back)
+//   HSZP_ND : q = cumsum along every axis (Lorenzo inverse)     -> decode + row scan + column scans
+// All arithmetic is int32 with wrap-around: every prefix equals a q value,
+// which fits int32, so modular sums are exact (the reference casts its int64
+// result back to int32, compressors.py:226).
+#include <cstdio>
+#include "tile.cuh"
+#include "lookback.cuh"
+
+namespace hszg {
+
+template <typename OutT>
+struct Conv;
+template <>
+struct Conv<int32_t> {
+    __device__ __forceinline__ static int32_t go(int32_t q, double) { return q; }
+};
+template <>
+struct Conv<float> {
+    __device__ __forceinline__ static float go(int32_t q, double s) { return __double2float_rn(__dmul_rn((double)q, s)); }
+};
+template <>
+struct Conv<double> {
+    __device__ __forceinline__ static double go(int32_t q, double s) { return __dmul_rn((double)q, s); }
+};
+
+// ---- stream-order tiles (HSZX; also stage 2 with add_meta=false) ------------
+
+template <bool AddMeta, typename OutT>
+__global__ void __launch_bounds__(TILE_CHUNKS) k_tile_stream(SegGeo sg, const uint8_t* payload, uint64_t len,
+                                                            const uint64_t* offsets, const int32_t* meta,
+                                                            double two_eps, OutT* out) {
+    TileCtx t = tile_stage(sg, payload, len, offsets, blockIdx.x);
+    const int64_t c = t.c0 + threadIdx.x;
+    if (c < t.c1) {
+        const ChunkLoc L = locate_chunk(sg, c);
+        const int local = (int)(L.start - t.e0);
+        const int32_t m = AddMeta ? __ldg(meta + L.seg) : 0;
+        int32_t* vals = t.vals;
+        decode_chunk_words(t.words, (uint32_t)(offsets[c] - t.base), L.count,
+                           [&](int j, int32_t v) { vals[pad_idx(local + j)] = v + m; });
+    }
+    __syncthreads();
+    const int n = (int)(t.e1 - t.e0);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[t.e0 + i] = Conv<OutT>::go(t.vals[pad_idx(i)], two_eps);
+}
+
+// ---- HSZX_ND: groups of k blocks along the last axis, transposed to row-major -----
+
+struct BlockTiles {
+    int64_t k;        // segments per tile
+    int64_t tpr;      // tiles per segment row = ceil(G2 / k)
+};
+
+template <typename OutT>
+__global__ void __launch_bounds__(TILE_CHUNKS) k_tile_blocks(SegGeo sg, BlockTiles bt, const uint8_t* payload,
+                                                            uint64_t len, const uint64_t* offsets,
+                                                            const int32_t* meta, double two_eps, OutT* out) {
+    extern __shared__ __align__(16) uint8_t tile_smem[];
+    __shared__ uint64_t s_lo, s_hi;
+    __shared__ int64_t s_c0, s_c1, s_e0;
+    const int64_t tile = blockIdx.x;
+    const int64_t row = tile / bt.tpr;             // segment row (b0, b1)
+    const int64_t tb = tile - row * bt.tpr;
+    const int64_t b0 = row / sg.G[1];
+    const int64_t b1 = row - b0 * sg.G[1];
+    const int64_t b2a = tb * bt.k;
+    const int64_t b2b = (b2a + bt.k < sg.G[2]) ? b2a + bt.k : sg.G[2];
+    const int c0cls = b0 == sg.G[0] - 1, c1cls = b1 == sg.G[1] - 1;
+    const int64_t s0 = seg_ext(sg, 0, b0), s1 = seg_ext(sg, 1, b1);
+    if (threadIdx.x == 0) {
+        s_c0 = seg_chunk_start(sg, b0, b1, b2a);
+        const int64_t last = b2b - 1;
+        s_c1 = seg_chunk_start(sg, b0, b1, last) + sg.cpb[(c0cls << 2) | (c1cls << 1) | (last == sg.G[2] - 1)];
+        s_lo = offsets[s_c0];
+        s_hi = s_c1 < sg.n_chunks ? offsets[s_c1] : len;
+        s_e0 = seg_elem_start(sg, b0, b1, b2a);
+    }
+    __syncthreads();
+    const uint64_t base = s_lo & ~(uint64_t)15;
+    const uint64_t nvec = (s_hi - base + 15) >> 4;
+    int32_t* vals = reinterpret_cast<int32_t*>(tile_smem);
+    uint4* sb = reinterpret_cast<uint4*>(tile_smem + (size_t)TILE_VALS * 4);
+    const uint4* g = reinterpret_cast<const uint4*>(payload + base);
+    for (uint64_t i = threadIdx.x; i < nvec; i += blockDim.x) sb[i] = __ldg(g + i);
+    if (threadIdx.x == 0) sb[nvec] = make_uint4(0, 0, 0, 0);
+    const uint32_t* words = reinterpret_cast<const uint32_t*>(sb);
+    __syncthreads();
+    const int64_t nch = s_c1 - s_c0;
+    for (int64_t ci = threadIdx.x; ci < nch; ci += blockDim.x) {
+        const int64_t c = s_c0 + ci;
+        const ChunkLoc L = locate_chunk(sg, c);
+        const int local = (int)(L.start - s_e0);
+        const int32_t m = __ldg(meta + L.seg);
+        decode_chunk_words(words, (uint32_t)(offsets[c] - base), L.count,
+                           [&](int j, int32_t v) { vals[pad_idx(local + j)] = v + m; });
+    }
+    __syncthreads();
+    // row-major write-out of the (s0, s1, W) box
+    const int64_t x0 = b2a * sg.B[2];
+    const int64_t xe = (b2b == sg.G[2]) ? sg.n[2] : b2b * sg.B[2];
+    const int W = (int)(xe - x0);
+    const int B2 = (int)sg.B[2];
+    const int last_ext = (int)seg_ext(sg, 2, b2b - 1);
+    const int nlast = (int)(b2b - 1 - b2a);
+    const int S1 = (int)s1;
+    const int segsz = (int)(s0 * s1) * B2;
+    const int total = (int)(s0 * s1) * W;
+    const int64_t z0 = b0 * sg.B[0], y0 = b1 * sg.B[1];
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+        const int zy = i / W;
+        const int xl = i - zy * W;
+        const int t = xl / B2;
+        const int xi = xl - t * B2;
+        const int s2t = (t == nlast) ? last_ext : B2;
+        const int local = t * segsz + zy * s2t + xi;
+        const int zl = zy / S1, yl = zy - zl * S1;
+        const int64_t gi = ((z0 + zl) * sg.n[1] + (y0 + yl)) * sg.n[2] + x0 + xl;
+        out[gi] = Conv<OutT>::go(vals[pad_idx(local)], two_eps);
+    }
+}
+
+// ---- HSZP: flat inclusive scan with decoupled look-back -------------------------
+
+template <typename OutT>
+__global__ void __launch_bounds__(TILE_CHUNKS) k_tile_scan(SegGeo sg, const uint8_t* payload, uint64_t len,
+                                                          const uint64_t* offsets, LBState st, double two_eps,
+                                                          OutT* out) {
+    __shared__ unsigned int s_tile;
+    __shared__ unsigned long long s_prefix;
+    if (threadIdx.x == 0) s_tile = atomicAdd(st.ticket, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    TileCtx t = tile_stage(sg, payload, len, offsets, tile);
+    const int64_t c = t.c0 + threadIdx.x;
+    uint32_t run = 0;
+    int local = 0, count = 0;
+    int32_t* vals = t.vals;
+    if (c < t.c1) {
+        const ChunkLoc L = locate_chunk(sg, c);
+        local = (int)(L.start - t.e0);
+        count = L.count;
+        decode_chunk_words(t.words, (uint32_t)(offsets[c] - t.base), L.count, [&](int j, int32_t v) {
+            run += (uint32_t)v;
+            vals[pad_idx(local + j)] = (int32_t)run;
+        });
+    }
+    unsigned long long tot;
+    const unsigned long long excl = block_exclusive_u64((unsigned long long)run, &tot);
+    if (threadIdx.x == 0) s_prefix = lookback_exclusive(st, tile, tot & 0xffffffffull);
+    __syncthreads();
+    const uint32_t add = (uint32_t)(s_prefix + excl);
+    for (int j = 0; j < count; j++) vals[pad_idx(local + j)] = (int32_t)((uint32_t)vals[pad_idx(local + j)] + add);
+    __syncthreads();
+    const int n = (int)(t.e1 - t.e0);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[t.e0 + i] = Conv<OutT>::go(t.vals[pad_idx(i)], two_eps);
+}
+
+// ---- HSZP_ND: row scans along the last axis, then column scans -----------------------
+
+constexpr int ROW_THREADS = 256, ROW_ITEMS = 8;
+
+__global__ void __launch_bounds__(ROW_THREADS) k_row_scan(int32_t* buf, int64_t L) {
+    const int64_t row = blockIdx.x;
+    int32_t* r = buf + row * L;
+    uint32_t carry = 0;
+    for (int64_t base = 0; base < L; base += ROW_THREADS * ROW_ITEMS) {
+        const int64_t i0 = base + (int64_t)threadIdx.x * ROW_ITEMS;
+        uint32_t v[ROW_ITEMS];
+        uint32_t run = 0;
+#pragma unroll
+        for (int k = 0; k < ROW_ITEMS; k++) {
+            v[k] = (i0 + k < L) ? (uint32_t)r[i0 + k] : 0u;
+            run += v[k];
+        }
+        unsigned long long tot;
+        const uint32_t ex = (uint32_t)block_exclusive_u64(run, &tot);
+        uint32_t acc = carry + ex;
+#pragma unroll
+        for (int k = 0; k < ROW_ITEMS; k++) {
+            acc += v[k];
+            if (i0 + k < L) r[i0 + k] = (int32_t)acc;
+        }
+        carry += (uint32_t)tot;
+    }
+}
+
+// view [A][M][Lc]; inclusive scan along M for every (a, l)
+template <typename OutT>
+__global__ void k_col_scan(const int32_t* src, int64_t A, int64_t M, int64_t Lc, double two_eps, OutT* dst) {
+    const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t a = blockIdx.y;
+    if (l >= Lc) return;
+    const int32_t* s = src + a * M * Lc + l;
+    OutT* d = dst + a * M * Lc + l;
+    uint32_t acc = 0;
+    int64_t m = 0;
+    for (; m + 4 <= M; m += 4) {
+        const uint32_t v0 = (uint32_t)s[(m + 0) * Lc], v1 = (uint32_t)s[(m + 1) * Lc];
+        const uint32_t v2 = (uint32_t)s[(m + 2) * Lc], v3 = (uint32_t)s[(m + 3) * Lc];
+        acc += v0; d[(m + 0) * Lc] = Conv<OutT>::go((int32_t)acc, two_eps);
+        acc += v1; d[(m + 1) * Lc] = Conv<OutT>::go((int32_t)acc, two_eps);
+        acc += v2; d[(m + 2) * Lc] = Conv<OutT>::go((int32_t)acc, two_eps);
+        acc += v3; d[(m + 3) * Lc] = Conv<OutT>::go((int32_t)acc, two_eps);
+    }
+    for (; m < M; m++) {
+        acc += (uint32_t)s[m * Lc];
+        d[m * Lc] = Conv<OutT>::go((int32_t)acc, two_eps);
+    }
+}
+
+template <typename OutT>
+static void launch_col_scan(const int32_t* src, int64_t A, int64_t M, int64_t Lc, double two_eps, OutT* dst,
+                            cudaStream_t st) {
+    // grid.y is limited to 65535: fold A into chunks
+    const int64_t ymax = 65535;
+    for (int64_t a0 = 0; a0 < A; a0 += ymax) {
+        const int64_t na = (A - a0) < ymax ? (A - a0) : ymax;
+        dim3 grid((unsigned)((Lc + 255) / 256), (unsigned)na);
+        k_col_scan<OutT><<<grid, 256, 0, st>>>(src + a0 * M * Lc, na, M, Lc, two_eps, dst + a0 * M * Lc);
+    }
+}
+
+template <typename OutT>
+__global__ void k_convert(const int32_t* q, int64_t n, double two_eps, OutT* out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = Conv<OutT>::go(__ldg(q + i), two_eps);
+}
+
+// flat inclusive int32 scan (device-wide, decoupled look-back); values wrap mod 2^32
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_i32(const int32_t* in, int32_t* out, int64_t n, LBState st) {
+    __shared__ unsigned int s_tile;
+    __shared__ unsigned long long s_prefix;
+    if (threadIdx.x == 0) s_tile = atomicAdd(st.ticket, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int64_t base = tile * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+    uint32_t v[SCAN_ITEMS];
+    uint32_t run = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; k++) {
+        const int64_t i = base + k;
+        v[k] = i < n ? (uint32_t)in[i] : 0u;
+        run += v[k];
+    }
+    unsigned long long tot;
+    const unsigned long long ex = block_exclusive_u64(run, &tot);
+    if (threadIdx.x == 0) s_prefix = lookback_exclusive(st, tile, tot & 0xffffffffull);
+    __syncthreads();
+    uint32_t acc = (uint32_t)(s_prefix + ex);
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; k++) {
+        const int64_t i = base + k;
+        acc += v[k];
+        if (i < n) out[i] = (int32_t)acc;
+    }
+}
+
+__global__ void k_add_plane(int32_t* q, const int32_t* carry, int64_t plane, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        q[i] = (int32_t)((uint32_t)q[i] + (uint32_t)__ldg(carry + (i % plane)));
+}
+
+// ---- permutation helpers (HSZX_ND block-contiguous order) ------------------------------
+
+template <typename Fn>
+__device__ __forceinline__ void for_chunk_elements(const SegGeo& sg, int64_t c, Fn fn) {
+    const ChunkLoc L = locate_chunk(sg, c);
+    const int64_t b2 = L.seg % sg.G[2];
+    const int64_t r = L.seg / sg.G[2];
+    const int64_t b1 = r % sg.G[1];
+    const int64_t b0 = r / sg.G[1];
+    const int64_t s1 = seg_ext(sg, 1, b1), s2 = seg_ext(sg, 2, b2);
+    int64_t l = (int64_t)L.j * kChunkCap;
+    int64_t zl = l / (s1 * s2);
+    int64_t rem = l - zl * s1 * s2;
+    int64_t yl = rem / s2;
+    int64_t xl = rem - yl * s2;
+    for (int j = 0; j < L.count; j++) {
+        const int64_t flat = ((b0 * sg.B[0] + zl) * sg.n[1] + (b1 * sg.B[1] + yl)) * sg.n[2] + b2 * sg.B[2] + xl;
+        fn(L.start + j, flat, L.seg);
+        if (++xl == s2) {
+            xl = 0;
+            if (++yl == s1) {
+                yl = 0;
+                ++zl;
+            }
+        }
+    }
+}
+
+__global__ void k_stream_perm(SegGeo sg, int64_t* perm) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < sg.n_chunks;
+         c += (int64_t)gridDim.x * blockDim.x)
+        for_chunk_elements(sg, c, [&](int64_t pos, int64_t flat, int64_t) { perm[pos] = flat; });
+}
+
+__global__ void k_scatter_grid(SegGeo sg, const int32_t* src, const int32_t* meta, int add_meta, int32_t* out) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < sg.n_chunks;
+         c += (int64_t)gridDim.x * blockDim.x)
+        for_chunk_elements(sg, c, [&](int64_t pos, int64_t flat, int64_t seg) {
+            out[flat] = src[pos] + (add_meta ? meta[seg] : 0);
+        });
+}
+
+__global__ void k_metadata_grid(SegGeo sg, const int32_t* meta, int64_t* out) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < sg.n_chunks;
+         c += (int64_t)gridDim.x * blockDim.x)
+        for_chunk_elements(sg, c, [&](int64_t, int64_t flat, int64_t seg) { out[flat] = (int64_t)meta[seg]; });
+}
+
+}  // namespace hszg
+
+using namespace hszg;
+
+int hszg_set_cuda_error(HszgErr* err, cudaError_t e, const char* where);
+int hszg_launch_decode(const HszgGeom* g, const HszgStream* s, int32_t* out, cudaStream_t st, HszgErr* err);
+
+static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+#define HSZG_CHECK_LAUNCH(where)                                           \
+    do {                                                                   \
+        cudaError_t _e = cudaGetLastError();                               \
+        if (_e != cudaSuccess) return hszg_set_cuda_error(err, _e, where); \
+    } while (0)
+
+static bool blocks_fit_tile(const SegGeo& sg) { return sg.cpb[0] <= TILE_CHUNKS; }
+
+// Stage 2 -> 3/4 on a stream-order int32 buffer `buf` (overwritten): the per-kind
+// recorrelation (compressors.py:201-226) followed by the output conversion.
+template <typename OutT>
+static int transform_decoded(const HszgGeom* g, const SegGeo& sg, const int32_t* meta, int32_t* buf, OutT* out,
+                             void* ws, size_t ws_bytes, cudaStream_t st, HszgErr* err) {
+    const double two_eps = 2.0 * g->eps;
+    const size_t need = (size_t)g->n * 4;
+    if (g->kind == HSZG_HSZP_ND) {
+        const int64_t N0 = sg.n[0], N1 = sg.n[1], N2 = sg.n[2];
+        k_row_scan<<<(unsigned)(N0 * N1), ROW_THREADS, 0, st>>>(buf, N2);
+        HSZG_CHECK_LAUNCH("row scan");
+        const bool zpass = N0 > 1;
+        if (N1 > 1) {
+            if (zpass) launch_col_scan<int32_t>(buf, N0, N1, N2, two_eps, buf, st);
+            else launch_col_scan<OutT>(buf, N0, N1, N2, two_eps, out, st);
+            HSZG_CHECK_LAUNCH("col scan y");
+        }
+        if (zpass) {
+            launch_col_scan<OutT>(buf, 1, N0, N1 * N2, two_eps, out, st);
+            HSZG_CHECK_LAUNCH("col scan z");
+        } else if (N1 <= 1) {
+            launch_col_scan<OutT>(buf, 1, 1, N2, two_eps, out, st);  // conversion only
+        }
+        return HSZG_OK;
+    }
+    if (g->kind == HSZG_HSZP) {
+        const int64_t tiles = (g->n + SCAN_TILE - 1) / SCAN_TILE;
+        if (ws_bytes < lookback_ws_bytes(g->n)) {
+            err->status = HSZG_INVALID_ARG;
+            snprintf(err->message, sizeof(err->message), "workspace too small for the flat scan");
+            return HSZG_INVALID_ARG;
+        }
+        LBState lb = lookback_carve(ws, tiles);
+        cudaMemsetAsync(ws, 0, lookback_clear_bytes(tiles), st);
+        k_scan_i32<<<(unsigned)tiles, SCAN_THREADS, 0, st>>>(buf, buf, g->n, lb);
+        HSZG_CHECK_LAUNCH("flat scan");
+        if (sizeof(OutT) != 4 || (void*)out != (void*)buf) launch_col_scan<OutT>(buf, 1, 1, g->n, two_eps, out, st);
+        else launch_col_scan<OutT>(buf, 1, 1, g->n, two_eps, out, st);
+        HSZG_CHECK_LAUNCH("convert");
+        return HSZG_OK;
+    }
+    // HSZX / HSZX_ND: add metadata (and scatter block-contiguous -> row-major), then convert
+    if (g->kind == HSZG_HSZX_ND) {
+        if (ws_bytes < need) {
+            err->status = HSZG_INVALID_ARG;
+            snprintf(err->message, sizeof(err->message), "workspace too small for block scatter");
+            return HSZG_INVALID_ARG;
+        }
+        int32_t* streamv = reinterpret_cast<int32_t*>(ws);
+        cudaMemcpyAsync(streamv, buf, need, cudaMemcpyDeviceToDevice, st);
+        k_scatter_grid<<<grid_for(g->n_chunks, 256, 148 * 64), 256, 0, st>>>(sg, streamv, meta, 1, buf);
+    } else {
+        k_scatter_grid<<<grid_for(g->n_chunks, 256, 148 * 64), 256, 0, st>>>(sg, buf, meta, 1, buf);
+    }
+    HSZG_CHECK_LAUNCH("scatter");
+    launch_col_scan<OutT>(buf, 1, 1, g->n, two_eps, out, st);  // M=1: pure conversion
+    HSZG_CHECK_LAUNCH("convert");
+    return HSZG_OK;
+}
+
+template <typename OutT>
+static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, void* ws, size_t ws_bytes,
+                             cudaStream_t st, HszgErr* err) {
+    const SegGeo sg = make_seggeo(*g);
+    const double two_eps = 2.0 * g->eps;
+    if (g->n == 0) return HSZG_OK;
+    const size_t smem = tile_smem_bytes(s->max_bitwidth);
+    const int64_t tiles = (g->n_chunks + TILE_CHUNKS - 1) / TILE_CHUNKS;
+    const bool fast = s->canonical != 0;
+    switch (g->kind) {
+        case HSZG_HSZX:
+            if (fast) {
+                k_tile_stream<true, OutT><<<(unsigned)tiles, TILE_CHUNKS, smem, st>>>(
+                    sg, s->payload, s->payload_len, s->offsets, s->metadata, two_eps, out);
+                HSZG_CHECK_LAUNCH("reconstruct hszx");
+                return HSZG_OK;
+            }
+            break;
+        case HSZG_HSZX_ND:
+            if (fast && blocks_fit_tile(sg)) {
+                BlockTiles bt;
+                // k full segments hold <= TILE_CHUNKS chunks, hence <= TILE_ELEMS values
+                bt.k = TILE_CHUNKS / sg.cpb[0];
+                bt.tpr = (sg.G[2] + bt.k - 1) / bt.k;
+                const int64_t nt = sg.G[0] * sg.G[1] * bt.tpr;
+                k_tile_blocks<OutT><<<(unsigned)nt, TILE_CHUNKS, smem, st>>>(sg, bt, s->payload, s->payload_len,
+                                                                               s->offsets, s->metadata, two_eps, out);
+                HSZG_CHECK_LAUNCH("reconstruct hszx-nd");
+                return HSZG_OK;
+            }
+            break;
+        case HSZG_HSZP:
+            if (fast) {
+                if (ws_bytes < lookback_ws_bytes(g->n_chunks)) break;
+                LBState lb = lookback_carve(ws, tiles);
+                cudaMemsetAsync(ws, 0, lookback_clear_bytes(tiles), st);
+                k_tile_scan<OutT><<<(unsigned)tiles, TILE_CHUNKS, smem, st>>>(sg, s->payload, s->payload_len,
+                                                                               s->offsets, lb, two_eps, out);
+                HSZG_CHECK_LAUNCH("reconstruct hszp");
+                return HSZG_OK;
+            }
+            break;
+        default:
+            break;
+    }
+    // generic path: stage-2 decode into an int32 buffer, then the per-kind transform
+    int32_t* buf;
+    const size_t need = (size_t)g->n * 4;
+    if (sizeof(OutT) == 4) {
+        buf = reinterpret_cast<int32_t*>(out);   // in place: int32 and fp32 have the same footprint
+    } else {
+        if (ws_bytes < need) {
+            err->status = HSZG_INVALID_ARG;
+            snprintf(err->message, sizeof(err->message), "workspace too small for reconstruct (%zu < %zu)",
+                     ws_bytes, need);
+            return HSZG_INVALID_ARG;
+        }
+        buf = reinterpret_cast<int32_t*>(ws);
+    }
+    int r = hszg_launch_decode(g, s, buf, st, err);
+    if (r) return r;
+    char* rest = reinterpret_cast<char*>(ws) + (sizeof(OutT) == 4 ? 0 : need);
+    const size_t rest_bytes = ws_bytes > (sizeof(OutT) == 4 ? 0 : need) ? ws_bytes - (sizeof(OutT) == 4 ? 0 : need) : 0;
+    return transform_decoded<OutT>(g, sg, s->metadata, buf, out, rest, rest_bytes, st, err);
+}
+
+extern "C" int hszg_reconstruct(const HszgGeom* g, const HszgStream* s, void* out, int out_type, void* ws,
+                                size_t ws_bytes, void* stream, HszgErr* err) {
+    err->status = HSZG_OK;
+    cudaStream_t st = as_stream(stream);
+    switch (out_type) {
+        case HSZG_I32: return reconstruct_typed<int32_t>(g, s, reinterpret_cast<int32_t*>(out), ws, ws_bytes, st, err);
+        case HSZG_F32: return reconstruct_typed<float>(g, s, reinterpret_cast<float*>(out), ws, ws_bytes, st, err);
+        case HSZG_F64: return reconstruct_typed<double>(g, s, reinterpret_cast<double*>(out), ws, ws_bytes, st, err);
+        default:
+            err->status = HSZG_INVALID_ARG;
+            snprintf(err->message, sizeof(err->message), "unknown output type %d", out_type);
+            return HSZG_INVALID_ARG;
+    }
+}
+
+extern "C" int hszg_stream_perm(const HszgGeom* g, int64_t* perm, void* stream) {
+    const SegGeo sg = make_seggeo(*g);
+    if (g->n_chunks == 0) return HSZG_OK;
+    k_stream_perm<<<grid_for(g->n_chunks, 256, 148 * 64), 256, 0, as_stream(stream)>>>(sg, perm);
+    return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
+}
+
+extern "C" int hszg_scatter_grid(const HszgGeom* g, const int32_t* src, const int32_t* metadata, int add_meta,
+                                 int32_t* out, void* stream) {
+    const SegGeo sg = make_seggeo(*g);
+    if (g->n_chunks == 0) return HSZG_OK;
+    k_scatter_grid<<<grid_for(g->n_chunks, 256, 148 * 64), 256, 0, as_stream(stream)>>>(sg, src, metadata, add_meta,
+                                                                                       out);
+    return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
+}
+
+extern "C" int hszg_metadata_grid(const HszgGeom* g, const int32_t* metadata, int64_t* out, void* stream) {
+    const SegGeo sg = make_seggeo(*g);
+    if (g->n_chunks == 0) return HSZG_OK;
+    k_metadata_grid<<<grid_for(g->n_chunks, 256, 148 * 64), 256, 0, as_stream(stream)>>>(sg, metadata, out);
+    return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
+}
+
+extern "C" int hszg_dequantize(const int32_t* q, int64_t n, double two_eps, void* out, int out_type, void* stream) {
+    if (n <= 0) return HSZG_OK;
+    cudaStream_t st = as_stream(stream);
+    const int grid = grid_for(n, 256 * 4, 148 * 32);
+    if (out_type == HSZG_F32) k_convert<float><<<grid, 256, 0, st>>>(q, n, two_eps, reinterpret_cast<float*>(out));
+    else if (out_type == HSZG_F64) k_convert<double><<<grid, 256, 0, st>>>(q, n, two_eps, reinterpret_cast<double*>(out));
+    else return HSZG_INVALID_ARG;
+    return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
+}
+
+template <typename OutT>
+static int recorrelate_typed(const HszgGeom* g, const int32_t* p, const int32_t* meta, OutT* out, void* ws,
+                             size_t ws_bytes, cudaStream_t st, HszgErr* err) {
+    const SegGeo sg = make_seggeo(*g);
+    const size_t need = (size_t)g->n * 4;
+    if (g->n == 0) return HSZG_OK;
+    int32_t* buf;
+    size_t head = 0;
+    if (sizeof(OutT) == 4) {
+        buf = reinterpret_cast<int32_t*>(out);
+    } else {
+        if (ws_bytes < need) {
+            err->status = HSZG_INVALID_ARG;
+            snprintf(err->message, sizeof(err->message), "workspace too small for recorrelate");
+            return HSZG_INVALID_ARG;
+        }
+        buf = reinterpret_cast<int32_t*>(ws);
+        head = need;
+    }
+    if ((const void*)buf != (const void*)p) cudaMemcpyAsync(buf, p, need, cudaMemcpyDeviceToDevice, st);
+    return transform_decoded<OutT>(g, sg, meta, buf, out, reinterpret_cast<char*>(ws) + head,
+                                   ws_bytes > head ? ws_bytes - head : 0, st, err);
+}
+
+extern "C" int hszg_recorrelate(const HszgGeom* g, const int32_t* p, const int32_t* metadata, void* out, int out_type,
+                                void* ws, size_t ws_bytes, void* stream, HszgErr* err) {
+    err->status = HSZG_OK;
+    cudaStream_t st = as_stream(stream);
+    switch (out_type) {
+        case HSZG_I32: return recorrelate_typed<int32_t>(g, p, metadata, reinterpret_cast<int32_t*>(out), ws, ws_bytes, st, err);
+        case HSZG_F32: return recorrelate_typed<float>(g, p, metadata, reinterpret_cast<float*>(out), ws, ws_bytes, st, err);
+        case HSZG_F64: return recorrelate_typed<double>(g, p, metadata, reinterpret_cast<double*>(out), ws, ws_bytes, st, err);
+        default: return HSZG_INVALID_ARG;
+    }
+}
+
+extern "C" int hszg_add_plane(int32_t* q, const int32_t* carry, int64_t plane, int64_t n, void* stream) {
+    if (n <= 0) return HSZG_OK;
+    k_add_plane<<<grid_for(n, 256 * 4, 148 * 32), 256, 0, as_stream(stream)>>>(q, carry, plane, n);
+    return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
+}

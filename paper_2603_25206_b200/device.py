@@ -1,0 +1,226 @@
+"""Device residency of a compressed stream and thin wrappers over the C ABI.
+
+``DeviceStream`` is the HBM mirror of a ``CompressedStream``: the payload
+(16-byte aligned, zero-padded), the chunk index and the block metadata,
+uploaded once.  The first use validates every chunk on the GPU
+(``hszg_validate``: the reference decoder's per-chunk checks,
+_bitpack.pyx:110-140, plus a proof that the index is the encoder's exclusive
+scan); later calls go straight to the fused kernels.  Everything here
+returns CUDA tensors; conversion to numpy happens in the drop-in modules.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+
+
+def _t():
+    return _lib.torch()
+
+
+class DeviceStream:
+    """A compressed stream resident in device memory."""
+
+    def __init__(self, kind, dims, block_dims, eps, payload_dev, payload_len, offsets_dev, metadata_dev=None):
+        t = _t()
+        self.kind = int(kind)
+        self.dims = tuple(int(d) for d in dims)
+        self.block_dims = tuple(int(b) for b in block_dims)
+        self.eps = float(eps)
+        self.payload = payload_dev            # uint8, len >= payload_len + PAYLOAD_PAD, 16-B aligned
+        self.payload_len = int(payload_len)
+        self.offsets = offsets_dev            # int64 view of uint64 offsets
+        self.metadata = metadata_dev          # int32 or None
+        self.geom = _lib.make_geom(self.kind, self.dims, self.block_dims, self.eps)
+        if self.offsets.numel() != self.geom.n_chunks:
+            from .errors import CorruptStreamError
+
+            raise CorruptStreamError("chunk index count disagrees with geometry")
+        assert payload_dev.dtype == t.uint8 and payload_dev.is_cuda
+        assert int(payload_dev.data_ptr()) % 16 == 0
+        self.desc = _lib.StreamDesc()
+        self.desc.payload = _lib.ptr(self.payload)
+        self.desc.payload_len = self.payload_len
+        self.desc.offsets = _lib.ptr(self.offsets)
+        self.desc.metadata = _lib.ptr(self.metadata) if self.metadata is not None else None
+        self.desc.canonical = 0
+        self.desc.max_bitwidth = 32
+        self.validated = False
+
+    # ---- construction -----------------------------------------------------------
+
+    @classmethod
+    def from_host(cls, kind, dims, block_dims, eps, payload: bytes, offsets, metadata=None):
+        t = _t()
+        dev = _lib.device()
+        n = len(payload)
+        buf = t.zeros(n + _lib.PAYLOAD_PAD, dtype=t.uint8, device=dev)
+        if n:
+            host = t.frombuffer(bytearray(payload), dtype=t.uint8)
+            buf[:n].copy_(host)
+        offs = np.ascontiguousarray(np.asarray(offsets, dtype=np.uint64)).view(np.int64)
+        offs_dev = t.from_numpy(offs.copy()).to(dev)
+        meta_dev = None
+        if metadata is not None:
+            meta_dev = t.from_numpy(np.ascontiguousarray(metadata, dtype=np.int32)).to(dev)
+        return cls(kind, dims, block_dims, eps, buf, n, offs_dev, meta_dev)
+
+    @property
+    def n(self) -> int:
+        return int(self.geom.n)
+
+    @property
+    def n_chunks(self) -> int:
+        return int(self.geom.n_chunks)
+
+    def nbytes(self) -> int:
+        """Container bytes resident on the device (payload + index + metadata)."""
+        meta = 0 if self.metadata is None else self.metadata.numel() * 4
+        return self.payload_len + self.n_chunks * 8 + meta
+
+    # ---- validation -----------------------------------------------------------------
+
+    def validate(self):
+        if self.validated:
+            return self
+        err = _lib.Err()
+        ws = _lib.workspace(_lib.ws_bytes(self.geom, None, _lib.WS_VALIDATE))
+        _lib.call("hszg_validate", ctypes.byref(self.geom), ctypes.byref(self.desc), _lib.ptr(ws), ws.numel(),
+                  _lib.stream_handle(), ctypes.byref(err), err=err)
+        self.validated = True
+        return self
+
+    # ---- stages ------------------------------------------------------------------
+
+    def decode(self, out=None):
+        """Stage 2: int32 residuals in stream order."""
+        t = _t()
+        self.validate()
+        if out is None:
+            out = t.empty(self.n, dtype=t.int32, device=_lib.device())
+        err = _lib.Err()
+        _lib.call("hszg_decode", ctypes.byref(self.geom), ctypes.byref(self.desc), _lib.ptr(out),
+                  _lib.stream_handle(), ctypes.byref(err), err=err)
+        return out
+
+    def reconstruct(self, dtype=None, out=None):
+        """Stage 3 (int32 q, row-major grid) or stage 4 (float32/float64 q*2eps)."""
+        t = _t()
+        self.validate()
+        dtype = dtype or t.int32
+        code = {t.int32: _lib.I32, t.float32: _lib.F32, t.float64: _lib.F64}[dtype]
+        if out is None:
+            out = t.empty(self.dims, dtype=dtype, device=_lib.device())
+        ws = _lib.workspace(_lib.ws_bytes(self.geom, self.desc, _lib.WS_RECONSTRUCT, code))
+        err = _lib.Err()
+        _lib.call("hszg_reconstruct", ctypes.byref(self.geom), ctypes.byref(self.desc), _lib.ptr(out), code,
+                  _lib.ptr(ws), ws.numel(), _lib.stream_handle(), ctypes.byref(err), err=err)
+        return out
+
+    # ---- reductions --------------------------------------------------------------
+
+    def reduce(self, mode: int, out=None):
+        """Fused reduction from the compressed bytes (see hszg_reduce_stream); device Sums buffer."""
+        self.validate()
+        out = _lib.sums_tensor() if out is None else out
+        ws = _lib.workspace(_lib.ws_bytes(self.geom, self.desc, _lib.WS_REDUCE))
+        err = _lib.Err()
+        _lib.call("hszg_reduce_stream", ctypes.byref(self.geom), ctypes.byref(self.desc), int(mode), _lib.ptr(out),
+                  _lib.ptr(ws), ws.numel(), _lib.stream_handle(), ctypes.byref(err), err=err)
+        return out
+
+
+# ---------------------------------------------------------------------------
+# array-level helpers (int32 CUDA tensors)
+
+REDUCE_WS = 148 * 16 * 64 + 4096
+
+
+def reduce_i32(x, out=None):
+    out = _lib.sums_tensor() if out is None else out
+    x = x.reshape(-1).contiguous()
+    ws = _lib.workspace(REDUCE_WS)
+    _lib.call("hszg_reduce_i32", _lib.ptr(x), x.numel(), _lib.ptr(out), _lib.ptr(ws), ws.numel(), _lib.stream_handle())
+    return out
+
+
+def reduce_dot(a, b, out=None):
+    out = _lib.sums_tensor() if out is None else out
+    a = a.reshape(-1).contiguous()
+    b = b.reshape(-1).contiguous()
+    ws = _lib.workspace(REDUCE_WS)
+    _lib.call("hszg_reduce_dot", _lib.ptr(a), _lib.ptr(b), a.numel(), _lib.ptr(out), _lib.ptr(ws), ws.numel(),
+              _lib.stream_handle())
+    return out
+
+
+def reduce_f64(q, scale, mean_dev=None, out=None):
+    out = _lib.sums_tensor() if out is None else out
+    q = q.reshape(-1).contiguous()
+    ws = _lib.workspace(REDUCE_WS)
+    _lib.call("hszg_reduce_f64", _lib.ptr(q), q.numel(), float(scale), _lib.ptr(mean_dev) if mean_dev is not None else None,
+              _lib.ptr(out), _lib.ptr(ws), ws.numel(), _lib.stream_handle())
+    return out
+
+
+def reduce_array(geom, p, metadata, mode, out=None):
+    out = _lib.sums_tensor() if out is None else out
+    ws = _lib.workspace(REDUCE_WS)
+    _lib.call("hszg_reduce_array", ctypes.byref(geom), _lib.ptr(p), _lib.ptr(metadata) if metadata is not None else None,
+              int(mode), _lib.ptr(out), _lib.ptr(ws), ws.numel(), _lib.stream_handle())
+    return out
+
+
+def stencil(op, q_list, eps_list, float_domain=False, dtype=None, outs=None):
+    """Run one K-STEN op over int32 grids; returns the list of output tensors."""
+    t = _t()
+    dtype = dtype or t.float64
+    code = _lib.F32 if dtype == t.float32 else _lib.F64
+    dims = tuple(q_list[0].shape)
+    nd = len(dims)
+    ncomp = len(q_list)
+    if op == _lib.OP_DERIV:
+        nout = nd
+    elif op == _lib.OP_CURL:
+        nout = 1 if ncomp == 2 else 3
+    else:
+        nout = 1
+    if outs is None:
+        outs = [t.empty(dims, dtype=dtype, device=_lib.device()) for _ in range(nout)]
+    qs = [q.contiguous() for q in q_list]
+    dims_arr = (ctypes.c_int64 * 3)(*(list(dims) + [1] * (3 - nd)))
+    qptr = (ctypes.c_void_p * 3)(*([_lib.ptr(q) for q in qs] + [None] * (3 - ncomp)))
+    eps_arr = (ctypes.c_double * 3)(*(list(map(float, eps_list)) + [0.0] * (3 - ncomp)))
+    optr = (ctypes.c_void_p * 3)(*([_lib.ptr(o) for o in outs] + [None] * (3 - nout)))
+    _lib.call("hszg_stencil", int(op), nd, ctypes.cast(dims_arr, ctypes.c_void_p), ncomp,
+              ctypes.cast(qptr, ctypes.c_void_p), ctypes.cast(eps_arr, ctypes.c_void_p), int(bool(float_domain)),
+              code, ctypes.cast(optr, ctypes.c_void_p), _lib.stream_handle())
+    return outs
+
+
+def region_reduce(q, region):
+    """Per-region exact (S1, S2, qmin, qmax, size) over an int32 grid (N2-N4)."""
+    t = _t()
+    dims = tuple(q.shape)
+    nd = len(dims)
+    reg = tuple(min(int(r), int(n)) for r, n in zip(region, dims))
+    grid = tuple(-(-n // r) for n, r in zip(dims, reg))
+    nr = int(np.prod(grid))
+    dev = _lib.device()
+    s1 = t.empty(nr, dtype=t.int64, device=dev)
+    s2lo = t.empty(nr, dtype=t.int64, device=dev)
+    s2hi = t.empty(nr, dtype=t.int64, device=dev)
+    qmin = t.empty(nr, dtype=t.int32, device=dev)
+    qmax = t.empty(nr, dtype=t.int32, device=dev)
+    size = t.empty(nr, dtype=t.int64, device=dev)
+    dims_arr = (ctypes.c_int64 * 3)(*(list(dims) + [1] * (3 - nd)))
+    reg_arr = (ctypes.c_int64 * 3)(*(list(reg) + [1] * (3 - nd)))
+    qc = q.contiguous()
+    _lib.call("hszg_region_reduce", _lib.ptr(qc), nd, ctypes.cast(dims_arr, ctypes.c_void_p),
+              ctypes.cast(reg_arr, ctypes.c_void_p), _lib.ptr(s1), _lib.ptr(s2lo), _lib.ptr(s2hi), _lib.ptr(qmin),
+              _lib.ptr(qmax), _lib.ptr(size), _lib.stream_handle())
+    return grid, s1, s2lo, s2hi, qmin, qmax, size
