@@ -1,0 +1,442 @@
+#!/usr/bin/env python
+"""bench.py — BASELINE.json headline workload on N B200s (one process per GPU).
+
+Workload (BASELINE configs[4], the one quoted for 1/2/4/8 GPUs): a 2048^3 fp32
+field (64 random 3-D sinusoid modes + Gaussian-smoothed noise, seed 5,
+generated on the device), rel error bound 1e-3 with the global value range,
+compressed as HSZP_ND and HSZX_ND and z-slab partitioned across the ranks
+(strong scaling).  One step = for each of the two compressed streams: exact
+global mean + variance (int128 sums, one all-gather) and the 3-component
+central-difference gradient + 5/7-point Laplacian straight from the
+compressed bytes (one int32 halo plane per neighbour, HSZP_ND Lorenzo carry
+by one all-gather), outputs written as fp32 grids.
+
+value      = 2 streams x 4 B x 2048^3 / step time   (GB/s of original fp32, whole job)
+e2e        = the same work from pinned HOST containers (H2D + validate + pipeline + D2H of every output)
+roofline   = the dominant kernel's algorithmic bytes / its CUDA-event time vs MEASURED_PEAKS hbm_gbs
+cpu_baseline = the reference path (oracle restatement: C codec + numpy) on a bounded sample, all host cores
+
+--impl reference runs that reference CPU path alone (rank 0) on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GB/s of original fp32 per decompress-stage+op, % of HBM roofline, 1/2/4/8 GPU"
+KINDS = (1, 3)              # HSZP_ND, HSZX_ND
+KIND_NAMES = {1: "hszp-nd", 3: "hszx-nd"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--dims", type=int, nargs=3, default=[2048, 2048, 2048])
+    ap.add_argument("--window", type=int, default=64)
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-planes", type=int, default=4, help="planes per CPU-sample sub-field")
+    ap.add_argument("--detail", default=None, help="write the per-kernel breakdown JSON here")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks (nvidia-smi sampled during the timed region)
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        import statistics
+
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for nm, v in zip(names, r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# helpers
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class EventTimer:
+    """CUDA events around each launch group on the launching (current) stream."""
+
+    def __init__(self):
+        import torch
+
+        self.torch = torch
+        self.open = {}
+        self.rec = {}
+
+    def begin(self, name):
+        e = self.torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.open[name] = e
+
+    def end(self, name, algo_bytes):
+        e = self.torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.rec.setdefault(name, []).append((self.open.pop(name), e, algo_bytes))
+
+    def summary(self):
+        self.torch.cuda.synchronize()
+        out = {}
+        for name, lst in self.rec.items():
+            ms = sum(a.elapsed_time(b) for a, b, _ in lst)
+            nbytes = sum(x for _, _, x in lst)
+            out[name] = {"launch_groups": len(lst), "ms": ms, "algo_bytes": nbytes,
+                         "gbs": nbytes / (ms / 1e3) / 1e9 if ms > 0 else None}
+        return out
+
+
+def count_kernel_launches(fn):
+    """Kernels launched by one call of fn, counted by CUPTI (torch.profiler); only libhszg kernels."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        fn()
+        torch.cuda.synchronize()
+    n = 0
+    names = {}
+    for evt in prof.events():
+        if evt.device_type == torch.autograd.DeviceType.CUDA and "hszg" in evt.name:
+            n += 1
+            key = evt.name.split("(")[0][:80]
+            names[key] = names.get(key, 0) + 1
+    return n, names
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2603_25206_b200 import _lib, pipeline, synthetic
+    from paper_2603_25206_b200.device import DeviceStream
+    from paper_2603_25206_b200.quant import field_minmax
+
+    comm = pipeline.Comm()
+    N0, N1, N2 = args.dims
+    n_total = N0 * N1 * N2
+    z0, z1 = pipeline.shard_planes(N0, world, rank, 16)
+    nz = z1 - z0
+    t_setup = time.time()
+
+    # ---- input: this rank's planes (+ one lead plane for the HSZP_ND predictor) -----------------
+    lead = 1 if z0 > 0 else 0
+    field = synthetic.gen_config5_slab(z0 - lead, z1, dims=(N0, N1, N2))
+    lo, hi, bad = field_minmax(field[lead:].reshape(-1))
+    mm = torch.tensor([lo, -hi], dtype=torch.float64, device="cuda")
+    comm.all_reduce(mm, "min")
+    eps = 1e-3 * (float(-mm[1]) - float(mm[0]))          # rel 1e-3 of the GLOBAL range (quant.py:56-66)
+    cpu_blobs = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu_blobs = build_cpu_sample(field[lead:], eps)
+    shards = {}
+    for kind in KINDS:
+        src = field if kind == 1 else field[lead:]
+        shards[kind] = pipeline.compress_shard(src, kind, eps, (8, 8, 8), z0, z1, (N0, N1, N2))
+    del field, src
+    torch.cuda.empty_cache()
+    for sh in shards.values():
+        sh.ds.validate()
+    outs = [torch.empty((nz, N1, N2), dtype=torch.float32, device="cuda") for _ in range(4)]
+    pipes = {k: pipeline.WindowPipeline(shards[k], comm, args.window) for k in KINDS}
+    container_bytes = {k: shards[k].ds.nbytes() for k in KINDS}
+    setup_s = time.time() - t_setup
+
+    results = {}
+
+    def step(timer=None):
+        for k in KINDS:
+            pipes[k].timer = timer
+            results[k] = pipes[k].run(outs)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    comm.barrier()
+    torch.cuda.synchronize()
+    timer = EventTimer()
+    with ClockSampler(local) as clocks:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for _ in range(args.steps):
+            step(timer)
+        ev1.record()
+        torch.cuda.synchronize()
+    comm.barrier()
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    tt = torch.tensor([ms_local], dtype=torch.float64, device="cuda")
+    comm.all_reduce(tt, "max")
+    ms = float(tt.item())
+    value = len(KINDS) * 4.0 * n_total / (ms / 1e3) / 1e9
+    kern = timer.summary()
+    launches_per_step, launch_names = count_kernel_launches(step)
+
+    # ---- roofline of the dominant kernel -----------------------------------------------------------
+    peak, peak_src = measured_peak()
+    dom = max(kern, key=lambda k: kern[k]["ms"])
+    d = kern[dom]
+    per_launch_bytes = d["algo_bytes"] / d["launch_groups"]
+    per_launch_ms = d["ms"] / d["launch_groups"]
+    achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
+                "share_of_step": round(d["ms"] / (ms * args.steps), 4)}
+
+    # ---- e2e: host containers in, every output back to the host ------------------------------------------
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, shards, pipes, outs, comm, n_total)
+
+    # ---- CPU baseline (rank 0, N = 1) ---------------------------------------------------------------
+    cpu = cpu_baseline(cpu_blobs) if cpu_blobs else None
+
+    if rank == 0:
+        s = results
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic: config-5 generator (64 random 3-D sinusoid modes + Gaussian-smoothed noise sigma 2, "
+                    "seed 5) generated on the device",
+            "config": {"workload": "config5: 2048^3 fp32, rel eb 1e-3, HSZP_ND + HSZX_ND streams; per step "
+                                   "global mean+variance and 3-comp gradient + Laplacian (fp32 out) from the "
+                                   "compressed bytes, z-slab sharded",
+                       "dims": [N0, N1, N2], "kinds": [KIND_NAMES[k] for k in KINDS], "window_planes": args.window,
+                       "eps": eps, "container_bytes_rank0": {KIND_NAMES[k]: container_bytes[k] for k in KINDS},
+                       "l2": "working set >> 126 MB L2 (inputs 5-8 GB, outputs 137 GB per stream)",
+                       "parallelism": f"z-slab x{world}", "setup_s": round(setup_s, 1)},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks.summary(),
+            "stats_check": {KIND_NAMES[k]: {"mean": s[k]["mean"], "var": s[k]["var"]} for k in KINDS},
+        }
+        print(json.dumps(line), flush=True)
+        if args.detail:
+            with open(args.detail, "w") as fh:
+                json.dump({"kernels": kern, "launch_names": launch_names, "launches_per_step": launches_per_step,
+                           "line": line}, fh, indent=1)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, shards, pipes, outs, comm, n_total):
+    """Containers from pinned host memory each step (+validation), outputs copied back to the host."""
+    import torch
+
+    host = {}
+    for k, sh in shards.items():
+        ds = sh.ds
+        host[k] = (ds.payload.cpu().pin_memory(), ds.offsets.cpu().pin_memory(),
+                   None if ds.metadata is None else ds.metadata.cpu().pin_memory())
+    stage = torch.empty(64 * 1024 * 1024, dtype=torch.float32).pin_memory()   # 256 MB staging
+    h2d = sum(sum(x.numel() * x.element_size() for x in host[k] if x is not None) for k in host)
+    d2h = 0
+
+    def e2e_step():
+        nonlocal d2h
+        moved = 0
+        for k, sh in shards.items():
+            ds = sh.ds
+            p, o, m = host[k]
+            ds.payload.copy_(p, non_blocking=True)
+            ds.offsets.copy_(o, non_blocking=True)
+            if m is not None:
+                ds.metadata.copy_(m, non_blocking=True)
+            ds.validated = False
+            ds.validate()                       # the reference decoder's checks, every call
+            pipes[k].run(outs)
+            for out in outs:                    # every output element back to host memory
+                flat = out.reshape(-1)
+                for s in range(0, flat.numel(), stage.numel()):
+                    n = min(stage.numel(), flat.numel() - s)
+                    stage[:n].copy_(flat[s:s + n])
+                    moved += 4 * n
+        d2h = moved
+
+    torch.cuda.synchronize()
+    comm.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        e2e_step()
+    torch.cuda.synchronize()
+    comm.barrier()
+    dt = (time.perf_counter() - t0) / args.e2e_steps
+    tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
+    comm.all_reduce(tt, "max")
+    dt = float(tt.item())
+    return {"value": round(len(KINDS) * 4.0 * n_total / dt / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "s_per_step": round(dt, 3),
+            "steps": args.e2e_steps, "path": "pinned host containers -> H2D -> hszg_validate -> windowed "
+                                             "pipeline -> D2H of all four fp32 outputs (per rank)"}
+
+
+def build_cpu_sample(field_dev, eps):
+    """The CPU sample's containers, compressed on the GPU (bit-identical to oracle.compress)."""
+    from oracle import cpu_pipeline as CP
+    from oracle import hsz_oracle as O
+    from paper_2603_25206_b200.compressors import compress_device
+
+    S = CP.sample_planes(CP.host_cores())
+    blobs = []
+    Z, N1, N2 = field_dev.shape
+    for z in range(0, min(S, Z) - CP.SUB_PLANES + 1, CP.SUB_PLANES):
+        for y in range(0, N1 - CP.SUB_ROWS + 1, CP.SUB_ROWS):
+            sub = field_dev[z:z + CP.SUB_PLANES, y:y + CP.SUB_ROWS].contiguous()
+            for kind in KINDS:
+                ds = compress_device(sub, kind, eps, (8, 8, 8))
+                meta = None if ds.metadata is None else ds.metadata.cpu().numpy().copy()
+                st = O.Stream(kind, ds.dims, ds.block_dims, eps, meta, ds.offsets.cpu().numpy().view("u8").copy(),
+                              ds.payload[:ds.payload_len].cpu().numpy().tobytes())
+                blobs.append(O.stream_to_bytes(st))
+    return blobs
+
+
+def cpu_baseline(blobs):
+    """The reference CPU path (oracle restatement) on the bounded sample, one process per host core."""
+    from oracle import cpu_pipeline as CP
+
+    cores = CP.host_cores()
+    pool = CP.make_pool(cores)
+    CP.run_sample(blobs[: max(1, min(len(blobs), cores))], pool)     # warm the workers
+    dt, elems, _ = CP.run_sample(blobs, pool)
+    if pool is not None:
+        pool.shutdown()
+    return {"value": round(4.0 * elems / dt / 1e9, 4), "unit": "GB/s", "cores": cores, "kind": "port",
+            "sample": f"{len(blobs)} containers of {CP.SUB_PLANES}x{CP.SUB_ROWS}x2048 from the config-5 field "
+                      f"({elems} values, HSZP_ND + HSZX_ND): oracle decode + recorrelate + exact sums + gradient "
+                      f"+ Laplacian, {min(cores, len(blobs))} processes, {dt:.2f} s"}
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import cpu_pipeline as CP
+
+    N0, N1, N2 = args.dims
+    cores = CP.host_cores()
+    S = CP.sample_planes(cores)
+    t0 = time.time()
+    field = CP.config5_sample_field(0, S, (N0, N1, N2))
+    eps = 1e-3 * (float(field.max()) - float(field.min()))   # sample range (the full field is not built here)
+    pool = CP.make_pool(cores)
+    blobs = CP.make_sample(CP.bands(field), KINDS, eps, pool)
+    del field
+    setup_s = time.time() - t0
+    for _ in range(args.warmup):
+        CP.run_sample(blobs, pool)
+    times = []
+    elems = 0
+    for _ in range(args.steps):
+        dt, elems, _ = CP.run_sample(blobs, pool)
+        times.append(dt)
+    if pool is not None:
+        pool.shutdown()
+    dt = sum(times) / len(times)
+    value = 4.0 * elems / dt / 1e9
+    sample = (f"{len(blobs)} containers of {CP.SUB_PLANES}x{CP.SUB_ROWS}x{N2} (planes 0-{S - 1} of the config-5 "
+              f"field, HSZP_ND + HSZX_ND, {elems} values per step), {min(cores, len(blobs))} processes")
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 1), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic: config-5 generator restated on the host (seed 5)",
+            "config": {"workload": "config5 bounded sample: per sub-field decode + recorrelate + exact mean/variance "
+                                   "sums + 3-comp gradient + Laplacian (reference path: oracle restatement)",
+                       "dims": [N0, N1, N2], "kinds": [KIND_NAMES[k] for k in KINDS], "setup_s": round(setup_s, 1)},
+            "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

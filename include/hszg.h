@@ -146,6 +146,10 @@ int hszg_reconstruct(const HszgGeom* g, const HszgStream* s, void* out, int out_
 /* recorrelate (compressors.py:201-226) of a decoded stream-order residual array p (not overwritten). */
 int hszg_recorrelate(const HszgGeom* g, const int32_t* p, const int32_t* metadata, void* out, int out_type, void* ws,
                      size_t ws_bytes, void* stream, HszgErr* err);
+/* HSZP_ND z-slab carry support (3-D, validated canonical stream): plane_out[y,x] = sum_z p[z,y,x]
+ * (int32 wrap-around), straight from the compressed bytes.  Its 2-D prefix is the slab's total
+ * contribution to every later plane. */
+int hszg_plane_sum(const HszgGeom* g, const HszgStream* s, int32_t* plane_out, void* stream, HszgErr* err);
 /* q[i] += carry[i % plane] for i < n (slab carries of slab_iter, stages.py:193-204). */
 int hszg_add_plane(int32_t* q, const int32_t* carry, int64_t plane, int64_t n, void* stream);
 /* Stage 3 -> 4 on a materialised index array: out = float(q) * two_eps (stages.py:88). */
@@ -202,13 +206,23 @@ enum {
     HSZG_OP_LAPLACIAN = 1,  /* out[0] = L(q) * 2eps (stage 2/3) or float stencil (stage 4)     */
     HSZG_OP_GRADMAG = 2,    /* out[0] = eps * sqrt(sum_k D_k^2)  (N5)                          */
     HSZG_OP_DIVERGENCE = 3, /* out[0] = sum_k D_k(q_k) * eps_k   (fields.py:216-222)           */
-    HSZG_OP_CURL = 4        /* out[...] = curl components        (fields.py:225-236)           */
+    HSZG_OP_CURL = 4,       /* out[...] = curl components        (fields.py:225-236)           */
+    HSZG_OP_GRAD_LAP = 5    /* out[0..nd-1] = derivatives, out[nd] = Laplacian, one pass         */
 };
 /* q[c]: row-major grids (c < ncomp); eps[c] per component.  float_domain 0: int32 indices with
  * integer stencils (stage 2/3); 1: int32 indices read as fl(q*2eps) with the float stencils of
  * fields.py:83-93 (stage 4); 2: float64 input grids, float stencils.  out[k]: HSZG_F32/F64 grids. */
 int hszg_stencil(int op, int32_t ndims, const int64_t* dims, int32_t ncomp, const void* const* q,
                  const double* eps, int float_domain, int32_t out_type, void* const* out, void* stream);
+
+/* Windowed 3-D stencil: computes box planes [zlo, zhi) of the (n0,n1,n2) int32 grids q, whose plane 0
+ * sits at global axis-0 coordinate gz0 of a field with gN0 planes (boundary layers are global);
+ * out[k] receives planes [zlo, zhi) contiguously.  Used by the windowed / sharded pipelines. */
+int hszg_stencil_window(int op, const int64_t* dims, int32_t ncomp, const void* const* q, const double* eps,
+                        int float_domain, int32_t out_type, void* const* out, int64_t zlo, int64_t zhi,
+                        int64_t gz0, int64_t gN0, void* stream);
+/* Combine an array of HszgSums (e.g. per-window partials) into one, deterministically. */
+int hszg_sums_combine(const HszgSums* parts, int64_t n, HszgSums* out, void* stream);
 
 /* ---- encode side (K-ENC) ------------------------------------------------ */
 /* min/max + NaN/Inf count of an fp32 field (resolve_eps, quant.py:56-66): out_dev = {min, max}

@@ -31,7 +31,7 @@ PAYLOAD_PAD = 16
 OK, CORRUPT, EPS_TOO_SMALL, INVALID_ARG, UNSUPPORTED_STAGE, CUDA_ERR, ZERO_RANGE, VALUE = range(8)
 I32, F32, F64 = 0, 1, 2
 WS_VALIDATE, WS_RECONSTRUCT, WS_REDUCE, WS_ENCODE, WS_QUANTIZE = range(5)
-OP_DERIV, OP_LAPLACIAN, OP_GRADMAG, OP_DIVERGENCE, OP_CURL = range(5)
+OP_DERIV, OP_LAPLACIAN, OP_GRADMAG, OP_DIVERGENCE, OP_CURL, OP_GRAD_LAP = range(6)
 
 
 class Geom(ctypes.Structure):
@@ -125,6 +125,7 @@ _SIGS = {
     "hszg_dequantize": [_P, _I64, _D, _P, _I32, _P],
     "hszg_recorrelate": [ctypes.POINTER(Geom), _P, _P, _P, _I32, _P, _SZ, _P, ctypes.POINTER(Err)],
     "hszg_add_plane": [_P, _P, _I64, _I64, _P],
+    "hszg_plane_sum": [ctypes.POINTER(Geom), ctypes.POINTER(StreamDesc), _P, _P, ctypes.POINTER(Err)],
     "hszg_stream_perm": [ctypes.POINTER(Geom), _P, _P],
     "hszg_scatter_grid": [ctypes.POINTER(Geom), _P, _P, _I32, _P, _P],
     "hszg_metadata_grid": [ctypes.POINTER(Geom), _P, _P, _P],
@@ -138,6 +139,8 @@ _SIGS = {
     "hszg_region_finalize": [_P, _P, _P, _P, _P, _P, _I64, _D, _D, _P, _P, _P, _P, _P, _P],
     "hszg_reduce_flt": [_P, _I64, _P, _P, _P, _SZ, _P],
     "hszg_stencil": [_I32, ctypes.c_int32, _P, ctypes.c_int32, _P, _P, _I32, ctypes.c_int32, _P, _P],
+    "hszg_stencil_window": [_I32, _P, ctypes.c_int32, _P, _P, _I32, ctypes.c_int32, _P, _I64, _I64, _I64, _I64, _P],
+    "hszg_sums_combine": [_P, _I64, _P, _P],
     "hszg_minmax_f32": [_P, _I64, _P, _P, _P, _SZ, _P],
     "hszg_minmax_f64": [_P, _I64, _P, _P, _P, _SZ, _P],
     "hszg_quantize_f32": [_P, _I64, _D, _P, _P, _SZ, _P, ctypes.POINTER(Err)],

@@ -292,8 +292,13 @@ struct StencilArgs {
     const void* q[3];
     double eps[3];
     double two_eps[3];
-    void* out[3];
+    void* out[4];
+    int64_t zlo;        // first box plane (axis 0) to compute; outputs are indexed from it
+    int64_t gz0;        // global axis-0 coordinate of box plane 0 (window / rank offset)
+    int64_t gN0;        // global axis-0 extent (boundary layers are global)
 };
+
+__device__ __forceinline__ int64_t gext(const StencilArgs& A, int a) { return a == 0 ? A.gN0 : A.n[a]; }
 
 __device__ __forceinline__ void put(const StencilArgs& A, int k, int64_t i, double v) {
     if (A.out_type == HSZG_F32) reinterpret_cast<float*>(A.out[k])[i] = __double2float_rn(v);
@@ -314,7 +319,7 @@ __device__ __forceinline__ double deriv(const StencilArgs& A, int c, int k, cons
                                         int64_t* dint) {
     const int a = 3 - A.nd + k;
     const int64_t s = a == 2 ? 1 : (a == 1 ? A.n[2] : A.n[1] * A.n[2]);
-    if (idx[a] == 0 || idx[a] == A.n[a] - 1) {
+    if (idx[a] == 0 || idx[a] == gext(A, a) - 1) {
         if (dint) *dint = 0;
         return 0.0;
     }
@@ -324,48 +329,50 @@ __device__ __forceinline__ double deriv(const StencilArgs& A, int c, int k, cons
     return __dmul_rn((double)d, A.eps[c]);                   // fields.py:70
 }
 
+__device__ __forceinline__ double laplacian_at(const StencilArgs& A, const int64_t* idx, int64_t i) {
+    for (int k = 0; k < A.nd; k++) {
+        const int a = 3 - A.nd + k;
+        if (!(idx[a] > 0 && idx[a] < gext(A, a) - 1)) return 0.0;
+    }
+    if (A.float_domain) {
+        // fields.py:47-60 on float64 values: acc = (-2*nd)*v; acc = acc + lo + hi per axis
+        double acc = __dmul_rn((double)(-2 * A.nd), fv(A, 0, i));
+        for (int k = 0; k < A.nd; k++) {
+            const int a = 3 - A.nd + k;
+            const int64_t st = a == 2 ? 1 : (a == 1 ? A.n[2] : A.n[1] * A.n[2]);
+            acc = __dadd_rn(acc, fv(A, 0, i - st));
+            acc = __dadd_rn(acc, fv(A, 0, i + st));
+        }
+        return acc;
+    }
+    int64_t acc = -2 * (int64_t)A.nd * qv(A, 0, i);
+    for (int k = 0; k < A.nd; k++) {
+        const int a = 3 - A.nd + k;
+        const int64_t st = a == 2 ? 1 : (a == 1 ? A.n[2] : A.n[1] * A.n[2]);
+        acc += (int64_t)qv(A, 0, i - st) + (int64_t)qv(A, 0, i + st);
+    }
+    return __dmul_rn((double)acc, A.two_eps[0]);   // fields.py:79
+}
+
 __global__ void k_stencil(StencilArgs A) {
     const int64_t i2 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i2 >= A.n[2]) return;
     const int64_t i1 = blockIdx.y;
-    const int64_t i0 = blockIdx.z;
-    const int64_t idx[3] = {i0, i1, i2};
-    const int64_t i = (i0 * A.n[1] + i1) * A.n[2] + i2;
+    const int64_t i0 = A.zlo + blockIdx.z;
+    const int64_t idx[3] = {A.gz0 + i0, i1, i2};          // global coordinates (boundary tests)
+    const int64_t i = (i0 * A.n[1] + i1) * A.n[2] + i2;   // input index
+    const int64_t oi = ((i0 - A.zlo) * A.n[1] + i1) * A.n[2] + i2;   // output index
     switch (A.op) {
         case HSZG_OP_DERIV:
-            for (int k = 0; k < A.nd; k++) put(A, k, i, deriv(A, 0, k, idx, i, nullptr));
+            for (int k = 0; k < A.nd; k++) put(A, k, oi, deriv(A, 0, k, idx, i, nullptr));
             break;
-        case HSZG_OP_LAPLACIAN: {
-            bool interior = true;
-            for (int k = 0; k < A.nd; k++) {
-                const int a = 3 - A.nd + k;
-                interior &= idx[a] > 0 && idx[a] < A.n[a] - 1;
-            }
-            if (!interior) {
-                put(A, 0, i, 0.0);
-                break;
-            }
-            if (A.float_domain) {
-                // fields.py:47-60 on float64 values: acc = (-2*nd)*v; acc = acc + lo + hi per axis
-                double acc = __dmul_rn((double)(-2 * A.nd), fv(A, 0, i));
-                for (int k = 0; k < A.nd; k++) {
-                    const int a = 3 - A.nd + k;
-                    const int64_t st = a == 2 ? 1 : (a == 1 ? A.n[2] : A.n[1] * A.n[2]);
-                    acc = __dadd_rn(acc, fv(A, 0, i - st));
-                    acc = __dadd_rn(acc, fv(A, 0, i + st));
-                }
-                put(A, 0, i, acc);
-            } else {
-                int64_t acc = -2 * (int64_t)A.nd * qv(A, 0, i);
-                for (int k = 0; k < A.nd; k++) {
-                    const int a = 3 - A.nd + k;
-                    const int64_t st = a == 2 ? 1 : (a == 1 ? A.n[2] : A.n[1] * A.n[2]);
-                    acc += (int64_t)qv(A, 0, i - st) + (int64_t)qv(A, 0, i + st);
-                }
-                put(A, 0, i, __dmul_rn((double)acc, A.two_eps[0]));   // fields.py:79
-            }
+        case HSZG_OP_LAPLACIAN:
+            put(A, 0, oi, laplacian_at(A, idx, i));
             break;
-        }
+        case HSZG_OP_GRAD_LAP:
+            for (int k = 0; k < A.nd; k++) put(A, k, oi, deriv(A, 0, k, idx, i, nullptr));
+            put(A, A.nd, oi, laplacian_at(A, idx, i));
+            break;
         case HSZG_OP_GRADMAG: {
             if (A.float_domain) {
                 double s = 0.0;
@@ -373,7 +380,7 @@ __global__ void k_stencil(StencilArgs A) {
                     const double d = deriv(A, 0, k, idx, i, nullptr);
                     s = __dadd_rn(s, __dmul_rn(d, d));
                 }
-                put(A, 0, i, __dsqrt_rn(s));
+                put(A, 0, oi, __dsqrt_rn(s));
             } else {
                 u128 s = 0;
                 for (int k = 0; k < A.nd; k++) {
@@ -386,23 +393,23 @@ __global__ void k_stencil(StencilArgs A) {
                 if ((uint64_t)(s >> 64) == 0) sd = __ull2double_rn((uint64_t)s);
                 else sd = __dadd_rn(__dmul_rn(__ull2double_rn((uint64_t)(s >> 64)), 18446744073709551616.0),
                                     __ull2double_rn((uint64_t)s));
-                put(A, 0, i, __dmul_rn(__dsqrt_rn(sd), A.eps[0]));
+                put(A, 0, oi, __dmul_rn(__dsqrt_rn(sd), A.eps[0]));
             }
             break;
         }
         case HSZG_OP_DIVERGENCE: {
             double acc = deriv(A, 0, 0, idx, i, nullptr);        // fields.py:219-221
             for (int k = 1; k < A.ncomp; k++) acc = __dadd_rn(acc, deriv(A, k, k, idx, i, nullptr));
-            put(A, 0, i, acc);
+            put(A, 0, oi, acc);
             break;
         }
         case HSZG_OP_CURL: {
             if (A.ncomp == 2) {                                     // fields.py:228-231
-                put(A, 0, i, __dsub_rn(deriv(A, 0, 1, idx, i, nullptr), deriv(A, 1, 0, idx, i, nullptr)));
+                put(A, 0, oi, __dsub_rn(deriv(A, 0, 1, idx, i, nullptr), deriv(A, 1, 0, idx, i, nullptr)));
             } else {                                                // fields.py:232-236
-                put(A, 0, i, __dsub_rn(deriv(A, 2, 1, idx, i, nullptr), deriv(A, 1, 2, idx, i, nullptr)));
-                put(A, 1, i, __dsub_rn(deriv(A, 0, 2, idx, i, nullptr), deriv(A, 2, 0, idx, i, nullptr)));
-                put(A, 2, i, __dsub_rn(deriv(A, 1, 0, idx, i, nullptr), deriv(A, 0, 1, idx, i, nullptr)));
+                put(A, 0, oi, __dsub_rn(deriv(A, 2, 1, idx, i, nullptr), deriv(A, 1, 2, idx, i, nullptr)));
+                put(A, 1, oi, __dsub_rn(deriv(A, 0, 2, idx, i, nullptr), deriv(A, 2, 0, idx, i, nullptr)));
+                put(A, 2, oi, __dsub_rn(deriv(A, 1, 0, idx, i, nullptr), deriv(A, 0, 1, idx, i, nullptr)));
             }
             break;
         }
@@ -562,8 +569,27 @@ extern "C" int hszg_region_reduce(const int32_t* q, int32_t ndims, const int64_t
     return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
 }
 
+static int stencil_impl(int op, int32_t ndims, const int64_t* dims, int32_t ncomp, const void* const* q,
+                        const double* eps, int float_domain, int32_t out_type, void* const* out, int64_t zlo,
+                        int64_t zhi, int64_t gz0, int64_t gN0, cudaStream_t st);
+
 extern "C" int hszg_stencil(int op, int32_t ndims, const int64_t* dims, int32_t ncomp, const void* const* q,
                             const double* eps, int float_domain, int32_t out_type, void* const* out, void* stream) {
+    const int64_t n0 = ndims == 3 ? dims[0] : 1;
+    return stencil_impl(op, ndims, dims, ncomp, q, eps, float_domain, out_type, out, 0, n0, 0, n0,
+                        as_stream(stream));
+}
+
+extern "C" int hszg_stencil_window(int op, const int64_t* dims, int32_t ncomp, const void* const* q, const double* eps,
+                                   int float_domain, int32_t out_type, void* const* out, int64_t zlo, int64_t zhi,
+                                   int64_t gz0, int64_t gN0, void* stream) {
+    return stencil_impl(op, 3, dims, ncomp, q, eps, float_domain, out_type, out, zlo, zhi, gz0, gN0,
+                        as_stream(stream));
+}
+
+static int stencil_impl(int op, int32_t ndims, const int64_t* dims, int32_t ncomp, const void* const* q,
+                        const double* eps, int float_domain, int32_t out_type, void* const* out, int64_t zlo,
+                        int64_t zhi, int64_t gz0, int64_t gN0, cudaStream_t st) {
     if (ndims < 1 || ndims > 3 || ncomp < 1 || ncomp > 3) return HSZG_INVALID_ARG;
     if (out_type != HSZG_F32 && out_type != HSZG_F64) return HSZG_INVALID_ARG;
     StencilArgs A = {};
@@ -580,12 +606,17 @@ extern "C" int hszg_stencil(int op, int32_t ndims, const int64_t* dims, int32_t 
     }
     int nout = 1;
     if (op == HSZG_OP_DERIV) nout = ndims;
+    if (op == HSZG_OP_GRAD_LAP) nout = ndims + 1;
     if (op == HSZG_OP_CURL) nout = ncomp == 2 ? 1 : 3;
     for (int k = 0; k < nout; k++) A.out[k] = out[k];
-    if (A.n[1] > 65535 || A.n[0] > 65535) return HSZG_INVALID_ARG;
-    dim3 grid((unsigned)((A.n[2] + 255) / 256), (unsigned)A.n[1], (unsigned)A.n[0]);
+    A.zlo = zlo;
+    A.gz0 = gz0;
+    A.gN0 = gN0;
+    if (zhi - zlo < 1) return HSZG_OK;
+    if (A.n[1] > 65535 || zhi - zlo > 65535) return HSZG_INVALID_ARG;
+    dim3 grid((unsigned)((A.n[2] + 255) / 256), (unsigned)A.n[1], (unsigned)(zhi - zlo));
     if (A.n[0] * A.n[1] * A.n[2] == 0) return HSZG_OK;
-    k_stencil<<<grid, 256, 0, as_stream(stream)>>>(A);
+    k_stencil<<<grid, 256, 0, st>>>(A);
     return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
 }
 
@@ -609,4 +640,8 @@ extern "C" int hszg_reduce_flt(const double* x, int64_t n, const double* mean_de
     const int grid = grid_for(n, RED_THREADS * 8, kMaxParts);
     k_reduce_flt<<<grid, RED_THREADS, 0, st>>>(x, n, mean_dev, partials);
     return finalize(partials, grid, out_dev, st);
+}
+
+extern "C" int hszg_sums_combine(const HszgSums* parts, int64_t n, HszgSums* out, void* stream) {
+    return finalize(const_cast<HszgSums*>(parts), n, out, as_stream(stream));
 }

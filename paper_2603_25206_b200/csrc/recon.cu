@@ -547,3 +547,40 @@ extern "C" int hszg_add_plane(int32_t* q, const int32_t* carry, int64_t plane, i
     k_add_plane<<<grid_for(n, 256 * 4, 148 * 32), 256, 0, as_stream(stream)>>>(q, carry, plane, n);
     return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
 }
+
+// ---- HSZP_ND shard carry: U[y,x] = sum_z p[z,y,x] over a stream's planes (wrap-around int32) ----
+// the carry plane of a z-slab is the 2-D prefix of this plane sum (Lorenzo linearity).
+namespace hszg {
+__global__ void __launch_bounds__(TILE_CHUNKS) k_plane_sum(SegGeo sg, const uint8_t* payload, uint64_t len,
+                                                          const uint64_t* offsets, int64_t plane,
+                                                          unsigned int* U) {
+    TileCtx t = tile_stage(sg, payload, len, offsets, blockIdx.x);
+    const int64_t c = t.c0 + threadIdx.x;
+    if (c < t.c1) {
+        const ChunkLoc L = locate_chunk(sg, c);
+        const int64_t base = L.start % plane;
+        decode_chunk_words(t.words, (uint32_t)(offsets[c] - t.base), L.count, [&](int j, int32_t v) {
+            if (v) atomicAdd(U + base + j, (unsigned int)v);
+        });
+    }
+}
+}  // namespace hszg
+
+extern "C" int hszg_plane_sum(const HszgGeom* g, const HszgStream* s, int32_t* plane_out, void* stream, HszgErr* err) {
+    err->status = HSZG_OK;
+    cudaStream_t st = as_stream(stream);
+    const SegGeo sg = make_seggeo(*g);
+    if (g->kind != HSZG_HSZP_ND || g->ndims != 3 || !s->canonical) {
+        err->status = HSZG_INVALID_ARG;
+        snprintf(err->message, sizeof(err->message), "plane_sum needs a validated canonical 3-D HSZP_ND stream");
+        return HSZG_INVALID_ARG;
+    }
+    const int64_t plane = sg.n[1] * sg.n[2];
+    cudaMemsetAsync(plane_out, 0, (size_t)plane * 4, st);
+    if (g->n_chunks == 0) return HSZG_OK;
+    const int64_t tiles = (g->n_chunks + TILE_CHUNKS - 1) / TILE_CHUNKS;
+    k_plane_sum<<<(unsigned)tiles, TILE_CHUNKS, tile_smem_bytes(s->max_bitwidth), st>>>(
+        sg, s->payload, s->payload_len, s->offsets, plane, reinterpret_cast<unsigned int*>(plane_out));
+    HSZG_CHECK_LAUNCH("plane sum");
+    return HSZG_OK;
+}

@@ -82,6 +82,43 @@ class DeviceStream:
         meta = 0 if self.metadata is None else self.metadata.numel() * 4
         return self.payload_len + self.n_chunks * 8 + meta
 
+    def plane_view(self, s: int, e: int) -> "DeviceStream":
+        """Sub-stream of axis-0 planes [s, e) of a 2-D/3-D HSZP_ND or HSZX_ND stream (zero-copy).
+
+        Chunks restart at every segment (compressors.py:105-119), so the planes form a contiguous chunk
+        range: same payload pointer, a slice of the index and of the metadata, and the payload length cut
+        at the range's last byte.  HSZX_ND ranges must be block-row aligned.
+        """
+        n0 = self.dims[0]
+        if not (0 <= s < e <= n0):
+            raise ValueError(f"plane range [{s}, {e}) outside [0, {n0})")
+        nc = self.n_chunks
+        if self.kind == 1:
+            cpp = nc // n0
+            first, last = s * cpp, e * cpp
+            meta = None
+        elif self.kind == 3:
+            b0 = self.block_dims[0]
+            if s % b0 or (e % b0 and e != n0):
+                raise ValueError("HSZX_ND plane ranges must be block-row aligned")
+            g = self.geom
+            per_row_blocks = int(g.sgrid[1] * g.sgrid[2])
+            full_row_chunks = _full_row_chunks(self)
+            first = (s // b0) * full_row_chunks
+            last = (e // b0) * full_row_chunks if e < n0 else nc
+            meta = self.metadata[(s // b0) * per_row_blocks:(-(-e // b0)) * per_row_blocks]
+        else:
+            raise ValueError("plane views need an nd kind")
+        offs = self.offsets[first:last]
+        end = int(self.offsets[last].item()) if last < nc else self.payload_len
+        dims = (e - s,) + self.dims[1:]
+        bd = tuple(min(b, n) for b, n in zip(self.block_dims, dims))
+        sub = DeviceStream(self.kind, dims, bd, self.eps, self.payload, end, offs, meta)
+        sub.desc.canonical = self.desc.canonical
+        sub.desc.max_bitwidth = self.desc.max_bitwidth
+        sub.validated = self.validated
+        return sub
+
     # ---- validation -----------------------------------------------------------------
 
     def validate(self):
@@ -134,6 +171,23 @@ class DeviceStream:
         return out
 
 
+def _full_row_chunks(ds: DeviceStream) -> int:
+    """Chunks in one full-thickness block-row of an HSZX_ND stream (closed form, host side)."""
+    if ds.dims[0] <= ds.block_dims[0]:
+        return ds.n_chunks
+    # first chunk of block-row 1 = chunks of block-row 0; found by bisection on the chunk starts
+    row_elems = ds.block_dims[0] * int(np.prod(ds.dims[1:]))
+    lo, hi = 0, ds.n_chunks
+    while lo < hi:
+        mid = (lo + hi) // 2
+        s, _, _ = _lib.locate_chunks(ds.geom, mid, 1)
+        if s[0] < row_elems:
+            lo = mid + 1
+        else:
+            hi = mid
+    return lo
+
+
 # ---------------------------------------------------------------------------
 # array-level helpers (int32 CUDA tensors)
 
@@ -175,31 +229,61 @@ def reduce_array(geom, p, metadata, mode, out=None):
     return out
 
 
+def _nout(op, nd, ncomp):
+    if op == _lib.OP_DERIV:
+        return nd
+    if op == _lib.OP_GRAD_LAP:
+        return nd + 1
+    if op == _lib.OP_CURL:
+        return 1 if ncomp == 2 else 3
+    return 1
+
+
+def _stencil_arrays(q_list, eps_list, outs):
+    dims = tuple(q_list[0].shape)
+    nd = len(dims)
+    ncomp = len(q_list)
+    dims_arr = (ctypes.c_int64 * 3)(*(list(dims) + [1] * (3 - nd)))
+    qptr = (ctypes.c_void_p * 3)(*([_lib.ptr(q) for q in q_list] + [None] * (3 - ncomp)))
+    eps_arr = (ctypes.c_double * 3)(*(list(map(float, eps_list)) + [0.0] * (3 - ncomp)))
+    optr = (ctypes.c_void_p * 4)(*([_lib.ptr(o) for o in outs] + [None] * (4 - len(outs))))
+    return dims_arr, qptr, eps_arr, optr
+
+
 def stencil(op, q_list, eps_list, float_domain=False, dtype=None, outs=None):
-    """Run one K-STEN op over int32 grids; returns the list of output tensors."""
+    """Run one K-STEN op over int32 (or float64, float_domain=2) grids; returns the output tensors."""
     t = _t()
     dtype = dtype or t.float64
     code = _lib.F32 if dtype == t.float32 else _lib.F64
     dims = tuple(q_list[0].shape)
     nd = len(dims)
-    ncomp = len(q_list)
-    if op == _lib.OP_DERIV:
-        nout = nd
-    elif op == _lib.OP_CURL:
-        nout = 1 if ncomp == 2 else 3
-    else:
-        nout = 1
+    nout = _nout(op, nd, len(q_list))
     if outs is None:
         outs = [t.empty(dims, dtype=dtype, device=_lib.device()) for _ in range(nout)]
     qs = [q.contiguous() for q in q_list]
-    dims_arr = (ctypes.c_int64 * 3)(*(list(dims) + [1] * (3 - nd)))
-    qptr = (ctypes.c_void_p * 3)(*([_lib.ptr(q) for q in qs] + [None] * (3 - ncomp)))
-    eps_arr = (ctypes.c_double * 3)(*(list(map(float, eps_list)) + [0.0] * (3 - ncomp)))
-    optr = (ctypes.c_void_p * 3)(*([_lib.ptr(o) for o in outs] + [None] * (3 - nout)))
-    _lib.call("hszg_stencil", int(op), nd, ctypes.cast(dims_arr, ctypes.c_void_p), ncomp,
-              ctypes.cast(qptr, ctypes.c_void_p), ctypes.cast(eps_arr, ctypes.c_void_p), int(bool(float_domain)),
+    dims_arr, qptr, eps_arr, optr = _stencil_arrays(qs, eps_list, outs)
+    _lib.call("hszg_stencil", int(op), nd, ctypes.cast(dims_arr, ctypes.c_void_p), len(qs),
+              ctypes.cast(qptr, ctypes.c_void_p), ctypes.cast(eps_arr, ctypes.c_void_p), int(float_domain),
               code, ctypes.cast(optr, ctypes.c_void_p), _lib.stream_handle())
     return outs
+
+
+def stencil_window(op, q_list, eps_list, outs, zlo, zhi, gz0, gN0, float_domain=False):
+    """3-D stencil over box planes [zlo, zhi) of q (plane 0 at global z = gz0 of gN0 planes) into outs."""
+    t = _t()
+    code = _lib.F32 if outs[0].dtype == t.float32 else _lib.F64
+    dims_arr, qptr, eps_arr, optr = _stencil_arrays(q_list, eps_list, outs)
+    _lib.call("hszg_stencil_window", int(op), ctypes.cast(dims_arr, ctypes.c_void_p), len(q_list),
+              ctypes.cast(qptr, ctypes.c_void_p), ctypes.cast(eps_arr, ctypes.c_void_p), int(float_domain), code,
+              ctypes.cast(optr, ctypes.c_void_p), int(zlo), int(zhi), int(gz0), int(gN0), _lib.stream_handle())
+    return outs
+
+
+def sums_combine(parts_buf, n, out=None):
+    """Combine n consecutive HszgSums records (uint8 CUDA buffer) into one."""
+    out = _lib.sums_tensor() if out is None else out
+    _lib.call("hszg_sums_combine", _lib.ptr(parts_buf), int(n), _lib.ptr(out), _lib.stream_handle())
+    return out
 
 
 def region_reduce(q, region):

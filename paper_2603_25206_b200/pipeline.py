@@ -1,0 +1,405 @@
+"""Windowed, z-slab-sharded analytics over 3-D compressed fields.
+
+Two reference mechanisms meet here:
+
+* Algorithm 3, the out-of-core sliding window (stages.py:173-258,
+  fields.py:243-272): a rank walks its planes in windows of
+  W planes, reconstructing q into a small device buffer (prefix carry for
+  HSZP_ND, block-row granularity for HSZX_ND) and running the fused
+  gradient+Laplacian stencil on it, so q is never materialised for the whole
+  field (2048^3 outputs alone are 137 GB of HBM).
+* the z-slab partition of SURVEY §8(e) across 1/2/4/8 GPUs (one process per
+  GPU, torch.distributed over NCCL): every rank owns planes [z0, z1) of the
+  global stream (a contiguous chunk range, bit-identical to the global
+  container), exchanges one int32 halo plane with each neighbour, HSZP_ND
+  ranks combine their slab-total planes with one all-gather (Lorenzo carry,
+  exact in int32 wrap-around), and the global mean/variance is the exact
+  int128 combination of the per-rank sums (one all-gather of 64-byte
+  records; Python-int finalisation as stats.py:58-62).
+
+The exchange helpers only use torch.distributed collectives on tensors, so
+the same code runs on NCCL/CUDA in production and on gloo/CPU in the
+multi-process CPU tests.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+HSZP_ND, HSZX_ND = 1, 3
+SUMS_BYTES = 64
+
+
+# ---------------------------------------------------------------------------
+# communication plumbing
+
+
+class Comm:
+    """Rank/world and the few collectives the pipeline needs (no-ops at world size 1)."""
+
+    def __init__(self, group=None):
+        try:
+            import torch.distributed as dist
+
+            ok = dist.is_available() and dist.is_initialized()
+        except Exception:  # noqa: BLE001
+            ok = False
+        self.dist = dist if ok else None
+        self.group = group
+        self.rank = dist.get_rank(group) if ok else 0
+        self.world = dist.get_world_size(group) if ok else 1
+
+    def all_gather(self, t):
+        """List of every rank's tensor (same shape/dtype)."""
+        if self.world == 1:
+            return [t]
+        import torch
+
+        outs = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(outs, t.contiguous(), group=self.group)
+        return outs
+
+    def all_reduce(self, t, op: str):
+        if self.world == 1:
+            return t
+        ops = {"sum": self.dist.ReduceOp.SUM, "min": self.dist.ReduceOp.MIN, "max": self.dist.ReduceOp.MAX}
+        self.dist.all_reduce(t, op=ops[op], group=self.group)
+        return t
+
+    def exchange(self, to_lower, to_upper, like):
+        """Send `to_lower` to rank-1 and `to_upper` to rank+1; return (from_lower, from_upper).
+
+        `like` gives the shape/dtype/device of the received planes; missing neighbours give None.
+        """
+        if self.world == 1:
+            return None, None
+        import torch
+
+        reqs = []
+        from_lower = from_upper = None
+        r, w = self.rank, self.world
+        if r > 0:
+            from_lower = torch.empty_like(like)
+            reqs.append(self.dist.irecv(from_lower, r - 1, group=self.group))
+            reqs.append(self.dist.isend(to_lower.contiguous(), r - 1, group=self.group))
+        if r < w - 1:
+            from_upper = torch.empty_like(like)
+            reqs.append(self.dist.irecv(from_upper, r + 1, group=self.group))
+            reqs.append(self.dist.isend(to_upper.contiguous(), r + 1, group=self.group))
+        for q in reqs:
+            q.wait()
+        return from_lower, from_upper
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier(group=self.group)
+
+
+def shard_planes(n0: int, world: int, rank: int, align: int = 16) -> tuple:
+    """Rank's plane range [z0, z1): contiguous, boundaries multiples of `align` (block depth x region)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    units = -(-n0 // align)
+    bounds = [min(n0, (units * r // world) * align) for r in range(world + 1)]
+    bounds[-1] = n0
+    z0, z1 = bounds[rank], bounds[rank + 1]
+    if z1 <= z0:
+        raise ValueError(f"{n0} planes cannot feed {world} ranks at {align}-plane alignment")
+    return z0, z1
+
+
+def exclusive_plane_prefix(planes, rank: int):
+    """C_rank = sum_{g < rank} T_g (int32 wrap-around) — the Lorenzo carry of a z-slab."""
+    import torch
+
+    acc = torch.zeros_like(planes[0])
+    for g in range(rank):
+        acc = (acc.to(torch.int64) + planes[g].to(torch.int64)).remainder(2**32)
+        acc = torch.where(acc >= 2**31, acc - 2**32, acc).to(planes[0].dtype)
+    return acc
+
+
+def sums_to_ints(buf) -> dict:
+    """Decode one 64-byte HszgSums record (host bytes or tensor) into exact Python ints."""
+    raw = bytes(buf.cpu().numpy().tobytes()) if hasattr(buf, "cpu") else bytes(buf)
+    s = _lib.Sums.from_buffer_copy(raw)
+    return dict(s1=s.s1, s2=s.s2, count=int(s.count), vmin=int(s.vmin), vmax=int(s.vmax))
+
+
+def combine_rank_sums(comm: Comm, local_sums_buf) -> dict:
+    """Exact global (sum q, sum q^2, count, min, max) from every rank's int128 record (one all-gather)."""
+    parts = comm.all_gather(local_sums_buf)
+    tot = dict(s1=0, s2=0, count=0, vmin=2**31, vmax=-(2**31))
+    for p in parts:
+        d = sums_to_ints(p)
+        tot["s1"] += d["s1"]
+        tot["s2"] += d["s2"]
+        tot["count"] += d["count"]
+        tot["vmin"] = min(tot["vmin"], d["vmin"])
+        tot["vmax"] = max(tot["vmax"], d["vmax"])
+    return tot
+
+
+def finalize_mean_var(s1: int, s2: int, n: int, eps: float) -> tuple:
+    """(mean, variance) with the reference's exact expressions (stats.py:58-62, 115-118; N1)."""
+    mean = s1 / n * (2.0 * eps)
+    var = (s2 * n - s1 * s1) / (n * (n - 1)) * ((2.0 * eps) * (2.0 * eps))
+    return mean, var
+
+
+# ---------------------------------------------------------------------------
+# sharded containers
+
+
+@dataclass
+class ShardedField:
+    """One rank's share of a z-partitioned 3-D compressed field."""
+
+    kind: int
+    eps: float
+    global_dims: tuple      # (N0, n1, n2)
+    block_dims: tuple
+    z0: int
+    z1: int
+    ds: object              # DeviceStream over planes [z0, z1)
+
+    @property
+    def nz(self) -> int:
+        return self.z1 - self.z0
+
+
+def compress_shard(field_dev, kind: int, eps: float, block_dims, z0: int, z1: int, global_dims) -> ShardedField:
+    """Compress planes [z0, z1) so the chunks equal the global stream's chunk range for those planes.
+
+    field_dev holds planes [z0 - lead, z1) where lead = 1 for HSZP_ND with z0 > 0 (the Lorenzo
+    predictor reads the previous plane; the lead plane's chunks are dropped — SURVEY §8(c)), else 0.
+    HSZX_ND needs z0 on a block-row boundary.  eps must be the GLOBAL absolute bound.
+    """
+    from .compressors import compress_device
+    from .device import DeviceStream
+
+    t = _lib.torch()
+    lead = 1 if (kind == HSZP_ND and z0 > 0) else 0
+    if field_dev.shape[0] != z1 - z0 + lead:
+        raise ValueError("field slab does not match the plane range (+ lead plane)")
+    if kind == HSZX_ND and z0 % block_dims[0]:
+        raise ValueError("HSZX_ND shards must start on a block-row boundary")
+    dims = tuple(field_dev.shape)
+    bd = tuple(min(b, n) for b, n in zip(block_dims, dims))
+    full = compress_device(field_dev, kind, eps, bd)
+    if not lead:
+        return ShardedField(kind, eps, tuple(global_dims), tuple(block_dims), z0, z1, full)
+    cpp = full.n_chunks // dims[0]
+    off0 = int(full.offsets[cpp].item())
+    plen = full.payload_len - off0
+    payload = t.zeros(plen + _lib.PAYLOAD_PAD, dtype=t.uint8, device=_lib.device())
+    payload[:plen].copy_(full.payload[off0:full.payload_len])
+    offs = full.offsets[cpp:] - off0
+    local_dims = (z1 - z0,) + dims[1:]
+    local_bd = tuple(min(b, n) for b, n in zip(block_dims, local_dims))
+    ds = DeviceStream(kind, local_dims, local_bd, eps, payload, plen, offs.contiguous(), None)
+    del full
+    return ShardedField(kind, eps, tuple(global_dims), tuple(block_dims), z0, z1, ds)
+
+
+# ---------------------------------------------------------------------------
+# the windowed pipeline
+
+
+class WindowPipeline:
+    """Global mean/variance + 3-component gradient + Laplacian of one rank's shard, window by window."""
+
+    def __init__(self, sf: ShardedField, comm: Comm | None = None, window: int = 64):
+        t = _lib.torch()
+        self.sf = sf
+        self.comm = comm or Comm()
+        self.ds = sf.ds.validate()
+        self.G = 1 if sf.kind == HSZP_ND else sf.ds.block_dims[0]
+        self.W = max(self.G, (window // self.G) * self.G)
+        n1, n2 = sf.global_dims[1], sf.global_dims[2]
+        self.plane = n1 * n2
+        cap = self.W + self.G + 2
+        self.buf = t.empty((cap, n1, n2), dtype=t.int32, device=_lib.device())
+        self.nwin = -(-sf.nz // self.W)
+        self.win_sums = t.zeros(max(self.nwin, 1) * SUMS_BYTES, dtype=t.uint8, device=_lib.device())
+        self.halo_lo = None
+        self.halo_hi = None
+        self.timer = None          # optional EventTimer (bench.py): CUDA events per launch group
+
+    def _range_bytes(self, s: int, e: int) -> int:
+        """Compressed bytes of local planes [s, e): payload range + 8 B per chunk + 4 B per block mean."""
+        if not hasattr(self, "_chunk_off_host"):
+            self._chunk_off_host = self.ds.offsets.cpu().numpy()
+            self._cpp = self.ds.n_chunks / self.sf.nz
+        nc = self.ds.n_chunks
+        c0 = int(round(s * self._cpp))
+        c1 = nc if e >= self.sf.nz else int(round(e * self._cpp))
+        p0 = int(self._chunk_off_host[c0]) if c0 < nc else self.ds.payload_len
+        p1 = int(self._chunk_off_host[c1]) if c1 < nc else self.ds.payload_len
+        meta = 0 if self.ds.metadata is None else 4 * self.ds.metadata.numel() * (e - s) // self.sf.nz
+        return (p1 - p0) + 8 * (c1 - c0) + meta
+
+    # -- per-container collective setup (inside the timed step: it depends on the data) -------
+    def _decode_planes(self, s: int, e: int, out):
+        """q of local planes [s, e) into `out` (no carry)."""
+        sub = self.ds.plane_view(s, e)
+        return sub.reconstruct(_lib.torch().int32, out=out)
+
+    def prepare(self):
+        comm = self.comm
+        mine = self.local_boundary(need_total=comm.world > 1)
+        gathered = comm.all_gather(mine["T"]) if mine.get("T") is not None else None
+        carry = self.carry_from(gathered, comm.rank)
+        first = self.finish_first(mine, carry)
+        lo, hi = comm.exchange(first if first is not None else mine["head"], mine["tail"], mine["tail"])
+        self.apply_boundary(carry, lo, hi)
+
+    # The three phases below are split so a multi-rank run can also be emulated rank by rank
+    # in one process (tests/test_gpu_pipeline.py); prepare() runs them around the collectives.
+    def local_boundary(self, need_total: bool) -> dict:
+        """Boundary planes computable from this rank's bytes alone.
+
+        HSZP_ND: the local 2-D prefix of the first plane, and (multi-rank) the slab total
+        T = P2(sum_z p) whose exclusive prefix over ranks is the Lorenzo carry.
+        HSZX_ND: q of the first and last planes (halos of the neighbours).
+        """
+        t = _lib.torch()
+        sf = self.sf
+        n1, n2 = sf.global_dims[1], sf.global_dims[2]
+        out = {"T": None, "head": None, "tail": None}
+        if sf.kind == HSZP_ND:
+            first = t.empty((1, n1, n2), dtype=t.int32, device=_lib.device())
+            self._decode_planes(0, 1, first)                     # P2(p[z0]) (local prefix)
+            out["first_local"] = first
+            if need_total:
+                U = t.empty((n1, n2), dtype=t.int32, device=_lib.device())
+                err = _lib.Err()
+                _lib.call("hszg_plane_sum", ctypes.byref(self.ds.geom), ctypes.byref(self.ds.desc), _lib.ptr(U),
+                          _lib.stream_handle(), ctypes.byref(err), err=err)
+                out["T"] = _plane_prefix(U)                      # slab total = P2(sum_z p)
+            out["tail"] = first[0]                               # placeholder shape for the exchange
+        else:
+            B0 = self.G
+            lo_rows = min(B0, sf.nz)
+            head = t.empty((lo_rows, n1, n2), dtype=t.int32, device=_lib.device())
+            self._decode_planes(0, lo_rows, head)
+            s_last = ((sf.nz - 1) // B0) * B0
+            tail = t.empty((sf.nz - s_last, n1, n2), dtype=t.int32, device=_lib.device())
+            self._decode_planes(s_last, sf.nz, tail)
+            out["head"], out["tail"] = head[0], tail[-1]
+        return out
+
+    def carry_from(self, gathered_T, rank: int):
+        """HSZP_ND carry C_rank = q[z0 - 1] from every rank's slab total (None for HSZX_ND)."""
+        if self.sf.kind != HSZP_ND:
+            return None
+        t = _lib.torch()
+        n1, n2 = self.sf.global_dims[1], self.sf.global_dims[2]
+        if gathered_T is None:
+            return t.zeros((n1, n2), dtype=t.int32, device=_lib.device())
+        return exclusive_plane_prefix(gathered_T, rank)
+
+    def finish_first(self, mine: dict, carry):
+        """HSZP_ND: q[z0] = C + P2(p[z0]) — the plane sent to rank-1 as its upper halo."""
+        if self.sf.kind != HSZP_ND:
+            return None
+        first = mine["first_local"]
+        _lib.call("hszg_add_plane", _lib.ptr(first), _lib.ptr(carry), self.plane, self.plane, _lib.stream_handle())
+        return first[0]
+
+    def apply_boundary(self, carry, from_lower, from_upper):
+        self.carry = carry                                       # = q[z0 - 1] (HSZP_ND)
+        if self.sf.kind == HSZP_ND:
+            self.halo_lo = carry if self.sf.z0 > 0 else None
+        else:
+            self.halo_lo = from_lower
+        self.halo_hi = from_upper
+
+    def run_prepared(self, outs, stats: bool = True):
+        """run() after the boundary phases were applied by the caller (single-process emulation)."""
+        return self.run(outs, stats, _prepared=True)
+
+    # -- the windowed pass ---------------------------------------------------------------
+    def run(self, outs, stats: bool = True, _prepared: bool = False):
+        """Fill outs = [dz, dy, dx, laplacian] (float tensors of shape (nz, n1, n2)); return global stats."""
+        from . import device as devmod
+
+        sf, buf, W, G = self.sf, self.buf, self.W, self.G
+        nz = sf.nz
+        if not _prepared:
+            self.prepare()
+        if self.halo_lo is not None:
+            buf[0].copy_(self.halo_lo)
+        decoded = 0                                      # next local plane to decode
+        for w, a in enumerate(range(0, nz, W)):
+            b = min(a + W, nz)
+            need = min(b + 1, nz)
+            if decoded < need:
+                e = min(nz, -(-need // G) * G)
+                s = decoded
+                if self.timer:
+                    self.timer.begin("reconstruct")
+                self._decode_planes(s, e, buf[s - a + 1:e - a + 1])
+                if sf.kind == HSZP_ND:
+                    carry = buf[s - a] if (s > 0 or sf.z0 > 0) else None
+                    if s == 0 and sf.z0 > 0:
+                        carry = self.carry
+                    if carry is not None:
+                        _lib.call("hszg_add_plane", _lib.ptr(buf[s - a + 1]), _lib.ptr(carry), self.plane,
+                                  (e - s) * self.plane, _lib.stream_handle())
+                if self.timer:
+                    self.timer.end("reconstruct", self._range_bytes(s, e) + 4 * (e - s) * self.plane)
+                decoded = e
+            if b == nz and self.halo_hi is not None:
+                buf[b - a + 1].copy_(self.halo_hi)
+            if self.timer:
+                self.timer.begin("stencil")
+            devmod.stencil_window(_lib.OP_GRAD_LAP, [buf], [sf.eps], [o[a:b] for o in outs], 1, 1 + (b - a),
+                                  sf.z0 + a - 1, sf.global_dims[0])
+            if self.timer:
+                self.timer.end("stencil", (4 + 4 * len(outs)) * (b - a) * self.plane)
+            if stats and sf.kind == HSZP_ND:
+                if self.timer:
+                    self.timer.begin("stats")
+                devmod.reduce_i32(buf[1:1 + (b - a)], out=self.win_sums[w * SUMS_BYTES:(w + 1) * SUMS_BYTES])
+                if self.timer:
+                    self.timer.end("stats", 4 * (b - a) * self.plane)
+            if b < nz:                                   # slide: planes [b-1, decoded) to the front
+                for k, z in enumerate(range(b - 1, decoded)):
+                    buf[k].copy_(buf[z - a + 1])
+        if not stats:
+            return None
+        if sf.kind == HSZP_ND:
+            local = devmod.sums_combine(self.win_sums, self.nwin)
+        else:
+            if self.timer:
+                self.timer.begin("stats")
+            local = self.ds.reduce(3)                    # fused: sum q, sum q^2 from the bytes (no scatter)
+            if self.timer:
+                self.timer.end("stats", self._range_bytes(0, nz))
+        self.local_sums = local
+        if _prepared:
+            return sums_to_ints(local)               # emulated rank: the caller combines
+        tot = combine_rank_sums(self.comm, local)
+        n = int(np.prod(sf.global_dims))
+        mean, var = finalize_mean_var(tot["s1"], tot["s2"], n, sf.eps)
+        return dict(mean=mean, var=var, **tot)
+
+
+def _plane_prefix(U):
+    """2-D inclusive prefix of an int32 plane (the Lorenzo inverse of a 2-D HSZP_ND stream)."""
+    t = _lib.torch()
+    n1, n2 = U.shape
+    g = _lib.make_geom(HSZP_ND, (n1, n2), (min(8, n1), min(8, n2)), 1.0)
+    out = t.empty((n1, n2), dtype=t.int32, device=_lib.device())
+    ws = _lib.workspace(_lib.ws_bytes(g, None, _lib.WS_RECONSTRUCT, _lib.I32))
+    err = _lib.Err()
+    _lib.call("hszg_recorrelate", ctypes.byref(g), _lib.ptr(U), None, _lib.ptr(out), _lib.I32, _lib.ptr(ws),
+              ws.numel(), _lib.stream_handle(), ctypes.byref(err), err=err)
+    return out
