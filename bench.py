@@ -164,7 +164,12 @@ def count_kernel_launches(fn):
         if evt.device_type == torch.autograd.DeviceType.CUDA and "hszg" in evt.name:
             n += 1
             key = evt.name.split("(")[0][:80]
-            names[key] = names.get(key, 0) + 1
+            rec = names.setdefault(key, {"launches": 0, "us": 0.0})
+            rec["launches"] += 1
+            dt = getattr(evt, "device_time", None)
+            if dt is None:
+                dt = getattr(evt, "cuda_time", 0.0)
+            rec["us"] += float(dt or 0.0)
     return n, names
 
 

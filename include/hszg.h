@@ -36,6 +36,7 @@ extern "C" {
 #endif
 
 #define HSZG_PAYLOAD_PAD 16
+#define HSZG_END_IN_INDEX (1ull << 63)
 
 /* status codes (hsz/errors.py) */
 enum {
@@ -76,7 +77,8 @@ typedef struct HszgGeom {
 /* A device-resident compressed stream (payload + chunk index + metadata). */
 typedef struct HszgStream {
     const uint8_t* payload;   /* 16-B aligned, len + HSZG_PAYLOAD_PAD bytes allocated */
-    uint64_t payload_len;
+    uint64_t payload_len;     /* or HSZG_END_IN_INDEX: the end is offsets[n_chunks] (a view into a longer
+                                 resident index whose next entry exists; set only on validated streams) */
     const uint64_t* offsets;  /* n_chunks byte offsets into payload */
     const int32_t* metadata;  /* n_blocks block means (HSZX*), else NULL */
     int32_t canonical;        /* 1 = offsets are the encoder's exclusive scan (set by hszg_validate) */

@@ -119,6 +119,14 @@ HSZG_HD ChunkLoc locate_chunk(const SegGeo& s, int64_t c) {
     return L;
 }
 
+// End of the stream's last chunk.  A plane view of a larger resident stream (sub-range of
+// its chunk index) passes payload_len with the top bit set: the end is then the parent
+// index entry just past the view, offsets[n_chunks] — no host round trip to look it up.
+constexpr uint64_t kEndInIndex = 1ull << 63;
+__device__ __forceinline__ uint64_t payload_end(const uint64_t* offsets, int64_t n_chunks, uint64_t len) {
+    return (len & kEndInIndex) ? offsets[n_chunks] : len;
+}
+
 // byte size of a chunk (_fallback.py:52-55)
 HSZG_HD int64_t chunk_bytes(int64_t count, int bw) {
     return bw == 0 ? 1 : 1 + (count + 7) / 8 + (count * bw + 7) / 8;

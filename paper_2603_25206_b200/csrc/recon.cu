@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_tile_blocks(SegGeo sg, BlockTil
         const int64_t last = b2b - 1;
         s_c1 = seg_chunk_start(sg, b0, b1, last) + sg.cpb[(c0cls << 2) | (c1cls << 1) | (last == sg.G[2] - 1)];
         s_lo = offsets[s_c0];
-        s_hi = s_c1 < sg.n_chunks ? offsets[s_c1] : len;
+        s_hi = s_c1 < sg.n_chunks ? offsets[s_c1] : payload_end(offsets, sg.n_chunks, len);
         s_e0 = seg_elem_start(sg, b0, b1, b2a);
     }
     __syncthreads();

@@ -46,7 +46,7 @@ __device__ __forceinline__ TileCtx tile_stage(const SegGeo& sg, const uint8_t* p
     t.c1 = t.c0 + TILE_CHUNKS < sg.n_chunks ? t.c0 + TILE_CHUNKS : sg.n_chunks;
     if (threadIdx.x == 0) {
         s_lo = offsets[t.c0];
-        s_hi = t.c1 < sg.n_chunks ? offsets[t.c1] : len;
+        s_hi = t.c1 < sg.n_chunks ? offsets[t.c1] : payload_end(offsets, sg.n_chunks, len);
         s_e0 = locate_chunk(sg, t.c0).start;
         s_e1 = t.c1 < sg.n_chunks ? locate_chunk(sg, t.c1).start : sg.total;
     }

@@ -25,7 +25,8 @@ def _t():
 class DeviceStream:
     """A compressed stream resident in device memory."""
 
-    def __init__(self, kind, dims, block_dims, eps, payload_dev, payload_len, offsets_dev, metadata_dev=None):
+    def __init__(self, kind, dims, block_dims, eps, payload_dev, payload_len, offsets_dev, metadata_dev=None,
+                 end_in_index: bool = False):
         t = _t()
         self.kind = int(kind)
         self.dims = tuple(int(d) for d in dims)
@@ -44,7 +45,8 @@ class DeviceStream:
         assert int(payload_dev.data_ptr()) % 16 == 0
         self.desc = _lib.StreamDesc()
         self.desc.payload = _lib.ptr(self.payload)
-        self.desc.payload_len = self.payload_len
+        # views of a longer resident index read their end from offsets[n_chunks] (no host sync)
+        self.desc.payload_len = (1 << 63) if end_in_index else self.payload_len
         self.desc.offsets = _lib.ptr(self.offsets)
         self.desc.metadata = _lib.ptr(self.metadata) if self.metadata is not None else None
         self.desc.canonical = 0
@@ -103,17 +105,20 @@ class DeviceStream:
                 raise ValueError("HSZX_ND plane ranges must be block-row aligned")
             g = self.geom
             per_row_blocks = int(g.sgrid[1] * g.sgrid[2])
-            full_row_chunks = _full_row_chunks(self)
+            if not hasattr(self, "_row_chunks"):
+                self._row_chunks = _full_row_chunks(self)
+            full_row_chunks = self._row_chunks
             first = (s // b0) * full_row_chunks
             last = (e // b0) * full_row_chunks if e < n0 else nc
             meta = self.metadata[(s // b0) * per_row_blocks:(-(-e // b0)) * per_row_blocks]
         else:
             raise ValueError("plane views need an nd kind")
         offs = self.offsets[first:last]
-        end = int(self.offsets[last].item()) if last < nc else self.payload_len
+        in_index = last < nc
         dims = (e - s,) + self.dims[1:]
         bd = tuple(min(b, n) for b, n in zip(self.block_dims, dims))
-        sub = DeviceStream(self.kind, dims, bd, self.eps, self.payload, end, offs, meta)
+        sub = DeviceStream(self.kind, dims, bd, self.eps, self.payload, self.payload_len, offs, meta,
+                           end_in_index=in_index or self.desc.payload_len == (1 << 63))
         sub.desc.canonical = self.desc.canonical
         sub.desc.max_bitwidth = self.desc.max_bitwidth
         sub.validated = self.validated
