@@ -325,6 +325,7 @@ int hszg_launch_decode(const HszgGeom* g, const HszgStream* s, int32_t* out, cud
     if (s->canonical) {
         const int64_t tiles = (g->n_chunks + TILE_CHUNKS - 1) / TILE_CHUNKS;
         const size_t smem = tile_smem_bytes(s->max_bitwidth);
+        allow_smem(k_decode_tiles, smem);
         k_decode_tiles<<<(unsigned)tiles, TILE_CHUNKS, smem, st>>>(sg, s->payload, s->payload_len, s->offsets, out);
     } else {
         GeoSpans sp{sg};

@@ -475,9 +475,11 @@ extern "C" int hszg_reduce_stream(const HszgGeom* g, const HszgStream* s, int mo
         }
         const size_t smem = tile_smem_bytes(s->max_bitwidth);
         if (mode == 3)
+            allow_smem(k_reduce_tiles<MetaChunk>, smem),
             k_reduce_tiles<MetaChunk><<<(unsigned)tiles, TILE_CHUNKS, smem, st>>>(sg, s->payload, s->payload_len,
                                                                                 s->offsets, s->metadata, partials);
         else
+            allow_smem(k_reduce_tiles<WeightedChunk>, smem),
             k_reduce_tiles<WeightedChunk><<<(unsigned)tiles, TILE_CHUNKS, smem, st>>>(
                 sg, s->payload, s->payload_len, s->offsets, s->metadata, partials);
         if (cudaGetLastError() != cudaSuccess) return hszg_set_cuda_error(err, cudaGetLastError(), "reduce tiles");
@@ -587,9 +589,95 @@ extern "C" int hszg_stencil_window(int op, const int64_t* dims, int32_t ncomp, c
                         as_stream(stream));
 }
 
+// ---- the hot stencil: 3-D gradient (3 comps) + Laplacian of int32 q into fp32 grids -------------
+// Four x-consecutive points per thread: one 16-B load per neighbour row (x+-1 from the adjacent
+// lanes by shuffle), fp64 scaling exactly as fields.py:70/79 (one rounding) then one cast to fp32,
+// and 16-B streaming stores (evict-first: the q window stays in L2 for its z/y neighbours).
+namespace hszg {
+
+__device__ __forceinline__ float4 scale4(int64_t a, int64_t b, int64_t c, int64_t d, double s) {
+    return make_float4(__double2float_rn(__dmul_rn((double)a, s)), __double2float_rn(__dmul_rn((double)b, s)),
+                       __double2float_rn(__dmul_rn((double)c, s)), __double2float_rn(__dmul_rn((double)d, s)));
+}
+
+constexpr int GL_THREADS = 128;   // 512 x-points per CTA row
+
+__global__ void __launch_bounds__(GL_THREADS) k_grad_lap_f32(const int32_t* __restrict__ q, int64_t n1, int64_t n2,
+                                                             int64_t zlo, int64_t gz0, int64_t gN0, double eps,
+                                                             double two_eps, float* __restrict__ o0,
+                                                             float* __restrict__ o1, float* __restrict__ o2,
+                                                             float* __restrict__ o3) {
+    const int lane = threadIdx.x & 31;
+    const int64_t x = ((int64_t)blockIdx.x * GL_THREADS + threadIdx.x) * 4;
+    const int64_t y = blockIdx.y;
+    const int64_t z = zlo + blockIdx.z;               // box plane
+    const int64_t gz = gz0 + z;                       // global plane
+    const int64_t plane = n1 * n2;
+    const bool active = x < n2;
+    const int64_t xi = active ? x : 0;
+    const int32_t* row = q + z * plane + y * n2;
+    int4 c = make_int4(0, 0, 0, 0);
+    if (active) c = __ldg(reinterpret_cast<const int4*>(row + xi));
+    // x neighbours: previous lane's .w, next lane's .x; warp edges load their own
+    int left = __shfl_up_sync(0xffffffffu, c.w, 1);
+    int right = __shfl_down_sync(0xffffffffu, c.x, 1);
+    if (active && lane == 0 && xi > 0) left = __ldg(row + xi - 1);
+    if (active && lane == 31 && xi + 4 < n2) right = __ldg(row + xi + 4);
+    if (!active) return;
+    const bool zin = gz > 0 && gz < gN0 - 1;
+    const bool yin = y > 0 && y < n1 - 1;
+    int4 zm = make_int4(0, 0, 0, 0), zp = zm, ym = zm, yp = zm;
+    if (zin) {
+        zm = __ldg(reinterpret_cast<const int4*>(row - plane + xi));
+        zp = __ldg(reinterpret_cast<const int4*>(row + plane + xi));
+    }
+    if (yin) {
+        ym = __ldg(reinterpret_cast<const int4*>(row - n2 + xi));
+        yp = __ldg(reinterpret_cast<const int4*>(row + n2 + xi));
+    }
+    const int64_t o = (z - zlo) * plane + y * n2 + xi;
+    // d/dz (axis 0), d/dy (axis 1): zero on their boundary layers (fields.py:34-44)
+    float4 dz = make_float4(0.f, 0.f, 0.f, 0.f), dy = dz, dx, lp = dz;
+    if (zin) dz = scale4((int64_t)zp.x - zm.x, (int64_t)zp.y - zm.y, (int64_t)zp.z - zm.z, (int64_t)zp.w - zm.w, eps);
+    if (yin) dy = scale4((int64_t)yp.x - ym.x, (int64_t)yp.y - ym.y, (int64_t)yp.z - ym.z, (int64_t)yp.w - ym.w, eps);
+    // d/dx (axis 2): zero at x = 0 and x = n2-1
+    int64_t d0 = (int64_t)c.y - left, d1 = (int64_t)c.z - c.x, d2 = (int64_t)c.w - c.y, d3 = (int64_t)right - c.z;
+    if (xi == 0) d0 = 0;
+    if (xi + 3 >= n2 - 1) d3 = 0;
+    dx = scale4(d0, d1, d2, d3, eps);
+    if (zin && yin) {   // Laplacian: zero on every boundary layer (fields.py:47-60)
+        int64_t l0 = (int64_t)zm.x + zp.x + ym.x + yp.x + left + c.y - 6ll * c.x;
+        int64_t l1 = (int64_t)zm.y + zp.y + ym.y + yp.y + c.x + c.z - 6ll * c.y;
+        int64_t l2 = (int64_t)zm.z + zp.z + ym.z + yp.z + c.y + c.w - 6ll * c.z;
+        int64_t l3 = (int64_t)zm.w + zp.w + ym.w + yp.w + c.z + right - 6ll * c.w;
+        if (xi == 0) l0 = 0;
+        if (xi + 3 >= n2 - 1) l3 = 0;
+        lp = scale4(l0, l1, l2, l3, two_eps);
+    }
+    __stcs(reinterpret_cast<float4*>(o0 + o), dz);
+    __stcs(reinterpret_cast<float4*>(o1 + o), dy);
+    __stcs(reinterpret_cast<float4*>(o2 + o), dx);
+    __stcs(reinterpret_cast<float4*>(o3 + o), lp);
+}
+
+}  // namespace hszg
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
 static int stencil_impl(int op, int32_t ndims, const int64_t* dims, int32_t ncomp, const void* const* q,
                         const double* eps, int float_domain, int32_t out_type, void* const* out, int64_t zlo,
                         int64_t zhi, int64_t gz0, int64_t gN0, cudaStream_t st) {
+    if (op == HSZG_OP_GRAD_LAP && ndims == 3 && ncomp == 1 && float_domain == 0 && out_type == HSZG_F32 &&
+        dims[2] % 4 == 0 && dims[2] >= 4 && aligned16(q[0]) && aligned16(out[0]) && aligned16(out[1]) &&
+        aligned16(out[2]) && aligned16(out[3]) && dims[1] <= 65535 && zhi - zlo <= 65535) {
+        if (zhi - zlo < 1) return HSZG_OK;
+        dim3 grid((unsigned)((dims[2] / 4 + GL_THREADS - 1) / GL_THREADS), (unsigned)dims[1], (unsigned)(zhi - zlo));
+        k_grad_lap_f32<<<grid, GL_THREADS, 0, st>>>(reinterpret_cast<const int32_t*>(q[0]), dims[1], dims[2], zlo,
+                                                     gz0, gN0, eps[0], 2.0 * eps[0],
+                                                     reinterpret_cast<float*>(out[0]), reinterpret_cast<float*>(out[1]),
+                                                     reinterpret_cast<float*>(out[2]), reinterpret_cast<float*>(out[3]));
+        return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
+    }
     if (ndims < 1 || ndims > 3 || ncomp < 1 || ncomp > 3) return HSZG_INVALID_ARG;
     if (out_type != HSZG_F32 && out_type != HSZG_F64) return HSZG_INVALID_ARG;
     StencilArgs A = {};

@@ -404,6 +404,7 @@ static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, 
     switch (g->kind) {
         case HSZG_HSZX:
             if (fast) {
+                allow_smem(k_tile_stream<true, OutT>, smem);
                 k_tile_stream<true, OutT><<<(unsigned)tiles, TILE_CHUNKS, smem, st>>>(
                     sg, s->payload, s->payload_len, s->offsets, s->metadata, two_eps, out);
                 HSZG_CHECK_LAUNCH("reconstruct hszx");
@@ -417,6 +418,7 @@ static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, 
                 bt.k = TILE_CHUNKS / sg.cpb[0];
                 bt.tpr = (sg.G[2] + bt.k - 1) / bt.k;
                 const int64_t nt = sg.G[0] * sg.G[1] * bt.tpr;
+                allow_smem(k_tile_blocks<OutT>, smem);
                 k_tile_blocks<OutT><<<(unsigned)nt, TILE_CHUNKS, smem, st>>>(sg, bt, s->payload, s->payload_len,
                                                                                s->offsets, s->metadata, two_eps, out);
                 HSZG_CHECK_LAUNCH("reconstruct hszx-nd");
@@ -428,6 +430,7 @@ static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, 
                 if (ws_bytes < lookback_ws_bytes(g->n_chunks)) break;
                 LBState lb = lookback_carve(ws, tiles);
                 cudaMemsetAsync(ws, 0, lookback_clear_bytes(tiles), st);
+                allow_smem(k_tile_scan<OutT>, smem);
                 k_tile_scan<OutT><<<(unsigned)tiles, TILE_CHUNKS, smem, st>>>(sg, s->payload, s->payload_len,
                                                                                s->offsets, lb, two_eps, out);
                 HSZG_CHECK_LAUNCH("reconstruct hszp");
@@ -579,6 +582,7 @@ extern "C" int hszg_plane_sum(const HszgGeom* g, const HszgStream* s, int32_t* p
     cudaMemsetAsync(plane_out, 0, (size_t)plane * 4, st);
     if (g->n_chunks == 0) return HSZG_OK;
     const int64_t tiles = (g->n_chunks + TILE_CHUNKS - 1) / TILE_CHUNKS;
+    allow_smem(k_plane_sum, tile_smem_bytes(s->max_bitwidth));
     k_plane_sum<<<(unsigned)tiles, TILE_CHUNKS, tile_smem_bytes(s->max_bitwidth), st>>>(
         sg, s->payload, s->payload_len, s->offsets, plane, reinterpret_cast<unsigned int*>(plane_out));
     HSZG_CHECK_LAUNCH("plane sum");

@@ -27,6 +27,14 @@ inline size_t tile_smem_bytes(int max_bw) {
     return (size_t)TILE_VALS * 4 + bytes + 16;
 }
 
+// Opt a tile kernel into > 48 KB of dynamic shared memory (wide bit widths need ~69 KB).
+template <typename K>
+inline void allow_smem(K kernel, size_t bytes) {
+    if (bytes > 48 * 1024)
+        cudaFuncSetAttribute(reinterpret_cast<const void*>(kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)bytes);
+}
+
 struct TileCtx {
     int64_t c0, c1;      // chunk range
     int64_t e0, e1;      // stream range

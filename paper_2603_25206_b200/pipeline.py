@@ -234,14 +234,25 @@ class WindowPipeline:
 
     def _range_bytes(self, s: int, e: int) -> int:
         """Compressed bytes of local planes [s, e): payload range + 8 B per chunk + 4 B per block mean."""
-        if not hasattr(self, "_chunk_off_host"):
-            self._chunk_off_host = self.ds.offsets.cpu().numpy()
-            self._cpp = self.ds.n_chunks / self.sf.nz
-        nc = self.ds.n_chunks
-        c0 = int(round(s * self._cpp))
-        c1 = nc if e >= self.sf.nz else int(round(e * self._cpp))
-        p0 = int(self._chunk_off_host[c0]) if c0 < nc else self.ds.payload_len
-        p1 = int(self._chunk_off_host[c1]) if c1 < nc else self.ds.payload_len
+        if not hasattr(self, "_plane_off"):
+            # byte offset / chunk index of every window-aligned plane boundary, fetched once (small D2H)
+            t = _lib.torch()
+            nz, nc = self.sf.nz, self.ds.n_chunks
+            if self.sf.kind == HSZP_ND:
+                per = nc // nz
+                chunks = [z * per for z in range(nz)]
+            else:
+                from .device import _full_row_chunks
+
+                rc = _full_row_chunks(self.ds)
+                chunks = [(z // self.G) * rc for z in range(nz)]
+            idx = t.tensor([min(c, nc - 1) for c in chunks], dtype=t.int64, device=self.ds.offsets.device)
+            offs = self.ds.offsets.index_select(0, idx).cpu().numpy().tolist()
+            self._plane_chunk = chunks + [nc]
+            self._plane_off = [o if c < nc else self.ds.payload_len for o, c in zip(offs, chunks)] + [
+                self.ds.payload_len]
+        c0, c1 = self._plane_chunk[s], self._plane_chunk[e]
+        p0, p1 = self._plane_off[s], self._plane_off[e]
         meta = 0 if self.ds.metadata is None else 4 * self.ds.metadata.numel() * (e - s) // self.sf.nz
         return (p1 - p0) + 8 * (c1 - c0) + meta
 
