@@ -55,7 +55,10 @@ def test_shard_containers_are_global_chunk_ranges(setup, kind, world):
         lo = int(vo[0])
         so = sf.ds.offsets.cpu().numpy().view(np.uint64)
         assert np.array_equal(so, vo - np.uint64(lo))
-        assert sf.ds.payload[:sf.ds.payload_len].cpu().numpy().tobytes() == gh.payload[lo:view.payload_len]
+        first = int(np.searchsorted(np.asarray(gh.offsets, dtype=np.uint64), np.uint64(lo)))
+        last = first + view.n_chunks
+        hi = int(gh.offsets[last]) if last < len(gh.offsets) else len(gh.payload)
+        assert sf.ds.payload[:sf.ds.payload_len].cpu().numpy().tobytes() == gh.payload[lo:hi]
         if kind == 3:
             assert np.array_equal(sf.ds.metadata.cpu().numpy(), view.metadata.cpu().numpy())
     del cpp_or_row
