@@ -242,6 +242,33 @@ int hszg_quantize_f64(const double* field, int64_t n, double recip, int32_t* q, 
 int hszg_decorrelate(const HszgGeom* g, const int32_t* q, int32_t* p, int32_t* metadata, void* ws,
                      size_t ws_bytes, void* stream, HszgErr* err);
 
+/* ---- windowed 3-D pipeline (pipeline.py; Algorithm 3 on the device) -------------------------- */
+/* Exact order-independent statistics: int128 sums split into 32-bit limbs accumulated with
+ * 64-bit atomics (limb 3 signed): value = sum_k limb_k * 2^(32k). */
+typedef struct HszgAcc {
+    uint64_t s1_limb[4];
+    uint64_t s2_limb[4];
+    int64_t count;
+    int32_t vmin, vmax;
+} HszgAcc;
+int hszg_acc_reset(HszgAcc* acc, void* stream);
+/* Gradient (dz, dy, dx) + Laplacian, fp32, of planes [zlo, zhi) of the int32 window q (box planes;
+ * plane 0 at global z gz0 of a gN0-plane field; planes zlo-1 / zhi are read where they exist).
+ * acc (optional) accumulates sum q, sum q^2, min, max of the output planes. */
+int hszg_zgrad_lap(const int32_t* q, int64_t n1, int64_t n2, int64_t zlo, int64_t zhi, int64_t gz0, int64_t gN0,
+                   double eps, float* const* out, HszgAcc* acc, void* stream);
+/* HSZP_ND z-sweep: from 2-D-prefixed planes P2 (planes a.., plus a lookahead plane when
+ * has_lookahead), the carry q[a-1] (NULL at the global first plane) and optionally the upper
+ * neighbour's q plane, emit gradient + Laplacian of nout planes, accumulate stats and write
+ * q[a+nout-1] to carry_out — q itself is never stored. */
+int hszg_zsweep_grad_lap(const int32_t* P2, int64_t n1, int64_t n2, int64_t nout, int has_lookahead,
+                         const int32_t* carry, const int32_t* q_upper, int32_t* carry_out, int64_t gz0, int64_t gN0,
+                         double eps, float* const* out, HszgAcc* acc, void* stream);
+/* HSZP_ND decode fused with the in-row prefix (rows of whole chunks, 256 % (n2/32) == 0). */
+int hszg_decode_rowscan(const HszgGeom* g, const HszgStream* s, int32_t* out, void* stream, HszgErr* err);
+/* In-place inclusive scan along the middle axis of an int32 [A][M][L] view. */
+int hszg_col_scan(int32_t* buf, int64_t A, int64_t M, int64_t L, void* stream);
+
 /* ---- synthetic input (BASELINE config 5, generated on the device; not the hot path) ---- */
 int hszg_gen_noise(float* out, int64_t e0, int64_t nz, const int64_t* dims, uint64_t seed, void* stream);
 int hszg_gauss_pass(const float* in, float* out, int64_t e0, int64_t nz, const int64_t* dims, int axis,

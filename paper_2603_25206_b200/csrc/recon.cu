@@ -588,3 +588,11 @@ extern "C" int hszg_plane_sum(const HszgGeom* g, const HszgStream* s, int32_t* p
     HSZG_CHECK_LAUNCH("plane sum");
     return HSZG_OK;
 }
+
+// In-place inclusive scan along the middle axis of an int32 view [A][M][L] (HSZP_ND y prefix of
+// the windowed pipeline: A planes, M rows, L columns).
+extern "C" int hszg_col_scan(int32_t* buf, int64_t A, int64_t M, int64_t L, void* stream) {
+    if (A <= 0 || M <= 0 || L <= 0) return HSZG_OK;
+    launch_col_scan<int32_t>(buf, A, M, L, 0.0, buf, as_stream(stream));
+    return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
+}

@@ -1,0 +1,335 @@
+// window.cu — the windowed 3-D analytics kernels of pipeline.py (config-5 hot loop).
+//
+// Per window of W planes:
+//   HSZX_ND : k_tile_blocks (decode + p+M + block->row-major transpose, recon.cu) into a q window,
+//             then k_zgrad_lap: gradient + Laplacian + exact stats, each thread sliding along z.
+//   HSZP_ND : k_tile_rowscan (decode + in-row prefix fused: R = x-prefix of p), k_col_scan (y prefix:
+//             P2 = 2-D prefix per plane), then k_zsweep: the z prefix q[z] = q[z-1] + P2[z] kept in
+//             registers as running sums at the centre row and the rows y+-1, producing gradient +
+//             Laplacian + stats without ever writing q, and handing q[b-1] to the next window.
+// Integer stencils and fp64 scaling reproduce fields.py:34-80 exactly; outputs are fp32
+// (one rounding of the reference float64), written with streaming stores.
+// Statistics: exact int128 per thread, warp-reduced, added into 32-bit limbs with 64-bit
+// atomics (HszgAcc) — order-independent and exact, finished on the host in Python ints.
+#include <cstdio>
+#include "tile.cuh"
+#include "lookback.cuh"
+
+namespace hszg {
+
+__device__ __forceinline__ void acc_add_i128(unsigned long long* limbs, i128 v) {
+    const u128 u = (u128)v;
+    const unsigned long long l0 = (unsigned long long)(uint32_t)u;
+    const unsigned long long l1 = (unsigned long long)(uint32_t)(u >> 32);
+    const unsigned long long l2 = (unsigned long long)(uint32_t)(u >> 64);
+    const long long l3 = (long long)(int32_t)(uint32_t)(u >> 96);   // signed top limb
+    if (l0) atomicAdd(limbs + 0, l0);
+    if (l1) atomicAdd(limbs + 1, l1);
+    if (l2) atomicAdd(limbs + 2, l2);
+    if (l3) atomicAdd(limbs + 3, (unsigned long long)l3);
+}
+
+struct WinStats {
+    i128 s1, s2;
+    int32_t vmin, vmax;
+    __device__ __forceinline__ void init() { s1 = 0; s2 = 0; vmin = INT32_MAX; vmax = INT32_MIN; }
+    __device__ __forceinline__ void add4(int4 q) {
+        s1 += (int64_t)q.x + q.y + q.z + q.w;
+        s2 += (i128)((int64_t)q.x * q.x + (int64_t)q.y * q.y) + (i128)((int64_t)q.z * q.z + (int64_t)q.w * q.w);
+        vmin = min(vmin, min(min(q.x, q.y), min(q.z, q.w)));
+        vmax = max(vmax, max(max(q.x, q.y), max(q.z, q.w)));
+    }
+    // warp-reduce, then one lane publishes
+    __device__ __forceinline__ void flush(HszgAcc* acc, int64_t count) {
+        for (int d = 16; d > 0; d >>= 1) {
+            s1 += shfl_down_i128(s1, d);
+            s2 += shfl_down_i128(s2, d);
+            vmin = min(vmin, __shfl_down_sync(0xffffffffu, vmin, d));
+            vmax = max(vmax, __shfl_down_sync(0xffffffffu, vmax, d));
+            count += __shfl_down_sync(0xffffffffu, count, d);
+        }
+        if ((threadIdx.x & 31) == 0 && count) {
+            acc_add_i128(reinterpret_cast<unsigned long long*>(acc->s1_limb), s1);
+            acc_add_i128(reinterpret_cast<unsigned long long*>(acc->s2_limb), s2);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&acc->count), (unsigned long long)count);
+            atomicMin(&acc->vmin, vmin);
+            atomicMax(&acc->vmax, vmax);
+        }
+    }
+};
+
+__device__ __forceinline__ float4 sc4(int64_t a, int64_t b, int64_t c, int64_t d, double s) {
+    return make_float4(__double2float_rn(__dmul_rn((double)a, s)), __double2float_rn(__dmul_rn((double)b, s)),
+                       __double2float_rn(__dmul_rn((double)c, s)), __double2float_rn(__dmul_rn((double)d, s)));
+}
+
+__device__ __forceinline__ int4 add4(int4 a, int4 b) {
+    return make_int4((int)((uint32_t)a.x + (uint32_t)b.x), (int)((uint32_t)a.y + (uint32_t)b.y),
+                     (int)((uint32_t)a.z + (uint32_t)b.z), (int)((uint32_t)a.w + (uint32_t)b.w));
+}
+
+__device__ __forceinline__ int4 ld4(const int32_t* p) { return __ldg(reinterpret_cast<const int4*>(p)); }
+
+// Emit gradient (dz, dy, dx) + Laplacian for 4 x-points given the 7-point neighbourhood.
+__device__ __forceinline__ void emit4(float* o0, float* o1, float* o2, float* o3, int64_t o, bool zin, bool yin,
+                                      int64_t xi, int64_t n2, int4 zm, int4 c, int4 zp, int4 ym, int4 yp,
+                                      int32_t left, int32_t right, double eps, double two_eps) {
+    const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 dz = zero, dy = zero, lp = zero;
+    if (zin) dz = sc4((int64_t)zp.x - zm.x, (int64_t)zp.y - zm.y, (int64_t)zp.z - zm.z, (int64_t)zp.w - zm.w, eps);
+    if (yin) dy = sc4((int64_t)yp.x - ym.x, (int64_t)yp.y - ym.y, (int64_t)yp.z - ym.z, (int64_t)yp.w - ym.w, eps);
+    int64_t d0 = (int64_t)c.y - left, d1 = (int64_t)c.z - c.x, d2 = (int64_t)c.w - c.y, d3 = (int64_t)right - c.z;
+    if (xi == 0) d0 = 0;
+    if (xi + 3 >= n2 - 1) d3 = 0;
+    const float4 dx = sc4(d0, d1, d2, d3, eps);
+    if (zin && yin) {
+        int64_t l0 = (int64_t)zm.x + zp.x + ym.x + yp.x + left + c.y - 6ll * c.x;
+        int64_t l1 = (int64_t)zm.y + zp.y + ym.y + yp.y + c.x + c.z - 6ll * c.y;
+        int64_t l2 = (int64_t)zm.z + zp.z + ym.z + yp.z + c.y + c.w - 6ll * c.z;
+        int64_t l3 = (int64_t)zm.w + zp.w + ym.w + yp.w + c.z + right - 6ll * c.w;
+        if (xi == 0) l0 = 0;
+        if (xi + 3 >= n2 - 1) l3 = 0;
+        lp = sc4(l0, l1, l2, l3, two_eps);
+    }
+    __stcs(reinterpret_cast<float4*>(o0 + o), dz);
+    __stcs(reinterpret_cast<float4*>(o1 + o), dy);
+    __stcs(reinterpret_cast<float4*>(o2 + o), dx);
+    __stcs(reinterpret_cast<float4*>(o3 + o), lp);
+}
+
+constexpr int ZG_THREADS = 128;   // 512 x-points per CTA
+
+// q window: box planes [0, np), outputs for planes [zlo, zhi) (plane zlo-1 and zhi are halos
+// when they exist); the box plane 0 sits at global z = gz0 of a gN0-plane field.
+__global__ void __launch_bounds__(ZG_THREADS) k_zgrad_lap(const int32_t* __restrict__ q, int64_t n1, int64_t n2,
+                                                          int64_t zlo, int64_t zhi, int64_t gz0, int64_t gN0,
+                                                          double eps, double two_eps, float* __restrict__ o0,
+                                                          float* __restrict__ o1, float* __restrict__ o2,
+                                                          float* __restrict__ o3, HszgAcc* acc) {
+    const int lane = threadIdx.x & 31;
+    const int64_t x = ((int64_t)blockIdx.x * ZG_THREADS + threadIdx.x) * 4;
+    const int64_t y = blockIdx.y;
+    const int64_t plane = n1 * n2;
+    const bool active = x < n2;
+    const int64_t xi = active ? x : 0;
+    const bool yin = y > 0 && y < n1 - 1;
+    const int32_t* col = q + y * n2 + xi;
+    WinStats st;
+    st.init();
+    int4 c = make_int4(0, 0, 0, 0), zm = c, zp = c;
+    if (active) {
+        c = ld4(col + zlo * plane);
+        const int64_t gz = gz0 + zlo;
+        if (gz > 0) zm = ld4(col + (zlo - 1) * plane);
+    }
+    for (int64_t z = zlo; z < zhi; z++) {
+        const int64_t gz = gz0 + z;
+        const bool zin = gz > 0 && gz < gN0 - 1;
+        if (active && gz < gN0 - 1) zp = ld4(col + (z + 1) * plane);
+        int left = __shfl_up_sync(0xffffffffu, c.w, 1);
+        int right = __shfl_down_sync(0xffffffffu, c.x, 1);
+        if (active) {
+            const int32_t* row = col + z * plane;
+            if (lane == 0 && xi > 0) left = __ldg(row - 1);
+            if (lane == 31 && xi + 4 < n2) right = __ldg(row + 4);
+            int4 ym = make_int4(0, 0, 0, 0), yp = ym;
+            if (yin) {
+                ym = ld4(row - n2);
+                yp = ld4(row + n2);
+            }
+            emit4(o0, o1, o2, o3, (z - zlo) * plane + y * n2 + xi, zin, yin, xi, n2, zm, c, zp, ym, yp, left, right,
+                  eps, two_eps);
+            if (acc) st.add4(c);
+        }
+        zm = c;
+        c = zp;
+    }
+    if (acc) st.flush(acc, active ? 4 * (zhi - zlo) : 0);
+}
+
+// HSZP_ND z-sweep.  P2: box planes [0, np) = planes [a, a+np) of 2-D prefixes (plane a+nout is the
+// lookahead when present); carry = q[a-1] (NULL: a is the global first plane); q_upper = q[a+nout]
+// from the next rank (NULL: use the lookahead P2 plane, or none at the global top).
+__global__ void __launch_bounds__(ZG_THREADS) k_zsweep(const int32_t* __restrict__ P2, int64_t n1, int64_t n2,
+                                                       int64_t nout, int has_lookahead, const int32_t* carry,
+                                                       const int32_t* q_upper, int32_t* carry_out, int64_t gz0,
+                                                       int64_t gN0, double eps, double two_eps,
+                                                       float* __restrict__ o0, float* __restrict__ o1,
+                                                       float* __restrict__ o2, float* __restrict__ o3, HszgAcc* acc) {
+    const int lane = threadIdx.x & 31;
+    const int64_t x = ((int64_t)blockIdx.x * ZG_THREADS + threadIdx.x) * 4;
+    const int64_t y = blockIdx.y;
+    const int64_t plane = n1 * n2;
+    const bool active = x < n2;
+    const int64_t xi = active ? x : 0;
+    const bool yin = y > 0 && y < n1 - 1;
+    const int64_t off = y * n2 + xi;
+    WinStats st;
+    st.init();
+    const int4 z4 = make_int4(0, 0, 0, 0);
+    // running q at plane a-1 (rows y-1, y, y+1 and the x-edge neighbours)
+    int4 qc = z4, qm = z4, qp = z4;
+    int ql = 0, qr = 0;
+    if (active && carry) {
+        qc = ld4(carry + off);
+        if (yin) {
+            qm = ld4(carry + off - n2);
+            qp = ld4(carry + off + n2);
+        }
+        if (lane == 0 && xi > 0) ql = __ldg(carry + off - 1);
+        if (lane == 31 && xi + 4 < n2) qr = __ldg(carry + off + 4);
+    }
+    int4 prev = qc;                                     // q[a-1]
+    // advance to plane a
+    if (active) {
+        const int32_t* p = P2 + off;
+        qc = add4(qc, ld4(p));
+        if (yin) {
+            qm = add4(qm, ld4(p - n2));
+            qp = add4(qp, ld4(p + n2));
+        }
+        if (lane == 0 && xi > 0) ql += __ldg(p - 1);
+        if (lane == 31 && xi + 4 < n2) qr += __ldg(p + 4);
+    }
+    for (int64_t z = 0; z < nout; z++) {
+        const int64_t gz = gz0 + z;
+        const bool zin = gz > 0 && gz < gN0 - 1;
+        // q[z+1] at the centre row (lookahead P2 plane or the upper neighbour's plane)
+        int4 next = z4, nm = z4, np_ = z4;
+        int nl = 0, nr = 0;
+        const bool more = z + 1 < nout || has_lookahead;
+        if (active && gz < gN0 - 1) {
+            if (z + 1 == nout && q_upper) {
+                next = ld4(q_upper + off);
+            } else if (more) {
+                const int32_t* p = P2 + (z + 1) * plane + off;
+                next = add4(qc, ld4(p));
+                if (yin) {
+                    nm = add4(qm, ld4(p - n2));
+                    np_ = add4(qp, ld4(p + n2));
+                }
+                if (lane == 0 && xi > 0) nl = ql + __ldg(p - 1);
+                if (lane == 31 && xi + 4 < n2) nr = qr + __ldg(p + 4);
+            }
+        }
+        int left = __shfl_up_sync(0xffffffffu, qc.w, 1);
+        int right = __shfl_down_sync(0xffffffffu, qc.x, 1);
+        if (lane == 0) left = ql;
+        if (lane == 31) right = qr;
+        if (active) {
+            emit4(o0, o1, o2, o3, z * plane + off, zin, yin, xi, n2, prev, qc, next, qm, qp, left, right, eps,
+                  two_eps);
+            if (acc) st.add4(qc);
+            if (z + 1 == nout && carry_out) *reinterpret_cast<int4*>(carry_out + off) = qc;
+        }
+        prev = qc;
+        qc = next;
+        qm = nm;
+        qp = np_;
+        ql = nl;
+        qr = nr;
+    }
+    if (acc) st.flush(acc, active ? 4 * nout : 0);
+}
+
+// HSZP_ND decode fused with the in-row prefix: rows are whole chunks (n2 % 32 == 0) and a tile
+// holds whole rows (256 % chunks_per_row == 0), so the row prefix is a segmented scan of the
+// per-chunk sums across the tile's lanes.
+__global__ void __launch_bounds__(TILE_CHUNKS) k_tile_rowscan(SegGeo sg, const uint8_t* payload, uint64_t len,
+                                                             const uint64_t* offsets, int cpr, int32_t* out) {
+    __shared__ unsigned long long ex[TILE_CHUNKS];
+    TileCtx t = tile_stage(sg, payload, len, offsets, blockIdx.x);
+    const int64_t c = t.c0 + threadIdx.x;
+    uint32_t run = 0;
+    int local = 0, count = 0;
+    int32_t* vals = t.vals;
+    if (c < t.c1) {
+        const ChunkLoc L = locate_chunk(sg, c);
+        local = (int)(L.start - t.e0);
+        count = L.count;
+        decode_chunk_words(t.words, (uint32_t)(offsets[c] - t.base), L.count, [&](int j, int32_t v) {
+            run += (uint32_t)v;
+            vals[pad_idx(local + j)] = (int32_t)run;
+        });
+    }
+    unsigned long long tot;
+    const unsigned long long e = block_exclusive_u64((unsigned long long)run, &tot);
+    ex[threadIdx.x] = e;
+    __syncthreads();
+    const uint32_t add = (uint32_t)(e - ex[(threadIdx.x / cpr) * cpr]);
+    for (int j = 0; j < count; j++) vals[pad_idx(local + j)] = (int32_t)((uint32_t)vals[pad_idx(local + j)] + add);
+    __syncthreads();
+    const int n = (int)(t.e1 - t.e0);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[t.e0 + i] = vals[pad_idx(i)];
+}
+
+__global__ void k_acc_reset(HszgAcc* acc) {
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < 4; k++) {
+            acc->s1_limb[k] = 0;
+            acc->s2_limb[k] = 0;
+        }
+        acc->count = 0;
+        acc->vmin = INT32_MAX;
+        acc->vmax = INT32_MIN;
+    }
+}
+
+}  // namespace hszg
+
+using namespace hszg;
+
+int hszg_set_cuda_error(HszgErr* err, cudaError_t e, const char* where);
+static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+extern "C" int hszg_acc_reset(HszgAcc* acc, void* stream) {
+    k_acc_reset<<<1, 32, 0, as_stream(stream)>>>(acc);
+    return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
+}
+
+extern "C" int hszg_zgrad_lap(const int32_t* q, int64_t n1, int64_t n2, int64_t zlo, int64_t zhi, int64_t gz0,
+                              int64_t gN0, double eps, float* const* out, HszgAcc* acc, void* stream) {
+    if (n2 % 4 || !al16(q) || !al16(out[0]) || !al16(out[1]) || !al16(out[2]) || !al16(out[3]) || n1 > 65535)
+        return HSZG_INVALID_ARG;
+    if (zhi <= zlo) return HSZG_OK;
+    dim3 grid((unsigned)((n2 / 4 + ZG_THREADS - 1) / ZG_THREADS), (unsigned)n1);
+    k_zgrad_lap<<<grid, ZG_THREADS, 0, as_stream(stream)>>>(q, n1, n2, zlo, zhi, gz0, gN0, eps, 2.0 * eps, out[0],
+                                                            out[1], out[2], out[3], acc);
+    return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
+}
+
+extern "C" int hszg_zsweep_grad_lap(const int32_t* P2, int64_t n1, int64_t n2, int64_t nout, int has_lookahead,
+                                    const int32_t* carry, const int32_t* q_upper, int32_t* carry_out, int64_t gz0,
+                                    int64_t gN0, double eps, float* const* out, HszgAcc* acc, void* stream) {
+    if (n2 % 4 || !al16(P2) || !al16(out[0]) || !al16(out[1]) || !al16(out[2]) || !al16(out[3]) || n1 > 65535 ||
+        (carry && !al16(carry)) || (q_upper && !al16(q_upper)) || (carry_out && !al16(carry_out)))
+        return HSZG_INVALID_ARG;
+    if (nout <= 0) return HSZG_OK;
+    dim3 grid((unsigned)((n2 / 4 + ZG_THREADS - 1) / ZG_THREADS), (unsigned)n1);
+    k_zsweep<<<grid, ZG_THREADS, 0, as_stream(stream)>>>(P2, n1, n2, nout, has_lookahead, carry, q_upper, carry_out,
+                                                         gz0, gN0, eps, 2.0 * eps, out[0], out[1], out[2], out[3],
+                                                         acc);
+    return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
+}
+
+extern "C" int hszg_decode_rowscan(const HszgGeom* g, const HszgStream* s, int32_t* out, void* stream, HszgErr* err) {
+    err->status = HSZG_OK;
+    const SegGeo sg = make_seggeo(*g);
+    const int64_t n2 = sg.n[2];
+    const int64_t cpr = n2 / kChunkCap;
+    if (g->kind != HSZG_HSZP_ND || !s->canonical || n2 % kChunkCap || cpr < 1 || TILE_CHUNKS % cpr) {
+        err->status = HSZG_INVALID_ARG;
+        snprintf(err->message, sizeof(err->message),
+                 "decode_rowscan needs a canonical HSZP_ND stream whose rows are whole chunks dividing a tile");
+        return HSZG_INVALID_ARG;
+    }
+    if (g->n_chunks == 0) return HSZG_OK;
+    const int64_t tiles = (g->n_chunks + TILE_CHUNKS - 1) / TILE_CHUNKS;
+    const size_t smem = tile_smem_bytes(s->max_bitwidth);
+    allow_smem(k_tile_rowscan, smem);
+    k_tile_rowscan<<<(unsigned)tiles, TILE_CHUNKS, smem, as_stream(stream)>>>(sg, s->payload, s->payload_len,
+                                                                             s->offsets, (int)cpr, out);
+    if (cudaGetLastError() != cudaSuccess) return hszg_set_cuda_error(err, cudaGetLastError(), "decode_rowscan");
+    return HSZG_OK;
+}

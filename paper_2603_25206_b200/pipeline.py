@@ -132,6 +132,24 @@ def sums_to_ints(buf) -> dict:
     return dict(s1=s.s1, s2=s.s2, count=int(s.count), vmin=int(s.vmin), vmax=int(s.vmax))
 
 
+ACC_BYTES = 80     # sizeof(HszgAcc)
+
+
+def acc_to_ints(buf) -> dict:
+    """Decode an HszgAcc (32-bit limbs of the int128 sums, limb 3 signed) into exact Python ints."""
+    raw = bytes(buf.cpu().numpy().tobytes()) if hasattr(buf, "cpu") else bytes(buf)
+    u = np.frombuffer(raw[:72], dtype="<u8").astype(object)
+    cnt = int(np.frombuffer(raw[64:72], dtype="<i8")[0])
+    vmin, vmax = (int(v) for v in np.frombuffer(raw[72:80], dtype="<i4"))
+
+    def val(limbs):
+        top = int(limbs[3])
+        top = top - 2**64 if top >= 2**63 else top
+        return int(limbs[0]) + (int(limbs[1]) << 32) + (int(limbs[2]) << 64) + (top << 96)
+
+    return dict(s1=val(u[0:4]), s2=val(u[4:8]), count=cnt, vmin=vmin, vmax=vmax)
+
+
 def combine_rank_sums(comm: Comm, local_sums_buf) -> dict:
     """Exact global (sum q, sum q^2, count, min, max) from every rank's int128 record (one all-gather)."""
     parts = comm.all_gather(local_sums_buf)
@@ -337,14 +355,137 @@ class WindowPipeline:
         return self.run(outs, stats, _prepared=True)
 
     # -- the windowed pass ---------------------------------------------------------------
+    def _fast_ok(self, outs) -> bool:
+        """The fused window kernels need rows of whole chunks (HSZP_ND), 16-B rows and fp32 outputs."""
+        t = _lib.torch()
+        n2 = self.sf.global_dims[2]
+        if n2 % 4 or outs[0].dtype != t.float32 or not self.ds.desc.canonical:
+            return False
+        if self.sf.kind == HSZP_ND:
+            return n2 % 32 == 0 and 256 % (n2 // 32) == 0
+        return True
+
     def run(self, outs, stats: bool = True, _prepared: bool = False):
         """Fill outs = [dz, dy, dx, laplacian] (float tensors of shape (nz, n1, n2)); return global stats."""
+        if not _prepared:
+            self.prepare()
+        if self._fast_ok(outs):
+            self._acc_reset()
+            if self.sf.kind == HSZP_ND:
+                self._run_zsweep(outs)
+            else:
+                self._run_blocks(outs)
+            if not stats:
+                return None
+            return self._finish_stats(_prepared)
+        return self._run_generic(outs, stats, _prepared)
+
+    # -- fused loops (window.cu) ---------------------------------------------------------------
+    def _acc_reset(self):
+        t = _lib.torch()
+        if not hasattr(self, "acc"):
+            self.acc = t.zeros(ACC_BYTES, dtype=t.uint8, device=_lib.device())
+        _lib.call("hszg_acc_reset", _lib.ptr(self.acc), _lib.stream_handle())
+
+    def _outs_arr(self, outs, a, b):
+        return (ctypes.c_void_p * 4)(*[_lib.ptr(o[a:b]) for o in outs])
+
+    def _run_blocks(self, outs):
+        """HSZX_ND: k_tile_blocks into the q window, k_zgrad_lap (+ stats) over it."""
+        sf, buf, W, G = self.sf, self.buf, self.W, self.G
+        nz = sf.nz
+        n1, n2 = sf.global_dims[1], sf.global_dims[2]
+        if self.halo_lo is not None:
+            buf[0].copy_(self.halo_lo)
+        decoded = 0
+        for a in range(0, nz, W):
+            b = min(a + W, nz)
+            need = min(b + 1, nz)
+            if decoded < need:
+                e = min(nz, -(-need // G) * G)
+                s = decoded
+                if self.timer:
+                    self.timer.begin("reconstruct")
+                self._decode_planes(s, e, buf[s - a + 1:e - a + 1])
+                if self.timer:
+                    self.timer.end("reconstruct", self._range_bytes(s, e) + 4 * (e - s) * self.plane)
+                decoded = e
+            if b == nz and self.halo_hi is not None:
+                buf[b - a + 1].copy_(self.halo_hi)
+            if self.timer:
+                self.timer.begin("stencil")
+            _lib.call("hszg_zgrad_lap", _lib.ptr(buf), n1, n2, 1, 1 + (b - a), sf.z0 + a - 1, sf.global_dims[0],
+                      ctypes.c_double(sf.eps), self._outs_arr(outs, a, b), _lib.ptr(self.acc), _lib.stream_handle())
+            if self.timer:
+                self.timer.end("stencil", (4 + 16) * (b - a) * self.plane)
+            if b < nz:
+                for k, z in enumerate(range(b - 1, decoded)):
+                    buf[k].copy_(buf[z - a + 1])
+
+    def _run_zsweep(self, outs):
+        """HSZP_ND: fused decode+row prefix, column prefix, then the z-sweep (q never stored)."""
+        t = _lib.torch()
+        sf, buf, W = self.sf, self.buf, self.W
+        nz = sf.nz
+        n1, n2 = sf.global_dims[1], sf.global_dims[2]
+        if not hasattr(self, "carries"):
+            self.carries = [t.empty((n1, n2), dtype=t.int32, device=_lib.device()) for _ in range(2)]
+        carry = self.carry if (sf.z0 > 0 and self.carry is not None) else None
+        flip = 0
+        decoded = 0                      # local planes [a, decoded) hold P2 at buffer index z - a
+        for a in range(0, nz, W):
+            b = min(a + W, nz)
+            need = min(b + 1, nz)
+            if decoded < need:
+                s, e = decoded, need
+                if self.timer:
+                    self.timer.begin("reconstruct")
+                sub = self.ds.plane_view(s, e)
+                err = _lib.Err()
+                _lib.call("hszg_decode_rowscan", ctypes.byref(sub.geom), ctypes.byref(sub.desc),
+                          _lib.ptr(buf[s - a]), _lib.stream_handle(), ctypes.byref(err), err=err)
+                _lib.call("hszg_col_scan", _lib.ptr(buf[s - a]), e - s, n1, n2, _lib.stream_handle())
+                if self.timer:
+                    self.timer.end("reconstruct", self._range_bytes(s, e) + 4 * (e - s) * self.plane)
+                decoded = e
+            upper = self.halo_hi if (b == nz and self.halo_hi is not None) else None
+            out_carry = self.carries[flip]
+            if self.timer:
+                self.timer.begin("stencil")
+            _lib.call("hszg_zsweep_grad_lap", _lib.ptr(buf), n1, n2, b - a, int(decoded > b),
+                      _lib.ptr(carry) if carry is not None else None, _lib.ptr(upper) if upper is not None else None,
+                      _lib.ptr(out_carry), sf.z0 + a, sf.global_dims[0], ctypes.c_double(sf.eps),
+                      self._outs_arr(outs, a, b), _lib.ptr(self.acc), _lib.stream_handle())
+            if self.timer:
+                self.timer.end("stencil", (4 + 16) * (b - a) * self.plane)
+            carry = out_carry
+            flip ^= 1
+            if b < nz:                   # the lookahead plane b becomes index 0
+                buf[0].copy_(buf[b - a])
+
+    def _finish_stats(self, _prepared):
+        self.local_sums = self.acc
+        if _prepared:
+            return acc_to_ints(self.acc)
+        parts = self.comm.all_gather(self.acc)
+        tot = dict(s1=0, s2=0, count=0, vmin=2**31, vmax=-(2**31))
+        for p in parts:
+            d = acc_to_ints(p)
+            tot["s1"] += d["s1"]
+            tot["s2"] += d["s2"]
+            tot["count"] += d["count"]
+            tot["vmin"] = min(tot["vmin"], d["vmin"])
+            tot["vmax"] = max(tot["vmax"], d["vmax"])
+        n = int(np.prod(self.sf.global_dims))
+        mean, var = finalize_mean_var(tot["s1"], tot["s2"], n, self.sf.eps)
+        return dict(mean=mean, var=var, **tot)
+
+    # -- general loop (any geometry / output type) ------------------------------------------------
+    def _run_generic(self, outs, stats, _prepared):
         from . import device as devmod
 
         sf, buf, W, G = self.sf, self.buf, self.W, self.G
         nz = sf.nz
-        if not _prepared:
-            self.prepare()
         if self.halo_lo is not None:
             buf[0].copy_(self.halo_lo)
         decoded = 0                                      # next local plane to decode
