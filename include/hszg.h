@@ -254,14 +254,16 @@ typedef struct HszgAcc {
 int hszg_acc_reset(HszgAcc* acc, void* stream);
 /* Gradient (dz, dy, dx) + Laplacian, fp32, of planes [zlo, zhi) of the int32 window q (box planes;
  * plane 0 at global z gz0 of a gN0-plane field; planes zlo-1 / zhi are read where they exist).
+ * qprev / qnext (optional) replace the in-window planes zlo-1 / zhi (ring-buffered windows).
  * acc (optional) accumulates sum q, sum q^2, min, max of the output planes. */
 int hszg_zgrad_lap(const int32_t* q, int64_t n1, int64_t n2, int64_t zlo, int64_t zhi, int64_t gz0, int64_t gN0,
-                   double eps, float* const* out, HszgAcc* acc, void* stream);
+                   double eps, float* const* out, HszgAcc* acc, const int32_t* qprev, const int32_t* qnext,
+                   void* stream);
 /* HSZP_ND z-sweep: from 2-D-prefixed planes P2 (planes a.., plus a lookahead plane when
- * has_lookahead), the carry q[a-1] (NULL at the global first plane) and optionally the upper
+ * lookahead != NULL: P2 of plane a+nout), the carry q[a-1] (NULL at the global first plane) and optionally the upper
  * neighbour's q plane, emit gradient + Laplacian of nout planes, accumulate stats and write
  * q[a+nout-1] to carry_out — q itself is never stored. */
-int hszg_zsweep_grad_lap(const int32_t* P2, int64_t n1, int64_t n2, int64_t nout, int has_lookahead,
+int hszg_zsweep_grad_lap(const int32_t* P2, int64_t n1, int64_t n2, int64_t nout, const int32_t* lookahead,
                          const int32_t* carry, const int32_t* q_upper, int32_t* carry_out, int64_t gz0, int64_t gN0,
                          double eps, float* const* out, HszgAcc* acc, void* stream);
 /* HSZP_ND decode fused with the in-row prefix (rows of whole chunks, 256 % (n2/32) == 0). */

@@ -92,37 +92,67 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_tile_blocks(SegGeo sg, BlockTil
     if (threadIdx.x == 0) sb[nvec] = make_uint4(0, 0, 0, 0);
     const uint32_t* words = reinterpret_cast<const uint32_t*>(sb);
     __syncthreads();
-    const int64_t nch = s_c1 - s_c0;
-    for (int64_t ci = threadIdx.x; ci < nch; ci += blockDim.x) {
-        const int64_t c = s_c0 + ci;
-        const ChunkLoc L = locate_chunk(sg, c);
-        const int local = (int)(L.start - s_e0);
-        const int32_t m = __ldg(meta + L.seg);
-        decode_chunk_words(words, (uint32_t)(offsets[c] - base), L.count,
-                           [&](int j, int32_t v) { vals[pad_idx(local + j)] = v + m; });
+    // Tile geometry in 32-bit: the tile's segments are one segment-row slice, all full along x
+    // except possibly the last one, so chunk -> (segment, chunk-in-segment) needs no 64-bit division.
+    const int B2 = (int)sg.B[2];
+    const int nlast = (int)(b2b - 1 - b2a);                 // index of the last segment in the tile
+    const int last_ext = (int)seg_ext(sg, 2, b2b - 1);
+    const int S1 = (int)s1;
+    const int plane01 = (int)(s0 * s1);                     // rows of a segment (z, y pairs)
+    const int segsz = plane01 * B2;                         // values in a full segment
+    const int cpb = (segsz + kChunkCap - 1) / kChunkCap;    // chunks in a full segment
+    const int lastsz = plane01 * last_ext;
+    const int nch = (int)(s_c1 - s_c0);
+    const int64_t mbase = (b0 * sg.G[1] + b1) * sg.G[2] + b2a;
+    for (int ci = threadIdx.x; ci < nch; ci += blockDim.x) {
+        int seg = ci / cpb;
+        if (seg > nlast) seg = nlast;
+        const int j = ci - seg * cpb;
+        const int size = seg == nlast ? lastsz : segsz;
+        const int left = size - j * kChunkCap;
+        const int count = left < kChunkCap ? left : kChunkCap;
+        const int local = seg * segsz + j * kChunkCap;
+        const int32_t m = __ldg(meta + mbase + seg);
+        decode_chunk_words(words, (uint32_t)(offsets[s_c0 + ci] - base), count,
+                           [&](int jj, int32_t v) { vals[pad_idx(local + jj)] = v + m; });
     }
     __syncthreads();
     // row-major write-out of the (s0, s1, W) box
     const int64_t x0 = b2a * sg.B[2];
     const int64_t xe = (b2b == sg.G[2]) ? sg.n[2] : b2b * sg.B[2];
     const int W = (int)(xe - x0);
-    const int B2 = (int)sg.B[2];
-    const int last_ext = (int)seg_ext(sg, 2, b2b - 1);
-    const int nlast = (int)(b2b - 1 - b2a);
-    const int S1 = (int)s1;
-    const int segsz = (int)(s0 * s1) * B2;
-    const int total = (int)(s0 * s1) * W;
     const int64_t z0 = b0 * sg.B[0], y0 = b1 * sg.B[1];
-    for (int i = threadIdx.x; i < total; i += blockDim.x) {
-        const int zy = i / W;
-        const int xl = i - zy * W;
+    const int64_t n1 = sg.n[1], n2 = sg.n[2];
+    if ((int)blockDim.x % W == 0) {
+        // every thread keeps one x column: the per-x parts are loop invariant
+        const int xl = threadIdx.x % W;
+        const int step = blockDim.x / W;
         const int t = xl / B2;
         const int xi = xl - t * B2;
         const int s2t = (t == nlast) ? last_ext : B2;
-        const int local = t * segsz + zy * s2t + xi;
-        const int zl = zy / S1, yl = zy - zl * S1;
-        const int64_t gi = ((z0 + zl) * sg.n[1] + (y0 + yl)) * sg.n[2] + x0 + xl;
-        out[gi] = Conv<OutT>::go(vals[pad_idx(local)], two_eps);
+        int zy = threadIdx.x / W;
+        int zl = zy / S1, yl = zy - zl * S1;
+        for (; zy < plane01; zy += step) {
+            const int local = t * segsz + zy * s2t + xi;
+            out[((z0 + zl) * n1 + (y0 + yl)) * n2 + x0 + xl] = Conv<OutT>::go(vals[pad_idx(local)], two_eps);
+            yl += step;
+            while (yl >= S1) {
+                yl -= S1;
+                zl++;
+            }
+        }
+    } else {
+        const int total = plane01 * W;
+        for (int i = threadIdx.x; i < total; i += blockDim.x) {
+            const int zy = i / W;
+            const int xl = i - zy * W;
+            const int t = xl / B2;
+            const int xi = xl - t * B2;
+            const int s2t = (t == nlast) ? last_ext : B2;
+            const int local = t * segsz + zy * s2t + xi;
+            const int zl = zy / S1, yl = zy - zl * S1;
+            out[((z0 + zl) * n1 + (y0 + yl)) * n2 + x0 + xl] = Conv<OutT>::go(vals[pad_idx(local)], two_eps);
+        }
     }
 }
 

@@ -10,6 +10,8 @@
 // bank-padded int32 value tile, which the epilogue consumes in stream order
 // with coalesced stores.
 #pragma once
+#include <mutex>
+#include <unordered_map>
 #include "common.cuh"
 
 namespace hszg {
@@ -27,12 +29,23 @@ inline size_t tile_smem_bytes(int max_bw) {
     return (size_t)TILE_VALS * 4 + bytes + 16;
 }
 
-// Opt a tile kernel into > 48 KB of dynamic shared memory (wide bit widths need ~69 KB).
+// Opt a tile kernel into > 48 KB of dynamic shared memory (wide bit widths need ~69 KB).  The
+// attribute is raised once per kernel to the largest size seen, so steady-state launches (and
+// launches under CUDA-graph capture) make no runtime call here.
+inline void allow_smem_raw(const void* kernel, size_t bytes) {
+    static std::mutex mu;
+    static std::unordered_map<const void*, size_t> set;
+    if (bytes <= 48 * 1024) return;
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& cur = set[kernel];
+    if (bytes <= cur) return;
+    const size_t want = bytes < 96 * 1024 ? 96 * 1024 : bytes;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want);
+    cur = want;
+}
 template <typename K>
 inline void allow_smem(K kernel, size_t bytes) {
-    if (bytes > 48 * 1024)
-        cudaFuncSetAttribute(reinterpret_cast<const void*>(kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)bytes);
+    allow_smem_raw(reinterpret_cast<const void*>(kernel), bytes);
 }
 
 struct TileCtx {

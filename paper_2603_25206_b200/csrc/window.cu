@@ -105,7 +105,9 @@ __global__ void __launch_bounds__(ZG_THREADS) k_zgrad_lap(const int32_t* __restr
                                                           int64_t zlo, int64_t zhi, int64_t gz0, int64_t gN0,
                                                           double eps, double two_eps, float* __restrict__ o0,
                                                           float* __restrict__ o1, float* __restrict__ o2,
-                                                          float* __restrict__ o3, HszgAcc* acc) {
+                                                          float* __restrict__ o3, HszgAcc* acc,
+                                                          const int32_t* __restrict__ qprev,
+                                                          const int32_t* __restrict__ qnext) {
     const int lane = threadIdx.x & 31;
     const int64_t x = ((int64_t)blockIdx.x * ZG_THREADS + threadIdx.x) * 4;
     const int64_t y = blockIdx.y;
@@ -113,19 +115,20 @@ __global__ void __launch_bounds__(ZG_THREADS) k_zgrad_lap(const int32_t* __restr
     const bool active = x < n2;
     const int64_t xi = active ? x : 0;
     const bool yin = y > 0 && y < n1 - 1;
-    const int32_t* col = q + y * n2 + xi;
+    const int64_t off = y * n2 + xi;
+    const int32_t* col = q + off;
     WinStats st;
     st.init();
     int4 c = make_int4(0, 0, 0, 0), zm = c, zp = c;
     if (active) {
         c = ld4(col + zlo * plane);
         const int64_t gz = gz0 + zlo;
-        if (gz > 0) zm = ld4(col + (zlo - 1) * plane);
+        if (gz > 0) zm = qprev ? ld4(qprev + off) : ld4(col + (zlo - 1) * plane);
     }
     for (int64_t z = zlo; z < zhi; z++) {
         const int64_t gz = gz0 + z;
         const bool zin = gz > 0 && gz < gN0 - 1;
-        if (active && gz < gN0 - 1) zp = ld4(col + (z + 1) * plane);
+        if (active && gz < gN0 - 1) zp = (z + 1 == zhi && qnext) ? ld4(qnext + off) : ld4(col + (z + 1) * plane);
         int left = __shfl_up_sync(0xffffffffu, c.w, 1);
         int right = __shfl_down_sync(0xffffffffu, c.x, 1);
         if (active) {
@@ -151,7 +154,7 @@ __global__ void __launch_bounds__(ZG_THREADS) k_zgrad_lap(const int32_t* __restr
 // lookahead when present); carry = q[a-1] (NULL: a is the global first plane); q_upper = q[a+nout]
 // from the next rank (NULL: use the lookahead P2 plane, or none at the global top).
 __global__ void __launch_bounds__(ZG_THREADS) k_zsweep(const int32_t* __restrict__ P2, int64_t n1, int64_t n2,
-                                                       int64_t nout, int has_lookahead, const int32_t* carry,
+                                                       int64_t nout, const int32_t* lookahead, const int32_t* carry,
                                                        const int32_t* q_upper, int32_t* carry_out, int64_t gz0,
                                                        int64_t gN0, double eps, double two_eps,
                                                        float* __restrict__ o0, float* __restrict__ o1,
@@ -197,12 +200,12 @@ __global__ void __launch_bounds__(ZG_THREADS) k_zsweep(const int32_t* __restrict
         // q[z+1] at the centre row (lookahead P2 plane or the upper neighbour's plane)
         int4 next = z4, nm = z4, np_ = z4;
         int nl = 0, nr = 0;
-        const bool more = z + 1 < nout || has_lookahead;
+        const bool more = z + 1 < nout || lookahead != nullptr;
         if (active && gz < gN0 - 1) {
             if (z + 1 == nout && q_upper) {
                 next = ld4(q_upper + off);
             } else if (more) {
-                const int32_t* p = P2 + (z + 1) * plane + off;
+                const int32_t* p = (z + 1 < nout ? P2 + (z + 1) * plane : lookahead) + off;
                 next = add4(qc, ld4(p));
                 if (yin) {
                     nm = add4(qm, ld4(p - n2));
@@ -289,17 +292,18 @@ extern "C" int hszg_acc_reset(HszgAcc* acc, void* stream) {
 }
 
 extern "C" int hszg_zgrad_lap(const int32_t* q, int64_t n1, int64_t n2, int64_t zlo, int64_t zhi, int64_t gz0,
-                              int64_t gN0, double eps, float* const* out, HszgAcc* acc, void* stream) {
+                              int64_t gN0, double eps, float* const* out, HszgAcc* acc, const int32_t* qprev,
+                              const int32_t* qnext, void* stream) {
     if (n2 % 4 || !al16(q) || !al16(out[0]) || !al16(out[1]) || !al16(out[2]) || !al16(out[3]) || n1 > 65535)
         return HSZG_INVALID_ARG;
     if (zhi <= zlo) return HSZG_OK;
     dim3 grid((unsigned)((n2 / 4 + ZG_THREADS - 1) / ZG_THREADS), (unsigned)n1);
     k_zgrad_lap<<<grid, ZG_THREADS, 0, as_stream(stream)>>>(q, n1, n2, zlo, zhi, gz0, gN0, eps, 2.0 * eps, out[0],
-                                                            out[1], out[2], out[3], acc);
+                                                            out[1], out[2], out[3], acc, qprev, qnext);
     return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
 }
 
-extern "C" int hszg_zsweep_grad_lap(const int32_t* P2, int64_t n1, int64_t n2, int64_t nout, int has_lookahead,
+extern "C" int hszg_zsweep_grad_lap(const int32_t* P2, int64_t n1, int64_t n2, int64_t nout, const int32_t* lookahead,
                                     const int32_t* carry, const int32_t* q_upper, int32_t* carry_out, int64_t gz0,
                                     int64_t gN0, double eps, float* const* out, HszgAcc* acc, void* stream) {
     if (n2 % 4 || !al16(P2) || !al16(out[0]) || !al16(out[1]) || !al16(out[2]) || !al16(out[3]) || n1 > 65535 ||
@@ -307,7 +311,7 @@ extern "C" int hszg_zsweep_grad_lap(const int32_t* P2, int64_t n1, int64_t n2, i
         return HSZG_INVALID_ARG;
     if (nout <= 0) return HSZG_OK;
     dim3 grid((unsigned)((n2 / 4 + ZG_THREADS - 1) / ZG_THREADS), (unsigned)n1);
-    k_zsweep<<<grid, ZG_THREADS, 0, as_stream(stream)>>>(P2, n1, n2, nout, has_lookahead, carry, q_upper, carry_out,
+    k_zsweep<<<grid, ZG_THREADS, 0, as_stream(stream)>>>(P2, n1, n2, nout, lookahead, carry, q_upper, carry_out,
                                                          gz0, gN0, eps, 2.0 * eps, out[0], out[1], out[2], out[3],
                                                          acc);
     return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;

@@ -242,8 +242,7 @@ class WindowPipeline:
         self.W = max(self.G, (window // self.G) * self.G)
         n1, n2 = sf.global_dims[1], sf.global_dims[2]
         self.plane = n1 * n2
-        cap = self.W + self.G + 2
-        self.buf = t.empty((cap, n1, n2), dtype=t.int32, device=_lib.device())
+        self._buf = None            # general-loop window buffer, allocated on first use
         self.nwin = -(-sf.nz // self.W)
         self.win_sums = t.zeros(max(self.nwin, 1) * SUMS_BYTES, dtype=t.uint8, device=_lib.device())
         self.halo_lo = None
@@ -366,102 +365,159 @@ class WindowPipeline:
         return True
 
     def run(self, outs, stats: bool = True, _prepared: bool = False):
-        """Fill outs = [dz, dy, dx, laplacian] (float tensors of shape (nz, n1, n2)); return global stats."""
+        """Fill outs = [dz, dy, dx, laplacian] (float tensors of shape (nz, n1, n2)); return global stats.
+
+        With ``use_graph`` the whole window loop (hundreds of launches) is captured once into a CUDA
+        graph and replayed; the per-container boundary phase (halos / carry, collectives) and the
+        final stats read-back stay outside it.
+        """
         if not _prepared:
             self.prepare()
         if self._fast_ok(outs):
-            self._acc_reset()
-            if self.sf.kind == HSZP_ND:
-                self._run_zsweep(outs)
+            self._stage_boundary()
+            if self.use_graph:
+                self._replay(outs)
             else:
-                self._run_blocks(outs)
+                self._fused_loop(outs)
             if not stats:
                 return None
             return self._finish_stats(_prepared)
         return self._run_generic(outs, stats, _prepared)
 
+    use_graph = False
+
     # -- fused loops (window.cu) ---------------------------------------------------------------
-    def _acc_reset(self):
+    def _persistent(self):
+        """Buffers whose addresses stay fixed across runs (graph-capture safe)."""
         t = _lib.torch()
-        if not hasattr(self, "acc"):
-            self.acc = t.zeros(ACC_BYTES, dtype=t.uint8, device=_lib.device())
+        if getattr(self, "_pers_W", None) == self.W:
+            return
+        n1, n2 = self.sf.global_dims[1], self.sf.global_dims[2]
+        dev = _lib.device()
+        nslots = 2 if self.sf.kind == HSZP_ND else 3
+        self.ring = [t.empty((self.W, n1, n2), dtype=t.int32, device=dev) for _ in range(nslots)]
+        self.halo_buf = t.zeros((2, n1, n2), dtype=t.int32, device=dev)       # [lower, upper]
+        self.carry_buf = t.zeros((3, n1, n2), dtype=t.int32, device=dev)      # [rank carry, ping, pong]
+        self.acc = t.zeros(ACC_BYTES, dtype=t.uint8, device=dev)
+        self._pers_W = self.W
+        self._graph = None
+
+    def _stage_boundary(self):
+        """Copy this run's halo / carry planes into the persistent buffers read by the loop."""
+        self._persistent()
+        if self.halo_lo is not None:
+            self.halo_buf[0].copy_(self.halo_lo)
+        if self.halo_hi is not None:
+            self.halo_buf[1].copy_(self.halo_hi)
+        if self.sf.kind == HSZP_ND and self.sf.z0 > 0 and self.carry is not None:
+            self.carry_buf[0].copy_(self.carry)
+
+    def _replay(self, outs):
+        t = _lib.torch()
+        key = tuple(_lib.ptr(o) for o in outs) + (self.halo_lo is not None, self.halo_hi is not None)
+        if self._graph is None or self._graph_key != key:
+            self._fused_loop(outs)                        # warm-up: workspaces, smem attributes
+            t.cuda.synchronize()
+            if self.timer is not None:
+                self.timer.clear()                        # keep only the captured event nodes
+            g = t.cuda.CUDAGraph()
+            with t.cuda.graph(g):
+                self._fused_loop(outs)
+            self._graph, self._graph_key = g, key
+        self._graph.replay()
+
+    def _fused_loop(self, outs):
         _lib.call("hszg_acc_reset", _lib.ptr(self.acc), _lib.stream_handle())
+        if self.sf.kind == HSZP_ND:
+            self._run_zsweep(outs)
+        else:
+            self._run_blocks(outs)
 
     def _outs_arr(self, outs, a, b):
         return (ctypes.c_void_p * 4)(*[_lib.ptr(o[a:b]) for o in outs])
 
+    def _windows(self):
+        nz = self.sf.nz
+        return [(a, min(a + self.W, nz)) for a in range(0, nz, self.W)]
+
     def _run_blocks(self, outs):
-        """HSZX_ND: k_tile_blocks into the q window, k_zgrad_lap (+ stats) over it."""
-        sf, buf, W, G = self.sf, self.buf, self.W, self.G
-        nz = sf.nz
+        """HSZX_ND: k_tile_blocks decodes window k+2 while k_zgrad_lap (+ stats) runs on window k;
+        three ring slots, halo planes by pointer (no copies)."""
+        sf, ring = self.sf, self.ring
         n1, n2 = sf.global_dims[1], sf.global_dims[2]
-        if self.halo_lo is not None:
-            buf[0].copy_(self.halo_lo)
-        decoded = 0
-        for a in range(0, nz, W):
-            b = min(a + W, nz)
-            need = min(b + 1, nz)
-            if decoded < need:
-                e = min(nz, -(-need // G) * G)
-                s = decoded
-                if self.timer:
-                    self.timer.begin("reconstruct")
-                self._decode_planes(s, e, buf[s - a + 1:e - a + 1])
-                if self.timer:
-                    self.timer.end("reconstruct", self._range_bytes(s, e) + 4 * (e - s) * self.plane)
-                decoded = e
-            if b == nz and self.halo_hi is not None:
-                buf[b - a + 1].copy_(self.halo_hi)
+        wins = self._windows()
+        nw = len(wins)
+
+        def decode(k):
+            a, b = wins[k]
+            if self.timer:
+                self.timer.begin("reconstruct")
+            self._decode_planes(a, b, ring[k % 3][: b - a])
+            if self.timer:
+                self.timer.end("reconstruct", self._range_bytes(a, b) + 4 * (b - a) * self.plane)
+
+        decode(0)
+        if nw > 1:
+            decode(1)
+        for k, (a, b) in enumerate(wins):
+            if k > 0:
+                pa, pb = wins[k - 1]
+                prev = ring[(k - 1) % 3][pb - pa - 1]
+            else:
+                prev = self.halo_buf[0] if self.halo_lo is not None else None
+            if k + 1 < nw:
+                nxt = ring[(k + 1) % 3][0]
+            else:
+                nxt = self.halo_buf[1] if self.halo_hi is not None else None
             if self.timer:
                 self.timer.begin("stencil")
-            _lib.call("hszg_zgrad_lap", _lib.ptr(buf), n1, n2, 1, 1 + (b - a), sf.z0 + a - 1, sf.global_dims[0],
-                      ctypes.c_double(sf.eps), self._outs_arr(outs, a, b), _lib.ptr(self.acc), _lib.stream_handle())
+            _lib.call("hszg_zgrad_lap", _lib.ptr(ring[k % 3]), n1, n2, 0, b - a, sf.z0 + a, sf.global_dims[0],
+                      ctypes.c_double(sf.eps), self._outs_arr(outs, a, b), _lib.ptr(self.acc),
+                      _lib.ptr(prev) if prev is not None else None, _lib.ptr(nxt) if nxt is not None else None,
+                      _lib.stream_handle())
             if self.timer:
                 self.timer.end("stencil", (4 + 16) * (b - a) * self.plane)
-            if b < nz:
-                for k, z in enumerate(range(b - 1, decoded)):
-                    buf[k].copy_(buf[z - a + 1])
+            if k + 2 < nw:
+                decode(k + 2)
 
     def _run_zsweep(self, outs):
-        """HSZP_ND: fused decode+row prefix, column prefix, then the z-sweep (q never stored)."""
-        t = _lib.torch()
-        sf, buf, W = self.sf, self.buf, self.W
-        nz = sf.nz
+        """HSZP_ND: fused decode+row prefix and column prefix of window k+1 (two ring slots) before the
+        register z-sweep of window k (q never stored; the lookahead plane is read in place)."""
+        sf, ring = self.sf, self.ring
         n1, n2 = sf.global_dims[1], sf.global_dims[2]
-        if not hasattr(self, "carries"):
-            self.carries = [t.empty((n1, n2), dtype=t.int32, device=_lib.device()) for _ in range(2)]
-        carry = self.carry if (sf.z0 > 0 and self.carry is not None) else None
-        flip = 0
-        decoded = 0                      # local planes [a, decoded) hold P2 at buffer index z - a
-        for a in range(0, nz, W):
-            b = min(a + W, nz)
-            need = min(b + 1, nz)
-            if decoded < need:
-                s, e = decoded, need
-                if self.timer:
-                    self.timer.begin("reconstruct")
-                sub = self.ds.plane_view(s, e)
-                err = _lib.Err()
-                _lib.call("hszg_decode_rowscan", ctypes.byref(sub.geom), ctypes.byref(sub.desc),
-                          _lib.ptr(buf[s - a]), _lib.stream_handle(), ctypes.byref(err), err=err)
-                _lib.call("hszg_col_scan", _lib.ptr(buf[s - a]), e - s, n1, n2, _lib.stream_handle())
-                if self.timer:
-                    self.timer.end("reconstruct", self._range_bytes(s, e) + 4 * (e - s) * self.plane)
-                decoded = e
-            upper = self.halo_hi if (b == nz and self.halo_hi is not None) else None
-            out_carry = self.carries[flip]
+        wins = self._windows()
+        nw = len(wins)
+
+        def decode(k):
+            a, b = wins[k]
+            if self.timer:
+                self.timer.begin("reconstruct")
+            sub = self.ds.plane_view(a, b)
+            err = _lib.Err()
+            _lib.call("hszg_decode_rowscan", ctypes.byref(sub.geom), ctypes.byref(sub.desc), _lib.ptr(ring[k % 2]),
+                      _lib.stream_handle(), ctypes.byref(err), err=err)
+            _lib.call("hszg_col_scan", _lib.ptr(ring[k % 2]), b - a, n1, n2, _lib.stream_handle())
+            if self.timer:
+                self.timer.end("reconstruct", self._range_bytes(a, b) + 4 * (b - a) * self.plane)
+
+        carry = self.carry_buf[0] if sf.z0 > 0 else None
+        decode(0)
+        for k, (a, b) in enumerate(wins):
+            if k + 1 < nw:
+                decode(k + 1)
+            look = ring[(k + 1) % 2][0] if k + 1 < nw else None
+            upper = self.halo_buf[1] if (k + 1 == nw and self.halo_hi is not None) else None
+            out_carry = self.carry_buf[1 + (k % 2)]
             if self.timer:
                 self.timer.begin("stencil")
-            _lib.call("hszg_zsweep_grad_lap", _lib.ptr(buf), n1, n2, b - a, int(decoded > b),
-                      _lib.ptr(carry) if carry is not None else None, _lib.ptr(upper) if upper is not None else None,
-                      _lib.ptr(out_carry), sf.z0 + a, sf.global_dims[0], ctypes.c_double(sf.eps),
-                      self._outs_arr(outs, a, b), _lib.ptr(self.acc), _lib.stream_handle())
+            _lib.call("hszg_zsweep_grad_lap", _lib.ptr(ring[k % 2]), n1, n2, b - a,
+                      _lib.ptr(look) if look is not None else None, _lib.ptr(carry) if carry is not None else None,
+                      _lib.ptr(upper) if upper is not None else None, _lib.ptr(out_carry), sf.z0 + a,
+                      sf.global_dims[0], ctypes.c_double(sf.eps), self._outs_arr(outs, a, b), _lib.ptr(self.acc),
+                      _lib.stream_handle())
             if self.timer:
                 self.timer.end("stencil", (4 + 16) * (b - a) * self.plane)
             carry = out_carry
-            flip ^= 1
-            if b < nz:                   # the lookahead plane b becomes index 0
-                buf[0].copy_(buf[b - a])
 
     def _finish_stats(self, _prepared):
         self.local_sums = self.acc
@@ -481,6 +537,14 @@ class WindowPipeline:
         return dict(mean=mean, var=var, **tot)
 
     # -- general loop (any geometry / output type) ------------------------------------------------
+    @property
+    def buf(self):
+        if self._buf is None:
+            t = _lib.torch()
+            n1, n2 = self.sf.global_dims[1], self.sf.global_dims[2]
+            self._buf = t.empty((self.W + self.G + 2, n1, n2), dtype=t.int32, device=_lib.device())
+        return self._buf
+
     def _run_generic(self, outs, stats, _prepared):
         from . import device as devmod
 
