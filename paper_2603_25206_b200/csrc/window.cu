@@ -119,33 +119,58 @@ __global__ void __launch_bounds__(ZG_THREADS) k_zgrad_lap(const int32_t* __restr
     const int32_t* col = q + off;
     WinStats st;
     st.init();
-    int4 c = make_int4(0, 0, 0, 0), zm = c, zp = c;
+    const int4 z4 = make_int4(0, 0, 0, 0);
+    // loads one iteration ahead (software pipelining): while plane z is computed, the centre row
+    // of plane z+2 and the y+-1 rows / x edges of plane z+1 are already in flight
+    auto centre = [&](int64_t z) -> int4 {   // plane z, row y (z == zhi may come from qnext)
+        return (z == zhi && qnext) ? ld4(qnext + off) : ld4(col + z * plane);
+    };
+    int4 c = z4, zm = z4, zp = z4, ym = z4, yp = z4;
+    int el = 0, er = 0;
     if (active) {
         c = ld4(col + zlo * plane);
         const int64_t gz = gz0 + zlo;
         if (gz > 0) zm = qprev ? ld4(qprev + off) : ld4(col + (zlo - 1) * plane);
+        if (gz < gN0 - 1) zp = centre(zlo + 1);
+        const int32_t* row = col + zlo * plane;
+        if (yin) {
+            ym = ld4(row - n2);
+            yp = ld4(row + n2);
+        }
+        if (lane == 0 && xi > 0) el = __ldg(row - 1);
+        if (lane == 31 && xi + 4 < n2) er = __ldg(row + 4);
     }
     for (int64_t z = zlo; z < zhi; z++) {
         const int64_t gz = gz0 + z;
         const bool zin = gz > 0 && gz < gN0 - 1;
-        if (active && gz < gN0 - 1) zp = (z + 1 == zhi && qnext) ? ld4(qnext + off) : ld4(col + (z + 1) * plane);
+        int4 zp2 = z4, ym2 = z4, yp2 = z4;
+        int el2 = 0, er2 = 0;
+        if (active && z + 1 < zhi) {
+            if (gz + 1 < gN0 - 1) zp2 = centre(z + 2);
+            const int32_t* row = col + (z + 1) * plane;
+            if (yin) {
+                ym2 = ld4(row - n2);
+                yp2 = ld4(row + n2);
+            }
+            if (lane == 0 && xi > 0) el2 = __ldg(row - 1);
+            if (lane == 31 && xi + 4 < n2) er2 = __ldg(row + 4);
+        }
         int left = __shfl_up_sync(0xffffffffu, c.w, 1);
         int right = __shfl_down_sync(0xffffffffu, c.x, 1);
+        if (lane == 0) left = el;
+        if (lane == 31) right = er;
         if (active) {
-            const int32_t* row = col + z * plane;
-            if (lane == 0 && xi > 0) left = __ldg(row - 1);
-            if (lane == 31 && xi + 4 < n2) right = __ldg(row + 4);
-            int4 ym = make_int4(0, 0, 0, 0), yp = ym;
-            if (yin) {
-                ym = ld4(row - n2);
-                yp = ld4(row + n2);
-            }
-            emit4(o0, o1, o2, o3, (z - zlo) * plane + y * n2 + xi, zin, yin, xi, n2, zm, c, zp, ym, yp, left, right,
-                  eps, two_eps);
+            emit4(o0, o1, o2, o3, (z - zlo) * plane + off, zin, yin, xi, n2, zm, c, zp, ym, yp, left, right, eps,
+                  two_eps);
             if (acc) st.add4(c);
         }
         zm = c;
         c = zp;
+        zp = zp2;
+        ym = ym2;
+        yp = yp2;
+        el = el2;
+        er = er2;
     }
     if (acc) st.flush(acc, active ? 4 * (zhi - zlo) : 0);
 }
@@ -194,27 +219,50 @@ __global__ void __launch_bounds__(ZG_THREADS) k_zsweep(const int32_t* __restrict
         if (lane == 0 && xi > 0) ql += __ldg(p - 1);
         if (lane == 31 && xi + 4 < n2) qr += __ldg(p + 4);
     }
+    // P2 rows of plane zz (zz == nout is the lookahead plane), loaded one iteration ahead so the
+    // loads of plane z+2 are in flight while plane z is emitted (software pipelining)
+    auto wanted = [&](int64_t zz) -> bool {       // will iteration zz-1 build q[zz] from P2[zz]?
+        const bool avail = zz < nout || (zz == nout && lookahead != nullptr && !q_upper);
+        return active && avail && gz0 + zz - 1 < gN0 - 1;
+    };
+    int4 pc = z4, pm = z4, pp = z4;
+    int pl = 0, pr = 0;
+    auto fetch = [&](int64_t zz, int4& c_, int4& m_, int4& p_, int& l_, int& r_) {
+        const int32_t* p = (zz < nout ? P2 + zz * plane : lookahead) + off;
+        c_ = ld4(p);
+        if (yin) {
+            m_ = ld4(p - n2);
+            p_ = ld4(p + n2);
+        }
+        if (lane == 0 && xi > 0) l_ = __ldg(p - 1);
+        if (lane == 31 && xi + 4 < n2) r_ = __ldg(p + 4);
+    };
+    if (wanted(1)) fetch(1, pc, pm, pp, pl, pr);
     for (int64_t z = 0; z < nout; z++) {
         const int64_t gz = gz0 + z;
         const bool zin = gz > 0 && gz < gN0 - 1;
-        // q[z+1] at the centre row (lookahead P2 plane or the upper neighbour's plane)
+        int4 pc2 = z4, pm2 = z4, pp2 = z4;
+        int pl2 = 0, pr2 = 0;
+        if (wanted(z + 2)) fetch(z + 2, pc2, pm2, pp2, pl2, pr2);
+        // q[z+1] at the centre row (P2 plane z+1 / lookahead, or the upper neighbour's plane)
         int4 next = z4, nm = z4, np_ = z4;
         int nl = 0, nr = 0;
-        const bool more = z + 1 < nout || lookahead != nullptr;
         if (active && gz < gN0 - 1) {
             if (z + 1 == nout && q_upper) {
                 next = ld4(q_upper + off);
-            } else if (more) {
-                const int32_t* p = (z + 1 < nout ? P2 + (z + 1) * plane : lookahead) + off;
-                next = add4(qc, ld4(p));
-                if (yin) {
-                    nm = add4(qm, ld4(p - n2));
-                    np_ = add4(qp, ld4(p + n2));
-                }
-                if (lane == 0 && xi > 0) nl = ql + __ldg(p - 1);
-                if (lane == 31 && xi + 4 < n2) nr = qr + __ldg(p + 4);
+            } else if (wanted(z + 1)) {
+                next = add4(qc, pc);
+                nm = add4(qm, pm);
+                np_ = add4(qp, pp);
+                nl = ql + pl;
+                nr = qr + pr;
             }
         }
+        pc = pc2;
+        pm = pm2;
+        pp = pp2;
+        pl = pl2;
+        pr = pr2;
         int left = __shfl_up_sync(0xffffffffu, qc.w, 1);
         int right = __shfl_down_sync(0xffffffffu, qc.x, 1);
         if (lane == 0) left = ql;
