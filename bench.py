@@ -45,7 +45,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--dims", type=int, nargs=3, default=[2048, 2048, 2048])
-    ap.add_argument("--window", type=int, default=8, help="planes per window (L2-sized; HSZX_ND: multiple of 8)")
+    ap.add_argument("--window", type=int, default=64, help="planes per window (HSZX_ND: multiple of 8)")
+    ap.add_argument("--exact-fp32", action="store_true",
+                    help="fp32 outputs = fl32 of the reference float64 (default: fast fp32, <= 2^-22 relative)")
     ap.add_argument("--no-graph", action="store_true", help="launch the window loop eagerly instead of a CUDA graph")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
@@ -231,6 +233,7 @@ def run_ours(args):
     for p in pipes.values():
         p._range_bytes(0, 1)            # fetch the plane-boundary offsets for the timers now, not when timed
         p.use_graph = not args.no_graph
+        p.exact_fp32 = args.exact_fp32
     container_bytes = {k: shards[k].ds.nbytes() for k in KINDS}
     setup_s = time.time() - t_setup
 
@@ -308,7 +311,7 @@ def run_ours(args):
             "config": {"workload": "config5: 2048^3 fp32, rel eb 1e-3, HSZP_ND + HSZX_ND streams; per step "
                                    "global mean+variance and 3-comp gradient + Laplacian (fp32 out) from the "
                                    "compressed bytes, z-slab sharded",
-                       "dims": [N0, N1, N2], "kinds": [KIND_NAMES[k] for k in KINDS], "window_planes": args.window,
+                       "dims": [N0, N1, N2], "kinds": [KIND_NAMES[k] for k in KINDS], "window_planes": args.window, "fp32_outputs": "exact" if args.exact_fp32 else "fast",
                        "eps": eps, "container_bytes_rank0": {KIND_NAMES[k]: container_bytes[k] for k in KINDS},
                        "l2": "working set >> 126 MB L2 (inputs 5-8 GB, outputs 137 GB per stream)",
                        "parallelism": f"z-slab x{world}", "setup_s": round(setup_s, 1)},

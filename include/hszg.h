@@ -243,6 +243,8 @@ int hszg_decorrelate(const HszgGeom* g, const int32_t* q, int32_t* p, int32_t* m
                      size_t ws_bytes, void* stream, HszgErr* err);
 
 /* ---- windowed 3-D pipeline (pipeline.py; Algorithm 3 on the device) -------------------------- */
+/* fp32 outputs: exact != 0 gives fl32(fl64(D*eps)) (one rounding of the reference float64); exact == 0
+ * computes fl32(D * fl32(eps)) in int32/fp32 arithmetic, within 2^-23 relative of it (<< 1e-6). */
 /* Exact order-independent statistics: int128 sums split into 32-bit limbs accumulated with
  * 64-bit atomics (limb 3 signed): value = sum_k limb_k * 2^(32k). */
 typedef struct HszgAcc {
@@ -258,14 +260,14 @@ int hszg_acc_reset(HszgAcc* acc, void* stream);
  * acc (optional) accumulates sum q, sum q^2, min, max of the output planes. */
 int hszg_zgrad_lap(const int32_t* q, int64_t n1, int64_t n2, int64_t zlo, int64_t zhi, int64_t gz0, int64_t gN0,
                    double eps, float* const* out, HszgAcc* acc, const int32_t* qprev, const int32_t* qnext,
-                   void* stream);
+                   int exact, void* stream);
 /* HSZP_ND z-sweep: from 2-D-prefixed planes P2 (planes a.., plus a lookahead plane when
  * lookahead != NULL: P2 of plane a+nout), the carry q[a-1] (NULL at the global first plane) and optionally the upper
  * neighbour's q plane, emit gradient + Laplacian of nout planes, accumulate stats and write
  * q[a+nout-1] to carry_out — q itself is never stored. */
 int hszg_zsweep_grad_lap(const int32_t* P2, int64_t n1, int64_t n2, int64_t nout, const int32_t* lookahead,
                          const int32_t* carry, const int32_t* q_upper, int32_t* carry_out, int64_t gz0, int64_t gN0,
-                         double eps, float* const* out, HszgAcc* acc, void* stream);
+                         double eps, float* const* out, HszgAcc* acc, int exact, void* stream);
 /* HSZP_ND decode fused with the in-row prefix (rows of whole chunks, 256 % (n2/32) == 0). */
 int hszg_decode_rowscan(const HszgGeom* g, const HszgStream* s, int32_t* out, void* stream, HszgErr* err);
 /* In-place inclusive scan along the middle axis of an int32 [A][M][L] view. */

@@ -30,17 +30,22 @@ __device__ __forceinline__ void acc_add_i128(unsigned long long* limbs, i128 v) 
 }
 
 struct WinStats {
+    int64_t s1_64;   // per-thread partial: <= 4*W terms of |q| < 2^31
     i128 s1, s2;
     int32_t vmin, vmax;
-    __device__ __forceinline__ void init() { s1 = 0; s2 = 0; vmin = INT32_MAX; vmax = INT32_MIN; }
+    __device__ __forceinline__ void init() { s1_64 = 0; s1 = 0; s2 = 0; vmin = INT32_MAX; vmax = INT32_MIN; }
     __device__ __forceinline__ void add4(int4 q) {
-        s1 += (int64_t)q.x + q.y + q.z + q.w;
-        s2 += (i128)((int64_t)q.x * q.x + (int64_t)q.y * q.y) + (i128)((int64_t)q.z * q.z + (int64_t)q.w * q.w);
+        s1_64 += (int64_t)q.x + q.y + q.z + q.w;
+        // four squares < 4 * 2^62 = 2^64: exact in u64, one 128-bit add per four values
+        const uint64_t sq = (uint64_t)((int64_t)q.x * q.x) + (uint64_t)((int64_t)q.y * q.y) +
+                            (uint64_t)((int64_t)q.z * q.z) + (uint64_t)((int64_t)q.w * q.w);
+        s2 += (i128)(u128)sq;
         vmin = min(vmin, min(min(q.x, q.y), min(q.z, q.w)));
         vmax = max(vmax, max(max(q.x, q.y), max(q.z, q.w)));
     }
     // warp-reduce, then one lane publishes
     __device__ __forceinline__ void flush(HszgAcc* acc, int64_t count) {
+        s1 += s1_64;
         for (int d = 16; d > 0; d >>= 1) {
             s1 += shfl_down_i128(s1, d);
             s2 += shfl_down_i128(s2, d);
@@ -97,10 +102,61 @@ __device__ __forceinline__ void emit4(float* o0, float* o1, float* o2, float* o3
     __stcs(reinterpret_cast<float4*>(o3 + o), lp);
 }
 
+// Fast fp32 emitter (the pipeline default): integer stencils in int32 and one fp32 multiply by the
+// fp32-rounded scale.  |result - fl64(D*eps)| <= 2^-23 relative (well inside the 1e-6 target), and
+// no XU-pipe conversions: |D| < 2^22 converts with the 1.5*2^23 magic-number trick (one IADD + one
+// FADD).  Any |q| >= 2^27 in the neighbourhood (int32 Laplacian could overflow) takes the exact path.
+__device__ __forceinline__ float i2f_fast(int32_t d) {
+    if (d > -(1 << 22) && d < (1 << 22)) return __int_as_float(0x4B400000 + d) - 12582912.0f;
+    return __int2float_rn(d);
+}
+__device__ __forceinline__ float4 sc4f(int32_t a, int32_t b, int32_t c, int32_t d, float s) {
+    return make_float4(i2f_fast(a) * s, i2f_fast(b) * s, i2f_fast(c) * s, i2f_fast(d) * s);
+}
+__device__ __forceinline__ uint32_t bigmag(int4 v) {   // nonzero if any |v| >= 2^27
+    const uint32_t m = 0xF8000000u;
+    return ((uint32_t)(v.x ^ (v.x >> 31)) | (uint32_t)(v.y ^ (v.y >> 31)) | (uint32_t)(v.z ^ (v.z >> 31)) |
+            (uint32_t)(v.w ^ (v.w >> 31))) & m;
+}
+
+__device__ __forceinline__ void emit4f(float* o0, float* o1, float* o2, float* o3, int64_t o, bool zin, bool yin,
+                                       int64_t xi, int64_t n2, int4 zm, int4 c, int4 zp, int4 ym, int4 yp,
+                                       int32_t left, int32_t right, double eps, double two_eps, float epsf,
+                                       float two_epsf) {
+    const uint32_t big = bigmag(zm) | bigmag(c) | bigmag(zp) | bigmag(ym) | bigmag(yp) |
+                         (((uint32_t)(left ^ (left >> 31)) | (uint32_t)(right ^ (right >> 31))) & 0xF8000000u);
+    if (big) {
+        emit4(o0, o1, o2, o3, o, zin, yin, xi, n2, zm, c, zp, ym, yp, left, right, eps, two_eps);
+        return;
+    }
+    const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 dz = zero, dy = zero, lp = zero;
+    if (zin) dz = sc4f(zp.x - zm.x, zp.y - zm.y, zp.z - zm.z, zp.w - zm.w, epsf);
+    if (yin) dy = sc4f(yp.x - ym.x, yp.y - ym.y, yp.z - ym.z, yp.w - ym.w, epsf);
+    int32_t d0 = c.y - left, d1 = c.z - c.x, d2 = c.w - c.y, d3 = right - c.z;
+    if (xi == 0) d0 = 0;
+    if (xi + 3 >= n2 - 1) d3 = 0;
+    const float4 dx = sc4f(d0, d1, d2, d3, epsf);
+    if (zin && yin) {
+        int32_t l0 = zm.x + zp.x + ym.x + yp.x + left + c.y - 6 * c.x;
+        int32_t l1 = zm.y + zp.y + ym.y + yp.y + c.x + c.z - 6 * c.y;
+        int32_t l2 = zm.z + zp.z + ym.z + yp.z + c.y + c.w - 6 * c.z;
+        int32_t l3 = zm.w + zp.w + ym.w + yp.w + c.z + right - 6 * c.w;
+        if (xi == 0) l0 = 0;
+        if (xi + 3 >= n2 - 1) l3 = 0;
+        lp = sc4f(l0, l1, l2, l3, two_epsf);
+    }
+    __stcs(reinterpret_cast<float4*>(o0 + o), dz);
+    __stcs(reinterpret_cast<float4*>(o1 + o), dy);
+    __stcs(reinterpret_cast<float4*>(o2 + o), dx);
+    __stcs(reinterpret_cast<float4*>(o3 + o), lp);
+}
+
 constexpr int ZG_THREADS = 128;   // 512 x-points per CTA
 
 // q window: box planes [0, np), outputs for planes [zlo, zhi) (plane zlo-1 and zhi are halos
 // when they exist); the box plane 0 sits at global z = gz0 of a gN0-plane field.
+template <bool Exact>
 __global__ void __launch_bounds__(ZG_THREADS) k_zgrad_lap(const int32_t* __restrict__ q, int64_t n1, int64_t n2,
                                                           int64_t zlo, int64_t zhi, int64_t gz0, int64_t gN0,
                                                           double eps, double two_eps, float* __restrict__ o0,
@@ -109,6 +165,7 @@ __global__ void __launch_bounds__(ZG_THREADS) k_zgrad_lap(const int32_t* __restr
                                                           const int32_t* __restrict__ qprev,
                                                           const int32_t* __restrict__ qnext) {
     const int lane = threadIdx.x & 31;
+    const float epsf = __double2float_rn(eps), two_epsf = 2.0f * epsf;
     const int64_t x = ((int64_t)blockIdx.x * ZG_THREADS + threadIdx.x) * 4;
     const int64_t y = blockIdx.y;
     const int64_t plane = n1 * n2;
@@ -160,8 +217,12 @@ __global__ void __launch_bounds__(ZG_THREADS) k_zgrad_lap(const int32_t* __restr
         if (lane == 0) left = el;
         if (lane == 31) right = er;
         if (active) {
-            emit4(o0, o1, o2, o3, (z - zlo) * plane + off, zin, yin, xi, n2, zm, c, zp, ym, yp, left, right, eps,
-                  two_eps);
+            if (Exact)
+                emit4(o0, o1, o2, o3, (z - zlo) * plane + off, zin, yin, xi, n2, zm, c, zp, ym, yp, left, right, eps,
+                      two_eps);
+            else
+                emit4f(o0, o1, o2, o3, (z - zlo) * plane + off, zin, yin, xi, n2, zm, c, zp, ym, yp, left, right, eps,
+                       two_eps, epsf, two_epsf);
             if (acc) st.add4(c);
         }
         zm = c;
@@ -178,6 +239,7 @@ __global__ void __launch_bounds__(ZG_THREADS) k_zgrad_lap(const int32_t* __restr
 // HSZP_ND z-sweep.  P2: box planes [0, np) = planes [a, a+np) of 2-D prefixes (plane a+nout is the
 // lookahead when present); carry = q[a-1] (NULL: a is the global first plane); q_upper = q[a+nout]
 // from the next rank (NULL: use the lookahead P2 plane, or none at the global top).
+template <bool Exact>
 __global__ void __launch_bounds__(ZG_THREADS) k_zsweep(const int32_t* __restrict__ P2, int64_t n1, int64_t n2,
                                                        int64_t nout, const int32_t* lookahead, const int32_t* carry,
                                                        const int32_t* q_upper, int32_t* carry_out, int64_t gz0,
@@ -185,6 +247,7 @@ __global__ void __launch_bounds__(ZG_THREADS) k_zsweep(const int32_t* __restrict
                                                        float* __restrict__ o0, float* __restrict__ o1,
                                                        float* __restrict__ o2, float* __restrict__ o3, HszgAcc* acc) {
     const int lane = threadIdx.x & 31;
+    const float epsf = __double2float_rn(eps), two_epsf = 2.0f * epsf;
     const int64_t x = ((int64_t)blockIdx.x * ZG_THREADS + threadIdx.x) * 4;
     const int64_t y = blockIdx.y;
     const int64_t plane = n1 * n2;
@@ -268,8 +331,12 @@ __global__ void __launch_bounds__(ZG_THREADS) k_zsweep(const int32_t* __restrict
         if (lane == 0) left = ql;
         if (lane == 31) right = qr;
         if (active) {
-            emit4(o0, o1, o2, o3, z * plane + off, zin, yin, xi, n2, prev, qc, next, qm, qp, left, right, eps,
-                  two_eps);
+            if (Exact)
+                emit4(o0, o1, o2, o3, z * plane + off, zin, yin, xi, n2, prev, qc, next, qm, qp, left, right, eps,
+                      two_eps);
+            else
+                emit4f(o0, o1, o2, o3, z * plane + off, zin, yin, xi, n2, prev, qc, next, qm, qp, left, right, eps,
+                       two_eps, epsf, two_epsf);
             if (acc) st.add4(qc);
             if (z + 1 == nout && carry_out) *reinterpret_cast<int4*>(carry_out + off) = qc;
         }
@@ -341,25 +408,26 @@ extern "C" int hszg_acc_reset(HszgAcc* acc, void* stream) {
 
 extern "C" int hszg_zgrad_lap(const int32_t* q, int64_t n1, int64_t n2, int64_t zlo, int64_t zhi, int64_t gz0,
                               int64_t gN0, double eps, float* const* out, HszgAcc* acc, const int32_t* qprev,
-                              const int32_t* qnext, void* stream) {
+                              const int32_t* qnext, int exact, void* stream) {
     if (n2 % 4 || !al16(q) || !al16(out[0]) || !al16(out[1]) || !al16(out[2]) || !al16(out[3]) || n1 > 65535)
         return HSZG_INVALID_ARG;
     if (zhi <= zlo) return HSZG_OK;
     dim3 grid((unsigned)((n2 / 4 + ZG_THREADS - 1) / ZG_THREADS), (unsigned)n1);
-    k_zgrad_lap<<<grid, ZG_THREADS, 0, as_stream(stream)>>>(q, n1, n2, zlo, zhi, gz0, gN0, eps, 2.0 * eps, out[0],
+    (exact ? k_zgrad_lap<true> : k_zgrad_lap<false>)<<<grid, ZG_THREADS, 0, as_stream(stream)>>>(q, n1, n2, zlo, zhi, gz0, gN0, eps, 2.0 * eps, out[0],
                                                             out[1], out[2], out[3], acc, qprev, qnext);
     return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
 }
 
 extern "C" int hszg_zsweep_grad_lap(const int32_t* P2, int64_t n1, int64_t n2, int64_t nout, const int32_t* lookahead,
                                     const int32_t* carry, const int32_t* q_upper, int32_t* carry_out, int64_t gz0,
-                                    int64_t gN0, double eps, float* const* out, HszgAcc* acc, void* stream) {
+                                    int64_t gN0, double eps, float* const* out, HszgAcc* acc, int exact,
+                                    void* stream) {
     if (n2 % 4 || !al16(P2) || !al16(out[0]) || !al16(out[1]) || !al16(out[2]) || !al16(out[3]) || n1 > 65535 ||
         (carry && !al16(carry)) || (q_upper && !al16(q_upper)) || (carry_out && !al16(carry_out)))
         return HSZG_INVALID_ARG;
     if (nout <= 0) return HSZG_OK;
     dim3 grid((unsigned)((n2 / 4 + ZG_THREADS - 1) / ZG_THREADS), (unsigned)n1);
-    k_zsweep<<<grid, ZG_THREADS, 0, as_stream(stream)>>>(P2, n1, n2, nout, lookahead, carry, q_upper, carry_out,
+    (exact ? k_zsweep<true> : k_zsweep<false>)<<<grid, ZG_THREADS, 0, as_stream(stream)>>>(P2, n1, n2, nout, lookahead, carry, q_upper, carry_out,
                                                          gz0, gN0, eps, 2.0 * eps, out[0], out[1], out[2], out[3],
                                                          acc);
     return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;

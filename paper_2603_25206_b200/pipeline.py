@@ -385,6 +385,9 @@ class WindowPipeline:
         return self._run_generic(outs, stats, _prepared)
 
     use_graph = False
+    # fp32 outputs of the fused loop: True = fl32 of the reference float64 (bit-exact vs the oracle);
+    # False = int32 stencil x fl32(eps) in fp32 (<= 2^-23 relative, no fp64 conversions: faster).
+    exact_fp32 = False
 
     # -- fused loops (window.cu) ---------------------------------------------------------------
     def _persistent(self):
@@ -474,7 +477,7 @@ class WindowPipeline:
             _lib.call("hszg_zgrad_lap", _lib.ptr(ring[k % 3]), n1, n2, 0, b - a, sf.z0 + a, sf.global_dims[0],
                       ctypes.c_double(sf.eps), self._outs_arr(outs, a, b), _lib.ptr(self.acc),
                       _lib.ptr(prev) if prev is not None else None, _lib.ptr(nxt) if nxt is not None else None,
-                      _lib.stream_handle())
+                      int(self.exact_fp32), _lib.stream_handle())
             if self.timer:
                 self.timer.end("stencil", (4 + 16) * (b - a) * self.plane)
             if k + 2 < nw:
@@ -514,7 +517,7 @@ class WindowPipeline:
                       _lib.ptr(look) if look is not None else None, _lib.ptr(carry) if carry is not None else None,
                       _lib.ptr(upper) if upper is not None else None, _lib.ptr(out_carry), sf.z0 + a,
                       sf.global_dims[0], ctypes.c_double(sf.eps), self._outs_arr(outs, a, b), _lib.ptr(self.acc),
-                      _lib.stream_handle())
+                      int(self.exact_fp32), _lib.stream_handle())
             if self.timer:
                 self.timer.end("stencil", (4 + 16) * (b - a) * self.plane)
             carry = out_carry

@@ -1,8 +1,9 @@
 """GPU tests of the windowed / z-slab-sharded pipeline (pipeline.py) against the oracle.
 
 * a rank's shard container is byte-identical to the global stream's chunk range (SURVEY §8(c) slab technique);
-* the windowed gradient + Laplacian equals the whole-field reference stencils bit for bit (fp32 outputs =
-  the reference float64 values rounded to float32), and the exact global mean/variance is bit-identical;
+* the windowed gradient + Laplacian equals the whole-field reference stencils: bit for bit in the exact
+  mode (fp32 outputs = the reference float64 values rounded to float32), within FAST_RTOL relative in the
+  default fast-fp32 mode; the exact global mean/variance is bit-identical in both;
 * a multi-rank run, emulated rank by rank in one process (halo planes, HSZP_ND Lorenzo carry from the
   slab totals), reproduces the same outputs.
 
@@ -18,6 +19,17 @@ from oracle import hsz_oracle as O
 pytestmark = pytest.mark.gpu
 
 ALL_DIMS = [(64, 40, 36), (48, 23, 64), (40, 17, 128)]
+
+# fast mode: fl32(fl32(D) * fl32(eps)) vs fl32(D * eps): at most 4 roundings of 2^-24 apart (< 1e-6 target)
+FAST_RTOL = 4 * 2.0**-24
+
+
+def _check_fp32(got, want, exact, msg):
+    if exact:
+        assert np.array_equal(got, want), msg
+    else:
+        err = np.abs(got.astype(np.float64) - want.astype(np.float64))
+        assert np.all(err <= FAST_RTOL * np.abs(want.astype(np.float64))), (msg, float(err.max()))
 
 
 @pytest.fixture(scope="module", params=ALL_DIMS, ids=lambda d: "x".join(map(str, d)))
@@ -77,16 +89,18 @@ def _oracle_outputs(field, kind, eps):
 
 @pytest.mark.parametrize("kind", [1, 3])
 @pytest.mark.parametrize("window", [8, 16, 64])
-def test_window_pipeline_single_rank(setup, kind, window):
+@pytest.mark.parametrize("exact", [True, False], ids=["exact", "fast"])
+def test_window_pipeline_single_rank(setup, kind, window, exact):
     torch, pipeline, compress_device, field, eps, dims = setup
     fd = torch.from_numpy(field).cuda()
     sf = pipeline.compress_shard(fd, kind, eps, (8, 8, 8), 0, dims[0], dims)
     pipe = pipeline.WindowPipeline(sf, pipeline.Comm(), window)
+    pipe.exact_fp32 = exact
     outs = [torch.empty(dims, dtype=torch.float32, device="cuda") for _ in range(4)]
     res = pipe.run(outs)
     want, s1, s2, mean, var = _oracle_outputs(field, kind, eps)
     for k, (got, w) in enumerate(zip(outs, want)):
-        assert np.array_equal(got.cpu().numpy(), w), (kind, window, k)
+        _check_fp32(got.cpu().numpy(), w, exact, (kind, window, k))
     assert res["s1"] == s1 and res["s2"] == s2
     assert res["mean"] == mean and res["var"] == var
     res2 = pipe.run(outs)                 # the pipeline is re-runnable (bench steps)
@@ -104,6 +118,7 @@ def test_window_pipeline_emulated_ranks(setup, kind, world):
         lead = 1 if (kind == 1 and z0 > 0) else 0
         sf = pipeline.compress_shard(fd[z0 - lead:z1].contiguous(), kind, eps, (8, 8, 8), z0, z1, dims)
         ranks.append(pipeline.WindowPipeline(sf, pipeline.Comm(), 8))
+        ranks[-1].exact_fp32 = True
     mine = [p.local_boundary(need_total=True) for p in ranks]
     Ts = [m["T"] for m in mine] if kind == 1 else None
     carries = [p.carry_from(Ts, r) for r, p in enumerate(ranks)]
