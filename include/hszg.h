@@ -264,10 +264,19 @@ int hszg_zgrad_lap(const int32_t* q, int64_t n1, int64_t n2, int64_t zlo, int64_
 /* HSZP_ND z-sweep: from 2-D-prefixed planes P2 (planes a.., plus a lookahead plane when
  * lookahead != NULL: P2 of plane a+nout), the carry q[a-1] (NULL at the global first plane) and optionally the upper
  * neighbour's q plane, emit gradient + Laplacian of nout planes, accumulate stats and write
- * q[a+nout-1] to carry_out — q itself is never stored. */
+ * q[a+nout-1] to carry_out — q itself is never stored.  With band_off (hszg_band_scan output) P2 is
+ * band-local: row y of plane z adds band_off[z][y / band_rows][:] (look_band_off: the lookahead's). */
 int hszg_zsweep_grad_lap(const int32_t* P2, int64_t n1, int64_t n2, int64_t nout, const int32_t* lookahead,
                          const int32_t* carry, const int32_t* q_upper, int32_t* carry_out, int64_t gz0, int64_t gN0,
-                         double eps, float* const* out, HszgAcc* acc, int exact, void* stream);
+                         double eps, float* const* out, HszgAcc* acc, const int32_t* band_off,
+                         const int32_t* look_band_off, int64_t band_rows, int exact, void* stream);
+/* HSZP_ND decode + row prefix + in-band column prefix in one pass (3-D, canonical, n2 % 32 == 0,
+ * n2 <= 4096, 256 % (n2/32) == 0).  L[z][y][x] = 2-D prefix of plane z restricted to the rows of
+ * y's band (bands of band_rows rows); band_off[z][b][x] = sum of the rows of bands < b, i.e.
+ * P2 = L + band_off[z][y / band_rows].  L: dims[0]*dims[1]*dims[2] int32; band_off:
+ * dims[0]*ceil(dims[1]/band_rows)*dims[2] int32. */
+int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t band_rows, int32_t* L, int32_t* band_off,
+                   void* stream, HszgErr* err);
 /* HSZP_ND decode fused with the in-row prefix (rows of whole chunks, 256 % (n2/32) == 0). */
 int hszg_decode_rowscan(const HszgGeom* g, const HszgStream* s, int32_t* out, void* stream, HszgErr* err);
 /* In-place inclusive scan along the middle axis of an int32 [A][M][L] view. */

@@ -156,6 +156,96 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_tile_blocks(SegGeo sg, BlockTil
     }
 }
 
+// Fast variant for full blocks (every n[i] % B[i] == 0, B2 % 4 == 0, 32 | B0*B1*B2 and
+// 256 % (2048 / (B0*B1)) == 0, e.g. 8x8x8): the tile is k = 8192 / |block| whole blocks along x
+// (a (B0, B1, k*B2) box), decoded with decode32 into the 36-word chunk layout, then written
+// row-major with one 16-byte load + 16-byte store per 4 values; every thread keeps one int4
+// column of the box (gpr = k*B2/4 columns, 256/gpr rows per pass).
+template <typename OutT>
+__device__ __forceinline__ void store4(OutT* p, int4 v, double s);
+template <>
+__device__ __forceinline__ void store4<int32_t>(int32_t* p, int4 v, double) {
+    *reinterpret_cast<int4*>(p) = v;
+}
+template <>
+__device__ __forceinline__ void store4<float>(float* p, int4 v, double s) {
+    *reinterpret_cast<float4*>(p) = make_float4(Conv<float>::go(v.x, s), Conv<float>::go(v.y, s),
+                                                Conv<float>::go(v.z, s), Conv<float>::go(v.w, s));
+}
+template <>
+__device__ __forceinline__ void store4<double>(double* p, int4 v, double s) {
+    reinterpret_cast<double2*>(p)[0] = make_double2(Conv<double>::go(v.x, s), Conv<double>::go(v.y, s));
+    reinterpret_cast<double2*>(p)[1] = make_double2(Conv<double>::go(v.z, s), Conv<double>::go(v.w, s));
+}
+
+template <typename OutT>
+__global__ void __launch_bounds__(TILE_CHUNKS) k_tile_blocks_fast(SegGeo sg, BlockTiles bt,
+                                                                 const uint8_t* __restrict__ payload, uint64_t len,
+                                                                 const uint64_t* __restrict__ offsets,
+                                                                 const int32_t* __restrict__ meta, double two_eps,
+                                                                 OutT* __restrict__ out) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ uint64_t s_lo, s_hi;
+    int32_t* tile = reinterpret_cast<int32_t*>(smem);
+    uint4* sb = reinterpret_cast<uint4*>(smem + kFastTileBytes);
+    const int B0 = (int)sg.B[0], B1 = (int)sg.B[1], B2 = (int)sg.B[2];
+    const int segsz = B0 * B1 * B2;
+    const int cps = segsz >> 5;                               // chunks per block
+    const int64_t tile_id = blockIdx.x;
+    const int64_t row = tile_id / bt.tpr;                     // block row (b0, b1)
+    const int64_t b2a = (tile_id - row * bt.tpr) * bt.k;
+    const int nseg = (int)(sg.G[2] - b2a < bt.k ? sg.G[2] - b2a : bt.k);
+    const int nch = nseg * cps;
+    const int64_t c0 = (row * sg.G[2] + b2a) * cps;           // all blocks full: chunk = block * cps + j
+    if (threadIdx.x == 0) {
+        s_lo = offsets[c0];
+        s_hi = c0 + nch < sg.n_chunks ? offsets[c0 + nch] : payload_end(offsets, sg.n_chunks, len);
+    }
+    __syncthreads();
+    const uint64_t base = stage_range(payload, s_lo, s_hi, sb);
+    uint32_t rel = 0;
+    int32_t m = 0;
+    if ((int)threadIdx.x < nch) {
+        rel = (uint32_t)(__ldg(offsets + c0 + threadIdx.x) - base);
+        m = __ldg(meta + row * sg.G[2] + b2a + threadIdx.x / cps);
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < nch)
+        decode32<false>(reinterpret_cast<const uint32_t*>(sb), rel, tile + threadIdx.x * kChunkStride, m);
+    __syncthreads();
+    const int gpr = (int)bt.k * B2 / 4;                       // int4 columns of a full tile row
+    const int gi = threadIdx.x % gpr;
+    const int step = TILE_CHUNKS / gpr;
+    if (4 * gi >= nseg * B2) return;
+    const int t = (4 * gi) / B2, xl = 4 * gi - t * B2;
+    const int64_t b0 = row / sg.G[1], b1 = row - b0 * sg.G[1];
+    const int64_t n1 = sg.n[1], n2 = sg.n[2];
+    OutT* o = out + (b0 * B0 * n1 + b1 * B1) * n2 + b2a * B2 + 4 * gi;
+    const int plane01 = B0 * B1;
+    int zy = threadIdx.x / gpr;
+    int zl = zy / B1, yl = zy - zl * B1;
+    for (; zy < plane01; zy += step) {
+        const int local = zy * B2 + xl;                       // within block t
+        const int ch = t * cps + (local >> 5);
+        const int4 v = *reinterpret_cast<const int4*>(tile + ch * kChunkStride + (local & 31));
+        store4<OutT>(o + ((int64_t)zl * n1 + yl) * n2, v, two_eps);
+        yl += step;
+        while (yl >= B1) {
+            yl -= B1;
+            zl++;
+        }
+    }
+}
+
+static bool blocks_fast_ok(const SegGeo& sg) {
+    const int64_t B0 = sg.B[0], B1 = sg.B[1], B2 = sg.B[2];
+    const int64_t segsz = B0 * B1 * B2;
+    if (sg.n[0] % B0 || sg.n[1] % B1 || sg.n[2] % B2 || B2 % 4 || segsz % 32 || segsz > TILE_ELEMS) return false;
+    if ((int64_t)TILE_ELEMS % segsz) return false;
+    const int64_t gpr = (TILE_ELEMS / segsz) * B2 / 4;
+    return gpr >= 1 && TILE_CHUNKS % gpr == 0;
+}
+
 // ---- HSZP: flat inclusive scan with decoupled look-back -------------------------
 
 template <typename OutT>
@@ -442,6 +532,18 @@ static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, 
             }
             break;
         case HSZG_HSZX_ND:
+            if (fast && blocks_fast_ok(sg)) {
+                BlockTiles bt;
+                bt.k = TILE_ELEMS / (sg.B[0] * sg.B[1] * sg.B[2]);
+                bt.tpr = (sg.G[2] + bt.k - 1) / bt.k;
+                const int64_t nt = sg.G[0] * sg.G[1] * bt.tpr;
+                const size_t fsmem = kFastTileBytes + stage_bytes(s->max_bitwidth);
+                allow_smem(k_tile_blocks_fast<OutT>, fsmem);
+                k_tile_blocks_fast<OutT><<<(unsigned)nt, TILE_CHUNKS, fsmem, st>>>(
+                    sg, bt, s->payload, s->payload_len, s->offsets, s->metadata, two_eps, out);
+                HSZG_CHECK_LAUNCH("reconstruct hszx-nd");
+                return HSZG_OK;
+            }
             if (fast && blocks_fit_tile(sg)) {
                 BlockTiles bt;
                 // k full segments hold <= TILE_CHUNKS chunks, hence <= TILE_ELEMS values

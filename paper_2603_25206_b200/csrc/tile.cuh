@@ -48,6 +48,87 @@ inline void allow_smem(K kernel, size_t bytes) {
     allow_smem_raw(reinterpret_cast<const void*>(kernel), bytes);
 }
 
+// ---- fast full-chunk decode (K-DEC fast path) -------------------------------------------------
+// Tiles of the fused window kernels hold each 32-value chunk in kChunkStride words: 16-byte aligned,
+// so a thread writes its chunk with 16-byte shared stores (8 threads of a store phase hit 8
+// distinct 4-bank groups: conflict-free) and the row-major write-out reads 16-byte vectors.
+constexpr int kChunkStride = 36;
+constexpr size_t kFastTileBytes = (size_t)TILE_CHUNKS * kChunkStride * 4;
+
+// Values of G = 4 / 2 / 1 per 32-bit funnel window (bw <= 8 / 16 / 32): one shift + mask per value,
+// one bit-cursor advance per group instead of per value, fully unrolled over the chunk's 32 values.
+template <int G, bool Prefix>
+__device__ __forceinline__ uint32_t decode32_g(const uint32_t* w, uint32_t rel, int bw, int32_t* dst, int32_t add) {
+    const uint32_t smask = smem_u32(w, rel + 1);          // 4 sign bytes, value j <-> bit j
+    const uint32_t bitpos = (rel + 5) * 8;
+    uint32_t wi = bitpos >> 5, sh = bitpos & 31;
+    uint32_t cur = w[wi], nxt = w[wi + 1];
+    const uint32_t mask = bw >= 32 ? 0xffffffffu : (1u << bw) - 1u;
+    const uint32_t adv = (uint32_t)(G * bw);
+    uint32_t run = 0;
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+        uint32_t v[4];
+#pragma unroll
+        for (int h = 0; h < 4; h += G) {
+            const uint32_t grp = __funnelshift_r(cur, nxt, sh);
+#pragma unroll
+            for (int i = 0; i < G; i++) {
+                const uint32_t mag = (grp >> (i * bw)) & mask;
+                v[h + i] = ((smask >> (q * 4 + h + i)) & 1u) ? 0u - mag : mag;
+            }
+            sh += adv;
+            if (sh >= 32) {
+                sh -= 32;
+                cur = nxt;
+                wi++;
+                nxt = w[wi + 1];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            run += v[i];
+            v[i] = Prefix ? run : v[i] + (uint32_t)add;
+        }
+        *reinterpret_cast<int4*>(dst + 4 * q) = make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]);
+    }
+    return run;
+}
+
+// Decode one validated FULL chunk (32 values) whose bytes start at byte `rel` of the staged words
+// into dst[0..32) (16-B aligned): the inclusive running sum (Prefix) or value + add.  Returns the
+// chunk sum mod 2^32.  Same bit layout as decode_chunk_words (_bitpack.pyx:124-143).
+template <bool Prefix>
+__device__ __forceinline__ uint32_t decode32(const uint32_t* w, uint32_t rel, int32_t* dst, int32_t add) {
+    const int bw = (int)smem_byte(w, rel);
+    if (bw == 0) {
+        const int4 c = Prefix ? make_int4(0, 0, 0, 0) : make_int4(add, add, add, add);
+#pragma unroll
+        for (int q = 0; q < 8; q++) *reinterpret_cast<int4*>(dst + 4 * q) = c;
+        return 0;
+    }
+    if (bw <= 8) return decode32_g<4, Prefix>(w, rel, bw, dst, add);
+    if (bw <= 16) return decode32_g<2, Prefix>(w, rel, bw, dst, add);
+    return decode32_g<1, Prefix>(w, rel, bw, dst, add);
+}
+
+// staging bytes (after the fast tile) for a tile of chunks whose widest has max_bw bits
+inline size_t stage_bytes(int max_bw) {
+    size_t bytes = (size_t)TILE_CHUNKS * (size_t)chunk_bytes(kChunkCap, max_bw) + 64;
+    return ((bytes + 15) & ~(size_t)15) + 16;
+}
+
+// Stage payload bytes [lo, hi) at 16-B granularity into sb (+ a zero vector after them, read by the
+// bit cursor's look-ahead word).  Returns the payload byte mapped to sb[0].  All threads call it.
+__device__ __forceinline__ uint64_t stage_range(const uint8_t* payload, uint64_t lo, uint64_t hi, uint4* sb) {
+    const uint64_t base = lo & ~(uint64_t)15;
+    const uint32_t nvec = (uint32_t)((hi - base + 15) >> 4);
+    const uint4* g = reinterpret_cast<const uint4*>(payload + base);
+    for (uint32_t i = threadIdx.x; i < nvec; i += blockDim.x) sb[i] = __ldg(g + i);
+    if (threadIdx.x == 0) sb[nvec] = make_uint4(0, 0, 0, 0);
+    return base;
+}
+
 struct TileCtx {
     int64_t c0, c1;      // chunk range
     int64_t e0, e1;      // stream range

@@ -245,7 +245,9 @@ __global__ void __launch_bounds__(ZG_THREADS) k_zsweep(const int32_t* __restrict
                                                        const int32_t* q_upper, int32_t* carry_out, int64_t gz0,
                                                        int64_t gN0, double eps, double two_eps,
                                                        float* __restrict__ o0, float* __restrict__ o1,
-                                                       float* __restrict__ o2, float* __restrict__ o3, HszgAcc* acc) {
+                                                       float* __restrict__ o2, float* __restrict__ o3, HszgAcc* acc,
+                                                       const int32_t* __restrict__ A, const int32_t* lookA,
+                                                       int64_t BR, int64_t nb) {
     const int lane = threadIdx.x & 31;
     const float epsf = __double2float_rn(eps), two_epsf = 2.0f * epsf;
     const int64_t x = ((int64_t)blockIdx.x * ZG_THREADS + threadIdx.x) * 4;
@@ -271,17 +273,11 @@ __global__ void __launch_bounds__(ZG_THREADS) k_zsweep(const int32_t* __restrict
         if (lane == 31 && xi + 4 < n2) qr = __ldg(carry + off + 4);
     }
     int4 prev = qc;                                     // q[a-1]
-    // advance to plane a
-    if (active) {
-        const int32_t* p = P2 + off;
-        qc = add4(qc, ld4(p));
-        if (yin) {
-            qm = add4(qm, ld4(p - n2));
-            qp = add4(qp, ld4(p + n2));
-        }
-        if (lane == 0 && xi > 0) ql += __ldg(p - 1);
-        if (lane == 31 && xi + 4 < n2) qr += __ldg(p + 4);
-    }
+    // band offsets (k_band_scan): row y' of plane zz adds A[zz][y' / BR]
+    const int64_t aplane = nb * n2;
+    const int64_t ac = A ? (y / BR) * n2 + xi : 0;
+    const int64_t am = (A && yin) ? ((y - 1) / BR) * n2 + xi : 0;
+    const int64_t ap = (A && yin) ? ((y + 1) / BR) * n2 + xi : 0;
     // P2 rows of plane zz (zz == nout is the lookahead plane), loaded one iteration ahead so the
     // loads of plane z+2 are in flight while plane z is emitted (software pipelining)
     auto wanted = [&](int64_t zz) -> bool {       // will iteration zz-1 build q[zz] from P2[zz]?
@@ -299,7 +295,28 @@ __global__ void __launch_bounds__(ZG_THREADS) k_zsweep(const int32_t* __restrict
         }
         if (lane == 0 && xi > 0) l_ = __ldg(p - 1);
         if (lane == 31 && xi + 4 < n2) r_ = __ldg(p + 4);
+        if (A) {
+            const int32_t* a = zz < nout ? A + zz * aplane : lookA;
+            c_ = add4(c_, ld4(a + ac));
+            if (yin) {
+                m_ = add4(m_, ld4(a + am));
+                p_ = add4(p_, ld4(a + ap));
+            }
+            if (lane == 0 && xi > 0) l_ += __ldg(a + ac - 1);
+            if (lane == 31 && xi + 4 < n2) r_ += __ldg(a + ac + 4);
+        }
     };
+    // advance to plane a
+    if (active) {
+        int4 t_c = z4, t_m = z4, t_p = z4;
+        int t_l = 0, t_r = 0;
+        fetch(0, t_c, t_m, t_p, t_l, t_r);
+        qc = add4(qc, t_c);
+        qm = add4(qm, t_m);
+        qp = add4(qp, t_p);
+        ql += t_l;
+        qr += t_r;
+    }
     if (wanted(1)) fetch(1, pc, pm, pp, pl, pr);
     for (int64_t z = 0; z < nout; z++) {
         const int64_t gz = gz0 + z;
@@ -381,6 +398,110 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_tile_rowscan(SegGeo sg, const u
     for (int i = threadIdx.x; i < n; i += blockDim.x) out[t.e0 + i] = vals[pad_idx(i)];
 }
 
+// ---- HSZP_ND band scan: decode + x prefix + y prefix in one pass (replaces rowscan + col_scan) ----
+// CTA (band b, plane z) walks the rows [b*BR, min((b+1)*BR, n1)) of plane z a tile at a time
+// (256 chunks = 256/cpr whole rows): fast decode with the in-chunk running sum, a segmented scan of
+// the chunk sums along each row (x prefix), then the row-major write-out adds each thread's running
+// column sums (y prefix inside the band).  It writes L = the band-local 2-D prefix and the band's
+// column totals A[z][b][:]; k_band_prefix makes A exclusive over the bands, so the 2-D prefix is
+// P2[z][y][x] = L[z][y][x] + A[z][y / BR][x], added by k_zsweep as it loads rows.  All int32
+// arithmetic wraps; every prefix is a q sum mod 2^32 (recon.cu header).
+constexpr int BS_MAXG = 4;   // int4 column groups per thread: n2 <= 4 * 4 * TILE_CHUNKS = 4096
+
+__device__ __forceinline__ int4 add4u(int4 a, uint32_t o) {
+    return make_int4((int)((uint32_t)a.x + o), (int)((uint32_t)a.y + o), (int)((uint32_t)a.z + o),
+                     (int)((uint32_t)a.w + o));
+}
+
+__global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __restrict__ payload, uint64_t len,
+                                                          const uint64_t* __restrict__ offsets, int64_t n_chunks,
+                                                          int n1, int n2, int BR, int32_t* __restrict__ L,
+                                                          int32_t* __restrict__ A) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ uint32_t s_off[TILE_CHUNKS];
+    __shared__ uint32_t s_wt[TILE_CHUNKS / 32];
+    __shared__ uint64_t s_lo, s_hi;
+    const int cpr = n2 >> 5;                 // chunks per row (a power of two dividing 256)
+    const int rpt = TILE_CHUNKS / cpr;       // rows per tile
+    const int b = blockIdx.x, nb = gridDim.x;
+    const int64_t z = blockIdx.y;
+    const int y0 = b * BR;
+    const int y1 = min(y0 + BR, n1);
+    const int ng = n2 >> 2;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int32_t* tile = reinterpret_cast<int32_t*>(smem);
+    uint4* sb = reinterpret_cast<uint4*>(smem + kFastTileBytes);
+    const uint32_t* words = reinterpret_cast<const uint32_t*>(sb);
+    int4 ysum[BS_MAXG];
+#pragma unroll
+    for (int k = 0; k < BS_MAXG; k++) ysum[k] = make_int4(0, 0, 0, 0);
+    for (int r0 = y0; r0 < y1; r0 += rpt) {
+        const int nr = min(rpt, y1 - r0);
+        const int nch = nr * cpr;
+        const int64_t c0 = (z * n1 + r0) * (int64_t)cpr;
+        if (threadIdx.x == 0) {
+            s_lo = offsets[c0];
+            s_hi = c0 + nch < n_chunks ? offsets[c0 + nch] : payload_end(offsets, n_chunks, len);
+        }
+        __syncthreads();
+        const uint64_t base = stage_range(payload, s_lo, s_hi, sb);
+        uint32_t rel = 0;
+        if ((int)threadIdx.x < nch) rel = (uint32_t)(__ldg(offsets + c0 + threadIdx.x) - base);
+        __syncthreads();
+        uint32_t tot = 0;
+        if ((int)threadIdx.x < nch) tot = decode32<true>(words, rel, tile + threadIdx.x * kChunkStride, 0);
+        // exclusive prefix of the chunk sums along each row
+        uint32_t inc = tot;
+        const int wseg = cpr < 32 ? cpr : 32;
+        for (int d = 1; d < wseg; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+            if ((lane & (wseg - 1)) >= d) inc += o;
+        }
+        if (cpr > 32) {
+            if (lane == 31) s_wt[warp] = inc;
+            __syncthreads();
+            for (int w2 = warp & ~((cpr >> 5) - 1); w2 < warp; w2++) inc += s_wt[w2];
+        }
+        s_off[threadIdx.x] = inc - tot;
+        __syncthreads();
+        for (int rr = 0; rr < nr; rr++) {
+            int32_t* orow = L + (z * n1 + r0 + rr) * (int64_t)n2;
+#pragma unroll
+            for (int k = 0; k < BS_MAXG; k++) {
+                const int gi = threadIdx.x + k * TILE_CHUNKS;
+                if (gi < ng) {
+                    const int ch = rr * cpr + (gi >> 3);
+                    const int4 v = *reinterpret_cast<const int4*>(tile + ch * kChunkStride + ((gi & 7) << 2));
+                    ysum[k] = add4(ysum[k], add4u(v, s_off[ch]));
+                    *reinterpret_cast<int4*>(orow + 4 * gi) = ysum[k];
+                }
+            }
+        }
+        __syncthreads();
+    }
+    int32_t* arow = A + (z * nb + b) * (int64_t)n2;
+#pragma unroll
+    for (int k = 0; k < BS_MAXG; k++) {
+        const int gi = threadIdx.x + k * TILE_CHUNKS;
+        if (gi < ng) *reinterpret_cast<int4*>(arow + 4 * gi) = ysum[k];
+    }
+}
+
+// A[z][b][:] band totals -> exclusive prefix over b (one thread per (plane, int4 column group))
+__global__ void k_band_prefix(int32_t* A, int nb, int64_t n2, int64_t np) {
+    const int64_t ng = n2 >> 2;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= np * ng) return;
+    const int64_t z = i / ng, g = i - z * ng;
+    int4* p = reinterpret_cast<int4*>(A + z * nb * n2) + g;
+    int4 run = make_int4(0, 0, 0, 0);
+    for (int b = 0; b < nb; b++) {
+        const int4 t = p[b * ng];
+        p[b * ng] = run;
+        run = add4(run, t);
+    }
+}
+
 __global__ void k_acc_reset(HszgAcc* acc) {
     if (threadIdx.x == 0) {
         for (int k = 0; k < 4; k++) {
@@ -420,17 +541,46 @@ extern "C" int hszg_zgrad_lap(const int32_t* q, int64_t n1, int64_t n2, int64_t 
 
 extern "C" int hszg_zsweep_grad_lap(const int32_t* P2, int64_t n1, int64_t n2, int64_t nout, const int32_t* lookahead,
                                     const int32_t* carry, const int32_t* q_upper, int32_t* carry_out, int64_t gz0,
-                                    int64_t gN0, double eps, float* const* out, HszgAcc* acc, int exact,
-                                    void* stream) {
+                                    int64_t gN0, double eps, float* const* out, HszgAcc* acc,
+                                    const int32_t* band_off, const int32_t* look_band_off, int64_t band_rows,
+                                    int exact, void* stream) {
     if (n2 % 4 || !al16(P2) || !al16(out[0]) || !al16(out[1]) || !al16(out[2]) || !al16(out[3]) || n1 > 65535 ||
-        (carry && !al16(carry)) || (q_upper && !al16(q_upper)) || (carry_out && !al16(carry_out)))
+        (carry && !al16(carry)) || (q_upper && !al16(q_upper)) || (carry_out && !al16(carry_out)) ||
+        (band_off && (band_rows < 1 || !al16(band_off) || (lookahead && (!look_band_off || !al16(look_band_off))))))
         return HSZG_INVALID_ARG;
+    const int64_t nb = band_off ? (n1 + band_rows - 1) / band_rows : 0;
     if (nout <= 0) return HSZG_OK;
     dim3 grid((unsigned)((n2 / 4 + ZG_THREADS - 1) / ZG_THREADS), (unsigned)n1);
     (exact ? k_zsweep<true> : k_zsweep<false>)<<<grid, ZG_THREADS, 0, as_stream(stream)>>>(P2, n1, n2, nout, lookahead, carry, q_upper, carry_out,
                                                          gz0, gN0, eps, 2.0 * eps, out[0], out[1], out[2], out[3],
-                                                         acc);
+                                                         acc, band_off, look_band_off, band_rows, nb);
     return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
+}
+
+extern "C" int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t band_rows, int32_t* L, int32_t* A,
+                              void* stream, HszgErr* err) {
+    err->status = HSZG_OK;
+    const int64_t n1 = g->dims[1], n2 = g->dims[2], np = g->dims[0];
+    const int64_t cpr = n2 / kChunkCap;
+    if (g->kind != HSZG_HSZP_ND || g->ndims != 3 || !s->canonical || n2 % kChunkCap || cpr < 1 ||
+        TILE_CHUNKS % cpr || n2 > 4 * BS_MAXG * TILE_CHUNKS || band_rows < 1 || n1 > INT32_MAX || np > 65535 ||
+        !al16(L) || !al16(A)) {
+        err->status = HSZG_INVALID_ARG;
+        snprintf(err->message, sizeof(err->message),
+                 "band_scan needs a canonical 3-D HSZP_ND stream with whole-chunk rows (n2 %% 32 == 0, "
+                 "n2 <= 4096, 256 %% (n2/32) == 0)");
+        return HSZG_INVALID_ARG;
+    }
+    if (g->n_chunks == 0) return HSZG_OK;
+    const int64_t nb = (n1 + band_rows - 1) / band_rows;
+    const size_t smem = kFastTileBytes + stage_bytes(s->max_bitwidth);
+    allow_smem(k_band_scan, smem);
+    k_band_scan<<<dim3((unsigned)nb, (unsigned)np), TILE_CHUNKS, smem, as_stream(stream)>>>(
+        s->payload, s->payload_len, s->offsets, g->n_chunks, (int)n1, (int)n2, (int)band_rows, L, A);
+    const int64_t threads = np * (n2 / 4);
+    k_band_prefix<<<(unsigned)((threads + 255) / 256), 256, 0, as_stream(stream)>>>(A, (int)nb, n2, np);
+    if (cudaGetLastError() != cudaSuccess) return hszg_set_cuda_error(err, cudaGetLastError(), "band_scan");
+    return HSZG_OK;
 }
 
 extern "C" int hszg_decode_rowscan(const HszgGeom* g, const HszgStream* s, int32_t* out, void* stream, HszgErr* err) {

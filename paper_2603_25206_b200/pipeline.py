@@ -32,6 +32,8 @@ import numpy as np
 
 from . import _lib
 
+_SMS = 148          # B200 SM count (grid sizing only)
+
 HSZP_ND, HSZX_ND = 1, 3
 SUMS_BYTES = 64
 
@@ -388,6 +390,7 @@ class WindowPipeline:
     # fp32 outputs of the fused loop: True = fl32 of the reference float64 (bit-exact vs the oracle);
     # False = int32 stencil x fl32(eps) in fp32 (<= 2^-23 relative, no fp64 conversions: faster).
     exact_fp32 = False
+    band_rows_req = None        # force a band height for hszg_band_scan (tests); None: sized for the grid
 
     # -- fused loops (window.cu) ---------------------------------------------------------------
     def _persistent(self):
@@ -402,8 +405,25 @@ class WindowPipeline:
         self.halo_buf = t.zeros((2, n1, n2), dtype=t.int32, device=dev)       # [lower, upper]
         self.carry_buf = t.zeros((3, n1, n2), dtype=t.int32, device=dev)      # [rank carry, ping, pong]
         self.acc = t.zeros(ACC_BYTES, dtype=t.uint8, device=dev)
+        self.band_rows = self._band_rows() if self.sf.kind == HSZP_ND else 0
+        if self.band_rows:
+            nb = -(-n1 // self.band_rows)
+            self.bands = [t.empty((self.W, nb, n2), dtype=t.int32, device=dev) for _ in range(nslots)]
         self._pers_W = self.W
         self._graph = None
+
+    def _band_rows(self) -> int:
+        """Rows per band of hszg_band_scan (0: not applicable -> decode_rowscan + col_scan): whole tiles
+        of 256 chunks, and enough bands that a window launches >= 8 CTAs per SM."""
+        n1, n2 = self.sf.global_dims[1], self.sf.global_dims[2]
+        if n2 % 32 or n2 > 4096 or 256 % (n2 // 32):
+            return 0
+        rpt = 256 // (n2 // 32)
+        if self.band_rows_req:
+            return int(self.band_rows_req)
+        want = -(-8 * _SMS // max(1, min(self.W, self.sf.nz)))
+        br = -(-n1 // want)
+        return max(rpt, -(-br // rpt) * rpt)
 
     def _stage_boundary(self):
         """Copy this run's halo / carry planes into the persistent buffers read by the loop."""
@@ -491,15 +511,22 @@ class WindowPipeline:
         wins = self._windows()
         nw = len(wins)
 
+        br = self.band_rows
+
         def decode(k):
             a, b = wins[k]
             if self.timer:
                 self.timer.begin("reconstruct")
             sub = self.ds.plane_view(a, b)
             err = _lib.Err()
-            _lib.call("hszg_decode_rowscan", ctypes.byref(sub.geom), ctypes.byref(sub.desc), _lib.ptr(ring[k % 2]),
-                      _lib.stream_handle(), ctypes.byref(err), err=err)
-            _lib.call("hszg_col_scan", _lib.ptr(ring[k % 2]), b - a, n1, n2, _lib.stream_handle())
+            if br:
+                _lib.call("hszg_band_scan", ctypes.byref(sub.geom), ctypes.byref(sub.desc), br,
+                          _lib.ptr(ring[k % 2]), _lib.ptr(self.bands[k % 2]), _lib.stream_handle(),
+                          ctypes.byref(err), err=err)
+            else:
+                _lib.call("hszg_decode_rowscan", ctypes.byref(sub.geom), ctypes.byref(sub.desc),
+                          _lib.ptr(ring[k % 2]), _lib.stream_handle(), ctypes.byref(err), err=err)
+                _lib.call("hszg_col_scan", _lib.ptr(ring[k % 2]), b - a, n1, n2, _lib.stream_handle())
             if self.timer:
                 self.timer.end("reconstruct", self._range_bytes(a, b) + 4 * (b - a) * self.plane)
 
@@ -517,6 +544,8 @@ class WindowPipeline:
                       _lib.ptr(look) if look is not None else None, _lib.ptr(carry) if carry is not None else None,
                       _lib.ptr(upper) if upper is not None else None, _lib.ptr(out_carry), sf.z0 + a,
                       sf.global_dims[0], ctypes.c_double(sf.eps), self._outs_arr(outs, a, b), _lib.ptr(self.acc),
+                      _lib.ptr(self.bands[k % 2]) if br else None,
+                      _lib.ptr(self.bands[(k + 1) % 2]) if (br and look is not None) else None, br,
                       int(self.exact_fp32), _lib.stream_handle())
             if self.timer:
                 self.timer.end("stencil", (4 + 16) * (b - a) * self.plane)

@@ -96,6 +96,8 @@ def test_window_pipeline_single_rank(setup, kind, window, exact):
     sf = pipeline.compress_shard(fd, kind, eps, (8, 8, 8), 0, dims[0], dims)
     pipe = pipeline.WindowPipeline(sf, pipeline.Comm(), window)
     pipe.exact_fp32 = exact
+    if kind == 1 and window == 16:
+        pipe.band_rows_req = 5          # several bands, partial tiles and a short last band
     outs = [torch.empty(dims, dtype=torch.float32, device="cuda") for _ in range(4)]
     res = pipe.run(outs)
     want, s1, s2, mean, var = _oracle_outputs(field, kind, eps)
@@ -119,6 +121,7 @@ def test_window_pipeline_emulated_ranks(setup, kind, world):
         sf = pipeline.compress_shard(fd[z0 - lead:z1].contiguous(), kind, eps, (8, 8, 8), z0, z1, dims)
         ranks.append(pipeline.WindowPipeline(sf, pipeline.Comm(), 8))
         ranks[-1].exact_fp32 = True
+        ranks[-1].band_rows_req = 3 + r
     mine = [p.local_boundary(need_total=True) for p in ranks]
     Ts = [m["T"] for m in mine] if kind == 1 else None
     carries = [p.carry_from(Ts, r) for r, p in enumerate(ranks)]
@@ -141,3 +144,52 @@ def test_window_pipeline_emulated_ranks(setup, kind, world):
     assert tot1 == s1 and tot2 == s2
     n = int(np.prod(dims))
     assert pipeline.finalize_mean_var(tot1, tot2, n, eps) == (mean, var)
+
+
+def _wide_bitwidth_field(rng, dims):
+    """Noise whose amplitude changes every 8 x-values (bit widths 0 .. ~22), plus a constant region."""
+    n2 = dims[2]
+    scale = 10.0 ** rng.uniform(-4, 3, size=n2 // 8).repeat(8)
+    f = rng.normal(size=dims) * scale[None, None, :]
+    f[:, :, :16] = 0.5                          # all-zero residual chunks (bw 0)
+    return f.astype(np.float32)
+
+
+@pytest.mark.parametrize("dims", [(16, 16, 256), (24, 8, 64)], ids=lambda d: "x".join(map(str, d)))
+def test_fast_decode_bitwidths_hszx_nd(dims):
+    """k_tile_blocks_fast (full 8^3 blocks) across bit widths 0..~22 vs the oracle's stage 3."""
+    import paper_2603_25206_b200 as h
+
+    rng = np.random.default_rng(123)
+    f = _wide_bitwidth_field(rng, dims)
+    c = h.compress(f, h.CompressorKind(3), h.ErrorBound("abs", 1e-3), (8, 8, 8))
+    ref = O.compress(f, 3, "abs", 1e-3, (8, 8, 8))
+    bws = {ref.payload[int(o)] for o in ref.offsets}
+    assert 0 in bws and max(bws) > 16 and any(8 < b <= 16 for b in bws)
+    q = h.partial_decompress(c, h.Stage.QUANTIZED).values
+    assert np.array_equal(np.asarray(q), O.stage3(ref))
+
+
+@pytest.mark.parametrize("dims", [(16, 16, 256), (24, 40, 64)], ids=lambda d: "x".join(map(str, d)))
+@pytest.mark.parametrize("band_rows", [None, 1, 7])
+def test_fast_decode_bitwidths_band_scan(dims, band_rows):
+    """hszg_band_scan (decode32 + row prefix + banded column prefix) across bit widths, through the
+    HSZP_ND window pipeline (exact mode), vs the oracle."""
+    import torch
+
+    from paper_2603_25206_b200 import pipeline
+
+    rng = np.random.default_rng(321)
+    f = _wide_bitwidth_field(rng, dims)
+    eps = 1e-3
+    fd = torch.from_numpy(f).cuda()
+    sf = pipeline.compress_shard(fd, 1, eps, (8, 8, 8), 0, dims[0], dims)
+    pipe = pipeline.WindowPipeline(sf, pipeline.Comm(), 8)
+    pipe.exact_fp32 = True
+    pipe.band_rows_req = band_rows
+    outs = [torch.empty(dims, dtype=torch.float32, device="cuda") for _ in range(4)]
+    res = pipe.run(outs)
+    want, s1, s2, mean, var = _oracle_outputs(f, 1, eps)
+    for k, (got, w) in enumerate(zip(outs, want)):
+        assert np.array_equal(got.cpu().numpy(), w), k
+    assert res["s1"] == s1 and res["s2"] == s2
