@@ -380,6 +380,9 @@ def run_e2e(args, shards, pipes, outs, comm, n_total):
                                              "pipeline -> D2H of all four fp32 outputs (per rank)"}
 
 
+CPU_SECONDS = 10.0
+
+
 def build_cpu_sample(field_dev, eps):
     """The CPU sample's containers, compressed on the GPU (bit-identical to oracle.compress)."""
     from oracle import cpu_pipeline as CP
@@ -409,12 +412,15 @@ def cpu_baseline(blobs):
     pool = CP.make_pool(cores)
     CP.run_sample(blobs[: max(1, min(len(blobs), cores))], pool)     # warm the workers
     dt, elems, _ = CP.run_sample(blobs, pool)
+    passes = max(1, math.ceil(CPU_SECONDS / max(dt, 1e-3)))          # ~10 s of CPU work
+    if passes > 1:
+        dt, elems, _ = CP.run_sample(blobs * passes, pool)
     if pool is not None:
         pool.shutdown()
     return {"value": round(4.0 * elems / dt / 1e9, 4), "unit": "GB/s", "cores": cores, "kind": "port",
             "sample": f"{len(blobs)} containers of {CP.SUB_PLANES}x{CP.SUB_ROWS}x2048 from the config-5 field "
-                      f"({elems} values, HSZP_ND + HSZX_ND): oracle decode + recorrelate + exact sums + gradient "
-                      f"+ Laplacian, {min(cores, len(blobs))} processes, {dt:.2f} s"}
+                      f"x {passes} passes ({elems} values, HSZP_ND + HSZX_ND): oracle decode + recorrelate + exact "
+                      f"sums + gradient + Laplacian, {min(cores, len(blobs))} processes, {dt:.2f} s"}
 
 
 # ---------------------------------------------------------------------------
