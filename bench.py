@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--exact-fp32", action="store_true",
                     help="fp32 outputs = fl32 of the reference float64 (default: fast fp32, <= 2^-22 relative)")
     ap.add_argument("--no-graph", action="store_true", help="launch the window loop eagerly instead of a CUDA graph")
+    ap.add_argument("--no-one-pass", action="store_true", help="HSZX_ND: two-pass (decode, then stencil) windows")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -234,6 +235,7 @@ def run_ours(args):
         p._range_bytes(0, 1)            # fetch the plane-boundary offsets for the timers now, not when timed
         p.use_graph = not args.no_graph
         p.exact_fp32 = args.exact_fp32
+        p.one_pass = not args.no_one_pass
     container_bytes = {k: shards[k].ds.nbytes() for k in KINDS}
     setup_s = time.time() - t_setup
 

@@ -270,6 +270,14 @@ int hszg_zsweep_grad_lap(const int32_t* P2, int64_t n1, int64_t n2, int64_t nout
                          const int32_t* carry, const int32_t* q_upper, int32_t* carry_out, int64_t gz0, int64_t gN0,
                          double eps, float* const* out, HszgAcc* acc, const int32_t* band_off,
                          const int32_t* look_band_off, int64_t band_rows, int exact, void* stream);
+/* HSZX_ND one-pass decode + gradient + Laplacian + stats (8x8x8 blocks dividing the 3-D box, canonical,
+ * max bit width <= 16): q never reaches memory.  The stream is a z-slab of a gN0-plane field whose
+ * first plane is global plane gz0; halo_lo / halo_hi (optional, n1*n2 int32) are q of the planes just
+ * below / above the slab.  zlayers = 8-plane block layers per CTA (z segment of the grid).
+ * out[4] = dz, dy, dx, Laplacian (fp32, slab-sized); acc (optional) accumulates the slab's stats. */
+int hszg_fused_blocks(const HszgGeom* g, const HszgStream* s, int64_t gz0, int64_t gN0, const int32_t* halo_lo,
+                      const int32_t* halo_hi, float* const* out, HszgAcc* acc, int64_t zlayers, int exact,
+                      void* stream, HszgErr* err);
 /* HSZP_ND decode + row prefix + in-band column prefix in one pass (3-D, canonical, n2 % 32 == 0,
  * n2 <= 4096, 256 % (n2/32) == 0).  L[z][y][x] = 2-D prefix of plane z restricted to the rows of
  * y's band (bands of band_rows rows); band_off[z][b][x] = sum of the rows of bands < b, i.e.

@@ -57,8 +57,8 @@ constexpr size_t kFastTileBytes = (size_t)TILE_CHUNKS * kChunkStride * 4;
 
 // Values of G = 4 / 2 / 1 per 32-bit funnel window (bw <= 8 / 16 / 32): one shift + mask per value,
 // one bit-cursor advance per group instead of per value, fully unrolled over the chunk's 32 values.
-template <int G, bool Prefix>
-__device__ __forceinline__ uint32_t decode32_g(const uint32_t* w, uint32_t rel, int bw, int32_t* dst, int32_t add) {
+template <int G, bool Prefix, typename Store>
+__device__ __forceinline__ uint32_t decode32_g(const uint32_t* w, uint32_t rel, int bw, int32_t add, Store store) {
     const uint32_t smask = smem_u32(w, rel + 1);          // 4 sign bytes, value j <-> bit j
     const uint32_t bitpos = (rel + 5) * 8;
     uint32_t wi = bitpos >> 5, sh = bitpos & 31;
@@ -90,26 +90,77 @@ __device__ __forceinline__ uint32_t decode32_g(const uint32_t* w, uint32_t rel, 
             run += v[i];
             v[i] = Prefix ? run : v[i] + (uint32_t)add;
         }
-        *reinterpret_cast<int4*>(dst + 4 * q) = make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]);
+        store(q, make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]));
     }
     return run;
 }
 
-// Decode one validated FULL chunk (32 values) whose bytes start at byte `rel` of the staged words
-// into dst[0..32) (16-B aligned): the inclusive running sum (Prefix) or value + add.  Returns the
-// chunk sum mod 2^32.  Same bit layout as decode_chunk_words (_bitpack.pyx:124-143).
-template <bool Prefix>
-__device__ __forceinline__ uint32_t decode32(const uint32_t* w, uint32_t rel, int32_t* dst, int32_t add) {
+// Decode one validated FULL chunk (32 values) whose bytes start at byte `rel` of the staged words:
+// store(g, int4) receives values 4g..4g+3 — the inclusive running sum (Prefix) or value + add.
+// Returns the chunk sum mod 2^32.  Same bit layout as decode_chunk_words (_bitpack.pyx:124-143).
+template <bool Prefix, typename Store>
+__device__ __forceinline__ uint32_t decode32s(const uint32_t* w, uint32_t rel, int32_t add, Store store) {
     const int bw = (int)smem_byte(w, rel);
     if (bw == 0) {
         const int4 c = Prefix ? make_int4(0, 0, 0, 0) : make_int4(add, add, add, add);
 #pragma unroll
-        for (int q = 0; q < 8; q++) *reinterpret_cast<int4*>(dst + 4 * q) = c;
+        for (int q = 0; q < 8; q++) store(q, c);
         return 0;
     }
-    if (bw <= 8) return decode32_g<4, Prefix>(w, rel, bw, dst, add);
-    if (bw <= 16) return decode32_g<2, Prefix>(w, rel, bw, dst, add);
-    return decode32_g<1, Prefix>(w, rel, bw, dst, add);
+    if (bw <= 8) return decode32_g<4, Prefix>(w, rel, bw, add, store);
+    if (bw <= 16) return decode32_g<2, Prefix>(w, rel, bw, add, store);
+    return decode32_g<1, Prefix>(w, rel, bw, add, store);
+}
+
+// Values 8k .. 8k+7 of a validated FULL chunk (k = 0..3): the bit cursor starts at value 8k
+// directly (the bit width is uniform in a chunk), so a chunk splits into 4 independent jobs.
+template <int G>
+__device__ __forceinline__ void decode8_g(const uint32_t* w, uint32_t rel, int bw, int k, int32_t add, int4& lo,
+                                          int4& hi) {
+    const uint32_t smask = smem_u32(w, rel + 1) >> (8 * k);
+    const uint32_t bitpos = (rel + 5) * 8 + (uint32_t)(8 * k * bw);
+    uint32_t wi = bitpos >> 5, sh = bitpos & 31;
+    uint32_t cur = w[wi], nxt = w[wi + 1];
+    const uint32_t mask = bw >= 32 ? 0xffffffffu : (1u << bw) - 1u;
+    const uint32_t adv = (uint32_t)(G * bw);
+    uint32_t v[8];
+#pragma unroll
+    for (int h = 0; h < 8; h += G) {
+        const uint32_t grp = __funnelshift_r(cur, nxt, sh);
+#pragma unroll
+        for (int i = 0; i < G; i++) {
+            const uint32_t mag = (grp >> (i * bw)) & mask;
+            v[h + i] = (((smask >> (h + i)) & 1u) ? 0u - mag : mag) + (uint32_t)add;
+        }
+        if (h + G < 8) {
+            sh += adv;
+            if (sh >= 32) {
+                sh -= 32;
+                cur = nxt;
+                wi++;
+                nxt = w[wi + 1];
+            }
+        }
+    }
+    lo = make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]);
+    hi = make_int4((int)v[4], (int)v[5], (int)v[6], (int)v[7]);
+}
+
+__device__ __forceinline__ void decode8(const uint32_t* w, uint32_t rel, int k, int32_t add, int4& lo, int4& hi) {
+    const int bw = (int)smem_byte(w, rel);
+    if (bw == 0) {
+        lo = hi = make_int4(add, add, add, add);
+        return;
+    }
+    if (bw <= 8) return decode8_g<4>(w, rel, bw, k, add, lo, hi);
+    if (bw <= 16) return decode8_g<2>(w, rel, bw, k, add, lo, hi);
+    return decode8_g<1>(w, rel, bw, k, add, lo, hi);
+}
+
+// decode32s into dst[0..32) (16-B aligned) with 16-byte shared stores
+template <bool Prefix>
+__device__ __forceinline__ uint32_t decode32(const uint32_t* w, uint32_t rel, int32_t* dst, int32_t add) {
+    return decode32s<Prefix>(w, rel, add, [&](int q, int4 v) { *reinterpret_cast<int4*>(dst + 4 * q) = v; });
 }
 
 // staging bytes (after the fast tile) for a tile of chunks whose widest has max_bw bits

@@ -14,143 +14,9 @@
 #include <cstdio>
 #include "tile.cuh"
 #include "lookback.cuh"
+#include "stencil.cuh"
 
 namespace hszg {
-
-__device__ __forceinline__ void acc_add_i128(unsigned long long* limbs, i128 v) {
-    const u128 u = (u128)v;
-    const unsigned long long l0 = (unsigned long long)(uint32_t)u;
-    const unsigned long long l1 = (unsigned long long)(uint32_t)(u >> 32);
-    const unsigned long long l2 = (unsigned long long)(uint32_t)(u >> 64);
-    const long long l3 = (long long)(int32_t)(uint32_t)(u >> 96);   // signed top limb
-    if (l0) atomicAdd(limbs + 0, l0);
-    if (l1) atomicAdd(limbs + 1, l1);
-    if (l2) atomicAdd(limbs + 2, l2);
-    if (l3) atomicAdd(limbs + 3, (unsigned long long)l3);
-}
-
-struct WinStats {
-    int64_t s1_64;   // per-thread partial: <= 4*W terms of |q| < 2^31
-    i128 s1, s2;
-    int32_t vmin, vmax;
-    __device__ __forceinline__ void init() { s1_64 = 0; s1 = 0; s2 = 0; vmin = INT32_MAX; vmax = INT32_MIN; }
-    __device__ __forceinline__ void add4(int4 q) {
-        s1_64 += (int64_t)q.x + q.y + q.z + q.w;
-        // four squares < 4 * 2^62 = 2^64: exact in u64, one 128-bit add per four values
-        const uint64_t sq = (uint64_t)((int64_t)q.x * q.x) + (uint64_t)((int64_t)q.y * q.y) +
-                            (uint64_t)((int64_t)q.z * q.z) + (uint64_t)((int64_t)q.w * q.w);
-        s2 += (i128)(u128)sq;
-        vmin = min(vmin, min(min(q.x, q.y), min(q.z, q.w)));
-        vmax = max(vmax, max(max(q.x, q.y), max(q.z, q.w)));
-    }
-    // warp-reduce, then one lane publishes
-    __device__ __forceinline__ void flush(HszgAcc* acc, int64_t count) {
-        s1 += s1_64;
-        for (int d = 16; d > 0; d >>= 1) {
-            s1 += shfl_down_i128(s1, d);
-            s2 += shfl_down_i128(s2, d);
-            vmin = min(vmin, __shfl_down_sync(0xffffffffu, vmin, d));
-            vmax = max(vmax, __shfl_down_sync(0xffffffffu, vmax, d));
-            count += __shfl_down_sync(0xffffffffu, count, d);
-        }
-        if ((threadIdx.x & 31) == 0 && count) {
-            acc_add_i128(reinterpret_cast<unsigned long long*>(acc->s1_limb), s1);
-            acc_add_i128(reinterpret_cast<unsigned long long*>(acc->s2_limb), s2);
-            atomicAdd(reinterpret_cast<unsigned long long*>(&acc->count), (unsigned long long)count);
-            atomicMin(&acc->vmin, vmin);
-            atomicMax(&acc->vmax, vmax);
-        }
-    }
-};
-
-__device__ __forceinline__ float4 sc4(int64_t a, int64_t b, int64_t c, int64_t d, double s) {
-    return make_float4(__double2float_rn(__dmul_rn((double)a, s)), __double2float_rn(__dmul_rn((double)b, s)),
-                       __double2float_rn(__dmul_rn((double)c, s)), __double2float_rn(__dmul_rn((double)d, s)));
-}
-
-__device__ __forceinline__ int4 add4(int4 a, int4 b) {
-    return make_int4((int)((uint32_t)a.x + (uint32_t)b.x), (int)((uint32_t)a.y + (uint32_t)b.y),
-                     (int)((uint32_t)a.z + (uint32_t)b.z), (int)((uint32_t)a.w + (uint32_t)b.w));
-}
-
-__device__ __forceinline__ int4 ld4(const int32_t* p) { return __ldg(reinterpret_cast<const int4*>(p)); }
-
-// Emit gradient (dz, dy, dx) + Laplacian for 4 x-points given the 7-point neighbourhood.
-__device__ __forceinline__ void emit4(float* o0, float* o1, float* o2, float* o3, int64_t o, bool zin, bool yin,
-                                      int64_t xi, int64_t n2, int4 zm, int4 c, int4 zp, int4 ym, int4 yp,
-                                      int32_t left, int32_t right, double eps, double two_eps) {
-    const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
-    float4 dz = zero, dy = zero, lp = zero;
-    if (zin) dz = sc4((int64_t)zp.x - zm.x, (int64_t)zp.y - zm.y, (int64_t)zp.z - zm.z, (int64_t)zp.w - zm.w, eps);
-    if (yin) dy = sc4((int64_t)yp.x - ym.x, (int64_t)yp.y - ym.y, (int64_t)yp.z - ym.z, (int64_t)yp.w - ym.w, eps);
-    int64_t d0 = (int64_t)c.y - left, d1 = (int64_t)c.z - c.x, d2 = (int64_t)c.w - c.y, d3 = (int64_t)right - c.z;
-    if (xi == 0) d0 = 0;
-    if (xi + 3 >= n2 - 1) d3 = 0;
-    const float4 dx = sc4(d0, d1, d2, d3, eps);
-    if (zin && yin) {
-        int64_t l0 = (int64_t)zm.x + zp.x + ym.x + yp.x + left + c.y - 6ll * c.x;
-        int64_t l1 = (int64_t)zm.y + zp.y + ym.y + yp.y + c.x + c.z - 6ll * c.y;
-        int64_t l2 = (int64_t)zm.z + zp.z + ym.z + yp.z + c.y + c.w - 6ll * c.z;
-        int64_t l3 = (int64_t)zm.w + zp.w + ym.w + yp.w + c.z + right - 6ll * c.w;
-        if (xi == 0) l0 = 0;
-        if (xi + 3 >= n2 - 1) l3 = 0;
-        lp = sc4(l0, l1, l2, l3, two_eps);
-    }
-    __stcs(reinterpret_cast<float4*>(o0 + o), dz);
-    __stcs(reinterpret_cast<float4*>(o1 + o), dy);
-    __stcs(reinterpret_cast<float4*>(o2 + o), dx);
-    __stcs(reinterpret_cast<float4*>(o3 + o), lp);
-}
-
-// Fast fp32 emitter (the pipeline default): integer stencils in int32 and one fp32 multiply by the
-// fp32-rounded scale.  |result - fl64(D*eps)| <= 2^-23 relative (well inside the 1e-6 target), and
-// no XU-pipe conversions: |D| < 2^22 converts with the 1.5*2^23 magic-number trick (one IADD + one
-// FADD).  Any |q| >= 2^27 in the neighbourhood (int32 Laplacian could overflow) takes the exact path.
-__device__ __forceinline__ float i2f_fast(int32_t d) {
-    if (d > -(1 << 22) && d < (1 << 22)) return __int_as_float(0x4B400000 + d) - 12582912.0f;
-    return __int2float_rn(d);
-}
-__device__ __forceinline__ float4 sc4f(int32_t a, int32_t b, int32_t c, int32_t d, float s) {
-    return make_float4(i2f_fast(a) * s, i2f_fast(b) * s, i2f_fast(c) * s, i2f_fast(d) * s);
-}
-__device__ __forceinline__ uint32_t bigmag(int4 v) {   // nonzero if any |v| >= 2^27
-    const uint32_t m = 0xF8000000u;
-    return ((uint32_t)(v.x ^ (v.x >> 31)) | (uint32_t)(v.y ^ (v.y >> 31)) | (uint32_t)(v.z ^ (v.z >> 31)) |
-            (uint32_t)(v.w ^ (v.w >> 31))) & m;
-}
-
-__device__ __forceinline__ void emit4f(float* o0, float* o1, float* o2, float* o3, int64_t o, bool zin, bool yin,
-                                       int64_t xi, int64_t n2, int4 zm, int4 c, int4 zp, int4 ym, int4 yp,
-                                       int32_t left, int32_t right, double eps, double two_eps, float epsf,
-                                       float two_epsf) {
-    const uint32_t big = bigmag(zm) | bigmag(c) | bigmag(zp) | bigmag(ym) | bigmag(yp) |
-                         (((uint32_t)(left ^ (left >> 31)) | (uint32_t)(right ^ (right >> 31))) & 0xF8000000u);
-    if (big) {
-        emit4(o0, o1, o2, o3, o, zin, yin, xi, n2, zm, c, zp, ym, yp, left, right, eps, two_eps);
-        return;
-    }
-    const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
-    float4 dz = zero, dy = zero, lp = zero;
-    if (zin) dz = sc4f(zp.x - zm.x, zp.y - zm.y, zp.z - zm.z, zp.w - zm.w, epsf);
-    if (yin) dy = sc4f(yp.x - ym.x, yp.y - ym.y, yp.z - ym.z, yp.w - ym.w, epsf);
-    int32_t d0 = c.y - left, d1 = c.z - c.x, d2 = c.w - c.y, d3 = right - c.z;
-    if (xi == 0) d0 = 0;
-    if (xi + 3 >= n2 - 1) d3 = 0;
-    const float4 dx = sc4f(d0, d1, d2, d3, epsf);
-    if (zin && yin) {
-        int32_t l0 = zm.x + zp.x + ym.x + yp.x + left + c.y - 6 * c.x;
-        int32_t l1 = zm.y + zp.y + ym.y + yp.y + c.x + c.z - 6 * c.y;
-        int32_t l2 = zm.z + zp.z + ym.z + yp.z + c.y + c.w - 6 * c.z;
-        int32_t l3 = zm.w + zp.w + ym.w + yp.w + c.z + right - 6 * c.w;
-        if (xi == 0) l0 = 0;
-        if (xi + 3 >= n2 - 1) l3 = 0;
-        lp = sc4f(l0, l1, l2, l3, two_epsf);
-    }
-    __stcs(reinterpret_cast<float4*>(o0 + o), dz);
-    __stcs(reinterpret_cast<float4*>(o1 + o), dy);
-    __stcs(reinterpret_cast<float4*>(o2 + o), dx);
-    __stcs(reinterpret_cast<float4*>(o3 + o), lp);
-}
 
 constexpr int ZG_THREADS = 128;   // 512 x-points per CTA
 
@@ -408,10 +274,6 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_tile_rowscan(SegGeo sg, const u
 // arithmetic wraps; every prefix is a q sum mod 2^32 (recon.cu header).
 constexpr int BS_MAXG = 4;   // int4 column groups per thread: n2 <= 4 * 4 * TILE_CHUNKS = 4096
 
-__device__ __forceinline__ int4 add4u(int4 a, uint32_t o) {
-    return make_int4((int)((uint32_t)a.x + o), (int)((uint32_t)a.y + o), (int)((uint32_t)a.z + o),
-                     (int)((uint32_t)a.w + o));
-}
 
 __global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __restrict__ payload, uint64_t len,
                                                           const uint64_t* __restrict__ offsets, int64_t n_chunks,

@@ -33,6 +33,8 @@ import numpy as np
 from . import _lib
 
 _SMS = 148          # B200 SM count (grid sizing only)
+FUSED_LAYERS = 16   # block layers (8 planes each) per CTA of the one-pass kernels
+FAST_QLIM = 1 << 27  # fast fp32 emitter validity bound on |q| (stencil.cuh)
 
 HSZP_ND, HSZX_ND = 1, 3
 SUMS_BYTES = 64
@@ -381,10 +383,27 @@ class WindowPipeline:
                 self._replay(outs)
             else:
                 self._fused_loop(outs)
-            if not stats:
-                return None
-            return self._finish_stats(_prepared)
+            res = self._finish_stats(_prepared)
+            if not self.exact_fp32 and not self._fast_valid(res, _prepared):
+                # the fast emitter needs |q| < 2^27 (FAST_QLIM, stencil.cuh): every q is some point's
+                # centre, so the exact min / max decide it; redo the pass with the exact emitter
+                self.exact_fp32 = True
+                try:
+                    self._fused_loop(outs)
+                    res = self._finish_stats(_prepared)
+                finally:
+                    self.exact_fp32 = False
+            return res if stats else None
         return self._run_generic(outs, stats, _prepared)
+
+    def _fast_valid(self, res, _prepared) -> bool:
+        lim = FAST_QLIM
+        ok = -lim < res["vmin"] and res["vmax"] < lim
+        if _prepared:       # local stats only: the neighbours' halo planes are checked here
+            for h in (self.halo_lo, self.halo_hi):
+                if h is not None and int(h.abs().max()) >= lim:
+                    ok = False
+        return ok
 
     use_graph = False
     # fp32 outputs of the fused loop: True = fl32 of the reference float64 (bit-exact vs the oracle);
@@ -400,7 +419,7 @@ class WindowPipeline:
             return
         n1, n2 = self.sf.global_dims[1], self.sf.global_dims[2]
         dev = _lib.device()
-        nslots = 2 if self.sf.kind == HSZP_ND else 3
+        nslots = 2 if self.sf.kind == HSZP_ND else (0 if self._one_pass_ok() else 3)
         self.ring = [t.empty((self.W, n1, n2), dtype=t.int32, device=dev) for _ in range(nslots)]
         self.halo_buf = t.zeros((2, n1, n2), dtype=t.int32, device=dev)       # [lower, upper]
         self.carry_buf = t.zeros((3, n1, n2), dtype=t.int32, device=dev)      # [rank carry, ping, pong]
@@ -453,8 +472,36 @@ class WindowPipeline:
         _lib.call("hszg_acc_reset", _lib.ptr(self.acc), _lib.stream_handle())
         if self.sf.kind == HSZP_ND:
             self._run_zsweep(outs)
+        elif self._one_pass_ok():
+            self._run_fused_blocks(outs)
         else:
             self._run_blocks(outs)
+
+    one_pass = True             # HSZX_ND: one-pass decode + analytics kernel when eligible (fused.cu)
+    fused_layers = FUSED_LAYERS
+
+    def _one_pass_ok(self) -> bool:
+        sf, ds = self.sf, self.ds
+        n = sf.global_dims
+        return (self.one_pass and sf.kind == HSZX_ND and tuple(sf.block_dims) == (8, 8, 8)
+                and sf.nz % 8 == 0 and n[1] % 8 == 0 and n[2] % 8 == 0 and ds.desc.max_bitwidth <= 16)
+
+    def _run_fused_blocks(self, outs):
+        """HSZX_ND in one launch over the whole slab: decode + gradient + Laplacian + stats, q never
+        stored (fused.cu).  z segments of FUSED_LAYERS block layers per CTA column."""
+        sf = self.sf
+        nlay = sf.nz // 8
+        if self.timer:
+            self.timer.begin("fused")
+        err = _lib.Err()
+        outs_arr = (ctypes.c_void_p * 4)(*[_lib.ptr(o) for o in outs])
+        _lib.call("hszg_fused_blocks", ctypes.byref(self.ds.geom), ctypes.byref(self.ds.desc), sf.z0,
+                  sf.global_dims[0], _lib.ptr(self.halo_buf[0]) if self.halo_lo is not None else None,
+                  _lib.ptr(self.halo_buf[1]) if self.halo_hi is not None else None, outs_arr, _lib.ptr(self.acc),
+                  max(1, min(nlay, self.fused_layers)), int(self.exact_fp32), _lib.stream_handle(), ctypes.byref(err),
+                  err=err)
+        if self.timer:
+            self.timer.end("fused", self._range_bytes(0, sf.nz) + 16 * sf.nz * self.plane)
 
     def _outs_arr(self, outs, a, b):
         return (ctypes.c_void_p * 4)(*[_lib.ptr(o[a:b]) for o in outs])

@@ -8,7 +8,8 @@
   slab totals), reproduces the same outputs.
 
 Shapes: (64, 40, 36) has rows that are not whole chunks (general window loop for HSZP_ND);
-(48, 23, 64) and (40, 17, 128) take the fused decode+row-prefix / z-sweep kernels.
+(48, 23, 64) and (40, 17, 128) take the band-scan / z-sweep kernels; (48, 24, 64) and (48, 40, 136)
+(8^3 blocks dividing the box: partial x and y strips) also take the one-pass HSZX_ND kernel.
 """
 
 import numpy as np
@@ -18,7 +19,7 @@ from oracle import hsz_oracle as O
 
 pytestmark = pytest.mark.gpu
 
-ALL_DIMS = [(64, 40, 36), (48, 23, 64), (40, 17, 128)]
+ALL_DIMS = [(64, 40, 36), (48, 23, 64), (40, 17, 128), (48, 24, 64), (48, 40, 136)]
 
 # fast mode: fl32(fl32(D) * fl32(eps)) vs fl32(D * eps): at most 4 roundings of 2^-24 apart (< 1e-6 target)
 FAST_RTOL = 4 * 2.0**-24
@@ -98,6 +99,8 @@ def test_window_pipeline_single_rank(setup, kind, window, exact):
     pipe.exact_fp32 = exact
     if kind == 1 and window == 16:
         pipe.band_rows_req = 5          # several bands, partial tiles and a short last band
+    if kind == 3 and window == 16:
+        pipe.fused_layers = 2           # several z segments of the one-pass kernel
     outs = [torch.empty(dims, dtype=torch.float32, device="cuda") for _ in range(4)]
     res = pipe.run(outs)
     want, s1, s2, mean, var = _oracle_outputs(field, kind, eps)
@@ -193,3 +196,27 @@ def test_fast_decode_bitwidths_band_scan(dims, band_rows):
     for k, (got, w) in enumerate(zip(outs, want)):
         assert np.array_equal(got.cpu().numpy(), w), k
     assert res["s1"] == s1 and res["s2"] == s2
+
+
+@pytest.mark.parametrize("kind", [1, 3])
+def test_fast_mode_falls_back_on_large_q(kind):
+    """|q| >= 2^27 breaks the fast emitter's int32 Laplacian: the pipeline must detect it from the exact
+    min / max and redo the pass exactly (outputs then bit-identical to the oracle)."""
+    import torch
+
+    from paper_2603_25206_b200 import pipeline
+
+    dims = (48, 24, 64)
+    rng = np.random.default_rng(9)
+    f = O.random_field(rng, dims, "smooth")
+    eps = 2e-9 * float(np.abs(f).max())            # |q| up to ~2.5e8 > 2^27
+    fd = torch.from_numpy(f).cuda()
+    sf = pipeline.compress_shard(fd, kind, eps, (8, 8, 8), 0, dims[0], dims)
+    pipe = pipeline.WindowPipeline(sf, pipeline.Comm(), 16)
+    outs = [torch.empty(dims, dtype=torch.float32, device="cuda") for _ in range(4)]
+    res = pipe.run(outs)
+    want, s1, s2, mean, var = _oracle_outputs(f, kind, eps)
+    assert max(-res["vmin"], res["vmax"]) >= pipeline.FAST_QLIM
+    for k, (got, w) in enumerate(zip(outs, want)):
+        assert np.array_equal(got.cpu().numpy(), w), k
+    assert res["s1"] == s1 and res["s2"] == s2 and not pipe.exact_fp32
