@@ -1,30 +1,69 @@
 // fused.cu — one-pass decode + analytics for the config-5 hot loop: the quantization indices q
-// never reach HBM.  Each CTA owns an (x, y) column of the slab and slides along z, decoding the
-// chunks it needs per plane from shared-memory-staged payload bytes into a 4-plane ring of q,
-// then emits gradient (dz, dy, dx) + Laplacian (fields.py:34-80, via stencil.cuh) and the exact
-// statistics of its planes.  HBM traffic per value: the compressed bytes + the 16 output bytes.
+// never reach HBM.  Each CTA owns an (x, y) column of a z-slab and slides along z; the payload
+// bytes it needs arrive in shared memory by TMA bulk copies one block layer ahead, producer warps
+// decode them plane by plane into a ring of q planes, and consumer warps emit gradient (dz, dy, dx)
+// + Laplacian (fields.py:34-80, via stencil.cuh) and the exact statistics of their planes.
+// HBM traffic per value: the compressed bytes + the 16 output bytes.
 //
 // HSZX_ND (8x8x8 blocks, compressors.py:170-199 / 214-218): q = p + M_b.  The CTA covers 16
-// blocks along x (128 values) and 2 block rows (16 y); per block layer it stages the byte ranges
-// of 4 block rows (top halo, 2 main, bottom halo), each extended by one block on both x sides,
-// and decodes, per plane, the two chunks of every block that hold that plane (block-local order
-// z, y, x: chunk 2*zl + h = rows 4h..4h+3 of plane zl) — halo rows only the half they need.
+// blocks along x (128 values) and 2 block rows (16 y).  Per block layer it stages 4 block rows
+// (top halo, 2 main, bottom halo), each extended by one block on both x sides: the payload range,
+// the chunk offsets and the block means of each (contiguous in the block-row-major stream).  A
+// decode job is one 8-value row of one block in one plane (a quarter chunk: block-local order z,
+// y, x, so chunk 2*zl + h holds rows 4h..4h+3 of plane zl); halo block rows decode only the row
+// next to the CTA.
+//
+// Pipeline: warps 0-7 produce, 8-15 consume.  full[s] / empty[s] mbarriers hand ring slot s
+// (plane z in slot z % NPL) between them; stage[b] mbarriers carry the TMA transaction bytes of
+// staging buffer b (layer L in buffer L & 1).
 #include <cstdio>
 #include "tile.cuh"
 #include "stencil.cuh"
 
 namespace hszg {
 
-constexpr int FX_T = 256;                  // threads (8 warps)
+constexpr int FX_T = 512;                  // threads
+constexpr int FX_PT = 256;                 // producers: warps 0-7
+constexpr int FX_CT = FX_T - FX_PT;        // consumers: warps 8-15
 constexpr int FX_BX = 16;                  // blocks along x per CTA
 constexpr int FX_BY = 2;                   // block rows per CTA
-constexpr int FX_ROWS = FX_BY * 8 + 2;     // smem rows: y0-1 .. y0+16
-constexpr int FX_X0 = 8;                   // smem column of x0 (x0-8 .. x0+135 stored)
-constexpr int FX_RW = 148;                 // words per smem row (144 + pad)
+constexpr int FX_ROWS = FX_BY * 8 + 2;     // ring rows: y0-1 .. y0+16
+constexpr int FX_X0 = 8;                   // ring column of x0 (x0-8 .. x0+135 stored)
+constexpr int FX_RW = 148;                 // words per ring row (144 + pad: odd 16-B stride)
 constexpr int FX_PLANE = FX_ROWS * FX_RW;  // words per ring plane
-constexpr int FX_NPL = 4;                  // ring planes (z-1, z, z+1, loading z+2)
 constexpr int FX_RANGES = FX_BY + 2;       // staged block rows per layer
 constexpr int FX_RBLK = FX_BX + 2;         // blocks per staged block row
+constexpr int FX_OSTR = FX_RBLK * 16;      // staged chunk offsets per range
+constexpr int FX_MSTR = FX_RBLK + 2;       // staged block means per range (16-B multiple of the buffer)
+
+// ---- mbarriers (PTX) ----------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(smem_addr(b)),
+        "r"(parity)
+        : "memory");
+}
+// 1-D TMA: bytes (multiple of 16, 16-B aligned ends) global -> shared, completing on mbarrier b
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(b))
+        : "memory");
+}
+__device__ __forceinline__ void producer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(FX_PT) : "memory"); }
 
 struct FxArgs {
     const uint8_t* payload;
@@ -45,27 +84,26 @@ struct FxArgs {
     HszgAcc* acc;
 };
 
-inline size_t fx_stage_bytes(int max_bw) {
-    return (size_t)FX_RANGES * ((size_t)FX_RBLK * 16 * (size_t)chunk_bytes(kChunkCap, max_bw) + 48);
+// staged bytes of one layer buffer: offsets, means, payload ranges (+1 spare vector each)
+inline size_t fx_payload_bytes(int max_bw) {
+    return (size_t)FX_RANGES * (((size_t)FX_OSTR * (size_t)chunk_bytes(kChunkCap, max_bw) + 15) / 16 * 16 + 32);
 }
-inline size_t fx_smem_bytes(int max_bw) {
-    return (size_t)FX_NPL * FX_PLANE * 4 + (size_t)FX_RANGES * FX_RBLK * (16 * 8 + 4) + fx_stage_bytes(max_bw);
+inline size_t fx_buffer_bytes(int max_bw) {
+    return (size_t)FX_RANGES * (FX_OSTR * 8 + FX_MSTR * 4) + fx_payload_bytes(max_bw);
+}
+inline size_t fx_smem_bytes(int max_bw, int npl) {
+    return (size_t)npl * FX_PLANE * 4 + 2 * fx_buffer_bytes(max_bw);
 }
 
-constexpr int FX_OSTR = FX_RBLK * 16;        // staged chunk offsets per range
-
-template <bool Exact>
-__global__ void __launch_bounds__(FX_T, 2) k_fused_blocks(FxArgs a) {
-    extern __shared__ __align__(16) uint8_t smem[];
+template <bool Exact, int NPL>
+__global__ void __launch_bounds__(FX_T, 1) k_fused_blocks(FxArgs a, uint32_t buf_bytes) {
+    extern __shared__ __align__(128) uint8_t smem[];
     int32_t* Q = reinterpret_cast<int32_t*>(smem);
-    uint64_t* OFFS = reinterpret_cast<uint64_t*>(smem + (size_t)FX_NPL * FX_PLANE * 4);
-    int32_t* MET = reinterpret_cast<int32_t*>(OFFS + FX_RANGES * FX_OSTR);
-    uint4* SB = reinterpret_cast<uint4*>(MET + FX_RANGES * FX_RBLK);
-    const uint32_t* SW = reinterpret_cast<const uint32_t*>(SB);
-    __shared__ uint64_t s_gbase[FX_RANGES];
-    __shared__ int64_t s_clo[FX_RANGES];
-    __shared__ uint32_t s_vbase[FX_RANGES], s_nvec[FX_RANGES];
-    __shared__ int s_ok[FX_RANGES], s_nblk[FX_RANGES];
+    uint8_t* BUF = smem + (size_t)NPL * FX_PLANE * 4;      // 2 layer buffers: [offsets | means | payload]
+    __shared__ __align__(8) uint64_t bar_full[NPL], bar_empty[NPL], bar_stage[2];
+    __shared__ uint64_t s_gbase[2][FX_RANGES];
+    __shared__ uint32_t s_vbase[2][FX_RANGES];
+    __shared__ int s_ok[2][FX_RANGES];
 
     const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
     const int64_t bx0 = (int64_t)blockIdx.x * FX_BX, by0 = (int64_t)blockIdx.y * FX_BY;
@@ -74,144 +112,182 @@ __global__ void __launch_bounds__(FX_T, 2) k_fused_blocks(FxArgs a) {
     const int64_t nlay = a.nz >> 3;
     const int64_t L0 = (int64_t)blockIdx.z * a.zlayers;
     const int64_t L1 = L0 + a.zlayers < nlay ? L0 + a.zlayers : nlay;
-    const int64_t Llast = L1 < nlay ? L1 : nlay - 1;          // last layer read (z halo included)
-    const int64_t plane = a.n1 * a.n2;
-    const float epsf = __double2float_rn(a.eps), two_epsf = 2.0f * epsf;
-    const double two_eps = 2.0 * a.eps;
-    const int64_t fbx = bx0 > 0 ? bx0 - 1 : 0;                 // first staged block column
+    const int64_t zb = L0 * 8, ze = L1 * 8;                  // planes emitted
+    const int64_t Lb = zb > 0 ? L0 - 1 : L0;                  // first / last layer read (z halos)
+    const int64_t Llast = L1 < nlay ? L1 : nlay - 1;
+    const int64_t fbx = bx0 > 0 ? bx0 - 1 : 0;                // staged block columns [fbx, lbx]
     const int64_t lbx = bx0 + FX_BX < a.G2 ? bx0 + FX_BX : a.G2 - 1;
+    const int nblk = (int)(lbx - fbx + 1);
 
-    for (int i = threadIdx.x; i < FX_NPL * FX_PLANE / 4; i += FX_T)
-        reinterpret_cast<int4*>(Q)[i] = make_int4(0, 0, 0, 0);
+    for (int i = threadIdx.x; i < NPL * FX_PLANE / 4; i += FX_T) reinterpret_cast<int4*>(Q)[i] = make_int4(0, 0, 0, 0);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NPL; i++) {
+            mbar_init(&bar_full[i], FX_PT);
+            mbar_init(&bar_empty[i], FX_CT);
+        }
+        mbar_init(&bar_stage[0], 1);
+        mbar_init(&bar_stage[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     __syncthreads();
 
-    // byte-range descriptor of block row r = threadIdx.x of a layer, loaded one layer ahead by
-    // threads 0..3 so the offsets' latency is off the staging path
-    int64_t d_L = -1, d_clo = 0;
-    uint64_t d_lo = 0, d_hi = 0;
-    int d_ok = 0;
-    auto describe = [&](int64_t L) {
-        const int64_t by = by0 - 1 + threadIdx.x;
-        d_L = L;
-        d_ok = by >= 0 && by < a.G1 && (int)threadIdx.x <= nby + 1;
-        if (!d_ok) return;
-        d_clo = ((L * a.G1 + by) * a.G2 + fbx) * 16;
-        const int64_t c_hi = ((L * a.G1 + by) * a.G2 + lbx + 1) * 16;
-        d_lo = __ldg(a.offsets + d_clo);
-        d_hi = c_hi < a.n_chunks ? __ldg(a.offsets + c_hi) : payload_end(a.offsets, a.n_chunks, a.len);
-    };
-    int64_t staged = -1;
-    auto stage = [&](int64_t L) {
-        if (wp == 0) {
-            uint32_t sz = 0;
-            if (lane < FX_RANGES) {
-                if (d_L != L) describe(L);
-                if (d_ok) sz = (uint32_t)((d_hi - (d_lo & ~(uint64_t)15) + 15) >> 4) + 1;
+    if (wp < FX_PT / 32) {
+        // ================================ producers ================================
+        // descriptor of block row r = lane (< FX_RANGES) of a layer, loaded one layer ahead by warp 0
+        int d_ok = 0;
+        int64_t d_clo = 0;
+        uint64_t d_lo = 0, d_hi = 0;
+        int32_t d_m[3] = {0, 0, 0};          // block means: range lane >> 3, blocks (lane & 7) + 8k
+        auto describe = [&](int64_t L) {
+            const int64_t by = by0 - 1 + lane;
+            const int mr = lane >> 3;
+            const int64_t mby = by0 - 1 + mr;
+            if (mr < FX_RANGES && mby >= 0 && mby < a.G1 && mr <= nby + 1) {
+#pragma unroll
+                for (int k = 0; k < 3; k++) {
+                    const int idx = (lane & 7) + 8 * k;
+                    if (idx < nblk) d_m[k] = __ldg(a.meta + (L * a.G1 + mby) * a.G2 + fbx + idx);
+                }
             }
-            uint32_t inc = sz;
+            d_ok = lane < FX_RANGES && by >= 0 && by < a.G1 && lane <= nby + 1;
+            if (!d_ok) return;
+            d_clo = ((L * a.G1 + by) * a.G2 + fbx) * 16;
+            const int64_t c_hi = d_clo + (int64_t)nblk * 16;
+            d_lo = __ldg(a.offsets + d_clo);
+            d_hi = c_hi < a.n_chunks ? __ldg(a.offsets + c_hi) : payload_end(a.offsets, a.n_chunks, a.len);
+        };
+        // warp 0: TMA the layer described by d_* into buffer b
+        auto issue = [&](int b) {
+            uint8_t* buf = BUF + (size_t)b * buf_bytes;
+            uint64_t* offs = reinterpret_cast<uint64_t*>(buf);
+            int32_t* means = reinterpret_cast<int32_t*>(offs + FX_RANGES * FX_OSTR);
+            uint4* pay = reinterpret_cast<uint4*>(means + FX_RANGES * FX_MSTR);
+            const uint64_t base = d_lo & ~(uint64_t)15;
+            const uint32_t nvec = d_ok ? (uint32_t)((d_hi - base + 15) >> 4) : 0;
+            uint32_t inc = d_ok ? nvec + 1 : 0;
 #pragma unroll
             for (int d = 1; d < FX_RANGES; d <<= 1) {
                 const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
                 if (lane >= d) inc += o;
             }
-            if (lane < FX_RANGES) {
-                s_ok[lane] = d_ok;
-                s_gbase[lane] = d_lo & ~(uint64_t)15;
-                s_vbase[lane] = inc - sz;
-                s_nvec[lane] = sz ? sz - 1 : 0;
-                s_clo[lane] = d_clo;
-                s_nblk[lane] = (int)(lbx - fbx + 1);
-            }
-        }
-        __syncthreads();
+            const uint32_t vbase = inc - (d_ok ? nvec + 1 : 0);
+            const uint32_t obytes = (uint32_t)nblk * 16 * 8;
+            uint32_t tx = d_ok ? nvec * 16 + obytes : 0;
 #pragma unroll
-        for (int r = 0; r < FX_RANGES; r++) {
-            if (!s_ok[r]) continue;
-            const uint4* g = reinterpret_cast<const uint4*>(a.payload + s_gbase[r]);
-            uint4* d = SB + s_vbase[r];
-            const uint32_t nv = s_nvec[r];
-            for (uint32_t i = threadIdx.x; i < nv; i += FX_T) d[i] = __ldg(g + i);
-            if (threadIdx.x == 0) d[nv] = make_uint4(0, 0, 0, 0);
-            const int nc = s_nblk[r] * 16;
-            const uint64_t* go = a.offsets + s_clo[r];
-            for (int i = threadIdx.x; i < nc; i += FX_T) OFFS[r * FX_OSTR + i] = __ldg(go + i);
-            if ((int)threadIdx.x < s_nblk[r]) MET[r * FX_RBLK + threadIdx.x] = __ldg(a.meta + s_clo[r] / 16 + threadIdx.x);
-        }
-        if (wp == 0 && lane < FX_RANGES && L + 1 <= Llast) describe(L + 1);
-    };
-
-    // fill ring slot (z & 3) with q of slab plane z, z in [-1, nz]
-    auto load_plane = [&](int64_t z) {
-        int32_t* P = Q + (int)(z & (FX_NPL - 1)) * FX_PLANE;
-        if (z < 0 || z >= a.nz) {
-            const int32_t* h = z < 0 ? a.halo_lo : a.halo_hi;
-            for (int i = threadIdx.x; i < FX_ROWS * (FX_RW / 4); i += FX_T) {
-                const int row = i / (FX_RW / 4), c4 = i - row * (FX_RW / 4);
-                const int64_t y = y0 - 1 + row, x = x0 - FX_X0 + 4 * c4;
-                int4 v = make_int4(0, 0, 0, 0);
-                if (h && c4 < 36 && y >= 0 && y < a.n1 && x >= 0 && x < a.n2) v = ld4(h + y * a.n2 + x);
-                *reinterpret_cast<int4*>(P + row * FX_RW + 4 * c4) = v;
+            for (int d = 16; d > 0; d >>= 1) tx += __shfl_xor_sync(0xffffffffu, tx, d);
+            if (lane < FX_RANGES) {
+                s_ok[b][lane] = d_ok;
+                s_gbase[b][lane] = base;
+                s_vbase[b][lane] = vbase;
             }
-            return;
+#pragma unroll
+            for (int k = 0; k < 3; k++) {                   // means: plain stores (read after producer_sync)
+                const int idx = (lane & 7) + 8 * k;
+                if ((lane >> 3) < FX_RANGES && idx < nblk) means[(lane >> 3) * FX_MSTR + idx] = d_m[k];
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (lane == 0) mbar_arrive_tx(&bar_stage[b], tx);
+            __syncwarp();
+            if (d_ok) {
+                tma_load_1d(pay + vbase, a.payload + base, nvec * 16, &bar_stage[b]);
+                tma_load_1d(offs + lane * FX_OSTR, a.offsets + d_clo, obytes, &bar_stage[b]);
+            }
+        };
+
+        if (wp == 0) {
+            describe(Lb);
+            issue((int)(Lb & 1));
+            if (Lb + 1 <= Llast) describe(Lb + 1);
         }
-        const int64_t L = z >> 3;
-        const int zl = (int)(z & 7);
-        if (L != staged) {
-            __syncthreads();                       // previous layer's bytes fully consumed
-            stage(L);
-            staged = L;
-            __syncthreads();
-        }
-        // one job = one 8-value row of one block in this plane (a quarter chunk): main block rows
-        // all 8 rows, halo block rows only the row adjacent to the CTA
-        const int nmain = FX_RBLK * 8 * nby;
-        const int njobs = nmain + 2 * FX_RBLK;
-        for (int i = threadIdx.x; i < njobs; i += FX_T) {
-            int r, blk, yl;
-            if (i < nmain) {
-                r = 1 + i / (8 * FX_RBLK);
-                const int rem = i - (r - 1) * 8 * FX_RBLK;
-                blk = rem >> 3;
-                yl = rem & 7;
+        int64_t cur = -1;
+        for (int64_t z = zb - 1; z <= ze; z++) {
+            const int s = (int)(z & (NPL - 1));
+            const int64_t use = (z - (zb - 1)) / NPL;
+            if (use > 0) mbar_wait(&bar_empty[s], (uint32_t)((use - 1) & 1));
+            int32_t* P = Q + s * FX_PLANE;
+            if (z < 0 || z >= a.nz) {
+                const int32_t* h = z < 0 ? a.halo_lo : a.halo_hi;
+                for (int i = threadIdx.x; i < FX_ROWS * (FX_RW / 4); i += FX_PT) {
+                    const int row = i / (FX_RW / 4), c4 = i - row * (FX_RW / 4);
+                    const int64_t y = y0 - 1 + row, x = x0 - FX_X0 + 4 * c4;
+                    int4 v = make_int4(0, 0, 0, 0);
+                    if (h && c4 < 36 && y >= 0 && y < a.n1 && x >= 0 && x < a.n2) v = ld4(h + y * a.n2 + x);
+                    *reinterpret_cast<int4*>(P + row * FX_RW + 4 * c4) = v;
+                }
             } else {
-                const int j = i - nmain;
-                const int side = j >= FX_RBLK;
-                blk = j - side * FX_RBLK;
-                r = side ? nby + 1 : 0;
-                yl = side ? 0 : 7;
+                const int64_t L = z >> 3;
+                const int b = (int)(L & 1);
+                if (L != cur) {
+                    mbar_wait(&bar_stage[b], (uint32_t)(((L - Lb) >> 1) & 1));
+                    producer_sync();                 // everyone is past layer L-1: its buffer is free
+                    if (wp == 0 && L + 1 <= Llast) {
+                        issue((int)((L + 1) & 1));
+                        if (L + 2 <= Llast) describe(L + 2);
+                    }
+                    cur = L;
+                }
+                const uint8_t* buf = BUF + (size_t)b * buf_bytes;
+                const uint64_t* offs = reinterpret_cast<const uint64_t*>(buf);
+                const int32_t* means = reinterpret_cast<const int32_t*>(offs + FX_RANGES * FX_OSTR);
+                const uint32_t* pw = reinterpret_cast<const uint32_t*>(means + FX_RANGES * FX_MSTR);
+                const int zl = (int)(z & 7);
+                const int nmain = FX_RBLK * 8 * nby;
+                const int njobs = nmain + 2 * FX_RBLK;
+                for (int i = threadIdx.x; i < njobs; i += FX_PT) {
+                    int r, blk, yl;
+                    if (i < nmain) {
+                        r = 1 + i / (8 * FX_RBLK);
+                        const int rem = i - (r - 1) * 8 * FX_RBLK;
+                        blk = rem >> 3;
+                        yl = rem & 7;
+                    } else {
+                        const int j = i - nmain;
+                        const int side = j >= FX_RBLK;
+                        blk = j - side * FX_RBLK;
+                        r = side ? nby + 1 : 0;
+                        yl = side ? 0 : 7;
+                    }
+                    const int64_t bx = bx0 - 1 + blk;
+                    if (bx < 0 || bx >= a.G2 || !s_ok[b][r]) continue;
+                    const int rb = (int)(bx - fbx);
+                    const int cl = rb * 16 + zl * 2 + (yl >> 2);
+                    const uint32_t rel = (uint32_t)(offs[r * FX_OSTR + cl] - s_gbase[b][r]) + s_vbase[b][r] * 16;
+                    int4 lo, hi;
+                    decode8(pw, rel, yl & 3, means[r * FX_MSTR + rb], lo, hi);
+                    int32_t* dst = P + (r * 8 + yl - 7) * FX_RW + FX_X0 + (int)(bx * 8 - x0);
+                    *reinterpret_cast<int4*>(dst) = lo;
+                    *reinterpret_cast<int4*>(dst + 4) = hi;
+                }
             }
-            const int64_t bx = bx0 - 1 + blk;
-            if (bx < 0 || bx >= a.G2 || !s_ok[r]) continue;
-            const int rb = (int)(bx - fbx);
-            const int cl = rb * 16 + zl * 2 + (yl >> 2);
-            const uint32_t rel = (uint32_t)(OFFS[r * FX_OSTR + cl] - s_gbase[r]) + s_vbase[r] * 16;
-            int4 lo, hi;
-            decode8(SW, rel, yl & 3, MET[r * FX_RBLK + rb], lo, hi);
-            const int row = r * 8 + yl - 7;        // (by0 - 1 + r) * 8 + yl - (y0 - 1)
-            int32_t* dst = P + row * FX_RW + FX_X0 + (int)(bx * 8 - x0);
-            *reinterpret_cast<int4*>(dst) = lo;
-            *reinterpret_cast<int4*>(dst + 4) = hi;
+            mbar_arrive(&bar_full[s]);
         }
-    };
+        return;
+    }
 
+    // ================================ consumers ================================
+    const int cw = wp - FX_PT / 32;                               // rows 2cw, 2cw+1
+    const int64_t plane = a.n1 * a.n2;
+    const float epsf = __double2float_rn(a.eps), two_epsf = 2.0f * epsf;
+    const double two_eps = 2.0 * a.eps;
     WinStats st;
     st.init();
     int64_t count = 0;
-    const int64_t zb = L0 * 8, ze = L1 * 8;
-    load_plane(zb - 1);
-    load_plane(zb);
     const int64_t x = x0 + 4 * lane;
+    auto wait_full = [&](int64_t z) {
+        mbar_wait(&bar_full[(int)(z & (NPL - 1))], (uint32_t)(((z - (zb - 1)) / NPL) & 1));
+    };
+    wait_full(zb - 1);
+    wait_full(zb);
     for (int64_t z = zb; z < ze; z++) {
-        load_plane(z + 1);
-        __syncthreads();
-        const int32_t* Pm = Q + (int)((z - 1) & (FX_NPL - 1)) * FX_PLANE;
-        const int32_t* Pc = Q + (int)(z & (FX_NPL - 1)) * FX_PLANE;
-        const int32_t* Pp = Q + (int)((z + 1) & (FX_NPL - 1)) * FX_PLANE;
+        wait_full(z + 1);
+        const int32_t* Pm = Q + (int)((z - 1) & (NPL - 1)) * FX_PLANE;
+        const int32_t* Pc = Q + (int)(z & (NPL - 1)) * FX_PLANE;
+        const int32_t* Pp = Q + (int)((z + 1) & (NPL - 1)) * FX_PLANE;
         const int64_t gz = a.gz0 + z;
         const bool zin = gz > 0 && gz < a.gN0 - 1;
 #pragma unroll
         for (int k = 0; k < 2; k++) {
-            const int r = wp + 8 * k;                      // output row within the CTA
+            const int r = 2 * cw + k;                             // output row within the CTA
             const int64_t y = y0 + r;
             const int so = (r + 1) * FX_RW + FX_X0 + 4 * lane;
             const int4 c = *reinterpret_cast<const int4*>(Pc + so);
@@ -236,6 +312,7 @@ __global__ void __launch_bounds__(FX_T, 2) k_fused_blocks(FxArgs a) {
                 count += 4;
             }
         }
+        mbar_arrive(&bar_empty[(int)((z - 1) & (NPL - 1))]);      // plane z-1 retired
     }
     if (a.acc) st.flush(a.acc, count);
 }
@@ -248,20 +325,30 @@ int hszg_set_cuda_error(HszgErr* err, cudaError_t e, const char* where);
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 static bool al16f(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+template <bool Exact, int NPL>
+static void launch_fused_blocks(const FxArgs& a, dim3 grid, size_t smem, uint32_t buf_bytes, cudaStream_t st) {
+    allow_smem(k_fused_blocks<Exact, NPL>, smem);
+    k_fused_blocks<Exact, NPL><<<grid, FX_T, smem, st>>>(a, buf_bytes);
+}
+
+static constexpr size_t kSmemLimit = 227 * 1024 - 2048;   // dynamic part (static barriers etc. aside)
+
 extern "C" int hszg_fused_blocks(const HszgGeom* g, const HszgStream* s, int64_t gz0, int64_t gN0,
                                  const int32_t* halo_lo, const int32_t* halo_hi, float* const* out, HszgAcc* acc,
                                  int64_t zlayers, int exact, void* stream, HszgErr* err) {
     err->status = HSZG_OK;
     const int64_t nz = g->dims[0], n1 = g->dims[1], n2 = g->dims[2];
-    const size_t smem = fx_smem_bytes(s->max_bitwidth);
+    const int npl = fx_smem_bytes(s->max_bitwidth, 8) <= kSmemLimit ? 8 : 4;
+    const size_t smem = fx_smem_bytes(s->max_bitwidth, npl);
     if (g->kind != HSZG_HSZX_ND || g->ndims != 3 || g->block_dims[0] != 8 || g->block_dims[1] != 8 ||
         g->block_dims[2] != 8 || nz % 8 || n1 % 8 || n2 % 8 || !s->canonical || !s->metadata || zlayers < 1 ||
-        smem > 200 * 1024 || !al16f(out[0]) || !al16f(out[1]) || !al16f(out[2]) || !al16f(out[3]) ||
-        (halo_lo && !al16f(halo_lo)) || (halo_hi && !al16f(halo_hi))) {
+        smem > kSmemLimit || !al16f(out[0]) || !al16f(out[1]) || !al16f(out[2]) || !al16f(out[3]) ||
+        (halo_lo && !al16f(halo_lo)) || (halo_hi && !al16f(halo_hi)) || !al16f(s->offsets) ||
+        !al16f(s->metadata) || !al16f(s->payload)) {
         err->status = HSZG_INVALID_ARG;
         snprintf(err->message, sizeof(err->message),
-                 "fused_blocks needs a canonical 3-D HSZX_ND stream with 8x8x8 blocks dividing the box and "
-                 "max bit width <= 16 (got %d)", s->max_bitwidth);
+                 "fused_blocks needs a canonical 3-D HSZX_ND stream with 8x8x8 blocks dividing the box, 16-B "
+                 "aligned buffers and staging that fits shared memory (max bit width %d)", s->max_bitwidth);
         return HSZG_INVALID_ARG;
     }
     if (g->n == 0) return HSZG_OK;
@@ -290,12 +377,14 @@ extern "C" int hszg_fused_blocks(const HszgGeom* g, const HszgStream* s, int64_t
     const int64_t nlay = nz / 8;
     dim3 grid((unsigned)((a.G2 + FX_BX - 1) / FX_BX), (unsigned)((a.G1 + FX_BY - 1) / FX_BY),
               (unsigned)((nlay + zlayers - 1) / zlayers));
+    const uint32_t bb = (uint32_t)fx_buffer_bytes(s->max_bitwidth);
+    cudaStream_t st = as_stream(stream);
     if (exact) {
-        allow_smem(k_fused_blocks<true>, smem);
-        k_fused_blocks<true><<<grid, FX_T, smem, as_stream(stream)>>>(a);
+        if (npl == 8) launch_fused_blocks<true, 8>(a, grid, smem, bb, st);
+        else launch_fused_blocks<true, 4>(a, grid, smem, bb, st);
     } else {
-        allow_smem(k_fused_blocks<false>, smem);
-        k_fused_blocks<false><<<grid, FX_T, smem, as_stream(stream)>>>(a);
+        if (npl == 8) launch_fused_blocks<false, 8>(a, grid, smem, bb, st);
+        else launch_fused_blocks<false, 4>(a, grid, smem, bb, st);
     }
     if (cudaGetLastError() != cudaSuccess) return hszg_set_cuda_error(err, cudaGetLastError(), "fused_blocks");
     return HSZG_OK;
