@@ -15,6 +15,7 @@
 #include "tile.cuh"
 #include "lookback.cuh"
 #include "stencil.cuh"
+#include "async.cuh"
 
 namespace hszg {
 
@@ -163,10 +164,11 @@ __global__ void __launch_bounds__(ZG_THREADS) k_zsweep(const int32_t* __restrict
         if (lane == 31 && xi + 4 < n2) r_ = __ldg(p + 4);
         if (A) {
             const int32_t* a = zz < nout ? A + zz * aplane : lookA;
-            c_ = add4(c_, ld4(a + ac));
-            if (yin) {
-                m_ = add4(m_, ld4(a + am));
-                p_ = add4(p_, ld4(a + ap));
+            const int4 av = ld4(a + ac);
+            c_ = add4(c_, av);
+            if (yin) {                              // rows y+-1 share y's band except at band edges
+                m_ = add4(m_, am == ac ? av : ld4(a + am));
+                p_ = add4(p_, ap == ac ? av : ld4(a + ap));
             }
             if (lane == 0 && xi > 0) l_ += __ldg(a + ac - 1);
             if (lane == 31 && xi + 4 < n2) r_ += __ldg(a + ac + 4);
@@ -278,40 +280,70 @@ constexpr int BS_MAXG = 4;   // int4 column groups per thread: n2 <= 4 * 4 * TIL
 __global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __restrict__ payload, uint64_t len,
                                                           const uint64_t* __restrict__ offsets, int64_t n_chunks,
                                                           int n1, int n2, int BR, int32_t* __restrict__ L,
-                                                          int32_t* __restrict__ A) {
-    extern __shared__ __align__(16) uint8_t smem[];
+                                                          int32_t* __restrict__ A, uint32_t sbytes) {
+    extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint32_t s_off[TILE_CHUNKS];
     __shared__ uint32_t s_wt[TILE_CHUNKS / 32];
-    __shared__ uint64_t s_lo, s_hi;
+    __shared__ uint64_t s_base[2];
+    __shared__ __align__(8) uint64_t bar[2];
     const int cpr = n2 >> 5;                 // chunks per row (a power of two dividing 256)
     const int rpt = TILE_CHUNKS / cpr;       // rows per tile
     const int b = blockIdx.x, nb = gridDim.x;
     const int64_t z = blockIdx.y;
     const int y0 = b * BR;
     const int y1 = min(y0 + BR, n1);
+    const int ntiles = (y1 - y0 + rpt - 1) / rpt;
     const int ng = n2 >> 2;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int32_t* tile = reinterpret_cast<int32_t*>(smem);
-    uint4* sb = reinterpret_cast<uint4*>(smem + kFastTileBytes);
-    const uint32_t* words = reinterpret_cast<const uint32_t*>(sb);
+    uint8_t* SB = smem + kFastTileBytes;     // two staging buffers of sbytes: tile t in buffer t & 1
+    const uint32_t* words = reinterpret_cast<const uint32_t*>(SB);
+    auto tile_c0 = [&](int t) { return (z * n1 + y0 + t * rpt) * (int64_t)cpr; };
+    auto tile_nch = [&](int t) { return min(rpt, y1 - (y0 + t * rpt)) * cpr; };
+    // thread 0: byte range of a tile (loaded a tile ahead) and its TMA into buffer t & 1
+    uint64_t n_lo = 0, n_hi = 0;
+    auto range = [&](int t) {
+        const int64_t c0 = tile_c0(t), c1 = c0 + tile_nch(t);
+        n_lo = __ldg(offsets + c0);
+        n_hi = c1 < n_chunks ? __ldg(offsets + c1) : payload_end(offsets, n_chunks, len);
+    };
+    auto issue = [&](int t) {
+        const uint64_t base = n_lo & ~(uint64_t)15;
+        const uint32_t bytes = (uint32_t)(((n_hi - base + 15) >> 4) << 4);
+        s_base[t & 1] = base;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_tx(&bar[t & 1], bytes);
+        tma_load_1d(SB + (size_t)(t & 1) * sbytes, payload + base, bytes, &bar[t & 1]);
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        range(0);
+        issue(0);
+        if (ntiles > 1) range(1);
+    }
+    uint64_t my_off = (int)threadIdx.x < tile_nch(0) ? __ldg(offsets + tile_c0(0) + threadIdx.x) : 0;
+    __syncthreads();
     int4 ysum[BS_MAXG];
 #pragma unroll
     for (int k = 0; k < BS_MAXG; k++) ysum[k] = make_int4(0, 0, 0, 0);
-    for (int r0 = y0; r0 < y1; r0 += rpt) {
+    for (int t = 0; t < ntiles; t++) {
+        const int r0 = y0 + t * rpt;
         const int nr = min(rpt, y1 - r0);
         const int nch = nr * cpr;
-        const int64_t c0 = (z * n1 + r0) * (int64_t)cpr;
-        if (threadIdx.x == 0) {
-            s_lo = offsets[c0];
-            s_hi = c0 + nch < n_chunks ? offsets[c0 + nch] : payload_end(offsets, n_chunks, len);
+        mbar_wait(&bar[t & 1], (uint32_t)((t >> 1) & 1));
+        if (threadIdx.x == 0 && t + 1 < ntiles) {        // buffer (t+1)&1 was released at the end of t-1
+            issue(t + 1);
+            if (t + 2 < ntiles) range(t + 2);
         }
-        __syncthreads();
-        const uint64_t base = stage_range(payload, s_lo, s_hi, sb);
-        uint32_t rel = 0;
-        if ((int)threadIdx.x < nch) rel = (uint32_t)(__ldg(offsets + c0 + threadIdx.x) - base);
-        __syncthreads();
+        const uint64_t cur_off = my_off;
+        if (t + 1 < ntiles && (int)threadIdx.x < tile_nch(t + 1)) my_off = __ldg(offsets + tile_c0(t + 1) + threadIdx.x);
         uint32_t tot = 0;
-        if ((int)threadIdx.x < nch) tot = decode32<true>(words, rel, tile + threadIdx.x * kChunkStride, 0);
+        if ((int)threadIdx.x < nch) {
+            const uint32_t rel = (uint32_t)(cur_off - s_base[t & 1]) + (uint32_t)(t & 1) * sbytes;
+            tot = decode32<true>(words, rel, tile + threadIdx.x * kChunkStride, 0);
+        }
         // exclusive prefix of the chunk sums along each row
         uint32_t inc = tot;
         const int wseg = cpr < 32 ? cpr : 32;
@@ -349,18 +381,26 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __rest
     }
 }
 
-// A[z][b][:] band totals -> exclusive prefix over b (one thread per (plane, int4 column group))
-__global__ void k_band_prefix(int32_t* A, int nb, int64_t n2, int64_t np) {
+// A[z][b][:] band totals -> exclusive prefix over b (one thread per (plane, int4 column group));
+// loads are issued 8 bands at a time so their latencies overlap
+__global__ void k_band_prefix(int32_t* __restrict__ A, int nb, int64_t n2, int64_t np) {
     const int64_t ng = n2 >> 2;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= np * ng) return;
     const int64_t z = i / ng, g = i - z * ng;
     int4* p = reinterpret_cast<int4*>(A + z * nb * n2) + g;
     int4 run = make_int4(0, 0, 0, 0);
-    for (int b = 0; b < nb; b++) {
-        const int4 t = p[b * ng];
-        p[b * ng] = run;
-        run = add4(run, t);
+    for (int b0 = 0; b0 < nb; b0 += 8) {
+        int4 t[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++)
+            if (b0 + k < nb) t[k] = p[(b0 + k) * ng];
+#pragma unroll
+        for (int k = 0; k < 8; k++)
+            if (b0 + k < nb) {
+                p[(b0 + k) * ng] = run;
+                run = add4(run, t[k]);
+            }
     }
 }
 
@@ -426,19 +466,20 @@ extern "C" int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t ba
     const int64_t cpr = n2 / kChunkCap;
     if (g->kind != HSZG_HSZP_ND || g->ndims != 3 || !s->canonical || n2 % kChunkCap || cpr < 1 ||
         TILE_CHUNKS % cpr || n2 > 4 * BS_MAXG * TILE_CHUNKS || band_rows < 1 || n1 > INT32_MAX || np > 65535 ||
-        !al16(L) || !al16(A)) {
+        !al16(L) || !al16(A) || !al16(s->payload)) {
         err->status = HSZG_INVALID_ARG;
         snprintf(err->message, sizeof(err->message),
                  "band_scan needs a canonical 3-D HSZP_ND stream with whole-chunk rows (n2 %% 32 == 0, "
-                 "n2 <= 4096, 256 %% (n2/32) == 0)");
+                 "n2 <= 4096, 256 %% (n2/32) == 0, 16-B aligned buffers)");
         return HSZG_INVALID_ARG;
     }
     if (g->n_chunks == 0) return HSZG_OK;
     const int64_t nb = (n1 + band_rows - 1) / band_rows;
-    const size_t smem = kFastTileBytes + stage_bytes(s->max_bitwidth);
+    const uint32_t sbytes = (uint32_t)((stage_bytes(s->max_bitwidth) + 15) / 16 * 16);
+    const size_t smem = kFastTileBytes + 2 * (size_t)sbytes + 16;
     allow_smem(k_band_scan, smem);
     k_band_scan<<<dim3((unsigned)nb, (unsigned)np), TILE_CHUNKS, smem, as_stream(stream)>>>(
-        s->payload, s->payload_len, s->offsets, g->n_chunks, (int)n1, (int)n2, (int)band_rows, L, A);
+        s->payload, s->payload_len, s->offsets, g->n_chunks, (int)n1, (int)n2, (int)band_rows, L, A, sbytes);
     const int64_t threads = np * (n2 / 4);
     k_band_prefix<<<(unsigned)((threads + 255) / 256), 256, 0, as_stream(stream)>>>(A, (int)nb, n2, np);
     if (cudaGetLastError() != cudaSuccess) return hszg_set_cuda_error(err, cudaGetLastError(), "band_scan");

@@ -440,7 +440,7 @@ class WindowPipeline:
         rpt = 256 // (n2 // 32)
         if self.band_rows_req:
             return int(self.band_rows_req)
-        want = -(-8 * _SMS // max(1, min(self.W, self.sf.nz)))
+        want = -(-24 * _SMS // max(1, min(self.W, self.sf.nz)))
         br = -(-n1 // want)
         return max(rpt, -(-br // rpt) * rpt)
 
