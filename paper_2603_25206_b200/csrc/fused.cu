@@ -13,9 +13,10 @@
 // y, x, so chunk 2*zl + h holds rows 4h..4h+3 of plane zl); halo block rows decode only the row
 // next to the CTA.
 //
-// Pipeline: warps 0-7 produce, 8-15 consume.  full[s] / empty[s] mbarriers hand ring slot s
-// (plane z in slot z % NPL) between them; stage[b] mbarriers carry the TMA transaction bytes of
-// staging buffer b (layer L in buffer L & 1).
+// Pipeline (warp-specialised): warp 0 loads (TMA), warps 1-7 decode, warps 8-23 emit.  full[s] /
+// empty[s] mbarriers hand ring slot s (plane z in slot z % NPL) between decoders and emitters;
+// stage[b] carries the TMA transaction bytes of staging buffer b (layer L in buffer L & 1) to the
+// decoders, free[b] hands the buffer back to the loader when the decoders moved past its layer.
 #include <cstdio>
 #include "tile.cuh"
 #include "stencil.cuh"
@@ -24,20 +25,22 @@
 namespace hszg {
 
 constexpr int FX_T = 512;                  // threads
-constexpr int FX_PT = 256;                 // producers: warps 0-7
+constexpr int FX_PT = 256;                 // producers: warp 0 loads, warps 1-7 decode
 constexpr int FX_CT = FX_T - FX_PT;        // consumers: warps 8-15
+constexpr int FX_DT = FX_PT - 32;          // decoders: warps 1-7 (warp 0 loads)
 constexpr int FX_BX = 16;                  // blocks along x per CTA
 constexpr int FX_BY = 2;                   // block rows per CTA
 constexpr int FX_ROWS = FX_BY * 8 + 2;     // ring rows: y0-1 .. y0+16
+constexpr int FX_RPW = FX_BY * 8 / (FX_CT / 32);   // output rows per consumer warp
 constexpr int FX_X0 = 8;                   // ring column of x0 (x0-8 .. x0+135 stored)
 constexpr int FX_RW = 148;                 // words per ring row (144 + pad: odd 16-B stride)
 constexpr int FX_PLANE = FX_ROWS * FX_RW;  // words per ring plane
 constexpr int FX_RANGES = FX_BY + 2;       // staged block rows per layer
 constexpr int FX_RBLK = FX_BX + 2;         // blocks per staged block row
 constexpr int FX_OSTR = FX_RBLK * 16;      // staged chunk offsets per range
+constexpr int FX_JOBS = (FX_RBLK * 8 * FX_BY + 2 * FX_RBLK + FX_DT - 1) / FX_DT;   // decode jobs per thread
 constexpr int FX_MSTR = FX_RBLK + 2;       // staged block means per range (16-B multiple of the buffer)
 
-__device__ __forceinline__ void producer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(FX_PT) : "memory"); }
 
 struct FxArgs {
     const uint8_t* payload;
@@ -74,7 +77,7 @@ __global__ void __launch_bounds__(FX_T, 1) k_fused_blocks(FxArgs a, uint32_t buf
     extern __shared__ __align__(128) uint8_t smem[];
     int32_t* Q = reinterpret_cast<int32_t*>(smem);
     uint8_t* BUF = smem + (size_t)NPL * FX_PLANE * 4;      // 2 layer buffers: [offsets | means | payload]
-    __shared__ __align__(8) uint64_t bar_full[NPL], bar_empty[NPL], bar_stage[2];
+    __shared__ __align__(8) uint64_t bar_full[NPL], bar_empty[NPL], bar_stage[2], bar_free[2];
     __shared__ uint64_t s_gbase[2][FX_RANGES];
     __shared__ uint32_t s_vbase[2][FX_RANGES];
     __shared__ int s_ok[2][FX_RANGES];
@@ -96,11 +99,13 @@ __global__ void __launch_bounds__(FX_T, 1) k_fused_blocks(FxArgs a, uint32_t buf
     for (int i = threadIdx.x; i < NPL * FX_PLANE / 4; i += FX_T) reinterpret_cast<int4*>(Q)[i] = make_int4(0, 0, 0, 0);
     if (threadIdx.x == 0) {
         for (int i = 0; i < NPL; i++) {
-            mbar_init(&bar_full[i], FX_PT);
+            mbar_init(&bar_full[i], FX_DT);
             mbar_init(&bar_empty[i], FX_CT);
         }
         mbar_init(&bar_stage[0], 1);
         mbar_init(&bar_stage[1], 1);
+        mbar_init(&bar_free[0], FX_DT);
+        mbar_init(&bar_free[1], FX_DT);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -155,7 +160,7 @@ __global__ void __launch_bounds__(FX_T, 1) k_fused_blocks(FxArgs a, uint32_t buf
                 s_vbase[b][lane] = vbase;
             }
 #pragma unroll
-            for (int k = 0; k < 3; k++) {                   // means: plain stores (read after producer_sync)
+            for (int k = 0; k < 3; k++) {                   // means: plain stores, published by the stage arrive
                 const int idx = (lane & 7) + 8 * k;
                 if ((lane >> 3) < FX_RANGES && idx < nblk) means[(lane >> 3) * FX_MSTR + idx] = d_m[k];
             }
@@ -169,9 +174,50 @@ __global__ void __launch_bounds__(FX_T, 1) k_fused_blocks(FxArgs a, uint32_t buf
         };
 
         if (wp == 0) {
+            // loader warp: TMA layer L into buffer L & 1 once the decoders released layer L-2
             describe(Lb);
-            issue((int)(Lb & 1));
-            if (Lb + 1 <= Llast) describe(Lb + 1);
+            for (int64_t L = Lb; L <= Llast; L++) {
+                const int b = (int)(L & 1);
+                const int64_t u = (L - Lb) >> 1;
+                if (u > 0) mbar_wait(&bar_free[b], (uint32_t)((u - 1) & 1));
+                issue(b);
+                if (L + 1 <= Llast) describe(L + 1);
+            }
+            return;
+        }
+        const int dt = threadIdx.x - 32;                // decoder thread (warps 1..7)
+        // this thread's decode jobs, the same in every plane: job = one 8-value row of one block
+        // (main block rows: all 8 rows; halo block rows: the row next to the CTA)
+        int jr[FX_JOBS], jc[FX_JOBS], jq[FX_JOBS], jm[FX_JOBS], jd[FX_JOBS];
+        bool jv[FX_JOBS];
+        {
+            const int nmain = FX_RBLK * 8 * nby;
+            const int njobs = nmain + 2 * FX_RBLK;
+#pragma unroll
+            for (int k = 0; k < FX_JOBS; k++) {
+                const int i = dt + k * FX_DT;
+                int r = 0, blk = 0, yl = 0;
+                if (i < nmain) {
+                    r = 1 + i / (8 * FX_RBLK);
+                    const int rem = i - (r - 1) * 8 * FX_RBLK;
+                    blk = rem >> 3;
+                    yl = rem & 7;
+                } else {
+                    const int j = i - nmain;
+                    const int side = j >= FX_RBLK;
+                    blk = j - side * FX_RBLK;
+                    r = side ? nby + 1 : 0;
+                    yl = side ? 0 : 7;
+                }
+                const int64_t bx = bx0 - 1 + blk, by = by0 - 1 + r;
+                jv[k] = i < njobs && bx >= 0 && bx < a.G2 && by >= 0 && by < a.G1;
+                const int rb = jv[k] ? (int)(bx - fbx) : 0;
+                jr[k] = r;
+                jc[k] = rb * 16 + (yl >> 2);
+                jq[k] = yl & 3;
+                jm[k] = r * FX_MSTR + rb;
+                jd[k] = (r * 8 + yl - 7) * FX_RW + FX_X0 + (int)(bx * 8 - x0);
+            }
         }
         int64_t cur = -1;
         for (int64_t z = zb - 1; z <= ze; z++) {
@@ -181,7 +227,7 @@ __global__ void __launch_bounds__(FX_T, 1) k_fused_blocks(FxArgs a, uint32_t buf
             int32_t* P = Q + s * FX_PLANE;
             if (z < 0 || z >= a.nz) {
                 const int32_t* h = z < 0 ? a.halo_lo : a.halo_hi;
-                for (int i = threadIdx.x; i < FX_ROWS * (FX_RW / 4); i += FX_PT) {
+                for (int i = dt; i < FX_ROWS * (FX_RW / 4); i += FX_DT) {
                     const int row = i / (FX_RW / 4), c4 = i - row * (FX_RW / 4);
                     const int64_t y = y0 - 1 + row, x = x0 - FX_X0 + 4 * c4;
                     int4 v = make_int4(0, 0, 0, 0);
@@ -192,12 +238,8 @@ __global__ void __launch_bounds__(FX_T, 1) k_fused_blocks(FxArgs a, uint32_t buf
                 const int64_t L = z >> 3;
                 const int b = (int)(L & 1);
                 if (L != cur) {
+                    if (cur >= 0) mbar_arrive(&bar_free[(int)(cur & 1)]);   // layer cur's buffer released
                     mbar_wait(&bar_stage[b], (uint32_t)(((L - Lb) >> 1) & 1));
-                    producer_sync();                 // everyone is past layer L-1: its buffer is free
-                    if (wp == 0 && L + 1 <= Llast) {
-                        issue((int)((L + 1) & 1));
-                        if (L + 2 <= Llast) describe(L + 2);
-                    }
                     cur = L;
                 }
                 const uint8_t* buf = BUF + (size_t)b * buf_bytes;
@@ -205,30 +247,15 @@ __global__ void __launch_bounds__(FX_T, 1) k_fused_blocks(FxArgs a, uint32_t buf
                 const int32_t* means = reinterpret_cast<const int32_t*>(offs + FX_RANGES * FX_OSTR);
                 const uint32_t* pw = reinterpret_cast<const uint32_t*>(means + FX_RANGES * FX_MSTR);
                 const int zl = (int)(z & 7);
-                const int nmain = FX_RBLK * 8 * nby;
-                const int njobs = nmain + 2 * FX_RBLK;
-                for (int i = threadIdx.x; i < njobs; i += FX_PT) {
-                    int r, blk, yl;
-                    if (i < nmain) {
-                        r = 1 + i / (8 * FX_RBLK);
-                        const int rem = i - (r - 1) * 8 * FX_RBLK;
-                        blk = rem >> 3;
-                        yl = rem & 7;
-                    } else {
-                        const int j = i - nmain;
-                        const int side = j >= FX_RBLK;
-                        blk = j - side * FX_RBLK;
-                        r = side ? nby + 1 : 0;
-                        yl = side ? 0 : 7;
-                    }
-                    const int64_t bx = bx0 - 1 + blk;
-                    if (bx < 0 || bx >= a.G2 || !s_ok[b][r]) continue;
-                    const int rb = (int)(bx - fbx);
-                    const int cl = rb * 16 + zl * 2 + (yl >> 2);
+#pragma unroll
+                for (int k = 0; k < FX_JOBS; k++) {
+                    if (!jv[k]) continue;
+                    const int r = jr[k];
+                    const int cl = jc[k] + 2 * zl;
                     const uint32_t rel = (uint32_t)(offs[r * FX_OSTR + cl] - s_gbase[b][r]) + s_vbase[b][r] * 16;
                     int4 lo, hi;
-                    decode8(pw, rel, yl & 3, means[r * FX_MSTR + rb], lo, hi);
-                    int32_t* dst = P + (r * 8 + yl - 7) * FX_RW + FX_X0 + (int)(bx * 8 - x0);
+                    decode8(pw, rel, jq[k], means[jm[k]], lo, hi);
+                    int32_t* dst = P + jd[k];
                     *reinterpret_cast<int4*>(dst) = lo;
                     *reinterpret_cast<int4*>(dst + 4) = hi;
                 }
@@ -239,7 +266,7 @@ __global__ void __launch_bounds__(FX_T, 1) k_fused_blocks(FxArgs a, uint32_t buf
     }
 
     // ================================ consumers ================================
-    const int cw = wp - FX_PT / 32;                               // rows 2cw, 2cw+1
+    const int cw = wp - FX_PT / 32;                               // rows FX_RPW*cw ..
     const int64_t plane = a.n1 * a.n2;
     const float epsf = __double2float_rn(a.eps), two_epsf = 2.0f * epsf;
     const double two_eps = 2.0 * a.eps;
@@ -260,8 +287,8 @@ __global__ void __launch_bounds__(FX_T, 1) k_fused_blocks(FxArgs a, uint32_t buf
         const int64_t gz = a.gz0 + z;
         const bool zin = gz > 0 && gz < a.gN0 - 1;
 #pragma unroll
-        for (int k = 0; k < 2; k++) {
-            const int r = 2 * cw + k;                             // output row within the CTA
+        for (int k = 0; k < FX_RPW; k++) {
+            const int r = FX_RPW * cw + k;                        // output row within the CTA
             const int64_t y = y0 + r;
             const int so = (r + 1) * FX_RW + FX_X0 + 4 * lane;
             const int4 c = *reinterpret_cast<const int4*>(Pc + so);
@@ -279,13 +306,20 @@ __global__ void __launch_bounds__(FX_T, 1) k_fused_blocks(FxArgs a, uint32_t buf
                 if (Exact)
                     emit4(a.o0, a.o1, a.o2, a.o3, o, zin, yin, x, a.n2, zm, c, zp, ym, yp, left, right, a.eps,
                           two_eps);
+                else if (zin && yin)                          // interior rows: no boundary branches
+                    emit4f(a.o0, a.o1, a.o2, a.o3, o, true, true, x, a.n2, zm, c, zp, ym, yp, left, right, a.eps,
+                           two_eps, epsf, two_epsf);
                 else
                     emit4f(a.o0, a.o1, a.o2, a.o3, o, zin, yin, x, a.n2, zm, c, zp, ym, yp, left, right, a.eps,
                            two_eps, epsf, two_epsf);
-                if (a.acc) st.add4(c);
+                if (a.acc) {
+                    if (Exact) st.add4(c);
+                    else st.add4f(c);
+                }
                 count += 4;
             }
         }
+        if (!Exact && (z & 15) == 15) st.fold();   // <= 32 add4f between folds
         mbar_arrive(&bar_empty[(int)((z - 1) & (NPL - 1))]);      // plane z-1 retired
     }
     if (a.acc) st.flush(a.acc, count);

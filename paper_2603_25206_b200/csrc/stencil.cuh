@@ -21,20 +21,42 @@ __device__ __forceinline__ void acc_add_i128(unsigned long long* limbs, i128 v) 
 
 struct WinStats {
     int64_t s1_64;   // per-thread partial: <= 4*W terms of |q| < 2^31
+    uint64_t sq;     // fast-path partial of q^2 (|q| < 2^27: four squares < 2^56), folded every <= 32 add4f
     i128 s1, s2;
     int32_t vmin, vmax;
-    __device__ __forceinline__ void init() { s1_64 = 0; s1 = 0; s2 = 0; vmin = INT32_MAX; vmax = INT32_MIN; }
+    __device__ __forceinline__ void init() {
+        s1_64 = 0;
+        sq = 0;
+        s1 = 0;
+        s2 = 0;
+        vmin = INT32_MAX;
+        vmax = INT32_MIN;
+    }
     __device__ __forceinline__ void add4(int4 q) {
         s1_64 += (int64_t)q.x + q.y + q.z + q.w;
         // four squares < 4 * 2^62 = 2^64: exact in u64, one 128-bit add per four values
-        const uint64_t sq = (uint64_t)((int64_t)q.x * q.x) + (uint64_t)((int64_t)q.y * q.y) +
-                            (uint64_t)((int64_t)q.z * q.z) + (uint64_t)((int64_t)q.w * q.w);
-        s2 += (i128)(u128)sq;
+        const uint64_t sq4 = (uint64_t)((int64_t)q.x * q.x) + (uint64_t)((int64_t)q.y * q.y) +
+                             (uint64_t)((int64_t)q.z * q.z) + (uint64_t)((int64_t)q.w * q.w);
+        s2 += (i128)(u128)sq4;
         vmin = min(vmin, min(min(q.x, q.y), min(q.z, q.w)));
         vmax = max(vmax, max(max(q.x, q.y), max(q.z, q.w)));
     }
+    // fast-path variant, exact while |q| < 2^27 (FAST_QLIM) — the condition the caller verifies from
+    // vmin / vmax (always exact) before trusting the fast pass; call fold() at least every 32 calls
+    __device__ __forceinline__ void add4f(int4 q) {
+        s1_64 += (int64_t)((q.x + q.y) + (q.z + q.w));
+        sq += (uint64_t)((int64_t)q.x * q.x) + (uint64_t)((int64_t)q.y * q.y) + (uint64_t)((int64_t)q.z * q.z) +
+              (uint64_t)((int64_t)q.w * q.w);
+        vmin = min(vmin, min(min(q.x, q.y), min(q.z, q.w)));
+        vmax = max(vmax, max(max(q.x, q.y), max(q.z, q.w)));
+    }
+    __device__ __forceinline__ void fold() {
+        s2 += (i128)(u128)sq;
+        sq = 0;
+    }
     // warp-reduce, then one lane publishes
     __device__ __forceinline__ void flush(HszgAcc* acc, int64_t count) {
+        fold();
         s1 += s1_64;
         for (int d = 16; d > 0; d >>= 1) {
             s1 += shfl_down_i128(s1, d);

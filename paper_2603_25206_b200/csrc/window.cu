@@ -12,6 +12,7 @@
 // Statistics: exact int128 per thread, warp-reduced, added into 32-bit limbs with 64-bit
 // atomics (HszgAcc) — order-independent and exact, finished on the host in Python ints.
 #include <cstdio>
+#include <cstdlib>
 #include "tile.cuh"
 #include "lookback.cuh"
 #include "stencil.cuh"
@@ -87,10 +88,20 @@ __global__ void __launch_bounds__(ZG_THREADS) k_zgrad_lap(const int32_t* __restr
             if (Exact)
                 emit4(o0, o1, o2, o3, (z - zlo) * plane + off, zin, yin, xi, n2, zm, c, zp, ym, yp, left, right, eps,
                       two_eps);
+            else if (zin && yin)                          // interior: no boundary branches
+                emit4f(o0, o1, o2, o3, (z - zlo) * plane + off, true, true, xi, n2, zm, c, zp, ym, yp, left, right,
+                       eps, two_eps, epsf, two_epsf);
             else
                 emit4f(o0, o1, o2, o3, (z - zlo) * plane + off, zin, yin, xi, n2, zm, c, zp, ym, yp, left, right, eps,
                        two_eps, epsf, two_epsf);
-            if (acc) st.add4(c);
+            if (acc) {
+                if (Exact) {
+                    st.add4(c);
+                } else {
+                    st.add4f(c);
+                    if ((z & 31) == 31) st.fold();
+                }
+            }
         }
         zm = c;
         c = zp;
@@ -219,10 +230,20 @@ __global__ void __launch_bounds__(ZG_THREADS) k_zsweep(const int32_t* __restrict
             if (Exact)
                 emit4(o0, o1, o2, o3, z * plane + off, zin, yin, xi, n2, prev, qc, next, qm, qp, left, right, eps,
                       two_eps);
+            else if (zin && yin)                          // interior: no boundary branches
+                emit4f(o0, o1, o2, o3, z * plane + off, true, true, xi, n2, prev, qc, next, qm, qp, left, right, eps,
+                       two_eps, epsf, two_epsf);
             else
                 emit4f(o0, o1, o2, o3, z * plane + off, zin, yin, xi, n2, prev, qc, next, qm, qp, left, right, eps,
                        two_eps, epsf, two_epsf);
-            if (acc) st.add4(qc);
+            if (acc) {
+                if (Exact) {
+                    st.add4(qc);
+                } else {
+                    st.add4f(qc);
+                    if ((z & 31) == 31) st.fold();
+                }
+            }
             if (z + 1 == nout && carry_out) *reinterpret_cast<int4*>(carry_out + off) = qc;
         }
         prev = qc;
