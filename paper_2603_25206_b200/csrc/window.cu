@@ -462,6 +462,13 @@ extern "C" int hszg_zgrad_lap(const int32_t* q, int64_t n1, int64_t n2, int64_t 
     return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
 }
 
+namespace hszg {
+int launch_zsweep_ring(const int32_t* L, int64_t n1, int64_t n2, int64_t nout, const int32_t* lookahead,
+                       const int32_t* carry, const int32_t* q_upper, int32_t* carry_out, int64_t gz0, int64_t gN0,
+                       double eps, float* const* out, HszgAcc* acc, const int32_t* A, const int32_t* lookA,
+                       int64_t BR, int64_t nb, int exact, cudaStream_t st);
+}
+
 extern "C" int hszg_zsweep_grad_lap(const int32_t* P2, int64_t n1, int64_t n2, int64_t nout, const int32_t* lookahead,
                                     const int32_t* carry, const int32_t* q_upper, int32_t* carry_out, int64_t gz0,
                                     int64_t gN0, double eps, float* const* out, HszgAcc* acc,
@@ -474,6 +481,14 @@ extern "C" int hszg_zsweep_grad_lap(const int32_t* P2, int64_t n1, int64_t n2, i
     const int64_t nb = band_off ? (n1 + band_rows - 1) / band_rows : 0;
     if (nout <= 0) return HSZG_OK;
     dim3 grid((unsigned)((n2 / 4 + ZG_THREADS - 1) / ZG_THREADS), (unsigned)n1);
+    static const char* zmode = getenv("HSZG_ZSWEEP");       // 'c': per-thread-column kernel (A/B runs)
+    if (band_off && band_rows % 16 == 0 && !(zmode && zmode[0] == 'c') && al16(lookahead) &&
+        al16(look_band_off)) {
+        return launch_zsweep_ring(P2, n1, n2, nout, lookahead, carry, q_upper, carry_out, gz0, gN0, eps, out, acc,
+                                  band_off, look_band_off, band_rows, nb, exact, as_stream(stream))
+                   ? HSZG_CUDA
+                   : HSZG_OK;
+    }
     (exact ? k_zsweep<true> : k_zsweep<false>)<<<grid, ZG_THREADS, 0, as_stream(stream)>>>(P2, n1, n2, nout, lookahead, carry, q_upper, carry_out,
                                                          gz0, gN0, eps, 2.0 * eps, out[0], out[1], out[2], out[3],
                                                          acc, band_off, look_band_off, band_rows, nb);

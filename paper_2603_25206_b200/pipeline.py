@@ -440,9 +440,10 @@ class WindowPipeline:
         rpt = 256 // (n2 // 32)
         if self.band_rows_req:
             return int(self.band_rows_req)
+        unit = max(rpt, 16)       # whole band_scan tiles; multiples of 16 take the ring z-sweep (zring.cu)
         want = -(-24 * _SMS // max(1, min(self.W, self.sf.nz)))
         br = -(-n1 // want)
-        return max(rpt, -(-br // rpt) * rpt)
+        return -(-br // unit) * unit
 
     def _stage_boundary(self):
         """Copy this run's halo / carry planes into the persistent buffers read by the loop."""

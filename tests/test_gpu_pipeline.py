@@ -98,7 +98,9 @@ def test_window_pipeline_single_rank(setup, kind, window, exact):
     pipe = pipeline.WindowPipeline(sf, pipeline.Comm(), window)
     pipe.exact_fp32 = exact
     if kind == 1 and window == 16:
-        pipe.band_rows_req = 5          # several bands, partial tiles and a short last band
+        pipe.band_rows_req = 5          # several bands, partial tiles and a short last band (column z-sweep)
+    if kind == 1 and window == 8:
+        pipe.band_rows_req = 16         # ring z-sweep with several bands
     if kind == 3 and window == 16:
         pipe.fused_layers = 2           # several z segments of the one-pass kernel
     outs = [torch.empty(dims, dtype=torch.float32, device="cuda") for _ in range(4)]
@@ -124,7 +126,7 @@ def test_window_pipeline_emulated_ranks(setup, kind, world):
         sf = pipeline.compress_shard(fd[z0 - lead:z1].contiguous(), kind, eps, (8, 8, 8), z0, z1, dims)
         ranks.append(pipeline.WindowPipeline(sf, pipeline.Comm(), 8))
         ranks[-1].exact_fp32 = True
-        ranks[-1].band_rows_req = 3 + r
+        ranks[-1].band_rows_req = (3 + r) if world == 2 else 16 * (r + 1)
     mine = [p.local_boundary(need_total=True) for p in ranks]
     Ts = [m["T"] for m in mine] if kind == 1 else None
     carries = [p.carry_from(Ts, r) for r, p in enumerate(ranks)]
@@ -174,7 +176,7 @@ def test_fast_decode_bitwidths_hszx_nd(dims):
 
 
 @pytest.mark.parametrize("dims", [(16, 16, 256), (24, 40, 64)], ids=lambda d: "x".join(map(str, d)))
-@pytest.mark.parametrize("band_rows", [None, 1, 7])
+@pytest.mark.parametrize("band_rows", [None, 1, 7, 16, 32])
 def test_fast_decode_bitwidths_band_scan(dims, band_rows):
     """hszg_band_scan (decode32 + row prefix + banded column prefix) across bit widths, through the
     HSZP_ND window pipeline (exact mode), vs the oracle."""
