@@ -292,7 +292,12 @@ def run_ours(args):
     achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
-                "share_of_step": round(d["ms"] / recorded_steps / ms, 4)}
+                "share_of_step": round(d["ms"] / recorded_steps / ms, 4),
+                "algo_bytes_per_launch": int(per_launch_bytes)}
+    prof = measured_traffic(dom, (N0, N1, N2), world, args.window)
+    if prof is not None:
+        roofline["traffic"] = prof["traffic_bytes_per_launch"]
+        roofline["traffic_source"] = prof["source"]
 
     # ---- e2e: host containers in, every output back to the host ------------------------------------------
     e2e = None
@@ -383,6 +388,21 @@ def run_e2e(args, shards, pipes, outs, comm, n_total):
 
 
 CPU_SECONDS = 10.0
+
+
+def measured_traffic(group, dims, world, window):
+    """DRAM bytes per launch of a launch group from the committed ncu `--set full` capture
+    (profiles/r01_traffic.json), when it was taken on this exact launch shape (config 5, 1 GPU)."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")
+    try:
+        with open(path) as f:
+            rec = json.load(f).get(group)
+    except (OSError, ValueError):
+        return None
+    if rec is None or tuple(dims) != (2048, 2048, 2048) or world != 1 or window != 64:
+        return None
+    return {"traffic_bytes_per_launch": int(rec["traffic_bytes_per_launch"]),
+            "source": f"profiles/r01_traffic.json: ncu --set full of {rec['kernel']} ({rec['launch']})"}
 
 
 def build_cpu_sample(field_dev, eps):
