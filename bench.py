@@ -197,9 +197,16 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # HSZG_DIST_BACKEND=gloo: plumbing check of the multi-rank path with ranks sharing one GPU
+    # (host-staged collectives; the timing of such a run is meaningless and is not a bench value)
+    backend = os.environ.get("HSZG_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend == "gloo" else local
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_2603_25206_b200 import _lib, pipeline, synthetic
     from paper_2603_25206_b200.device import DeviceStream
     from paper_2603_25206_b200.quant import field_minmax

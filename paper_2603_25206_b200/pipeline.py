@@ -58,6 +58,12 @@ class Comm:
         self.group = group
         self.rank = dist.get_rank(group) if ok else 0
         self.world = dist.get_world_size(group) if ok else 1
+        # gloo moves host tensors: device tensors are staged through host copies (CPU tests, and
+        # plumbing checks with several ranks on one GPU); NCCL takes device tensors directly
+        self.host_staged = ok and dist.get_backend(group) == "gloo"
+
+    def _host(self, t):
+        return t.cpu() if (self.host_staged and t.is_cuda) else t
 
     def all_gather(self, t):
         """List of every rank's tensor (same shape/dtype)."""
@@ -65,15 +71,19 @@ class Comm:
             return [t]
         import torch
 
-        outs = [torch.empty_like(t) for _ in range(self.world)]
-        self.dist.all_gather(outs, t.contiguous(), group=self.group)
-        return outs
+        h = self._host(t.contiguous())
+        outs = [torch.empty_like(h) for _ in range(self.world)]
+        self.dist.all_gather(outs, h, group=self.group)
+        return [o.to(t.device) for o in outs] if h is not t else outs
 
     def all_reduce(self, t, op: str):
         if self.world == 1:
             return t
         ops = {"sum": self.dist.ReduceOp.SUM, "min": self.dist.ReduceOp.MIN, "max": self.dist.ReduceOp.MAX}
-        self.dist.all_reduce(t, op=ops[op], group=self.group)
+        h = self._host(t)
+        self.dist.all_reduce(h, op=ops[op], group=self.group)
+        if h is not t:
+            t.copy_(h)
         return t
 
     def exchange(self, to_lower, to_upper, like):
@@ -88,16 +98,20 @@ class Comm:
         reqs = []
         from_lower = from_upper = None
         r, w = self.rank, self.world
+        like_h = self._host(like)
         if r > 0:
-            from_lower = torch.empty_like(like)
+            from_lower = torch.empty_like(like_h)
             reqs.append(self.dist.irecv(from_lower, r - 1, group=self.group))
-            reqs.append(self.dist.isend(to_lower.contiguous(), r - 1, group=self.group))
+            reqs.append(self.dist.isend(self._host(to_lower.contiguous()), r - 1, group=self.group))
         if r < w - 1:
-            from_upper = torch.empty_like(like)
+            from_upper = torch.empty_like(like_h)
             reqs.append(self.dist.irecv(from_upper, r + 1, group=self.group))
-            reqs.append(self.dist.isend(to_upper.contiguous(), r + 1, group=self.group))
+            reqs.append(self.dist.isend(self._host(to_upper.contiguous()), r + 1, group=self.group))
         for q in reqs:
             q.wait()
+        if like_h is not like:
+            from_lower = None if from_lower is None else from_lower.to(like.device)
+            from_upper = None if from_upper is None else from_upper.to(like.device)
         return from_lower, from_upper
 
     def barrier(self):

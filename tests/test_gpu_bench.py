@@ -1,0 +1,42 @@
+"""bench.py end to end on the GPU: the single-rank line, and the multi-rank z-slab path (halo
+planes, HSZP_ND carry, all-gathered exact statistics) run as 2 ranks sharing one GPU over gloo —
+a plumbing check (its timing is meaningless): the global mean / variance must equal the
+single-rank run's exactly."""
+
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ARGS = ["--dims", "96", "512", "512", "--steps", "1", "--warmup", "3", "--no-e2e", "--no-cpu", "--window", "32"]
+
+
+def _line(out: str) -> dict:
+    return json.loads([x for x in out.splitlines() if x.startswith("{")][-1])
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_bench_single_and_two_ranks():
+    one = subprocess.run([sys.executable, "bench.py", *ARGS], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert one.returncode == 0, one.stderr[-2000:]
+    l1 = _line(one.stdout)
+    assert l1["n_gpus"] == 1 and l1["value"] > 0 and l1["gpu_launches"] > 0
+    env = dict(os.environ, HSZG_DIST_BACKEND="gloo")
+    two = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py",
+                          "--gpus", "2", *ARGS], cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    assert two.returncode == 0, two.stderr[-3000:]
+    l2 = _line(two.stdout)
+    assert l2["n_gpus"] == 2
+    assert l2["stats_check"] == l1["stats_check"]
