@@ -278,13 +278,23 @@ int hszg_zsweep_grad_lap(const int32_t* P2, int64_t n1, int64_t n2, int64_t nout
 int hszg_fused_blocks(const HszgGeom* g, const HszgStream* s, int64_t gz0, int64_t gN0, const int32_t* halo_lo,
                       const int32_t* halo_hi, float* const* out, HszgAcc* acc, int64_t zlayers, int exact,
                       void* stream, HszgErr* err);
+/* HSZP_ND in one pass over a z-slab (3-D, canonical, n2 % 32 == 0, n2 <= 4096): decode + Lorenzo
+ * inversion (x, y, z prefixes) + gradient + Laplacian (+ stats into acc) with q never in memory.
+ * band_off / strip_edges: hszg_band_scan of the same stream with band_rows = 16 and L = NULL.
+ * carry: q of the plane below the slab (NULL at the field's first plane); q_upper: q of the plane
+ * above (NULL at the field's last plane).  out[4] = dz, dy, dx, Laplacian (fp32, slab-sized). */
+int hszg_lorenzo_onepass(const HszgGeom* g, const HszgStream* s, const int32_t* band_off,
+                         const int32_t* strip_edges, const int32_t* carry, const int32_t* q_upper, int64_t gz0,
+                         int64_t gN0, float* const* out, HszgAcc* acc, int exact, void* stream, HszgErr* err);
 /* HSZP_ND decode + row prefix + in-band column prefix in one pass (3-D, canonical, n2 % 32 == 0,
- * n2 <= 4096, 256 % (n2/32) == 0).  L[z][y][x] = 2-D prefix of plane z restricted to the rows of
- * y's band (bands of band_rows rows); band_off[z][b][x] = sum of the rows of bands < b, i.e.
- * P2 = L + band_off[z][y / band_rows].  L: dims[0]*dims[1]*dims[2] int32; band_off:
- * dims[0]*ceil(dims[1]/band_rows)*dims[2] int32. */
+ * n2 <= 4096, 256 % (n2/32) == 0).  L[z][y][x] (optional) = 2-D prefix of plane z restricted to the
+ * rows of y's band (bands of band_rows rows); band_off[z][b][x] = sum of the rows of bands < b, i.e.
+ * P2 = L + band_off[z][y / band_rows].  strip_edges (optional): for 128-wide x strips s,
+ * [z][s][y][0] = row prefix at x = 128s - 1 (0 for s = 0), [z][s][y][1] = at x = 128s + 128 (0 past
+ * the row).  L: dims[0]*dims[1]*dims[2] int32; band_off: dims[0]*ceil(dims[1]/band_rows)*dims[2];
+ * strip_edges: dims[0]*ceil(dims[2]/128)*E*2 int32 with E = dims[1] rounded up to even (+ 64 spare). */
 int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t band_rows, int32_t* L, int32_t* band_off,
-                   void* stream, HszgErr* err);
+                   int32_t* strip_edges, void* stream, HszgErr* err);
 /* HSZP_ND decode fused with the in-row prefix (rows of whole chunks, 256 % (n2/32) == 0). */
 int hszg_decode_rowscan(const HszgGeom* g, const HszgStream* s, int32_t* out, void* stream, HszgErr* err);
 /* In-place inclusive scan along the middle axis of an int32 [A][M][L] view. */

@@ -31,4 +31,13 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
         "l"(src), "r"(bytes), "r"(smem_addr(b))
         : "memory");
 }
+// 16-byte asynchronous global -> shared copy (L2 only) and the mbarrier arrive that fires when all of
+// the thread's earlier cp.async copies have landed (counts as one of the barrier's arrivals)
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* b) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+
 }  // namespace hszg

@@ -296,12 +296,15 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_tile_rowscan(SegGeo sg, const u
 // P2[z][y][x] = L[z][y][x] + A[z][y / BR][x], added by k_zsweep as it loads rows.  All int32
 // arithmetic wraps; every prefix is a q sum mod 2^32 (recon.cu header).
 constexpr int BS_MAXG = 4;   // int4 column groups per thread: n2 <= 4 * 4 * TILE_CHUNKS = 4096
+constexpr int SE_W = 128;    // strip width of the strip-edge table (the one-pass HSZP_ND kernel's x tile)
 
 
+template <bool Edges>
 __global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __restrict__ payload, uint64_t len,
                                                           const uint64_t* __restrict__ offsets, int64_t n_chunks,
                                                           int n1, int n2, int BR, int32_t* __restrict__ L,
-                                                          int32_t* __restrict__ A, uint32_t sbytes) {
+                                                          int32_t* __restrict__ A, int32_t* __restrict__ EF,
+                                                          uint32_t sbytes) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint32_t s_off[TILE_CHUNKS];
     __shared__ uint32_t s_wt[TILE_CHUNKS / 32];
@@ -379,16 +382,34 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __rest
         }
         s_off[threadIdx.x] = inc - tot;
         __syncthreads();
+        const int nstrips = (n2 + SE_W - 1) / SE_W;
         for (int rr = 0; rr < nr; rr++) {
-            int32_t* orow = L + (z * n1 + r0 + rr) * (int64_t)n2;
+            const int y = r0 + rr;
+            int32_t* orow = L ? L + (z * n1 + y) * (int64_t)n2 : nullptr;
 #pragma unroll
             for (int k = 0; k < BS_MAXG; k++) {
                 const int gi = threadIdx.x + k * TILE_CHUNKS;
                 if (gi < ng) {
                     const int ch = rr * cpr + (gi >> 3);
                     const int4 v = *reinterpret_cast<const int4*>(tile + ch * kChunkStride + ((gi & 7) << 2));
-                    ysum[k] = add4(ysum[k], add4u(v, s_off[ch]));
-                    *reinterpret_cast<int4*>(orow + 4 * gi) = ysum[k];
+                    const int4 rv = add4u(v, s_off[ch]);          // row prefix R at x = 4gi .. 4gi+3
+                    ysum[k] = add4(ysum[k], rv);
+                    if (orow) *reinterpret_cast<int4*>(orow + 4 * gi) = ysum[k];
+                    if (Edges) {                                  // strip edges: E[s] = R(128s-1), F[s] = R(128s+128)
+                        const int xg = 4 * gi;
+                        const int64_t n1e = ((int64_t)n1 + 1) & ~(int64_t)1;   // even rows per strip block
+                        int32_t* ef = EF + ((z * nstrips) * n1e + y) * 2;
+                        if ((xg & (SE_W - 1)) == SE_W - 4 && (xg + 4) / SE_W < nstrips)
+                            ef[(int64_t)((xg + 4) / SE_W) * n1e * 2] = rv.w;
+                        if ((xg & (SE_W - 1)) == 0) {
+                            const int s2 = xg / SE_W;
+                            if (s2 > 0) ef[(int64_t)(s2 - 1) * n1e * 2 + 1] = rv.x;
+                            else {
+                                ef[0] = 0;
+                                ef[(int64_t)(nstrips - 1) * n1e * 2 + 1] = 0;
+                            }
+                        }
+                    }
                 }
             }
         }
@@ -496,13 +517,13 @@ extern "C" int hszg_zsweep_grad_lap(const int32_t* P2, int64_t n1, int64_t n2, i
 }
 
 extern "C" int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t band_rows, int32_t* L, int32_t* A,
-                              void* stream, HszgErr* err) {
+                              int32_t* strip_edges, void* stream, HszgErr* err) {
     err->status = HSZG_OK;
     const int64_t n1 = g->dims[1], n2 = g->dims[2], np = g->dims[0];
     const int64_t cpr = n2 / kChunkCap;
     if (g->kind != HSZG_HSZP_ND || g->ndims != 3 || !s->canonical || n2 % kChunkCap || cpr < 1 ||
         TILE_CHUNKS % cpr || n2 > 4 * BS_MAXG * TILE_CHUNKS || band_rows < 1 || n1 > INT32_MAX || np > 65535 ||
-        !al16(L) || !al16(A) || !al16(s->payload)) {
+        !al16(L) || !al16(A) || !al16(s->payload) || (!L && !strip_edges)) {
         err->status = HSZG_INVALID_ARG;
         snprintf(err->message, sizeof(err->message),
                  "band_scan needs a canonical 3-D HSZP_ND stream with whole-chunk rows (n2 %% 32 == 0, "
@@ -513,9 +534,17 @@ extern "C" int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t ba
     const int64_t nb = (n1 + band_rows - 1) / band_rows;
     const uint32_t sbytes = (uint32_t)((stage_bytes(s->max_bitwidth) + 15) / 16 * 16);
     const size_t smem = kFastTileBytes + 2 * (size_t)sbytes + 16;
-    allow_smem(k_band_scan, smem);
-    k_band_scan<<<dim3((unsigned)nb, (unsigned)np), TILE_CHUNKS, smem, as_stream(stream)>>>(
-        s->payload, s->payload_len, s->offsets, g->n_chunks, (int)n1, (int)n2, (int)band_rows, L, A, sbytes);
+    if (strip_edges) {
+        allow_smem(k_band_scan<true>, smem);
+        k_band_scan<true><<<dim3((unsigned)nb, (unsigned)np), TILE_CHUNKS, smem, as_stream(stream)>>>(
+            s->payload, s->payload_len, s->offsets, g->n_chunks, (int)n1, (int)n2, (int)band_rows, L, A, strip_edges,
+            sbytes);
+    } else {
+        allow_smem(k_band_scan<false>, smem);
+        k_band_scan<false><<<dim3((unsigned)nb, (unsigned)np), TILE_CHUNKS, smem, as_stream(stream)>>>(
+            s->payload, s->payload_len, s->offsets, g->n_chunks, (int)n1, (int)n2, (int)band_rows, L, A, nullptr,
+            sbytes);
+    }
     const int64_t threads = np * (n2 / 4);
     k_band_prefix<<<(unsigned)((threads + 255) / 256), 256, 0, as_stream(stream)>>>(A, (int)nb, n2, np);
     if (cudaGetLastError() != cudaSuccess) return hszg_set_cuda_error(err, cudaGetLastError(), "band_scan");

@@ -433,12 +433,17 @@ class WindowPipeline:
             return
         n1, n2 = self.sf.global_dims[1], self.sf.global_dims[2]
         dev = _lib.device()
-        nslots = 2 if self.sf.kind == HSZP_ND else (0 if self._one_pass_ok() else 3)
+        one = self._one_pass_ok()
+        nslots = 0 if one else (2 if self.sf.kind == HSZP_ND else 3)
         self.ring = [t.empty((self.W, n1, n2), dtype=t.int32, device=dev) for _ in range(nslots)]
+        if one and self.sf.kind == HSZP_ND:
+            nz = self.sf.nz
+            self.lz_bands = t.empty((nz, -(-n1 // 16), n2), dtype=t.int32, device=dev)
+            self.lz_edges = t.empty(nz * -(-n2 // 128) * ((n1 + 1) // 2 * 2) * 2 + 64, dtype=t.int32, device=dev)
         self.halo_buf = t.zeros((2, n1, n2), dtype=t.int32, device=dev)       # [lower, upper]
         self.carry_buf = t.zeros((3, n1, n2), dtype=t.int32, device=dev)      # [rank carry, ping, pong]
         self.acc = t.zeros(ACC_BYTES, dtype=t.uint8, device=dev)
-        self.band_rows = self._band_rows() if self.sf.kind == HSZP_ND else 0
+        self.band_rows = self._band_rows() if (self.sf.kind == HSZP_ND and not one) else 0
         if self.band_rows:
             nb = -(-n1 // self.band_rows)
             self.bands = [t.empty((self.W, nb, n2), dtype=t.int32, device=dev) for _ in range(nslots)]
@@ -454,8 +459,8 @@ class WindowPipeline:
         rpt = 256 // (n2 // 32)
         if self.band_rows_req:
             return int(self.band_rows_req)
-        unit = max(rpt, 16)       # whole band_scan tiles; multiples of 16 take the ring z-sweep (zring.cu)
-        want = -(-24 * _SMS // max(1, min(self.W, self.sf.nz)))
+        unit = max(rpt, 64)       # whole band_scan tiles; multiples of 16 take the ring z-sweep (zring.cu)
+        want = -(-16 * _SMS // max(1, min(self.W, self.sf.nz)))
         br = -(-n1 // want)
         return -(-br // unit) * unit
 
@@ -485,7 +490,9 @@ class WindowPipeline:
 
     def _fused_loop(self, outs):
         _lib.call("hszg_acc_reset", _lib.ptr(self.acc), _lib.stream_handle())
-        if self.sf.kind == HSZP_ND:
+        if self.sf.kind == HSZP_ND and self._one_pass_ok():
+            self._run_lorenzo(outs)
+        elif self.sf.kind == HSZP_ND:
             self._run_zsweep(outs)
         elif self._one_pass_ok():
             self._run_fused_blocks(outs)
@@ -493,13 +500,41 @@ class WindowPipeline:
             self._run_blocks(outs)
 
     one_pass = True             # HSZX_ND: one-pass decode + analytics kernel when eligible (fused.cu)
+    # HSZP_ND one pass (lorenzo.cu): correct and tested, but slower than band scan + ring z-sweep so far
+    lorenzo_one_pass = False
     fused_layers = FUSED_LAYERS
 
     def _one_pass_ok(self) -> bool:
         sf, ds = self.sf, self.ds
         n = sf.global_dims
-        return (self.one_pass and sf.kind == HSZX_ND and tuple(sf.block_dims) == (8, 8, 8)
-                and sf.nz % 8 == 0 and n[1] % 8 == 0 and n[2] % 8 == 0 and ds.desc.max_bitwidth <= 16)
+        if not self.one_pass or ds.desc.max_bitwidth > 16:
+            return False
+        if sf.kind == HSZP_ND:
+            return self.lorenzo_one_pass and n[2] % 64 == 0 and n[2] <= 4096
+        return (sf.kind == HSZX_ND and tuple(sf.block_dims) == (8, 8, 8)
+                and sf.nz % 8 == 0 and n[1] % 8 == 0 and n[2] % 8 == 0)
+
+    def _run_lorenzo(self, outs):
+        """HSZP_ND in one pass over the slab (lorenzo.cu): a band-total pre-pass (hszg_band_scan with
+        16-row bands, no L) then decode + x/y/z prefixes + gradient + Laplacian + stats in one kernel."""
+        sf = self.sf
+        if self.timer:
+            self.timer.begin("prepass")
+        err = _lib.Err()
+        _lib.call("hszg_band_scan", ctypes.byref(self.ds.geom), ctypes.byref(self.ds.desc), 16, None,
+                  _lib.ptr(self.lz_bands), _lib.ptr(self.lz_edges), _lib.stream_handle(), ctypes.byref(err), err=err)
+        if self.timer:
+            self.timer.end("prepass", self._range_bytes(0, sf.nz) + self.lz_bands.numel() * 4 + self.lz_edges.numel() * 4)
+            self.timer.begin("fused")
+        carry = self.carry_buf[0] if sf.z0 > 0 else None
+        upper = self.halo_buf[1] if self.halo_hi is not None else None
+        outs_arr = (ctypes.c_void_p * 4)(*[_lib.ptr(o) for o in outs])
+        _lib.call("hszg_lorenzo_onepass", ctypes.byref(self.ds.geom), ctypes.byref(self.ds.desc),
+                  _lib.ptr(self.lz_bands), _lib.ptr(self.lz_edges), _lib.ptr(carry) if carry is not None else None,
+                  _lib.ptr(upper) if upper is not None else None, sf.z0, sf.global_dims[0], outs_arr,
+                  _lib.ptr(self.acc), int(self.exact_fp32), _lib.stream_handle(), ctypes.byref(err), err=err)
+        if self.timer:
+            self.timer.end("fused", self._range_bytes(0, sf.nz) + 16 * sf.nz * self.plane)
 
     def _run_fused_blocks(self, outs):
         """HSZX_ND in one launch over the whole slab: decode + gradient + Laplacian + stats, q never
@@ -583,7 +618,7 @@ class WindowPipeline:
             err = _lib.Err()
             if br:
                 _lib.call("hszg_band_scan", ctypes.byref(sub.geom), ctypes.byref(sub.desc), br,
-                          _lib.ptr(ring[k % 2]), _lib.ptr(self.bands[k % 2]), _lib.stream_handle(),
+                          _lib.ptr(ring[k % 2]), _lib.ptr(self.bands[k % 2]), None, _lib.stream_handle(),
                           ctypes.byref(err), err=err)
             else:
                 _lib.call("hszg_decode_rowscan", ctypes.byref(sub.geom), ctypes.byref(sub.desc),

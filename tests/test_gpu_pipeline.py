@@ -91,12 +91,15 @@ def _oracle_outputs(field, kind, eps):
 @pytest.mark.parametrize("kind", [1, 3])
 @pytest.mark.parametrize("window", [8, 16, 64])
 @pytest.mark.parametrize("exact", [True, False], ids=["exact", "fast"])
-def test_window_pipeline_single_rank(setup, kind, window, exact):
+@pytest.mark.parametrize("one_pass", [True, False], ids=["onepass", "windows"])
+def test_window_pipeline_single_rank(setup, kind, window, exact, one_pass):
     torch, pipeline, compress_device, field, eps, dims = setup
     fd = torch.from_numpy(field).cuda()
     sf = pipeline.compress_shard(fd, kind, eps, (8, 8, 8), 0, dims[0], dims)
     pipe = pipeline.WindowPipeline(sf, pipeline.Comm(), window)
     pipe.exact_fp32 = exact
+    pipe.one_pass = one_pass
+    pipe.lorenzo_one_pass = one_pass
     if kind == 1 and window == 16:
         pipe.band_rows_req = 5          # several bands, partial tiles and a short last band (column z-sweep)
     if kind == 1 and window == 8:
@@ -106,6 +109,8 @@ def test_window_pipeline_single_rank(setup, kind, window, exact):
     outs = [torch.empty(dims, dtype=torch.float32, device="cuda") for _ in range(4)]
     res = pipe.run(outs)
     want, s1, s2, mean, var = _oracle_outputs(field, kind, eps)
+    if one_pass and kind == 1 and dims[2] % 64 == 0:
+        assert hasattr(pipe, "lz_bands")        # took lorenzo.cu, not a silent fallback
     for k, (got, w) in enumerate(zip(outs, want)):
         _check_fp32(got.cpu().numpy(), w, exact, (kind, window, k))
     assert res["s1"] == s1 and res["s2"] == s2
@@ -116,7 +121,8 @@ def test_window_pipeline_single_rank(setup, kind, window, exact):
 
 @pytest.mark.parametrize("kind", [1, 3])
 @pytest.mark.parametrize("world", [2, 3])
-def test_window_pipeline_emulated_ranks(setup, kind, world):
+@pytest.mark.parametrize("one_pass", [True, False], ids=["onepass", "windows"])
+def test_window_pipeline_emulated_ranks(setup, kind, world, one_pass):
     torch, pipeline, compress_device, field, eps, dims = setup
     fd = torch.from_numpy(field).cuda()
     ranks = []
@@ -126,6 +132,8 @@ def test_window_pipeline_emulated_ranks(setup, kind, world):
         sf = pipeline.compress_shard(fd[z0 - lead:z1].contiguous(), kind, eps, (8, 8, 8), z0, z1, dims)
         ranks.append(pipeline.WindowPipeline(sf, pipeline.Comm(), 8))
         ranks[-1].exact_fp32 = True
+        ranks[-1].one_pass = one_pass
+        ranks[-1].lorenzo_one_pass = one_pass
         ranks[-1].band_rows_req = (3 + r) if world == 2 else 16 * (r + 1)
     mine = [p.local_boundary(need_total=True) for p in ranks]
     Ts = [m["T"] for m in mine] if kind == 1 else None
@@ -192,6 +200,7 @@ def test_fast_decode_bitwidths_band_scan(dims, band_rows):
     pipe = pipeline.WindowPipeline(sf, pipeline.Comm(), 8)
     pipe.exact_fp32 = True
     pipe.band_rows_req = band_rows
+    pipe.one_pass = pipe.lorenzo_one_pass = band_rows is None   # None: the one-pass kernel; else two passes
     outs = [torch.empty(dims, dtype=torch.float32, device="cuda") for _ in range(4)]
     res = pipe.run(outs)
     want, s1, s2, mean, var = _oracle_outputs(f, 1, eps)
