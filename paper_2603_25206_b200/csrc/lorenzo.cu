@@ -7,14 +7,15 @@
 // strip s and row y the row prefix just left / right of the strip, E = R(128s-1), F = R(128s+128).
 // Main kernel: a CTA owns x in [128s, 128s+128) by y in [16b, 16b+16) and slides along z over the
 // whole slab.  Per plane:
-//   warp 0      TMA-loads the payload bytes of the 17 rows y0..y0+16 restricted to the strip's 4
+//   warps 0-1   load (lane-parallel cp.async) the payload bytes of the 17 rows y0..y0+16 restricted to the strip's 4
 //               chunks, the band-offset row A[z][b] and the strip edges (and writes the chunk
 //               offsets, prefetched a plane ahead, into the staging slot);
-//   warps 1-8   decode quarter-chunk jobs and prefix each row (half-warp scan + E) into R, then
-//               run the column prefix from A[z][b] (y) and add the previous q plane (z) —
+//   warps 1-8   decode quarter-chunk jobs and prefix each row (half-warp scan + E) into R (double
+//               buffered);
+//   warps 9-13  run the column prefix from A[z][b] (y) and add the previous q plane (z):
 //               P2[y][x] = A[b][x] + sum_{y0<=y'<=y} R[y'][x], q[z] = q[z-1] + P2[z]; the halo
 //               columns x0-1 / x0+128 come from E / F, the halo row y0-1 from A alone;
-//   warps 9-16  emit from the q ring (as fused.cu / zring.cu).
+//   warps 14-21 emit from the q ring (as fused.cu / zring.cu).
 #include <cstdio>
 #include "tile.cuh"
 #include "stencil.cuh"
@@ -22,9 +23,10 @@
 
 namespace hszg {
 
-constexpr int LR_T = 544;
-constexpr int LR_DT = 256;                  // decoders: warps 1-8
-constexpr int LR_CT = 256;                  // emitters: warps 9-16, 2 rows each
+constexpr int LR_T = 736;
+constexpr int LR_DT = 256;                  // decoders: warps 2-9
+constexpr int LR_ST = 160;                  // scanners: warps 10-14 (130 columns)
+constexpr int LR_CT = 256;                  // emitters: warps 15-22, 2 rows each
 constexpr int LR_TX = 128, LR_TY = 16;
 constexpr int LR_ROWS = LR_TY + 2;          // q ring rows y0-1 .. y0+16
 constexpr int LR_DROWS = LR_TY + 1;         // decoded rows y0 .. y0+16
@@ -65,21 +67,20 @@ __host__ __device__ inline uint32_t lr_ef_off(uint32_t pr) { return lr_a_off(pr)
 inline uint32_t lr_pr(int max_bw) { return (uint32_t)((4 * chunk_bytes(kChunkCap, max_bw) + 31 + 15) / 16 * 16); }
 inline uint32_t lr_slot(int max_bw) { return (lr_ef_off(lr_pr(max_bw)) + LR_EFN * 4 + 127) / 128 * 128; }
 inline size_t lr_smem(int max_bw) {
-    return (size_t)LR_NPL * LR_PLANE * 4 + (size_t)LR_D * lr_slot(max_bw) + (size_t)LR_DROWS * LR_TX * 4;
+    return (size_t)LR_NPL * LR_PLANE * 4 + (size_t)LR_D * lr_slot(max_bw) + (size_t)2 * LR_DROWS * LR_TX * 4;
 }
 
 // strip-edge table rows per (plane, strip): even, so every (plane, strip) block starts 16-B aligned
 __host__ __device__ inline int64_t ef_rows(int64_t n1) { return (n1 + 1) & ~(int64_t)1; }
-
-__device__ __forceinline__ void decoder_sync() { asm volatile("bar.sync 1, %0;" ::"n"(LR_DT) : "memory"); }
 
 template <bool Exact>
 __global__ void __launch_bounds__(LR_T, 1) k_lorenzo_ring(LrArgs a) {
     extern __shared__ __align__(128) uint8_t lsm[];
     int32_t* Q = reinterpret_cast<int32_t*>(lsm);                         // [NPL][ROWS][RW]
     uint8_t* SL = lsm + (size_t)LR_NPL * LR_PLANE * 4;                    // [D][slot]
-    int32_t* RB = reinterpret_cast<int32_t*>(SL + (size_t)LR_D * a.slot);  // [DROWS][TX]
-    __shared__ __align__(8) uint64_t s_full[LR_D], s_empty[LR_D], q_full[LR_NPL], q_empty[LR_NPL], o_full[LR_OD];
+    int32_t* RB = reinterpret_cast<int32_t*>(SL + (size_t)LR_D * a.slot);  // [2][DROWS][TX]
+    __shared__ __align__(8) uint64_t s_full[LR_D], s_empty[LR_D], q_full[LR_NPL], q_empty[LR_NPL], o_full[LR_OD],
+        rb_full[2], rb_empty[2];
     __shared__ __align__(16) uint64_t OR[LR_OD * LR_DROWS * 6];        // offsets ring (loader only)
     const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
     const int64_t s = blockIdx.x, b = blockIdx.y;
@@ -95,14 +96,18 @@ __global__ void __launch_bounds__(LR_T, 1) k_lorenzo_ring(LrArgs a) {
     for (int i = threadIdx.x; i < LR_NPL * LR_PLANE / 4; i += LR_T) reinterpret_cast<int4*>(Q)[i] = make_int4(0, 0, 0, 0);
     if (threadIdx.x == 0) {
         for (int i = 0; i < LR_D; i++) {
-            mbar_init(&s_full[i], 33);                // 32 cp.async completions + the rel-table arrive
-            mbar_init(&s_empty[i], LR_DT);
+            mbar_init(&s_full[i], 65);                // 2 x 32 cp.async completions + the rel-table arrive
+            mbar_init(&s_empty[i], LR_DT + LR_ST);
         }
         for (int i = 0; i < LR_NPL; i++) {
-            mbar_init(&q_full[i], LR_DT);
+            mbar_init(&q_full[i], LR_ST);
             mbar_init(&q_empty[i], LR_CT);
         }
         for (int i = 0; i < LR_OD; i++) mbar_init(&o_full[i], 32);
+        for (int i = 0; i < 2; i++) {
+            mbar_init(&rb_full[i], LR_DT);
+            mbar_init(&rb_empty[i], LR_ST);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -111,55 +116,50 @@ __global__ void __launch_bounds__(LR_T, 1) k_lorenzo_ring(LrArgs a) {
         // ================================ loader ================================
         const bool row_ok = lane < nrow;
         // Lane-parallel 16-B async copies (cp.async, completion tracked by the mbarriers): per plane
-        // ~30 small pieces, which one elected lane would otherwise issue one TMA at a time.
+        // ~30 small pieces, which one elected lane would otherwise issue one TMA at a time.  All
+        // addresses advance by a fixed stride per plane (no 64-bit index math in the loop).
         // Chunk offsets of this lane's row arrive LR_OD planes ahead (6 entries from an even chunk
-        // index: the strip's 4 starts + the end; 4 entries at the index's end, where the end is the
-        // payload end).
+        // index: the strip's 4 starts + the end; 4 entries for the index's last row, whose end is
+        // the payload end).
+        const int64_t ostride = n1 * cpr;                              // chunks per plane
+        const uint64_t* osrc0 = a.offsets + (y0 + lane) * cpr + 4 * s;  // this lane's row, plane 0
+        const bool tail = row_ok && (y0 + lane == n1 - 1) && (4 * s + nch == cpr);   // ends the index
+        const uint64_t pay_end = payload_end(a.offsets, a.n_chunks, a.len);
         auto oissue = [&](int64_t zz) {
             const int os = (int)(zz % LR_OD);
             if (row_ok) {
-                const int64_t c0 = (zz * n1 + y0 + lane) * cpr + 4 * s;
-                const int nv = c0 + 6 <= a.n_chunks ? 3 : 2;
+                const uint64_t* src = osrc0 + zz * ostride;
                 uint64_t* dst = OR + (os * LR_DROWS + lane) * 6;
-                for (int v = 0; v < nv; v++) cp_async16(dst + 2 * v, a.offsets + c0 + 2 * v);
+                cp_async16(dst, src);
+                cp_async16(dst + 2, src + 2);
+                if (!(tail && zz == nz - 1)) cp_async16(dst + 4, src + 4);
             }
             cp_async_arrive_noinc(&o_full[os]);
         };
         for (int64_t zz = 0; zz < LR_OD && zz < nz; zz++) oissue(zz);
-        const int anv = (int)(xe - xs) / 4;               // 16-B vectors of the band-offset row
+        const uint32_t rowoff = (uint32_t)lane * a.pr;
         for (int64_t zz = 0; zz < nz; zz++) {
             const int slot = (int)(zz % LR_D);
-            const int64_t u = zz / LR_D;
-            if (u > 0) mbar_wait(&s_empty[slot], (uint32_t)((u - 1) & 1));
+            if (zz >= LR_D) mbar_wait(&s_empty[slot], (uint32_t)((zz / LR_D - 1) & 1));
             const int os = (int)(zz % LR_OD);
             mbar_wait(&o_full[os], (uint32_t)((zz / LR_OD) & 1));
-            uint64_t o[5];
-#pragma unroll
-            for (int k = 0; k < 5; k++) o[k] = OR[(os * LR_DROWS + lane) * 6 + k];
             uint8_t* sp = SL + (size_t)slot * a.slot;
             if (row_ok) {
-                const int64_t c0 = (zz * n1 + y0 + lane) * cpr + 4 * s;
-                const uint64_t end = c0 + nch < a.n_chunks
-                                         ? (nch == 4 ? o[4] : nch == 3 ? o[3] : nch == 2 ? o[2] : o[1])
-                                         : payload_end(a.offsets, a.n_chunks, a.len);
-                const uint64_t base = o[0] & ~(uint64_t)15;
-                const int nv = (int)((end - base + 15) >> 4);
-                uint32_t* rel = reinterpret_cast<uint32_t*>(sp + lr_rel_off(a.pr)) + 4 * lane;
-#pragma unroll
-                for (int k = 0; k < 4; k++)
-                    if (k < nch) rel[k] = (uint32_t)(o[k] - base) + (uint32_t)lane * a.pr;
-                uint8_t* dst = sp + (size_t)lane * a.pr;
+                const uint64_t* ob = OR + (os * LR_DROWS + lane) * 6;
+                const uint64_t o0 = ob[0];
+                const uint64_t end = (tail && zz == nz - 1) ? pay_end : ob[nch];
+                const uint64_t base = o0 & ~(uint64_t)15;
+                const uint32_t b0 = (uint32_t)(o0 - base) + rowoff;
+                uint4 rl;
+                rl.x = b0;
+                rl.y = (uint32_t)(ob[1] - o0) + b0;
+                rl.z = (uint32_t)(ob[2] - o0) + b0;
+                rl.w = (uint32_t)(ob[3] - o0) + b0;
+                *reinterpret_cast<uint4*>(sp + lr_rel_off(a.pr) + 16 * lane) = rl;
+                const int nv = (int)((uint32_t)(end - base + 15) >> 4);
+                uint8_t* dst = sp + rowoff;
                 const uint8_t* src = a.payload + base;
                 for (int v = 0; v < nv; v++) cp_async16(dst + 16 * v, src + 16 * v);
-            } else {
-                // the other lanes: the band-offset row (x0-4 .. x0+132) and the strip edges
-                const int l = lane - nrow, nl = 32 - nrow;
-                const int32_t* asrc = a.A + (zz * a.nb + b) * n2 + xs;
-                int32_t* adst = reinterpret_cast<int32_t*>(sp + lr_a_off(a.pr)) + (xs - (x0 - 4));
-                for (int v = l; v < anv; v += nl) cp_async16(adst + 4 * v, asrc + 4 * v);
-                const int32_t* esrc = a.EF + ((zz * a.nstrips + s) * ef_rows(n1) + y0) * 2;
-                int32_t* edst = reinterpret_cast<int32_t*>(sp + lr_ef_off(a.pr));
-                for (int v = l; v < LR_EFN / 4; v += nl) cp_async16(edst + 4 * v, esrc + 4 * v);
             }
             cp_async_arrive_noinc(&s_full[slot]);
             __syncwarp();
@@ -169,43 +169,46 @@ __global__ void __launch_bounds__(LR_T, 1) k_lorenzo_ring(LrArgs a) {
         return;
     }
 
-    if (wp <= LR_DT / 32) {
-        // ================================ decoders ================================
-        const int dt = threadIdx.x - 32;
-        constexpr int C4 = LR_AW / 4;
-        auto copy_plane = [&](const int32_t* g, int32_t* P) {
-            for (int i = dt; i < LR_ROWS * C4; i += LR_DT) {
-                const int r = i / C4, j = 4 * (i - r * C4);
-                const int64_t y = y0 - 1 + r, x = x0 - 4 + j;
-                int4 v = make_int4(0, 0, 0, 0);
-                if (g && y >= 0 && y < n1 && x >= 0 && x < n2) v = ld4(g + y * n2 + x);
-                *reinterpret_cast<int4*>(P + r * LR_RW + LR_X0 - 4 + j) = v;
-            }
-        };
-        copy_plane(a.carry, Q);                                        // plane -1 in slot 0
-        mbar_arrive(&q_full[0]);
-        for (int64_t zz = 0; zz <= nz; zz++) {
-            const int qs = (int)((zz + 1) % LR_NPL);
-            const int64_t u = (zz + 1) / LR_NPL;
-            if (u > 0) mbar_wait(&q_empty[qs], (uint32_t)((u - 1) & 1));
-            int32_t* Pn = Q + qs * LR_PLANE;
-            if (zz == nz) {                                             // the plane above the slab
-                copy_plane(a.q_upper, Pn);
-                mbar_arrive(&q_full[qs]);
-                break;
-            }
+    if (wp == 1) {
+        // ============================ loader, band offsets ============================
+        // the band-offset row (x0-4 .. x0+132) and the strip edges of every plane
+        const int anv = (int)(xe - xs) / 4;
+        const int32_t* asrc = a.A + b * n2 + xs;
+        const int64_t astride = a.nb * n2;
+        const int32_t* esrc = a.EF + (s * ef_rows(n1) + y0) * 2;
+        const int64_t estride = a.nstrips * ef_rows(n1) * 2;
+        const uint32_t aoff = lr_a_off(a.pr) + (uint32_t)(xs - (x0 - 4)) * 4, eoff = lr_ef_off(a.pr);
+        for (int64_t zz = 0; zz < nz; zz++) {
             const int slot = (int)(zz % LR_D);
+            if (zz >= LR_D) mbar_wait(&s_empty[slot], (uint32_t)((zz / LR_D - 1) & 1));
+            uint8_t* sp = SL + (size_t)slot * a.slot;
+            const int32_t* as = asrc + zz * astride;
+            int32_t* ad = reinterpret_cast<int32_t*>(sp + aoff);
+            for (int v = lane; v < anv; v += 32) cp_async16(ad + 4 * v, as + 4 * v);
+            if (lane < LR_EFN / 4) cp_async16(reinterpret_cast<int32_t*>(sp + eoff) + 4 * lane, esrc + zz * estride + 4 * lane);
+            cp_async_arrive_noinc(&s_full[slot]);
+        }
+        return;
+    }
+
+    if (wp <= 1 + LR_DT / 32) {
+        // ================================ decoders ================================
+        // decode quarter-chunk jobs (a half-warp per row) and prefix the rows into RB[zz & 1]
+        const int dt = threadIdx.x - 64;
+        for (int64_t zz = 0; zz < nz; zz++) {
+            const int slot = (int)(zz % LR_D);
+            const int rb = (int)(zz & 1);
             mbar_wait(&s_full[slot], (uint32_t)((zz / LR_D) & 1));
+            if (zz >= 2) mbar_wait(&rb_empty[rb], (uint32_t)(((zz >> 1) - 1) & 1));
             const uint8_t* sp = SL + (size_t)slot * a.slot;
             const uint32_t* pw = reinterpret_cast<const uint32_t*>(sp);
             const uint32_t* rel = reinterpret_cast<const uint32_t*>(sp + lr_rel_off(a.pr));
-            const int32_t* SA = reinterpret_cast<const int32_t*>(sp + lr_a_off(a.pr));
             const int32_t* EF = reinterpret_cast<const int32_t*>(sp + lr_ef_off(a.pr));
-            // -- 1. decode quarter-chunk jobs (a half-warp per row) and prefix the rows into RB
-            decoder_sync();                                             // RB of the previous plane consumed
+            int32_t* R = RB + rb * LR_DROWS * LR_TX;
 #pragma unroll
             for (int pass = 0; pass < (LR_DROWS * 16 + LR_DT - 1) / LR_DT; pass++) {
                 const int i = dt + pass * LR_DT;
+                if (pass > 0 && (i & ~31) >= LR_DROWS * 16) break;        // warp-uniform: no jobs left
                 const int r = i >> 4, qj = i & 15, kq = qj >> 2;
                 const bool ok = r < nrow && kq < nch;
                 uint32_t v[8];
@@ -231,30 +234,67 @@ __global__ void __launch_bounds__(LR_T, 1) k_lorenzo_ring(LrArgs a) {
                 }
                 if (ok) {
                     const uint32_t base = (uint32_t)EF[2 * r] + inc - t;   // row prefix before this job
-                    int32_t* dst = RB + r * LR_TX + 8 * qj;
+                    int32_t* dst = R + r * LR_TX + 8 * qj;
                     *reinterpret_cast<int4*>(dst) = make_int4((int)(base + v[0]), (int)(base + v[1]),
                                                               (int)(base + v[2]), (int)(base + v[3]));
                     *reinterpret_cast<int4*>(dst + 4) = make_int4((int)(base + v[4]), (int)(base + v[5]),
                                                                   (int)(base + v[6]), (int)(base + v[7]));
                 }
             }
-            decoder_sync();
-            // -- 2. column prefix from the band offsets (y) + previous plane (z), one column per thread
-            const int32_t* Pp = Q + (int)(zz % LR_NPL) * LR_PLANE;
-            // thread dt < 128: column x0+dt; dt == 128 / 129: the halo columns x0-1 / x0+128 (from E / F)
-            const bool edge = dt >= LR_TX;
-            const int which = dt - LR_TX;                          // 0: left halo, 1: right halo
-            bool colok;
-            int col, jx;
-            if (!edge) {
-                colok = x0 + dt < n2;
-                col = LR_X0 + dt;
-                jx = 4 + dt;
-            } else {
-                colok = which == 0 ? x0 > 0 : (which == 1 && x0 + LR_TX < n2);
-                col = which == 0 ? LR_X0 - 1 : LR_X0 + LR_TX;
-                jx = which == 0 ? 3 : 4 + LR_TX;
+            mbar_arrive(&s_empty[slot]);
+            mbar_arrive(&rb_full[rb]);
+        }
+        return;
+    }
+
+    if (wp <= 1 + (LR_DT + LR_ST) / 32) {
+        // ================================ scanners ================================
+        // column prefix from the band offsets (y) + the previous q plane (z): thread st < 128 owns
+        // column x0+st, st == 128 / 129 the halo columns x0-1 / x0+128 (their R comes from E / F)
+        const int st = threadIdx.x - 64 - LR_DT;
+        constexpr int C4 = LR_AW / 4;
+        auto copy_plane = [&](const int32_t* g, int32_t* P) {
+            for (int i = st; i < LR_ROWS * C4; i += LR_ST) {
+                const int r = i / C4, j = 4 * (i - r * C4);
+                const int64_t y = y0 - 1 + r, x = x0 - 4 + j;
+                int4 v = make_int4(0, 0, 0, 0);
+                if (g && y >= 0 && y < n1 && x >= 0 && x < n2) v = ld4(g + y * n2 + x);
+                *reinterpret_cast<int4*>(P + r * LR_RW + LR_X0 - 4 + j) = v;
             }
+        };
+        copy_plane(a.carry, Q);                                        // plane -1 in slot 0
+        mbar_arrive(&q_full[0]);
+        const bool edge = st >= LR_TX;
+        const int which = st - LR_TX;                                  // 0: left halo, 1: right halo
+        bool colok;
+        int col, jx;
+        if (!edge) {
+            colok = x0 + st < n2;
+            col = LR_X0 + st;
+            jx = 4 + st;
+        } else {
+            colok = which == 0 ? x0 > 0 : (which == 1 && x0 + LR_TX < n2);
+            col = which == 0 ? LR_X0 - 1 : LR_X0 + LR_TX;
+            jx = which == 0 ? 3 : 4 + LR_TX;
+        }
+        for (int64_t zz = 0; zz <= nz; zz++) {
+            const int qs = (int)((zz + 1) % LR_NPL);
+            const int64_t u = (zz + 1) / LR_NPL;
+            if (u > 0) mbar_wait(&q_empty[qs], (uint32_t)((u - 1) & 1));
+            int32_t* Pn = Q + qs * LR_PLANE;
+            if (zz == nz) {                                             // the plane above the slab
+                copy_plane(a.q_upper, Pn);
+                mbar_arrive(&q_full[qs]);
+                break;
+            }
+            const int slot = (int)(zz % LR_D);
+            const int rb = (int)(zz & 1);
+            mbar_wait(&rb_full[rb], (uint32_t)((zz >> 1) & 1));          // implies the slot's data landed
+            const uint8_t* sp = SL + (size_t)slot * a.slot;
+            const int32_t* SA = reinterpret_cast<const int32_t*>(sp + lr_a_off(a.pr));
+            const int32_t* EF = reinterpret_cast<const int32_t*>(sp + lr_ef_off(a.pr));
+            const int32_t* R = RB + rb * LR_DROWS * LR_TX;
+            const int32_t* Pp = Q + (int)(zz % LR_NPL) * LR_PLANE;
             if (colok) {
                 const uint32_t av = (uint32_t)SA[jx];
                 if (y0 > 0) Pn[col] = (int)((uint32_t)Pp[col] + av);     // halo row y0-1: P2 = A
@@ -262,12 +302,13 @@ __global__ void __launch_bounds__(LR_T, 1) k_lorenzo_ring(LrArgs a) {
 #pragma unroll
                 for (int r = 0; r < LR_DROWS; r++) {
                     if (r < nrow) {
-                        run += edge ? (uint32_t)EF[2 * r + which] : (uint32_t)RB[r * LR_TX + dt];
+                        run += edge ? (uint32_t)EF[2 * r + which] : (uint32_t)R[r * LR_TX + st];
                         const int o = (r + 1) * LR_RW + col;
                         Pn[o] = (int)((uint32_t)Pp[o] + av + run);
                     }
                 }
             }
+            mbar_arrive(&rb_empty[rb]);
             mbar_arrive(&s_empty[slot]);
             mbar_arrive(&q_full[qs]);
         }
@@ -275,7 +316,7 @@ __global__ void __launch_bounds__(LR_T, 1) k_lorenzo_ring(LrArgs a) {
     }
 
     // ================================ emitters ================================
-    const int cw = wp - 1 - LR_DT / 32;
+    const int cw = wp - 2 - (LR_DT + LR_ST) / 32;
     const float epsf = __double2float_rn(a.eps), two_epsf = 2.0f * epsf;
     const double two_eps = 2.0 * a.eps;
     WinStats st;
