@@ -24,7 +24,7 @@ from .errors import (
 )
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhszg.so")
+LIB_PATH = os.environ.get("HSZG_LIB") or os.path.join(HERE, "libhszg.so")   # HSZG_LIB: A/B builds
 
 PAYLOAD_PAD = 16
 

@@ -45,8 +45,13 @@ struct WinStats {
     // vmin / vmax (always exact) before trusting the fast pass; call fold() at least every 32 calls
     __device__ __forceinline__ void add4f(int4 q) {
         s1_64 += (int64_t)((q.x + q.y) + (q.z + q.w));
-        sq += (uint64_t)((int64_t)q.x * q.x) + (uint64_t)((int64_t)q.y * q.y) + (uint64_t)((int64_t)q.z * q.z) +
-              (uint64_t)((int64_t)q.w * q.w);
+        // chained 64-bit multiply-adds (one IMAD.WIDE each); |q| < 2^27 keeps 128 squares < 2^63
+        int64_t t = (int64_t)sq;
+        t += (int64_t)q.x * q.x;
+        t += (int64_t)q.y * q.y;
+        t += (int64_t)q.z * q.z;
+        t += (int64_t)q.w * q.w;
+        sq = (uint64_t)t;
         vmin = min(vmin, min(min(q.x, q.y), min(q.z, q.w)));
         vmax = max(vmax, max(max(q.x, q.y), max(q.z, q.w)));
     }

@@ -208,10 +208,8 @@ __global__ void __launch_bounds__(ZR_T, 2) k_zsweep_ring(ZrArgs a) {
                 else
                     emit4f(a.o0, a.o1, a.o2, a.o3, o, zin, yin, x, n2, zm, c, zp, ym, yp, left, right, a.eps,
                            two_eps, epsf, two_epsf);
-                if (a.acc) {
-                    if (Exact) st.add4(c);
-                    else st.add4f(c);
-                }
+                if (Exact) st.add4(c);                    // stats always kept (acc may be null)
+                else st.add4f(c);
                 count += 4;
                 if (z + 1 == nout && a.carry_out) *reinterpret_cast<int4*>(a.carry_out + y * n2 + x) = c;
             }
