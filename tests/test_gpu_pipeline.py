@@ -104,6 +104,7 @@ def test_window_pipeline_single_rank(setup, kind, window, exact, one_pass):
         pipe.band_rows_req = 5          # several bands, partial tiles and a short last band (column z-sweep)
     if kind == 1 and window == 8:
         pipe.band_rows_req = 16         # ring z-sweep with several bands
+        pipe.overlap = True             # band scans on the side stream
     if kind == 3 and window == 16:
         pipe.fused_layers = 2           # several z segments of the one-pass kernel
     outs = [torch.empty(dims, dtype=torch.float32, device="cuda") for _ in range(4)]
