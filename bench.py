@@ -13,7 +13,9 @@ by one all-gather), outputs written as fp32 grids.
 
 value      = 2 streams x 4 B x 2048^3 / step time   (GB/s of original fp32, whole job)
 e2e        = the same work from pinned HOST containers (H2D + validate + pipeline + D2H of every output)
-roofline   = the dominant kernel's algorithmic bytes / its CUDA-event time vs MEASURED_PEAKS hbm_gbs
+roofline   = the dominant op's SURVEY §8(d) algorithmic bytes (compressed bytes + 16 B/value of fp32 outputs;
+             intermediates do not count) / its CUDA-event time vs MEASURED_PEAKS hbm_gbs; per-kernel
+             times in roofline.kernels
 cpu_baseline = the reference path (oracle restatement: C codec + numpy) on a bounded sample, all host cores
 
 --impl reference runs that reference CPU path alone (rank 0) on a bounded sample of the same workload.
@@ -292,20 +294,35 @@ def run_ours(args):
     else:
         launches_per_step, launch_names = count_kernel_launches(step)
 
-    # ---- roofline of the dominant kernel -----------------------------------------------------------
+    # ---- roofline of the dominant operation ----------------------------------------------------------
+    # algorithmic bytes of "gradient (3 comps) + Laplacian, fp32, from the container" are
+    # the compressed bytes read once (payload + index + block means) + 16 B/value written; passes over
+    # intermediates (HSZP_ND's band-local prefix L) do not count.  An op = every kernel of one stream's
+    # step (HSZP_ND: band scans + ring z-sweeps; HSZX_ND: the one-pass kernel); the dominant op is the
+    # slower one.  Per-kernel numbers (with their own bytes) stay in `kernels`.
     peak, peak_src = measured_peak()
-    dom = max(kern, key=lambda k: kern[k]["ms"])
-    d = kern[dom]
-    per_launch_bytes = d["algo_bytes"] / d["launch_groups"]
-    per_launch_ms = d["ms"] / d["launch_groups"]
-    achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
-                "share_of_step": round(d["ms"] / recorded_steps / ms, 4),
-                "algo_bytes_per_launch": int(per_launch_bytes)}
+    ops = {}
+    for k in KINDS:
+        name = KIND_NAMES[k]
+        groups = [g for g in kern if g.endswith(":" + name)]
+        op_ms = sum(kern[g]["ms"] for g in groups) / recorded_steps
+        algo = container_bytes[k] + 16 * nz * N1 * N2
+        ops[name] = {"ms": op_ms, "algo_bytes": algo, "groups": groups}
+    dom = max(ops, key=lambda k: ops[k]["ms"])
+    d = ops[dom]
+    achieved = d["algo_bytes"] / (d["ms"] / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": f"op:{dom} ({' + '.join(d['groups'])})", "achieved": round(achieved, 1),
+                "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                "peak_source": peak_src, "share_of_step": round(d["ms"] / ms, 4),
+                "algo_bytes_per_launch": int(d["algo_bytes"]), "launch": "one step of the op (all its kernels)",
+                "other_ops": {o: {"achieved": round(v["algo_bytes"] / (v["ms"] / 1e3) / 1e9, 1),
+                                  "frac": round(v["algo_bytes"] / (v["ms"] / 1e3) / 1e9 / peak, 4),
+                                  "ms": round(v["ms"], 3)} for o, v in ops.items() if o != dom},
+                "kernels": {g: {"ms_per_step": round(v["ms"] / recorded_steps, 3),
+                                "gbs_own_bytes": round(v["gbs"], 1)} for g, v in kern.items()}}
     prof = measured_traffic(dom, (N0, N1, N2), world, args.window)
     if prof is not None:
-        roofline["traffic"] = prof["traffic_bytes_per_launch"]
+        roofline["traffic"] = prof["traffic_bytes_per_step"]
         roofline["traffic_source"] = prof["source"]
 
     # ---- e2e: host containers in, every output back to the host ------------------------------------------
@@ -399,19 +416,19 @@ def run_e2e(args, shards, pipes, outs, comm, n_total):
 CPU_SECONDS = 10.0
 
 
-def measured_traffic(group, dims, world, window):
-    """DRAM bytes per launch of a launch group from the committed ncu `--set full` capture
-    (profiles/r01_traffic.json), when it was taken on this exact launch shape (config 5, 1 GPU)."""
+def measured_traffic(op, dims, world, window):
+    """DRAM bytes per step of an op from the committed ncu `--set full` captures of its kernels
+    (profiles/r01_traffic.json), when they were taken on this exact shape (config 5, 1 GPU, W = 64)."""
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")
     try:
         with open(path) as f:
-            rec = json.load(f).get(group)
-    except (OSError, ValueError):
+            rec = json.load(f)["ops"].get(op)
+    except (OSError, ValueError, KeyError):
         return None
     if rec is None or tuple(dims) != (2048, 2048, 2048) or world != 1 or window != 64:
         return None
-    return {"traffic_bytes_per_launch": int(rec["traffic_bytes_per_launch"]),
-            "source": f"profiles/r01_traffic.json: ncu --set full of {rec['kernel']} ({rec['launch']})"}
+    return {"traffic_bytes_per_step": int(rec["traffic_bytes_per_step"]),
+            "source": "profiles/r01_traffic.json: ncu --set full of " + ", ".join(rec["kernels"])}
 
 
 def build_cpu_sample(field_dev, eps):
