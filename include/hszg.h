@@ -265,11 +265,12 @@ int hszg_zgrad_lap(const int32_t* q, int64_t n1, int64_t n2, int64_t zlo, int64_
  * lookahead != NULL: P2 of plane a+nout), the carry q[a-1] (NULL at the global first plane) and optionally the upper
  * neighbour's q plane, emit gradient + Laplacian of nout planes, accumulate stats and write
  * q[a+nout-1] to carry_out — q itself is never stored.  With band_off (hszg_band_scan output) P2 is
- * band-local: row y of plane z adds band_off[z][y / band_rows][:] (look_band_off: the lookahead's). */
+ * band-local: row y of plane z adds band_off[z][y / band_rows][:] (look_band_off: the lookahead's);
+ * p2_int16: P2 / lookahead hold those band-local prefixes as int16 (hszg_band_scan l_int16). */
 int hszg_zsweep_grad_lap(const int32_t* P2, int64_t n1, int64_t n2, int64_t nout, const int32_t* lookahead,
                          const int32_t* carry, const int32_t* q_upper, int32_t* carry_out, int64_t gz0, int64_t gN0,
                          double eps, float* const* out, HszgAcc* acc, const int32_t* band_off,
-                         const int32_t* look_band_off, int64_t band_rows, int exact, void* stream);
+                         const int32_t* look_band_off, int64_t band_rows, int p2_int16, int exact, void* stream);
 /* HSZX_ND one-pass decode + gradient + Laplacian + stats (8x8x8 blocks dividing the 3-D box, canonical,
  * max bit width <= 16): q never reaches memory.  The stream is a z-slab of a gN0-plane field whose
  * first plane is global plane gz0; halo_lo / halo_hi (optional, n1*n2 int32) are q of the planes just
@@ -292,9 +293,11 @@ int hszg_lorenzo_onepass(const HszgGeom* g, const HszgStream* s, const int32_t* 
  * P2 = L + band_off[z][y / band_rows].  strip_edges (optional): for 128-wide x strips s,
  * [z][s][y][0] = row prefix at x = 128s - 1 (0 for s = 0), [z][s][y][1] = at x = 128s + 128 (0 past
  * the row).  L: dims[0]*dims[1]*dims[2] int32; band_off: dims[0]*ceil(dims[1]/band_rows)*dims[2];
- * strip_edges: dims[0]*ceil(dims[2]/128)*E*2 int32 with E = dims[1] rounded up to even (+ 64 spare). */
-int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t band_rows, int32_t* L, int32_t* band_off,
-                   int32_t* strip_edges, void* stream, HszgErr* err);
+ * strip_edges: dims[0]*ceil(dims[2]/128)*E*2 int32 with E = dims[1] rounded up to even (+ 64 spare).
+ * l_int16: write L as int16 (n2 % 8 == 0); any value that does not fit sets *l_overflow = 1 (the
+ * caller then redoes the window with int32 L). */
+int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t band_rows, void* L, int32_t* band_off,
+                   int32_t* strip_edges, int l_int16, int32_t* l_overflow, void* stream, HszgErr* err);
 /* HSZP_ND decode fused with the in-row prefix (rows of whole chunks, 256 % (n2/32) == 0). */
 int hszg_decode_rowscan(const HszgGeom* g, const HszgStream* s, int32_t* out, void* stream, HszgErr* err);
 /* In-place inclusive scan along the middle axis of an int32 [A][M][L] view. */

@@ -148,12 +148,14 @@ _SIGS = {
     "hszg_decorrelate": [ctypes.POINTER(Geom), _P, _P, _P, _P, _SZ, _P, ctypes.POINTER(Err)],
     "hszg_acc_reset": [_P, _P],
     "hszg_zgrad_lap": [_P, _I64, _I64, _I64, _I64, _I64, _I64, _D, _P, _P, _P, _P, _I32, _P],
-    "hszg_zsweep_grad_lap": [_P, _I64, _I64, _I64, _P, _P, _P, _P, _I64, _I64, _D, _P, _P, _P, _P, _I64, _I32, _P],
+    "hszg_zsweep_grad_lap": [_P, _I64, _I64, _I64, _P, _P, _P, _P, _I64, _I64, _D, _P, _P, _P, _P, _I64, _I32, _I32,
+                             _P],
     "hszg_fused_blocks": [ctypes.POINTER(Geom), ctypes.POINTER(StreamDesc), _I64, _I64, _P, _P, _P, _P, _I64, _I32,
                           _P, ctypes.POINTER(Err)],
     "hszg_lorenzo_onepass": [ctypes.POINTER(Geom), ctypes.POINTER(StreamDesc), _P, _P, _P, _P, _I64, _I64, _P, _P,
                              _I32, _P, ctypes.POINTER(Err)],
-    "hszg_band_scan": [ctypes.POINTER(Geom), ctypes.POINTER(StreamDesc), _I64, _P, _P, _P, _P, ctypes.POINTER(Err)],
+    "hszg_band_scan": [ctypes.POINTER(Geom), ctypes.POINTER(StreamDesc), _I64, _P, _P, _P, _I32, _P, _P,
+                       ctypes.POINTER(Err)],
     "hszg_decode_rowscan": [ctypes.POINTER(Geom), ctypes.POINTER(StreamDesc), _P, _P, ctypes.POINTER(Err)],
     "hszg_col_scan": [_P, _I64, _I64, _I64, _P],
     "hszg_gen_noise": [_P, _I64, _I64, _P, ctypes.c_uint64, _P],

@@ -299,12 +299,13 @@ constexpr int BS_MAXG = 4;   // int4 column groups per thread: n2 <= 4 * 4 * TIL
 constexpr int SE_W = 128;    // strip width of the strip-edge table (the one-pass HSZP_ND kernel's x tile)
 
 
-template <bool Edges>
+template <bool Edges, bool L16>
 __global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __restrict__ payload, uint64_t len,
                                                           const uint64_t* __restrict__ offsets, int64_t n_chunks,
-                                                          int n1, int n2, int BR, int32_t* __restrict__ L,
+                                                          int n1, int n2, int BR, void* __restrict__ L,
                                                           int32_t* __restrict__ A, int32_t* __restrict__ EF,
-                                                          uint32_t sbytes) {
+                                                          int32_t* __restrict__ l_ovf, uint32_t sbytes) {
+    bool ovf = false;                        // an int16 L value did not fit
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint32_t s_off[TILE_CHUNKS];
     __shared__ uint32_t s_wt[TILE_CHUNKS / 32];
@@ -385,7 +386,8 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __rest
         const int nstrips = (n2 + SE_W - 1) / SE_W;
         for (int rr = 0; rr < nr; rr++) {
             const int y = r0 + rr;
-            int32_t* orow = L ? L + (z * n1 + y) * (int64_t)n2 : nullptr;
+            int32_t* orow = (L && !L16) ? static_cast<int32_t*>(L) + (z * n1 + y) * (int64_t)n2 : nullptr;
+            int16_t* orow16 = (L && L16) ? static_cast<int16_t*>(L) + (z * n1 + y) * (int64_t)n2 : nullptr;
 #pragma unroll
             for (int k = 0; k < BS_MAXG; k++) {
                 const int gi = threadIdx.x + k * TILE_CHUNKS;
@@ -395,6 +397,13 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __rest
                     const int4 rv = add4u(v, s_off[ch]);          // row prefix R at x = 4gi .. 4gi+3
                     ysum[k] = add4(ysum[k], rv);
                     if (orow) *reinterpret_cast<int4*>(orow + 4 * gi) = ysum[k];
+                    if (orow16) {
+                        const int4 v4 = ysum[k];
+                        ovf |= (v4.x != (int16_t)v4.x) | (v4.y != (int16_t)v4.y) | (v4.z != (int16_t)v4.z) |
+                               (v4.w != (int16_t)v4.w);
+                        *reinterpret_cast<short4*>(orow16 + 4 * gi) =
+                            make_short4((short)v4.x, (short)v4.y, (short)v4.z, (short)v4.w);
+                    }
                     if (Edges) {                                  // strip edges: E[s] = R(128s-1), F[s] = R(128s+128)
                         const int xg = 4 * gi;
                         const int64_t n1e = ((int64_t)n1 + 1) & ~(int64_t)1;   // even rows per strip block
@@ -421,6 +430,7 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __rest
         const int gi = threadIdx.x + k * TILE_CHUNKS;
         if (gi < ng) *reinterpret_cast<int4*>(arow + 4 * gi) = ysum[k];
     }
+    if (L16 && __any_sync(0xffffffffu, ovf) && (threadIdx.x & 31) == 0) atomicOr(l_ovf, 1);
 }
 
 // A[z][b][:] band totals -> exclusive prefix over b (one thread per (plane, int4 column group));
@@ -487,14 +497,14 @@ namespace hszg {
 int launch_zsweep_ring(const int32_t* L, int64_t n1, int64_t n2, int64_t nout, const int32_t* lookahead,
                        const int32_t* carry, const int32_t* q_upper, int32_t* carry_out, int64_t gz0, int64_t gN0,
                        double eps, float* const* out, HszgAcc* acc, const int32_t* A, const int32_t* lookA,
-                       int64_t BR, int64_t nb, int exact, cudaStream_t st);
+                       int64_t BR, int64_t nb, int l16, int exact, cudaStream_t st);
 }
 
 extern "C" int hszg_zsweep_grad_lap(const int32_t* P2, int64_t n1, int64_t n2, int64_t nout, const int32_t* lookahead,
                                     const int32_t* carry, const int32_t* q_upper, int32_t* carry_out, int64_t gz0,
                                     int64_t gN0, double eps, float* const* out, HszgAcc* acc,
                                     const int32_t* band_off, const int32_t* look_band_off, int64_t band_rows,
-                                    int exact, void* stream) {
+                                    int p2_int16, int exact, void* stream) {
     if (n2 % 4 || !al16(P2) || !al16(out[0]) || !al16(out[1]) || !al16(out[2]) || !al16(out[3]) || n1 > 65535 ||
         (carry && !al16(carry)) || (q_upper && !al16(q_upper)) || (carry_out && !al16(carry_out)) ||
         (band_off && (band_rows < 1 || !al16(band_off) || (lookahead && (!look_band_off || !al16(look_band_off))))))
@@ -504,26 +514,28 @@ extern "C" int hszg_zsweep_grad_lap(const int32_t* P2, int64_t n1, int64_t n2, i
     dim3 grid((unsigned)((n2 / 4 + ZG_THREADS - 1) / ZG_THREADS), (unsigned)n1);
     static const char* zmode = getenv("HSZG_ZSWEEP");       // 'c': per-thread-column kernel (A/B runs)
     if (band_off && band_rows % 16 == 0 && !(zmode && zmode[0] == 'c') && al16(lookahead) &&
-        al16(look_band_off)) {
+        al16(look_band_off) && (!p2_int16 || n2 % 8 == 0)) {
         return launch_zsweep_ring(P2, n1, n2, nout, lookahead, carry, q_upper, carry_out, gz0, gN0, eps, out, acc,
-                                  band_off, look_band_off, band_rows, nb, exact, as_stream(stream))
+                                  band_off, look_band_off, band_rows, nb, p2_int16, exact, as_stream(stream))
                    ? HSZG_CUDA
                    : HSZG_OK;
     }
+    if (p2_int16) return HSZG_INVALID_ARG;                   // int16 band-local prefixes: ring sweep only
     (exact ? k_zsweep<true> : k_zsweep<false>)<<<grid, ZG_THREADS, 0, as_stream(stream)>>>(P2, n1, n2, nout, lookahead, carry, q_upper, carry_out,
                                                          gz0, gN0, eps, 2.0 * eps, out[0], out[1], out[2], out[3],
                                                          acc, band_off, look_band_off, band_rows, nb);
     return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
 }
 
-extern "C" int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t band_rows, int32_t* L, int32_t* A,
-                              int32_t* strip_edges, void* stream, HszgErr* err) {
+extern "C" int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t band_rows, void* L, int32_t* A,
+                              int32_t* strip_edges, int l_int16, int32_t* l_overflow, void* stream, HszgErr* err) {
     err->status = HSZG_OK;
     const int64_t n1 = g->dims[1], n2 = g->dims[2], np = g->dims[0];
     const int64_t cpr = n2 / kChunkCap;
     if (g->kind != HSZG_HSZP_ND || g->ndims != 3 || !s->canonical || n2 % kChunkCap || cpr < 1 ||
         TILE_CHUNKS % cpr || n2 > 4 * BS_MAXG * TILE_CHUNKS || band_rows < 1 || n1 > INT32_MAX || np > 65535 ||
-        !al16(L) || !al16(A) || !al16(s->payload) || (!L && !strip_edges)) {
+        !al16(L) || !al16(A) || !al16(s->payload) || (!L && !strip_edges) ||
+        (l_int16 && (!l_overflow || strip_edges || n2 % 8))) {
         err->status = HSZG_INVALID_ARG;
         snprintf(err->message, sizeof(err->message),
                  "band_scan needs a canonical 3-D HSZP_ND stream with whole-chunk rows (n2 %% 32 == 0, "
@@ -534,16 +546,23 @@ extern "C" int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t ba
     const int64_t nb = (n1 + band_rows - 1) / band_rows;
     const uint32_t sbytes = (uint32_t)((stage_bytes(s->max_bitwidth) + 15) / 16 * 16);
     const size_t smem = kFastTileBytes + 2 * (size_t)sbytes + 16;
+    const dim3 grid((unsigned)nb, (unsigned)np);
+    cudaStream_t st = as_stream(stream);
     if (strip_edges) {
-        allow_smem(k_band_scan<true>, smem);
-        k_band_scan<true><<<dim3((unsigned)nb, (unsigned)np), TILE_CHUNKS, smem, as_stream(stream)>>>(
-            s->payload, s->payload_len, s->offsets, g->n_chunks, (int)n1, (int)n2, (int)band_rows, L, A, strip_edges,
-            sbytes);
+        allow_smem(k_band_scan<true, false>, smem);
+        k_band_scan<true, false><<<grid, TILE_CHUNKS, smem, st>>>(s->payload, s->payload_len, s->offsets,
+                                                                  g->n_chunks, (int)n1, (int)n2, (int)band_rows, L,
+                                                                  A, strip_edges, nullptr, sbytes);
+    } else if (l_int16) {
+        allow_smem(k_band_scan<false, true>, smem);
+        k_band_scan<false, true><<<grid, TILE_CHUNKS, smem, st>>>(s->payload, s->payload_len, s->offsets,
+                                                                  g->n_chunks, (int)n1, (int)n2, (int)band_rows, L,
+                                                                  A, nullptr, l_overflow, sbytes);
     } else {
-        allow_smem(k_band_scan<false>, smem);
-        k_band_scan<false><<<dim3((unsigned)nb, (unsigned)np), TILE_CHUNKS, smem, as_stream(stream)>>>(
-            s->payload, s->payload_len, s->offsets, g->n_chunks, (int)n1, (int)n2, (int)band_rows, L, A, nullptr,
-            sbytes);
+        allow_smem(k_band_scan<false, false>, smem);
+        k_band_scan<false, false><<<grid, TILE_CHUNKS, smem, st>>>(s->payload, s->payload_len, s->offsets,
+                                                                   g->n_chunks, (int)n1, (int)n2, (int)band_rows, L,
+                                                                   A, nullptr, nullptr, sbytes);
     }
     const int64_t threads = np * (n2 / 4);
     k_band_prefix<<<(unsigned)((threads + 255) / 256), 256, 0, as_stream(stream)>>>(A, (int)nb, n2, np);

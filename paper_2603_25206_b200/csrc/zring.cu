@@ -27,14 +27,17 @@ constexpr int ZR_RW = 148;                  // q ring row words (odd 16-B stride
 constexpr int ZR_PLANE = ZR_ROWS * ZR_RW;
 constexpr int ZR_NPL = 4;                   // q planes in the ring
 constexpr int ZR_D = 4;                     // staged P2 planes in flight
-constexpr int ZR_SW = ZR_TX + 8;            // staged row: x0-4 .. x0+132
+constexpr int ZR_SW = ZR_TX + 8;            // staged int32 row: x0-4 .. x0+132
+constexpr int ZR_SW16 = ZR_TX + 16;         // staged int16 row: x0-8 .. x0+136 (16-B aligned ends)
 constexpr int ZR_SROWS = ZR_ROWS + 3;       // 18 L rows + band-offset rows (above, tile, below)
-constexpr int ZR_SPLANE = ZR_SROWS * ZR_SW;
-constexpr size_t ZR_SMEM = (size_t)(ZR_NPL * ZR_PLANE + ZR_D * ZR_SPLANE) * 4;
+// staging slot bytes: 18 L rows (int32 or int16) + 3 int32 band-offset rows
+__host__ __device__ constexpr int zr_lrow_bytes(bool l16) { return l16 ? ZR_SW16 * 2 : ZR_SW * 4; }
+__host__ __device__ constexpr int zr_slot_bytes(bool l16) { return ZR_ROWS * zr_lrow_bytes(l16) + 3 * ZR_SW * 4; }
+constexpr size_t zr_smem(bool l16) { return (size_t)ZR_NPL * ZR_PLANE * 4 + (size_t)ZR_D * zr_slot_bytes(l16); }
 
 struct ZrArgs {
-    const int32_t* L;
-    const int32_t* lookahead;
+    const void* L;                          // band-local 2-D prefixes, int32 or (L16) int16
+    const void* lookahead;
     const int32_t* carry;
     const int32_t* q_upper;
     int32_t* carry_out;
@@ -49,11 +52,12 @@ struct ZrArgs {
     HszgAcc* acc;
 };
 
-template <bool Exact>
+template <bool Exact, bool L16>
 __global__ void __launch_bounds__(ZR_T, 2) k_zsweep_ring(ZrArgs a) {
     extern __shared__ __align__(128) int32_t zsm[];
     int32_t* Q = zsm;                                     // [ZR_NPL][ZR_ROWS][ZR_RW]
-    int32_t* S = zsm + ZR_NPL * ZR_PLANE;                 // [ZR_D][ZR_SROWS][ZR_SW]
+    uint8_t* S = reinterpret_cast<uint8_t*>(zsm + ZR_NPL * ZR_PLANE);   // [ZR_D][slot]
+    constexpr int LB = zr_lrow_bytes(L16), SLOT = zr_slot_bytes(L16);
     __shared__ __align__(8) uint64_t s_full[ZR_D], s_empty[ZR_D], q_full[ZR_NPL], q_empty[ZR_NPL];
     const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
     const int64_t x0 = (int64_t)blockIdx.x * ZR_TX, y0 = (int64_t)blockIdx.y * ZR_TY;
@@ -67,8 +71,7 @@ __global__ void __launch_bounds__(ZR_T, 2) k_zsweep_ring(ZrArgs a) {
     const bool has_look = a.lookahead != nullptr && a.q_upper == nullptr;
     const int64_t nst = nout + (has_look ? 1 : 0);         // staged planes
 
-    for (int i = threadIdx.x; i < (ZR_NPL * ZR_PLANE + ZR_D * ZR_SPLANE) / 4; i += ZR_T)
-        reinterpret_cast<int4*>(zsm)[i] = make_int4(0, 0, 0, 0);
+    for (int i = threadIdx.x; i < (int)(zr_smem(L16) / 16); i += ZR_T) reinterpret_cast<int4*>(zsm)[i] = make_int4(0, 0, 0, 0);
     if (threadIdx.x == 0) {
         for (int i = 0; i < ZR_D; i++) {
             mbar_init(&s_full[i], 1);
@@ -85,20 +88,31 @@ __global__ void __launch_bounds__(ZR_T, 2) k_zsweep_ring(ZrArgs a) {
     if (wp == 0) {
         // ================================ loader ================================
         const uint32_t rbytes = (uint32_t)(xe - xs) * 4;
+        const int64_t xs16 = x0 >= 8 ? x0 - 8 : 0;
+        const int64_t xe16 = x0 + ZR_TX + 8 < n2 ? x0 + ZR_TX + 8 : n2;
         const int64_t y = y0 - 1 + lane;                  // lanes 0..17: L rows; 18..20: band rows
         bool ok;
         int64_t row_off;
+        uint32_t bytes, dst_off;
         if (lane < ZR_ROWS) {
             ok = y >= 0 && y < n1;
-            row_off = y * n2 + xs;
+            row_off = y * n2 + (L16 ? xs16 : xs);
+            bytes = L16 ? (uint32_t)(xe16 - xs16) * 2 : rbytes;
+            dst_off = lane * LB + (L16 ? (uint32_t)(xs16 - (x0 - 8)) * 2 : (uint32_t)scol * 4);
         } else if (lane < ZR_SROWS) {
             ok = band[lane - ZR_ROWS] >= 0;
             row_off = band[lane - ZR_ROWS] * n2 + xs;
+            bytes = rbytes;
+            dst_off = ZR_ROWS * LB + (lane - ZR_ROWS) * ZR_SW * 4 + (uint32_t)scol * 4;
         } else {
             ok = false;
             row_off = 0;
+            bytes = 0;
+            dst_off = 0;
         }
-        const uint32_t tx = (uint32_t)__popc(__ballot_sync(0xffffffffu, ok)) * rbytes;
+        uint32_t tx = ok ? bytes : 0;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) tx += __shfl_xor_sync(0xffffffffu, tx, d);
         for (int64_t zz = 0; zz < nst; zz++) {
             const int slot = (int)(zz % ZR_D);
             const int64_t u = zz / ZR_D;
@@ -109,9 +123,14 @@ __global__ void __launch_bounds__(ZR_T, 2) k_zsweep_ring(ZrArgs a) {
             }
             __syncwarp();
             if (ok) {
-                const int32_t* src = lane < ZR_ROWS ? (zz < nout ? a.L + zz * plane : a.lookahead)
-                                                    : (zz < nout ? a.A + zz * a.nb * n2 : a.lookA);
-                tma_load_1d(S + (slot * ZR_SROWS + lane) * ZR_SW + scol, src + row_off, rbytes, &s_full[slot]);
+                const void* src;
+                if (lane < ZR_ROWS) {
+                    if (L16) src = static_cast<const int16_t*>(zz < nout ? a.L : a.lookahead) + (zz < nout ? zz * plane : 0) + row_off;
+                    else src = static_cast<const int32_t*>(zz < nout ? a.L : a.lookahead) + (zz < nout ? zz * plane : 0) + row_off;
+                } else {
+                    src = (zz < nout ? a.A + zz * a.nb * n2 : a.lookA) + row_off;
+                }
+                tma_load_1d(S + (size_t)slot * SLOT + dst_off, src, bytes, &s_full[slot]);
             }
         }
         return;
@@ -120,7 +139,7 @@ __global__ void __launch_bounds__(ZR_T, 2) k_zsweep_ring(ZrArgs a) {
     if (wp < 1 + ZR_AT / 32) {
         // ================================ adders ================================
         const int at = threadIdx.x - 32;
-        constexpr int C4 = ZR_SW / 4;                      // int4 columns of a staged row
+        constexpr int C4 = ZR_SW / 4;                      // int4 columns x0-4 .. x0+132
         // plane a-1 (the carry) into ring slot 0, planes zz = 0..nout into slot (zz + 1) % NPL
         auto copy_plane = [&](const int32_t* g, int32_t* P) {      // g: a q plane in HBM, or null
             for (int i = at; i < ZR_ROWS * C4; i += ZR_AT) {
@@ -144,12 +163,20 @@ __global__ void __launch_bounds__(ZR_T, 2) k_zsweep_ring(ZrArgs a) {
                 const int slot = (int)(zz % ZR_D);
                 mbar_wait(&s_full[slot], (uint32_t)((zz / ZR_D) & 1));
                 const int32_t* Pprev = Q + (int)(zz % ZR_NPL) * ZR_PLANE;
-                const int32_t* St = S + slot * ZR_SPLANE;
+                const uint8_t* St = S + (size_t)slot * SLOT;
+                const int32_t* Sa = reinterpret_cast<const int32_t*>(St + ZR_ROWS * LB);
                 for (int i = at; i < ZR_ROWS * C4; i += ZR_AT) {
                     const int r = i / C4, j = 4 * (i - r * C4);
-                    const int br = ZR_ROWS + (r == 0 ? 0 : (r == ZR_ROWS - 1 ? 2 : 1));
-                    const int4 l = *reinterpret_cast<const int4*>(St + r * ZR_SW + j);
-                    const int4 b = *reinterpret_cast<const int4*>(St + br * ZR_SW + j);
+                    const int br = r == 0 ? 0 : (r == ZR_ROWS - 1 ? 2 : 1);
+                    int4 l;
+                    if (L16) {
+                        const short4 h = *reinterpret_cast<const short4*>(
+                            reinterpret_cast<const int16_t*>(St + r * LB) + j + 4);
+                        l = make_int4(h.x, h.y, h.z, h.w);
+                    } else {
+                        l = *reinterpret_cast<const int4*>(reinterpret_cast<const int32_t*>(St + r * LB) + j);
+                    }
+                    const int4 b = *reinterpret_cast<const int4*>(Sa + br * ZR_SW + j);
                     const int4 q = *reinterpret_cast<const int4*>(Pprev + r * ZR_RW + ZR_X0 - 4 + j);
                     *reinterpret_cast<int4*>(P + r * ZR_RW + ZR_X0 - 4 + j) = add4(q, add4(l, b));
                 }
@@ -224,7 +251,7 @@ __global__ void __launch_bounds__(ZR_T, 2) k_zsweep_ring(ZrArgs a) {
 int launch_zsweep_ring(const int32_t* L, int64_t n1, int64_t n2, int64_t nout, const int32_t* lookahead,
                        const int32_t* carry, const int32_t* q_upper, int32_t* carry_out, int64_t gz0, int64_t gN0,
                        double eps, float* const* out, HszgAcc* acc, const int32_t* A, const int32_t* lookA,
-                       int64_t BR, int64_t nb, int exact, cudaStream_t st) {
+                       int64_t BR, int64_t nb, int l16, int exact, cudaStream_t st) {
     ZrArgs a;
     a.L = L;
     a.lookahead = lookahead;
@@ -247,13 +274,19 @@ int launch_zsweep_ring(const int32_t* L, int64_t n1, int64_t n2, int64_t nout, c
     a.o3 = out[3];
     a.acc = acc;
     dim3 grid((unsigned)((n2 + ZR_TX - 1) / ZR_TX), (unsigned)((n1 + ZR_TY - 1) / ZR_TY));
+#define ZR_LAUNCH(E, H)                                                   \
+    do {                                                                  \
+        allow_smem(k_zsweep_ring<E, H>, zr_smem(H));                      \
+        k_zsweep_ring<E, H><<<grid, ZR_T, zr_smem(H), st>>>(a);           \
+    } while (0)
     if (exact) {
-        allow_smem(k_zsweep_ring<true>, ZR_SMEM);
-        k_zsweep_ring<true><<<grid, ZR_T, ZR_SMEM, st>>>(a);
+        if (l16) ZR_LAUNCH(true, true);
+        else ZR_LAUNCH(true, false);
     } else {
-        allow_smem(k_zsweep_ring<false>, ZR_SMEM);
-        k_zsweep_ring<false><<<grid, ZR_T, ZR_SMEM, st>>>(a);
+        if (l16) ZR_LAUNCH(false, true);
+        else ZR_LAUNCH(false, false);
     }
+#undef ZR_LAUNCH
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 

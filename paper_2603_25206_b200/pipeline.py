@@ -398,6 +398,13 @@ class WindowPipeline:
             else:
                 self._fused_loop(outs)
             res = self._finish_stats(_prepared)
+            if self._l16_overflowed(_prepared):
+                # an int16 band-local prefix did not fit: this field needs int32 L (kept from now on)
+                self.l16 = False
+                self._pers_W = None
+                self._stage_boundary()
+                self._fused_loop(outs)
+                res = self._finish_stats(_prepared)
             if not self.exact_fp32 and not self._fast_valid(res, _prepared):
                 # the fast emitter needs |q| < 2^27 (FAST_QLIM, stencil.cuh): every q is some point's
                 # centre, so the exact min / max decide it; redo the pass with the exact emitter
@@ -409,6 +416,22 @@ class WindowPipeline:
                     self.exact_fp32 = False
             return res if stats else None
         return self._run_generic(outs, stats, _prepared)
+
+    # HSZP_ND two-pass: band-local prefixes L stored as int16 (half the intermediate traffic); a
+    # device flag reports any value that did not fit and the pass is redone with int32 L
+    l16 = True
+
+    def _l16_active(self) -> bool:
+        # int16 L feeds only the ring z-sweep (band rows a multiple of 16)
+        return bool(self.band_rows) and self.band_rows % 16 == 0 and self.l16 and self.sf.global_dims[2] % 8 == 0
+
+    def _l16_overflowed(self, _prepared) -> bool:
+        if not getattr(self, "_l16_used", False):
+            return False
+        flag = self.l16_ovf.clone()
+        if not _prepared:
+            self.comm.all_reduce(flag, "max")          # every rank redoes the pass together
+        return int(flag.item()) != 0
 
     def _fast_valid(self, res, _prepared) -> bool:
         lim = FAST_QLIM
@@ -435,7 +458,9 @@ class WindowPipeline:
         dev = _lib.device()
         one = self._one_pass_ok()
         nslots = 0 if one else 3
-        self.ring = [t.empty((self.W, n1, n2), dtype=t.int32, device=dev) for _ in range(nslots)]
+        self.band_rows = self._band_rows() if (self.sf.kind == HSZP_ND and not one) else 0
+        rtype = t.int16 if self._l16_active() else t.int32
+        self.ring = [t.empty((self.W, n1, n2), dtype=rtype, device=dev) for _ in range(nslots)]
         if one and self.sf.kind == HSZP_ND:
             nz = self.sf.nz
             self.lz_bands = t.empty((nz, -(-n1 // 16), n2), dtype=t.int32, device=dev)
@@ -443,10 +468,10 @@ class WindowPipeline:
         self.halo_buf = t.zeros((2, n1, n2), dtype=t.int32, device=dev)       # [lower, upper]
         self.carry_buf = t.zeros((3, n1, n2), dtype=t.int32, device=dev)      # [rank carry, ping, pong]
         self.acc = t.zeros(ACC_BYTES, dtype=t.uint8, device=dev)
-        self.band_rows = self._band_rows() if (self.sf.kind == HSZP_ND and not one) else 0
         if self.band_rows:
             nb = -(-n1 // self.band_rows)
             self.bands = [t.empty((self.W, nb, n2), dtype=t.int32, device=dev) for _ in range(nslots)]
+            self.l16_ovf = t.zeros(1, dtype=t.int32, device=dev)
         self._pers_W = self.W
         self._graph = None
 
@@ -522,7 +547,8 @@ class WindowPipeline:
             self.timer.begin("prepass")
         err = _lib.Err()
         _lib.call("hszg_band_scan", ctypes.byref(self.ds.geom), ctypes.byref(self.ds.desc), 16, None,
-                  _lib.ptr(self.lz_bands), _lib.ptr(self.lz_edges), _lib.stream_handle(), ctypes.byref(err), err=err)
+                  _lib.ptr(self.lz_bands), _lib.ptr(self.lz_edges), 0, None, _lib.stream_handle(), ctypes.byref(err),
+                  err=err)
         if self.timer:
             self.timer.end("prepass", self._range_bytes(0, sf.nz) + self.lz_bands.numel() * 4 + self.lz_edges.numel() * 4)
             self.timer.begin("fused")
@@ -616,6 +642,10 @@ class WindowPipeline:
         nw = len(wins)
         ns = len(ring)
         br = self.band_rows
+        l16 = bool(br) and ring[0].dtype == t.int16
+        self._l16_used = l16
+        if l16:
+            self.l16_ovf.zero_()
         main = t.cuda.current_stream()
         side = self._side_stream() if (self.overlap and ns >= 3) else main
         dec_done = [t.cuda.Event() for _ in range(nw)]
@@ -629,8 +659,8 @@ class WindowPipeline:
             err = _lib.Err()
             if br:
                 _lib.call("hszg_band_scan", ctypes.byref(sub.geom), ctypes.byref(sub.desc), br,
-                          _lib.ptr(ring[k % ns]), _lib.ptr(self.bands[k % ns]), None, _lib.stream_handle(),
-                          ctypes.byref(err), err=err)
+                          _lib.ptr(ring[k % ns]), _lib.ptr(self.bands[k % ns]), None, int(l16),
+                          _lib.ptr(self.l16_ovf) if l16 else None, _lib.stream_handle(), ctypes.byref(err), err=err)
             else:
                 _lib.call("hszg_decode_rowscan", ctypes.byref(sub.geom), ctypes.byref(sub.desc),
                           _lib.ptr(ring[k % ns]), _lib.stream_handle(), ctypes.byref(err), err=err)
@@ -671,7 +701,7 @@ class WindowPipeline:
                       sf.global_dims[0], ctypes.c_double(sf.eps), self._outs_arr(outs, a, b), _lib.ptr(self.acc),
                       _lib.ptr(self.bands[k % ns]) if br else None,
                       _lib.ptr(self.bands[(k + 1) % ns]) if (br and look is not None) else None, br,
-                      int(self.exact_fp32), _lib.stream_handle())
+                      int(l16), int(self.exact_fp32), _lib.stream_handle())
             if self.timer:
                 self.timer.end("stencil", (4 + 16) * (b - a) * self.plane)
             sweep_done[k].record(main)
