@@ -643,6 +643,7 @@ class WindowPipeline:
         ns = len(ring)
         br = self.band_rows
         l16 = bool(br) and ring[0].dtype == t.int16
+        lsz = 2 if l16 else 4                            # bytes per value of the L intermediate
         self._l16_used = l16
         if l16:
             self.l16_ovf.zero_()
@@ -666,7 +667,7 @@ class WindowPipeline:
                           _lib.ptr(ring[k % ns]), _lib.stream_handle(), ctypes.byref(err), err=err)
                 _lib.call("hszg_col_scan", _lib.ptr(ring[k % ns]), b - a, n1, n2, _lib.stream_handle())
             if self.timer:
-                self.timer.end("reconstruct", self._range_bytes(a, b) + 4 * (b - a) * self.plane)
+                self.timer.end("reconstruct", self._range_bytes(a, b) + lsz * (b - a) * self.plane)
 
         issued = 0
 
@@ -703,7 +704,7 @@ class WindowPipeline:
                       _lib.ptr(self.bands[(k + 1) % ns]) if (br and look is not None) else None, br,
                       int(l16), int(self.exact_fp32), _lib.stream_handle())
             if self.timer:
-                self.timer.end("stencil", (4 + 16) * (b - a) * self.plane)
+                self.timer.end("stencil", (lsz + 16) * (b - a) * self.plane)
             sweep_done[k].record(main)
             carry = out_carry
         if side is not main:
