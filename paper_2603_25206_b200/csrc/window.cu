@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __rest
                                                           int n1, int n2, int BR, void* __restrict__ L,
                                                           int32_t* __restrict__ A, int32_t* __restrict__ EF,
                                                           int32_t* __restrict__ l_ovf, uint32_t sbytes) {
-    bool ovf = false;                        // an int16 L value did not fit
+    int32_t lo16 = 0, hi16 = 0;              // range of the values stored as int16
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint32_t s_off[TILE_CHUNKS];
     __shared__ uint32_t s_wt[TILE_CHUNKS / 32];
@@ -399,10 +399,12 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __rest
                     if (orow) *reinterpret_cast<int4*>(orow + 4 * gi) = ysum[k];
                     if (orow16) {
                         const int4 v4 = ysum[k];
-                        ovf |= (v4.x != (int16_t)v4.x) | (v4.y != (int16_t)v4.y) | (v4.z != (int16_t)v4.z) |
-                               (v4.w != (int16_t)v4.w);
-                        *reinterpret_cast<short4*>(orow16 + 4 * gi) =
-                            make_short4((short)v4.x, (short)v4.y, (short)v4.z, (short)v4.w);
+                        lo16 = min(lo16, min(min(v4.x, v4.y), min(v4.z, v4.w)));   // range, checked once
+                        hi16 = max(hi16, max(max(v4.x, v4.y), max(v4.z, v4.w)));
+                        uint2 pk;                                                  // low halves, 2 PRMTs
+                        pk.x = __byte_perm((uint32_t)v4.x, (uint32_t)v4.y, 0x5410);
+                        pk.y = __byte_perm((uint32_t)v4.z, (uint32_t)v4.w, 0x5410);
+                        *reinterpret_cast<uint2*>(orow16 + 4 * gi) = pk;
                     }
                     if (Edges) {                                  // strip edges: E[s] = R(128s-1), F[s] = R(128s+128)
                         const int xg = 4 * gi;
@@ -430,6 +432,7 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __rest
         const int gi = threadIdx.x + k * TILE_CHUNKS;
         if (gi < ng) *reinterpret_cast<int4*>(arow + 4 * gi) = ysum[k];
     }
+    const bool ovf = lo16 < INT16_MIN || hi16 > INT16_MAX;   // an int16 L value did not fit
     if (L16 && __any_sync(0xffffffffu, ovf) && (threadIdx.x & 31) == 0) atomicOr(l_ovf, 1);
 }
 

@@ -95,19 +95,22 @@ class Comm:
             return None, None
         import torch
 
-        reqs = []
+        ops = []
         from_lower = from_upper = None
         r, w = self.rank, self.world
         like_h = self._host(like)
+        P2P = self.dist.P2POp
         if r > 0:
             from_lower = torch.empty_like(like_h)
-            reqs.append(self.dist.irecv(from_lower, r - 1, group=self.group))
-            reqs.append(self.dist.isend(self._host(to_lower.contiguous()), r - 1, group=self.group))
+            ops.append(P2P(self.dist.irecv, from_lower, r - 1, group=self.group))
+            ops.append(P2P(self.dist.isend, self._host(to_lower.contiguous()), r - 1, group=self.group))
         if r < w - 1:
             from_upper = torch.empty_like(like_h)
-            reqs.append(self.dist.irecv(from_upper, r + 1, group=self.group))
-            reqs.append(self.dist.isend(self._host(to_upper.contiguous()), r + 1, group=self.group))
-        for q in reqs:
+            ops.append(P2P(self.dist.irecv, from_upper, r + 1, group=self.group))
+            ops.append(P2P(self.dist.isend, self._host(to_upper.contiguous()), r + 1, group=self.group))
+        # one grouped launch (ncclGroupStart/End under NCCL): separately issued send/recv pairs
+        # whose both ends start with a recv would wait on each other
+        for q in self.dist.batch_isend_irecv(ops) if ops else []:
             q.wait()
         if like_h is not like:
             from_lower = None if from_lower is None else from_lower.to(like.device)
