@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--no-graph", action="store_true", help="launch the window loop eagerly instead of a CUDA graph")
     ap.add_argument("--no-one-pass", action="store_true", help="HSZX_ND: two-pass (decode, then stencil) windows")
     ap.add_argument("--hszp-one-pass", action="store_true", help="HSZP_ND: the one-pass kernel (lorenzo.cu)")
+    ap.add_argument("--overlap", type=int, default=None, help="HSZP_ND: band scans on a side stream (1) or not (0)")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -247,6 +248,8 @@ def run_ours(args):
         p.exact_fp32 = args.exact_fp32
         p.one_pass = not args.no_one_pass
         p.lorenzo_one_pass = args.hszp_one_pass
+        if args.overlap is not None:
+            p.overlap = bool(args.overlap)
     container_bytes = {k: shards[k].ds.nbytes() for k in KINDS}
     setup_s = time.time() - t_setup
 
