@@ -34,7 +34,8 @@ class RegionStats:
     region: tuple
     grid: tuple          # regions per axis
     s1: np.ndarray       # int64
-    s2: np.ndarray       # Python ints (object) — exact int128
+    s2_lo: np.ndarray    # uint64 low / int64 high halves of the exact int128 S2 (see .s2)
+    s2_hi: np.ndarray
     qmin: np.ndarray     # int32
     qmax: np.ndarray     # int32
     size: np.ndarray     # int64
@@ -44,6 +45,16 @@ class RegionStats:
     vmax: np.ndarray     # float64 = qmax * 2eps
     threshold: float | None = None
     crossing_count: int | None = None
+
+    @property
+    def s2(self) -> np.ndarray:
+        """Exact S2 per region: int64 when every value fits, else Python ints (object)."""
+        hi = self.s2_hi.astype(np.int64)
+        lo = self.s2_lo.astype(np.uint64)
+        if not hi.any() and (lo < np.uint64(1 << 63)).all():
+            return lo.astype(np.int64).reshape(self.grid)
+        vals = [(int(h) << 64) | int(l) for h, l in zip(hi.ravel(), lo.ravel())]
+        return np.array(vals, dtype=object).reshape(self.grid)
 
 
 def _region_tuple(region, nd):
@@ -86,12 +97,10 @@ def region_stats(c: CompressedStream, region, stage: Stage = Stage.QUANTIZED,
     q = _quantized(c, stage)
     r = region_reduce_device(q, c.eps, region, float("nan") if tau is None else tau)
     g = r["grid"]
-    s2 = [(int(h) << 64) | (int(l) & 0xFFFFFFFFFFFFFFFF) for h, l in zip(r["s2hi"].cpu().numpy(),
-                                                                         r["s2lo"].cpu().numpy())]
     return RegionStats(
         region=r["region"], grid=g,
         s1=r["s1"].cpu().numpy().reshape(g),
-        s2=np.array(s2, dtype=object).reshape(g),
+        s2_lo=r["s2lo"].cpu().numpy().view(np.uint64).reshape(g), s2_hi=r["s2hi"].cpu().numpy().reshape(g),
         qmin=r["qmin"].cpu().numpy().reshape(g), qmax=r["qmax"].cpu().numpy().reshape(g),
         size=r["size"].cpu().numpy().reshape(g),
         mean=r["mean"].cpu().numpy().reshape(g), var=r["var"].cpu().numpy().reshape(g),
@@ -107,8 +116,9 @@ def region_minmax(c: CompressedStream, region, stage: Stage = Stage.QUANTIZED):
 
 
 def threshold_count(c: CompressedStream, region, tau: float, stage: Stage = Stage.QUANTIZED) -> int:
-    """N4: number of regions with min_r < tau <= max_r."""
-    return region_stats(c, region, stage, tau).crossing_count
+    """N4: number of regions with min_r < tau <= max_r (only the count leaves the device)."""
+    q = _quantized(c, stage)
+    return int(region_reduce_device(q, c.eps, region, float(tau))["count"].item())
 
 
 def gradient_magnitude(c: CompressedStream, stage: Stage = Stage.QUANTIZED, out: str = "numpy", out_dtype=None):

@@ -244,7 +244,7 @@ extern "C" int hszg_decorrelate(const HszgGeom* g, const int32_t* q, int32_t* p,
                 break;
             }
         }
-        if (cudaGetLastError() != cudaSuccess) return hszg_set_cuda_error(err, cudaGetLastError(), "decorrelate");
+        { const cudaError_t e_ = cudaGetLastError(); if (e_ != cudaSuccess) return hszg_set_cuda_error(err, e_, "decorrelate"); }
     }
     unsigned int h = 0;
     int r = read_flags(flags, &h, st, err);

@@ -392,6 +392,6 @@ extern "C" int hszg_fused_blocks(const HszgGeom* g, const HszgStream* s, int64_t
         if (npl == 8) launch_fused_blocks<false, 8>(a, grid, smem, bb, st);
         else launch_fused_blocks<false, 4>(a, grid, smem, bb, st);
     }
-    if (cudaGetLastError() != cudaSuccess) return hszg_set_cuda_error(err, cudaGetLastError(), "fused_blocks");
+    { const cudaError_t e_ = cudaGetLastError(); if (e_ != cudaSuccess) return hszg_set_cuda_error(err, e_, "fused_blocks"); }
     return HSZG_OK;
 }

@@ -431,6 +431,6 @@ extern "C" int hszg_lorenzo_onepass(const HszgGeom* g, const HszgStream* s, cons
         allow_smem(k_lorenzo_ring<false>, smem);
         k_lorenzo_ring<false><<<grid, LR_T, smem, st>>>(a);
     }
-    if (cudaGetLastError() != cudaSuccess) return hszg_set_cuda_error(err, cudaGetLastError(), "lorenzo_onepass");
+    { const cudaError_t e_ = cudaGetLastError(); if (e_ != cudaSuccess) return hszg_set_cuda_error(err, e_, "lorenzo_onepass"); }
     return HSZG_OK;
 }

@@ -482,7 +482,7 @@ extern "C" int hszg_reduce_stream(const HszgGeom* g, const HszgStream* s, int mo
             allow_smem(k_reduce_tiles<WeightedChunk>, smem),
             k_reduce_tiles<WeightedChunk><<<(unsigned)tiles, TILE_CHUNKS, smem, st>>>(
                 sg, s->payload, s->payload_len, s->offsets, s->metadata, partials);
-        if (cudaGetLastError() != cudaSuccess) return hszg_set_cuda_error(err, cudaGetLastError(), "reduce tiles");
+        { const cudaError_t e_ = cudaGetLastError(); if (e_ != cudaSuccess) return hszg_set_cuda_error(err, e_, "reduce tiles"); }
         return finalize(partials, tiles, out_dev, st);
     }
     // non-canonical: decode into the workspace tail, then reduce per chunk

@@ -10,6 +10,7 @@
 // bank-padded int32 value tile, which the epilogue consumes in stream order
 // with coalesced stores.
 #pragma once
+#include <cstdio>
 #include <mutex>
 #include <unordered_map>
 #include "common.cuh"
@@ -29,18 +30,23 @@ inline size_t tile_smem_bytes(int max_bw) {
     return (size_t)TILE_VALS * 4 + bytes + 16;
 }
 
-// Opt a tile kernel into > 48 KB of dynamic shared memory (wide bit widths need ~69 KB).  The
-// attribute is raised once per kernel to the largest size seen, so steady-state launches (and
-// launches under CUDA-graph capture) make no runtime call here.
+// Opt a tile kernel into more dynamic shared memory than the default 48 KB minus its static shared
+// memory (wide bit widths need ~69 KB).  The attribute is raised once per kernel to the largest
+// size seen, so steady-state launches (and launches under CUDA-graph capture) make no runtime call.
 inline void allow_smem_raw(const void* kernel, size_t bytes) {
     static std::mutex mu;
     static std::unordered_map<const void*, size_t> set;
-    if (bytes <= 48 * 1024) return;
+    if (bytes <= 32 * 1024) return;              // below every kernel's default limit (static < 16 KB)
     std::lock_guard<std::mutex> lock(mu);
     size_t& cur = set[kernel];
     if (bytes <= cur) return;
     const size_t want = bytes < 96 * 1024 ? 96 * 1024 : bytes;
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want);
+    const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want);
+    if (e != cudaSuccess) {
+        fprintf(stderr, "hszg: cudaFuncSetAttribute(%zu) failed: %s\n", want, cudaGetErrorString(e));
+        cudaGetLastError();
+        return;
+    }
     cur = want;
 }
 template <typename K>

@@ -569,7 +569,7 @@ extern "C" int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t ba
     }
     const int64_t threads = np * (n2 / 4);
     k_band_prefix<<<(unsigned)((threads + 255) / 256), 256, 0, as_stream(stream)>>>(A, (int)nb, n2, np);
-    if (cudaGetLastError() != cudaSuccess) return hszg_set_cuda_error(err, cudaGetLastError(), "band_scan");
+    { const cudaError_t e_ = cudaGetLastError(); if (e_ != cudaSuccess) return hszg_set_cuda_error(err, e_, "band_scan"); }
     return HSZG_OK;
 }
 
@@ -590,6 +590,6 @@ extern "C" int hszg_decode_rowscan(const HszgGeom* g, const HszgStream* s, int32
     allow_smem(k_tile_rowscan, smem);
     k_tile_rowscan<<<(unsigned)tiles, TILE_CHUNKS, smem, as_stream(stream)>>>(sg, s->payload, s->payload_len,
                                                                              s->offsets, (int)cpr, out);
-    if (cudaGetLastError() != cudaSuccess) return hszg_set_cuda_error(err, cudaGetLastError(), "decode_rowscan");
+    { const cudaError_t e_ = cudaGetLastError(); if (e_ != cudaSuccess) return hszg_set_cuda_error(err, e_, "decode_rowscan"); }
     return HSZG_OK;
 }

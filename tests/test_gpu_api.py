@@ -390,3 +390,21 @@ def test_config1_parity(H, kind):
     d = H.fields.compute_field_op(c, "derivative", H.h.Stage.QUANTIZED).components
     for a, b in zip(d, O.derivative_q(q, ref.eps)):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("kind", ALL)
+def test_stats_wide_bitwidths(H, kind):
+    """Bit widths ~13 put the tile kernels' shared memory just above the 48 KB default minus their
+    static shared memory (a launch failure once): config-4-like log-normal field, 64^3."""
+    from paper_2603_25206_b200 import synthetic
+
+    f = synthetic.config4_field(dims=(64, 64, 64))
+    c = H.h.compress(f, H.h.CompressorKind(kind), H.h.ErrorBound("rel", 1e-4))
+    oc = _oracle_of(c)
+    d = c.device().validate()
+    assert d.desc.max_bitwidth >= 12
+    for st in (H.h.Stage.DECORRELATED, H.h.Stage.QUANTIZED):
+        got = H.stats.compute_stat(c, "var", st).value
+        want = O.var_from_dq(O.stage3(oc), c.eps) if st == H.h.Stage.QUANTIZED or not c.kind.is_block_mean else None
+        if want is not None:
+            assert got == want, (kind, st)
