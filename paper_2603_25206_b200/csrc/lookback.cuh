@@ -72,6 +72,55 @@ __device__ __forceinline__ unsigned long long lookback_exclusive(const LBState& 
     return excl;
 }
 
+// Called by ALL 32 lanes of one warp of the tile: the same result, but the look-back inspects 32
+// predecessors per step (flags loaded in parallel, ballot for the nearest inclusive prefix, warp sum
+// of the aggregates before it) instead of walking them one at a time.
+__device__ __forceinline__ unsigned long long lookback_exclusive_warp(const LBState& st, int64_t tile,
+                                                                      unsigned long long agg) {
+    const int lane = threadIdx.x & 31;
+    volatile int* flag = st.flag;
+    volatile unsigned long long* vagg = st.agg;
+    volatile unsigned long long* vincl = st.incl;
+    if (tile == 0) {
+        if (lane == 0) {
+            vincl[0] = agg;
+            __threadfence();
+            flag[0] = 2;
+        }
+        return 0ull;
+    }
+    if (lane == 0) {
+        vagg[tile] = agg;
+        __threadfence();
+        flag[tile] = 1;
+    }
+    unsigned long long excl = 0;
+    int64_t p = tile - 1;
+    while (true) {
+        const int64_t idx = p - lane;
+        const int f = idx >= 0 ? flag[idx] : 2;          // before tile 0: an inclusive prefix of 0
+        const unsigned incl = __ballot_sync(0xffffffffu, f == 2);
+        const unsigned zero = __ballot_sync(0xffffffffu, f == 0);
+        const int k = incl ? __ffs(incl) - 1 : 31;      // nearest inclusive, else the whole window
+        const unsigned need = (2u << k) - 1u;            // lanes 0..k (k = 31: all)
+        if (zero & need) continue;                       // an aggregate in between is not out yet
+        __threadfence();
+        unsigned long long v = 0;
+        if (lane <= k && idx >= 0) v = (lane == k && incl) ? vincl[idx] : vagg[idx];
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+        excl += v;
+        if (incl) break;
+        p -= 32;
+    }
+    if (lane == 0) {
+        vincl[tile] = excl + agg;
+        __threadfence();
+        flag[tile] = 2;
+    }
+    return excl;
+}
+
 // block-wide exclusive scan of one u64 per thread; returns exclusive value, *total = block sum
 __device__ __forceinline__ unsigned long long block_exclusive_u64(unsigned long long v, unsigned long long* total) {
     __shared__ unsigned long long warp_tot[32];
@@ -121,7 +170,10 @@ static __global__ void __launch_bounds__(SCAN_THREADS) k_scan_u64(const uint64_t
     }
     unsigned long long tot;
     const unsigned long long texcl = block_exclusive_u64(run, &tot);
-    if (threadIdx.x == 0) s_prefix = lookback_exclusive(st, tile, tot);
+    if (threadIdx.x < 32) {
+        const unsigned long long e = lookback_exclusive_warp(st, tile, tot);
+        if (threadIdx.x == 0) s_prefix = e;
+    }
     __syncthreads();
     unsigned long long acc = s_prefix + texcl;
 #pragma unroll

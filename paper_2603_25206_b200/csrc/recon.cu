@@ -13,6 +13,9 @@
 #include "tile.cuh"
 #include "lookback.cuh"
 
+extern "C" int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t band_rows, void* L, int32_t* A,
+                              int32_t* strip_edges, int l_int16, int32_t* l_overflow, void* stream, HszgErr* err);
+
 namespace hszg {
 
 template <typename OutT>
@@ -273,7 +276,10 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_tile_scan(SegGeo sg, const uint
     }
     unsigned long long tot;
     const unsigned long long excl = block_exclusive_u64((unsigned long long)run, &tot);
-    if (threadIdx.x == 0) s_prefix = lookback_exclusive(st, tile, tot & 0xffffffffull);
+    if (threadIdx.x < 32) {
+        const unsigned long long e = lookback_exclusive_warp(st, tile, tot & 0xffffffffull);
+        if (threadIdx.x == 0) s_prefix = e;
+    }
     __syncthreads();
     const uint32_t add = (uint32_t)(s_prefix + excl);
     for (int j = 0; j < count; j++) vals[pad_idx(local + j)] = (int32_t)((uint32_t)vals[pad_idx(local + j)] + add);
@@ -371,7 +377,10 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_i32(const int32_t* in, in
     }
     unsigned long long tot;
     const unsigned long long ex = block_exclusive_u64(run, &tot);
-    if (threadIdx.x == 0) s_prefix = lookback_exclusive(st, tile, tot & 0xffffffffull);
+    if (threadIdx.x < 32) {
+        const unsigned long long e = lookback_exclusive_warp(st, tile, tot & 0xffffffffull);
+        if (threadIdx.x == 0) s_prefix = e;
+    }
     __syncthreads();
     uint32_t acc = (uint32_t)(s_prefix + ex);
 #pragma unroll
@@ -529,6 +538,25 @@ static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, 
                     sg, s->payload, s->payload_len, s->offsets, s->metadata, two_eps, out);
                 HSZG_CHECK_LAUNCH("reconstruct hszx");
                 return HSZG_OK;
+            }
+            break;
+        case HSZG_HSZP_ND:
+            // 3-D with whole-chunk rows: one band per plane in hszg_band_scan (decode + x + y prefix in
+            // one pass), then the z prefix (+ conversion) — instead of decode, row, y and z passes
+            if (fast && g->ndims == 3 && sg.n[2] % 32 == 0 && sg.n[2] <= 4096 && TILE_CHUNKS % (sg.n[2] / 32) == 0 &&
+                sg.n[0] <= 65535) {
+                const size_t n4 = (size_t)g->n * 4;
+                const size_t need = (sizeof(OutT) == 4 ? 0 : n4) + (size_t)sg.n[0] * sg.n[2] * 4;
+                if (ws_bytes >= need) {
+                    int32_t* buf = sizeof(OutT) == 4 ? reinterpret_cast<int32_t*>(out) : reinterpret_cast<int32_t*>(ws);
+                    int32_t* A = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ws) + (sizeof(OutT) == 4 ? 0 : n4));
+                    const int rr = hszg_band_scan(g, s, sg.n[1], buf, A, nullptr, 0, nullptr, st, err);
+                    if (rr) return rr;
+                    if (sg.n[0] > 1) launch_col_scan<OutT>(buf, 1, sg.n[0], sg.n[1] * sg.n[2], two_eps, out, st);
+                    else launch_col_scan<OutT>(buf, 1, 1, sg.n[1] * sg.n[2], two_eps, out, st);   // conversion
+                    HSZG_CHECK_LAUNCH("z scan");
+                    return HSZG_OK;
+                }
             }
             break;
         case HSZG_HSZX_ND:

@@ -158,7 +158,7 @@ def test_compress_rejects_nan(H):
 
 
 @pytest.mark.parametrize("kind", ALL)
-@pytest.mark.parametrize("dims", [(64,), (12, 10), (6, 7, 8), (37, 3, 41)])
+@pytest.mark.parametrize("dims", [(64,), (12, 10), (6, 7, 8), (37, 3, 41), (5, 9, 64), (3, 17, 256)])
 def test_stage_composition_and_error_bound(H, rng, kind, dims):
     if kind in ND and len(dims) < 2:
         pytest.skip("nd compressor needs 2D+")
@@ -263,7 +263,7 @@ def test_exact_helpers(H, example_field):
 
 
 @pytest.mark.parametrize("kind", ALL)
-@pytest.mark.parametrize("dims", [(97,), (17, 13), (7, 6, 11), (64, 40, 30)])
+@pytest.mark.parametrize("dims", [(97,), (17, 13), (7, 6, 11), (64, 40, 30), (4, 9, 128)])
 def test_stats_vs_oracle(H, rng, kind, dims):
     if kind in ND and len(dims) < 2:
         pytest.skip("nd compressor needs 2D+")
@@ -292,7 +292,7 @@ def test_std_at_meta_rejected(H, rng):
 # ---- fields (test_fields.py) -----------------------------------------------------------------
 
 
-@pytest.mark.parametrize("dims", [(15, 11), (6, 7, 8), (30, 41, 19)])
+@pytest.mark.parametrize("dims", [(15, 11), (6, 7, 8), (30, 41, 19), (6, 9, 64)])
 @pytest.mark.parametrize("kind", ALL)
 def test_stencils_vs_oracle(H, rng, kind, dims):
     field = O.random_field(rng, dims)
