@@ -10,6 +10,7 @@
 // domain, fields.py:83-93 operation by operation), then round to the output
 // type.
 #include <cstdio>
+#include <cstdlib>
 #include "tile.cuh"
 
 namespace hszg {
@@ -660,6 +661,209 @@ __global__ void __launch_bounds__(GL_THREADS) k_grad_lap_f32(const int32_t* __re
     __stcs(reinterpret_cast<float4*>(o3 + o), lp);
 }
 
+// ---- vectorised K-STEN: every op of k_stencil on 2-D / 3-D int32 grids, four x-points per thread ----
+// Same per-point arithmetic as deriv / laplacian_at / k_stencil (so bit-identical results), but
+// 16-B neighbour-row loads (x+-1 by shuffle), no per-point index math and 16/32-B streaming stores.
+constexpr int SV_THREADS = 128;
+
+struct Nb4 {            // one component around four x-points: centre, z+-1, y+-1 rows and the x edges
+    int4 c, zm, zp, ym, yp;
+    int l, r;
+};
+
+__device__ __forceinline__ Nb4 nb4_load(const int32_t* q, int64_t plane, int64_t n2, int64_t off, bool active,
+                                        bool zin, bool yin, int lane, int64_t xi) {
+    Nb4 b;
+    const int4 z4 = make_int4(0, 0, 0, 0);
+    b.c = b.zm = b.zp = b.ym = b.yp = z4;
+    if (active) b.c = __ldg(reinterpret_cast<const int4*>(q + off));
+    b.l = __shfl_up_sync(0xffffffffu, b.c.w, 1);     // every lane takes part in the shuffles
+    b.r = __shfl_down_sync(0xffffffffu, b.c.x, 1);
+    if (!active) return b;
+    if (lane == 0 && xi > 0) b.l = __ldg(q + off - 1);
+    if (lane == 31 && xi + 4 < n2) b.r = __ldg(q + off + 4);
+    if (zin) {
+        b.zm = __ldg(reinterpret_cast<const int4*>(q + off - plane));
+        b.zp = __ldg(reinterpret_cast<const int4*>(q + off + plane));
+    }
+    if (yin) {
+        b.ym = __ldg(reinterpret_cast<const int4*>(q + off - n2));
+        b.yp = __ldg(reinterpret_cast<const int4*>(q + off + n2));
+    }
+    return b;
+}
+
+__device__ __forceinline__ int el(const int4& v, int j) { return j == 0 ? v.x : (j == 1 ? v.y : (j == 2 ? v.z : v.w)); }
+// x-neighbours of point j: (x-1, x+1)
+__device__ __forceinline__ int xm1(const Nb4& b, int j) { return j == 0 ? b.l : el(b.c, j - 1); }
+__device__ __forceinline__ int xp1(const Nb4& b, int j) { return j == 3 ? b.r : el(b.c, j + 1); }
+
+struct Pt4 {            // per-thread geometry shared by every component
+    bool zin, yin, x0, xl;   // interior along z / y; point 0 at x = 0; point 3 at x = n2-1
+};
+
+// derivative of one component along BOX axis a at point j (deriv(): fields.py:43/70, stage 4: :85)
+__device__ __forceinline__ double dv4(const Nb4& b, const Pt4& p, int a, int j, double eps, double two_eps, bool fd) {
+    int m, h;
+    if (a == 0) {
+        if (!p.zin) return 0.0;
+        m = el(b.zm, j), h = el(b.zp, j);
+    } else if (a == 1) {
+        if (!p.yin) return 0.0;
+        m = el(b.ym, j), h = el(b.yp, j);
+    } else {
+        if ((j == 0 && p.x0) || (j == 3 && p.xl)) return 0.0;
+        m = xm1(b, j), h = xp1(b, j);
+    }
+    if (fd) return __ddiv_rn(__dsub_rn(__dmul_rn((double)h, two_eps), __dmul_rn((double)m, two_eps)), 2.0);
+    return __dmul_rn((double)((int64_t)h - (int64_t)m), eps);
+}
+// integer derivative (GRADMAG)
+__device__ __forceinline__ int64_t di4(const Nb4& b, const Pt4& p, int a, int j) {
+    if (a == 0) return p.zin ? (int64_t)el(b.zp, j) - el(b.zm, j) : 0;
+    if (a == 1) return p.yin ? (int64_t)el(b.yp, j) - el(b.ym, j) : 0;
+    if ((j == 0 && p.x0) || (j == 3 && p.xl)) return 0;
+    return (int64_t)xp1(b, j) - xm1(b, j);
+}
+template <int ND>
+__device__ __forceinline__ double lap4(const Nb4& b, const Pt4& p, int j, double two_eps, bool fd) {
+    if ((ND == 3 && !p.zin) || !p.yin || (j == 0 && p.x0) || (j == 3 && p.xl)) return 0.0;
+    if (fd) {   // fields.py:47-60 in float64, axis order z (3-D), y, x
+        double acc = __dmul_rn((double)(-2 * ND), __dmul_rn((double)el(b.c, j), two_eps));
+        if (ND == 3) {
+            acc = __dadd_rn(acc, __dmul_rn((double)el(b.zm, j), two_eps));
+            acc = __dadd_rn(acc, __dmul_rn((double)el(b.zp, j), two_eps));
+        }
+        acc = __dadd_rn(acc, __dmul_rn((double)el(b.ym, j), two_eps));
+        acc = __dadd_rn(acc, __dmul_rn((double)el(b.yp, j), two_eps));
+        acc = __dadd_rn(acc, __dmul_rn((double)xm1(b, j), two_eps));
+        acc = __dadd_rn(acc, __dmul_rn((double)xp1(b, j), two_eps));
+        return acc;
+    }
+    int64_t acc = -2 * (int64_t)ND * el(b.c, j) + (int64_t)el(b.ym, j) + el(b.yp, j) + xm1(b, j) + xp1(b, j);
+    if (ND == 3) acc += (int64_t)el(b.zm, j) + el(b.zp, j);
+    return __dmul_rn((double)acc, two_eps);
+}
+
+__device__ __forceinline__ void st4(float* o, int64_t i, const double* v) {
+    __stcs(reinterpret_cast<float4*>(o + i), make_float4(__double2float_rn(v[0]), __double2float_rn(v[1]),
+                                                         __double2float_rn(v[2]), __double2float_rn(v[3])));
+}
+__device__ __forceinline__ void st4(double* o, int64_t i, const double* v) {
+    __stcs(reinterpret_cast<double2*>(o + i), make_double2(v[0], v[1]));
+    __stcs(reinterpret_cast<double2*>(o + i + 2), make_double2(v[2], v[3]));
+}
+
+template <int OP, int ND, typename OutT>
+__global__ void __launch_bounds__(SV_THREADS) k_stencil_v4(StencilArgs A) {
+    const int lane = threadIdx.x & 31;
+    const int64_t xi0 = ((int64_t)blockIdx.x * SV_THREADS + threadIdx.x) * 4;
+    const bool active = xi0 < A.n[2];
+    const int64_t xi = active ? xi0 : 0;
+    const int64_t y = blockIdx.y;
+    const int64_t z = A.zlo + blockIdx.z;
+    const int64_t n1 = A.n[1], n2 = A.n[2], plane = n1 * n2;
+    Pt4 p;
+    p.zin = ND == 3 && A.gz0 + z > 0 && A.gz0 + z < A.gN0 - 1;
+    p.yin = y > 0 && y < n1 - 1;
+    p.x0 = xi == 0;
+    p.xl = xi + 3 >= n2 - 1;
+    const int64_t off = z * plane + y * n2 + xi;
+    const int64_t oi = (z - A.zlo) * plane + y * n2 + xi;
+    const bool fd = A.float_domain == 1;
+    constexpr int a0 = 3 - ND;                        // box axis of original axis 0
+    constexpr int NC = (OP == HSZG_OP_DIVERGENCE || OP == HSZG_OP_CURL) ? ND : 1;
+    Nb4 b[NC];
+#pragma unroll
+    for (int c = 0; c < NC; c++)
+        b[c] = nb4_load(reinterpret_cast<const int32_t*>(A.q[c]), plane, n2, off, active, p.zin, p.yin, lane, xi);
+    if (!active) return;
+    double v[4];
+    auto D = [&](int c, int k, int j) { return dv4(b[c], p, a0 + k, j, A.eps[c], A.two_eps[c], fd); };
+    OutT* const* out = reinterpret_cast<OutT* const*>(A.out);
+    if (OP == HSZG_OP_DERIV || OP == HSZG_OP_GRAD_LAP) {
+#pragma unroll
+        for (int k = 0; k < ND; k++) {
+#pragma unroll
+            for (int j = 0; j < 4; j++) v[j] = D(0, k, j);
+            st4(out[k], oi, v);
+        }
+    }
+    if (OP == HSZG_OP_LAPLACIAN || OP == HSZG_OP_GRAD_LAP) {
+#pragma unroll
+        for (int j = 0; j < 4; j++) v[j] = lap4<ND>(b[0], p, j, A.two_eps[0], fd);
+        st4(out[OP == HSZG_OP_GRAD_LAP ? ND : 0], oi, v);
+    }
+    if (OP == HSZG_OP_GRADMAG) {
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            if (fd) {
+                double s = 0.0;
+#pragma unroll
+                for (int k = 0; k < ND; k++) {
+                    const double d = D(0, k, j);
+                    s = __dadd_rn(s, __dmul_rn(d, d));
+                }
+                v[j] = __dsqrt_rn(s);
+            } else {
+                u128 s = 0;
+#pragma unroll
+                for (int k = 0; k < ND; k++) {
+                    const int64_t d = di4(b[0], p, a0 + k, j);
+                    const uint64_t ad = (uint64_t)(d < 0 ? -d : d);
+                    s += (u128)ad * ad;
+                }
+                const double sd = (uint64_t)(s >> 64) == 0
+                                      ? __ull2double_rn((uint64_t)s)
+                                      : __dadd_rn(__dmul_rn(__ull2double_rn((uint64_t)(s >> 64)), 18446744073709551616.0),
+                                                  __ull2double_rn((uint64_t)s));
+                v[j] = __dmul_rn(__dsqrt_rn(sd), A.eps[0]);
+            }
+        }
+        st4(out[0], oi, v);
+    }
+    if (OP == HSZG_OP_DIVERGENCE) {
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            double acc = D(0, 0, j);
+#pragma unroll
+            for (int k = 1; k < NC; k++) acc = __dadd_rn(acc, D(k, k, j));
+            v[j] = acc;
+        }
+        st4(out[0], oi, v);
+    }
+    if (OP == HSZG_OP_CURL) {
+        if (ND == 2) {
+#pragma unroll
+            for (int j = 0; j < 4; j++) v[j] = __dsub_rn(D(0, 1, j), D(1 % NC, 0, j));
+            st4(out[0], oi, v);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; j++) v[j] = __dsub_rn(D(2 % NC, 1, j), D(1 % NC, 2 % ND, j));
+            st4(out[0], oi, v);
+#pragma unroll
+            for (int j = 0; j < 4; j++) v[j] = __dsub_rn(D(0, 2 % ND, j), D(2 % NC, 0, j));
+            st4(out[1], oi, v);
+#pragma unroll
+            for (int j = 0; j < 4; j++) v[j] = __dsub_rn(D(1 % NC, 0, j), D(0, 1, j));
+            st4(out[2], oi, v);
+        }
+    }
+}
+
+template <int ND, typename OutT>
+static void launch_sv4(const StencilArgs& A, dim3 grid, cudaStream_t st) {
+    switch (A.op) {
+        case HSZG_OP_DERIV: k_stencil_v4<HSZG_OP_DERIV, ND, OutT><<<grid, SV_THREADS, 0, st>>>(A); break;
+        case HSZG_OP_LAPLACIAN: k_stencil_v4<HSZG_OP_LAPLACIAN, ND, OutT><<<grid, SV_THREADS, 0, st>>>(A); break;
+        case HSZG_OP_GRAD_LAP: k_stencil_v4<HSZG_OP_GRAD_LAP, ND, OutT><<<grid, SV_THREADS, 0, st>>>(A); break;
+        case HSZG_OP_GRADMAG: k_stencil_v4<HSZG_OP_GRADMAG, ND, OutT><<<grid, SV_THREADS, 0, st>>>(A); break;
+        case HSZG_OP_DIVERGENCE: k_stencil_v4<HSZG_OP_DIVERGENCE, ND, OutT><<<grid, SV_THREADS, 0, st>>>(A); break;
+        case HSZG_OP_CURL: k_stencil_v4<HSZG_OP_CURL, ND, OutT><<<grid, SV_THREADS, 0, st>>>(A); break;
+        default: break;
+    }
+}
+
 }  // namespace hszg
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -702,8 +906,24 @@ static int stencil_impl(int op, int32_t ndims, const int64_t* dims, int32_t ncom
     A.gN0 = gN0;
     if (zhi - zlo < 1) return HSZG_OK;
     if (A.n[1] > 65535 || zhi - zlo > 65535) return HSZG_INVALID_ARG;
-    dim3 grid((unsigned)((A.n[2] + 255) / 256), (unsigned)A.n[1], (unsigned)(zhi - zlo));
     if (A.n[0] * A.n[1] * A.n[2] == 0) return HSZG_OK;
+    bool vec = ndims >= 2 && float_domain <= 1 && A.n[2] % 4 == 0 &&
+               ((op == HSZG_OP_DIVERGENCE || op == HSZG_OP_CURL) ? ncomp == ndims : true);
+    for (int c = 0; c < ncomp; c++) vec = vec && aligned16(q[c]);
+    for (int k = 0; k < nout; k++) vec = vec && aligned16(out[k]);
+    static const char* sv = getenv("HSZG_STENCIL");          // 's': scalar k_stencil only (A/B runs)
+    if (vec && !(sv && sv[0] == 's')) {
+        const dim3 g4((unsigned)((A.n[2] / 4 + SV_THREADS - 1) / SV_THREADS), (unsigned)A.n[1], (unsigned)(zhi - zlo));
+        if (ndims == 3) {
+            if (out_type == HSZG_F32) launch_sv4<3, float>(A, g4, st);
+            else launch_sv4<3, double>(A, g4, st);
+        } else {
+            if (out_type == HSZG_F32) launch_sv4<2, float>(A, g4, st);
+            else launch_sv4<2, double>(A, g4, st);
+        }
+        return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
+    }
+    dim3 grid((unsigned)((A.n[2] + 255) / 256), (unsigned)A.n[1], (unsigned)(zhi - zlo));
     k_stencil<<<grid, 256, 0, st>>>(A);
     return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
 }

@@ -543,7 +543,7 @@ static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, 
         case HSZG_HSZP_ND:
             // 3-D with whole-chunk rows: one band per plane in hszg_band_scan (decode + x + y prefix in
             // one pass), then the z prefix (+ conversion) — instead of decode, row, y and z passes
-            if (fast && g->ndims == 3 && sg.n[2] % 32 == 0 && sg.n[2] <= 4096 && TILE_CHUNKS % (sg.n[2] / 32) == 0 &&
+            if (fast && g->ndims == 3 && sg.n[2] % 32 == 0 && sg.n[2] <= 4096 &&
                 sg.n[0] <= 65535) {
                 const size_t n4 = (size_t)g->n * 4;
                 const size_t need = (sizeof(OutT) == 4 ? 0 : n4) + (size_t)sg.n[0] * sg.n[2] * 4;

@@ -311,8 +311,8 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __rest
     __shared__ uint32_t s_wt[TILE_CHUNKS / 32];
     __shared__ uint64_t s_base[2];
     __shared__ __align__(8) uint64_t bar[2];
-    const int cpr = n2 >> 5;                 // chunks per row (a power of two dividing 256)
-    const int rpt = TILE_CHUNKS / cpr;       // rows per tile
+    const int cpr = n2 >> 5;                 // chunks per row (<= 128)
+    const int rpt = TILE_CHUNKS / cpr;       // rows per tile (whole rows: rpt * cpr <= 256 chunks)
     const int b = blockIdx.x, nb = gridDim.x;
     const int64_t z = blockIdx.y;
     const int y0 = b * BR;
@@ -371,17 +371,33 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __rest
         }
         // exclusive prefix of the chunk sums along each row
         uint32_t inc = tot;
-        const int wseg = cpr < 32 ? cpr : 32;
-        for (int d = 1; d < wseg; d <<= 1) {
-            const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
-            if ((lane & (wseg - 1)) >= d) inc += o;
-        }
-        if (cpr > 32) {
+        if ((cpr & (cpr - 1)) == 0) {            // rows align with warp segments: segmented shuffle scan
+            const int wseg = cpr < 32 ? cpr : 32;
+            for (int d = 1; d < wseg; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+                if ((lane & (wseg - 1)) >= d) inc += o;
+            }
+            if (cpr > 32) {
+                if (lane == 31) s_wt[warp] = inc;
+                __syncthreads();
+                for (int w2 = warp & ~((cpr >> 5) - 1); w2 < warp; w2++) inc += s_wt[w2];
+            }
+            s_off[threadIdx.x] = inc - tot;
+        } else {                                  // any cpr: tile-wide scan minus the row start's prefix
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= d) inc += o;
+            }
             if (lane == 31) s_wt[warp] = inc;
             __syncthreads();
-            for (int w2 = warp & ~((cpr >> 5) - 1); w2 < warp; w2++) inc += s_wt[w2];
+            for (int w2 = 0; w2 < warp; w2++) inc += s_wt[w2];
+            s_off[threadIdx.x] = inc;
+            __syncthreads();
+            const int rs = ((int)threadIdx.x / cpr) * cpr;
+            const uint32_t before = rs > 0 ? s_off[rs - 1] : 0u;
+            __syncthreads();
+            s_off[threadIdx.x] = inc - tot - before;
         }
-        s_off[threadIdx.x] = inc - tot;
         __syncthreads();
         const int nstrips = (n2 + SE_W - 1) / SE_W;
         for (int rr = 0; rr < nr; rr++) {
@@ -536,13 +552,13 @@ extern "C" int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t ba
     const int64_t n1 = g->dims[1], n2 = g->dims[2], np = g->dims[0];
     const int64_t cpr = n2 / kChunkCap;
     if (g->kind != HSZG_HSZP_ND || g->ndims != 3 || !s->canonical || n2 % kChunkCap || cpr < 1 ||
-        TILE_CHUNKS % cpr || n2 > 4 * BS_MAXG * TILE_CHUNKS || band_rows < 1 || n1 > INT32_MAX || np > 65535 ||
+        n2 > 4 * BS_MAXG * TILE_CHUNKS || band_rows < 1 || n1 > INT32_MAX || np > 65535 ||
         !al16(L) || !al16(A) || !al16(s->payload) || (!L && !strip_edges) ||
         (l_int16 && (!l_overflow || strip_edges || n2 % 8))) {
         err->status = HSZG_INVALID_ARG;
         snprintf(err->message, sizeof(err->message),
                  "band_scan needs a canonical 3-D HSZP_ND stream with whole-chunk rows (n2 %% 32 == 0, "
-                 "n2 <= 4096, 256 %% (n2/32) == 0, 16-B aligned buffers)");
+                 "n2 <= 4096, 16-B aligned buffers)");
         return HSZG_INVALID_ARG;
     }
     if (g->n_chunks == 0) return HSZG_OK;

@@ -382,7 +382,7 @@ class WindowPipeline:
         if n2 % 4 or outs[0].dtype != t.float32 or not self.ds.desc.canonical:
             return False
         if self.sf.kind == HSZP_ND:
-            return n2 % 32 == 0 and 256 % (n2 // 32) == 0
+            return n2 % 32 == 0 and n2 <= 4096
         return True
 
     def run(self, outs, stats: bool = True, _prepared: bool = False):
@@ -482,12 +482,14 @@ class WindowPipeline:
         """Rows per band of hszg_band_scan (0: not applicable -> decode_rowscan + col_scan): whole tiles
         of 256 chunks, and enough bands that a window launches >= 8 CTAs per SM."""
         n1, n2 = self.sf.global_dims[1], self.sf.global_dims[2]
-        if n2 % 32 or n2 > 4096 or 256 % (n2 // 32):
+        if n2 % 32 or n2 > 4096:
             return 0
         rpt = 256 // (n2 // 32)
         if self.band_rows_req:
             return int(self.band_rows_req)
-        unit = max(rpt, 64)       # whole band_scan tiles; multiples of 16 take the ring z-sweep (zring.cu)
+        # whole band_scan tiles where rpt is a multiple of 16 (multiples of 16 take the ring z-sweep,
+        # zring.cu); otherwise 64 rows (the band's last tile is partial)
+        unit = rpt if rpt >= 64 and rpt % 16 == 0 else 64
         want = -(-16 * _SMS // max(1, min(self.W, self.sf.nz)))
         br = -(-n1 // want)
         return -(-br // unit) * unit

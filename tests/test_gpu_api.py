@@ -158,7 +158,7 @@ def test_compress_rejects_nan(H):
 
 
 @pytest.mark.parametrize("kind", ALL)
-@pytest.mark.parametrize("dims", [(64,), (12, 10), (6, 7, 8), (37, 3, 41), (5, 9, 64), (3, 17, 256)])
+@pytest.mark.parametrize("dims", [(64,), (12, 10), (6, 7, 8), (37, 3, 41), (5, 9, 64), (3, 17, 256), (3, 17, 96), (4, 25, 384)])
 def test_stage_composition_and_error_bound(H, rng, kind, dims):
     if kind in ND and len(dims) < 2:
         pytest.skip("nd compressor needs 2D+")
@@ -263,7 +263,7 @@ def test_exact_helpers(H, example_field):
 
 
 @pytest.mark.parametrize("kind", ALL)
-@pytest.mark.parametrize("dims", [(97,), (17, 13), (7, 6, 11), (64, 40, 30), (4, 9, 128)])
+@pytest.mark.parametrize("dims", [(97,), (17, 13), (7, 6, 11), (64, 40, 30), (4, 9, 128), (3, 21, 160)])
 def test_stats_vs_oracle(H, rng, kind, dims):
     if kind in ND and len(dims) < 2:
         pytest.skip("nd compressor needs 2D+")

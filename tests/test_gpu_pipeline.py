@@ -19,7 +19,7 @@ from oracle import hsz_oracle as O
 
 pytestmark = pytest.mark.gpu
 
-ALL_DIMS = [(64, 40, 36), (48, 23, 64), (40, 17, 128), (48, 24, 64), (48, 40, 136)]
+ALL_DIMS = [(64, 40, 36), (48, 23, 64), (40, 17, 128), (48, 24, 64), (48, 40, 136), (48, 30, 96)]
 
 # fast mode: fl32(fl32(D) * fl32(eps)) vs fl32(D * eps): at most 4 roundings of 2^-24 apart (< 1e-6 target)
 FAST_RTOL = 4 * 2.0**-24
@@ -184,7 +184,9 @@ def test_fast_decode_bitwidths_hszx_nd(dims):
     assert np.array_equal(np.asarray(q), O.stage3(ref))
 
 
-@pytest.mark.parametrize("dims", [(16, 16, 256), (24, 40, 64)], ids=lambda d: "x".join(map(str, d)))
+# n2 = 96 / 160 / 384: 3 / 5 / 12 chunks per row, which do not divide a 256-chunk tile (partial tiles)
+@pytest.mark.parametrize("dims", [(16, 16, 256), (24, 40, 64), (12, 30, 96), (5, 44, 160), (6, 50, 384)],
+                         ids=lambda d: "x".join(map(str, d)))
 @pytest.mark.parametrize("band_rows", [None, 1, 7, 16, 32])
 def test_fast_decode_bitwidths_band_scan(dims, band_rows):
     """hszg_band_scan (decode32 + row prefix + banded column prefix) across bit widths, through the
