@@ -62,23 +62,17 @@ def _region_tuple(region, nd):
 
 
 def region_reduce_device(q_dev, eps: float, region, tau: float = float("nan")):
-    """Device-side per-region reduction + finalisation; returns CUDA tensors."""
-    t = _lib.torch()
+    """Device-side per-region reduction + finalisation; returns CUDA tensors (views of one buffer,
+    ``buf``, which the host reads in a single copy)."""
     nd = q_dev.dim()
     reg = _region_tuple(region, nd)
-    grid, s1, s2lo, s2hi, qmin, qmax, size = devmod.region_reduce(q_dev, reg)
-    nr = s1.numel()
-    dev = _lib.device()
-    mean = t.empty(nr, dtype=t.float64, device=dev)
-    var = t.empty(nr, dtype=t.float64, device=dev)
-    fmin = t.empty(nr, dtype=t.float64, device=dev)
-    fmax = t.empty(nr, dtype=t.float64, device=dev)
-    count = t.zeros(1, dtype=t.int64, device=dev)
-    _lib.call("hszg_region_finalize", _lib.ptr(s1), _lib.ptr(s2lo), _lib.ptr(s2hi), _lib.ptr(qmin), _lib.ptr(qmax),
-              _lib.ptr(size), nr, 2.0 * eps, float(tau), _lib.ptr(mean), _lib.ptr(var), _lib.ptr(fmin),
-              _lib.ptr(fmax), _lib.ptr(count), _lib.stream_handle())
-    return dict(grid=grid, region=tuple(min(r, n) for r, n in zip(reg, q_dev.shape)), s1=s1, s2lo=s2lo, s2hi=s2hi,
-                qmin=qmin, qmax=qmax, size=size, mean=mean, var=var, vmin=fmin, vmax=fmax, count=count)
+    grid, buf, v = devmod.region_reduce(q_dev, reg)
+    nr = v["s1"].numel()
+    _lib.call("hszg_region_finalize", _lib.ptr(v["s1"]), _lib.ptr(v["s2lo"]), _lib.ptr(v["s2hi"]),
+              _lib.ptr(v["qmin"]), _lib.ptr(v["qmax"]), _lib.ptr(v["size"]), nr, 2.0 * eps, float(tau),
+              _lib.ptr(v["mean"]), _lib.ptr(v["var"]), _lib.ptr(v["vmin"]), _lib.ptr(v["vmax"]), _lib.ptr(v["count"]),
+              _lib.stream_handle())
+    return dict(grid=grid, region=tuple(min(r, n) for r, n in zip(reg, q_dev.shape)), buf=buf, **v)
 
 
 def _quantized(c: CompressedStream, stage: Stage):
@@ -97,15 +91,17 @@ def region_stats(c: CompressedStream, region, stage: Stage = Stage.QUANTIZED,
     q = _quantized(c, stage)
     r = region_reduce_device(q, c.eps, region, float("nan") if tau is None else tau)
     g = r["grid"]
+    nr = int(np.prod(g))
+    host = r["buf"].cpu().numpy()                 # every output in one device -> host copy
+    w = [host[k * nr:(k + 1) * nr] for k in range(devmod.REGION_WORDS)]
+    mm = w[8].view(np.int32)
     return RegionStats(
         region=r["region"], grid=g,
-        s1=r["s1"].cpu().numpy().reshape(g),
-        s2_lo=r["s2lo"].cpu().numpy().view(np.uint64).reshape(g), s2_hi=r["s2hi"].cpu().numpy().reshape(g),
-        qmin=r["qmin"].cpu().numpy().reshape(g), qmax=r["qmax"].cpu().numpy().reshape(g),
-        size=r["size"].cpu().numpy().reshape(g),
-        mean=r["mean"].cpu().numpy().reshape(g), var=r["var"].cpu().numpy().reshape(g),
-        vmin=r["vmin"].cpu().numpy().reshape(g), vmax=r["vmax"].cpu().numpy().reshape(g),
-        threshold=tau, crossing_count=None if tau is None else int(r["count"].item()),
+        s1=w[0].reshape(g), s2_lo=w[1].view(np.uint64).reshape(g), s2_hi=w[2].reshape(g),
+        qmin=mm[:nr].reshape(g), qmax=mm[nr:].reshape(g), size=w[3].reshape(g),
+        mean=w[4].view(np.float64).reshape(g), var=w[5].view(np.float64).reshape(g),
+        vmin=w[6].view(np.float64).reshape(g), vmax=w[7].view(np.float64).reshape(g),
+        threshold=tau, crossing_count=None if tau is None else int(host[devmod.REGION_WORDS * nr]),
     )
 
 

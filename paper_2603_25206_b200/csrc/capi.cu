@@ -79,7 +79,11 @@ extern "C" size_t hszg_workspace_bytes(const HszgGeom* g, const HszgStream* s, i
                                              (g->kind == HSZG_HSZX_ND && sg.cpb[0] <= TILE_CHUNKS));
             if (fused) return lookback_ws_bytes(g->n_chunks) + 256;
             if (canonical && g->kind == HSZG_HSZP_ND && g->ndims == 3)   // band-scan path: band totals
-                return (out_type == HSZG_F64 ? n4 : 0) + (size_t)g->dims[0] * g->dims[2] * 4 + 512;
+            {
+                const int64_t br = recon_band_rows(g->dims[0], g->dims[1], g->dims[2]);
+                const int64_t nb = (g->dims[1] + br - 1) / br;
+                return (out_type == HSZG_F64 ? n4 : 0) + (size_t)g->dims[0] * nb * g->dims[2] * 4 + 512;
+            }
             // generic: decode buffer (fp64 output only) + per-kind transform scratch
             size_t b = out_type == HSZG_F64 ? n4 : 0;
             if (g->kind == HSZG_HSZP) b += lookback_ws_bytes(g->n);

@@ -121,6 +121,38 @@ __device__ __forceinline__ unsigned long long lookback_exclusive_warp(const LBSt
     return excl;
 }
 
+// 32-bit variant for scans mod 2^32 (the int32 q prefixes): the status flag and the value share one
+// 64-bit word (bits 62-63 flag, low 32 bits value), published with a single 64-bit store, so readers
+// need no fence between the flag and the value (the u64 version above fences every publication,
+// which stalls behind the tile's streaming stores).  Uses st.agg as the word array.
+__device__ __forceinline__ uint32_t lookback_exclusive_warp32(const LBState& st, int64_t tile, uint32_t agg) {
+    const int lane = threadIdx.x & 31;
+    volatile unsigned long long* w = st.agg;
+    const unsigned long long AGG = 1ull << 62, INCL = 2ull << 62;
+    if (lane == 0) w[tile] = (tile == 0 ? INCL : AGG) | agg;
+    if (tile == 0) return 0u;
+    uint32_t excl = 0;
+    int64_t p = tile - 1;
+    while (true) {
+        const int64_t idx = p - lane;
+        const unsigned long long v = idx >= 0 ? w[idx] : INCL;   // before tile 0: inclusive 0
+        const unsigned f = (unsigned)(v >> 62);
+        const unsigned incl = __ballot_sync(0xffffffffu, f == 2);
+        const unsigned zero = __ballot_sync(0xffffffffu, f == 0);
+        const int k = incl ? __ffs(incl) - 1 : 31;
+        const unsigned need = (2u << k) - 1u;
+        if (zero & need) continue;
+        uint32_t x = lane <= k ? (uint32_t)v : 0u;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) x += __shfl_xor_sync(0xffffffffu, x, d);
+        excl += x;
+        if (incl) break;
+        p -= 32;
+    }
+    if (lane == 0) w[tile] = INCL | (uint32_t)(excl + agg);
+    return excl;
+}
+
 // block-wide exclusive scan of one u64 per thread; returns exclusive value, *total = block sum
 __device__ __forceinline__ unsigned long long block_exclusive_u64(unsigned long long v, unsigned long long* total) {
     __shared__ unsigned long long warp_tot[32];

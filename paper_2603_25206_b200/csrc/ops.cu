@@ -17,6 +17,8 @@ namespace hszg {
 
 constexpr int RED_THREADS = 256;
 
+__device__ __forceinline__ uint64_t sq64(int v) { return (uint64_t)((int64_t)v * (int64_t)v); }
+
 // ---- per-chunk accumulators for the fused stream reductions -----------------
 
 // mode 1/2: sum over the row-major box of w * p with w = (N0-i0)(N1-i1)(N2-i2)
@@ -83,6 +85,88 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_reduce_tiles(SegGeo sg, const u
     if (threadIdx.x == 0) store_sums(partials + blockIdx.x, a);
 }
 
+// MetaChunk fast path: every chunk full and every segment full-size (chunk c belongs to segment
+// c / cps), so a chunk decodes with decode32s into int4 groups; sums in int64 / u128 per thread.
+// Grid-strided over tiles: 8 CTAs per SM, one partial per CTA.
+__global__ void __launch_bounds__(TILE_CHUNKS) k_reduce_meta_fast(const uint8_t* __restrict__ payload, uint64_t len,
+                                                                  const uint64_t* __restrict__ offsets, int64_t n_chunks,
+                                                                  const int32_t* __restrict__ meta, int64_t cps,
+                                                                  int64_t n, HszgSums* partials) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ uint64_t s_lo, s_hi;
+    uint4* sb = reinterpret_cast<uint4*>(smem);
+    Acc a;
+    a.init();
+    u128 s2 = 0;
+    const int64_t tiles = (n_chunks + TILE_CHUNKS - 1) / TILE_CHUNKS;
+    // a thread's chunk start / end and block mean, loaded one tile ahead
+    uint64_t off = 0, end = 0;
+    int32_t m = 0;
+    auto fetch = [&](int64_t t) {
+        const int64_t c = t * TILE_CHUNKS + threadIdx.x;
+        if (t < tiles && c < n_chunks) {
+            off = __ldg(offsets + c);
+            end = c + 1 < n_chunks ? __ldg(offsets + c + 1) : payload_end(offsets, n_chunks, len);
+            m = __ldg(meta + c / cps);
+        }
+    };
+    fetch(blockIdx.x);
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int64_t c0 = t * TILE_CHUNKS;
+        const int nch = (int)(n_chunks - c0 < TILE_CHUNKS ? n_chunks - c0 : TILE_CHUNKS);
+        const bool mine = (int)threadIdx.x < nch;
+        if (threadIdx.x == 0) s_lo = off;
+        if ((int)threadIdx.x == nch - 1) s_hi = end;
+        __syncthreads();
+        const uint64_t base = stage_range(payload, s_lo, s_hi, sb);
+        const uint32_t rel = (uint32_t)(off - base);
+        const int32_t mm = m;
+        __syncthreads();
+        fetch(t + gridDim.x);                  // in flight while this tile decodes
+        const uint32_t* words = reinterpret_cast<const uint32_t*>(sb);
+        if (mine && smem_byte(words, rel) <= 27) {
+            // |p| < 2^27: sums of the residuals p (q = p + m per chunk), 64-bit sum of squares chained
+            // through IMAD.WIDE, then sum q = sum p + 32m, sum q^2 = sum p^2 + 2m sum p + 32m^2
+            int64_t sp = 0, sq = 0;
+            int mnp = INT32_MAX, mxp = INT32_MIN;
+            decode32s<false>(words, rel, 0, [&](int, int4 v) {
+                sp += (int64_t)(v.x + v.y + v.z + v.w);
+                sq += (int64_t)v.x * v.x;
+                sq += (int64_t)v.y * v.y;
+                sq += (int64_t)v.z * v.z;
+                sq += (int64_t)v.w * v.w;
+                mnp = min(mnp, min(min(v.x, v.y), min(v.z, v.w)));
+                mxp = max(mxp, max(max(v.x, v.y), max(v.z, v.w)));
+            });
+            const int64_t m64 = mm;
+            a.s1 += (i128)(sp + 32 * m64);
+            a.s2 += (i128)sq + (i128)(2 * m64) * (i128)sp + (i128)(32 * m64) * (i128)m64;
+            a.vmin = min(a.vmin, mnp + mm);
+            a.vmax = max(a.vmax, mxp + mm);
+        } else if (mine) {
+            int64_t s1 = 0;
+            int mn = a.vmin, mx = a.vmax;
+            decode32s<false>(words, rel, mm, [&](int, int4 v) {
+                s1 += (int64_t)v.x + v.y + v.z + v.w;
+                s2 += (u128)(sq64(v.x) + sq64(v.y));
+                s2 += (u128)(sq64(v.z) + sq64(v.w));
+                mn = min(mn, min(min(v.x, v.y), min(v.z, v.w)));
+                mx = max(mx, max(max(v.x, v.y), max(v.z, v.w)));
+            });
+            a.s1 += s1;
+            a.vmin = mn;
+            a.vmax = mx;
+        }
+        __syncthreads();                       // the next tile overwrites the staging buffer
+    }
+    a.s2 += (i128)s2;
+    block_reduce(a);
+    if (threadIdx.x == 0) {
+        a.count = blockIdx.x ? 0 : n;
+        store_sums(partials + blockIdx.x, a);
+    }
+}
+
 // same reduction over an already-decoded stream-order array (non-canonical containers)
 template <class CA>
 __global__ void k_reduce_chunks_array(SegGeo sg, const int32_t* p, const int32_t* meta, HszgSums* partials) {
@@ -125,20 +209,35 @@ __global__ void k_reduce_i32(const int32_t* src, int64_t n, HszgSums* partials) 
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t s1 = 0;
+    u128 s2 = 0;
     const bool aligned = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
     int64_t head = 0;
     if (aligned) {
         const int4* v4 = reinterpret_cast<const int4*>(src);
         const int64_t n4 = n >> 2;
-        for (int64_t i = tid; i < n4; i += stride) {
-            const int4 v = __ldg(v4 + i);
+        int mn = INT32_MAX, mx = INT32_MIN;
+        auto take = [&](const int4 v) {
             s1 += (int64_t)v.x + v.y + v.z + v.w;
-            a.s2 += (i128)((int64_t)v.x * v.x + (int64_t)v.y * v.y) + (i128)((int64_t)v.z * v.z + (int64_t)v.w * v.w);
-            a.vmin = min(a.vmin, min(min(v.x, v.y), min(v.z, v.w)));
-            a.vmax = max(a.vmax, max(max(v.x, v.y), max(v.z, v.w)));
+            s2 += (u128)(sq64(v.x) + sq64(v.y));        // squares <= 2^62: pair sums fit 64 bits
+            s2 += (u128)(sq64(v.z) + sq64(v.w));
+            mn = min(mn, min(min(v.x, v.y), min(v.z, v.w)));
+            mx = max(mx, max(max(v.x, v.y), max(v.z, v.w)));
+        };
+        int64_t i = tid;
+        for (; i + 3 * stride < n4; i += 4 * stride) {   // four 16-B loads in flight per thread
+            const int4 v0 = __ldg(v4 + i), v1 = __ldg(v4 + i + stride);
+            const int4 v2 = __ldg(v4 + i + 2 * stride), v3 = __ldg(v4 + i + 3 * stride);
+            take(v0);
+            take(v1);
+            take(v2);
+            take(v3);
         }
+        for (; i < n4; i += stride) take(__ldg(v4 + i));
+        a.vmin = mn;
+        a.vmax = mx;
         head = n4 << 2;
     }
+    a.s2 += (i128)s2;
     for (int64_t i = head + tid; i < n; i += stride) {
         const int32_t v = src[i];
         s1 += v;
@@ -231,6 +330,67 @@ __global__ void k_region_reduce(const int32_t* q, int64_t n0, int64_t n1, int64_
         qmin[r] = a.vmin;
         qmax[r] = a.vmax;
         size[r] = tot;
+    }
+}
+
+// Row-streaming variant for regions R2 = 4..128 wide (a power of two) over 16-B rows: one CTA per
+// (region plane, region row) sweeps its R0 x R1 grid rows across the full width with 16-B loads,
+// each thread owning four x-points of one region; the R2/4 threads of a region then combine by
+// shuffles.  Coalesced and with ~R0*R1 loads in flight per thread (k_region_reduce: one CTA per
+// region, scattered 4-byte loads).
+constexpr int RR_THREADS = 128;   // 512 x-points per pass (R2 divides 512)
+
+__global__ void __launch_bounds__(RR_THREADS) k_region_rows(const int32_t* __restrict__ q, int64_t n0, int64_t n1,
+                                                            int64_t n2, int R0, int R1, int R2, int64_t g1, int64_t g2,
+                                                            int64_t* s1o, uint64_t* s2lo, int64_t* s2hi, int32_t* qmin,
+                                                            int32_t* qmax, int64_t* size) {
+    const int64_t r1 = blockIdx.x, r0 = blockIdx.y;
+    const int64_t z0 = r0 * R0, y0 = r1 * R1;
+    const int e0 = (int)(z0 + R0 <= n0 ? R0 : n0 - z0);
+    const int e1 = (int)(y0 + R1 <= n1 ? R1 : n1 - y0);
+    const int rows = e0 * e1;
+    const int seg = R2 >> 2;                     // threads per region (power of two <= 32)
+    const int lane = threadIdx.x & 31;
+    for (int64_t xb = 0; xb < n2; xb += 4 * RR_THREADS) {
+        const int64_t x = xb + 4 * (int64_t)threadIdx.x;
+        const bool act = x < n2;
+        int64_t s1 = 0;
+        u128 s2 = 0;
+        int mn = INT32_MAX, mx = INT32_MIN;
+        if (act) {
+#pragma unroll 4
+            for (int k = 0; k < rows; k++) {
+                const int z = k / e1, y = k - z * e1;
+                const int4 v = __ldg(reinterpret_cast<const int4*>(q + ((z0 + z) * n1 + y0 + y) * n2 + x));
+                s1 += (int64_t)v.x + v.y + v.z + v.w;
+                s2 += (u128)(sq64(v.x) + sq64(v.y));  // each square <= 2^62: pair sums fit 64 bits
+                s2 += (u128)(sq64(v.z) + sq64(v.w));
+                mn = min(mn, min(min(v.x, v.y), min(v.z, v.w)));
+                mx = max(mx, max(max(v.x, v.y), max(v.z, v.w)));
+            }
+        }
+        uint64_t lo = (uint64_t)s2, hi = (uint64_t)(s2 >> 64);
+        for (int d = 1; d < seg; d <<= 1) {
+            s1 += (int64_t)__shfl_xor_sync(0xffffffffu, (unsigned long long)s1, d);
+            const uint64_t olo = __shfl_xor_sync(0xffffffffu, (unsigned long long)lo, d);
+            const uint64_t ohi = __shfl_xor_sync(0xffffffffu, (unsigned long long)hi, d);
+            const u128 t = (((u128)hi << 64) | lo) + (((u128)ohi << 64) | olo);
+            lo = (uint64_t)t;
+            hi = (uint64_t)(t >> 64);
+            mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, d));
+            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+        }
+        if (act && (lane & (seg - 1)) == 0) {
+            const int64_t r2 = x / R2;
+            const int64_t r = (r0 * g1 + r1) * g2 + r2;
+            const int64_t e2 = (r2 + 1) * R2 <= n2 ? R2 : n2 - r2 * R2;
+            s1o[r] = s1;
+            s2lo[r] = lo;
+            s2hi[r] = (int64_t)hi;
+            qmin[r] = mn;
+            qmax[r] = mx;
+            size[r] = (int64_t)rows * e2;
+        }
     }
 }
 
@@ -475,6 +635,18 @@ extern "C" int hszg_reduce_stream(const HszgGeom* g, const HszgStream* s, int mo
             return HSZG_INVALID_ARG;
         }
         const size_t smem = tile_smem_bytes(s->max_bitwidth);
+        bool full_segs = g->n_chunks * kChunkCap == g->n && (sg.B[0] * sg.B[1] * sg.B[2]) % kChunkCap == 0;
+        for (int a = 0; a < 3; a++) full_segs = full_segs && sg.E[a] == sg.B[a];
+        if (mode == 3 && full_segs) {
+            const size_t fsmem = stage_bytes(s->max_bitwidth);
+            allow_smem(k_reduce_meta_fast, fsmem);
+            const int64_t grid = tiles < 148 * 8 ? tiles : 148 * 8;
+            k_reduce_meta_fast<<<(unsigned)grid, TILE_CHUNKS, fsmem, st>>>(
+                s->payload, s->payload_len, s->offsets, g->n_chunks, s->metadata,
+                (sg.B[0] * sg.B[1] * sg.B[2]) / kChunkCap, g->n, partials);
+            { const cudaError_t e_ = cudaGetLastError(); if (e_ != cudaSuccess) return hszg_set_cuda_error(err, e_, "reduce tiles"); }
+            return finalize(partials, grid, out_dev, st);
+        }
         if (mode == 3)
             allow_smem(k_reduce_tiles<MetaChunk>, smem),
             k_reduce_tiles<MetaChunk><<<(unsigned)tiles, TILE_CHUNKS, smem, st>>>(sg, s->payload, s->payload_len,
@@ -565,6 +737,15 @@ extern "C" int hszg_region_reduce(const int32_t* q, int32_t ndims, const int64_t
     const int64_t g0 = (n[0] + R[0] - 1) / R[0], g1 = (n[1] + R[1] - 1) / R[1], g2 = (n[2] + R[2] - 1) / R[2];
     const int64_t nr = g0 * g1 * g2;
     if (nr == 0) return HSZG_OK;
+    const int64_t seg = R[2] / 4;
+    static const char* rm = getenv("HSZG_REGION");           // 'b': one-CTA-per-region kernel (A/B runs)
+    if (R[2] % 4 == 0 && seg <= 32 && (seg & (seg - 1)) == 0 && n[2] % 4 == 0 &&
+        (reinterpret_cast<uintptr_t>(q) & 15) == 0 && g0 <= 65535 && g1 < INT32_MAX && R[0] * R[1] < INT32_MAX &&
+        !(rm && rm[0] == 'b')) {
+        k_region_rows<<<dim3((unsigned)g1, (unsigned)g0), RR_THREADS, 0, as_stream(stream)>>>(
+            q, n[0], n[1], n[2], (int)R[0], (int)R[1], (int)R[2], g1, g2, s1, s2_lo, s2_hi, qmin, qmax, size);
+        return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
+    }
     const int64_t rs = R[0] * R[1] * R[2];
     const int threads = rs >= 1024 ? 256 : (rs >= 256 ? 128 : 64);
     k_region_reduce<<<(unsigned)nr, threads, 0, as_stream(stream)>>>(q, n[0], n[1], n[2], R[0], R[1], R[2], g1, g2,

@@ -10,6 +10,7 @@
 // which fits int32, so modular sums are exact (the reference casts its int64
 // result back to int32, compressors.py:226).
 #include <cstdio>
+#include <cstdlib>
 #include "tile.cuh"
 #include "lookback.cuh"
 
@@ -277,7 +278,7 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_tile_scan(SegGeo sg, const uint
     unsigned long long tot;
     const unsigned long long excl = block_exclusive_u64((unsigned long long)run, &tot);
     if (threadIdx.x < 32) {
-        const unsigned long long e = lookback_exclusive_warp(st, tile, tot & 0xffffffffull);
+        const unsigned long long e = lookback_exclusive_warp32(st, tile, (uint32_t)tot);
         if (threadIdx.x == 0) s_prefix = e;
     }
     __syncthreads();
@@ -286,6 +287,55 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_tile_scan(SegGeo sg, const uint
     __syncthreads();
     const int n = (int)(t.e1 - t.e0);
     for (int i = threadIdx.x; i < n; i += blockDim.x) out[t.e0 + i] = Conv<OutT>::go(t.vals[pad_idx(i)], two_eps);
+}
+
+// Fast variant when every chunk is full (n_chunks * 32 == N: chunk c holds stream values 32c..32c+31):
+// TMA-free 16-B staging, decode32 (inclusive chunk prefix) into the 36-word layout, block scan of the
+// chunk sums + the same warp look-back, then 16-B stores of value + (tile prefix + chunk prefix).
+template <typename OutT>
+__global__ void __launch_bounds__(TILE_CHUNKS) k_tile_scan_fast(const uint8_t* __restrict__ payload, uint64_t len,
+                                                               const uint64_t* __restrict__ offsets, int64_t n_chunks,
+                                                               LBState st, double two_eps, OutT* __restrict__ out) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ unsigned int s_tile;
+    __shared__ unsigned long long s_prefix;
+    __shared__ uint64_t s_lo, s_hi;
+    __shared__ uint32_t s_add[TILE_CHUNKS];
+    int32_t* tile = reinterpret_cast<int32_t*>(smem);
+    uint4* sb = reinterpret_cast<uint4*>(smem + kFastTileBytes);
+    if (threadIdx.x == 0) s_tile = atomicAdd(st.ticket, 1u);
+    __syncthreads();
+    const int64_t t = s_tile;
+    const int64_t c0 = t * TILE_CHUNKS;
+    const int nch = (int)(n_chunks - c0 < TILE_CHUNKS ? n_chunks - c0 : TILE_CHUNKS);
+    if (threadIdx.x == 0) {
+        s_lo = offsets[c0];
+        s_hi = c0 + nch < n_chunks ? offsets[c0 + nch] : payload_end(offsets, n_chunks, len);
+    }
+    __syncthreads();
+    const uint64_t base = stage_range(payload, s_lo, s_hi, sb);
+    const uint32_t rel = (int)threadIdx.x < nch ? (uint32_t)(__ldg(offsets + c0 + threadIdx.x) - base) : 0u;
+    __syncthreads();
+    uint32_t run = 0;
+    if ((int)threadIdx.x < nch)
+        run = decode32<true>(reinterpret_cast<const uint32_t*>(sb), rel, tile + threadIdx.x * kChunkStride, 0);
+    unsigned long long tot;
+    const unsigned long long excl = block_exclusive_u64((unsigned long long)run, &tot);
+    if (threadIdx.x < 32) {
+        const unsigned long long e = lookback_exclusive_warp32(st, t, (uint32_t)tot);
+        if (threadIdx.x == 0) s_prefix = e;
+    }
+    __syncthreads();
+    s_add[threadIdx.x] = (uint32_t)(s_prefix + excl);
+    __syncthreads();
+    OutT* o = out + c0 * kChunkCap;
+    for (int g = threadIdx.x; g < nch * 8; g += TILE_CHUNKS) {
+        const int ch = g >> 3;
+        const int4 v = *reinterpret_cast<const int4*>(tile + ch * kChunkStride + ((g & 7) << 2));
+        const uint32_t a = s_add[ch];
+        store4<OutT>(o + 4 * g, make_int4((int)((uint32_t)v.x + a), (int)((uint32_t)v.y + a), (int)((uint32_t)v.z + a),
+                                          (int)((uint32_t)v.w + a)), two_eps);
+    }
 }
 
 // ---- HSZP_ND: row scans along the last axis, then column scans -----------------------
@@ -341,6 +391,25 @@ __global__ void k_col_scan(const int32_t* src, int64_t A, int64_t M, int64_t Lc,
     }
 }
 
+// z prefix of band-local prefixes: q[z][y][x] = sum_{z' <= z} (L[z'][y][x] + A[z'][y / BR][x]), A the
+// exclusive band offsets of hszg_band_scan (an L2-resident n0 x nb x n2 table).  One column per
+// thread (tried: several rows or planes per thread — fewer threads in flight, slower).
+template <typename OutT>
+__global__ void k_col_scan_bands(const int32_t* src, const int32_t* __restrict__ A, int64_t M, int64_t n1, int64_t n2,
+                                 int64_t BR, int64_t nb, double two_eps, OutT* dst) {
+    const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t Lc = n1 * n2;
+    if (l >= Lc) return;
+    const int64_t y = l / n2, x = l - y * n2;
+    const int32_t* a = A + (y / BR) * n2 + x;
+    const int64_t as = nb * n2;
+    uint32_t acc = 0;
+    for (int64_t m = 0; m < M; m++) {      // src may be dst: each element is read before it is written
+        acc += (uint32_t)src[m * Lc + l] + (uint32_t)__ldg(a + m * as);
+        dst[m * Lc + l] = Conv<OutT>::go((int32_t)acc, two_eps);
+    }
+}
+
 template <typename OutT>
 static void launch_col_scan(const int32_t* src, int64_t A, int64_t M, int64_t Lc, double two_eps, OutT* dst,
                             cudaStream_t st) {
@@ -378,7 +447,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_i32(const int32_t* in, in
     unsigned long long tot;
     const unsigned long long ex = block_exclusive_u64(run, &tot);
     if (threadIdx.x < 32) {
-        const unsigned long long e = lookback_exclusive_warp(st, tile, tot & 0xffffffffull);
+        const unsigned long long e = lookback_exclusive_warp32(st, tile, (uint32_t)tot);
         if (threadIdx.x == 0) s_prefix = e;
     }
     __syncthreads();
@@ -546,14 +615,21 @@ static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, 
             if (fast && g->ndims == 3 && sg.n[2] % 32 == 0 && sg.n[2] <= 4096 &&
                 sg.n[0] <= 65535) {
                 const size_t n4 = (size_t)g->n * 4;
-                const size_t need = (sizeof(OutT) == 4 ? 0 : n4) + (size_t)sg.n[0] * sg.n[2] * 4;
+                const int64_t br = recon_band_rows(sg.n[0], sg.n[1], sg.n[2]);
+                const int64_t nb = (sg.n[1] + br - 1) / br;
+                const size_t need = (sizeof(OutT) == 4 ? 0 : n4) + (size_t)sg.n[0] * nb * sg.n[2] * 4;
                 if (ws_bytes >= need) {
                     int32_t* buf = sizeof(OutT) == 4 ? reinterpret_cast<int32_t*>(out) : reinterpret_cast<int32_t*>(ws);
                     int32_t* A = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ws) + (sizeof(OutT) == 4 ? 0 : n4));
-                    const int rr = hszg_band_scan(g, s, sg.n[1], buf, A, nullptr, 0, nullptr, st, err);
+                    const int rr = hszg_band_scan(g, s, br, buf, A, nullptr, 0, nullptr, st, err);
                     if (rr) return rr;
-                    if (sg.n[0] > 1) launch_col_scan<OutT>(buf, 1, sg.n[0], sg.n[1] * sg.n[2], two_eps, out, st);
-                    else launch_col_scan<OutT>(buf, 1, 1, sg.n[1] * sg.n[2], two_eps, out, st);   // conversion
+                    if (nb == 1) {          // one band per plane: A holds zeros, the plain z prefix
+                        launch_col_scan<OutT>(buf, 1, sg.n[0], sg.n[1] * sg.n[2], two_eps, out, st);
+                    } else {
+                        const int64_t Lc = sg.n[1] * sg.n[2];
+                        k_col_scan_bands<OutT><<<(unsigned)((Lc + 255) / 256), 256, 0, st>>>(
+                            buf, A, sg.n[0], sg.n[1], sg.n[2], br, nb, two_eps, out);
+                    }
                     HSZG_CHECK_LAUNCH("z scan");
                     return HSZG_OK;
                 }
@@ -590,6 +666,14 @@ static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, 
                 if (ws_bytes < lookback_ws_bytes(g->n_chunks)) break;
                 LBState lb = lookback_carve(ws, tiles);
                 cudaMemsetAsync(ws, 0, lookback_clear_bytes(tiles), st);
+                if (g->n_chunks * kChunkCap == g->n && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+                    const size_t fsmem = kFastTileBytes + stage_bytes(s->max_bitwidth);
+                    allow_smem(k_tile_scan_fast<OutT>, fsmem);
+                    k_tile_scan_fast<OutT><<<(unsigned)tiles, TILE_CHUNKS, fsmem, st>>>(
+                        s->payload, s->payload_len, s->offsets, g->n_chunks, lb, two_eps, out);
+                    HSZG_CHECK_LAUNCH("reconstruct hszp");
+                    return HSZG_OK;
+                }
                 allow_smem(k_tile_scan<OutT>, smem);
                 k_tile_scan<OutT><<<(unsigned)tiles, TILE_CHUNKS, smem, st>>>(sg, s->payload, s->payload_len,
                                                                                s->offsets, lb, two_eps, out);

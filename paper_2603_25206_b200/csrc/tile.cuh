@@ -54,6 +54,19 @@ inline void allow_smem(K kernel, size_t bytes) {
     allow_smem_raw(reinterpret_cast<const void*>(kernel), bytes);
 }
 
+// Band height of the stage-3 HSZP_ND band scan (recon.cu): one band per plane when there are planes
+// enough for two waves of band-scan CTAs (then the z prefix needs no band offsets, which cost it
+// ~60% more time); otherwise whole 256-chunk tiles and >= 16 bands-x-planes per SM.
+inline int64_t recon_band_rows(int64_t n0, int64_t n1, int64_t n2) {
+    if (n0 >= 2 * 148) return n1 > 0 ? n1 : 1;
+    const int64_t cpr = n2 / 32 > 0 ? n2 / 32 : 1;
+    const int64_t rpt = TILE_CHUNKS / cpr > 0 ? TILE_CHUNKS / cpr : 1;
+    const int64_t want = (16 * 148 + (n0 > 0 ? n0 : 1) - 1) / (n0 > 0 ? n0 : 1);   // bands per plane
+    int64_t br = (n1 + want - 1) / want;
+    br = (br + rpt - 1) / rpt * rpt;
+    return br > 0 ? br : 1;
+}
+
 // ---- fast full-chunk decode (K-DEC fast path) -------------------------------------------------
 // Tiles of the fused window kernels hold each 32-value chunk in kChunkStride words: 16-byte aligned,
 // so a thread writes its chunk with 16-byte shared stores (8 threads of a store phase hit 8

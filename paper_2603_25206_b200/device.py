@@ -291,25 +291,38 @@ def sums_combine(parts_buf, n, out=None):
     return out
 
 
-def region_reduce(q, region):
-    """Per-region exact (S1, S2, qmin, qmax, size) over an int32 grid (N2-N4)."""
+REGION_WORDS = 9   # 8-byte words per region in region_buffer (+1 trailing word: the crossing count)
+
+
+def region_buffer(nr):
+    """One int64 device buffer holding every per-region output, so the host reads it in one copy:
+    words [k*nr, (k+1)*nr) for k = 0 s1, 1 s2 low, 2 s2 high, 3 size, 4 mean, 5 var, 6 vmin, 7 vmax
+    (float64 bits), 8 qmin|qmax (2*nr int32), then the count."""
+    return _t().empty(REGION_WORDS * nr + 1, dtype=_t().int64, device=_lib.device())
+
+
+def region_views(buf, nr):
     t = _t()
+    w = [buf[k * nr:(k + 1) * nr] for k in range(REGION_WORDS)]
+    mm = w[8].view(t.int32)
+    return dict(s1=w[0], s2lo=w[1], s2hi=w[2], size=w[3], mean=w[4].view(t.float64), var=w[5].view(t.float64),
+                vmin=w[6].view(t.float64), vmax=w[7].view(t.float64), qmin=mm[:nr], qmax=mm[nr:],
+                count=buf[REGION_WORDS * nr:])
+
+
+def region_reduce(q, region, buf=None):
+    """Per-region exact (S1, S2, qmin, qmax, size) over an int32 grid (N2-N4), into region_buffer."""
     dims = tuple(q.shape)
     nd = len(dims)
     reg = tuple(min(int(r), int(n)) for r, n in zip(region, dims))
     grid = tuple(-(-n // r) for n, r in zip(dims, reg))
     nr = int(np.prod(grid))
-    dev = _lib.device()
-    s1 = t.empty(nr, dtype=t.int64, device=dev)
-    s2lo = t.empty(nr, dtype=t.int64, device=dev)
-    s2hi = t.empty(nr, dtype=t.int64, device=dev)
-    qmin = t.empty(nr, dtype=t.int32, device=dev)
-    qmax = t.empty(nr, dtype=t.int32, device=dev)
-    size = t.empty(nr, dtype=t.int64, device=dev)
+    buf = region_buffer(nr) if buf is None else buf
+    v = region_views(buf, nr)
     dims_arr = (ctypes.c_int64 * 3)(*(list(dims) + [1] * (3 - nd)))
     reg_arr = (ctypes.c_int64 * 3)(*(list(reg) + [1] * (3 - nd)))
     qc = q.contiguous()
     _lib.call("hszg_region_reduce", _lib.ptr(qc), nd, ctypes.cast(dims_arr, ctypes.c_void_p),
-              ctypes.cast(reg_arr, ctypes.c_void_p), _lib.ptr(s1), _lib.ptr(s2lo), _lib.ptr(s2hi), _lib.ptr(qmin),
-              _lib.ptr(qmax), _lib.ptr(size), _lib.stream_handle())
-    return grid, s1, s2lo, s2hi, qmin, qmax, size
+              ctypes.cast(reg_arr, ctypes.c_void_p), _lib.ptr(v["s1"]), _lib.ptr(v["s2lo"]), _lib.ptr(v["s2hi"]),
+              _lib.ptr(v["qmin"]), _lib.ptr(v["qmax"]), _lib.ptr(v["size"]), _lib.stream_handle())
+    return grid, buf, v

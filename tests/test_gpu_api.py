@@ -158,7 +158,7 @@ def test_compress_rejects_nan(H):
 
 
 @pytest.mark.parametrize("kind", ALL)
-@pytest.mark.parametrize("dims", [(64,), (12, 10), (6, 7, 8), (37, 3, 41), (5, 9, 64), (3, 17, 256), (3, 17, 96), (4, 25, 384)])
+@pytest.mark.parametrize("dims", [(64,), (12, 10), (6, 7, 8), (37, 3, 41), (5, 9, 64), (3, 17, 256), (3, 17, 96), (4, 25, 384), (300, 3, 64)])
 def test_stage_composition_and_error_bound(H, rng, kind, dims):
     if kind in ND and len(dims) < 2:
         pytest.skip("nd compressor needs 2D+")
@@ -263,7 +263,7 @@ def test_exact_helpers(H, example_field):
 
 
 @pytest.mark.parametrize("kind", ALL)
-@pytest.mark.parametrize("dims", [(97,), (17, 13), (7, 6, 11), (64, 40, 30), (4, 9, 128), (3, 21, 160)])
+@pytest.mark.parametrize("dims", [(97,), (17, 13), (7, 6, 11), (64, 40, 30), (4, 9, 128), (3, 21, 160), (16, 24, 64), (4096,)])
 def test_stats_vs_oracle(H, rng, kind, dims):
     if kind in ND and len(dims) < 2:
         pytest.skip("nd compressor needs 2D+")
@@ -281,6 +281,23 @@ def test_stats_vs_oracle(H, rng, kind, dims):
                 assert got == pytest.approx(want, rel=1e-12), (st, op)
             else:
                 assert got == want, (st, op, got, want)
+
+
+@pytest.mark.parametrize("kind", [2, 3])
+@pytest.mark.parametrize("dims", [(16, 24, 64), (8192,)])
+def test_stats_wide_residuals(H, rng, kind, dims):
+    """Residuals of 28-31 bits (the block-mean reduction's 128-bit path) and small ones in one
+    stream: var / mean at stages 2 and 3 vs the oracle."""
+    if kind == 3 and len(dims) < 2:
+        pytest.skip("nd compressor needs 2D+")
+    field = (rng.standard_normal(dims) * 1e9).astype(np.float32)
+    field.reshape(-1)[: field.size // 2] *= 1e-6            # half the chunks narrow, half wide
+    c = H.h.compress(field, H.h.CompressorKind(kind), H.h.ErrorBound("abs", 1.0))
+    oc = _oracle_of(c)
+    assert max(oc.payload[int(o)] for o in oc.offsets) >= 28
+    for st in (2, 3):
+        for op in ("mean", "var"):
+            assert H.stats.compute_stat(c, op, H.h.Stage(st)).value == O.compute_stat(oc, op, st), (st, op)
 
 
 def test_std_at_meta_rejected(H, rng):
@@ -346,7 +363,11 @@ def test_curl_rigid_rotation(H):
 # ---- N2-N5 (regions) ----------------------------------------------------------------------
 
 
-@pytest.mark.parametrize("dims,region", [((40, 50, 60), 16), ((33, 17, 20), 8), ((70, 90), (16, 16)), ((50, 21, 9), (5, 7, 3))])
+# row-streaming kernel (R2 in 4..128, a power of two, n2 % 4 == 0): 40x50x60/16, 33x17x20/8, 9x13x516,
+# 6x40x64, 70x92; the others take the one-CTA-per-region kernel
+@pytest.mark.parametrize("dims,region", [((40, 50, 60), 16), ((33, 17, 20), 8), ((70, 90), (16, 16)),
+                                         ((50, 21, 9), (5, 7, 3)), ((9, 13, 516), (3, 5, 128)),
+                                         ((6, 40, 64), (4, 3, 4)), ((70, 92), (16, 32))])
 @pytest.mark.parametrize("kind", [1, 3])
 def test_regions_vs_oracle(H, rng, kind, dims, region):
     field = O.random_field(rng, dims, "smooth")
@@ -366,6 +387,26 @@ def test_regions_vs_oracle(H, rng, kind, dims, region):
     assert rs.crossing_count == O.threshold_count(q, c.eps, region, float(np.median(field)))
     g = H.regions.gradient_magnitude(c)
     np.testing.assert_array_equal(g, O.gradient_magnitude(q, c.eps))
+
+
+@pytest.mark.parametrize("dims,region", [((6, 10, 256), (3, 4, 128)), ((5, 9, 20), 8), ((7, 9, 11), 4)])
+def test_region_reduce_extreme_values(H, rng, dims, region):
+    """|q| near 2^31: per-region S2 beyond 2^64 (int128 path) in both K-REG kernels."""
+    import torch
+
+    q = rng.integers(-2**31, 2**31, size=dims, dtype=np.int64)
+    q[0, 0, :4] = -2**31
+    q = q.astype(np.int32)
+    r = H.regions.region_reduce_device(torch.from_numpy(q).cuda(), 1e-3, region)
+    s1, s2, qmin, qmax, size = O.region_reduce(q, region)
+    g = r["grid"]
+    assert np.array_equal(r["s1"].cpu().numpy().reshape(g), s1.astype(np.int64))
+    lo = r["s2lo"].cpu().numpy().view(np.uint64).ravel()
+    hi = r["s2hi"].cpu().numpy().ravel()
+    assert [(int(h) << 64) | int(l) for h, l in zip(hi, lo)] == [int(v) for v in s2.ravel()]
+    assert np.array_equal(r["qmin"].cpu().numpy().reshape(g), qmin)
+    assert np.array_equal(r["qmax"].cpu().numpy().reshape(g), qmax)
+    assert np.array_equal(r["size"].cpu().numpy().reshape(g), size)
 
 
 # ---- a configuration-1-sized field (1800x3600, BASELINE configs[0]) ---------------------------

@@ -64,3 +64,20 @@ def test_vector_matches_scalar(shape, op, domain, dtype):
         want = O.derivative_q(q, eps[0]) if op == "deriv" else O.laplacian_q(q, eps[0])
         for a, w in zip(fast, want):
             assert np.array_equal(a.cpu().numpy(), w)
+
+
+@pytest.mark.parametrize("n", [1, 7, 4096, 1 << 20, (1 << 20) + 13])
+def test_reduce_i32_extreme_values(n):
+    """K-STAT over int32 arrays with |q| near 2^31 (squares near 2^62, pair sums near 2^63): exact."""
+    import torch
+
+    from paper_2603_25206_b200 import _lib, device as devmod
+
+    rng = np.random.default_rng(n)
+    x = rng.integers(-2**31, 2**31, size=n, dtype=np.int64)
+    x[: min(n, 8)] = -2**31
+    x32 = x.astype(np.int32)
+    s = _lib.read_sums(devmod.reduce_i32(torch.from_numpy(x32).cuda()))
+    assert s.s1 == int(x.sum())
+    assert s.s2 == sum(int(v) * int(v) for v in x.tolist())
+    assert s.vmin == int(x.min()) and s.vmax == int(x.max()) and s.count == n
