@@ -231,6 +231,83 @@ __global__ void k_encode_pack(Spans spans, int64_t n_chunks, const int32_t* vals
     }
 }
 
+// Full-chunk fast path (every chunk holds 32 values: chunk c = stream values 32c .. 32c+31): one
+// warp per chunk, lane j owns value j — coalesced 128-B loads, the bit width by a warp max, the sign
+// bitmap by a ballot (bit j = value j, LSB-first bytes as _bitpack.pyx:24-87), the magnitudes
+// OR-ed into bw shared words at bit j*bw (LSB-first), then the chunk's bytes stored by the lanes.
+constexpr int ENC_WARPS = 8;                 // warps per CTA
+constexpr int ENC_UNROLL = 4;                // chunks per warp per step (loads in flight)
+
+__global__ void __launch_bounds__(ENC_WARPS * 32) k_encode_sizes_full(int64_t n_chunks, const int32_t* __restrict__ vals,
+                                                                     uint64_t* sizes, uint8_t* bws,
+                                                                     unsigned long long* bad) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c0 = w0 * ENC_UNROLL; c0 < n_chunks; c0 += nw * ENC_UNROLL) {
+        int32_t v[ENC_UNROLL];
+#pragma unroll
+        for (int u = 0; u < ENC_UNROLL; u++) v[u] = c0 + u < n_chunks ? __ldg(vals + (c0 + u) * kChunkCap + lane) : 0;
+#pragma unroll
+        for (int u = 0; u < ENC_UNROLL; u++) {
+            const int64_t c = c0 + u;
+            if (c >= n_chunks) break;
+            const uint32_t mag = v[u] < 0 ? 0u - (uint32_t)v[u] : (uint32_t)v[u];
+            const uint32_t mx = __reduce_max_sync(0xffffffffu, mag);
+            if (__any_sync(0xffffffffu, v[u] == INT32_MIN) && lane == 0) atomicMin(bad, (unsigned long long)c);
+            if (lane == 0) {
+                const int bw = mx ? 32 - __clz(mx) : 0;
+                bws[c] = (uint8_t)bw;
+                sizes[c] = (uint64_t)chunk_bytes(kChunkCap, bw);
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(ENC_WARPS * 32) k_encode_pack_full(int64_t n_chunks, const int32_t* __restrict__ vals,
+                                                                    const uint64_t* __restrict__ offsets,
+                                                                    const uint8_t* __restrict__ bws, uint8_t* payload) {
+    __shared__ uint32_t sw[ENC_WARPS][36];   // [0] pad, [1] sign bitmap, [2..] packed words (+1 spill)
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    uint32_t* w = sw[wib];
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c0 = w0 * ENC_UNROLL; c0 < n_chunks; c0 += nw * ENC_UNROLL) {
+        int32_t v[ENC_UNROLL];
+#pragma unroll
+        for (int u = 0; u < ENC_UNROLL; u++) v[u] = c0 + u < n_chunks ? __ldg(vals + (c0 + u) * kChunkCap + lane) : 0;
+#pragma unroll
+        for (int u = 0; u < ENC_UNROLL; u++) {
+            const int64_t c = c0 + u;
+            if (c >= n_chunks) break;
+            const int bw = __ldg(bws + c);
+            uint8_t* out = payload + __ldg(offsets + c);
+            if (bw == 0) {                                   // the bit-width byte only
+                if (lane == 0) out[0] = 0;
+                continue;
+            }
+            const uint32_t mag = v[u] < 0 ? 0u - (uint32_t)v[u] : (uint32_t)v[u];
+            const uint32_t sgn = __ballot_sync(0xffffffffu, v[u] < 0);
+            // the chunk's bytes laid out contiguously from byte 3 of w: bw, 4 sign bytes, packed words
+            w[2 + lane] = 0;
+            if (lane == 0) {
+                w[0] = (uint32_t)bw << 24;
+                w[1] = sgn;
+            }
+            __syncwarp();
+            const uint32_t bit = (uint32_t)(lane * bw);
+            const uint32_t wi = 2 + (bit >> 5), sh = bit & 31;
+            atomicOr(&w[wi], mag << sh);
+            if (sh + bw > 32) atomicOr(&w[wi + 1], mag >> (32 - sh));
+            __syncwarp();
+            const uint8_t* wb = reinterpret_cast<const uint8_t*>(w) + 3;
+            const int total = 5 + 4 * bw;                    // bw byte + 4 sign bytes + 32*bw bits
+            for (int k = lane; k < total; k += 32) out[k] = wb[k];
+            __syncwarp();                                    // w is reused by the next chunk
+        }
+    }
+}
+
 }  // namespace hszg
 
 using namespace hszg;
@@ -360,7 +437,8 @@ extern "C" int hszg_decode_spans(const uint8_t* payload, uint64_t len, const int
 
 template <class Spans>
 static int encode_sizes_impl(Spans sp, int64_t n_chunks, const int32_t* vals, uint64_t* offsets, uint8_t* bws,
-                             uint64_t* total_host, void* ws, size_t ws_bytes, cudaStream_t st, HszgErr* err) {
+                             uint64_t* total_host, void* ws, size_t ws_bytes, cudaStream_t st, HszgErr* err,
+                             bool full = false) {
     // workspace: [bad u64][total u64][scan state]
     const size_t need = 16 + lookback_ws_bytes(n_chunks);
     if (ws_bytes < need) {
@@ -375,7 +453,12 @@ static int encode_sizes_impl(Spans sp, int64_t n_chunks, const int32_t* vals, ui
     cudaMemcpyAsync(bad, &none, 8, cudaMemcpyHostToDevice, st);
     if (n_chunks > 0) {
         // sizes are written into `offsets`, then scanned in place (exclusive)
-        k_encode_sizes<Spans><<<grid_for(n_chunks, 256, 148 * 64), 256, 0, st>>>(sp, n_chunks, vals, offsets, bws, bad);
+        if (full)
+            k_encode_sizes_full<<<grid_for(n_chunks, ENC_WARPS * ENC_UNROLL, 148 * 16), ENC_WARPS * 32, 0, st>>>(
+                n_chunks, vals, offsets, bws, bad);
+        else
+            k_encode_sizes<Spans><<<grid_for(n_chunks, 256, 148 * 64), 256, 0, st>>>(sp, n_chunks, vals, offsets, bws,
+                                                                                     bad);
         HSZG_CHECK_LAUNCH("encode_sizes");
         int r = exclusive_scan_u64(offsets, offsets, n_chunks, total, scan_ws, st);
         if (r) return hszg_set_cuda_error(err, cudaGetLastError(), "encode scan");
@@ -419,15 +502,19 @@ extern "C" int hszg_encode_sizes(const HszgGeom* g, const int32_t* p, uint64_t* 
                                  uint64_t* total_host, void* ws, size_t ws_bytes, void* stream, HszgErr* err) {
     err->status = HSZG_OK;
     return encode_sizes_impl(GeoSpans{make_seggeo(*g)}, g->n_chunks, p, offsets, bitwidths, total_host, ws, ws_bytes,
-                             as_stream(stream), err);
+                             as_stream(stream), err, g->n_chunks * kChunkCap == g->n);
 }
 
 extern "C" int hszg_encode_pack(const HszgGeom* g, const int32_t* p, const uint64_t* offsets,
                                 const uint8_t* bitwidths, uint8_t* payload, void* stream, HszgErr* err) {
     err->status = HSZG_OK;
     if (g->n_chunks == 0) return HSZG_OK;
-    k_encode_pack<GeoSpans><<<grid_for(g->n_chunks, 256, 148 * 64), 256, 0, as_stream(stream)>>>(
-        GeoSpans{make_seggeo(*g)}, g->n_chunks, p, offsets, bitwidths, payload);
+    if (g->n_chunks * kChunkCap == g->n)
+        k_encode_pack_full<<<grid_for(g->n_chunks, ENC_WARPS * ENC_UNROLL, 148 * 16), ENC_WARPS * 32, 0,
+                             as_stream(stream)>>>(g->n_chunks, p, offsets, bitwidths, payload);
+    else
+        k_encode_pack<GeoSpans><<<grid_for(g->n_chunks, 256, 148 * 64), 256, 0, as_stream(stream)>>>(
+            GeoSpans{make_seggeo(*g)}, g->n_chunks, p, offsets, bitwidths, payload);
     HSZG_CHECK_LAUNCH("encode_pack");
     return HSZG_OK;
 }

@@ -8,6 +8,7 @@
 // The chunk encoder proper (bit widths, scan, pack) lives in codec.cu.
 #include <cstdio>
 #include <cfloat>
+#include <type_traits>
 #include "common.cuh"
 
 namespace hszg {
@@ -110,36 +111,299 @@ __global__ void k_decor_lorenzo(const int32_t* q, int64_t N0, int64_t N1, int64_
     if (f) atomicOr(flags, f);
 }
 
-// HSZX / HSZX_ND: one warp per segment; truncated integer mean; p in stream order
-__global__ void k_decor_blockmean(SegGeo sg, const int32_t* q, int32_t* p, int32_t* meta, unsigned int* flags) {
+// HSZX 1-D with segments of B | 32 values (B a power of two): one value per lane, the B lanes of a
+// segment reduce by xor-shuffles inside their aligned group (no per-segment index arithmetic); four
+// 32-value groups per warp and step (loads in flight), 32-bit sums when every |q| < 2^26.
+__device__ __forceinline__ int64_t trunc_div(int64_t s, int size, int lgB, bool full) {
+    if (full) return s >= 0 ? (s >> lgB) : -((-s) >> lgB);       // truncation toward zero
+    return (s >= INT32_MIN && s <= INT32_MAX) ? (int64_t)((int32_t)s / size) : s / size;
+}
+
+__global__ void k_decor_blockmean_1d(const int32_t* __restrict__ q, int64_t n, int lgB, int32_t* __restrict__ p,
+                                     int32_t* __restrict__ meta, unsigned int* flags) {
+    constexpr int U = 4;
+    const int lane = threadIdx.x & 31;
+    const int B = 1 << lgB;
+    unsigned int f = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * U;
+    for (int64_t base = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~(int64_t)31) * U; base < n;
+         base += stride) {
+        int32_t v[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int64_t i = base + u * 32 + lane;
+            v[u] = i < n ? __ldg(q + i) : 0;
+        }
+        bool narrow = true;
+#pragma unroll
+        for (int u = 0; u < U; u++) narrow = narrow && v[u] > -(1 << 26) && v[u] < (1 << 26);
+        narrow = __all_sync(0xffffffffu, narrow);
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int64_t i = base + u * 32 + lane;
+            int64_t sum;
+            if (narrow) {
+                int32_t s32 = v[u];
+                for (int d = 1; d < B; d <<= 1) s32 += __shfl_xor_sync(0xffffffffu, s32, d);
+                sum = s32;
+            } else {
+                sum = v[u];
+                for (int d = 1; d < B; d <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, d);
+            }
+            if (i < n) {
+                const int64_t seg0 = i - (lane & (B - 1));
+                const bool full = seg0 + B <= n;
+                const int64_t mean = trunc_div(sum, full ? B : (int)(n - seg0), lgB, full);
+                if ((lane & (B - 1)) == 0) meta[seg0 >> lgB] = (int32_t)mean;
+                const int64_t d = (int64_t)v[u] - mean;
+                if (d > kPmax || d < -kPmax) f |= 1u;
+                p[i] = (int32_t)d;
+            }
+        }
+    }
+    if (f) atomicOr(flags, f);
+}
+
+// ---- vectorised variants (16-B aligned arrays): four values per thread and step -----------------
+
+__device__ __forceinline__ int32_t quant1(double d, double recip, unsigned int& f) {
+    const double s = floor(__dadd_rn(__dmul_rn(d, recip), 0.5));
+    if (fabs(s) > (double)kQmax) f |= 1u;
+    if (s != s) f |= 2u;
+    return (fabs(s) <= (double)kQmax) ? (int32_t)s : 0;
+}
+
+__global__ void k_quantize_f32x4(const float4* __restrict__ x, int64_t n4, double recip, int4* __restrict__ q,
+                                 unsigned int* flags) {
+    unsigned int f = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (; i + stride < n4; i += 2 * stride) {                 // two 16-B loads in flight
+        const float4 a = __ldg(x + i), b = __ldg(x + i + stride);
+        q[i] = make_int4(quant1(a.x, recip, f), quant1(a.y, recip, f), quant1(a.z, recip, f), quant1(a.w, recip, f));
+        q[i + stride] =
+            make_int4(quant1(b.x, recip, f), quant1(b.y, recip, f), quant1(b.z, recip, f), quant1(b.w, recip, f));
+    }
+    for (; i < n4; i += stride) {
+        const float4 a = __ldg(x + i);
+        q[i] = make_int4(quant1(a.x, recip, f), quant1(a.y, recip, f), quant1(a.z, recip, f), quant1(a.w, recip, f));
+    }
+    if (f) atomicOr(flags, f);
+}
+
+__device__ __forceinline__ int32_t diff1(int64_t a, int64_t b, unsigned int& f) {
+    const int64_t d = a - b;
+    if (d > kPmax || d < -kPmax) f |= 1u;
+    return (int32_t)d;
+}
+
+// HSZP on 4-value groups: the previous value of a group's first element is the previous lane's .w
+__global__ void k_decor_prev_x4(const int4* __restrict__ q, int64_t n4, int4* __restrict__ p, unsigned int* flags) {
+    unsigned int f = 0;
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n4; base += stride) {
+        const int64_t i = base + threadIdx.x;
+        const bool act = i < n4;
+        const int4 v = act ? __ldg(q + i) : make_int4(0, 0, 0, 0);
+        int prev = __shfl_up_sync(0xffffffffu, v.w, 1);
+        if (lane == 0) prev = (act && i > 0) ? __ldg(reinterpret_cast<const int32_t*>(q) + 4 * i - 1) : 0;
+        if (act)
+            p[i] = make_int4(diff1(v.x, prev, f), diff1(v.y, v.x, f), diff1(v.z, v.y, f), diff1(v.w, v.z, f));
+    }
+    if (f) atomicOr(flags, f);
+}
+
+// HSZP_ND 3-D (box view) on 4 x-consecutive points: p = sum over the 2^3 lower corners with signs,
+// written as the x-differences of the rows (z,y), (z,y-1), (z-1,y), (z-1,y-1); x-1 by shuffle
+__global__ void k_decor_lorenzo_x4(const int32_t* __restrict__ q, int64_t N0, int64_t N1, int64_t N2,
+                                   int32_t* __restrict__ p, unsigned int* flags) {
+    const int lane = threadIdx.x & 31;
+    const int64_t x = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    const int64_t i1 = blockIdx.y, i0 = blockIdx.z;
+    const bool act = x < N2;
+    const int64_t xi = act ? x : 0;
+    const int64_t plane = N1 * N2;
+    const int32_t* c = q + (i0 * N1 + i1) * N2 + xi;
+    const int4 z4 = make_int4(0, 0, 0, 0);
+    int4 r[4];                         // rows (z,y), (z,y-1), (z-1,y), (z-1,y-1)
+    const bool hy = i1 > 0, hz = i0 > 0;
+    r[0] = act ? __ldg(reinterpret_cast<const int4*>(c)) : z4;
+    r[1] = act && hy ? __ldg(reinterpret_cast<const int4*>(c - N2)) : z4;
+    r[2] = act && hz ? __ldg(reinterpret_cast<const int4*>(c - plane)) : z4;
+    r[3] = act && hy && hz ? __ldg(reinterpret_cast<const int4*>(c - plane - N2)) : z4;
+    int64_t d[4][4];                   // x-difference of each row at the 4 points
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        int left = __shfl_up_sync(0xffffffffu, r[k].w, 1);
+        const int32_t* rowp = c - (k & 1 ? N2 : 0) - (k & 2 ? plane : 0);
+        const bool has = act && (!(k & 1) || hy) && (!(k & 2) || hz);
+        if (lane == 0) left = (has && xi > 0) ? __ldg(rowp - 1) : 0;
+        d[k][0] = (int64_t)r[k].x - left;
+        d[k][1] = (int64_t)r[k].y - r[k].x;
+        d[k][2] = (int64_t)r[k].z - r[k].y;
+        d[k][3] = (int64_t)r[k].w - r[k].z;
+    }
+    if (!act) return;
+    unsigned int f = 0;
+    int32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        const int64_t acc = d[0][j] - d[1][j] - d[2][j] + d[3][j];
+        if (acc > kPmax || acc < -kPmax) f |= 1u;
+        o[j] = (int32_t)acc;
+    }
+    *reinterpret_cast<int4*>(p + (i0 * N1 + i1) * N2 + xi) = make_int4(o[0], o[1], o[2], o[3]);
+    if (f) atomicOr(flags, f);
+}
+
+// HSZX / HSZX_ND: one warp per segment; truncated integer mean; p in stream order.  Lane l walks the
+// segment's values l, l+32, ... in stream (block row-major) order with incrementally advanced 32-bit
+// (z, y, x) offsets — no per-value division; the second pass re-reads the segment from L1/L2.
+// Full blocks (every n[a] % B[a] == 0, B2 % 4 == 0, 32 | B0*B1*B2 <= 8192): the mirror of recon.cu's
+// k_tile_blocks_fast — a CTA loads a (B0, B1, k*B2) box of q with 16-B row-major loads into shared
+// memory in stream (block-contiguous) order, then each warp reduces whole blocks from shared memory
+// and stores p with 16-B stores.  k = 8192 / |block| blocks along x per tile.
+constexpr int BT_THREADS = 256, BT_ELEMS = 8192;
+
+__global__ void __launch_bounds__(BT_THREADS) k_decor_blockmean_tiles(SegGeo sg, int64_t tpr, int kb,
+                                                                      const int32_t* __restrict__ q,
+                                                                      int32_t* __restrict__ p,
+                                                                      int32_t* __restrict__ meta, unsigned int* flags) {
+    __shared__ __align__(16) int32_t tile[BT_ELEMS];
+    const int B0 = (int)sg.B[0], B1 = (int)sg.B[1], B2 = (int)sg.B[2];
+    const int segsz = B0 * B1 * B2;
+    const int64_t row = blockIdx.x / tpr;                      // block row (b0, b1)
+    const int64_t b2a = (blockIdx.x - row * tpr) * kb;
+    const int nseg = (int)(sg.G[2] - b2a < kb ? sg.G[2] - b2a : kb);
+    const int64_t b0 = row / sg.G[1], b1 = row - b0 * sg.G[1];
+    const int64_t n1 = sg.n[1], n2 = sg.n[2];
+    const int gpr = nseg * B2 / 4;                             // int4 columns of the box
+    const int rows = B0 * B1;
+    const int32_t* qb = q + (b0 * B0 * n1 + b1 * B1) * n2 + b2a * B2;
+    for (int i = threadIdx.x; i < rows * gpr; i += BT_THREADS) {
+        const int zy = i / gpr, g = i - zy * gpr;
+        const int zl = zy / B1, yl = zy - zl * B1;
+        const int x = 4 * g, t = x / B2, xl = x - t * B2;
+        const int4 v = __ldg(reinterpret_cast<const int4*>(qb + ((int64_t)zl * n1 + yl) * n2 + x));
+        *reinterpret_cast<int4*>(tile + t * segsz + zy * B2 + xl) = v;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned int f = 0;
+    const int64_t seg0 = row * sg.G[2] + b2a;                   // segment index of the tile's first block
+    for (int t = warp; t < nseg; t += BT_THREADS / 32) {
+        const int32_t* tb = tile + t * segsz;
+        int64_t sum = 0;
+        for (int j = lane; j < segsz / 4; j += 32) {
+            const int4 v = *reinterpret_cast<const int4*>(tb + 4 * j);
+            sum += (int64_t)v.x + v.y + v.z + v.w;
+        }
+        for (int d = 16; d > 0; d >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, d);
+        const int64_t mean = (sum >= INT32_MIN && sum <= INT32_MAX) ? (int64_t)((int32_t)sum / segsz) : sum / segsz;
+        if (lane == 0) meta[seg0 + t] = (int32_t)mean;
+        int4* pb = reinterpret_cast<int4*>(p + (seg0 + t) * segsz);
+        for (int j = lane; j < segsz / 4; j += 32) {
+            const int4 v = *reinterpret_cast<const int4*>(tb + 4 * j);
+            int32_t o[4];
+            const int32_t a[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                const int64_t d = (int64_t)a[e] - mean;
+                if (d > kPmax || d < -kPmax) f |= 1u;
+                o[e] = (int32_t)d;
+            }
+            pb[j] = make_int4(o[0], o[1], o[2], o[3]);
+        }
+    }
+    if (f) atomicOr(flags, f);
+}
+
+constexpr int BM_REG = 16;   // segments of <= 512 values (8^3, 8x8) are held in registers
+
+__global__ void k_decor_blockmean(SegGeo sg, const int32_t* __restrict__ q, int32_t* __restrict__ p,
+                                  int32_t* __restrict__ meta, unsigned int* flags) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t nb = sg.G[0] * sg.G[1] * sg.G[2];
+    const int64_t n1 = sg.n[1], n2 = sg.n[2];
     unsigned int f = 0;
+    const bool small = nb < INT32_MAX;                // 32-bit segment-index arithmetic
+    const uint32_t G1 = (uint32_t)sg.G[1], G2 = (uint32_t)sg.G[2];
     for (int64_t b = warp; b < nb; b += nwarps) {
-        const int64_t b2 = b % sg.G[2];
-        const int64_t r = b / sg.G[2];
-        const int64_t b1 = r % sg.G[1];
-        const int64_t b0 = r / sg.G[1];
-        const int64_t s0 = seg_ext(sg, 0, b0), s1 = seg_ext(sg, 1, b1), s2 = seg_ext(sg, 2, b2);
-        const int64_t size = s0 * s1 * s2;
-        const int64_t z0 = b0 * sg.B[0], y0 = b1 * sg.B[1], x0 = b2 * sg.B[2];
+        int64_t b0, b1, b2;
+        if (small) {
+            const uint32_t bb = (uint32_t)b, r = bb / G2;
+            b2 = bb - r * G2;
+            b1 = r % G1;
+            b0 = r / G1;
+        } else {
+            b2 = b % sg.G[2];
+            const int64_t r = b / sg.G[2];
+            b1 = r % sg.G[1];
+            b0 = r / sg.G[1];
+        }
+        const int s0 = (int)seg_ext(sg, 0, b0), s1 = (int)seg_ext(sg, 1, b1), s2 = (int)seg_ext(sg, 2, b2);
+        const int size = s0 * s1 * s2;
+        const int32_t* qb = q + (b0 * sg.B[0] * n1 + b1 * sg.B[1]) * n2 + b2 * sg.B[2];
+        // lane's first value and the per-step advance of 32 values, as (z, y, x) within the segment
+        const int zl0 = lane / (s1 * s2), rem0 = lane - zl0 * s1 * s2;
+        const int yl0 = rem0 / s2, xl0 = rem0 - yl0 * s2;
+        auto walk = [&](auto&& body) {
+            int zl = zl0, yl = yl0, xl = xl0;
+            for (int l = lane; l < size; l += 32) {
+                body(l, qb + ((int64_t)zl * n1 + yl) * n2 + xl);
+                xl += 32;
+                while (xl >= s2) {
+                    xl -= s2;
+                    if (++yl == s1) {
+                        yl = 0;
+                        ++zl;
+                    }
+                }
+            }
+        };
+        int32_t* pb = p + seg_elem_start(sg, b0, b1, b2);
+        if (size <= 32 * BM_REG && s2 <= 32 && !(s2 & (s2 - 1)) && !(s1 & (s1 - 1))) {
+            // power-of-two rows (8^3, 8x8 blocks): the whole segment in registers, value l = lane + 32k at
+            // (z, y, x) = (r >> lg1, r & (s1-1), l & (s2-1)) with r = l >> lg2 — BM_REG independent loads
+            // in flight per lane, one read of q
+            const int lg2 = __ffs(s2) - 1, lg1 = __ffs(s1) - 1;
+            int32_t v[BM_REG];
+#pragma unroll
+            for (int k = 0; k < BM_REG; k++) {
+                const int l = lane + 32 * k;
+                const int r = l >> lg2;
+                v[k] = l < size ? __ldg(qb + ((int64_t)(r >> lg1) * n1 + (r & (s1 - 1))) * n2 + (l & (s2 - 1))) : 0;
+            }
+            int64_t sum = 0;
+#pragma unroll
+            for (int k = 0; k < BM_REG; k++) sum += v[k];
+            for (int d = 16; d > 0; d >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, d);
+            const int64_t mean = (sum >= INT32_MIN && sum <= INT32_MAX) ? (int64_t)((int32_t)sum / size) : sum / size;
+            if (lane == 0) meta[b] = (int32_t)mean;
+#pragma unroll
+            for (int k = 0; k < BM_REG; k++) {
+                if (lane + 32 * k < size) {
+                    const int64_t d = (int64_t)v[k] - mean;
+                    if (d > kPmax || d < -kPmax) f |= 1u;
+                    pb[lane + 32 * k] = (int32_t)d;
+                }
+            }
+            continue;
+        }
         int64_t sum = 0;
-        for (int64_t l = lane; l < size; l += 32) {
-            const int64_t zl = l / (s1 * s2), rem = l - zl * s1 * s2, yl = rem / s2, xl = rem - yl * s2;
-            sum += q[((z0 + zl) * sg.n[1] + (y0 + yl)) * sg.n[2] + x0 + xl];
-        }
+        walk([&](int, const int32_t* a) { sum += __ldg(a); });
         for (int d = 16; d > 0; d >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, d);
-        const int64_t mean = sum / size;   // C division truncates toward zero (compressors.py:134-138)
+        // C division truncates toward zero (compressors.py:134-138); 32-bit when the sum fits
+        const int64_t mean = (sum >= INT32_MIN && sum <= INT32_MAX) ? (int64_t)((int32_t)sum / size) : sum / size;
         if (lane == 0) meta[b] = (int32_t)mean;
-        const int64_t e0 = seg_elem_start(sg, b0, b1, b2);
-        for (int64_t l = lane; l < size; l += 32) {
-            const int64_t zl = l / (s1 * s2), rem = l - zl * s1 * s2, yl = rem / s2, xl = rem - yl * s2;
-            const int64_t d = (int64_t)q[((z0 + zl) * sg.n[1] + (y0 + yl)) * sg.n[2] + x0 + xl] - mean;
+        walk([&](int l, const int32_t* a) {
+            const int64_t d = (int64_t)__ldg(a) - mean;
             if (d > kPmax || d < -kPmax) f |= 1u;
-            p[e0 + l] = (int32_t)d;
-        }
+            pb[l] = (int32_t)d;
+        });
     }
     if (f) atomicOr(flags, f);
 }
@@ -150,6 +414,7 @@ using namespace hszg;
 
 int hszg_set_cuda_error(HszgErr* err, cudaError_t e, const char* where);
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 template <typename T>
 static int minmax_impl(const T* field, int64_t n, double* out_dev, int64_t* nonfinite_dev, void* ws,
@@ -186,7 +451,14 @@ static int quantize_impl(const T* field, int64_t n, double recip, int32_t* q, vo
     if (ws_bytes < 4) return HSZG_INVALID_ARG;
     unsigned int* flags = reinterpret_cast<unsigned int*>(ws);
     cudaMemsetAsync(flags, 0, 4, st);
-    if (n > 0) k_quantize<T><<<grid_for(n, 256 * 4, 148 * 32), 256, 0, st>>>(field, n, recip, q, flags);
+    const bool vec = std::is_same<T, float>::value && n % 4 == 0 && (reinterpret_cast<uintptr_t>(field) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(q) & 15) == 0;
+    if (n > 0 && vec)
+        k_quantize_f32x4<<<grid_for(n / 4, 256 * 4, 148 * 16), 256, 0, st>>>(reinterpret_cast<const float4*>(field),
+                                                                             n / 4, recip, reinterpret_cast<int4*>(q),
+                                                                             flags);
+    else if (n > 0)
+        k_quantize<T><<<grid_for(n, 256 * 4, 148 * 32), 256, 0, st>>>(field, n, recip, q, flags);
     unsigned int h = 0;
     int r = read_flags(flags, &h, st, err);
     if (r) return r;
@@ -224,7 +496,11 @@ extern "C" int hszg_decorrelate(const HszgGeom* g, const int32_t* q, int32_t* p,
     if (g->n > 0) {
         switch (g->kind) {
             case HSZG_HSZP:
-                k_decor_prev<<<grid_for(g->n, 256 * 4, 148 * 32), 256, 0, st>>>(q, g->n, p, flags);
+                if (g->n % 4 == 0 && al16(q) && al16(p))
+                    k_decor_prev_x4<<<grid_for(g->n / 4, 256 * 4, 148 * 16), 256, 0, st>>>(
+                        reinterpret_cast<const int4*>(q), g->n / 4, reinterpret_cast<int4*>(p), flags);
+                else
+                    k_decor_prev<<<grid_for(g->n, 256 * 4, 148 * 32), 256, 0, st>>>(q, g->n, p, flags);
                 break;
             case HSZG_HSZP_ND: {
                 int64_t n[3] = {1, 1, 1};
@@ -234,12 +510,33 @@ extern "C" int hszg_decorrelate(const HszgGeom* g, const int32_t* q, int32_t* p,
                     snprintf(err->message, sizeof(err->message), "grid too large for the Lorenzo launch");
                     return HSZG_INVALID_ARG;
                 }
-                dim3 grid((unsigned)((n[2] + 255) / 256), (unsigned)n[1], (unsigned)n[0]);
-                k_decor_lorenzo<<<grid, 256, 0, st>>>(q, n[0], n[1], n[2], p, flags);
+                if (n[2] % 4 == 0 && al16(q) && al16(p)) {
+                    dim3 grid4((unsigned)((n[2] / 4 + 127) / 128), (unsigned)n[1], (unsigned)n[0]);
+                    k_decor_lorenzo_x4<<<grid4, 128, 0, st>>>(q, n[0], n[1], n[2], p, flags);
+                } else {
+                    dim3 grid((unsigned)((n[2] + 255) / 256), (unsigned)n[1], (unsigned)n[0]);
+                    k_decor_lorenzo<<<grid, 256, 0, st>>>(q, n[0], n[1], n[2], p, flags);
+                }
                 break;
             }
             default: {
                 const int64_t nb = sg.G[0] * sg.G[1] * sg.G[2];
+                const int64_t B = sg.B[2];
+                if (sg.n[0] == 1 && sg.n[1] == 1 && B <= 32 && (32 % B) == 0) {
+                    const int lgB = __builtin_ctzll((unsigned long long)B);
+                    k_decor_blockmean_1d<<<grid_for(g->n, 256 * 4, 148 * 16), 256, 0, st>>>(q, g->n, lgB, p, metadata,
+                                                                                          flags);
+                    break;
+                }
+                const int64_t segsz = sg.B[0] * sg.B[1] * sg.B[2];
+                if (sg.n[0] % sg.B[0] == 0 && sg.n[1] % sg.B[1] == 0 && sg.n[2] % sg.B[2] == 0 && sg.B[2] % 4 == 0 &&
+                    segsz % 32 == 0 && segsz <= BT_ELEMS && al16(q) && al16(p) && sg.n[2] % 4 == 0) {
+                    const int kb = (int)(BT_ELEMS / segsz);
+                    const int64_t tpr = (sg.G[2] + kb - 1) / kb;
+                    k_decor_blockmean_tiles<<<(unsigned)(sg.G[0] * sg.G[1] * tpr), BT_THREADS, 0, st>>>(
+                        sg, tpr, kb, q, p, metadata, flags);
+                    break;
+                }
                 k_decor_blockmean<<<grid_for(nb * 32, 256, 148 * 64), 256, 0, st>>>(sg, q, p, metadata, flags);
                 break;
             }
