@@ -308,6 +308,89 @@ __global__ void __launch_bounds__(ENC_WARPS * 32) k_encode_pack_full(int64_t n_c
     }
 }
 
+// Tiled full-chunk packer: one thread per chunk (a warp-instruction packs 32 chunks, not one), its
+// 32 values read from a conflict-free shared tile (36-word stride) filled by coalesced 16-B loads; the
+// chunk's bytes go to a shared staging copy of the tile's contiguous payload range, which the CTA then
+// stores with aligned 16-B vectors (byte stores only at the two range edges shared with neighbours).
+constexpr int PK_STRIDE = 36;
+constexpr size_t PK_VALS_BYTES = (size_t)TILE_CHUNKS * PK_STRIDE * 4;
+inline size_t pack_tile_smem(int max_bw) {
+    return PK_VALS_BYTES + (size_t)TILE_CHUNKS * (size_t)chunk_bytes(kChunkCap, max_bw) + 32;
+}
+
+__global__ void __launch_bounds__(TILE_CHUNKS) k_encode_pack_tiles(int64_t n_chunks, const int32_t* __restrict__ vals,
+                                                                  const uint64_t* __restrict__ offsets,
+                                                                  const uint8_t* __restrict__ bws, uint8_t* payload) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ uint64_t s_lo, s_hi;
+    int32_t* tv = reinterpret_cast<int32_t*>(smem);
+    const int64_t c0 = (int64_t)blockIdx.x * TILE_CHUNKS;
+    const int nch = (int)(n_chunks - c0 < TILE_CHUNKS ? n_chunks - c0 : TILE_CHUNKS);
+    const int4* src = reinterpret_cast<const int4*>(vals + c0 * kChunkCap);
+    for (int i = threadIdx.x; i < nch * 8; i += TILE_CHUNKS)
+        *reinterpret_cast<int4*>(tv + (i >> 3) * PK_STRIDE + ((i & 7) << 2)) = __ldg(src + i);
+    const bool mine = (int)threadIdx.x < nch;
+    uint64_t off = 0;
+    int bw = 0;
+    if (mine) {
+        off = __ldg(offsets + c0 + threadIdx.x);
+        bw = __ldg(bws + c0 + threadIdx.x);
+        if (threadIdx.x == 0) s_lo = off;
+        if ((int)threadIdx.x == nch - 1) s_hi = off + (uint64_t)chunk_bytes(kChunkCap, bw);
+    }
+    __syncthreads();
+    const uint64_t lo = s_lo, hi = s_hi;
+    uint8_t* sb = smem + PK_VALS_BYTES + (lo & 15);          // payload byte g lives at sb[g - lo]
+    if (mine) {
+        uint8_t* o = sb + (off - lo);
+        o[0] = (uint8_t)bw;
+        if (bw) {
+            const int32_t* v = tv + threadIdx.x * PK_STRIDE;
+            uint32_t sgn = 0;
+            uint64_t acc = 0;
+            int nb = 0, k = 5;
+#pragma unroll
+            for (int g = 0; g < 8; g++) {
+                const int4 w = *reinterpret_cast<const int4*>(v + 4 * g);
+                const int32_t a[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    const uint32_t mag = a[e] < 0 ? 0u - (uint32_t)a[e] : (uint32_t)a[e];
+                    sgn |= (uint32_t)(a[e] < 0) << (4 * g + e);
+                    acc |= (uint64_t)mag << nb;
+                    nb += bw;
+                    if (nb >= 32) {                          // emit a full 32-bit group, LSB-first
+                        o[k] = (uint8_t)acc;
+                        o[k + 1] = (uint8_t)(acc >> 8);
+                        o[k + 2] = (uint8_t)(acc >> 16);
+                        o[k + 3] = (uint8_t)(acc >> 24);
+                        k += 4;
+                        acc >>= 32;
+                        nb -= 32;
+                    }
+                }
+            }
+            // 32 * bw bits is a whole number of 32-bit groups: nothing is left in acc
+            o[1] = (uint8_t)sgn;
+            o[2] = (uint8_t)(sgn >> 8);
+            o[3] = (uint8_t)(sgn >> 16);
+            o[4] = (uint8_t)(sgn >> 24);
+        }
+    }
+    __syncthreads();
+    // store [lo, hi): byte edges, aligned 16-B body
+    const uint64_t a0 = (lo + 15) & ~(uint64_t)15, a1 = hi & ~(uint64_t)15;
+    if (a0 >= a1) {
+        for (uint64_t g = lo + threadIdx.x; g < hi; g += TILE_CHUNKS) payload[g] = sb[g - lo];
+        return;
+    }
+    if (lo + threadIdx.x < a0) payload[lo + threadIdx.x] = sb[threadIdx.x];
+    if (a1 + threadIdx.x < hi) payload[a1 + threadIdx.x] = sb[a1 - lo + threadIdx.x];
+    const uint4* sv = reinterpret_cast<const uint4*>(sb + (a0 - lo));
+    uint4* gv = reinterpret_cast<uint4*>(payload + a0);
+    for (uint64_t i = threadIdx.x; i < (a1 - a0) >> 4; i += TILE_CHUNKS) gv[i] = sv[i];
+}
+
 }  // namespace hszg
 
 using namespace hszg;
@@ -509,7 +592,12 @@ extern "C" int hszg_encode_pack(const HszgGeom* g, const int32_t* p, const uint6
                                 const uint8_t* bitwidths, uint8_t* payload, void* stream, HszgErr* err) {
     err->status = HSZG_OK;
     if (g->n_chunks == 0) return HSZG_OK;
-    if (g->n_chunks * kChunkCap == g->n)
+    if (g->n_chunks * kChunkCap == g->n && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+        const size_t smem = pack_tile_smem(32);
+        allow_smem(k_encode_pack_tiles, smem);
+        k_encode_pack_tiles<<<(unsigned)((g->n_chunks + TILE_CHUNKS - 1) / TILE_CHUNKS), TILE_CHUNKS, smem,
+                              as_stream(stream)>>>(g->n_chunks, p, offsets, bitwidths, payload);
+    } else if (g->n_chunks * kChunkCap == g->n)
         k_encode_pack_full<<<grid_for(g->n_chunks, ENC_WARPS * ENC_UNROLL, 148 * 16), ENC_WARPS * 32, 0,
                              as_stream(stream)>>>(g->n_chunks, p, offsets, bitwidths, payload);
     else
