@@ -196,7 +196,7 @@ def curl(sources, stage: Stage, out: str = "numpy", out_dtype=None) -> DerivedFi
 # Out-of-core streaming (Algorithm 3)
 
 
-def streamed_derivative(c: CompressedStream, out: str = "numpy", out_dtype=None) -> DerivedField:
+def streamed_derivative(c: CompressedStream, out: str = "numpy", out_dtype=None, from_host=None) -> DerivedField:
     """Slab-streamed derivative holding at most three quantized slabs (fields.py:243-272).
 
     Each window (prev[-1], cur, nxt[:1]) is assembled on the device and run
@@ -207,9 +207,15 @@ def streamed_derivative(c: CompressedStream, out: str = "numpy", out_dtype=None)
     t = _lib.torch()
     dims = c.shape.dims
     dtype = _dtype(out_dtype)
-    comps = [t.zeros(dims, dtype=dtype, device=_lib.device()) for _ in dims]
+    # out="numpy": the components are filled slab by slab in host memory (with from_host, nothing
+    # field-sized ever lives on the device: the out-of-core use of Algorithm 3)
+    on_host = out != "torch"
+    if on_host:
+        comps = [np.zeros(dims, dtype=np.float32 if dtype == t.float32 else np.float64) for _ in dims]
+    else:
+        comps = [t.zeros(dims, dtype=dtype, device=_lib.device()) for _ in dims]
     row = 0
-    for _, prev, cur, nxt in sliding_window(c, Stage.QUANTIZED, out="torch"):
+    for _, prev, cur, nxt in sliding_window(c, Stage.QUANTIZED, out="torch", from_host=from_host):
         rows = cur.shape[0]
         parts = [cur]
         top = 0
@@ -225,6 +231,9 @@ def streamed_derivative(c: CompressedStream, out: str = "numpy", out_dtype=None)
             r0 += p.shape[0]
         outs = devmod.stencil(_lib.OP_DERIV, [ext], [c.eps], False, dtype)
         for ax in range(len(dims)):
-            comps[ax][row:row + rows].copy_(outs[ax][top:top + rows])
+            if on_host:
+                comps[ax][row:row + rows] = outs[ax][top:top + rows].cpu().numpy()
+            else:
+                comps[ax][row:row + rows].copy_(outs[ax][top:top + rows])
         row += rows
-    return DerivedField("derivative", _host(comps, out), AXIS_NAMES[: len(dims)])
+    return DerivedField("derivative", tuple(comps) if on_host else _host(comps, out), AXIS_NAMES[: len(dims)])

@@ -155,10 +155,20 @@ def slab_bounds(c: CompressedStream) -> list:
     return [(s, min(s + extent, n1)) for s in range(0, n1, extent)]
 
 
+def _host_geom(c: CompressedStream):
+    """The stream's geometry struct without uploading it (the device mirror's when it exists)."""
+    if c._device is not None:
+        return c._device.geom
+    g = getattr(c, "_geom_cache", None)
+    if g is None:
+        g = _lib.make_geom(int(c.kind), c.shape.dims, c.block_dims, c.eps)
+        c._geom_cache = g
+    return g
+
+
 def _slab_chunk_range(c: CompressedStream, lo: int, hi: int) -> tuple:
     """First/last chunk of slab rows [lo, hi): closed form (chunks restart per segment)."""
-    d = c.device()
-    g = d.geom
+    g = _host_geom(c)
     if c.kind == CompressorKind.HSZP_ND:
         per = int(g.n_chunks) // c.shape.dims[0]       # every plane/row has the same chunk count
         return lo * per, hi * per
@@ -180,8 +190,21 @@ def _slab_chunk_range(c: CompressedStream, lo: int, hi: int) -> tuple:
     return first, last
 
 
+_ROWC_CACHE: dict = {}
+
+
 def _rowc(g, edge: int) -> int:
-    """Chunks in one block-row (all segments of one first-axis block index) of an HSZX_ND stream."""
+    """Chunks in one block-row (all segments of one first-axis block index) of an HSZX_ND stream
+    (memoised per geometry: slab iteration asks for it once per slab)."""
+    key = (int(g.ndims), tuple(int(g.dims[k]) for k in range(g.ndims)),
+           tuple(int(g.block_dims[k]) for k in range(g.ndims)), int(edge))
+    v = _ROWC_CACHE.get(key)
+    if v is None:
+        v = _ROWC_CACHE[key] = _rowc_compute(g, edge)
+    return v
+
+
+def _rowc_compute(g, edge: int) -> int:
     nd = g.ndims
     dims = [g.dims[k] for k in range(nd)]
     bds = [g.block_dims[k] for k in range(nd)]
@@ -196,45 +219,74 @@ def _rowc(g, edge: int) -> int:
     return total
 
 
-def _slab_view(c: CompressedStream, lo: int, hi: int):
-    """(DeviceStream over the slab's chunks, chunk count, payload bytes): same payload pointer,
-    sliced chunk index and metadata, payload length cut at the slab's last byte."""
-    d = c.device().validate()
+def _slab_layout(c: CompressedStream, lo: int, hi: int) -> tuple:
+    """(first chunk, last chunk, metadata [lo, hi), dims, block dims) of slab rows [lo, hi)."""
     first, last = _slab_chunk_range(c, lo, hi)
-    offs = d.offsets[first:last]
-    end = int(d.offsets[last].item()) if last < d.n_chunks else d.payload_len
     if c.kind.is_nd:
         dims = (hi - lo,) + tuple(c.shape.dims[1:])
         bd = tuple(min(b, n) for b, n in zip(c.block_dims, dims))
     else:
         dims = (hi - lo,)
         bd = (min(c.block_dims[0], hi - lo),)
-    meta = None
+    mlo = mhi = 0
     if c.kind.is_block_mean:
         if c.kind == CompressorKind.HSZX_ND:
             per_row = int(np.prod([-(-n // b) for n, b in zip(c.shape.dims[1:], c.block_dims[1:])]))
             b0 = lo // c.block_dims[0]
-            meta = d.metadata[b0 * per_row:(b0 + 1) * per_row]
+            mlo, mhi = b0 * per_row, (b0 + 1) * per_row
         else:
             S = c.block_dims[0]
-            meta = d.metadata[lo // S:lo // S + 1]
+            mlo, mhi = lo // S, lo // S + 1
+    return first, last, mlo, mhi, dims, bd
+
+
+def _slab_view(c: CompressedStream, lo: int, hi: int):
+    """(DeviceStream over the slab's chunks, chunk count, payload bytes): same payload pointer,
+    sliced chunk index and metadata, payload length cut at the slab's last byte."""
+    d = c.device().validate()
+    first, last, mlo, mhi, dims, bd = _slab_layout(c, lo, hi)
+    offs = d.offsets[first:last]
+    host = c.chunk_offsets            # host copy of the index (downloaded once): no per-slab sync
+    end = int(host[last]) if last < d.n_chunks else d.payload_len
+    meta = d.metadata[mlo:mhi] if c.kind.is_block_mean else None
     sub = DeviceStream.__new__(DeviceStream)
     DeviceStream.__init__(sub, int(c.kind), dims, bd, c.eps, d.payload, end, offs, meta)
     sub.desc.canonical = d.desc.canonical
     sub.desc.max_bitwidth = d.desc.max_bitwidth
     sub.validated = True
-    return sub, last - first, end - (int(d.offsets[first].item()) if first < d.n_chunks else end)
+    return sub, last - first, end - (int(host[first]) if first < d.n_chunks else end)
 
 
-def slab_iter(c: CompressedStream, stage: Stage, out: str = "numpy"):
-    """Yield per-slab views in axis-0 order (stages.py:173-225); concatenation == whole stage."""
+def slab_iter(c: CompressedStream, stage: Stage, out: str = "numpy", from_host=None,
+              budget: int | None = None):
+    """Yield per-slab views in axis-0 order (stages.py:173-225); concatenation == whole stage.
+
+    ``from_host=True`` streams the container from (pinned) host memory unit by unit instead of
+    uploading it whole (streaming.HostSlabSource); ``None`` decides by size
+    (streaming.should_stream).  Results are identical either way.
+    """
+    from . import streaming
+
     stage = Stage(stage)
     if stage not in supported_stages(c.kind) or stage == Stage.META:
         raise UnsupportedStageError(f"stage {stage.cli_name} is not slab-iterable for {c.kind.cli_name}")
     t = _lib.torch()
     carry = None
-    for lo, hi in slab_bounds(c):
-        sub, nch, nbytes = _slab_view(c, lo, hi)
+    bounds = slab_bounds(c)
+    src = None
+    if streaming.should_stream(c, from_host):
+        src = streaming.HostSlabSource(c, bounds, lambda lo, hi: _slab_layout(c, lo, hi),
+                                       budget or streaming.DEFAULT_BUDGET)
+    cur_unit = -1
+    for k, (lo, hi) in enumerate(bounds):
+        if src is None:
+            sub, nch, nbytes = _slab_view(c, lo, hi)
+        else:
+            u = int(src.unit_of[k])
+            if u != cur_unit and cur_unit >= 0:
+                src.release(cur_unit)          # its slabs' kernels are queued: the slot may refill
+            cur_unit = u
+            sub, nch, nbytes, _ = src.slab(k)
         decode_counters.chunks_decoded += nch
         decode_counters.bytes_read += nbytes
         if stage == Stage.DECORRELATED:
@@ -268,9 +320,9 @@ def slab_iter(c: CompressedStream, stage: Stage, out: str = "numpy"):
             yield f.cpu().numpy() if out == "numpy" else f
 
 
-def sliding_window(c: CompressedStream, stage: Stage, out: str = "numpy"):
+def sliding_window(c: CompressedStream, stage: Stage, out: str = "numpy", from_host=None):
     """Yield (index, prev, cur, nxt) slab triples holding at most 3 slabs (stages.py:228-258)."""
-    it = slab_iter(c, stage, out)
+    it = slab_iter(c, stage, out, from_host=from_host)
     window: list = []
     try:
         window.append(next(it))

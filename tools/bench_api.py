@@ -124,6 +124,23 @@ def main():
             if cfg == 3 and kind in (K.HSZP_ND, K.HSZX_ND):
                 t = timed(lambda: fields.divergence(cs, S.QUANTIZED, out="torch", out_dtype=np.float32))
                 record(cfg, kind, "A16 divergence (3 comps)", 3 * n, t, (3 * (P + I + Mb) + 4) / 3)
+            if cfg == 4 and kind in (K.HSZP_ND, K.HSZX_ND):
+                # A7 slab iteration (reference slab semantics: one plane / one block row per slab), the
+                # container device-resident vs streamed from pinned host memory
+                from paper_2603_25206_b200 import io as hio
+
+                hc = hio.stream_from_bytes(hio.stream_to_bytes(c))
+
+                def drain(src, **kw):
+                    for _ in h.slab_iter(src, S.QUANTIZED, out="torch", **kw):
+                        pass
+
+                t = timed(lambda: drain(c), reps=3)
+                record(cfg, kind, "A7 slab_iter stage 3 (resident)", n, t, P + I + Mb + 4)
+                t = timed(lambda: drain(hc, from_host=True), reps=3)
+                record(cfg, kind, "A7 slab_iter stage 3 (from host)", n, t, P + I + Mb + 4,
+                       note="container streamed H2D in 256 MB units; includes the pinned staging copy")
+                del hc
             if cfg in (2, 4) and kind in (K.HSZP_ND, K.HSZX_ND):
                 R = 16 if cfg == 2 else 8
                 t = timed(lambda: regions.region_stats(c, R))
