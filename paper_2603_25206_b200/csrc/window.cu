@@ -299,13 +299,13 @@ constexpr int BS_MAXG = 4;   // int4 column groups per thread: n2 <= 4 * 4 * TIL
 constexpr int SE_W = 128;    // strip width of the strip-edge table (the one-pass HSZP_ND kernel's x tile)
 
 
-template <bool Edges, bool L16>
+template <bool Edges, bool L16, bool Full>
 __global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __restrict__ payload, uint64_t len,
                                                           const uint64_t* __restrict__ offsets, int64_t n_chunks,
                                                           int n1, int n2, int BR, void* __restrict__ L,
                                                           int32_t* __restrict__ A, int32_t* __restrict__ EF,
                                                           int32_t* __restrict__ l_ovf, uint32_t sbytes) {
-    int32_t lo16 = 0, hi16 = 0;              // range of the values stored as int16
+    uint32_t rng16 = 0;                      // OR of (value + 2^15) over the values stored as int16
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint32_t s_off[TILE_CHUNKS];
     __shared__ uint32_t s_wt[TILE_CHUNKS / 32];
@@ -319,6 +319,7 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __rest
     const int y1 = min(y0 + BR, n1);
     const int ntiles = (y1 - y0 + rpt - 1) / rpt;
     const int ng = n2 >> 2;
+    const int kmax = (ng + TILE_CHUNKS - 1) / TILE_CHUNKS;   // column groups per thread (uniform)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int32_t* tile = reinterpret_cast<int32_t*>(smem);
     uint8_t* SB = smem + kFastTileBytes;     // two staging buffers of sbytes: tile t in buffer t & 1
@@ -400,27 +401,30 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __rest
         }
         __syncthreads();
         const int nstrips = (n2 + SE_W - 1) / SE_W;
-        for (int rr = 0; rr < nr; rr++) {
+        // rows of the tile: incremental row offsets, uniform k bound (no divergent skips when every
+        // thread owns kmax column groups: Full), int16 range by OR of v + 2^15 (bits >= 16 flag it)
+        int64_t rowoff = (z * n1 + r0) * (int64_t)n2;
+        for (int rr = 0; rr < nr; rr++, rowoff += n2) {
             const int y = r0 + rr;
-            int32_t* orow = (L && !L16) ? static_cast<int32_t*>(L) + (z * n1 + y) * (int64_t)n2 : nullptr;
-            int16_t* orow16 = (L && L16) ? static_cast<int16_t*>(L) + (z * n1 + y) * (int64_t)n2 : nullptr;
+            const int chrow = rr * cpr;
 #pragma unroll
             for (int k = 0; k < BS_MAXG; k++) {
+                if (k >= kmax) break;
                 const int gi = threadIdx.x + k * TILE_CHUNKS;
-                if (gi < ng) {
-                    const int ch = rr * cpr + (gi >> 3);
+                if (Full || gi < ng) {
+                    const int ch = chrow + (gi >> 3);
                     const int4 v = *reinterpret_cast<const int4*>(tile + ch * kChunkStride + ((gi & 7) << 2));
                     const int4 rv = add4u(v, s_off[ch]);          // row prefix R at x = 4gi .. 4gi+3
                     ysum[k] = add4(ysum[k], rv);
-                    if (orow) *reinterpret_cast<int4*>(orow + 4 * gi) = ysum[k];
-                    if (orow16) {
+                    if (L && !L16) *reinterpret_cast<int4*>(static_cast<int32_t*>(L) + rowoff + 4 * gi) = ysum[k];
+                    if (L && L16) {
                         const int4 v4 = ysum[k];
-                        lo16 = min(lo16, min(min(v4.x, v4.y), min(v4.z, v4.w)));   // range, checked once
-                        hi16 = max(hi16, max(max(v4.x, v4.y), max(v4.z, v4.w)));
+                        rng16 |= ((uint32_t)v4.x + 0x8000u) | ((uint32_t)v4.y + 0x8000u) | ((uint32_t)v4.z + 0x8000u) |
+                                 ((uint32_t)v4.w + 0x8000u);
                         uint2 pk;                                                  // low halves, 2 PRMTs
                         pk.x = __byte_perm((uint32_t)v4.x, (uint32_t)v4.y, 0x5410);
                         pk.y = __byte_perm((uint32_t)v4.z, (uint32_t)v4.w, 0x5410);
-                        *reinterpret_cast<uint2*>(orow16 + 4 * gi) = pk;
+                        *reinterpret_cast<uint2*>(static_cast<int16_t*>(L) + rowoff + 4 * gi) = pk;
                     }
                     if (Edges) {                                  // strip edges: E[s] = R(128s-1), F[s] = R(128s+128)
                         const int xg = 4 * gi;
@@ -448,7 +452,7 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __rest
         const int gi = threadIdx.x + k * TILE_CHUNKS;
         if (gi < ng) *reinterpret_cast<int4*>(arow + 4 * gi) = ysum[k];
     }
-    const bool ovf = lo16 < INT16_MIN || hi16 > INT16_MAX;   // an int16 L value did not fit
+    const bool ovf = (rng16 & 0xffff0000u) != 0;            // an int16 L value did not fit
     if (L16 && __any_sync(0xffffffffu, ovf) && (threadIdx.x & 31) == 0) atomicOr(l_ovf, 1);
 }
 
@@ -567,22 +571,27 @@ extern "C" int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t ba
     const size_t smem = kFastTileBytes + 2 * (size_t)sbytes + 16;
     const dim3 grid((unsigned)nb, (unsigned)np);
     cudaStream_t st = as_stream(stream);
+    const bool full = (n2 / 4) % TILE_CHUNKS == 0;
+#define HSZG_BS(E, LS, F)                                                                                    \
+    do {                                                                                                     \
+        allow_smem(k_band_scan<E, LS, F>, smem);                                                             \
+        k_band_scan<E, LS, F><<<grid, TILE_CHUNKS, smem, st>>>(s->payload, s->payload_len, s->offsets,        \
+                                                              g->n_chunks, (int)n1, (int)n2, (int)band_rows, \
+                                                              L_, A, E ? strip_edges : nullptr,              \
+                                                              l_overflow, sbytes);                           \
+    } while (0)
+    void* L_ = L;
     if (strip_edges) {
-        allow_smem(k_band_scan<true, false>, smem);
-        k_band_scan<true, false><<<grid, TILE_CHUNKS, smem, st>>>(s->payload, s->payload_len, s->offsets,
-                                                                  g->n_chunks, (int)n1, (int)n2, (int)band_rows, L,
-                                                                  A, strip_edges, nullptr, sbytes);
+        if (full) HSZG_BS(true, false, true);
+        else HSZG_BS(true, false, false);
     } else if (l_int16) {
-        allow_smem(k_band_scan<false, true>, smem);
-        k_band_scan<false, true><<<grid, TILE_CHUNKS, smem, st>>>(s->payload, s->payload_len, s->offsets,
-                                                                  g->n_chunks, (int)n1, (int)n2, (int)band_rows, L,
-                                                                  A, nullptr, l_overflow, sbytes);
+        if (full) HSZG_BS(false, true, true);
+        else HSZG_BS(false, true, false);
     } else {
-        allow_smem(k_band_scan<false, false>, smem);
-        k_band_scan<false, false><<<grid, TILE_CHUNKS, smem, st>>>(s->payload, s->payload_len, s->offsets,
-                                                                   g->n_chunks, (int)n1, (int)n2, (int)band_rows, L,
-                                                                   A, nullptr, nullptr, sbytes);
+        if (full) HSZG_BS(false, false, true);
+        else HSZG_BS(false, false, false);
     }
+#undef HSZG_BS
     const int64_t threads = np * (n2 / 4);
     k_band_prefix<<<(unsigned)((threads + 255) / 256), 256, 0, as_stream(stream)>>>(A, (int)nb, n2, np);
     { const cudaError_t e_ = cudaGetLastError(); if (e_ != cudaSuccess) return hszg_set_cuda_error(err, e_, "band_scan"); }
