@@ -400,6 +400,8 @@ using namespace hszg;
 
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+int hszg_decode_full(const HszgGeom* g, const HszgStream* s, int32_t* out, cudaStream_t st);
+
 int hszg_set_cuda_error(HszgErr* err, cudaError_t e, const char* where) {
     if (err) {
         err->status = HSZG_CUDA;
@@ -483,6 +485,9 @@ int hszg_launch_decode(const HszgGeom* g, const HszgStream* s, int32_t* out, cud
     const SegGeo sg = make_seggeo(*g);
     if (g->n_chunks == 0) return HSZG_OK;
     if (s->canonical) {
+        const int rf = hszg_decode_full(g, s, out, st);      // register-resident full-chunk path
+        if (rf == 0) return HSZG_OK;
+        if (rf < 0) HSZG_CHECK_LAUNCH("decode");
         const int64_t tiles = (g->n_chunks + TILE_CHUNKS - 1) / TILE_CHUNKS;
         const size_t smem = tile_smem_bytes(s->max_bitwidth);
         allow_smem(k_decode_tiles, smem);
