@@ -318,6 +318,7 @@ class CompressedStream:
     def payload(self, value):
         self._payload = value
         self._device = None
+        self._pinned_payload = None
 
     @property
     def chunk_offsets(self) -> np.ndarray:
@@ -351,12 +352,20 @@ class CompressedStream:
             return self._device.n_chunks
         return len(self._chunk_offsets)
 
+    def pinned_payload(self):
+        """The pinned torch buffer the payload views (streams from io.read_compressed), else None."""
+        pin = getattr(self, "_pinned_payload", None)
+        if pin is None or not isinstance(self._payload, memoryview) or pin.numel() != len(self._payload):
+            return None
+        return pin
+
     # -- device mirror -------------------------------------------------------------
     def device(self) -> DeviceStream:
         """The HBM-resident mirror (uploaded once, validated on first use)."""
         if self._device is None:
             self._device = DeviceStream.from_host(int(self.kind), self.shape.dims, self.block_dims, self.eps,
-                                                  self._payload, self._chunk_offsets, self._metadata)
+                                                  self._payload, self._chunk_offsets, self._metadata,
+                                                  pinned_payload=self.pinned_payload())
         return self._device
 
     # -- geometry --------------------------------------------------------------------

@@ -56,14 +56,17 @@ class DeviceStream:
     # ---- construction -----------------------------------------------------------
 
     @classmethod
-    def from_host(cls, kind, dims, block_dims, eps, payload: bytes, offsets, metadata=None):
+    def from_host(cls, kind, dims, block_dims, eps, payload: bytes, offsets, metadata=None, pinned_payload=None):
         t = _t()
         dev = _lib.device()
         n = len(payload)
         buf = t.zeros(n + _lib.PAYLOAD_PAD, dtype=t.uint8, device=dev)
         if n:
-            host = t.frombuffer(bytearray(payload), dtype=t.uint8)
-            buf[:n].copy_(host)
+            if pinned_payload is not None:                   # in-place DMA from the pinned file buffer
+                buf[:n].copy_(pinned_payload[:n], non_blocking=True)
+            else:
+                host = t.frombuffer(bytearray(payload), dtype=t.uint8)
+                buf[:n].copy_(host)
         offs = np.ascontiguousarray(np.asarray(offsets, dtype=np.uint64)).view(np.int64)
         offs_dev = t.from_numpy(offs.copy()).to(dev)
         meta_dev = None

@@ -42,9 +42,11 @@ class HostSlabSource:
         key = (id(payload), id(c._chunk_offsets), id(c._metadata))
         pin = getattr(c, "_pinned", None)
         if pin is None or pin[0] != key:
-            h_payload = t.empty(max(self.plen, 1), dtype=t.uint8, pin_memory=True)
-            if self.plen:
-                h_payload[: self.plen].copy_(t.frombuffer(bytearray(payload), dtype=t.uint8))
+            h_payload = c.pinned_payload()                    # read_compressed: the file buffer itself
+            if h_payload is None:
+                h_payload = t.empty(max(self.plen, 1), dtype=t.uint8, pin_memory=True)
+                if self.plen:
+                    h_payload[: self.plen].copy_(t.frombuffer(bytearray(payload), dtype=t.uint8))
             offs = np.ascontiguousarray(np.asarray(c.chunk_offsets, dtype=np.uint64)).view(np.int64).copy()
             meta = c.metadata
             h_meta = None if meta is None else t.from_numpy(np.ascontiguousarray(meta, dtype=np.int32)).pin_memory()

@@ -75,7 +75,7 @@ def _grf(rng, dims, amp_exponent):
     f *= k2 ** (amp_exponent / 2.0)
     f.flat[0] = 0.0
     del k2
-    g = np.fft.irfftn(f, s=dims)
+    g = np.fft.irfftn(f, s=dims, axes=tuple(range(len(dims))))
     g -= g.mean()
     g /= g.std()
     return g

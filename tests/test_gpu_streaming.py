@@ -80,3 +80,33 @@ def test_streamed_corruption_is_detected_in_its_unit():
         for _ in it:
             seen += 1
     assert seen >= 1                                   # earlier units decoded before the bad one
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2, 3])
+def test_pinned_file_io_roundtrip(tmp_path, kind):
+    """read_compressed reads into pinned memory and keeps the payload a view of it; the device
+    upload, the streamed slabs and write_compressed (from a device-resident stream) all agree
+    byte for byte with the bytes path."""
+    import paper_2603_25206_b200 as h
+    from paper_2603_25206_b200 import io
+
+    rng = np.random.default_rng(kind)
+    dims = (12, 16, 64) if kind in (1, 3) else (6000,)
+    f = O.random_field(rng, dims, "smooth")
+    c = h.compress(f, h.CompressorKind(kind), h.ErrorBound("rel", 1e-3))
+    path = tmp_path / "c.hsz"
+    io.write_compressed(c, path)                       # device-resident payload -> pinned -> file
+    raw = path.read_bytes()
+    assert raw == io.stream_to_bytes(c)
+    pc = io.read_compressed(path)
+    assert pc.pinned_payload() is not None and isinstance(pc.payload, memoryview)
+    assert io.stream_to_bytes(pc) == raw
+    q = h.partial_decompress(pc, h.Stage.QUANTIZED).values
+    assert np.array_equal(q, h.partial_decompress(c, h.Stage.QUANTIZED).values)
+    pc2 = io.read_compressed(path)
+    for a, b in zip(h.slab_iter(pc2, h.Stage.QUANTIZED, from_host=True, budget=4096),
+                    h.slab_iter(c, h.Stage.QUANTIZED)):
+        assert np.array_equal(a, b)
+    assert pc2._device is None
+    bc = io.read_compressed(path, pinned=False)
+    assert isinstance(bc.payload, bytes) and bc.pinned_payload() is None
