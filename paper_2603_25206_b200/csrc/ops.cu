@@ -846,6 +846,7 @@ __global__ void __launch_bounds__(GL_THREADS) k_grad_lap_f32(const int32_t* __re
 // Same per-point arithmetic as deriv / laplacian_at / k_stencil (so bit-identical results), but
 // 16-B neighbour-row loads (x+-1 by shuffle), no per-point index math and 16/32-B streaming stores.
 constexpr int SV_THREADS = 128;
+constexpr int SV_ZC = 8;          // planes per CTA of the 3-D z-sliding stencil
 
 struct Nb4 {            // one component around four x-points: centre, z+-1, y+-1 rows and the x edges
     int4 c, zm, zp, ym, yp;
@@ -936,29 +937,63 @@ __device__ __forceinline__ void st4(double* o, int64_t i, const double* v) {
 }
 
 template <int OP, int ND, typename OutT>
-__global__ void __launch_bounds__(SV_THREADS) k_stencil_v4(StencilArgs A) {
+__global__ void __launch_bounds__(SV_THREADS) k_stencil_v4(StencilArgs A, int zc, int64_t zend) {
     const int lane = threadIdx.x & 31;
     const int64_t xi0 = ((int64_t)blockIdx.x * SV_THREADS + threadIdx.x) * 4;
     const bool active = xi0 < A.n[2];
     const int64_t xi = active ? xi0 : 0;
     const int64_t y = blockIdx.y;
-    const int64_t z = A.zlo + blockIdx.z;
-    const int64_t n1 = A.n[1], n2 = A.n[2], plane = n1 * n2;
+    const int64_t n1 = A.n[1], n2 = A.n[2], plane = n1 * n2, nbox = A.n[0];
+    const int64_t zs = A.zlo + (int64_t)blockIdx.z * zc;
+    const int64_t ze = zs + zc < zend ? zs + zc : zend;
     Pt4 p;
-    p.zin = ND == 3 && A.gz0 + z > 0 && A.gz0 + z < A.gN0 - 1;
     p.yin = y > 0 && y < n1 - 1;
     p.x0 = xi == 0;
     p.xl = xi + 3 >= n2 - 1;
-    const int64_t off = z * plane + y * n2 + xi;
-    const int64_t oi = (z - A.zlo) * plane + y * n2 + xi;
     const bool fd = A.float_domain == 1;
     constexpr int a0 = 3 - ND;                        // box axis of original axis 0
     constexpr int NC = (OP == HSZG_OP_DIVERGENCE || OP == HSZG_OP_CURL) ? ND : 1;
-    Nb4 b[NC];
+    const int4 z4 = make_int4(0, 0, 0, 0);
+    // the thread slides along z through zc planes: rows z-1, z, z+1 stay in registers; the loads of
+    // the next plane (its y+-1 rows and x edges, and row z+2) are issued before plane z is computed
+    int4 cm[NC], cc[NC], cp[NC], ymn[NC], ypn[NC];
+    int eln[NC], ern[NC];
+    auto load_nb = [&](int c, int64_t zz, int4& ym, int4& yp, int& el, int& er) {
+        const int32_t* row = reinterpret_cast<const int32_t*>(A.q[c]) + zz * plane + y * n2 + xi;
+        ym = active && p.yin ? __ldg(reinterpret_cast<const int4*>(row - n2)) : z4;
+        yp = active && p.yin ? __ldg(reinterpret_cast<const int4*>(row + n2)) : z4;
+        el = lane == 0 && active && xi > 0 ? __ldg(row - 1) : 0;
+        er = lane == 31 && active && xi + 4 < n2 ? __ldg(row + 4) : 0;
+    };
 #pragma unroll
-    for (int c = 0; c < NC; c++)
-        b[c] = nb4_load(reinterpret_cast<const int32_t*>(A.q[c]), plane, n2, off, active, p.zin, p.yin, lane, xi);
-    if (!active) return;
+    for (int c = 0; c < NC; c++) {
+        const int32_t* col = reinterpret_cast<const int32_t*>(A.q[c]) + y * n2 + xi;
+        cc[c] = active ? __ldg(reinterpret_cast<const int4*>(col + zs * plane)) : z4;
+        cm[c] = active && zs > 0 ? __ldg(reinterpret_cast<const int4*>(col + (zs - 1) * plane)) : z4;
+        cp[c] = active && zs + 1 < nbox ? __ldg(reinterpret_cast<const int4*>(col + (zs + 1) * plane)) : z4;
+        load_nb(c, zs, ymn[c], ypn[c], eln[c], ern[c]);
+    }
+    for (int64_t z = zs; z < ze; z++) {
+    p.zin = ND == 3 && A.gz0 + z > 0 && A.gz0 + z < A.gN0 - 1;
+    Nb4 b[NC];
+    int4 nx[NC];
+#pragma unroll
+    for (int c = 0; c < NC; c++) {
+        b[c].c = cc[c];
+        b[c].zm = cm[c];
+        b[c].zp = cp[c];
+        b[c].ym = ymn[c];
+        b[c].yp = ypn[c];
+        b[c].l = __shfl_up_sync(0xffffffffu, cc[c].w, 1);
+        b[c].r = __shfl_down_sync(0xffffffffu, cc[c].x, 1);
+        if (lane == 0) b[c].l = eln[c];
+        if (lane == 31) b[c].r = ern[c];
+        const int32_t* row = reinterpret_cast<const int32_t*>(A.q[c]) + z * plane + y * n2 + xi;
+        nx[c] = active && z + 1 < ze && z + 2 < nbox ? __ldg(reinterpret_cast<const int4*>(row + 2 * plane)) : z4;
+        if (z + 1 < ze) load_nb(c, z + 1, ymn[c], ypn[c], eln[c], ern[c]);
+    }
+    const int64_t oi = (z - A.zlo) * plane + y * n2 + xi;
+    if (active) {
     double v[4];
     auto D = [&](int c, int k, int j) { return dv4(b[c], p, a0 + k, j, A.eps[c], A.two_eps[c], fd); };
     OutT* const* out = reinterpret_cast<OutT* const*>(A.out);
@@ -1030,17 +1065,31 @@ __global__ void __launch_bounds__(SV_THREADS) k_stencil_v4(StencilArgs A) {
             st4(out[2], oi, v);
         }
     }
+    }   // active
+#pragma unroll
+    for (int c = 0; c < NC; c++) {
+        cm[c] = cc[c];
+        cc[c] = cp[c];
+        cp[c] = nx[c];
+    }
+    }   // z
 }
 
 template <int ND, typename OutT>
-static void launch_sv4(const StencilArgs& A, dim3 grid, cudaStream_t st) {
+static void launch_sv4(const StencilArgs& A, dim3 grid, int zc, int64_t zend, cudaStream_t st) {
     switch (A.op) {
-        case HSZG_OP_DERIV: k_stencil_v4<HSZG_OP_DERIV, ND, OutT><<<grid, SV_THREADS, 0, st>>>(A); break;
-        case HSZG_OP_LAPLACIAN: k_stencil_v4<HSZG_OP_LAPLACIAN, ND, OutT><<<grid, SV_THREADS, 0, st>>>(A); break;
-        case HSZG_OP_GRAD_LAP: k_stencil_v4<HSZG_OP_GRAD_LAP, ND, OutT><<<grid, SV_THREADS, 0, st>>>(A); break;
-        case HSZG_OP_GRADMAG: k_stencil_v4<HSZG_OP_GRADMAG, ND, OutT><<<grid, SV_THREADS, 0, st>>>(A); break;
-        case HSZG_OP_DIVERGENCE: k_stencil_v4<HSZG_OP_DIVERGENCE, ND, OutT><<<grid, SV_THREADS, 0, st>>>(A); break;
-        case HSZG_OP_CURL: k_stencil_v4<HSZG_OP_CURL, ND, OutT><<<grid, SV_THREADS, 0, st>>>(A); break;
+        case HSZG_OP_DERIV: k_stencil_v4<HSZG_OP_DERIV, ND, OutT><<<grid, SV_THREADS, 0, st>>>(A, zc, zend); break;
+        case HSZG_OP_LAPLACIAN:
+            k_stencil_v4<HSZG_OP_LAPLACIAN, ND, OutT><<<grid, SV_THREADS, 0, st>>>(A, zc, zend);
+            break;
+        case HSZG_OP_GRAD_LAP:
+            k_stencil_v4<HSZG_OP_GRAD_LAP, ND, OutT><<<grid, SV_THREADS, 0, st>>>(A, zc, zend);
+            break;
+        case HSZG_OP_GRADMAG: k_stencil_v4<HSZG_OP_GRADMAG, ND, OutT><<<grid, SV_THREADS, 0, st>>>(A, zc, zend); break;
+        case HSZG_OP_DIVERGENCE:
+            k_stencil_v4<HSZG_OP_DIVERGENCE, ND, OutT><<<grid, SV_THREADS, 0, st>>>(A, zc, zend);
+            break;
+        case HSZG_OP_CURL: k_stencil_v4<HSZG_OP_CURL, ND, OutT><<<grid, SV_THREADS, 0, st>>>(A, zc, zend); break;
         default: break;
     }
 }
@@ -1094,13 +1143,15 @@ static int stencil_impl(int op, int32_t ndims, const int64_t* dims, int32_t ncom
     for (int k = 0; k < nout; k++) vec = vec && aligned16(out[k]);
     static const char* sv = getenv("HSZG_STENCIL");          // 's': scalar k_stencil only (A/B runs)
     if (vec && !(sv && sv[0] == 's')) {
-        const dim3 g4((unsigned)((A.n[2] / 4 + SV_THREADS - 1) / SV_THREADS), (unsigned)A.n[1], (unsigned)(zhi - zlo));
+        const int zc = ndims == 3 ? SV_ZC : 1;                 // planes per CTA (z sliding)
+        const dim3 g4((unsigned)((A.n[2] / 4 + SV_THREADS - 1) / SV_THREADS), (unsigned)A.n[1],
+                      (unsigned)((zhi - zlo + zc - 1) / zc));
         if (ndims == 3) {
-            if (out_type == HSZG_F32) launch_sv4<3, float>(A, g4, st);
-            else launch_sv4<3, double>(A, g4, st);
+            if (out_type == HSZG_F32) launch_sv4<3, float>(A, g4, zc, zhi, st);
+            else launch_sv4<3, double>(A, g4, zc, zhi, st);
         } else {
-            if (out_type == HSZG_F32) launch_sv4<2, float>(A, g4, st);
-            else launch_sv4<2, double>(A, g4, st);
+            if (out_type == HSZG_F32) launch_sv4<2, float>(A, g4, zc, zhi, st);
+            else launch_sv4<2, double>(A, g4, zc, zhi, st);
         }
         return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
     }
