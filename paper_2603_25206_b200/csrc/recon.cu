@@ -349,26 +349,22 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_tile_scan_fast(const uint8_t* _
 // the byte range of 256 chunks (16-B loads, ~15 KB of shared memory, so many CTAs per SM overlap their
 // phases), each thread decodes its chunk with decode32s and stores it straight from registers
 // (8 x 16-B stores per thread; every 128-B line is completed by one thread, merged in L2).
-//   Mode 0: p (stage 2)   Mode 1: p + M_b (HSZX stage 3/4)   Mode 2: flat prefix (HSZP), look-back
+//   Mode 0: p (stage 2)   Mode 1: p + M_b (HSZX stage 3/4)
+//   Mode 2: p + M_b scattered from block-contiguous to row-major (HSZX_ND stage 3/4; rows of B2 | 32
+//           values, so a chunk is whole block rows and every 16-B store completes its sectors)
+// (A register variant of the HSZP look-back scan measured slower than k_tile_scan_fast: 0.41 vs
+// 0.34 ms at 512^3 — the look-back chain wants short-lived CTAs.)
 constexpr int SF_THREADS = TILE_CHUNKS;
 
 template <int Mode, typename OutT>
 __global__ void __launch_bounds__(SF_THREADS) k_stream_full(const uint8_t* __restrict__ payload, uint64_t len,
                                                            const uint64_t* __restrict__ offsets, int64_t n_chunks,
-                                                           const int32_t* __restrict__ meta, int64_t cps, LBState lb,
-                                                           double two_eps, OutT* __restrict__ out) {
+                                                           const int32_t* __restrict__ meta, int64_t cps,
+                                                           double two_eps, OutT* __restrict__ out, SegGeo sg) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint64_t s_lo, s_hi;
-    __shared__ unsigned int s_tile;
-    __shared__ unsigned long long s_prefix;
     uint4* sb = reinterpret_cast<uint4*>(smem);
-    int64_t t = blockIdx.x;
-    if (Mode == 2) {
-        if (threadIdx.x == 0) s_tile = atomicAdd(lb.ticket, 1u);
-        __syncthreads();
-        t = s_tile;
-    }
-    const int64_t c0 = t * SF_THREADS;
+    const int64_t c0 = (int64_t)blockIdx.x * SF_THREADS;
     const int nch = (int)(n_chunks - c0 < SF_THREADS ? n_chunks - c0 : SF_THREADS);
     const bool mine = (int)threadIdx.x < nch;
     const int64_t c = c0 + threadIdx.x;
@@ -378,34 +374,30 @@ __global__ void __launch_bounds__(SF_THREADS) k_stream_full(const uint8_t* __res
         off = __ldg(offsets + c);
         if (threadIdx.x == 0) s_lo = off;
         if ((int)threadIdx.x == nch - 1) s_hi = c + 1 < n_chunks ? __ldg(offsets + c + 1) : payload_end(offsets, n_chunks, len);
-        if (Mode == 1) m = __ldg(meta + c / cps);
+        if (Mode != 0) m = __ldg(meta + c / cps);
     }
     __syncthreads();
     const uint64_t base = stage_range(payload, s_lo, s_hi, sb);
     __syncthreads();
-    const uint32_t* words = reinterpret_cast<const uint32_t*>(sb);
-    OutT* o = out + c * kChunkCap;
+    if (!mine) return;
     if (Mode != 2) {
-        if (mine)
-            decode32s<false>(words, (uint32_t)(off - base), m, [&](int q, int4 v) { store4<OutT>(o + 4 * q, v, two_eps); });
+        OutT* o = out + c * kChunkCap;
+        decode32s<false>(reinterpret_cast<const uint32_t*>(sb), (uint32_t)(off - base), m,
+                         [&](int q, int4 v) { store4<OutT>(o + 4 * q, v, two_eps); });
         return;
     }
-    int4 v[8];
-    uint32_t run = 0;
-    if (mine) run = decode32s<true>(words, (uint32_t)(off - base), 0, [&](int q, int4 x) { v[q] = x; });
-    unsigned long long tot;
-    const unsigned long long excl = block_exclusive_u64((unsigned long long)run, &tot);
-    if (threadIdx.x < 32) {
-        const uint32_t e = lookback_exclusive_warp32(lb, t, (uint32_t)tot);
-        if (threadIdx.x == 0) s_prefix = e;
-    }
-    __syncthreads();
-    if (!mine) return;
-    const uint32_t add = (uint32_t)(s_prefix + excl);
-#pragma unroll
-    for (int q = 0; q < 8; q++)
-        store4<OutT>(o + 4 * q, make_int4((int)((uint32_t)v[q].x + add), (int)((uint32_t)v[q].y + add),
-                                          (int)((uint32_t)v[q].z + add), (int)((uint32_t)v[q].w + add)), two_eps);
+    // chunk j of block b: block-row-major values 32j .. 32j+31
+    const uint32_t b = (uint32_t)(c / cps), j = (uint32_t)(c - (int64_t)b * cps);
+    const uint32_t G1 = (uint32_t)sg.G[1], G2 = (uint32_t)sg.G[2], B1 = (uint32_t)sg.B[1], B2 = (uint32_t)sg.B[2];
+    const uint32_t r = b / G2, b2 = b - r * G2, b0 = r / G1, b1 = r - b0 * G1;
+    const int64_t n1 = sg.n[1], n2 = sg.n[2];
+    OutT* ob = out + ((int64_t)b0 * sg.B[0] * n1 + (int64_t)b1 * B1) * n2 + (int64_t)b2 * B2;
+    decode32s<false>(reinterpret_cast<const uint32_t*>(sb), (uint32_t)(off - base), m, [&](int q, int4 v) {
+        const uint32_t l = 32 * j + 4 * q;
+        const uint32_t row = l / B2, xl = l - row * B2;
+        const uint32_t zl = row / B1, yl = row - zl * B1;
+        store4<OutT>(ob + ((int64_t)zl * n1 + yl) * n2 + xl, v, two_eps);
+    });
 }
 
 // full chunks and full-size segments (chunk c of segment c / cps)
@@ -417,14 +409,13 @@ static bool stream_full_ok(const HszgGeom* g, const SegGeo& sg, const void* out)
 }
 
 template <int Mode, typename OutT>
-static void launch_stream_full(const HszgGeom* g, const HszgStream* s, const SegGeo& sg, LBState lb, OutT* out,
-                               cudaStream_t st) {
+static void launch_stream_full(const HszgGeom* g, const HszgStream* s, const SegGeo& sg, OutT* out, cudaStream_t st) {
     const size_t smem = stage_bytes(s->max_bitwidth);
     allow_smem(k_stream_full<Mode, OutT>, smem);
     const int64_t tiles = (g->n_chunks + SF_THREADS - 1) / SF_THREADS;
     k_stream_full<Mode, OutT><<<(unsigned)tiles, SF_THREADS, smem, st>>>(
         s->payload, s->payload_len, s->offsets, g->n_chunks, s->metadata, (sg.B[0] * sg.B[1] * sg.B[2]) / kChunkCap,
-        lb, 2.0 * g->eps, out);
+        2.0 * g->eps, out, sg);
 }
 
 // ---- HSZP_ND: row scans along the last axis, then column scans -----------------------
@@ -691,7 +682,7 @@ static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, 
     switch (g->kind) {
         case HSZG_HSZX:
             if (fast && stream_full_ok(g, sg, out) && !sf_off()) {
-                launch_stream_full<1, OutT>(g, s, sg, LBState{}, out, st);
+                launch_stream_full<1, OutT>(g, s, sg, out, st);
                 HSZG_CHECK_LAUNCH("reconstruct hszx");
                 return HSZG_OK;
             }
@@ -730,6 +721,11 @@ static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, 
             }
             break;
         case HSZG_HSZX_ND:
+            if (fast && stream_full_ok(g, sg, out) && sg.B[2] % 4 == 0 && 32 % sg.B[2] == 0 && !sf_off()) {
+                launch_stream_full<2, OutT>(g, s, sg, out, st);
+                HSZG_CHECK_LAUNCH("reconstruct hszx-nd");
+                return HSZG_OK;
+            }
             if (fast && blocks_fast_ok(sg)) {
                 BlockTiles bt;
                 bt.k = TILE_ELEMS / (sg.B[0] * sg.B[1] * sg.B[2]);
@@ -760,8 +756,6 @@ static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, 
                 if (ws_bytes < lookback_ws_bytes(g->n_chunks)) break;
                 LBState lb = lookback_carve(ws, tiles);
                 cudaMemsetAsync(ws, 0, lookback_clear_bytes(tiles), st);
-                // (k_stream_full<2> — registers instead of the shared tile — measured slower here:
-                // 0.41 vs 0.34 ms at 512^3; the look-back chain wants short-lived CTAs)
                 if (g->n_chunks * kChunkCap == g->n && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
                     const size_t fsmem = kFastTileBytes + stage_bytes(s->max_bitwidth);
                     allow_smem(k_tile_scan_fast<OutT>, fsmem);
@@ -942,6 +936,6 @@ int hszg_decode_full(const HszgGeom* g, const HszgStream* s, int32_t* out, cudaS
     const SegGeo sg = make_seggeo(*g);
     if (!s->canonical || g->n_chunks * kChunkCap != g->n || (reinterpret_cast<uintptr_t>(out) & 15) || sf_off())
         return 1;
-    launch_stream_full<0, int32_t>(g, s, sg, LBState{}, out, st);
+    launch_stream_full<0, int32_t>(g, s, sg, out, st);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
