@@ -422,6 +422,42 @@ static void launch_stream_full(const HszgGeom* g, const HszgStream* s, const Seg
 
 constexpr int ROW_THREADS = 256, ROW_ITEMS = 8;
 
+// short rows (L <= 32 * 4 * RW_VEC, 16-B aligned, L % 4 == 0): one warp per row, each lane a contiguous
+// run of int4 groups (local prefix), a warp scan of the lane totals, then the offsets added
+constexpr int RW_VEC = 8;     // int4 groups per lane: rows up to 1024 values
+__global__ void __launch_bounds__(256) k_row_scan_warp(int32_t* buf, int64_t rows, int64_t L) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (row >= rows) return;
+    int4* r = reinterpret_cast<int4*>(buf + row * L);
+    const int ng = (int)(L >> 2);
+    const int per = (ng + 31) / 32;                 // groups per lane
+    const int g0 = lane * per;
+    int4 v[RW_VEC];
+    uint32_t run = 0;
+#pragma unroll
+    for (int k = 0; k < RW_VEC; k++) {
+        if (k < per && g0 + k < ng) {
+            v[k] = r[g0 + k];
+            v[k].x = (int)(run += (uint32_t)v[k].x);
+            v[k].y = (int)(run += (uint32_t)v[k].y);
+            v[k].z = (int)(run += (uint32_t)v[k].z);
+            v[k].w = (int)(run += (uint32_t)v[k].w);
+        }
+    }
+    uint32_t inc = run;
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += o;
+    }
+    const uint32_t add = inc - run;
+#pragma unroll
+    for (int k = 0; k < RW_VEC; k++)
+        if (k < per && g0 + k < ng)
+            r[g0 + k] = make_int4((int)((uint32_t)v[k].x + add), (int)((uint32_t)v[k].y + add),
+                                  (int)((uint32_t)v[k].z + add), (int)((uint32_t)v[k].w + add));
+}
+
 __global__ void __launch_bounds__(ROW_THREADS) k_row_scan(int32_t* buf, int64_t L) {
     const int64_t row = blockIdx.x;
     int32_t* r = buf + row * L;
@@ -490,9 +526,59 @@ __global__ void k_col_scan_bands(const int32_t* src, const int32_t* __restrict__
     }
 }
 
+// Few, long columns (e.g. the y pass of a 2-D field: 3600 columns of 1800): S threads per column
+// scan S segments — sums, an exclusive prefix across the segments in shared memory, then the
+// segment rescans (re-read from L2) — so the launch has ~150k threads instead of one per column.
+// src may be dst: every element is read in the first pass before any thread writes.
+template <typename OutT>
+__global__ void k_col_scan_seg(const int32_t* src, int64_t M, int64_t Lc, double two_eps, OutT* dst) {
+    __shared__ uint32_t part[32][33];
+    const int tx = threadIdx.x, sy = threadIdx.y, S = blockDim.y;
+    const int64_t l = blockIdx.x * 32 + tx;
+    const int64_t a = blockIdx.y;
+    const bool act = l < Lc;
+    const int64_t seg = (M + S - 1) / S;
+    const int64_t m0 = sy * seg, m1 = m0 + seg < M ? m0 + seg : M;
+    const int32_t* s = src + a * M * Lc + l;
+    OutT* d = dst + a * M * Lc + l;
+    uint32_t sum = 0;
+    if (act) {
+        int64_t m = m0;
+        for (; m + 4 <= m1; m += 4)
+            sum += (uint32_t)s[m * Lc] + (uint32_t)s[(m + 1) * Lc] + (uint32_t)s[(m + 2) * Lc] + (uint32_t)s[(m + 3) * Lc];
+        for (; m < m1; m++) sum += (uint32_t)s[m * Lc];
+    }
+    part[sy][tx] = sum;
+    __syncthreads();
+    uint32_t acc = 0;
+    for (int k = 0; k < sy; k++) acc += part[k][tx];
+    if (!act) return;
+    int64_t m = m0;
+    for (; m + 4 <= m1; m += 4) {             // four loads in flight before the dependent stores
+        const uint32_t v0 = (uint32_t)s[m * Lc], v1 = (uint32_t)s[(m + 1) * Lc];
+        const uint32_t v2 = (uint32_t)s[(m + 2) * Lc], v3 = (uint32_t)s[(m + 3) * Lc];
+        acc += v0; d[m * Lc] = Conv<OutT>::go((int32_t)acc, two_eps);
+        acc += v1; d[(m + 1) * Lc] = Conv<OutT>::go((int32_t)acc, two_eps);
+        acc += v2; d[(m + 2) * Lc] = Conv<OutT>::go((int32_t)acc, two_eps);
+        acc += v3; d[(m + 3) * Lc] = Conv<OutT>::go((int32_t)acc, two_eps);
+    }
+    for (; m < m1; m++) {
+        acc += (uint32_t)s[m * Lc];
+        d[m * Lc] = Conv<OutT>::go((int32_t)acc, two_eps);
+    }
+}
+
 template <typename OutT>
 static void launch_col_scan(const int32_t* src, int64_t A, int64_t M, int64_t Lc, double two_eps, OutT* dst,
                             cudaStream_t st) {
+    const int64_t cols = A * Lc;
+    if (M >= 64 && cols < 148 * 1024 && A <= 65535) {
+        int S = 1;
+        while (S < 32 && cols * S < 148 * 2048 && S * 16 < M) S <<= 1;
+        k_col_scan_seg<OutT><<<dim3((unsigned)((Lc + 31) / 32), (unsigned)A), dim3(32, S), 0, st>>>(src, M, Lc, two_eps,
+                                                                                                   dst);
+        return;
+    }
     // grid.y is limited to 65535: fold A into chunks
     const int64_t ymax = 65535;
     for (int64_t a0 = 0; a0 < A; a0 += ymax) {
@@ -619,7 +705,10 @@ static int transform_decoded(const HszgGeom* g, const SegGeo& sg, const int32_t*
     const size_t need = (size_t)g->n * 4;
     if (g->kind == HSZG_HSZP_ND) {
         const int64_t N0 = sg.n[0], N1 = sg.n[1], N2 = sg.n[2];
-        k_row_scan<<<(unsigned)(N0 * N1), ROW_THREADS, 0, st>>>(buf, N2);
+        if (N2 % 4 == 0 && N2 <= 32 * 4 * RW_VEC && (reinterpret_cast<uintptr_t>(buf) & 15) == 0)
+            k_row_scan_warp<<<(unsigned)((N0 * N1 + 7) / 8), 256, 0, st>>>(buf, N0 * N1, N2);
+        else
+            k_row_scan<<<(unsigned)(N0 * N1), ROW_THREADS, 0, st>>>(buf, N2);
         HSZG_CHECK_LAUNCH("row scan");
         const bool zpass = N0 > 1;
         if (N1 > 1) {

@@ -5,7 +5,9 @@ has it; scalar results are host values, so their D2H is inside the timing), warm
 REPS CUDA-event timings.  Throughput is GB/s of original fp32 (4 N / t); the roofline fraction
 uses SURVEY §8(d)'s algorithmic bytes per value with this stream's measured P (payload), I (index)
 and Mb (block means) against MEASURED_PEAKS hbm_gbs.  Synthetic inputs follow §8(d)'s generators
-(`paper_2603_25206_b200.synthetic`), seeded.
+(`paper_2603_25206_b200.synthetic`), seeded.  On configs 1-2 (``--cpu-configs``) every row is also timed
+once on the CPU oracle (the reference algorithm restated, oracle/, single thread) on the same
+container: ``cpu_oracle_ms`` and ``speedup_vs_cpu`` (the CPU path timed beside it).
 
     python tools/bench_api.py [--configs 1 2 3 4] [--out profiles/r01_api_bench.json]
 """
@@ -19,7 +21,7 @@ import time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-REPS = 7
+REPS = 21
 
 
 def timed(fn, reps=REPS):
@@ -43,6 +45,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", type=int, nargs="*", default=[1, 2, 3, 4])
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_api_bench.json"))
+    ap.add_argument("--cpu-configs", type=int, nargs="*", default=[1, 2],
+                    help="also time the CPU oracle (reference algorithm restated, 1 thread) on these configs")
     args = ap.parse_args()
 
     import numpy as np
@@ -59,14 +63,28 @@ def main():
     S = h.Stage
     rows = []
 
-    def record(cfg, kind, row, n, t, algo_per_value, note=""):
+    from oracle import hsz_oracle as O
+
+    O.set_threads(1)
+    cpu_on = {"cfg": None}
+
+    def record(cfg, kind, row, n, t, algo_per_value, note="", cpu=None):
         gbs = 4.0 * n / t / 1e9
         ach = algo_per_value * n / t / 1e9
-        rows.append({"config": cfg, "kind": kind.name, "row": row, "ms": round(t * 1e3, 3),
-                     "gbs_fp32": round(gbs, 1), "algo_B_per_value": round(algo_per_value, 3),
-                     "achieved_gbs": round(ach, 1), "frac": round(ach / peak, 3), "note": note})
+        r = {"config": cfg, "kind": kind.name, "row": row, "ms": round(t * 1e3, 3),
+             "gbs_fp32": round(gbs, 1), "algo_B_per_value": round(algo_per_value, 3),
+             "achieved_gbs": round(ach, 1), "frac": round(ach / peak, 3), "note": note}
+        extra = ""
+        if cpu is not None and cfg in args.cpu_configs:
+            t0 = time.perf_counter()
+            cpu()
+            tc = time.perf_counter() - t0
+            r["cpu_oracle_ms"] = round(tc * 1e3, 2)
+            r["speedup_vs_cpu"] = round(tc / t, 1)
+            extra = f"  cpu {tc * 1e3:9.1f} ms (x{tc / t:.0f})"
+        rows.append(r)
         print(f"cfg{cfg} {kind.name:8s} {row:28s} {t * 1e3:9.3f} ms  {gbs:8.1f} GB/s-fp32  "
-              f"{ach:8.1f} GB/s algo ({ach / peak:5.3f})", flush=True)
+              f"{ach:8.1f} GB/s algo ({ach / peak:5.3f}){extra}", flush=True)
 
     gens = {
         1: (lambda: [synthetic.config1_field()], ("abs", 1e-4), [K.HSZP, K.HSZP_ND, K.HSZX, K.HSZX_ND]),
@@ -90,6 +108,15 @@ def main():
                 cs.append(h.compress(f, kind, bnd))
             c = cs[0]
             n = c.shape.total
+            from paper_2603_25206_b200 import io as hio
+
+            oc = O.stream_from_bytes(hio.stream_to_bytes(c)) if cfg in args.cpu_configs else None
+            q3 = {}
+
+            def oq():
+                if "q" not in q3:
+                    q3["q"] = O.stage3(oc)
+                return q3["q"]
             d = c.device()
             P = d.payload_len / n
             I = 8.0 * d.n_chunks / n
@@ -98,29 +125,34 @@ def main():
             fd = torch.from_numpy(fields_np[0]).cuda()
             # E1-E5: compress from a device field (quantize + decorrelate + encode)
             t = timed(lambda: compress_device(fd, kind, c.eps, c.block_dims))
-            record(cfg, kind, "E compress (device field)", n, t, 4 + P + I + Mb)
+            record(cfg, kind, "E compress (device field)", n, t, 4 + P + I + Mb,
+                   cpu=lambda: O.compress(fields_np[0], int(kind), "abs", c.eps,
+                                          c.block_dims if kind.is_nd else c.block_dims[0]))
             # A1 / A3-A5: stages 2, 3, 4
             t = timed(lambda: h.partial_decompress(c, S.DECORRELATED, out="torch"))
-            record(cfg, kind, "A1 stage 2 (p)", n, t, P + I + 4)
+            record(cfg, kind, "A1 stage 2 (p)", n, t, P + I + 4, cpu=lambda: O.stage2(oc))
             t = timed(lambda: h.partial_decompress(c, S.QUANTIZED, out="torch"))
-            record(cfg, kind, "A3 stage 3 (q)", n, t, P + I + Mb + 4)
+            record(cfg, kind, "A3 stage 3 (q)", n, t, P + I + Mb + 4, cpu=lambda: O.stage3(oc))
             t = timed(lambda: h.partial_decompress(c, S.FULL, out="torch", dtype=torch.float32))
-            record(cfg, kind, "A5 stage 4 (fp32)", n, t, P + I + Mb + 4)
+            record(cfg, kind, "A5 stage 4 (fp32)", n, t, P + I + Mb + 4, cpu=lambda: O.stage4(oc))
             # A8-A12, N1: statistics from the bytes
             if kind.is_block_mean:
                 t = timed(lambda: stats.compute_stat(c, "mean", S.META))
-                record(cfg, kind, "A8 mean at stage 1", n, t, Mb)
+                record(cfg, kind, "A8 mean at stage 1", n, t, Mb, cpu=lambda: O.compute_stat(oc, "mean", 1))
             for st, name in ((S.DECORRELATED, "stage 2"), (S.QUANTIZED, "stage 3")):
                 t = timed(lambda: stats.compute_stat(c, "var", st))
-                record(cfg, kind, f"N1 variance at {name}", n, t, P + I + Mb)
+                record(cfg, kind, f"N1 variance at {name}", n, t, P + I + Mb,
+                       cpu=lambda: O.compute_stat(oc, "var", int(st)))
             # A13/A14 (+A15 at stage 2 for nd kinds)
             if kind in (K.HSZP_ND, K.HSZX_ND):
                 t = timed(lambda: fields.compute_field_op(c, "derivative", S.QUANTIZED, out="torch",
                                                           out_dtype=np.float32))
-                record(cfg, kind, "A13 gradient at stage 3", n, t, P + I + Mb + 4 * nd)
+                record(cfg, kind, "A13 gradient at stage 3", n, t, P + I + Mb + 4 * nd,
+                       cpu=lambda: O.field_op(oc, "derivative", 3))
                 t = timed(lambda: fields.compute_field_op(c, "laplacian", S.QUANTIZED, out="torch",
                                                           out_dtype=np.float32))
-                record(cfg, kind, "A14 Laplacian at stage 3", n, t, P + I + Mb + 4)
+                record(cfg, kind, "A14 Laplacian at stage 3", n, t, P + I + Mb + 4,
+                       cpu=lambda: O.field_op(oc, "laplacian", 3))
             if cfg == 3 and kind in (K.HSZP_ND, K.HSZX_ND):
                 t = timed(lambda: fields.divergence(cs, S.QUANTIZED, out="torch", out_dtype=np.float32))
                 record(cfg, kind, "A16 divergence (3 comps)", 3 * n, t, (3 * (P + I + Mb) + 4) / 3)
@@ -144,13 +176,15 @@ def main():
             if cfg in (2, 4) and kind in (K.HSZP_ND, K.HSZX_ND):
                 R = 16 if cfg == 2 else 8
                 t = timed(lambda: regions.region_stats(c, R))
-                record(cfg, kind, f"N2/N3 region stats R={R}", n, t, P + I + Mb)
+                record(cfg, kind, f"N2/N3 region stats R={R}", n, t, P + I + Mb,
+                       cpu=lambda: (O.region_stats(oq(), c.eps, R), O.region_minmax(oq(), c.eps, R)))
                 if cfg == 4:
                     t = timed(lambda: regions.threshold_count(c, 8, 1.0))
                     record(cfg, kind, "N4 threshold count", n, t, P + I + Mb)
                 if cfg == 2:
                     t = timed(lambda: regions.gradient_magnitude(c, S.QUANTIZED, out="torch", out_dtype=np.float32))
-                    record(cfg, kind, "N5 gradient magnitude", n, t, P + I + Mb + 4)
+                    record(cfg, kind, "N5 gradient magnitude", n, t, P + I + Mb + 4,
+                           cpu=lambda: O.gradient_magnitude(oq(), c.eps))
             del fd
             torch.cuda.empty_cache()
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
