@@ -266,11 +266,12 @@ int hszg_zgrad_lap(const int32_t* q, int64_t n1, int64_t n2, int64_t zlo, int64_
  * neighbour's q plane, emit gradient + Laplacian of nout planes, accumulate stats and write
  * q[a+nout-1] to carry_out — q itself is never stored.  With band_off (hszg_band_scan output) P2 is
  * band-local: row y of plane z adds band_off[z][y / band_rows][:] (look_band_off: the lookahead's);
- * p2_int16: P2 / lookahead hold those band-local prefixes as int16 (hszg_band_scan l_int16). */
+ * p2_mode: width codes of those band-local prefixes (hszg_band_scan l_mode) — bits 0-3 for P2, bits 4-7
+ * for the lookahead plane: 0 int32, 1 int16, 2 int8; pairs equal, or int16 P2 with an int8 lookahead. */
 int hszg_zsweep_grad_lap(const int32_t* P2, int64_t n1, int64_t n2, int64_t nout, const int32_t* lookahead,
                          const int32_t* carry, const int32_t* q_upper, int32_t* carry_out, int64_t gz0, int64_t gN0,
                          double eps, float* const* out, HszgAcc* acc, const int32_t* band_off,
-                         const int32_t* look_band_off, int64_t band_rows, int p2_int16, int exact, void* stream);
+                         const int32_t* look_band_off, int64_t band_rows, int p2_mode, int exact, void* stream);
 /* HSZX_ND one-pass decode + gradient + Laplacian + stats (8x8x8 blocks dividing the 3-D box, canonical,
  * max bit width <= 16): q never reaches memory.  The stream is a z-slab of a gN0-plane field whose
  * first plane is global plane gz0; halo_lo / halo_hi (optional, n1*n2 int32) are q of the planes just
@@ -288,16 +289,16 @@ int hszg_lorenzo_onepass(const HszgGeom* g, const HszgStream* s, const int32_t* 
                          const int32_t* strip_edges, const int32_t* carry, const int32_t* q_upper, int64_t gz0,
                          int64_t gN0, float* const* out, HszgAcc* acc, int exact, void* stream, HszgErr* err);
 /* HSZP_ND decode + row prefix + in-band column prefix in one pass (3-D, canonical, n2 % 32 == 0,
- * n2 <= 4096, 256 % (n2/32) == 0).  L[z][y][x] (optional) = 2-D prefix of plane z restricted to the
+ * n2 <= 4096).  L[z][y][x] (optional) = 2-D prefix of plane z restricted to the
  * rows of y's band (bands of band_rows rows); band_off[z][b][x] = sum of the rows of bands < b, i.e.
  * P2 = L + band_off[z][y / band_rows].  strip_edges (optional): for 128-wide x strips s,
  * [z][s][y][0] = row prefix at x = 128s - 1 (0 for s = 0), [z][s][y][1] = at x = 128s + 128 (0 past
  * the row).  L: dims[0]*dims[1]*dims[2] int32; band_off: dims[0]*ceil(dims[1]/band_rows)*dims[2];
  * strip_edges: dims[0]*ceil(dims[2]/128)*E*2 int32 with E = dims[1] rounded up to even (+ 64 spare).
- * l_int16: write L as int16 (n2 % 8 == 0); any value that does not fit sets *l_overflow = 1 (the
- * caller then redoes the window with int32 L). */
+ * l_mode: 0 writes L as int32; 1 as int16 (n2 % 8 == 0), any value that does not fit setting bit 2
+ * of *l_overflow; 2 as int8 (n2 % 16 == 0), setting bit 1 (the caller then redoes the pass wider). */
 int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t band_rows, void* L, int32_t* band_off,
-                   int32_t* strip_edges, int l_int16, int32_t* l_overflow, void* stream, HszgErr* err);
+                   int32_t* strip_edges, int l_mode, int32_t* l_overflow, void* stream, HszgErr* err);
 /* HSZP_ND decode fused with the in-row prefix (rows of whole chunks, 256 % (n2/32) == 0). */
 int hszg_decode_rowscan(const HszgGeom* g, const HszgStream* s, int32_t* out, void* stream, HszgErr* err);
 /* In-place inclusive scan along the middle axis of an int32 [A][M][L] view. */

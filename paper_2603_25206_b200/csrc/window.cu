@@ -299,13 +299,13 @@ constexpr int BS_MAXG = 4;   // int4 column groups per thread: n2 <= 4 * 4 * TIL
 constexpr int SE_W = 128;    // strip width of the strip-edge table (the one-pass HSZP_ND kernel's x tile)
 
 
-template <bool Edges, bool L16, bool Full>
+template <bool Edges, int LW, bool Full>
 __global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __restrict__ payload, uint64_t len,
                                                           const uint64_t* __restrict__ offsets, int64_t n_chunks,
                                                           int n1, int n2, int BR, void* __restrict__ L,
                                                           int32_t* __restrict__ A, int32_t* __restrict__ EF,
                                                           int32_t* __restrict__ l_ovf, uint32_t sbytes) {
-    uint32_t rng16 = 0;                      // OR of (value + 2^15) over the values stored as int16
+    uint32_t rng16 = 0;                      // OR of (value + 2^15 / 2^7) over the values stored narrow
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint32_t s_off[TILE_CHUNKS];
     __shared__ uint32_t s_wt[TILE_CHUNKS / 32];
@@ -416,8 +416,8 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __rest
                     const int4 v = *reinterpret_cast<const int4*>(tile + ch * kChunkStride + ((gi & 7) << 2));
                     const int4 rv = add4u(v, s_off[ch]);          // row prefix R at x = 4gi .. 4gi+3
                     ysum[k] = add4(ysum[k], rv);
-                    if (L && !L16) *reinterpret_cast<int4*>(static_cast<int32_t*>(L) + rowoff + 4 * gi) = ysum[k];
-                    if (L && L16) {
+                    if (L && LW == 4) *reinterpret_cast<int4*>(static_cast<int32_t*>(L) + rowoff + 4 * gi) = ysum[k];
+                    if (L && LW == 2) {
                         const int4 v4 = ysum[k];
                         rng16 |= ((uint32_t)v4.x + 0x8000u) | ((uint32_t)v4.y + 0x8000u) | ((uint32_t)v4.z + 0x8000u) |
                                  ((uint32_t)v4.w + 0x8000u);
@@ -425,6 +425,14 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __rest
                         pk.x = __byte_perm((uint32_t)v4.x, (uint32_t)v4.y, 0x5410);
                         pk.y = __byte_perm((uint32_t)v4.z, (uint32_t)v4.w, 0x5410);
                         *reinterpret_cast<uint2*>(static_cast<int16_t*>(L) + rowoff + 4 * gi) = pk;
+                    }
+                    if (L && LW == 1) {
+                        const int4 v4 = ysum[k];
+                        rng16 |= ((uint32_t)v4.x + 0x80u) | ((uint32_t)v4.y + 0x80u) | ((uint32_t)v4.z + 0x80u) |
+                                 ((uint32_t)v4.w + 0x80u);
+                        const uint32_t lo = __byte_perm((uint32_t)v4.x, (uint32_t)v4.y, 0x0040);   // low bytes
+                        const uint32_t hi = __byte_perm((uint32_t)v4.z, (uint32_t)v4.w, 0x0040);
+                        *reinterpret_cast<uint32_t*>(static_cast<int8_t*>(L) + rowoff + 4 * gi) = __byte_perm(lo, hi, 0x5410);
                     }
                     if (Edges) {                                  // strip edges: E[s] = R(128s-1), F[s] = R(128s+128)
                         const int xg = 4 * gi;
@@ -452,8 +460,9 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __rest
         const int gi = threadIdx.x + k * TILE_CHUNKS;
         if (gi < ng) *reinterpret_cast<int4*>(arow + 4 * gi) = ysum[k];
     }
-    const bool ovf = (rng16 & 0xffff0000u) != 0;            // an int16 L value did not fit
-    if (L16 && __any_sync(0xffffffffu, ovf) && (threadIdx.x & 31) == 0) atomicOr(l_ovf, 1);
+    // a narrow L value did not fit: flag bit 1 (int8) or 2 (int16)
+    const bool ovf = (rng16 & (LW == 1 ? 0xffffff00u : 0xffff0000u)) != 0;
+    if (LW < 4 && __any_sync(0xffffffffu, ovf) && (threadIdx.x & 31) == 0) atomicOr(l_ovf, LW);
 }
 
 // A[z][b][:] band totals -> exclusive prefix over b (one thread per (plane, int4 column group));
@@ -520,14 +529,17 @@ namespace hszg {
 int launch_zsweep_ring(const int32_t* L, int64_t n1, int64_t n2, int64_t nout, const int32_t* lookahead,
                        const int32_t* carry, const int32_t* q_upper, int32_t* carry_out, int64_t gz0, int64_t gN0,
                        double eps, float* const* out, HszgAcc* acc, const int32_t* A, const int32_t* lookA,
-                       int64_t BR, int64_t nb, int l16, int exact, cudaStream_t st);
+                       int64_t BR, int64_t nb, int lmode, int lamode, int exact, cudaStream_t st);
 }
 
 extern "C" int hszg_zsweep_grad_lap(const int32_t* P2, int64_t n1, int64_t n2, int64_t nout, const int32_t* lookahead,
                                     const int32_t* carry, const int32_t* q_upper, int32_t* carry_out, int64_t gz0,
                                     int64_t gN0, double eps, float* const* out, HszgAcc* acc,
                                     const int32_t* band_off, const int32_t* look_band_off, int64_t band_rows,
-                                    int p2_int16, int exact, void* stream) {
+                                    int p2_mode, int exact, void* stream) {
+    // p2_mode: bits 0-3 the width code of P2 (0 int32, 1 int16, 2 int8), bits 4-7 that of the lookahead
+    const int lmode = p2_mode & 15, lamode = lookahead ? (p2_mode >> 4) & 15 : lmode;
+    const bool narrow = lmode != 0 || lamode != 0;
     if (n2 % 4 || !al16(P2) || !al16(out[0]) || !al16(out[1]) || !al16(out[2]) || !al16(out[3]) || n1 > 65535 ||
         (carry && !al16(carry)) || (q_upper && !al16(q_upper)) || (carry_out && !al16(carry_out)) ||
         (band_off && (band_rows < 1 || !al16(band_off) || (lookahead && (!look_band_off || !al16(look_band_off))))))
@@ -536,14 +548,17 @@ extern "C" int hszg_zsweep_grad_lap(const int32_t* P2, int64_t n1, int64_t n2, i
     if (nout <= 0) return HSZG_OK;
     dim3 grid((unsigned)((n2 / 4 + ZG_THREADS - 1) / ZG_THREADS), (unsigned)n1);
     static const char* zmode = getenv("HSZG_ZSWEEP");       // 'c': per-thread-column kernel (A/B runs)
+    const bool modes_ok = lmode <= 2 && lamode <= 2 && (lmode == lamode || (lmode == 1 && lamode == 2)) &&
+                          (!narrow || n2 % ((lmode == 2 || lamode == 2) ? 16 : 8) == 0);
+    if (!modes_ok) return HSZG_INVALID_ARG;
     if (band_off && band_rows % 16 == 0 && !(zmode && zmode[0] == 'c') && al16(lookahead) &&
-        al16(look_band_off) && (!p2_int16 || n2 % 8 == 0)) {
+        al16(look_band_off)) {
         return launch_zsweep_ring(P2, n1, n2, nout, lookahead, carry, q_upper, carry_out, gz0, gN0, eps, out, acc,
-                                  band_off, look_band_off, band_rows, nb, p2_int16, exact, as_stream(stream))
+                                  band_off, look_band_off, band_rows, nb, lmode, lamode, exact, as_stream(stream))
                    ? HSZG_CUDA
                    : HSZG_OK;
     }
-    if (p2_int16) return HSZG_INVALID_ARG;                   // int16 band-local prefixes: ring sweep only
+    if (narrow) return HSZG_INVALID_ARG;                     // narrow band-local prefixes: ring sweep only
     (exact ? k_zsweep<true> : k_zsweep<false>)<<<grid, ZG_THREADS, 0, as_stream(stream)>>>(P2, n1, n2, nout, lookahead, carry, q_upper, carry_out,
                                                          gz0, gN0, eps, 2.0 * eps, out[0], out[1], out[2], out[3],
                                                          acc, band_off, look_band_off, band_rows, nb);
@@ -551,14 +566,14 @@ extern "C" int hszg_zsweep_grad_lap(const int32_t* P2, int64_t n1, int64_t n2, i
 }
 
 extern "C" int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t band_rows, void* L, int32_t* A,
-                              int32_t* strip_edges, int l_int16, int32_t* l_overflow, void* stream, HszgErr* err) {
+                              int32_t* strip_edges, int l_mode, int32_t* l_overflow, void* stream, HszgErr* err) {
     err->status = HSZG_OK;
     const int64_t n1 = g->dims[1], n2 = g->dims[2], np = g->dims[0];
     const int64_t cpr = n2 / kChunkCap;
     if (g->kind != HSZG_HSZP_ND || g->ndims != 3 || !s->canonical || n2 % kChunkCap || cpr < 1 ||
         n2 > 4 * BS_MAXG * TILE_CHUNKS || band_rows < 1 || n1 > INT32_MAX || np > 65535 ||
         !al16(L) || !al16(A) || !al16(s->payload) || (!L && !strip_edges) ||
-        (l_int16 && (!l_overflow || strip_edges || n2 % 8))) {
+        l_mode < 0 || l_mode > 2 || (l_mode && (!l_overflow || strip_edges || n2 % (l_mode == 2 ? 16 : 8)))) {
         err->status = HSZG_INVALID_ARG;
         snprintf(err->message, sizeof(err->message),
                  "band_scan needs a canonical 3-D HSZP_ND stream with whole-chunk rows (n2 %% 32 == 0, "
@@ -582,14 +597,17 @@ extern "C" int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t ba
     } while (0)
     void* L_ = L;
     if (strip_edges) {
-        if (full) HSZG_BS(true, false, true);
-        else HSZG_BS(true, false, false);
-    } else if (l_int16) {
-        if (full) HSZG_BS(false, true, true);
-        else HSZG_BS(false, true, false);
+        if (full) HSZG_BS(true, 4, true);
+        else HSZG_BS(true, 4, false);
+    } else if (l_mode == 1) {
+        if (full) HSZG_BS(false, 2, true);
+        else HSZG_BS(false, 2, false);
+    } else if (l_mode == 2) {
+        if (full) HSZG_BS(false, 1, true);
+        else HSZG_BS(false, 1, false);
     } else {
-        if (full) HSZG_BS(false, false, true);
-        else HSZG_BS(false, false, false);
+        if (full) HSZG_BS(false, 4, true);
+        else HSZG_BS(false, 4, false);
     }
 #undef HSZG_BS
     const int64_t threads = np * (n2 / 4);

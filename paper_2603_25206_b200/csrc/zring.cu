@@ -10,6 +10,7 @@
 // mbarriers: s_full / s_empty hand the staging slots between loader and adders, q_full / q_empty
 // the q planes between adders and emitters.  q never goes to HBM (except the window carry).
 #include <cstdio>
+#include <type_traits>
 #include "tile.cuh"
 #include "stencil.cuh"
 #include "async.cuh"
@@ -29,14 +30,22 @@ constexpr int ZR_NPL = 4;                   // q planes in the ring
 constexpr int ZR_D = 4;                     // staged P2 planes in flight
 constexpr int ZR_SW = ZR_TX + 8;            // staged int32 row: x0-4 .. x0+132
 constexpr int ZR_SW16 = ZR_TX + 16;         // staged int16 row: x0-8 .. x0+136 (16-B aligned ends)
+constexpr int ZR_SW8 = ZR_TX + 32;          // staged int8 row: x0-16 .. x0+144 (16-B aligned ends)
 constexpr int ZR_SROWS = ZR_ROWS + 3;       // 18 L rows + band-offset rows (above, tile, below)
-// staging slot bytes: 18 L rows (int32 or int16) + 3 int32 band-offset rows
-__host__ __device__ constexpr int zr_lrow_bytes(bool l16) { return l16 ? ZR_SW16 * 2 : ZR_SW * 4; }
-__host__ __device__ constexpr int zr_slot_bytes(bool l16) { return ZR_ROWS * zr_lrow_bytes(l16) + 3 * ZR_SW * 4; }
-constexpr size_t zr_smem(bool l16) { return (size_t)ZR_NPL * ZR_PLANE * 4 + (size_t)ZR_D * zr_slot_bytes(l16); }
+// staged L row of width lw bytes per value: first column, value count, bytes
+__host__ __device__ constexpr int zr_lead(int lw) { return lw == 4 ? 4 : (lw == 2 ? 8 : 16); }
+__host__ __device__ constexpr int zr_row_vals(int lw) { return lw == 4 ? ZR_SW : (lw == 2 ? ZR_SW16 : ZR_SW8); }
+__host__ __device__ constexpr int zr_lrow_bytes(int lw) { return zr_row_vals(lw) * lw; }
+__host__ __device__ constexpr int zr_max(int a, int b) { return a > b ? a : b; }
+// staging slot: 18 L rows (row stride = the wider of the L and lookahead rows) + 3 int32 band-offset rows
+__host__ __device__ constexpr int zr_lb(int lw, int law) { return zr_max(zr_lrow_bytes(lw), zr_lrow_bytes(law)); }
+__host__ __device__ constexpr int zr_slot_bytes(int lw, int law) { return ZR_ROWS * zr_lb(lw, law) + 3 * ZR_SW * 4; }
+constexpr size_t zr_smem(int lw, int law) {
+    return (size_t)ZR_NPL * ZR_PLANE * 4 + (size_t)ZR_D * zr_slot_bytes(lw, law);
+}
 
 struct ZrArgs {
-    const void* L;                          // band-local 2-D prefixes, int32 or (L16) int16
+    const void* L;                          // band-local 2-D prefixes: int32, int16 or int8 (LW bytes)
     const void* lookahead;
     const int32_t* carry;
     const int32_t* q_upper;
@@ -52,12 +61,14 @@ struct ZrArgs {
     HszgAcc* acc;
 };
 
-template <bool Exact, bool L16>
+// LW: bytes per L value of the window's planes, LAW: of the lookahead plane (the next window's first,
+// which may be narrower: int16 window 0 + int8 rest)
+template <bool Exact, int LW, int LAW>
 __global__ void __launch_bounds__(ZR_T, 2) k_zsweep_ring(ZrArgs a) {
     extern __shared__ __align__(128) int32_t zsm[];
     int32_t* Q = zsm;                                     // [ZR_NPL][ZR_ROWS][ZR_RW]
     uint8_t* S = reinterpret_cast<uint8_t*>(zsm + ZR_NPL * ZR_PLANE);   // [ZR_D][slot]
-    constexpr int LB = zr_lrow_bytes(L16), SLOT = zr_slot_bytes(L16);
+    constexpr int LB = zr_lb(LW, LAW), SLOT = zr_slot_bytes(LW, LAW);
     __shared__ __align__(8) uint64_t s_full[ZR_D], s_empty[ZR_D], q_full[ZR_NPL], q_empty[ZR_NPL];
     const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
     const int64_t x0 = (int64_t)blockIdx.x * ZR_TX, y0 = (int64_t)blockIdx.y * ZR_TY;
@@ -71,7 +82,7 @@ __global__ void __launch_bounds__(ZR_T, 2) k_zsweep_ring(ZrArgs a) {
     const bool has_look = a.lookahead != nullptr && a.q_upper == nullptr;
     const int64_t nst = nout + (has_look ? 1 : 0);         // staged planes
 
-    for (int i = threadIdx.x; i < (int)(zr_smem(L16) / 16); i += ZR_T) reinterpret_cast<int4*>(zsm)[i] = make_int4(0, 0, 0, 0);
+    for (int i = threadIdx.x; i < (int)(zr_smem(LW, LAW) / 16); i += ZR_T) reinterpret_cast<int4*>(zsm)[i] = make_int4(0, 0, 0, 0);
     if (threadIdx.x == 0) {
         for (int i = 0; i < ZR_D; i++) {
             mbar_init(&s_full[i], 1);
@@ -88,49 +99,59 @@ __global__ void __launch_bounds__(ZR_T, 2) k_zsweep_ring(ZrArgs a) {
     if (wp == 0) {
         // ================================ loader ================================
         const uint32_t rbytes = (uint32_t)(xe - xs) * 4;
-        const int64_t xs16 = x0 >= 8 ? x0 - 8 : 0;
-        const int64_t xe16 = x0 + ZR_TX + 8 < n2 ? x0 + ZR_TX + 8 : n2;
         const int64_t y = y0 - 1 + lane;                  // lanes 0..17: L rows; 18..20: band rows
+        // one L row of width w bytes per value: source element offset, bytes, staging offset
+        struct Row {
+            int64_t off;
+            uint32_t bytes, dst;
+        };
+        auto lrow = [&](int w) {
+            const int lead = zr_lead(w);
+            const int64_t s0 = x0 >= lead ? x0 - lead : 0;
+            const int64_t s1 = x0 + ZR_TX + lead < n2 ? x0 + ZR_TX + lead : n2;
+            return Row{y * n2 + s0, (uint32_t)(s1 - s0) * w, (uint32_t)lane * LB + (uint32_t)(s0 - (x0 - lead)) * w};
+        };
         bool ok;
-        int64_t row_off;
-        uint32_t bytes, dst_off;
+        Row rw, ra;                                       // the window's planes / the lookahead plane
         if (lane < ZR_ROWS) {
             ok = y >= 0 && y < n1;
-            row_off = y * n2 + (L16 ? xs16 : xs);
-            bytes = L16 ? (uint32_t)(xe16 - xs16) * 2 : rbytes;
-            dst_off = lane * LB + (L16 ? (uint32_t)(xs16 - (x0 - 8)) * 2 : (uint32_t)scol * 4);
+            rw = lrow(LW);
+            ra = lrow(LAW);
         } else if (lane < ZR_SROWS) {
             ok = band[lane - ZR_ROWS] >= 0;
-            row_off = band[lane - ZR_ROWS] * n2 + xs;
-            bytes = rbytes;
-            dst_off = ZR_ROWS * LB + (lane - ZR_ROWS) * ZR_SW * 4 + (uint32_t)scol * 4;
+            rw.off = band[lane - ZR_ROWS] * n2 + xs;
+            rw.bytes = rbytes;
+            rw.dst = ZR_ROWS * LB + (lane - ZR_ROWS) * ZR_SW * 4 + (uint32_t)scol * 4;
+            ra = rw;
         } else {
             ok = false;
-            row_off = 0;
-            bytes = 0;
-            dst_off = 0;
+            rw = ra = Row{0, 0, 0};
         }
-        uint32_t tx = ok ? bytes : 0;
+        uint32_t txw = ok ? rw.bytes : 0, txa = ok ? ra.bytes : 0;
 #pragma unroll
-        for (int d = 16; d > 0; d >>= 1) tx += __shfl_xor_sync(0xffffffffu, tx, d);
+        for (int d = 16; d > 0; d >>= 1) {
+            txw += __shfl_xor_sync(0xffffffffu, txw, d);
+            txa += __shfl_xor_sync(0xffffffffu, txa, d);
+        }
         for (int64_t zz = 0; zz < nst; zz++) {
             const int slot = (int)(zz % ZR_D);
             const int64_t u = zz / ZR_D;
+            const bool look = zz >= nout;
             if (u > 0) mbar_wait(&s_empty[slot], (uint32_t)((u - 1) & 1));
             if (lane == 0) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_arrive_tx(&s_full[slot], tx);
+                mbar_arrive_tx(&s_full[slot], look ? txa : txw);
             }
             __syncwarp();
             if (ok) {
-                const void* src;
-                if (lane < ZR_ROWS) {
-                    if (L16) src = static_cast<const int16_t*>(zz < nout ? a.L : a.lookahead) + (zz < nout ? zz * plane : 0) + row_off;
-                    else src = static_cast<const int32_t*>(zz < nout ? a.L : a.lookahead) + (zz < nout ? zz * plane : 0) + row_off;
-                } else {
-                    src = (zz < nout ? a.A + zz * a.nb * n2 : a.lookA) + row_off;
-                }
-                tma_load_1d(S + (size_t)slot * SLOT + dst_off, src, bytes, &s_full[slot]);
+                const Row& r = look ? ra : rw;
+                const uint8_t* src;
+                if (lane < ZR_ROWS)
+                    src = static_cast<const uint8_t*>(look ? a.lookahead : a.L) +
+                          ((look ? 0 : zz * plane) + r.off) * (look ? LAW : LW);
+                else
+                    src = reinterpret_cast<const uint8_t*>((look ? a.lookA : a.A + zz * a.nb * n2) + r.off);
+                tma_load_1d(S + (size_t)slot * SLOT + r.dst, src, r.bytes, &s_full[slot]);
             }
         }
         return;
@@ -165,21 +186,30 @@ __global__ void __launch_bounds__(ZR_T, 2) k_zsweep_ring(ZrArgs a) {
                 const int32_t* Pprev = Q + (int)(zz % ZR_NPL) * ZR_PLANE;
                 const uint8_t* St = S + (size_t)slot * SLOT;
                 const int32_t* Sa = reinterpret_cast<const int32_t*>(St + ZR_ROWS * LB);
-                for (int i = at; i < ZR_ROWS * C4; i += ZR_AT) {
-                    const int r = i / C4, j = 4 * (i - r * C4);
-                    const int br = r == 0 ? 0 : (r == ZR_ROWS - 1 ? 2 : 1);
-                    int4 l;
-                    if (L16) {
-                        const short4 h = *reinterpret_cast<const short4*>(
-                            reinterpret_cast<const int16_t*>(St + r * LB) + j + 4);
-                        l = make_int4(h.x, h.y, h.z, h.w);
-                    } else {
-                        l = *reinterpret_cast<const int4*>(reinterpret_cast<const int32_t*>(St + r * LB) + j);
+                auto add_rows = [&](auto wtag) {
+                    constexpr int W = decltype(wtag)::value;
+                    for (int i = at; i < ZR_ROWS * C4; i += ZR_AT) {
+                        const int r = i / C4, j = 4 * (i - r * C4);
+                        const int br = r == 0 ? 0 : (r == ZR_ROWS - 1 ? 2 : 1);
+                        int4 l;
+                        if (W == 4) {
+                            l = *reinterpret_cast<const int4*>(reinterpret_cast<const int32_t*>(St + r * LB) + j);
+                        } else if (W == 2) {
+                            const short4 h = *reinterpret_cast<const short4*>(
+                                reinterpret_cast<const int16_t*>(St + r * LB) + j + 4);
+                            l = make_int4(h.x, h.y, h.z, h.w);
+                        } else {
+                            const char4 h = *reinterpret_cast<const char4*>(
+                                reinterpret_cast<const int8_t*>(St + r * LB) + j + 12);
+                            l = make_int4(h.x, h.y, h.z, h.w);
+                        }
+                        const int4 b = *reinterpret_cast<const int4*>(Sa + br * ZR_SW + j);
+                        const int4 q = *reinterpret_cast<const int4*>(Pprev + r * ZR_RW + ZR_X0 - 4 + j);
+                        *reinterpret_cast<int4*>(P + r * ZR_RW + ZR_X0 - 4 + j) = add4(q, add4(l, b));
                     }
-                    const int4 b = *reinterpret_cast<const int4*>(Sa + br * ZR_SW + j);
-                    const int4 q = *reinterpret_cast<const int4*>(Pprev + r * ZR_RW + ZR_X0 - 4 + j);
-                    *reinterpret_cast<int4*>(P + r * ZR_RW + ZR_X0 - 4 + j) = add4(q, add4(l, b));
-                }
+                };
+                if (LAW != LW && zz >= nout) add_rows(std::integral_constant<int, LAW>());
+                else add_rows(std::integral_constant<int, LW>());
                 mbar_arrive(&s_empty[slot]);
             } else {
                 copy_plane(nullptr, P);                     // q[a+nout] not needed (global last plane)
@@ -251,7 +281,7 @@ __global__ void __launch_bounds__(ZR_T, 2) k_zsweep_ring(ZrArgs a) {
 int launch_zsweep_ring(const int32_t* L, int64_t n1, int64_t n2, int64_t nout, const int32_t* lookahead,
                        const int32_t* carry, const int32_t* q_upper, int32_t* carry_out, int64_t gz0, int64_t gN0,
                        double eps, float* const* out, HszgAcc* acc, const int32_t* A, const int32_t* lookA,
-                       int64_t BR, int64_t nb, int l16, int exact, cudaStream_t st) {
+                       int64_t BR, int64_t nb, int lmode, int lamode, int exact, cudaStream_t st) {
     ZrArgs a;
     a.L = L;
     a.lookahead = lookahead;
@@ -274,17 +304,25 @@ int launch_zsweep_ring(const int32_t* L, int64_t n1, int64_t n2, int64_t nout, c
     a.o3 = out[3];
     a.acc = acc;
     dim3 grid((unsigned)((n2 + ZR_TX - 1) / ZR_TX), (unsigned)((n1 + ZR_TY - 1) / ZR_TY));
-#define ZR_LAUNCH(E, H)                                                   \
-    do {                                                                  \
-        allow_smem(k_zsweep_ring<E, H>, zr_smem(H));                      \
-        k_zsweep_ring<E, H><<<grid, ZR_T, zr_smem(H), st>>>(a);           \
+#define ZR_LAUNCH(E, W, WA)                                                           \
+    do {                                                                              \
+        allow_smem(k_zsweep_ring<E, W, WA>, zr_smem(W, WA));                          \
+        k_zsweep_ring<E, W, WA><<<grid, ZR_T, zr_smem(W, WA), st>>>(a);               \
     } while (0)
+    // width codes 0/1/2 = int32/int16/int8; supported pairs: equal, or int16 window + int8 lookahead
+    const int key = lmode * 3 + lamode;
     if (exact) {
-        if (l16) ZR_LAUNCH(true, true);
-        else ZR_LAUNCH(true, false);
+        if (key == 0) ZR_LAUNCH(true, 4, 4);
+        else if (key == 4) ZR_LAUNCH(true, 2, 2);
+        else if (key == 8) ZR_LAUNCH(true, 1, 1);
+        else if (key == 5) ZR_LAUNCH(true, 2, 1);
+        else return 1;
     } else {
-        if (l16) ZR_LAUNCH(false, true);
-        else ZR_LAUNCH(false, false);
+        if (key == 0) ZR_LAUNCH(false, 4, 4);
+        else if (key == 4) ZR_LAUNCH(false, 2, 2);
+        else if (key == 8) ZR_LAUNCH(false, 1, 1);
+        else if (key == 5) ZR_LAUNCH(false, 2, 1);
+        else return 1;
     }
 #undef ZR_LAUNCH
     return cudaGetLastError() == cudaSuccess ? 0 : 1;

@@ -401,13 +401,23 @@ class WindowPipeline:
             else:
                 self._fused_loop(outs)
             res = self._finish_stats(_prepared)
-            if self._l16_overflowed(_prepared):
-                # an int16 band-local prefix did not fit: this field needs int32 L (kept from now on)
-                self.l16 = False
+            ovf = self._l_overflow(_prepared)
+            if ovf:
+                # a narrow band-local prefix did not fit: widen (int8 -> int16, int16 -> int32; kept from
+                # now on) and redo the pass
+                if ovf & 2:
+                    self.l16 = False
+                self.l8 = False
                 self._pers_W = None
                 self._stage_boundary()
                 self._fused_loop(outs)
                 res = self._finish_stats(_prepared)
+                if self._l_overflow(_prepared):
+                    self.l16 = False
+                    self._pers_W = None
+                    self._stage_boundary()
+                    self._fused_loop(outs)
+                    res = self._finish_stats(_prepared)
             if not self.exact_fp32 and not self._fast_valid(res, _prepared):
                 # the fast emitter needs |q| < 2^27 (FAST_QLIM, stencil.cuh): every q is some point's
                 # centre, so the exact min / max decide it; redo the pass with the exact emitter
@@ -420,21 +430,35 @@ class WindowPipeline:
             return res if stats else None
         return self._run_generic(outs, stats, _prepared)
 
-    # HSZP_ND two-pass: band-local prefixes L stored as int16 (half the intermediate traffic); a
-    # device flag reports any value that did not fit and the pass is redone with int32 L
+    # HSZP_ND two-pass: band-local prefixes L stored narrow — int8 (a quarter of the int32 traffic)
+    # except in the window holding the field's first plane (there L is the y-difference of q itself,
+    # int16), or int16 everywhere; a device flag (bit 1: int8, bit 2: int16) reports any value that did
+    # not fit and the pass is redone one width up
     l16 = True
+    l8 = True
 
     def _l16_active(self) -> bool:
-        # int16 L feeds only the ring z-sweep (band rows a multiple of 16)
+        # narrow L feeds only the ring z-sweep (band rows a multiple of 16)
         return bool(self.band_rows) and self.band_rows % 16 == 0 and self.l16 and self.sf.global_dims[2] % 8 == 0
 
-    def _l16_overflowed(self, _prepared) -> bool:
+    def _l_mode(self, a: int) -> int:
+        """Width code of window [a, ...)'s L: 0 int32, 1 int16, 2 int8."""
+        if not self._l16_active():
+            return 0
+        if self.l8 and self.sf.global_dims[2] % 16 == 0 and self.sf.z0 + a > 0:
+            return 2
+        return 1
+
+    def _l_overflow(self, _prepared) -> int:
         if not getattr(self, "_l16_used", False):
-            return False
+            return 0
         flag = self.l16_ovf.clone()
         if not _prepared:
             self.comm.all_reduce(flag, "max")          # every rank redoes the pass together
-        return int(flag.item()) != 0
+        return int(flag.item())
+
+    def _l16_overflowed(self, _prepared) -> bool:
+        return self._l_overflow(_prepared) != 0
 
     def _fast_valid(self, res, _prepared) -> bool:
         lim = FAST_QLIM
@@ -647,8 +671,8 @@ class WindowPipeline:
         nw = len(wins)
         ns = len(ring)
         br = self.band_rows
-        l16 = bool(br) and ring[0].dtype == t.int16
-        lsz = 2 if l16 else 4                            # bytes per value of the L intermediate
+        l16 = bool(br) and ring[0].dtype == t.int16      # narrow L (int16 slots, int8 windows use half)
+        modes = [self._l_mode(a) if l16 else 0 for a, _ in wins]
         self._l16_used = l16
         if l16:
             self.l16_ovf.zero_()
@@ -665,14 +689,14 @@ class WindowPipeline:
             err = _lib.Err()
             if br:
                 _lib.call("hszg_band_scan", ctypes.byref(sub.geom), ctypes.byref(sub.desc), br,
-                          _lib.ptr(ring[k % ns]), _lib.ptr(self.bands[k % ns]), None, int(l16),
+                          _lib.ptr(ring[k % ns]), _lib.ptr(self.bands[k % ns]), None, modes[k],
                           _lib.ptr(self.l16_ovf) if l16 else None, _lib.stream_handle(), ctypes.byref(err), err=err)
             else:
                 _lib.call("hszg_decode_rowscan", ctypes.byref(sub.geom), ctypes.byref(sub.desc),
                           _lib.ptr(ring[k % ns]), _lib.stream_handle(), ctypes.byref(err), err=err)
                 _lib.call("hszg_col_scan", _lib.ptr(ring[k % ns]), b - a, n1, n2, _lib.stream_handle())
             if self.timer:
-                self.timer.end("reconstruct", self._range_bytes(a, b) + lsz * (b - a) * self.plane)
+                self.timer.end("reconstruct", self._range_bytes(a, b) + (4, 2, 1)[modes[k]] * (b - a) * self.plane)
 
         issued = 0
 
@@ -707,9 +731,10 @@ class WindowPipeline:
                       sf.global_dims[0], ctypes.c_double(sf.eps), self._outs_arr(outs, a, b), _lib.ptr(self.acc),
                       _lib.ptr(self.bands[k % ns]) if br else None,
                       _lib.ptr(self.bands[(k + 1) % ns]) if (br and look is not None) else None, br,
-                      int(l16), int(self.exact_fp32), _lib.stream_handle())
+                      modes[k] | ((modes[k + 1] if k + 1 < nw else modes[k]) << 4), int(self.exact_fp32),
+                      _lib.stream_handle())
             if self.timer:
-                self.timer.end("stencil", (lsz + 16) * (b - a) * self.plane)
+                self.timer.end("stencil", ((4, 2, 1)[modes[k]] + 16) * (b - a) * self.plane)
             sweep_done[k].record(main)
             carry = out_carry
         if side is not main:

@@ -236,3 +236,38 @@ def test_fast_mode_falls_back_on_large_q(kind):
     assert res["s1"] == s1 and res["s2"] == s2 and not pipe.exact_fp32
     if kind == 1:
         assert not pipe.l16            # the int16 band-local prefixes overflowed: redone with int32
+
+
+@pytest.mark.parametrize("case", ["smooth", "noise"])
+def test_narrow_band_prefix_widths(case):
+    """HSZP_ND two-pass with int8 band-local prefixes (int16 in the window holding the field's first
+    plane): a field whose z-differences are smooth keeps int8; white noise overflows int8 (flag bit 1),
+    the pass is redone with int16 everywhere — bit-exact against the oracle either way."""
+    import torch
+
+    from paper_2603_25206_b200 import pipeline
+
+    dims = (48, 32, 64)
+    z, y, x = np.meshgrid(*[np.arange(n, dtype=np.float64) for n in dims], indexing="ij")
+    if case == "smooth":
+        f = (np.sin(2 * np.pi * z / 48) + 0.5 * np.sin(2 * np.pi * x / 64) + 0.25 * np.cos(2 * np.pi * y / 32))
+    else:
+        f = np.random.default_rng(5).uniform(-1, 1, dims)
+    f = f.astype(np.float32)
+    eps = 1e-3 * float(f.max() - f.min())
+    fd = torch.from_numpy(f).cuda()
+    sf = pipeline.compress_shard(fd, 1, eps, (8, 8, 8), 0, dims[0], dims)
+    pipe = pipeline.WindowPipeline(sf, pipeline.Comm(), 16)
+    pipe.one_pass = pipe.lorenzo_one_pass = False
+    pipe.band_rows_req = 16
+    pipe.exact_fp32 = True
+    outs = [torch.empty(dims, dtype=torch.float32, device="cuda") for _ in range(4)]
+    res = pipe.run(outs)
+    want, s1, s2, mean, var = _oracle_outputs(f, 1, eps)
+    for k, (got, w) in enumerate(zip(outs, want)):
+        assert np.array_equal(got.cpu().numpy(), w), (case, k)
+    assert res["s1"] == s1 and res["s2"] == s2
+    assert pipe.l16
+    assert pipe.l8 == (case == "smooth")
+    res2 = pipe.run(outs)                              # the chosen width is kept for later passes
+    assert res2["s1"] == s1 and pipe.l8 == (case == "smooth")
