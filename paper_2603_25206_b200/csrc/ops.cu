@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include "tile.cuh"
+#include "async.cuh"
 
 namespace hszg {
 
@@ -85,46 +86,81 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_reduce_tiles(SegGeo sg, const u
     if (threadIdx.x == 0) store_sums(partials + blockIdx.x, a);
 }
 
+// Grid-strided 256-chunk tiles with double-buffered staging: the byte range of the CTA's next tile is
+// copied with 16-B cp.async into the other buffer while the current one decodes (two barriers per
+// tile).  body(c, words, rel) handles chunk c (words: the staged bytes, rel: its byte offset there).
+template <typename Body>
+__device__ __forceinline__ void staged_tiles(const uint8_t* __restrict__ payload, uint64_t len,
+                                             const uint64_t* __restrict__ offsets, int64_t n_chunks, uint8_t* smem,
+                                             uint32_t buf_bytes, Body body) {
+    // byte ranges of the CTA's i-th tile in slot i % 3: a thread one iteration ahead writes a slot no
+    // thread still reads (barrier A of the next iteration separates the third)
+    __shared__ uint64_t s_lo[3], s_hi[3];
+    const int64_t tiles = (n_chunks + TILE_CHUNKS - 1) / TILE_CHUNKS;
+    uint64_t off = 0, end = 0;
+    auto fetch = [&](int64_t t) {                  // this thread's chunk of tile t: start / end bytes
+        const int64_t c = t * TILE_CHUNKS + threadIdx.x;
+        if (t < tiles && c < n_chunks) {
+            off = __ldg(offsets + c);
+            end = c + 1 < n_chunks ? __ldg(offsets + c + 1) : payload_end(offsets, n_chunks, len);
+        }
+    };
+    auto publish = [&](int64_t t, int r) {         // the tile's byte range, from its first / last chunk
+        const int64_t c0 = t * TILE_CHUNKS;
+        const int nch = (int)(n_chunks - c0 < TILE_CHUNKS ? n_chunks - c0 : TILE_CHUNKS);
+        if (threadIdx.x == 0) s_lo[r] = off;
+        if ((int)threadIdx.x == nch - 1) s_hi[r] = end;
+    };
+    auto issue = [&](int b, int r) {
+        uint4* sb = reinterpret_cast<uint4*>(smem + (size_t)b * buf_bytes);
+        const uint64_t base = s_lo[r] & ~(uint64_t)15;
+        const uint32_t nvec = (uint32_t)((s_hi[r] - base + 15) >> 4);
+        const uint4* g = reinterpret_cast<const uint4*>(payload + base);
+        for (uint32_t i = threadIdx.x; i < nvec; i += blockDim.x) cp_async16(sb + i, g + i);
+        if (threadIdx.x == 0) sb[nvec] = make_uint4(0, 0, 0, 0);   // the bit cursor's look-ahead word
+        cp_async_commit();
+    };
+    int64_t t = blockIdx.x;
+    if (t >= tiles) return;
+    fetch(t);
+    publish(t, 0);
+    __syncthreads();
+    issue(0, 0);
+    uint64_t cur = off;
+    for (int i = 0; t < tiles; t += gridDim.x, i++) {
+        const int b = i & 1, r = i % 3, rn = (i + 1) % 3;
+        const int64_t tn = t + gridDim.x;
+        fetch(tn);
+        if (tn < tiles) publish(tn, rn);
+        __syncthreads();                            // (A) next range visible; buffer b^1 no longer read
+        if (tn < tiles) issue(b ^ 1, rn);
+        else cp_async_commit();                     // keep one group per iteration
+        cp_async_wait<1>();                         // this thread's copies of tile t landed
+        __syncthreads();                            // (B) everyone's
+        const int64_t c = t * TILE_CHUNKS + threadIdx.x;
+        if (c < n_chunks) {
+            const uint64_t base = s_lo[r] & ~(uint64_t)15;
+            body(c, reinterpret_cast<const uint32_t*>(smem + (size_t)b * buf_bytes), (uint32_t)(cur - base));
+        }
+        cur = off;
+    }
+    cp_async_wait<0>();
+}
+
 // MetaChunk fast path: every chunk full and every segment full-size (chunk c belongs to segment
 // c / cps), so a chunk decodes with decode32s into int4 groups; sums in int64 / u128 per thread.
 // Grid-strided over tiles: 8 CTAs per SM, one partial per CTA.
 __global__ void __launch_bounds__(TILE_CHUNKS) k_reduce_meta_fast(const uint8_t* __restrict__ payload, uint64_t len,
                                                                   const uint64_t* __restrict__ offsets, int64_t n_chunks,
                                                                   const int32_t* __restrict__ meta, int64_t cps,
-                                                                  int64_t n, HszgSums* partials) {
+                                                                  int64_t n, HszgSums* partials, uint32_t buf_bytes) {
     extern __shared__ __align__(16) uint8_t smem[];
-    __shared__ uint64_t s_lo, s_hi;
-    uint4* sb = reinterpret_cast<uint4*>(smem);
     Acc a;
     a.init();
     u128 s2 = 0;
-    const int64_t tiles = (n_chunks + TILE_CHUNKS - 1) / TILE_CHUNKS;
-    // a thread's chunk start / end and block mean, loaded one tile ahead
-    uint64_t off = 0, end = 0;
-    int32_t m = 0;
-    auto fetch = [&](int64_t t) {
-        const int64_t c = t * TILE_CHUNKS + threadIdx.x;
-        if (t < tiles && c < n_chunks) {
-            off = __ldg(offsets + c);
-            end = c + 1 < n_chunks ? __ldg(offsets + c + 1) : payload_end(offsets, n_chunks, len);
-            m = __ldg(meta + c / cps);
-        }
-    };
-    fetch(blockIdx.x);
-    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int64_t c0 = t * TILE_CHUNKS;
-        const int nch = (int)(n_chunks - c0 < TILE_CHUNKS ? n_chunks - c0 : TILE_CHUNKS);
-        const bool mine = (int)threadIdx.x < nch;
-        if (threadIdx.x == 0) s_lo = off;
-        if ((int)threadIdx.x == nch - 1) s_hi = end;
-        __syncthreads();
-        const uint64_t base = stage_range(payload, s_lo, s_hi, sb);
-        const uint32_t rel = (uint32_t)(off - base);
-        const int32_t mm = m;
-        __syncthreads();
-        fetch(t + gridDim.x);                  // in flight while this tile decodes
-        const uint32_t* words = reinterpret_cast<const uint32_t*>(sb);
-        if (mine && smem_byte(words, rel) <= 27) {
+    staged_tiles(payload, len, offsets, n_chunks, smem, buf_bytes, [&](int64_t c, const uint32_t* words, uint32_t rel) {
+        const int32_t mm = __ldg(meta + c / cps);
+        if (smem_byte(words, rel) <= 27) {
             // |p| < 2^27: sums of the residuals p (q = p + m per chunk), 64-bit sum of squares chained
             // through IMAD.WIDE, then sum q = sum p + 32m, sum q^2 = sum p^2 + 2m sum p + 32m^2
             int64_t sp = 0, sq = 0;
@@ -143,7 +179,7 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_reduce_meta_fast(const uint8_t*
             a.s2 += (i128)sq + (i128)(2 * m64) * (i128)sp + (i128)(32 * m64) * (i128)m64;
             a.vmin = min(a.vmin, mnp + mm);
             a.vmax = max(a.vmax, mxp + mm);
-        } else if (mine) {
+        } else {
             int64_t s1 = 0;
             int mn = a.vmin, mx = a.vmax;
             decode32s<false>(words, rel, mm, [&](int, int4 v) {
@@ -157,9 +193,40 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_reduce_meta_fast(const uint8_t*
             a.vmin = mn;
             a.vmax = mx;
         }
-        __syncthreads();                       // the next tile overwrites the staging buffer
-    }
+    });
     a.s2 += (i128)s2;
+    block_reduce(a);
+    if (threadIdx.x == 0) {
+        a.count = blockIdx.x ? 0 : n;
+        store_sums(partials + blockIdx.x, a);
+    }
+}
+
+// WeightedChunk fast path (stats.py:80-112: sum of (N0-i0)(N1-i1)(N2-i2) p over the box): every chunk
+// full and inside one row (n2 % 32 == 0), so a chunk starting at (i0, i1, x0) contributes
+// (N0-i0)(N1-i1)[(N2-x0) S - T] with S = sum p_j, T = sum j p_j — two integer sums per value, decoded
+// with decode32s; grid-strided tiles as k_reduce_meta_fast.
+__global__ void __launch_bounds__(TILE_CHUNKS) k_reduce_weighted_fast(const uint8_t* __restrict__ payload,
+                                                                      uint64_t len,
+                                                                      const uint64_t* __restrict__ offsets,
+                                                                      int64_t n_chunks, int64_t N0, int64_t N1,
+                                                                      int64_t N2, int64_t n, HszgSums* partials,
+                                                                      uint32_t buf_bytes) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    Acc a;
+    a.init();
+    const int64_t cpr = N2 / kChunkCap;
+    staged_tiles(payload, len, offsets, n_chunks, smem, buf_bytes, [&](int64_t c, const uint32_t* words, uint32_t rel) {
+        int64_t S = 0, T = 0;
+        decode32s<false>(words, rel, 0, [&](int q, int4 v) {
+            S += (int64_t)v.x + v.y + v.z + v.w;
+            T += (int64_t)(4 * q) * v.x + (int64_t)(4 * q + 1) * v.y + (int64_t)(4 * q + 2) * v.z +
+                 (int64_t)(4 * q + 3) * v.w;
+        });
+        const int64_t row = c / cpr, x0 = (c - row * cpr) * kChunkCap;
+        const int64_t i0 = row / N1, i1 = row - i0 * N1;
+        a.s1 += (i128)((N0 - i0) * (N1 - i1)) * ((i128)(N2 - x0) * S - T);
+    });
     block_reduce(a);
     if (threadIdx.x == 0) {
         a.count = blockIdx.x ? 0 : n;
@@ -637,13 +704,22 @@ extern "C" int hszg_reduce_stream(const HszgGeom* g, const HszgStream* s, int mo
         const size_t smem = tile_smem_bytes(s->max_bitwidth);
         bool full_segs = g->n_chunks * kChunkCap == g->n && (sg.B[0] * sg.B[1] * sg.B[2]) % kChunkCap == 0;
         for (int a = 0; a < 3; a++) full_segs = full_segs && sg.E[a] == sg.B[a];
+        if (mode != 3 && g->n_chunks * kChunkCap == g->n && sg.n[2] % kChunkCap == 0) {
+            const uint32_t bb = (uint32_t)((stage_bytes(s->max_bitwidth) + 15) / 16 * 16);
+            allow_smem(k_reduce_weighted_fast, 2 * (size_t)bb);
+            const int64_t grid = tiles < 148 * 6 ? tiles : 148 * 6;
+            k_reduce_weighted_fast<<<(unsigned)grid, TILE_CHUNKS, 2 * (size_t)bb, st>>>(
+                s->payload, s->payload_len, s->offsets, g->n_chunks, sg.n[0], sg.n[1], sg.n[2], g->n, partials, bb);
+            { const cudaError_t e_ = cudaGetLastError(); if (e_ != cudaSuccess) return hszg_set_cuda_error(err, e_, "reduce tiles"); }
+            return finalize(partials, grid, out_dev, st);
+        }
         if (mode == 3 && full_segs) {
-            const size_t fsmem = stage_bytes(s->max_bitwidth);
-            allow_smem(k_reduce_meta_fast, fsmem);
-            const int64_t grid = tiles < 148 * 8 ? tiles : 148 * 8;
-            k_reduce_meta_fast<<<(unsigned)grid, TILE_CHUNKS, fsmem, st>>>(
+            const uint32_t bb = (uint32_t)((stage_bytes(s->max_bitwidth) + 15) / 16 * 16);
+            allow_smem(k_reduce_meta_fast, 2 * (size_t)bb);
+            const int64_t grid = tiles < 148 * 6 ? tiles : 148 * 6;
+            k_reduce_meta_fast<<<(unsigned)grid, TILE_CHUNKS, 2 * (size_t)bb, st>>>(
                 s->payload, s->payload_len, s->offsets, g->n_chunks, s->metadata,
-                (sg.B[0] * sg.B[1] * sg.B[2]) / kChunkCap, g->n, partials);
+                (sg.B[0] * sg.B[1] * sg.B[2]) / kChunkCap, g->n, partials, bb);
             { const cudaError_t e_ = cudaGetLastError(); if (e_ != cudaSuccess) return hszg_set_cuda_error(err, e_, "reduce tiles"); }
             return finalize(partials, grid, out_dev, st);
         }

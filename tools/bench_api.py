@@ -139,6 +139,8 @@ def main():
             if kind.is_block_mean:
                 t = timed(lambda: stats.compute_stat(c, "mean", S.META))
                 record(cfg, kind, "A8 mean at stage 1", n, t, Mb, cpu=lambda: O.compute_stat(oc, "mean", 1))
+            t = timed(lambda: stats.compute_stat(c, "mean", S.DECORRELATED))
+            record(cfg, kind, "A9 mean at stage 2", n, t, P + I + Mb, cpu=lambda: O.compute_stat(oc, "mean", 2))
             for st, name in ((S.DECORRELATED, "stage 2"), (S.QUANTIZED, "stage 3")):
                 t = timed(lambda: stats.compute_stat(c, "var", st))
                 record(cfg, kind, f"N1 variance at {name}", n, t, P + I + Mb,
