@@ -111,7 +111,8 @@ enum {
     HSZG_WS_RECONSTRUCT = 1,   /* out_type selects I32/F32 (in place) or F64 */
     HSZG_WS_REDUCE = 2,
     HSZG_WS_ENCODE = 3,
-    HSZG_WS_QUANTIZE = 4       /* quantize, decorrelate, minmax */
+    HSZG_WS_QUANTIZE = 4,      /* quantize, decorrelate, minmax */
+    HSZG_WS_QSUMS = 5          /* hszg_quantized_sums (0: not supported for this stream) */
 };
 size_t hszg_workspace_bytes(const HszgGeom* g, const HszgStream* s, int op, int out_type);
 const char* hszg_version(void);
@@ -272,6 +273,13 @@ int hszg_zsweep_grad_lap(const int32_t* P2, int64_t n1, int64_t n2, int64_t nout
                          const int32_t* carry, const int32_t* q_upper, int32_t* carry_out, int64_t gz0, int64_t gN0,
                          double eps, float* const* out, HszgAcc* acc, const int32_t* band_off,
                          const int32_t* look_band_off, int64_t band_rows, int p2_mode, int exact, void* stream);
+/* Exact sums of the stage-3 indices q (S1, S2, min, max, count) without writing q: HSZP (every chunk
+ * full: the look-back scan reduces instead of storing) and 3-D HSZP_ND (n2 % 32 == 0, one band per
+ * plane: band scan + a z prefix that reduces).  hszg_workspace_bytes(HSZG_WS_QSUMS) is 0 for other
+ * streams (callers then reconstruct and reduce).  Replaces stats.py:115-173's q = recorrelate(...)
+ * followed by the sums. */
+int hszg_quantized_sums(const HszgGeom* g, const HszgStream* s, HszgSums* out_dev, void* ws, size_t ws_bytes,
+                        void* stream, HszgErr* err);
 /* HSZX_ND one-pass decode + gradient + Laplacian + stats (8x8x8 blocks dividing the 3-D box, canonical,
  * max bit width <= 16): q never reaches memory.  The stream is a z-slab of a gN0-plane field whose
  * first plane is global plane gz0; halo_lo / halo_hi (optional, n1*n2 int32) are q of the planes just

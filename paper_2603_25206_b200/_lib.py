@@ -30,7 +30,7 @@ PAYLOAD_PAD = 16
 
 OK, CORRUPT, EPS_TOO_SMALL, INVALID_ARG, UNSUPPORTED_STAGE, CUDA_ERR, ZERO_RANGE, VALUE = range(8)
 I32, F32, F64 = 0, 1, 2
-WS_VALIDATE, WS_RECONSTRUCT, WS_REDUCE, WS_ENCODE, WS_QUANTIZE = range(5)
+WS_VALIDATE, WS_RECONSTRUCT, WS_REDUCE, WS_ENCODE, WS_QUANTIZE, WS_QSUMS = range(6)
 OP_DERIV, OP_LAPLACIAN, OP_GRADMAG, OP_DIVERGENCE, OP_CURL, OP_GRAD_LAP = range(6)
 
 
@@ -129,6 +129,8 @@ _SIGS = {
     "hszg_stream_perm": [ctypes.POINTER(Geom), _P, _P],
     "hszg_scatter_grid": [ctypes.POINTER(Geom), _P, _P, _I32, _P, _P],
     "hszg_metadata_grid": [ctypes.POINTER(Geom), _P, _P, _P],
+    "hszg_quantized_sums": [ctypes.POINTER(Geom), ctypes.POINTER(StreamDesc), _P, _P, _SZ, _P,
+                            ctypes.POINTER(Err)],
     "hszg_reduce_stream": [ctypes.POINTER(Geom), ctypes.POINTER(StreamDesc), _I32, _P, _P, _SZ, _P,
                            ctypes.POINTER(Err)],
     "hszg_reduce_array": [ctypes.POINTER(Geom), _P, _P, _I32, _P, _P, _SZ, _P],

@@ -255,6 +255,9 @@ def stream_sums(c: CompressedStream, stage: Stage):
         return _lib.read_sums(d.reduce(MODE_META))
     if c.kind.is_block_mean:
         return _lib.read_sums(d.reduce(MODE_BLOCK_MEAN_Q))
+    fused = d.quantized_sums()          # q reduced where it is formed, never written (HSZP, 3-D HSZP_ND)
+    if fused is not None:
+        return _lib.read_sums(fused)
     q = d.reconstruct(t.int32)
     return _lib.read_sums(devmod.reduce_i32(q))
 

@@ -7,6 +7,7 @@
 using namespace hszg;
 
 size_t hszg_reduce_ws_bytes(int64_t tiles);
+size_t hszg_quantized_sums_ws(const HszgGeom* g, const HszgStream* s);
 
 // Derive the segment view of a stream (see common.cuh) from the container's
 // kind / dims / block dims (compressors.py:87-119, 245-270).
@@ -100,6 +101,8 @@ extern "C" size_t hszg_workspace_bytes(const HszgGeom* g, const HszgStream* s, i
             return 16 + lookback_ws_bytes(g->n_chunks) + 256;
         case HSZG_WS_QUANTIZE:
             return 148 * 8 * 32 + 256;
+        case HSZG_WS_QSUMS:
+            return hszg_quantized_sums_ws(g, s);
         default:
             return 0;
     }

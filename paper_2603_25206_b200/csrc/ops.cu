@@ -667,6 +667,10 @@ static int finalize(HszgSums* partials, int64_t nparts, HszgSums* out, cudaStrea
     return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
 }
 
+int hszg_finalize_sums(HszgSums* partials, int64_t nparts, HszgSums* out, cudaStream_t st) {
+    return finalize(partials, nparts, out, st);
+}
+
 extern "C" int hszg_reduce_stream(const HszgGeom* g, const HszgStream* s, int mode, HszgSums* out_dev, void* ws,
                                   size_t ws_bytes, void* stream, HszgErr* err) {
     err->status = HSZG_OK;

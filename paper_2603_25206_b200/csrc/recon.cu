@@ -301,7 +301,8 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_tile_scan(SegGeo sg, const uint
 template <typename OutT>
 __global__ void __launch_bounds__(TILE_CHUNKS) k_tile_scan_fast(const uint8_t* __restrict__ payload, uint64_t len,
                                                                const uint64_t* __restrict__ offsets, int64_t n_chunks,
-                                                               LBState st, double two_eps, OutT* __restrict__ out) {
+                                                               LBState st, double two_eps, OutT* __restrict__ out,
+                                                               HszgSums* partials) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ unsigned int s_tile;
     __shared__ unsigned long long s_prefix;
@@ -334,6 +335,35 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_tile_scan_fast(const uint8_t* _
     __syncthreads();
     s_add[threadIdx.x] = (uint32_t)(s_prefix + excl);
     __syncthreads();
+    if (partials) {                                    // hszg_quantized_sums: reduce q instead of storing it
+        int64_t s1 = 0;
+        u128 s2 = 0;
+        int mn = INT32_MAX, mx = INT32_MIN;
+        for (int g = threadIdx.x; g < nch * 8; g += TILE_CHUNKS) {
+            const int ch = g >> 3;
+            const int4 v = *reinterpret_cast<const int4*>(tile + ch * kChunkStride + ((g & 7) << 2));
+            const uint32_t a = s_add[ch];
+            const int4 q = make_int4((int)((uint32_t)v.x + a), (int)((uint32_t)v.y + a), (int)((uint32_t)v.z + a),
+                                     (int)((uint32_t)v.w + a));
+            s1 += (int64_t)q.x + q.y + q.z + q.w;
+            s2 += (u128)((uint64_t)((int64_t)q.x * q.x) + (uint64_t)((int64_t)q.y * q.y));
+            s2 += (u128)((uint64_t)((int64_t)q.z * q.z) + (uint64_t)((int64_t)q.w * q.w));
+            mn = min(mn, min(min(q.x, q.y), min(q.z, q.w)));
+            mx = max(mx, max(max(q.x, q.y), max(q.z, q.w)));
+        }
+        Acc acc;
+        acc.init();
+        acc.s1 = s1;
+        acc.s2 = (i128)s2;
+        acc.vmin = mn;
+        acc.vmax = mx;
+        block_reduce(acc);
+        if (threadIdx.x == 0) {
+            acc.count = (int64_t)nch * kChunkCap;
+            store_sums(partials + t, acc);
+        }
+        return;
+    }
     OutT* o = out + c0 * kChunkCap;
     for (int g = threadIdx.x; g < nch * 8; g += TILE_CHUNKS) {
         const int ch = g >> 3;
@@ -341,6 +371,50 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_tile_scan_fast(const uint8_t* _
         const uint32_t a = s_add[ch];
         store4<OutT>(o + 4 * g, make_int4((int)((uint32_t)v.x + a), (int)((uint32_t)v.y + a), (int)((uint32_t)v.z + a),
                                           (int)((uint32_t)v.w + a)), two_eps);
+    }
+}
+
+// z prefix (one band per plane: L is the plane's 2-D prefix) reduced instead of stored
+__global__ void __launch_bounds__(256) k_col_scan_sums(const int32_t* __restrict__ src, int64_t M, int64_t Lc,
+                                                       HszgSums* partials) {
+    const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t s1 = 0;
+    u128 s2 = 0;
+    int mn = INT32_MAX, mx = INT32_MIN;
+    if (l < Lc) {
+        uint32_t acc = 0;
+        int64_t m = 0;
+        auto take = [&](uint32_t v) {
+            acc += v;
+            const int q = (int)acc;
+            s1 += q;
+            s2 += (u128)(uint64_t)((int64_t)q * q);
+            mn = min(mn, q);
+            mx = max(mx, q);
+        };
+        for (; m + 4 <= M; m += 4) {
+            const uint32_t v0 = (uint32_t)__ldg(src + m * Lc + l), v1 = (uint32_t)__ldg(src + (m + 1) * Lc + l);
+            const uint32_t v2 = (uint32_t)__ldg(src + (m + 2) * Lc + l), v3 = (uint32_t)__ldg(src + (m + 3) * Lc + l);
+            take(v0);
+            take(v1);
+            take(v2);
+            take(v3);
+        }
+        for (; m < M; m++) take((uint32_t)__ldg(src + m * Lc + l));
+    }
+    Acc a;
+    a.init();
+    a.s1 = s1;
+    a.s2 = (i128)s2;
+    a.vmin = mn;
+    a.vmax = mx;
+    block_reduce(a);
+    // counts are summed by the finalizer: each CTA contributes its active columns x M
+    const int64_t active = (Lc - blockIdx.x * (int64_t)blockDim.x) < blockDim.x ? (Lc - blockIdx.x * (int64_t)blockDim.x)
+                                                                              : blockDim.x;
+    if (threadIdx.x == 0) {
+        a.count = active * M;
+        store_sums(partials + blockIdx.x, a);
     }
 }
 
@@ -849,7 +923,7 @@ static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, 
                     const size_t fsmem = kFastTileBytes + stage_bytes(s->max_bitwidth);
                     allow_smem(k_tile_scan_fast<OutT>, fsmem);
                     k_tile_scan_fast<OutT><<<(unsigned)tiles, TILE_CHUNKS, fsmem, st>>>(
-                        s->payload, s->payload_len, s->offsets, g->n_chunks, lb, two_eps, out);
+                        s->payload, s->payload_len, s->offsets, g->n_chunks, lb, two_eps, out, nullptr);
                     HSZG_CHECK_LAUNCH("reconstruct hszp");
                     return HSZG_OK;
                 }
@@ -1027,4 +1101,62 @@ int hszg_decode_full(const HszgGeom* g, const HszgStream* s, int32_t* out, cudaS
         return 1;
     launch_stream_full<0, int32_t>(g, s, sg, out, st);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+// ---- hszg_quantized_sums -------------------------------------------------------------------------
+size_t hszg_reduce_ws_bytes(int64_t tiles);
+int hszg_finalize_sums(HszgSums* partials, int64_t nparts, HszgSums* out, cudaStream_t st);
+
+// 0 when the stream has no fused path (see include/hszg.h)
+size_t hszg_quantized_sums_ws(const HszgGeom* g, const HszgStream* s) {
+    if (!s || !s->canonical || g->n == 0) return 0;
+    const SegGeo sg = make_seggeo(*g);
+    if (g->kind == HSZG_HSZP && g->n_chunks * kChunkCap == g->n) {
+        const int64_t tiles = (g->n_chunks + TILE_CHUNKS - 1) / TILE_CHUNKS;
+        return lookback_ws_bytes(g->n_chunks) + hszg_reduce_ws_bytes(tiles) + 256;
+    }
+    if (g->kind == HSZG_HSZP_ND && g->ndims == 3 && sg.n[2] % 32 == 0 && sg.n[2] <= 4096 && sg.n[0] <= 65535 &&
+        recon_band_rows(sg.n[0], sg.n[1], sg.n[2]) >= sg.n[1]) {
+        const int64_t Lc = sg.n[1] * sg.n[2];
+        return (size_t)g->n * 4 + (size_t)sg.n[0] * sg.n[2] * 4 + hszg_reduce_ws_bytes((Lc + 255) / 256) + 512;
+    }
+    return 0;
+}
+
+extern "C" int hszg_quantized_sums(const HszgGeom* g, const HszgStream* s, HszgSums* out_dev, void* ws,
+                                   size_t ws_bytes, void* stream, HszgErr* err) {
+    err->status = HSZG_OK;
+    cudaStream_t st = as_stream(stream);
+    const size_t need = hszg_quantized_sums_ws(g, s);
+    if (need == 0 || ws_bytes < need) {
+        err->status = HSZG_INVALID_ARG;
+        snprintf(err->message, sizeof(err->message), "quantized_sums: no fused path for this stream or workspace too small");
+        return HSZG_INVALID_ARG;
+    }
+    const SegGeo sg = make_seggeo(*g);
+    char* w = reinterpret_cast<char*>(ws);
+    if (g->kind == HSZG_HSZP) {
+        const int64_t tiles = (g->n_chunks + TILE_CHUNKS - 1) / TILE_CHUNKS;
+        LBState lb = lookback_carve(ws, tiles);
+        HszgSums* partials = reinterpret_cast<HszgSums*>(w + ((lookback_ws_bytes(g->n_chunks) + 255) & ~(size_t)255));
+        cudaMemsetAsync(ws, 0, lookback_clear_bytes(tiles), st);
+        const size_t fsmem = kFastTileBytes + stage_bytes(s->max_bitwidth);
+        allow_smem(k_tile_scan_fast<int32_t>, fsmem);
+        k_tile_scan_fast<int32_t><<<(unsigned)tiles, TILE_CHUNKS, fsmem, st>>>(
+            s->payload, s->payload_len, s->offsets, g->n_chunks, lb, 0.0, nullptr, partials);
+        HSZG_CHECK_LAUNCH("quantized sums hszp");
+        return hszg_finalize_sums(partials, tiles, out_dev, st);
+    }
+    // HSZP_ND 3-D, one band per plane
+    int32_t* L = reinterpret_cast<int32_t*>(w);
+    int32_t* A = reinterpret_cast<int32_t*>(w + (size_t)g->n * 4);
+    HszgSums* partials = reinterpret_cast<HszgSums*>(w + (((size_t)g->n * 4 + (size_t)sg.n[0] * sg.n[2] * 4 + 255) &
+                                                          ~(size_t)255));
+    const int rr = hszg_band_scan(g, s, sg.n[1], L, A, nullptr, 0, nullptr, st, err);
+    if (rr) return rr;
+    const int64_t Lc = sg.n[1] * sg.n[2];
+    const int64_t nblk = (Lc + 255) / 256;
+    k_col_scan_sums<<<(unsigned)nblk, 256, 0, st>>>(L, sg.n[0], Lc, partials);
+    HSZG_CHECK_LAUNCH("quantized sums hszp-nd");
+    return hszg_finalize_sums(partials, nblk, out_dev, st);
 }

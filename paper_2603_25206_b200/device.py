@@ -168,6 +168,20 @@ class DeviceStream:
 
     # ---- reductions --------------------------------------------------------------
 
+    def quantized_sums(self, out=None):
+        """Exact sums of stage-3 q without writing q (hszg_quantized_sums), or None when this stream
+        has no fused path (the caller reconstructs and reduces)."""
+        self.validate()
+        n = _lib.ws_bytes(self.geom, self.desc, _lib.WS_QSUMS)
+        if n == 0:
+            return None
+        out = _lib.sums_tensor() if out is None else out
+        ws = _lib.workspace(n)
+        err = _lib.Err()
+        _lib.call("hszg_quantized_sums", ctypes.byref(self.geom), ctypes.byref(self.desc), _lib.ptr(out),
+                  _lib.ptr(ws), ws.numel(), _lib.stream_handle(), ctypes.byref(err), err=err)
+        return out
+
     def reduce(self, mode: int, out=None):
         """Fused reduction from the compressed bytes (see hszg_reduce_stream); device Sums buffer."""
         self.validate()

@@ -81,3 +81,23 @@ def test_reduce_i32_extreme_values(n):
     assert s.s1 == int(x.sum())
     assert s.s2 == sum(int(v) * int(v) for v in x.tolist())
     assert s.vmin == int(x.min()) and s.vmax == int(x.max()) and s.count == n
+
+
+@pytest.mark.parametrize("kind,dims,scale", [(0, (8192,), 1.0), (0, (40, 64), 1e6), (1, (12, 10, 64), 1.0),
+                                             (1, (20, 8, 96), 1e6), (1, (300, 3, 32), 1.0)])
+def test_quantized_sums_fused_matches_materialised(kind, dims, scale):
+    """hszg_quantized_sums (q reduced where it is formed) == reconstruct + exact reduce, including
+    |q| near 2^31 (per-thread int128 squares)."""
+    import paper_2603_25206_b200 as h
+    from paper_2603_25206_b200 import _lib, device as devmod
+
+    rng = np.random.default_rng(len(dims) * 10 + kind)
+    f = (O.random_field(rng, dims, "smooth") * scale).astype(np.float32)
+    eps = 1e-6 * float(f.max() - f.min()) if scale > 1 else 1e-3 * float(f.max() - f.min())
+    c = h.compress(f, h.CompressorKind(kind), h.ErrorBound("abs", eps))
+    d = c.device()
+    fused = d.quantized_sums()
+    assert fused is not None
+    a = _lib.read_sums(fused)
+    b = _lib.read_sums(devmod.reduce_i32(d.reconstruct()))
+    assert (a.s1, a.s2, a.vmin, a.vmax, a.count) == (b.s1, b.s2, b.vmin, b.vmax, b.count)
