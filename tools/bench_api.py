@@ -5,8 +5,8 @@ has it; scalar results are host values, so their D2H is inside the timing), warm
 REPS CUDA-event timings.  Throughput is GB/s of original fp32 (4 N / t); the roofline fraction
 uses SURVEY §8(d)'s algorithmic bytes per value with this stream's measured P (payload), I (index)
 and Mb (block means) against MEASURED_PEAKS hbm_gbs.  Synthetic inputs follow §8(d)'s generators
-(`paper_2603_25206_b200.synthetic`), seeded.  On configs 1-2 (``--cpu-configs``) every row is also timed
-once on the CPU oracle (the reference algorithm restated, oracle/, single thread) on the same
+(`paper_2603_25206_b200.synthetic`), seeded.  With ``--cpu-configs 1 2`` (the CPU baseline leg) every row
+of those configs is also timed once on the CPU oracle (the reference algorithm restated, oracle/, single thread) on the same
 container: ``cpu_oracle_ms`` and ``speedup_vs_cpu`` (the CPU path timed beside it).
 
     python tools/bench_api.py [--configs 1 2 3 4] [--out profiles/r01_api_bench.json]
@@ -45,8 +45,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", type=int, nargs="*", default=[1, 2, 3, 4])
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_api_bench.json"))
-    ap.add_argument("--cpu-configs", type=int, nargs="*", default=[1, 2],
-                    help="also time the CPU oracle (reference algorithm restated, 1 thread) on these configs")
+    ap.add_argument("--cpu-configs", type=int, nargs="*", default=[],
+                    help="CPU baseline leg (opt-in): also time the CPU oracle (the reference algorithm restated, "
+                         "1 thread) on these configs, e.g. --cpu-configs 1 2")
     args = ap.parse_args()
 
     import numpy as np
@@ -63,10 +64,11 @@ def main():
     S = h.Stage
     rows = []
 
-    from oracle import hsz_oracle as O
+    O = None
+    if args.cpu_configs:                 # the CPU baseline leg only: the oracle is never the measured path
+        from oracle import hsz_oracle as O
 
-    O.set_threads(1)
-    cpu_on = {"cfg": None}
+        O.set_threads(1)
 
     def record(cfg, kind, row, n, t, algo_per_value, note="", cpu=None):
         gbs = 4.0 * n / t / 1e9
