@@ -374,9 +374,17 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __rest
         uint32_t inc = tot;
         if ((cpr & (cpr - 1)) == 0) {            // rows align with warp segments: segmented shuffle scan
             const int wseg = cpr < 32 ? cpr : 32;
-            for (int d = 1; d < wseg; d <<= 1) {
-                const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
-                if ((lane & (wseg - 1)) >= d) inc += o;
+            if (wseg == 32) {                     // whole-warp rows (n2 >= 1024): unrolled
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+                    if (lane >= d) inc += o;
+                }
+            } else {
+                for (int d = 1; d < wseg; d <<= 1) {
+                    const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+                    if ((lane & (wseg - 1)) >= d) inc += o;
+                }
             }
             if (cpr > 32) {
                 if (lane == 31) s_wt[warp] = inc;
@@ -404,17 +412,17 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __rest
         // rows of the tile: incremental row offsets, uniform k bound (no divergent skips when every
         // thread owns kmax column groups: Full), int16 range by OR of v + 2^15 (bits >= 16 flag it)
         int64_t rowoff = (z * n1 + r0) * (int64_t)n2;
-        for (int rr = 0; rr < nr; rr++, rowoff += n2) {
+        const int32_t* trow = tile;                   // tile row rr: chunks rr*cpr ..
+        const uint32_t* orow = s_off;
+        for (int rr = 0; rr < nr; rr++, rowoff += n2, trow += cpr * kChunkStride, orow += cpr) {
             const int y = r0 + rr;
-            const int chrow = rr * cpr;
 #pragma unroll
             for (int k = 0; k < BS_MAXG; k++) {
                 if (k >= kmax) break;
                 const int gi = threadIdx.x + k * TILE_CHUNKS;
                 if (Full || gi < ng) {
-                    const int ch = chrow + (gi >> 3);
-                    const int4 v = *reinterpret_cast<const int4*>(tile + ch * kChunkStride + ((gi & 7) << 2));
-                    const int4 rv = add4u(v, s_off[ch]);          // row prefix R at x = 4gi .. 4gi+3
+                    const int4 v = *reinterpret_cast<const int4*>(trow + (gi >> 3) * kChunkStride + ((gi & 7) << 2));
+                    const int4 rv = add4u(v, orow[gi >> 3]);      // row prefix R at x = 4gi .. 4gi+3
                     ysum[k] = add4(ysum[k], rv);
                     if (L && LW == 4) *reinterpret_cast<int4*>(static_cast<int32_t*>(L) + rowoff + 4 * gi) = ysum[k];
                     if (L && LW == 2) {
