@@ -118,8 +118,10 @@ __global__ void __launch_bounds__(ZR_T, 2) k_zsweep_ring(ZrArgs a) {
             rw = lrow(LW);
             ra = lrow(LAW);
         } else if (lane < ZR_SROWS) {
-            ok = band[lane - ZR_ROWS] >= 0;
-            rw.off = band[lane - ZR_ROWS] * n2 + xs;
+            const int bi = lane - ZR_ROWS;                 // select, not a dynamically indexed array
+            const int64_t bnd = bi == 0 ? band[0] : (bi == 1 ? band[1] : band[2]);
+            ok = bnd >= 0;
+            rw.off = bnd * n2 + xs;
             rw.bytes = rbytes;
             rw.dst = ZR_ROWS * LB + (lane - ZR_ROWS) * ZR_SW * 4 + (uint32_t)scol * 4;
             ra = rw;
@@ -144,14 +146,15 @@ __global__ void __launch_bounds__(ZR_T, 2) k_zsweep_ring(ZrArgs a) {
             }
             __syncwarp();
             if (ok) {
-                const Row& r = look ? ra : rw;
+                const int64_t roff = look ? ra.off : rw.off;       // by value: no stack copy of the rows
+                const uint32_t rbytes_ = look ? ra.bytes : rw.bytes, rdst = look ? ra.dst : rw.dst;
                 const uint8_t* src;
                 if (lane < ZR_ROWS)
                     src = static_cast<const uint8_t*>(look ? a.lookahead : a.L) +
-                          ((look ? 0 : zz * plane) + r.off) * (look ? LAW : LW);
+                          ((look ? 0 : zz * plane) + roff) * (look ? LAW : LW);
                 else
-                    src = reinterpret_cast<const uint8_t*>((look ? a.lookA : a.A + zz * a.nb * n2) + r.off);
-                tma_load_1d(S + (size_t)slot * SLOT + r.dst, src, r.bytes, &s_full[slot]);
+                    src = reinterpret_cast<const uint8_t*>((look ? a.lookA : a.A + zz * a.nb * n2) + roff);
+                tma_load_1d(S + (size_t)slot * SLOT + rdst, src, rbytes_, &s_full[slot]);
             }
         }
         return;
