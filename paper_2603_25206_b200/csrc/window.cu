@@ -7,8 +7,9 @@
 //             P2 = 2-D prefix per plane), then k_zsweep: the z prefix q[z] = q[z-1] + P2[z] kept in
 //             registers as running sums at the centre row and the rows y+-1, producing gradient +
 //             Laplacian + stats without ever writing q, and handing q[b-1] to the next window.
-// Integer stencils and fp64 scaling reproduce fields.py:34-80 exactly; outputs are fp32
-// (one rounding of the reference float64), written with streaming stores.
+// Integer stencils reproduce fields.py:34-80 exactly; fp32 outputs are either one rounding of the
+// reference float64 (exact mode) or int32 stencil x fl32(eps) in fp32 (fast mode, <= 4 ulp, valid
+// while |q| < 2^27 — the pipeline checks and redoes exactly), written with streaming stores.
 // Statistics: exact int128 per thread, warp-reduced, added into 32-bit limbs with 64-bit
 // atomics (HszgAcc) — order-independent and exact, finished on the host in Python ints.
 #include <cstdio>
@@ -410,7 +411,8 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __rest
         __syncthreads();
         const int nstrips = (n2 + SE_W - 1) / SE_W;
         // rows of the tile: incremental row offsets, uniform k bound (no divergent skips when every
-        // thread owns kmax column groups: Full), int16 range by OR of v + 2^15 (bits >= 16 flag it)
+        // thread owns kmax column groups: Full), narrow-range check by OR of v + 2^15 / 2^7 (bits >= 16 / 8
+        // flag it)
         int64_t rowoff = (z * n1 + r0) * (int64_t)n2;
         const int32_t* trow = tile;                   // tile row rr: chunks rr*cpr ..
         const uint32_t* orow = s_off;
