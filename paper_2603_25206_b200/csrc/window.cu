@@ -1,12 +1,12 @@
 // window.cu — the windowed 3-D analytics kernels of pipeline.py (config-5 hot loop).
 //
-// Per window of W planes:
-//   HSZX_ND : k_tile_blocks (decode + p+M + block->row-major transpose, recon.cu) into a q window,
-//             then k_zgrad_lap: gradient + Laplacian + exact stats, each thread sliding along z.
-//   HSZP_ND : k_tile_rowscan (decode + in-row prefix fused: R = x-prefix of p), k_col_scan (y prefix:
-//             P2 = 2-D prefix per plane), then k_zsweep: the z prefix q[z] = q[z-1] + P2[z] kept in
-//             registers as running sums at the centre row and the rows y+-1, producing gradient +
-//             Laplacian + stats without ever writing q, and handing q[b-1] to the next window.
+// Default path (pipeline.py): HSZX_ND in one pass (fused.cu); HSZP_ND per window of W planes:
+//   k_band_scan (here): decode + row (x) prefix + in-band column (y) prefix -> band-local L (int8 /
+//             int16 / int32) and band totals, k_band_prefix -> exclusive band offsets A;
+//   k_zsweep_ring (zring.cu): q[z] = q[z-1] + L + A in a shared ring + gradient + Laplacian + stats,
+//             q never written, q[b-1] handed to the next window.
+// Also here, for other shapes: k_zgrad_lap (HSZX_ND windows decoded by k_tile_blocks) and k_zsweep
+// (per-column z prefix over int32 P2), each thread sliding along z.
 // Integer stencils reproduce fields.py:34-80 exactly; fp32 outputs are either one rounding of the
 // reference float64 (exact mode) or int32 stencil x fl32(eps) in fp32 (fast mode, <= 4 ulp, valid
 // while |q| < 2^27 — the pipeline checks and redoes exactly), written with streaming stores.
