@@ -1,10 +1,11 @@
 // encode.cu — the compress side (K-ENC): value range, quantization and decorrelation.
 //
 //   resolve_eps  quant.py:56-66         -> k_minmax (+ NaN/Inf count)
-//   quantize     quant.py:69-82         -> k_quantize: floor(d*recip + 0.5) in fp64 with the
+//   quantize     quant.py:69-82         -> k_quantize(_f32x4): floor(d*recip + 0.5) in fp64 with the
 //                                          multiply and add rounded separately (no FMA, as numpy)
-//   decorrelate  compressors.py:149-198 -> k_decor_prev (HSZP), k_decor_lorenzo (HSZP_ND),
-//                                          k_decor_blockmean (HSZX, HSZX_ND; truncating means 134-138)
+//   decorrelate  compressors.py:149-198 -> k_decor_prev(_x4) (HSZP), k_decor_lorenzo(_x4) (HSZP_ND),
+//                                          k_decor_blockmean(_tiles, _1d) (HSZX, HSZX_ND; truncating
+//                                          means 134-138)
 // The chunk encoder proper (bit widths, scan, pack) lives in codec.cu.
 #include <cstdio>
 #include <cfloat>

@@ -2,10 +2,14 @@
 //
 // Reference: recorrelate (compressors.py:201-226) and the stage-4 dequantize
 // q.astype(float64) * (2.0*eps) (stages.py:88).
-//   HSZX    : q = p + M_b, stream order == row-major          -> k_tile_stream<add_meta>
-//   HSZX_ND : q = p + M_b scattered block-contiguous -> row-major -> k_tile_blocks (smem transpose)
-//   HSZP    : q = inclusive cumsum of p over the flat stream  -> k_tile_scan (decoupled look-back)
-//   HSZP_ND : q = cumsum along every axis (Lorenzo inverse)     -> decode + row scan + column scans
+//   HSZX    : q = p + M_b, stream order == row-major          -> k_stream_full<1> (full chunks) /
+//                                                                 k_tile_stream<add_meta>
+//   HSZX_ND : q = p + M_b scattered block-contiguous -> row-major -> k_stream_full<2> / k_tile_blocks_fast /
+//                                                                 k_tile_blocks (smem transpose)
+//   HSZP    : q = inclusive cumsum of p over the flat stream  -> k_tile_scan(_fast) (decoupled look-back)
+//   HSZP_ND : q = cumsum along every axis (Lorenzo inverse)     -> 3-D, n2 % 32 == 0: hszg_band_scan +
+//             z prefix (k_col_scan / k_col_scan_bands); otherwise decode + row scan + column scans
+//   hszg_quantized_sums: the HSZP / 3-D HSZP_ND scans reduce q instead of storing it
 // All arithmetic is int32 with wrap-around: every prefix equals a q value,
 // which fits int32, so modular sums are exact (the reference casts its int64
 // result back to int32, compressors.py:226).
