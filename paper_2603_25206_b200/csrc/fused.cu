@@ -13,7 +13,7 @@
 // y, x, so chunk 2*zl + h holds rows 4h..4h+3 of plane zl); halo block rows decode only the row
 // next to the CTA.
 //
-// Pipeline (warp-specialised): warp 0 loads (TMA), warps 1-7 decode, warps 8-23 emit.  full[s] /
+// Pipeline (warp-specialised): warp 0 loads (TMA), warps 1-11 decode, warps 12-19 emit.  full[s] /
 // empty[s] mbarriers hand ring slot s (plane z in slot z % NPL) between decoders and emitters;
 // stage[b] carries the TMA transaction bytes of staging buffer b (layer L in buffer L & 1) to the
 // decoders, free[b] hands the buffer back to the loader when the decoders moved past its layer.
@@ -24,10 +24,11 @@
 
 namespace hszg {
 
-constexpr int FX_T = 512;                  // threads
-constexpr int FX_PT = 256;                 // producers: warp 0 loads, warps 1-7 decode
-constexpr int FX_CT = FX_T - FX_PT;        // consumers: warps 8-15
-constexpr int FX_DT = FX_PT - 32;          // decoders: warps 1-7 (warp 0 loads)
+constexpr int FX_T = 640;                  // threads
+constexpr int FX_PT = 384;                 // producers: warp 0 loads, warps 1-11 decode
+constexpr int FX_CT = FX_T - FX_PT;        // consumers: warps 12-19
+constexpr int FX_DT = FX_PT - 32;          // decoders: warps 1-11 (warp 0 loads): 352 >= the 324 row
+                                           // jobs of a plane, one job each (7 warps: two; 3.5% slower)
 constexpr int FX_BX = 16;                  // blocks along x per CTA
 constexpr int FX_BY = 2;                   // block rows per CTA
 constexpr int FX_ROWS = FX_BY * 8 + 2;     // ring rows: y0-1 .. y0+16
