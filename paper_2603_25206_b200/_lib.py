@@ -341,7 +341,7 @@ def sums_tensor():
     return t.empty(SUMS_BYTES, dtype=t.uint8, device=device())
 
 
-_PINNED_SUMS: dict = {}
+_PINNED_SUMS = threading.local()      # per thread: the API stays reentrant across threads
 
 
 def read_sums(buf) -> Sums:
@@ -350,9 +350,12 @@ def read_sums(buf) -> Sums:
     if buf.numel() != SUMS_BYTES or not buf.is_cuda:
         return Sums.from_buffer_copy(buf.cpu().numpy().tobytes())
     idx = buf.device.index
-    host = _PINNED_SUMS.get(idx)
+    cache = getattr(_PINNED_SUMS, "bufs", None)
+    if cache is None:
+        cache = _PINNED_SUMS.bufs = {}
+    host = cache.get(idx)
     if host is None:
-        host = _PINNED_SUMS[idx] = t.empty(SUMS_BYTES, dtype=t.uint8, pin_memory=True)
+        host = cache[idx] = t.empty(SUMS_BYTES, dtype=t.uint8, pin_memory=True)
     host.copy_(buf, non_blocking=True)
     t.cuda.current_stream(buf.device).synchronize()
     return Sums.from_buffer_copy(host.numpy().tobytes())
