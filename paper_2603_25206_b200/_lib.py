@@ -237,22 +237,23 @@ def ptr(t) -> int:
 
 
 # ---------------------------------------------------------------------------
-# workspace: one growing device buffer per device (kernels on one stream use it in order)
+# workspace: one growing device buffer per (device, stream) — kernels on one stream use it in order,
+# callers on different streams (threads) get different buffers
 
 _WS: dict = {}
 
 
 def workspace(nbytes: int):
     t = torch()
-    dev = t.cuda.current_device()
-    buf = _WS.get(dev)
+    key = (t.cuda.current_device(), stream_handle())
+    buf = _WS.get(key)
     nbytes = max(int(nbytes), 256)
     if buf is None or buf.numel() < nbytes:
-        _WS[dev] = None
+        _WS[key] = None
         if buf is not None:
             del buf
         buf = t.empty(nbytes, dtype=t.uint8, device=device())
-        _WS[dev] = buf
+        _WS[key] = buf
     return buf
 
 
