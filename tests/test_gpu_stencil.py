@@ -101,3 +101,40 @@ def test_quantized_sums_fused_matches_materialised(kind, dims, scale):
     a = _lib.read_sums(fused)
     b = _lib.read_sums(devmod.reduce_i32(d.reconstruct()))
     assert (a.s1, a.s2, a.vmin, a.vmax, a.count) == (b.s1, b.s2, b.vmin, b.vmax, b.count)
+
+
+def test_api_reentrant_across_threads():
+    """Two threads, each on its own CUDA stream, run the statistics / stage-3 API concurrently on
+    different streams: per-stream workspaces and per-thread read-back buffers keep them apart."""
+    import threading
+
+    import torch
+
+    import paper_2603_25206_b200 as h
+    from paper_2603_25206_b200.analytics import stats
+
+    rng = np.random.default_rng(11)
+    fields = [O.random_field(rng, (24, 40, 64), "smooth") for _ in range(2)]
+    cs = [h.compress(f, h.CompressorKind(k), h.ErrorBound("rel", 1e-3)) for f, k in zip(fields, (1, 3))]
+    want = [(stats.compute_stat(c, "var", h.Stage.QUANTIZED).value,
+             h.partial_decompress(c, h.Stage.QUANTIZED).values.copy()) for c in cs]
+    errors = []
+
+    def work(i):
+        try:
+            with torch.cuda.stream(torch.cuda.Stream()):
+                for _ in range(20):
+                    v = stats.compute_stat(cs[i], "var", h.Stage.QUANTIZED).value
+                    q = h.partial_decompress(cs[i], h.Stage.QUANTIZED).values
+                    if v != want[i][0] or not np.array_equal(q, want[i][1]):
+                        errors.append(i)
+                        return
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(repr(e))
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errors, errors
