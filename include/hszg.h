@@ -242,6 +242,15 @@ int hszg_quantize_f64(const double* field, int64_t n, double recip, int32_t* q, 
 /* p (stream order) + metadata from q (row-major); synchronous status (EpsTooSmallError). */
 int hszg_decorrelate(const HszgGeom* g, const int32_t* q, int32_t* p, int32_t* metadata, void* ws,
                      size_t ws_bytes, void* stream, HszgErr* err);
+/* hszg_decorrelate fused with the encoder's per-chunk bit widths and byte sizes (_bitpack.pyx:24-51):
+ * when every chunk holds 32 values and the decorrelation kernel sees whole chunks, sizes[c] /
+ * bitwidths[c] are written too and *fused = 1 (then hszg_encode_offsets scans them, and p is not
+ * re-read); otherwise *fused = 0 and the caller runs hszg_encode_sizes. */
+int hszg_decorrelate_sized(const HszgGeom* g, const int32_t* q, int32_t* p, int32_t* metadata, uint64_t* sizes,
+                           uint8_t* bitwidths, int* fused, void* ws, size_t ws_bytes, void* stream, HszgErr* err);
+/* Exclusive scan of precomputed chunk sizes (in place: sizes -> offsets) and the payload total. */
+int hszg_encode_offsets(const HszgGeom* g, uint64_t* offsets, uint64_t* total_host, void* ws, size_t ws_bytes,
+                        void* stream, HszgErr* err);
 
 /* ---- windowed 3-D pipeline (pipeline.py; Algorithm 3 on the device) -------------------------- */
 /* fp32 outputs: exact != 0 gives fl32(fl64(D*eps)) (one rounding of the reference float64); exact == 0

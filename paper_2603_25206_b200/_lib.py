@@ -148,6 +148,10 @@ _SIGS = {
     "hszg_quantize_f32": [_P, _I64, _D, _P, _P, _SZ, _P, ctypes.POINTER(Err)],
     "hszg_quantize_f64": [_P, _I64, _D, _P, _P, _SZ, _P, ctypes.POINTER(Err)],
     "hszg_decorrelate": [ctypes.POINTER(Geom), _P, _P, _P, _P, _SZ, _P, ctypes.POINTER(Err)],
+    "hszg_decorrelate_sized": [ctypes.POINTER(Geom), _P, _P, _P, _P, _P, ctypes.POINTER(ctypes.c_int), _P, _SZ, _P,
+                               ctypes.POINTER(Err)],
+    "hszg_encode_offsets": [ctypes.POINTER(Geom), _P, ctypes.POINTER(ctypes.c_uint64), _P, _SZ, _P,
+                            ctypes.POINTER(Err)],
     "hszg_acc_reset": [_P, _P],
     "hszg_zgrad_lap": [_P, _I64, _I64, _I64, _I64, _I64, _I64, _D, _P, _P, _P, _P, _I32, _P],
     "hszg_zsweep_grad_lap": [_P, _I64, _I64, _I64, _P, _P, _P, _P, _I64, _I64, _D, _P, _P, _P, _P, _I64, _I32, _I32,

@@ -398,21 +398,36 @@ class CompressedStream:
 
 
 def compress_device(field_dev, kind: CompressorKind, eps: float, block_dims) -> DeviceStream:
-    """Quantize + decorrelate + encode a CUDA float field into a DeviceStream (no host copies)."""
+    """Quantize + decorrelate + encode a CUDA float field into a DeviceStream (no host copies).  The
+    decorrelation kernel also emits the chunk bit widths / sizes when every chunk is full
+    (hszg_decorrelate_sized), so p is read once more only by the packer."""
     t = _lib.torch()
     kind = CompressorKind(kind)
     shape = GridShape(tuple(field_dev.shape))
     q = quantize_device(field_dev, eps)
-    p, meta, g = _decorrelate_device(q, kind, shape, block_dims, eps)
-    del q
+    g = _lib.make_geom(int(kind), shape.dims, block_dims, eps)
     n_chunks = int(g.n_chunks)
     offs = t.empty(max(n_chunks, 1), dtype=t.int64, device=_lib.device())[:n_chunks]
     bws = t.empty(max(n_chunks, 1), dtype=t.uint8, device=_lib.device())
-    total = ctypes.c_uint64(0)
+    p = t.empty(shape.total, dtype=t.int32, device=_lib.device())
+    meta = t.empty(max(int(g.n_blocks), 1), dtype=t.int32, device=_lib.device()) if kind.is_block_mean else None
+    fused = ctypes.c_int(0)
     err = _lib.Err()
-    ws = _lib.workspace(_lib.ws_bytes(g, None, _lib.WS_ENCODE))
-    _lib.call("hszg_encode_sizes", ctypes.byref(g), _lib.ptr(p), _lib.ptr(offs), _lib.ptr(bws), ctypes.byref(total),
+    ws = _lib.workspace(256)
+    _lib.call("hszg_decorrelate_sized", ctypes.byref(g), _lib.ptr(_as_device(q, t.int32).reshape(-1)), _lib.ptr(p),
+              _lib.ptr(meta) if meta is not None else None, _lib.ptr(offs), _lib.ptr(bws), ctypes.byref(fused),
               _lib.ptr(ws), ws.numel(), _lib.stream_handle(), ctypes.byref(err), err=err)
+    if meta is not None:
+        meta = meta[: int(g.n_blocks)]
+    del q
+    total = ctypes.c_uint64(0)
+    ws = _lib.workspace(_lib.ws_bytes(g, None, _lib.WS_ENCODE))
+    if fused.value:
+        _lib.call("hszg_encode_offsets", ctypes.byref(g), _lib.ptr(offs), ctypes.byref(total), _lib.ptr(ws),
+                  ws.numel(), _lib.stream_handle(), ctypes.byref(err), err=err)
+    else:
+        _lib.call("hszg_encode_sizes", ctypes.byref(g), _lib.ptr(p), _lib.ptr(offs), _lib.ptr(bws),
+                  ctypes.byref(total), _lib.ptr(ws), ws.numel(), _lib.stream_handle(), ctypes.byref(err), err=err)
     plen = int(total.value)
     payload = t.zeros(plen + _lib.PAYLOAD_PAD, dtype=t.uint8, device=_lib.device())
     _lib.call("hszg_encode_pack", ctypes.byref(g), _lib.ptr(p), _lib.ptr(offs), _lib.ptr(bws), _lib.ptr(payload),

@@ -567,6 +567,32 @@ static int encode_sizes_impl(Spans sp, int64_t n_chunks, const int32_t* vals, ui
     return HSZG_OK;
 }
 
+// sizes already written (hszg_decorrelate_sized): the exclusive scan into offsets and the total
+extern "C" int hszg_encode_offsets(const HszgGeom* g, uint64_t* offsets, uint64_t* total_host, void* ws,
+                                   size_t ws_bytes, void* stream, HszgErr* err) {
+    err->status = HSZG_OK;
+    cudaStream_t st = as_stream(stream);
+    const int64_t n_chunks = g->n_chunks;
+    const size_t need = 16 + lookback_ws_bytes(n_chunks);
+    if (ws_bytes < need) {
+        err->status = HSZG_INVALID_ARG;
+        snprintf(err->message, sizeof(err->message), "workspace too small for encode (%zu < %zu)", ws_bytes, need);
+        return HSZG_INVALID_ARG;
+    }
+    uint64_t* total = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(ws) + 8);
+    void* scan_ws = reinterpret_cast<char*>(ws) + 16;
+    if (n_chunks > 0) {
+        int r = exclusive_scan_u64(offsets, offsets, n_chunks, total, scan_ws, st);
+        if (r) return hszg_set_cuda_error(err, cudaGetLastError(), "encode scan");
+    } else {
+        cudaMemsetAsync(total, 0, 8, st);
+    }
+    cudaMemcpyAsync(total_host, total, 8, cudaMemcpyDeviceToHost, st);
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return hszg_set_cuda_error(err, e, "encode sync");
+    return HSZG_OK;
+}
+
 extern "C" int hszg_encode_spans_sizes(const int32_t* values, const int64_t* starts, const int64_t* ends,
                                        int64_t n_chunks, uint64_t* offsets, uint8_t* bitwidths,
                                        uint64_t* total_host, void* ws, size_t ws_bytes, void* stream, HszgErr* err) {

@@ -112,6 +112,23 @@ __global__ void k_decor_lorenzo(const int32_t* q, int64_t N0, int64_t N1, int64_
     if (f) atomicOr(flags, f);
 }
 
+// Fused encoder front (hszg_decorrelate_sized): the bit width of a full 32-value chunk from its
+// lanes' magnitude maxima (a group of G aligned lanes, xor-reduced), recorded by the group's first lane
+// as the encoder's per-chunk size (_bitpack.pyx:24-51), so hszg_encode_sizes' read of p is skipped.
+template <int G>
+__device__ __forceinline__ void chunk_size_out(uint32_t m, int lane, int64_t chunk, uint64_t* sizes, uint8_t* bws) {
+#pragma unroll
+    for (int d = 1; d < G; d <<= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, d));
+    if ((lane & (G - 1)) == 0 && chunk >= 0) {
+        const int bw = m ? 32 - __clz(m) : 0;
+        bws[chunk] = (uint8_t)bw;
+        sizes[chunk] = (uint64_t)chunk_bytes(kChunkCap, bw);
+    }
+}
+__device__ __forceinline__ uint32_t mag4(int32_t a, int32_t b, int32_t c, int32_t d) {
+    return max(max((uint32_t)abs(a), (uint32_t)abs(b)), max((uint32_t)abs(c), (uint32_t)abs(d)));
+}
+
 // HSZX 1-D with segments of B | 32 values (B a power of two): one value per lane, the B lanes of a
 // segment reduce by xor-shuffles inside their aligned group (no per-segment index arithmetic); four
 // 32-value groups per warp and step (loads in flight), 32-bit sums when every |q| < 2^26.
@@ -121,7 +138,8 @@ __device__ __forceinline__ int64_t trunc_div(int64_t s, int size, int lgB, bool 
 }
 
 __global__ void k_decor_blockmean_1d(const int32_t* __restrict__ q, int64_t n, int lgB, int32_t* __restrict__ p,
-                                     int32_t* __restrict__ meta, unsigned int* flags) {
+                                     int32_t* __restrict__ meta, unsigned int* flags, uint64_t* sizes,
+                                     uint8_t* bws) {
     constexpr int U = 4;
     const int lane = threadIdx.x & 31;
     const int B = 1 << lgB;
@@ -159,7 +177,12 @@ __global__ void k_decor_blockmean_1d(const int32_t* __restrict__ q, int64_t n, i
                 const int64_t d = (int64_t)v[u] - mean;
                 if (d > kPmax || d < -kPmax) f |= 1u;
                 p[i] = (int32_t)d;
+                v[u] = (int32_t)d;
+            } else {
+                v[u] = 0;
             }
+            if (sizes)   // B == 32, n % 32 == 0: these 32 lanes are one chunk
+                chunk_size_out<32>((uint32_t)abs(v[u]), lane, i < n ? i >> 5 : -1, sizes, bws);
         }
     }
     if (f) atomicOr(flags, f);
@@ -199,7 +222,8 @@ __device__ __forceinline__ int32_t diff1(int64_t a, int64_t b, unsigned int& f) 
 }
 
 // HSZP on 4-value groups: the previous value of a group's first element is the previous lane's .w
-__global__ void k_decor_prev_x4(const int4* __restrict__ q, int64_t n4, int4* __restrict__ p, unsigned int* flags) {
+__global__ void k_decor_prev_x4(const int4* __restrict__ q, int64_t n4, int4* __restrict__ p, unsigned int* flags,
+                                uint64_t* sizes, uint8_t* bws) {
     unsigned int f = 0;
     const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -209,8 +233,12 @@ __global__ void k_decor_prev_x4(const int4* __restrict__ q, int64_t n4, int4* __
         const int4 v = act ? __ldg(q + i) : make_int4(0, 0, 0, 0);
         int prev = __shfl_up_sync(0xffffffffu, v.w, 1);
         if (lane == 0) prev = (act && i > 0) ? __ldg(reinterpret_cast<const int32_t*>(q) + 4 * i - 1) : 0;
-        if (act)
-            p[i] = make_int4(diff1(v.x, prev, f), diff1(v.y, v.x, f), diff1(v.z, v.y, f), diff1(v.w, v.z, f));
+        int4 o = make_int4(0, 0, 0, 0);
+        if (act) {
+            o = make_int4(diff1(v.x, prev, f), diff1(v.y, v.x, f), diff1(v.z, v.y, f), diff1(v.w, v.z, f));
+            p[i] = o;
+        }
+        if (sizes) chunk_size_out<8>(mag4(o.x, o.y, o.z, o.w), lane, act ? i >> 3 : -1, sizes, bws);
     }
     if (f) atomicOr(flags, f);
 }
@@ -218,7 +246,7 @@ __global__ void k_decor_prev_x4(const int4* __restrict__ q, int64_t n4, int4* __
 // HSZP_ND 3-D (box view) on 4 x-consecutive points: p = sum over the 2^3 lower corners with signs,
 // written as the x-differences of the rows (z,y), (z,y-1), (z-1,y), (z-1,y-1); x-1 by shuffle
 __global__ void k_decor_lorenzo_x4(const int32_t* __restrict__ q, int64_t N0, int64_t N1, int64_t N2,
-                                   int32_t* __restrict__ p, unsigned int* flags) {
+                                   int32_t* __restrict__ p, unsigned int* flags, uint64_t* sizes, uint8_t* bws) {
     const int lane = threadIdx.x & 31;
     const int64_t x = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
     const int64_t i1 = blockIdx.y, i0 = blockIdx.z;
@@ -245,15 +273,18 @@ __global__ void k_decor_lorenzo_x4(const int32_t* __restrict__ q, int64_t N0, in
         d[k][2] = (int64_t)r[k].z - r[k].y;
         d[k][3] = (int64_t)r[k].w - r[k].z;
     }
-    if (!act) return;
     unsigned int f = 0;
     int32_t o[4];
 #pragma unroll
     for (int j = 0; j < 4; j++) {
         const int64_t acc = d[0][j] - d[1][j] - d[2][j] + d[3][j];
         if (acc > kPmax || acc < -kPmax) f |= 1u;
-        o[j] = (int32_t)acc;
+        o[j] = act ? (int32_t)acc : 0;
     }
+    if (sizes)   // n2 % 32 == 0: 8 lanes = one chunk of this row
+        chunk_size_out<8>(mag4(o[0], o[1], o[2], o[3]), lane, act ? ((i0 * N1 + i1) * N2 + xi) >> 5 : -1, sizes,
+                          bws);
+    if (!act) return;
     *reinterpret_cast<int4*>(p + (i0 * N1 + i1) * N2 + xi) = make_int4(o[0], o[1], o[2], o[3]);
     if (f) atomicOr(flags, f);
 }
@@ -270,7 +301,8 @@ constexpr int BT_THREADS = 256, BT_ELEMS = 8192;
 __global__ void __launch_bounds__(BT_THREADS) k_decor_blockmean_tiles(SegGeo sg, int64_t tpr, int kb,
                                                                       const int32_t* __restrict__ q,
                                                                       int32_t* __restrict__ p,
-                                                                      int32_t* __restrict__ meta, unsigned int* flags) {
+                                                                      int32_t* __restrict__ meta, unsigned int* flags,
+                                                                      uint64_t* sizes, uint8_t* bws) {
     __shared__ __align__(16) int32_t tile[BT_ELEMS];
     const int B0 = (int)sg.B[0], B1 = (int)sg.B[1], B2 = (int)sg.B[2];
     const int segsz = B0 * B1 * B2;
@@ -304,17 +336,24 @@ __global__ void __launch_bounds__(BT_THREADS) k_decor_blockmean_tiles(SegGeo sg,
         const int64_t mean = (sum >= INT32_MIN && sum <= INT32_MAX) ? (int64_t)((int32_t)sum / segsz) : sum / segsz;
         if (lane == 0) meta[seg0 + t] = (int32_t)mean;
         int4* pb = reinterpret_cast<int4*>(p + (seg0 + t) * segsz);
-        for (int j = lane; j < segsz / 4; j += 32) {
-            const int4 v = *reinterpret_cast<const int4*>(tb + 4 * j);
-            int32_t o[4];
-            const int32_t a[4] = {v.x, v.y, v.z, v.w};
+        for (int j0 = 0; j0 < segsz / 4; j0 += 32) {          // every lane takes part (chunk shuffles)
+            const int j = j0 + lane;
+            const bool act = j < segsz / 4;
+            int32_t o[4] = {0, 0, 0, 0};
+            if (act) {
+                const int4 v = *reinterpret_cast<const int4*>(tb + 4 * j);
+                const int32_t a[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-            for (int e = 0; e < 4; e++) {
-                const int64_t d = (int64_t)a[e] - mean;
-                if (d > kPmax || d < -kPmax) f |= 1u;
-                o[e] = (int32_t)d;
+                for (int e = 0; e < 4; e++) {
+                    const int64_t d = (int64_t)a[e] - mean;
+                    if (d > kPmax || d < -kPmax) f |= 1u;
+                    o[e] = (int32_t)d;
+                }
+                pb[j] = make_int4(o[0], o[1], o[2], o[3]);
             }
-            pb[j] = make_int4(o[0], o[1], o[2], o[3]);
+            if (sizes)   // 8 lanes = one chunk of the block (32 | segsz)
+                chunk_size_out<8>(mag4(o[0], o[1], o[2], o[3]), lane,
+                                  act ? (seg0 + t) * (segsz / kChunkCap) + (j >> 3) : -1, sizes, bws);
         }
     }
     if (f) atomicOr(flags, f);
@@ -486,8 +525,24 @@ extern "C" int hszg_quantize_f64(const double* field, int64_t n, double recip, i
     return quantize_impl(field, n, recip, q, ws, ws_bytes, as_stream(stream), err);
 }
 
+static int decorrelate_impl(const HszgGeom* g, const int32_t* q, int32_t* p, int32_t* metadata, uint64_t* sizes,
+                            uint8_t* bws, int* fused, void* ws, size_t ws_bytes, void* stream, HszgErr* err);
+
 extern "C" int hszg_decorrelate(const HszgGeom* g, const int32_t* q, int32_t* p, int32_t* metadata, void* ws,
                                 size_t ws_bytes, void* stream, HszgErr* err) {
+    return decorrelate_impl(g, q, p, metadata, nullptr, nullptr, nullptr, ws, ws_bytes, stream, err);
+}
+
+extern "C" int hszg_decorrelate_sized(const HszgGeom* g, const int32_t* q, int32_t* p, int32_t* metadata,
+                                      uint64_t* sizes, uint8_t* bitwidths, int* fused, void* ws, size_t ws_bytes,
+                                      void* stream, HszgErr* err) {
+    return decorrelate_impl(g, q, p, metadata, sizes, bitwidths, fused, ws, ws_bytes, stream, err);
+}
+
+static int decorrelate_impl(const HszgGeom* g, const int32_t* q, int32_t* p, int32_t* metadata, uint64_t* sizes,
+                            uint8_t* bws, int* fused, void* ws, size_t ws_bytes, void* stream, HszgErr* err) {
+    if (fused) *fused = 0;
+    const bool full = sizes && bws && g->n_chunks * kChunkCap == g->n;   // every chunk 32 values
     err->status = HSZG_OK;
     cudaStream_t st = as_stream(stream);
     if (ws_bytes < 4) return HSZG_INVALID_ARG;
@@ -497,10 +552,12 @@ extern "C" int hszg_decorrelate(const HszgGeom* g, const int32_t* q, int32_t* p,
     if (g->n > 0) {
         switch (g->kind) {
             case HSZG_HSZP:
-                if (g->n % 4 == 0 && al16(q) && al16(p))
+                if (g->n % 4 == 0 && al16(q) && al16(p)) {
                     k_decor_prev_x4<<<grid_for(g->n / 4, 256 * 4, 148 * 16), 256, 0, st>>>(
-                        reinterpret_cast<const int4*>(q), g->n / 4, reinterpret_cast<int4*>(p), flags);
-                else
+                        reinterpret_cast<const int4*>(q), g->n / 4, reinterpret_cast<int4*>(p), flags,
+                        full ? sizes : nullptr, bws);
+                    if (full) *fused = 1;
+                } else
                     k_decor_prev<<<grid_for(g->n, 256 * 4, 148 * 32), 256, 0, st>>>(q, g->n, p, flags);
                 break;
             case HSZG_HSZP_ND: {
@@ -512,8 +569,11 @@ extern "C" int hszg_decorrelate(const HszgGeom* g, const int32_t* q, int32_t* p,
                     return HSZG_INVALID_ARG;
                 }
                 if (n[2] % 4 == 0 && al16(q) && al16(p)) {
+                    const bool fz = full && n[2] % kChunkCap == 0;
                     dim3 grid4((unsigned)((n[2] / 4 + 127) / 128), (unsigned)n[1], (unsigned)n[0]);
-                    k_decor_lorenzo_x4<<<grid4, 128, 0, st>>>(q, n[0], n[1], n[2], p, flags);
+                    k_decor_lorenzo_x4<<<grid4, 128, 0, st>>>(q, n[0], n[1], n[2], p, flags, fz ? sizes : nullptr,
+                                                              bws);
+                    if (fz) *fused = 1;
                 } else {
                     dim3 grid((unsigned)((n[2] + 255) / 256), (unsigned)n[1], (unsigned)n[0]);
                     k_decor_lorenzo<<<grid, 256, 0, st>>>(q, n[0], n[1], n[2], p, flags);
@@ -525,8 +585,10 @@ extern "C" int hszg_decorrelate(const HszgGeom* g, const int32_t* q, int32_t* p,
                 const int64_t B = sg.B[2];
                 if (sg.n[0] == 1 && sg.n[1] == 1 && B <= 32 && (32 % B) == 0) {
                     const int lgB = __builtin_ctzll((unsigned long long)B);
-                    k_decor_blockmean_1d<<<grid_for(g->n, 256 * 4, 148 * 16), 256, 0, st>>>(q, g->n, lgB, p, metadata,
-                                                                                          flags);
+                    const bool fz = full && B == 32;
+                    k_decor_blockmean_1d<<<grid_for(g->n, 256 * 4, 148 * 16), 256, 0, st>>>(
+                        q, g->n, lgB, p, metadata, flags, fz ? sizes : nullptr, bws);
+                    if (fz) *fused = 1;
                     break;
                 }
                 const int64_t segsz = sg.B[0] * sg.B[1] * sg.B[2];
@@ -535,7 +597,8 @@ extern "C" int hszg_decorrelate(const HszgGeom* g, const int32_t* q, int32_t* p,
                     const int kb = (int)(BT_ELEMS / segsz);
                     const int64_t tpr = (sg.G[2] + kb - 1) / kb;
                     k_decor_blockmean_tiles<<<(unsigned)(sg.G[0] * sg.G[1] * tpr), BT_THREADS, 0, st>>>(
-                        sg, tpr, kb, q, p, metadata, flags);
+                        sg, tpr, kb, q, p, metadata, flags, full ? sizes : nullptr, bws);
+                    if (full) *fused = 1;
                     break;
                 }
                 k_decor_blockmean<<<grid_for(nb * 32, 256, 148 * 64), 256, 0, st>>>(sg, q, p, metadata, flags);
