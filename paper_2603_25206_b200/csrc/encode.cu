@@ -4,7 +4,7 @@
 //   quantize     quant.py:69-82         -> k_quantize(_f32x4): floor(d*recip + 0.5) in fp64 with the
 //                                          multiply and add rounded separately (no FMA, as numpy)
 //   decorrelate  compressors.py:149-198 -> k_decor_prev(_x4) (HSZP), k_decor_lorenzo(_x4) (HSZP_ND),
-//                                          k_decor_blockmean(_tiles, _1d) (HSZX, HSZX_ND; truncating
+//                                          k_decor_blockmean(_tiles, _b32, _1d) (HSZX, HSZX_ND; truncating
 //                                          means 134-138)
 // The chunk encoder proper (bit widths, scan, pack) lives in codec.cu.
 #include <cstdio>
@@ -127,6 +127,56 @@ __device__ __forceinline__ void chunk_size_out(uint32_t m, int lane, int64_t chu
 }
 __device__ __forceinline__ uint32_t mag4(int32_t a, int32_t b, int32_t c, int32_t d) {
     return max(max((uint32_t)abs(a), (uint32_t)abs(b)), max((uint32_t)abs(c), (uint32_t)abs(d)));
+}
+
+// HSZX 1-D with 32-value blocks (the default) and n % 32 == 0: a CTA stages 256 blocks with 16-B
+// coalesced loads into shared memory (36-word stride: conflict-free per-thread 16-B reads), each
+// thread reduces its block (sum, truncated mean, residuals, bit width / chunk size: one block = one
+// chunk), and the residuals leave through shared memory with coalesced 16-B stores.
+__global__ void __launch_bounds__(256) k_decor_blockmean_b32(const int4* __restrict__ q, int64_t nblk,
+                                                             int4* __restrict__ p, int32_t* __restrict__ meta,
+                                                             unsigned int* flags, uint64_t* sizes, uint8_t* bws) {
+    __shared__ __align__(16) int32_t tile[256 * 36];
+    const int64_t b0 = (int64_t)blockIdx.x * 256;
+    const int nb = (int)(nblk - b0 < 256 ? nblk - b0 : 256);
+    for (int i = threadIdx.x; i < nb * 8; i += 256)
+        *reinterpret_cast<int4*>(tile + (i >> 3) * 36 + ((i & 7) << 2)) = __ldg(q + b0 * 8 + i);
+    __syncthreads();
+    unsigned int f = 0;
+    if ((int)threadIdx.x < nb) {
+        int32_t* t = tile + threadIdx.x * 36;
+        int4 v[8];
+        int64_t sum = 0;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            v[k] = *reinterpret_cast<const int4*>(t + 4 * k);
+            sum += (int64_t)v[k].x + v[k].y + v[k].z + v[k].w;
+        }
+        const int64_t mean = sum >= 0 ? (sum >> 5) : -((-sum) >> 5);     // truncation toward zero
+        uint32_t m = 0;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            const int64_t d0 = (int64_t)v[k].x - mean, d1 = (int64_t)v[k].y - mean;
+            const int64_t d2 = (int64_t)v[k].z - mean, d3 = (int64_t)v[k].w - mean;
+            if (d0 > kPmax || d0 < -kPmax || d1 > kPmax || d1 < -kPmax || d2 > kPmax || d2 < -kPmax || d3 > kPmax ||
+                d3 < -kPmax)
+                f |= 1u;
+            const int4 o = make_int4((int32_t)d0, (int32_t)d1, (int32_t)d2, (int32_t)d3);
+            m = max(m, mag4(o.x, o.y, o.z, o.w));
+            *reinterpret_cast<int4*>(t + 4 * k) = o;
+        }
+        const int64_t b = b0 + threadIdx.x;
+        meta[b] = (int32_t)mean;
+        if (sizes) {
+            const int bw = m ? 32 - __clz(m) : 0;
+            bws[b] = (uint8_t)bw;
+            sizes[b] = (uint64_t)chunk_bytes(kChunkCap, bw);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nb * 8; i += 256)
+        p[b0 * 8 + i] = *reinterpret_cast<const int4*>(tile + (i >> 3) * 36 + ((i & 7) << 2));
+    if (f) atomicOr(flags, f);
 }
 
 // HSZX 1-D with segments of B | 32 values (B a power of two): one value per lane, the B lanes of a
@@ -583,6 +633,14 @@ static int decorrelate_impl(const HszgGeom* g, const int32_t* q, int32_t* p, int
             default: {
                 const int64_t nb = sg.G[0] * sg.G[1] * sg.G[2];
                 const int64_t B = sg.B[2];
+                if (sg.n[0] == 1 && sg.n[1] == 1 && B == 32 && g->n % 32 == 0 && al16(q) && al16(p)) {
+                    const int64_t nblk = g->n / 32;
+                    k_decor_blockmean_b32<<<(unsigned)((nblk + 255) / 256), 256, 0, st>>>(
+                        reinterpret_cast<const int4*>(q), nblk, reinterpret_cast<int4*>(p), metadata, flags,
+                        full ? sizes : nullptr, bws);
+                    if (full) *fused = 1;
+                    break;
+                }
                 if (sg.n[0] == 1 && sg.n[1] == 1 && B <= 32 && (32 % B) == 0) {
                     const int lgB = __builtin_ctzll((unsigned long long)B);
                     const bool fz = full && B == 32;
