@@ -22,13 +22,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 REPS = 21
-_last = {}   # the call timed last: record() measures its kernel time too
 
 
 def timed(fn, reps=REPS):
     import torch
 
-    _last["fn"] = fn
     fn()
     torch.cuda.synchronize()
     times = []
@@ -43,34 +41,6 @@ def timed(fn, reps=REPS):
     return times[len(times) // 2]
 
 
-def kernel_time(fn, reps=3):
-    """Device time of one call's kernels (CUPTI via torch.profiler, median of ``reps`` calls):
-    the sum of kernel durations, so the host overhead of the API (Python, ctypes, the scalar
-    read-back) separates from kernel efficiency.  Memcpy/memset time is reported apart."""
-    import torch
-    from torch.profiler import ProfilerActivity, profile
-
-    ks, cs = [], []
-    for _ in range(reps):
-        with profile(activities=[ProfilerActivity.CUDA]) as prof:
-            fn()
-            torch.cuda.synchronize()
-        k = c = 0.0
-        for e in prof.events():
-            if e.device_type.name != "CUDA":
-                continue
-            nm = e.name.lower()
-            if "memcpy" in nm or "memset" in nm:
-                c += e.device_time
-            else:
-                k += e.device_time
-        ks.append(k / 1e6)
-        cs.append(c / 1e6)
-    ks.sort()
-    cs.sort()
-    return ks[len(ks) // 2], cs[len(cs) // 2]
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", type=int, nargs="*", default=[1, 2, 3, 4])
@@ -78,8 +48,6 @@ def main():
     ap.add_argument("--cpu-configs", type=int, nargs="*", default=[],
                     help="CPU baseline leg (opt-in): also time the CPU oracle (the reference algorithm restated, "
                          "1 thread) on these configs, e.g. --cpu-configs 1 2")
-    ap.add_argument("--no-kernel-time", dest="kernel_time", action="store_false",
-                    help="skip the per-row CUPTI pass (kernel_ms / kernel_frac: the summed kernel time of one call)")
     args = ap.parse_args()
 
     import numpy as np
@@ -109,14 +77,6 @@ def main():
              "gbs_fp32": round(gbs, 1), "algo_B_per_value": round(algo_per_value, 3),
              "achieved_gbs": round(ach, 1), "frac": round(ach / peak, 3), "note": note}
         extra = ""
-        if args.kernel_time and _last.get("fn") is not None:
-            tk, tc = kernel_time(_last.pop("fn"))
-            if tk > 0:
-                r["kernel_ms"] = round(tk * 1e3, 4)
-                r["copy_ms"] = round(tc * 1e3, 4)
-                r["kernel_gbs_algo"] = round(algo_per_value * n / tk / 1e9, 1)
-                r["kernel_frac"] = round(algo_per_value * n / tk / 1e9 / peak, 3)
-                extra += f"  kernels {tk * 1e3:8.3f} ms ({r['kernel_frac']:5.3f})"
         if cpu is not None and cfg in args.cpu_configs:
             t0 = time.perf_counter()
             cpu()
