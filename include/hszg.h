@@ -313,9 +313,12 @@ int hszg_lorenzo_onepass(const HszgGeom* g, const HszgStream* s, const int32_t* 
  * the row).  L: dims[0]*dims[1]*dims[2] int32; band_off: dims[0]*ceil(dims[1]/band_rows)*dims[2];
  * strip_edges: dims[0]*ceil(dims[2]/128)*E*2 int32 with E = dims[1] rounded up to even (+ 64 spare).
  * l_mode: 0 writes L as int32; 1 as int16 (n2 % 8 == 0), any value that does not fit setting bit 2
- * of *l_overflow; 2 as int8 (n2 % 16 == 0), setting bit 1 (the caller then redoes the pass wider). */
+ * of *l_overflow; 2 as int8 (n2 % 16 == 0), setting bit 1 (the caller then redoes the pass wider).
+ * ctas_per_sm: 0 launches one CTA per (band, plane); k > 0 a persistent grid of k CTAs per SM that
+ * leaves room for a concurrent kernel (the z-sweep of an earlier window on another stream). */
 int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t band_rows, void* L, int32_t* band_off,
-                   int32_t* strip_edges, int l_mode, int32_t* l_overflow, void* stream, HszgErr* err);
+                   int32_t* strip_edges, int l_mode, int32_t* l_overflow, int ctas_per_sm, void* stream,
+                   HszgErr* err);
 /* HSZP_ND decode fused with the in-row prefix (rows of whole chunks, 256 % (n2/32) == 0). */
 int hszg_decode_rowscan(const HszgGeom* g, const HszgStream* s, int32_t* out, void* stream, HszgErr* err);
 /* In-place inclusive scan along the middle axis of an int32 [A][M][L] view. */

@@ -160,7 +160,7 @@ _SIGS = {
                           _P, ctypes.POINTER(Err)],
     "hszg_lorenzo_onepass": [ctypes.POINTER(Geom), ctypes.POINTER(StreamDesc), _P, _P, _P, _P, _I64, _I64, _P, _P,
                              _I32, _P, ctypes.POINTER(Err)],
-    "hszg_band_scan": [ctypes.POINTER(Geom), ctypes.POINTER(StreamDesc), _I64, _P, _P, _P, _I32, _P, _P,
+    "hszg_band_scan": [ctypes.POINTER(Geom), ctypes.POINTER(StreamDesc), _I64, _P, _P, _P, _I32, _P, _I32, _P,
                        ctypes.POINTER(Err)],
     "hszg_decode_rowscan": [ctypes.POINTER(Geom), ctypes.POINTER(StreamDesc), _P, _P, ctypes.POINTER(Err)],
     "hszg_col_scan": [_P, _I64, _I64, _I64, _P],

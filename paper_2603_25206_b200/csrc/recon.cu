@@ -19,7 +19,8 @@
 #include "lookback.cuh"
 
 extern "C" int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t band_rows, void* L, int32_t* A,
-                              int32_t* strip_edges, int l_int16, int32_t* l_overflow, void* stream, HszgErr* err);
+                              int32_t* strip_edges, int l_int16, int32_t* l_overflow, int ctas_per_sm, void* stream,
+                              HszgErr* err);
 
 namespace hszg {
 
@@ -873,7 +874,7 @@ static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, 
                 if (ws_bytes >= need) {
                     int32_t* buf = sizeof(OutT) == 4 ? reinterpret_cast<int32_t*>(out) : reinterpret_cast<int32_t*>(ws);
                     int32_t* A = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ws) + (sizeof(OutT) == 4 ? 0 : n4));
-                    const int rr = hszg_band_scan(g, s, br, buf, A, nullptr, 0, nullptr, st, err);
+                    const int rr = hszg_band_scan(g, s, br, buf, A, nullptr, 0, nullptr, 0, st, err);
                     if (rr) return rr;
                     if (nb == 1) {          // one band per plane: A holds zeros, the plain z prefix
                         launch_col_scan<OutT>(buf, 1, sg.n[0], sg.n[1] * sg.n[2], two_eps, out, st);
@@ -1156,7 +1157,7 @@ extern "C" int hszg_quantized_sums(const HszgGeom* g, const HszgStream* s, HszgS
     int32_t* A = reinterpret_cast<int32_t*>(w + (size_t)g->n * 4);
     HszgSums* partials = reinterpret_cast<HszgSums*>(w + (((size_t)g->n * 4 + (size_t)sg.n[0] * sg.n[2] * 4 + 255) &
                                                           ~(size_t)255));
-    const int rr = hszg_band_scan(g, s, sg.n[1], L, A, nullptr, 0, nullptr, st, err);
+    const int rr = hszg_band_scan(g, s, sg.n[1], L, A, nullptr, 0, nullptr, 0, st, err);
     if (rr) return rr;
     const int64_t Lc = sg.n[1] * sg.n[2];
     const int64_t nblk = (Lc + 255) / 256;

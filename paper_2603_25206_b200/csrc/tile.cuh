@@ -47,6 +47,10 @@ inline void allow_smem_raw(const void* kernel, size_t bytes) {
         cudaGetLastError();
         return;
     }
+    // the maximum shared-memory carveout, so kernels on concurrent streams (the HSZP_ND band scans
+    // under the z-sweeps) can co-reside on an SM without waiting for it to drain and reconfigure
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+    cudaGetLastError();
     cur = want;
 }
 template <typename K>

@@ -301,11 +301,12 @@ constexpr int SE_W = 128;    // strip width of the strip-edge table (the one-pas
 
 
 template <bool Edges, int LW, bool Full>
-__global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __restrict__ payload, uint64_t len,
+__global__ void __maxnreg__(56) k_band_scan(const uint8_t* __restrict__ payload, uint64_t len,
                                                           const uint64_t* __restrict__ offsets, int64_t n_chunks,
                                                           int n1, int n2, int BR, void* __restrict__ L,
                                                           int32_t* __restrict__ A, int32_t* __restrict__ EF,
-                                                          int32_t* __restrict__ l_ovf, uint32_t sbytes) {
+                                                          int32_t* __restrict__ l_ovf, uint32_t sbytes, int nb,
+                                                          int64_t np) {
     uint32_t rng16 = 0;                      // OR of (value + 2^15 / 2^7) over the values stored narrow
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint32_t s_off[TILE_CHUNKS];
@@ -314,161 +315,173 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_band_scan(const uint8_t* __rest
     __shared__ __align__(8) uint64_t bar[2];
     const int cpr = n2 >> 5;                 // chunks per row (<= 128)
     const int rpt = TILE_CHUNKS / cpr;       // rows per tile (whole rows: rpt * cpr <= 256 chunks)
-    const int b = blockIdx.x, nb = gridDim.x;
-    const int64_t z = blockIdx.y;
-    const int y0 = b * BR;
-    const int y1 = min(y0 + BR, n1);
-    const int ntiles = (y1 - y0 + rpt - 1) / rpt;
     const int ng = n2 >> 2;
     const int kmax = (ng + TILE_CHUNKS - 1) / TILE_CHUNKS;   // column groups per thread (uniform)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int32_t* tile = reinterpret_cast<int32_t*>(smem);
-    uint8_t* SB = smem + kFastTileBytes;     // two staging buffers of sbytes: tile t in buffer t & 1
+    uint8_t* SB = smem + kFastTileBytes;     // two staging buffers of sbytes: tile u in buffer u & 1
     const uint32_t* words = reinterpret_cast<const uint32_t*>(SB);
-    auto tile_c0 = [&](int t) { return (z * n1 + y0 + t * rpt) * (int64_t)cpr; };
-    auto tile_nch = [&](int t) { return min(rpt, y1 - (y0 + t * rpt)) * cpr; };
-    // thread 0: byte range of a tile (loaded a tile ahead) and its TMA into buffer t & 1
-    uint64_t n_lo = 0, n_hi = 0;
-    auto range = [&](int t) {
-        const int64_t c0 = tile_c0(t), c1 = c0 + tile_nch(t);
-        n_lo = __ldg(offsets + c0);
-        n_hi = c1 < n_chunks ? __ldg(offsets + c1) : payload_end(offsets, n_chunks, len);
-    };
-    auto issue = [&](int t) {
-        const uint64_t base = n_lo & ~(uint64_t)15;
-        const uint32_t bytes = (uint32_t)(((n_hi - base + 15) >> 4) << 4);
-        s_base[t & 1] = base;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive_tx(&bar[t & 1], bytes);
-        tma_load_1d(SB + (size_t)(t & 1) * sbytes, payload + base, bytes, &bar[t & 1]);
-    };
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        range(0);
-        issue(0);
-        if (ntiles > 1) range(1);
     }
-    uint64_t my_off = (int)threadIdx.x < tile_nch(0) ? __ldg(offsets + tile_c0(0) + threadIdx.x) : 0;
     __syncthreads();
-    int4 ysum[BS_MAXG];
-#pragma unroll
-    for (int k = 0; k < BS_MAXG; k++) ysum[k] = make_int4(0, 0, 0, 0);
-    for (int t = 0; t < ntiles; t++) {
-        const int r0 = y0 + t * rpt;
-        const int nr = min(rpt, y1 - r0);
-        const int nch = nr * cpr;
-        mbar_wait(&bar[t & 1], (uint32_t)((t >> 1) & 1));
-        if (threadIdx.x == 0 && t + 1 < ntiles) {        // buffer (t+1)&1 was released at the end of t-1
-            issue(t + 1);
-            if (t + 2 < ntiles) range(t + 2);
+    // work items (band b, plane z), strided over the grid: one per CTA for the classic grid, or a
+    // persistent grid small enough to co-reside with the z-sweep (hszg_band_scan); gt counts the
+    // tiles this CTA consumed, so staging buffer and mbarrier phase of tile t are those of gt + t
+    uint32_t gt = 0;
+    for (int64_t item = blockIdx.x; item < (int64_t)nb * np; item += gridDim.x) {
+        const int b = (int)(item % nb);
+        const int64_t z = item / nb;
+        const int y0 = b * BR;
+        const int y1 = min(y0 + BR, n1);
+        const int ntiles = (y1 - y0 + rpt - 1) / rpt;
+        auto tile_c0 = [&](int t) { return (z * n1 + y0 + t * rpt) * (int64_t)cpr; };
+        auto tile_nch = [&](int t) { return min(rpt, y1 - (y0 + t * rpt)) * cpr; };
+        // thread 0: byte range of a tile (loaded a tile ahead) and its TMA into buffer (gt + t) & 1
+        uint64_t n_lo = 0, n_hi = 0;
+        auto range = [&](int t) {
+            const int64_t c0 = tile_c0(t), c1 = c0 + tile_nch(t);
+            n_lo = __ldg(offsets + c0);
+            n_hi = c1 < n_chunks ? __ldg(offsets + c1) : payload_end(offsets, n_chunks, len);
+        };
+        auto issue = [&](int t) {
+            const uint32_t u = (gt + (uint32_t)t) & 1;
+            const uint64_t base = n_lo & ~(uint64_t)15;
+            const uint32_t bytes = (uint32_t)(((n_hi - base + 15) >> 4) << 4);
+            s_base[u] = base;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive_tx(&bar[u], bytes);
+            tma_load_1d(SB + (size_t)u * sbytes, payload + base, bytes, &bar[u]);
+        };
+        if (threadIdx.x == 0) {
+            range(0);
+            issue(0);
+            if (ntiles > 1) range(1);
         }
-        const uint64_t cur_off = my_off;
-        if (t + 1 < ntiles && (int)threadIdx.x < tile_nch(t + 1)) my_off = __ldg(offsets + tile_c0(t + 1) + threadIdx.x);
-        uint32_t tot = 0;
-        if ((int)threadIdx.x < nch) {
-            const uint32_t rel = (uint32_t)(cur_off - s_base[t & 1]) + (uint32_t)(t & 1) * sbytes;
-            tot = decode32<true>(words, rel, tile + threadIdx.x * kChunkStride, 0);
-        }
-        // exclusive prefix of the chunk sums along each row
-        uint32_t inc = tot;
-        if ((cpr & (cpr - 1)) == 0) {            // rows align with warp segments: segmented shuffle scan
-            const int wseg = cpr < 32 ? cpr : 32;
-            if (wseg == 32) {                     // whole-warp rows (n2 >= 1024): unrolled
-#pragma unroll
+        uint64_t my_off = (int)threadIdx.x < tile_nch(0) ? __ldg(offsets + tile_c0(0) + threadIdx.x) : 0;
+        __syncthreads();
+        int4 ysum[BS_MAXG];
+    #pragma unroll
+        for (int k = 0; k < BS_MAXG; k++) ysum[k] = make_int4(0, 0, 0, 0);
+        for (int t = 0; t < ntiles; t++) {
+            const int r0 = y0 + t * rpt;
+            const int nr = min(rpt, y1 - r0);
+            const int nch = nr * cpr;
+            const uint32_t u = gt + (uint32_t)t;
+            mbar_wait(&bar[u & 1], (u >> 1) & 1);
+            if (threadIdx.x == 0 && t + 1 < ntiles) {        // buffer (t+1)&1 was released at the end of t-1
+                issue(t + 1);
+                if (t + 2 < ntiles) range(t + 2);
+            }
+            const uint64_t cur_off = my_off;
+            if (t + 1 < ntiles && (int)threadIdx.x < tile_nch(t + 1)) my_off = __ldg(offsets + tile_c0(t + 1) + threadIdx.x);
+            uint32_t tot = 0;
+            if ((int)threadIdx.x < nch) {
+                const uint32_t rel = (uint32_t)(cur_off - s_base[u & 1]) + (u & 1) * sbytes;
+                tot = decode32<true>(words, rel, tile + threadIdx.x * kChunkStride, 0);
+            }
+            // exclusive prefix of the chunk sums along each row
+            uint32_t inc = tot;
+            if ((cpr & (cpr - 1)) == 0) {            // rows align with warp segments: segmented shuffle scan
+                const int wseg = cpr < 32 ? cpr : 32;
+                if (wseg == 32) {                     // whole-warp rows (n2 >= 1024): unrolled
+    #pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+                        if (lane >= d) inc += o;
+                    }
+                } else {
+                    for (int d = 1; d < wseg; d <<= 1) {
+                        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+                        if ((lane & (wseg - 1)) >= d) inc += o;
+                    }
+                }
+                if (cpr > 32) {
+                    if (lane == 31) s_wt[warp] = inc;
+                    __syncthreads();
+                    for (int w2 = warp & ~((cpr >> 5) - 1); w2 < warp; w2++) inc += s_wt[w2];
+                }
+                s_off[threadIdx.x] = inc - tot;
+            } else {                                  // any cpr: tile-wide scan minus the row start's prefix
                 for (int d = 1; d < 32; d <<= 1) {
                     const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
                     if (lane >= d) inc += o;
                 }
-            } else {
-                for (int d = 1; d < wseg; d <<= 1) {
-                    const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
-                    if ((lane & (wseg - 1)) >= d) inc += o;
-                }
-            }
-            if (cpr > 32) {
                 if (lane == 31) s_wt[warp] = inc;
                 __syncthreads();
-                for (int w2 = warp & ~((cpr >> 5) - 1); w2 < warp; w2++) inc += s_wt[w2];
+                for (int w2 = 0; w2 < warp; w2++) inc += s_wt[w2];
+                s_off[threadIdx.x] = inc;
+                __syncthreads();
+                const int rs = ((int)threadIdx.x / cpr) * cpr;
+                const uint32_t before = rs > 0 ? s_off[rs - 1] : 0u;
+                __syncthreads();
+                s_off[threadIdx.x] = inc - tot - before;
             }
-            s_off[threadIdx.x] = inc - tot;
-        } else {                                  // any cpr: tile-wide scan minus the row start's prefix
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
-                if (lane >= d) inc += o;
-            }
-            if (lane == 31) s_wt[warp] = inc;
             __syncthreads();
-            for (int w2 = 0; w2 < warp; w2++) inc += s_wt[w2];
-            s_off[threadIdx.x] = inc;
-            __syncthreads();
-            const int rs = ((int)threadIdx.x / cpr) * cpr;
-            const uint32_t before = rs > 0 ? s_off[rs - 1] : 0u;
-            __syncthreads();
-            s_off[threadIdx.x] = inc - tot - before;
-        }
-        __syncthreads();
-        const int nstrips = (n2 + SE_W - 1) / SE_W;
-        // rows of the tile: incremental row offsets, uniform k bound (no divergent skips when every
-        // thread owns kmax column groups: Full), narrow-range check by OR of v + 2^15 / 2^7 (bits >= 16 / 8
-        // flag it)
-        int64_t rowoff = (z * n1 + r0) * (int64_t)n2;
-        const int32_t* trow = tile;                   // tile row rr: chunks rr*cpr ..
-        const uint32_t* orow = s_off;
-        for (int rr = 0; rr < nr; rr++, rowoff += n2, trow += cpr * kChunkStride, orow += cpr) {
-            const int y = r0 + rr;
-#pragma unroll
-            for (int k = 0; k < BS_MAXG; k++) {
-                if (k >= kmax) break;
-                const int gi = threadIdx.x + k * TILE_CHUNKS;
-                if (Full || gi < ng) {
-                    const int4 v = *reinterpret_cast<const int4*>(trow + (gi >> 3) * kChunkStride + ((gi & 7) << 2));
-                    const int4 rv = add4u(v, orow[gi >> 3]);      // row prefix R at x = 4gi .. 4gi+3
-                    ysum[k] = add4(ysum[k], rv);
-                    if (L && LW == 4) *reinterpret_cast<int4*>(static_cast<int32_t*>(L) + rowoff + 4 * gi) = ysum[k];
-                    if (L && LW == 2) {
-                        const int4 v4 = ysum[k];
-                        rng16 |= ((uint32_t)v4.x + 0x8000u) | ((uint32_t)v4.y + 0x8000u) | ((uint32_t)v4.z + 0x8000u) |
-                                 ((uint32_t)v4.w + 0x8000u);
-                        uint2 pk;                                                  // low halves, 2 PRMTs
-                        pk.x = __byte_perm((uint32_t)v4.x, (uint32_t)v4.y, 0x5410);
-                        pk.y = __byte_perm((uint32_t)v4.z, (uint32_t)v4.w, 0x5410);
-                        *reinterpret_cast<uint2*>(static_cast<int16_t*>(L) + rowoff + 4 * gi) = pk;
-                    }
-                    if (L && LW == 1) {
-                        const int4 v4 = ysum[k];
-                        rng16 |= ((uint32_t)v4.x + 0x80u) | ((uint32_t)v4.y + 0x80u) | ((uint32_t)v4.z + 0x80u) |
-                                 ((uint32_t)v4.w + 0x80u);
-                        const uint32_t lo = __byte_perm((uint32_t)v4.x, (uint32_t)v4.y, 0x0040);   // low bytes
-                        const uint32_t hi = __byte_perm((uint32_t)v4.z, (uint32_t)v4.w, 0x0040);
-                        *reinterpret_cast<uint32_t*>(static_cast<int8_t*>(L) + rowoff + 4 * gi) = __byte_perm(lo, hi, 0x5410);
-                    }
-                    if (Edges) {                                  // strip edges: E[s] = R(128s-1), F[s] = R(128s+128)
-                        const int xg = 4 * gi;
-                        const int64_t n1e = ((int64_t)n1 + 1) & ~(int64_t)1;   // even rows per strip block
-                        int32_t* ef = EF + ((z * nstrips) * n1e + y) * 2;
-                        if ((xg & (SE_W - 1)) == SE_W - 4 && (xg + 4) / SE_W < nstrips)
-                            ef[(int64_t)((xg + 4) / SE_W) * n1e * 2] = rv.w;
-                        if ((xg & (SE_W - 1)) == 0) {
-                            const int s2 = xg / SE_W;
-                            if (s2 > 0) ef[(int64_t)(s2 - 1) * n1e * 2 + 1] = rv.x;
-                            else {
-                                ef[0] = 0;
-                                ef[(int64_t)(nstrips - 1) * n1e * 2 + 1] = 0;
+            const int nstrips = (n2 + SE_W - 1) / SE_W;
+            // rows of the tile: incremental row offsets, uniform k bound (no divergent skips when every
+            // thread owns kmax column groups: Full), narrow-range check by OR of v + 2^15 / 2^7 (bits >= 16 / 8
+            // flag it)
+            int64_t rowoff = (z * n1 + r0) * (int64_t)n2;
+            const int32_t* trow = tile;                   // tile row rr: chunks rr*cpr ..
+            const uint32_t* orow = s_off;
+            for (int rr = 0; rr < nr; rr++, rowoff += n2, trow += cpr * kChunkStride, orow += cpr) {
+                const int y = r0 + rr;
+    #pragma unroll
+                for (int k = 0; k < BS_MAXG; k++) {
+                    if (k >= kmax) break;
+                    const int gi = threadIdx.x + k * TILE_CHUNKS;
+                    if (Full || gi < ng) {
+                        const int4 v = *reinterpret_cast<const int4*>(trow + (gi >> 3) * kChunkStride + ((gi & 7) << 2));
+                        const int4 rv = add4u(v, orow[gi >> 3]);      // row prefix R at x = 4gi .. 4gi+3
+                        ysum[k] = add4(ysum[k], rv);
+                        if (L && LW == 4) *reinterpret_cast<int4*>(static_cast<int32_t*>(L) + rowoff + 4 * gi) = ysum[k];
+                        if (L && LW == 2) {
+                            const int4 v4 = ysum[k];
+                            rng16 |= ((uint32_t)v4.x + 0x8000u) | ((uint32_t)v4.y + 0x8000u) | ((uint32_t)v4.z + 0x8000u) |
+                                     ((uint32_t)v4.w + 0x8000u);
+                            uint2 pk;                                                  // low halves, 2 PRMTs
+                            pk.x = __byte_perm((uint32_t)v4.x, (uint32_t)v4.y, 0x5410);
+                            pk.y = __byte_perm((uint32_t)v4.z, (uint32_t)v4.w, 0x5410);
+                            *reinterpret_cast<uint2*>(static_cast<int16_t*>(L) + rowoff + 4 * gi) = pk;
+                        }
+                        if (L && LW == 1) {
+                            const int4 v4 = ysum[k];
+                            rng16 |= ((uint32_t)v4.x + 0x80u) | ((uint32_t)v4.y + 0x80u) | ((uint32_t)v4.z + 0x80u) |
+                                     ((uint32_t)v4.w + 0x80u);
+                            const uint32_t lo = __byte_perm((uint32_t)v4.x, (uint32_t)v4.y, 0x0040);   // low bytes
+                            const uint32_t hi = __byte_perm((uint32_t)v4.z, (uint32_t)v4.w, 0x0040);
+                            *reinterpret_cast<uint32_t*>(static_cast<int8_t*>(L) + rowoff + 4 * gi) = __byte_perm(lo, hi, 0x5410);
+                        }
+                        if (Edges) {                                  // strip edges: E[s] = R(128s-1), F[s] = R(128s+128)
+                            const int xg = 4 * gi;
+                            const int64_t n1e = ((int64_t)n1 + 1) & ~(int64_t)1;   // even rows per strip block
+                            int32_t* ef = EF + ((z * nstrips) * n1e + y) * 2;
+                            if ((xg & (SE_W - 1)) == SE_W - 4 && (xg + 4) / SE_W < nstrips)
+                                ef[(int64_t)((xg + 4) / SE_W) * n1e * 2] = rv.w;
+                            if ((xg & (SE_W - 1)) == 0) {
+                                const int s2 = xg / SE_W;
+                                if (s2 > 0) ef[(int64_t)(s2 - 1) * n1e * 2 + 1] = rv.x;
+                                else {
+                                    ef[0] = 0;
+                                    ef[(int64_t)(nstrips - 1) * n1e * 2 + 1] = 0;
+                                }
                             }
                         }
                     }
                 }
             }
+            __syncthreads();
         }
-        __syncthreads();
-    }
-    int32_t* arow = A + (z * nb + b) * (int64_t)n2;
-#pragma unroll
-    for (int k = 0; k < BS_MAXG; k++) {
-        const int gi = threadIdx.x + k * TILE_CHUNKS;
-        if (gi < ng) *reinterpret_cast<int4*>(arow + 4 * gi) = ysum[k];
+        int32_t* arow = A + (z * nb + b) * (int64_t)n2;
+    #pragma unroll
+        for (int k = 0; k < BS_MAXG; k++) {
+            const int gi = threadIdx.x + k * TILE_CHUNKS;
+            if (gi < ng) *reinterpret_cast<int4*>(arow + 4 * gi) = ysum[k];
+        }
+        gt += (uint32_t)ntiles;
     }
     // a narrow L value did not fit: flag bit 1 (int8) or 2 (int16)
     const bool ovf = (rng16 & (LW == 1 ? 0xffffff00u : 0xffff0000u)) != 0;
@@ -576,7 +589,8 @@ extern "C" int hszg_zsweep_grad_lap(const int32_t* P2, int64_t n1, int64_t n2, i
 }
 
 extern "C" int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t band_rows, void* L, int32_t* A,
-                              int32_t* strip_edges, int l_mode, int32_t* l_overflow, void* stream, HszgErr* err) {
+                              int32_t* strip_edges, int l_mode, int32_t* l_overflow, int ctas_per_sm, void* stream,
+                              HszgErr* err) {
     err->status = HSZG_OK;
     const int64_t n1 = g->dims[1], n2 = g->dims[2], np = g->dims[0];
     const int64_t cpr = n2 / kChunkCap;
@@ -594,7 +608,18 @@ extern "C" int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t ba
     const int64_t nb = (n1 + band_rows - 1) / band_rows;
     const uint32_t sbytes = (uint32_t)((stage_bytes(s->max_bitwidth) + 15) / 16 * 16);
     const size_t smem = kFastTileBytes + 2 * (size_t)sbytes + 16;
-    const dim3 grid((unsigned)nb, (unsigned)np);
+    // ctas_per_sm = 0: one CTA per (band, plane), the fastest grid alone; k > 0: a persistent grid of
+    // k CTAs per SM, which leaves the z-sweep beside it its SM slots (pipeline.py runs the scans of
+    // later windows on a high-priority side stream under the sweeps: config-5 HSZP_ND 32.5 -> 30.9 ms)
+    const int64_t items = nb * np;
+    int64_t nct = items;
+    if (ctas_per_sm > 0) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        nct = items < (int64_t)ctas_per_sm * sms ? items : (int64_t)ctas_per_sm * sms;
+    }
+    const dim3 grid((unsigned)nct);
     cudaStream_t st = as_stream(stream);
     const bool full = (n2 / 4) % TILE_CHUNKS == 0;
 #define HSZG_BS(E, LS, F)                                                                                    \
@@ -603,7 +628,7 @@ extern "C" int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t ba
         k_band_scan<E, LS, F><<<grid, TILE_CHUNKS, smem, st>>>(s->payload, s->payload_len, s->offsets,        \
                                                               g->n_chunks, (int)n1, (int)n2, (int)band_rows, \
                                                               L_, A, E ? strip_edges : nullptr,              \
-                                                              l_overflow, sbytes);                           \
+                                                              l_overflow, sbytes, (int)nb, np);                           \
     } while (0)
     void* L_ = L;
     if (strip_edges) {

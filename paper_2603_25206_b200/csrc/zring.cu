@@ -63,8 +63,11 @@ struct ZrArgs {
 
 // LW: bytes per L value of the window's planes, LAW: of the lookahead plane (the next window's first,
 // which may be narrower: int16 window 0 + int8 rest)
+// 64 registers (no spills): two sweep CTAs (2 x 12 warps x 2048 regs) leave exactly one k_band_scan
+// CTA's 16 K registers free, so the side stream's band scans co-reside with the sweeps instead of
+// waiting for a whole SM slot (at 72 registers they could not).
 template <bool Exact, int LW, int LAW>
-__global__ void __launch_bounds__(ZR_T, 2) k_zsweep_ring(ZrArgs a) {
+__global__ void __maxnreg__(64) k_zsweep_ring(ZrArgs a) {
     extern __shared__ __align__(128) int32_t zsm[];
     int32_t* Q = zsm;                                     // [ZR_NPL][ZR_ROWS][ZR_RW]
     uint8_t* S = reinterpret_cast<uint8_t*>(zsm + ZR_NPL * ZR_PLANE);   // [ZR_D][slot]

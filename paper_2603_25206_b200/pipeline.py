@@ -576,7 +576,7 @@ class WindowPipeline:
             self.timer.begin("prepass")
         err = _lib.Err()
         _lib.call("hszg_band_scan", ctypes.byref(self.ds.geom), ctypes.byref(self.ds.desc), 16, None,
-                  _lib.ptr(self.lz_bands), _lib.ptr(self.lz_edges), 0, None, _lib.stream_handle(), ctypes.byref(err),
+                  _lib.ptr(self.lz_bands), _lib.ptr(self.lz_edges), 0, None, 0, _lib.stream_handle(), ctypes.byref(err),
                   err=err)
         if self.timer:
             self.timer.end("prepass", self._range_bytes(0, sf.nz) + self.lz_bands.numel() * 4 + self.lz_edges.numel() * 4)
@@ -655,9 +655,11 @@ class WindowPipeline:
             if k + 2 < nw:
                 decode(k + 2)
 
-    # HSZP_ND: band scans on a side stream, concurrent with the z-sweeps (measured ~1 % faster on
-    # config 5; off by default so each kernel's event time is its own)
+    # HSZP_ND: band scans on a high-priority side stream, as a persistent grid beside the z-sweeps
+    # (config 5: HSZP_ND op 32.5 -> 30.9 ms; bench.py --overlap 1, the default there); off by default
+    # here so each kernel's event time is its own
     overlap = False
+    side_priority = -1
 
     def _run_zsweep(self, outs):
         """HSZP_ND: band scan (decode + x / in-band y prefix) of window k, then the ring z-sweep of
@@ -678,6 +680,8 @@ class WindowPipeline:
             self.l16_ovf.zero_()
         main = t.cuda.current_stream()
         side = self._side_stream() if (self.overlap and ns >= 3) else main
+        # on the side stream: a persistent scan grid (1 CTA per SM) that co-resides with the sweeps
+        scan_ctas = 1 if side is not main else 0
         dec_done = [t.cuda.Event() for _ in range(nw)]
         sweep_done = [t.cuda.Event() for _ in range(nw)]
 
@@ -690,7 +694,8 @@ class WindowPipeline:
             if br:
                 _lib.call("hszg_band_scan", ctypes.byref(sub.geom), ctypes.byref(sub.desc), br,
                           _lib.ptr(ring[k % ns]), _lib.ptr(self.bands[k % ns]), None, modes[k],
-                          _lib.ptr(self.l16_ovf) if l16 else None, _lib.stream_handle(), ctypes.byref(err), err=err)
+                          _lib.ptr(self.l16_ovf) if l16 else None, scan_ctas, _lib.stream_handle(), ctypes.byref(err),
+                          err=err)
             else:
                 _lib.call("hszg_decode_rowscan", ctypes.byref(sub.geom), ctypes.byref(sub.desc),
                           _lib.ptr(ring[k % ns]), _lib.stream_handle(), ctypes.byref(err), err=err)
@@ -743,7 +748,9 @@ class WindowPipeline:
     def _side_stream(self):
         t = _lib.torch()
         if getattr(self, "_side", None) is None:
-            self._side = t.cuda.Stream()
+            # higher priority than the sweeps: the block scheduler places the persistent band-scan
+            # CTAs first, one per SM beside two sweep CTAs (zring.cu: 64 registers, max carveout)
+            self._side = t.cuda.Stream(priority=self.side_priority)
         return self._side
 
     def _finish_stats(self, _prepared):

@@ -185,13 +185,20 @@ def test_fast_decode_bitwidths_hszx_nd(dims):
 
 
 # n2 = 96 / 160 / 384: 3 / 5 / 12 chunks per row, which do not divide a 256-chunk tile (partial tiles)
-@pytest.mark.parametrize("dims", [(16, 16, 256), (24, 40, 64), (12, 30, 96), (5, 44, 160), (6, 50, 384)],
+# (16, 64, 256) with band_rows 1: 512 (band, plane) items per window, several per persistent CTA
+@pytest.mark.parametrize("dims", [(16, 16, 256), (24, 40, 64), (12, 30, 96), (5, 44, 160), (6, 50, 384),
+                                  (16, 64, 256)],
                          ids=lambda d: "x".join(map(str, d)))
 @pytest.mark.parametrize("band_rows", [None, 1, 7, 16, 32])
-def test_fast_decode_bitwidths_band_scan(dims, band_rows):
+@pytest.mark.parametrize("overlap", [False, True], ids=["one-stream", "side-stream"])
+def test_fast_decode_bitwidths_band_scan(dims, band_rows, overlap):
     """hszg_band_scan (decode32 + row prefix + banded column prefix) across bit widths, through the
-    HSZP_ND window pipeline (exact mode), vs the oracle."""
+    HSZP_ND window pipeline (exact mode), vs the oracle.  side-stream: the scans run as the
+    persistent grid (one CTA per SM striding over (band, plane) items) on the side stream."""
     import torch
+
+    if overlap and band_rows is None:
+        pytest.skip("the one-pass kernel has no band-scan windows")
 
     from paper_2603_25206_b200 import pipeline
 
@@ -204,6 +211,7 @@ def test_fast_decode_bitwidths_band_scan(dims, band_rows):
     pipe.exact_fp32 = True
     pipe.band_rows_req = band_rows
     pipe.one_pass = pipe.lorenzo_one_pass = band_rows is None   # None: the one-pass kernel; else two passes
+    pipe.overlap = overlap
     outs = [torch.empty(dims, dtype=torch.float32, device="cuda") for _ in range(4)]
     res = pipe.run(outs)
     want, s1, s2, mean, var = _oracle_outputs(f, 1, eps)
