@@ -247,7 +247,8 @@ def test_fast_mode_falls_back_on_large_q(kind):
 
 
 @pytest.mark.parametrize("case", ["smooth", "noise"])
-def test_narrow_band_prefix_widths(case):
+@pytest.mark.parametrize("overlap", [False, True], ids=["one-stream", "side-stream"])
+def test_narrow_band_prefix_widths(case, overlap):
     """HSZP_ND two-pass with int8 band-local prefixes (int16 in the window holding the field's first
     plane): a field whose z-differences are smooth keeps int8; white noise overflows int8 (flag bit 1),
     the pass is redone with int16 everywhere — bit-exact against the oracle either way."""
@@ -269,6 +270,7 @@ def test_narrow_band_prefix_widths(case):
     pipe.one_pass = pipe.lorenzo_one_pass = False
     pipe.band_rows_req = 16
     pipe.exact_fp32 = True
+    pipe.overlap = overlap              # side-stream: the bench's persistent scan grid, overflow redone too
     outs = [torch.empty(dims, dtype=torch.float32, device="cuda") for _ in range(4)]
     res = pipe.run(outs)
     want, s1, s2, mean, var = _oracle_outputs(f, 1, eps)
