@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--window", type=int, default=64, help="planes per window (HSZX_ND: multiple of 8)")
     ap.add_argument("--exact-fp32", action="store_true",
                     help="fp32 outputs = fl32 of the reference float64 (default: fast fp32, <= 2^-22 relative)")
+    ap.add_argument("--band-rows", type=int, default=None,
+                    help="HSZP_ND band height of the band scan (default: sized by the pipeline; multiples of 16)")
     ap.add_argument("--no-graph", action="store_true", help="launch the window loop eagerly instead of a CUDA graph")
     ap.add_argument("--no-one-pass", action="store_true", help="HSZX_ND: two-pass (decode, then stencil) windows")
     ap.add_argument("--hszp-one-pass", action="store_true", help="HSZP_ND: the one-pass kernel (lorenzo.cu)")
@@ -251,6 +253,8 @@ def run_ours(args):
         p.lorenzo_one_pass = args.hszp_one_pass
         if args.overlap is not None:
             p.overlap = bool(args.overlap)
+        if args.band_rows:
+            p.band_rows_req = args.band_rows
     container_bytes = {k: shards[k].ds.nbytes() for k in KINDS}
     setup_s = time.time() - t_setup
 

@@ -516,7 +516,15 @@ class WindowPipeline:
         unit = rpt if rpt >= 64 and rpt % 16 == 0 else 64
         want = -(-16 * _SMS // max(1, min(self.W, self.sf.nz)))
         br = -(-n1 // want)
-        return -(-br // unit) * unit
+        br = -(-br // unit) * unit
+        if self.overlap:
+            # persistent scans under the sweeps: the grid no longer needs many (band, plane) items,
+            # and taller bands mean fewer band-offset rows (A) to write, prefix and re-read — up to
+            # 256 rows while >= 2 items per SM remain (config 5: 64 -> 256 rows, step 56.1 -> 55.5 ms;
+            # taller bands risk the int8 L range: 512 / 1024 gain < 0.1 ms more, 2048 overflows)
+            cap = n1 * max(1, min(self.W, self.sf.nz)) // (2 * _SMS)
+            br = max(br, min(256, cap) // unit * unit)
+        return br
 
     def _stage_boundary(self):
         """Copy this run's halo / carry planes into the persistent buffers read by the loop."""
