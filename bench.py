@@ -63,6 +63,9 @@ def parse():
     ap.add_argument("--cpu-planes", type=int, default=4, help="planes per CPU-sample sub-field")
     ap.add_argument("--detail", default=None, help="write the per-kernel breakdown JSON here")
     ap.add_argument("--under-ncu", action="store_true", help="skip the CUPTI launch count (ncu owns the profiler)")
+    ap.add_argument("--no-parity", action="store_true", help="skip the post-timed oracle parity probe")
+    ap.add_argument("--no-exact", action="store_true", help="skip the exact-fp32 timing after the headline")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline: seconds of all-core work")
     return ap.parse_args()
 
 
@@ -204,6 +207,8 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     # HSZG_DIST_BACKEND=gloo: plumbing check of the multi-rank path with ranks sharing one GPU
     # (host-staged collectives; the timing of such a run is meaningless and is not a bench value)
     backend = os.environ.get("HSZG_DIST_BACKEND", "nccl")
@@ -263,8 +268,11 @@ def run_ours(args):
     # nodes of the captured graph and hold the last timed step's times
     timers = {k: EventTimer() for k in KINDS}
     spans = {k: EventTimer() for k in KINDS}     # one op = its whole run (launch groups may overlap)
+    comm_timers = {k: EventTimer() for k in KINDS}
     for k in KINDS:
         pipes[k].timer = timers[k]
+        if world > 1:
+            pipes[k].comm_timer = comm_timers[k]
 
     def step():
         for k in KINDS:
@@ -278,7 +286,7 @@ def run_ours(args):
     if args.no_graph:
         for tm in timers.values():
             tm.clear()
-    for tm in spans.values():
+    for tm in list(spans.values()) + list(comm_timers.values()):
         tm.clear()
     comm.barrier()
     torch.cuda.synchronize()
@@ -341,13 +349,32 @@ def run_ours(args):
         roofline["traffic"] = prof["traffic_bytes_per_step"]
         roofline["traffic_source"] = prof["source"]
 
+    comm_ms = {}
+    if world > 1:
+        for k in KINDS:
+            for name, v in comm_timers[k].summary().items():
+                comm_ms[f"{name}:{KIND_NAMES[k]}"] = round(v["ms"] / max(1, v["launch_groups"]), 3)
+        cm = torch.tensor(list(comm_ms.values()) or [0.0], dtype=torch.float64, device="cuda")
+        comm.all_reduce(cm, "max")
+        comm_ms = dict(zip(comm_ms, [round(x, 3) for x in cm.cpu().tolist()]))
+
+    # ---- exact-fp32 emitter: the same step timed (fp32 outputs = fl32 of the reference float64) ----------
+    exact = None
+    if not args.no_exact and not args.exact_fp32:
+        exact = time_exact(args, pipes, outs, comm, step, n_total)
+
+    # ---- parity probe vs the oracle (after the timed region; the checker is not timed) ------------------
+    parity = None
+    if not args.no_parity:
+        parity = parity_probe(args, pipes, outs, comm, eps, (N0, N1, N2), z0, z1)
+
     # ---- e2e: host containers in, every output back to the host ------------------------------------------
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, shards, pipes, outs, comm, n_total)
 
     # ---- CPU baseline (rank 0, N = 1) ---------------------------------------------------------------
-    cpu = cpu_baseline(cpu_blobs) if cpu_blobs else None
+    cpu = cpu_baseline(cpu_blobs, args.cpu_seconds) if cpu_blobs else None
 
     if rank == 0:
         s = results
@@ -368,7 +395,11 @@ def run_ours(args):
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks.summary(),
             "stats_check": {KIND_NAMES[k]: {"mean": s[k]["mean"], "var": s[k]["var"]} for k in KINDS},
+            "exact_fp32": exact, "parity": parity,
         }
+        if world > 1:
+            line["comm_ms_per_step"] = comm_ms
+            line["nccl"] = {"backend": comm.dist.get_backend() if comm.dist else None, "ranks": world}
         print(json.dumps(line), flush=True)
         if args.detail:
             with open(args.detail, "w") as fh:
@@ -448,6 +479,134 @@ def run_e2e(args, shards, pipes, outs, comm, n_total):
                                "path": "same, outputs left on the device (statistics D2H only)"}}
 
 
+def time_exact(args, pipes, outs, comm, step, n_total):
+    """The headline step with the exact fp32 emitter (fp32 outputs = fl32 of the reference float64,
+    bit-exact vs the oracle): W warm-up steps (graph re-capture), then K steps timed like the headline."""
+    import torch
+
+    for p in pipes.values():
+        p.exact_fp32 = True
+    for _ in range(max(2, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    comm.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        step()
+    ev1.record()
+    torch.cuda.synchronize()
+    comm.barrier()
+    tt = torch.tensor([ev0.elapsed_time(ev1) / args.steps], dtype=torch.float64, device="cuda")
+    comm.all_reduce(tt, "max")
+    ms = float(tt.item())
+    for p in pipes.values():
+        p.exact_fp32 = False
+    return {"ms_per_step": round(ms, 3), "value": round(len(KINDS) * 4.0 * n_total / (ms / 1e3) / 1e9, 2),
+            "unit": "GB/s", "steps": args.steps}
+
+
+def _plane_checksums(t, step=32):
+    """Per-plane int64 sums of the fp32 bit patterns of one output (device, chunked)."""
+    import torch
+
+    return torch.cat([t[a:a + step].view(torch.int32).to(torch.int64).sum(dim=(1, 2))
+                      for a in range(0, t.shape[0], step)])
+
+
+def parity_probe(args, pipes, outs, comm, eps, dims, z0, z1):
+    """Post-timed check of the timed configuration against the oracle (oracle/parity.py).
+
+    Per rank, the first and last <= 9 planes of its slab (rank-boundary planes at N > 1; at N = 1 the
+    top planes sit beyond flat index 2^32) in the fast emitter (<= 4*2^-24 relative) and the exact
+    emitter (bit-exact): oracle = fields.py stencils on oracle.quantize of the regenerated field
+    planes.  Rank 0 also decodes its first planes from the GPU containers with the oracle decoder and
+    checks them against quantize.  Every plane of every output: per-plane checksums of HSZP_ND ==
+    HSZX_ND (both derive from the same q), and the exact global sums equal across kinds and emitters.
+    """
+    import numpy as np
+    import torch
+
+    from oracle import hsz_oracle as O
+    from oracle import parity as PAR
+    from paper_2603_25206_b200 import synthetic
+
+    t0 = time.time()
+    N0 = dims[0]
+    wins = [(z0, min(z1, z0 + 9)), (max(z0, z1 - 9), z1)]
+    want = []
+    qs = []
+    for a, b in wins:
+        s, e = max(0, a - 1), min(N0, b + 1)
+        f = synthetic.gen_config5_slab(s, e, dims=dims).cpu().numpy()
+        q = O.quantize(f, eps)
+        za, zb, w = PAR.stencil_planes(q, s, N0, eps)
+        want.append((a, b, [x[a - za:b - za] for x in w]))
+        qs.append((s, q))
+    container_ok = None
+    if z0 == 0:
+        # the oracle's own decode of the GPU containers' first planes (no carry needed at z0 = 0)
+        container_ok = True
+        s, q = qs[0]
+        n1, n2 = dims[1], dims[2]
+        for k, p in pipes.items():
+            ds = p.ds
+            nplanes = 8 if k == 3 else min(10, q.shape[0])
+            if k == 1:
+                c1 = nplanes * (ds.n_chunks // p.sf.nz)
+                m1 = 0
+            else:
+                from paper_2603_25206_b200.device import _full_row_chunks
+
+                c1 = _full_row_chunks(ds)
+                m1 = (n1 // 8) * (n2 // 8)
+            c1 = min(c1, ds.n_chunks)
+            hi = int(ds.offsets[c1].item()) if c1 < ds.n_chunks else ds.payload_len
+            offs = ds.offsets[:c1].cpu().numpy().view(np.uint64)
+            payload = ds.payload[:hi].cpu().numpy().tobytes()
+            meta = None if ds.metadata is None else ds.metadata[:m1].cpu().numpy()
+            st = PAR.sub_stream(k, dims, (8, 8, 8), eps, payload, offs, meta, 0, c1, 0, m1, nplanes=nplanes)
+            container_ok &= bool(np.array_equal(O.stage3(st), q[:nplanes]))
+    rec = {"exact": {}, "fast": {}}
+    sums = {}
+    for mode in ("fast", "exact"):
+        for k, p in pipes.items():
+            p.exact_fp32 = mode == "exact"
+            res = p.run(outs)
+            sums[(mode, k)] = (res["s1"], res["s2"])
+            worst, ok, n = 0.0, True, 0
+            for a, b, w in want:
+                r = PAR.compare([o[a - z0:b - z0].cpu().numpy() for o in outs], w, mode == "exact")
+                worst, ok, n = max(worst, r["max_rel_err"]), ok and r["ok"], n + r["values"]
+            rec[mode][k] = {"ok": ok, "max_rel_err": worst, "values": n,
+                            "checksums": torch.stack([_plane_checksums(o) for o in outs])}
+        p.exact_fp32 = False
+    for p in pipes.values():
+        p.exact_fp32 = False
+    same_ck = all(torch.equal(rec[m][1]["checksums"], rec[m][3]["checksums"]) for m in rec)
+    same_sums = len(set(sums.values())) == 1
+    flags = torch.tensor([float(all(rec["exact"][k]["ok"] for k in pipes)),
+                          float(all(rec["fast"][k]["ok"] for k in pipes)), float(same_ck), float(same_sums),
+                          float(container_ok if container_ok is not None else 1.0)], dtype=torch.float64,
+                         device="cuda")
+    comm.all_reduce(flags, "min")
+    worst = torch.tensor([max(rec["fast"][k]["max_rel_err"] for k in pipes),
+                          max(rec["exact"][k]["max_rel_err"] for k in pipes)], dtype=torch.float64, device="cuda")
+    comm.all_reduce(worst, "max")
+    nval = torch.tensor([float(sum(rec["fast"][k]["values"] for k in pipes))], dtype=torch.float64, device="cuda")
+    comm.all_reduce(nval, "sum")
+    f = [bool(x) for x in flags.cpu().tolist()]
+    w = worst.cpu().tolist()
+    return {"planes_rank0": [list(x) for x in wins], "values_checked_per_mode": int(nval.item()),
+            "exact_bit_exact": f[0], "fast_within_tol": f[1], "fast_tol_rel": PAR.FAST_RTOL,
+            "fast_max_rel_err": w[0], "exact_max_rel_err_vs_f64": w[1],
+            "all_planes_hszp_nd_eq_hszx_nd": f[2], "bit_exact_sums_across_kinds_and_emitters": f[3],
+            "rank0_container_decode_eq_quantize": f[4],
+            "oracle": "oracle/parity.py: fields.py:34-80 stencils on quantize (quant.py:69-82) of the regenerated "
+                      "field planes; oracle decoder on the GPU containers (rank 0)",
+            "seconds": round(time.time() - t0, 1)}
+
+
 CPU_SECONDS = 10.0
 
 
@@ -487,27 +646,79 @@ def build_cpu_sample(field_dev, eps):
     return blobs
 
 
-def cpu_baseline(blobs):
-    """The reference CPU path (oracle restatement) on the bounded sample, one process per host core."""
+def cpu_measure(blobs, seconds: float, steps: int | None = None, warmup: int = 1):
+    """The reference CPU path on the sample: every container decoded by the reference's Cython codec
+    (oracle/_ref, _bitpack.pyx) then recorrelated / summed / differenced with the reference's numpy
+    expressions (oracle restatement), one container per worker process.
+
+    all-core: a step = one pass over the sample on a pool of one process per host core (`steps` timed
+    passes after `warmup`, or as many as fill `seconds`); one-thread: containers run in this process
+    one after another for about a third of `seconds` (the reference is single-threaded by contract,
+    SPEC.md:286)."""
     from oracle import cpu_pipeline as CP
 
     cores = CP.host_cores()
     pool = CP.make_pool(cores)
-    CP.run_sample(blobs[: max(1, min(len(blobs), cores))], pool)     # warm the workers
-    dt, elems, _ = CP.run_sample(blobs, pool)
-    passes = max(1, math.ceil(CPU_SECONDS / max(dt, 1e-3)))          # ~10 s of CPU work
-    if passes > 1:
-        dt, elems, _ = CP.run_sample(blobs * passes, pool)
+    for _ in range(max(1, warmup)):
+        CP.run_sample(blobs, pool)
+    times, elems = [], 0
+    while (steps is not None and len(times) < steps) or (steps is None and (not times or sum(times) < seconds)):
+        dt, elems, _ = CP.run_sample(blobs, pool)
+        times.append(dt)
     if pool is not None:
         pool.shutdown()
-    return {"value": round(4.0 * elems / dt / 1e9, 4), "unit": "GB/s", "cores": cores, "kind": "port",
-            "sample": f"{len(blobs)} containers of {CP.SUB_PLANES}x{CP.SUB_ROWS}x2048 from the config-5 field "
-                      f"x {passes} passes ({elems} values, HSZP_ND + HSZX_ND): oracle decode + recorrelate + exact "
-                      f"sums + gradient + Laplacian, {min(cores, len(blobs))} processes, {dt:.2f} s"}
+    dt = sum(times) / len(times)
+    t0 = time.perf_counter()
+    n1, e1 = 0, 0
+    while n1 < len(blobs) and (n1 < 2 or time.perf_counter() - t0 < seconds / 3):
+        _, e, _ = CP.run_sample([blobs[n1]], None)
+        e1 += e
+        n1 += 1
+    d1 = time.perf_counter() - t0
+    codec = "reference Cython _bitpack (oracle/_ref)" if CP.ref_codec() else "oracle C codec (oracle/_ref not built)"
+    return {"value": round(4.0 * elems / dt / 1e9, 4), "unit": "GB/s", "cores": cores,
+            "kind": "reference" if CP.ref_codec() else "port", "ms_per_pass": round(dt * 1e3, 1),
+            "passes": len(times),
+            "one_thread": {"value": round(4.0 * e1 / d1 / 1e9, 4), "unit": "GB/s", "cores": 1, "containers": n1},
+            "sample": f"{len(blobs)} containers of {CP.SUB_PLANES}x{CP.SUB_ROWS}x2048 sub-fields of planes "
+                      f"[0, {CP.sample_planes(cores)}) of the config-5 field (HSZP_ND + HSZX_ND, global eps), "
+                      f"{elems} values per pass; per container: decode ({codec}) + recorrelate + exact sum/sumsq "
+                      f"+ 3-comp gradient + Laplacian (reference numpy expressions); {min(cores, len(blobs))} "
+                      f"processes", "same_config": True}
+
+
+def cpu_baseline(blobs, seconds=CPU_SECONDS):
+    return cpu_measure(blobs, seconds)
 
 
 # ---------------------------------------------------------------------------
 # reference arm
+
+
+def reference_containers(dims):
+    """The CPU sample's containers exactly as the GPU arm builds them: config-5 field generated on the
+    device, eps = 1e-3 x the GLOBAL value range (min/max over every plane), sub-fields compressed
+    (bit-identical to oracle.compress, tests/test_gpu_api.py)."""
+    import torch
+
+    from oracle import cpu_pipeline as CP
+    from paper_2603_25206_b200 import synthetic
+    from paper_2603_25206_b200.quant import field_minmax
+
+    N0 = dims[0]
+    lo, hi = math.inf, -math.inf
+    for z in range(0, N0, 128):
+        f = synthetic.gen_config5_slab(z, min(N0, z + 128), dims=dims)
+        a, b, _ = field_minmax(f.reshape(-1))
+        lo, hi = min(lo, a), max(hi, b)
+        del f
+    eps = 1e-3 * (hi - lo)
+    S = CP.sample_planes(CP.host_cores())
+    f = synthetic.gen_config5_slab(0, S, dims=dims)
+    blobs = build_cpu_sample(f, eps)
+    del f
+    torch.cuda.empty_cache()
+    return blobs, eps
 
 
 def run_reference(args):
@@ -515,46 +726,47 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from oracle import cpu_pipeline as CP
+    import torch
 
+    torch.cuda.set_device(0)
     N0, N1, N2 = args.dims
-    cores = CP.host_cores()
-    S = CP.sample_planes(cores)
     t0 = time.time()
-    field = CP.config5_sample_field(0, S, (N0, N1, N2))
-    eps = 1e-3 * (float(field.max()) - float(field.min()))   # sample range (the full field is not built here)
-    pool = CP.make_pool(cores)
-    blobs = CP.make_sample(CP.bands(field), KINDS, eps, pool)
-    del field
+    blobs, eps = reference_containers((N0, N1, N2))
     setup_s = time.time() - t0
-    for _ in range(args.warmup):
-        CP.run_sample(blobs, pool)
-    times = []
-    elems = 0
-    for _ in range(args.steps):
-        dt, elems, _ = CP.run_sample(blobs, pool)
-        times.append(dt)
-    if pool is not None:
-        pool.shutdown()
-    dt = sum(times) / len(times)
-    value = 4.0 * elems / dt / 1e9
-    sample = (f"{len(blobs)} containers of {CP.SUB_PLANES}x{CP.SUB_ROWS}x{N2} (planes 0-{S - 1} of the config-5 "
-              f"field, HSZP_ND + HSZX_ND, {elems} values per step), {min(cores, len(blobs))} processes")
-    line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 1), "higher_is_better": True,
+    cpu = cpu_measure(blobs, CPU_SECONDS, steps=args.steps, warmup=args.warmup)
+    value = cpu["value"]
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": cpu["ms_per_pass"], "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int32",
-            "data": "synthetic: config-5 generator restated on the host (seed 5)",
-            "config": {"workload": "config5 bounded sample: per sub-field decode + recorrelate + exact mean/variance "
-                                   "sums + 3-comp gradient + Laplacian (reference path: oracle restatement)",
-                       "dims": [N0, N1, N2], "kinds": [KIND_NAMES[k] for k in KINDS], "setup_s": round(setup_s, 1)},
-            "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": "port",
-                             "sample": sample},
-            "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "data": "synthetic: config-5 field (device generator, seed 5), the GPU arm's CPU-sample containers",
+            "config": {"workload": "config5 bounded sample: per sub-field container decode (reference Cython codec) "
+                                   "+ recorrelate + exact mean/variance sums + 3-comp gradient + Laplacian",
+                       "dims": [N0, N1, N2], "kinds": [KIND_NAMES[k] for k in KINDS], "eps": eps,
+                       "setup_s": round(setup_s, 1)},
+            "cpu_baseline": cpu,
+            "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def spawn(args):
+    """--gpus N without a torchrun environment: re-launch this command as N ranks (one per GPU)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return subprocess.call(cmd, env=env)
 
 
 def main():
     args = parse()
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn(args))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -93,10 +93,44 @@ def bands(field: np.ndarray):
             for z in range(0, Z - SUB_PLANES + 1, SUB_PLANES) for y in range(0, N1 - SUB_ROWS + 1, SUB_ROWS)]
 
 
+_REF = None
+
+
+def ref_codec():
+    """The reference's own Cython chunk codec (_bitpack.pyx, compiled into oracle/_ref by
+    oracle/build_ref.sh), or None when it was not built."""
+    global _REF
+    if _REF is None:
+        import sys
+
+        d = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_ref")
+        try:
+            if d not in sys.path:
+                sys.path.insert(0, d)
+            import _bitpack  # noqa: PLC0415
+
+            _REF = _bitpack
+        except ImportError:
+            _REF = False
+    return _REF or None
+
+
+def ref_stage2(c):
+    """Stage 2 through the reference decoder when present (_bitpack.decode_stream, _bitpack.pyx:90-144;
+    called as codec.decode_stream does, codec.py:114-121), else the oracle's C restatement."""
+    bp = ref_codec()
+    if bp is None:
+        return O.stage2(c)
+    sp = c.spans
+    return bp.decode_stream(c.payload, np.ascontiguousarray(sp[:, 0], dtype=np.int64),
+                            np.ascontiguousarray(sp[:, 1], dtype=np.int64),
+                            np.ascontiguousarray(c.offsets, dtype=np.uint64))
+
+
 def _analyse(blob: bytes):
     """One worker: decompress a container to q and run the step's analytics (reference semantics)."""
     c = O.stream_from_bytes(blob)
-    q = O.stage3(c)                                            # decode + recorrelate (stages.py:76-83)
+    q = O.stage3(c, ref_stage2(c))                             # decode + recorrelate (stages.py:76-83)
     v = q.ravel()
     s1, s2 = O.exact_sum(v), O.exact_dot(v, v)                 # stats.py:168-173 sums
     grads = O.derivative_q(q, c.eps)                           # fields.py:67-72

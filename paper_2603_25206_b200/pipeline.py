@@ -39,6 +39,23 @@ FAST_QLIM = 1 << 27  # fast fp32 emitter validity bound on |q| (stencil.cuh)
 HSZP_ND, HSZX_ND = 1, 3
 SUMS_BYTES = 64
 
+# The configuration bench.py times (and tests/test_gpu_headline.py checks against the oracle): CUDA-graph
+# replay of the window loop, HSZX_ND one-pass kernel, HSZP_ND persistent side-stream band scans (band height
+# sized by _band_rows: 256 rows at 2048^2 planes) under the ring z-sweeps, fast fp32 emitter.
+HEADLINE_SETTINGS = dict(use_graph=True, exact_fp32=False, one_pass=True, lorenzo_one_pass=False, overlap=True,
+                         band_rows_req=None)
+SETTINGS = ("use_graph", "exact_fp32", "one_pass", "lorenzo_one_pass", "overlap", "band_rows_req", "fused_layers")
+
+
+def apply_settings(pipe, **kw):
+    """Set pipeline options by name (unknown names are an error); cached buffers and the captured
+    graph are rebuilt on the next run when a setting they depend on changed (_settings_key)."""
+    for k, v in kw.items():
+        if k not in SETTINGS:
+            raise ValueError(f"unknown pipeline setting {k!r}")
+        setattr(pipe, k, v)
+    return pipe
+
 
 # ---------------------------------------------------------------------------
 # communication plumbing
@@ -302,12 +319,50 @@ class WindowPipeline:
 
     def prepare(self):
         comm = self.comm
-        mine = self.local_boundary(need_total=comm.world > 1)
+        self._agree_paths()
+        if comm.world == 1:
+            # no neighbours: no halo planes, no Lorenzo carry (z0 = 0) — nothing to decode here
+            self.apply_boundary(None, None, None)
+            return
+        ct = self.comm_timer
+        if ct:
+            ct.begin("boundary_decode")
+        mine = self.local_boundary(need_total=True)
+        if ct:
+            ct.end("boundary_decode", 0)
+            ct.begin("carry_allgather")
         gathered = comm.all_gather(mine["T"]) if mine.get("T") is not None else None
         carry = self.carry_from(gathered, comm.rank)
         first = self.finish_first(mine, carry)
+        if ct:
+            ct.end("carry_allgather", 0)
+            ct.begin("halo_exchange")
         lo, hi = comm.exchange(first if first is not None else mine["head"], mine["tail"], mine["tail"])
+        if ct:
+            ct.end("halo_exchange", 0)
         self.apply_boundary(carry, lo, hi)
+
+    comm_timer = None   # optional EventTimer (bench.py): the boundary / collective phases outside the graph
+
+    def _agree_paths(self):
+        """Every rank must take the same kernel path (the paths issue different collectives): the
+        data-dependent eligibility flags (canonical index, bit widths <= 16) are agreed with one MIN
+        all-reduce, once per container."""
+        if getattr(self, "_agreed", None) is not None:
+            return
+        t = _lib.torch()
+        flags = t.tensor([int(bool(self.ds.desc.canonical)), int(self.ds.desc.max_bitwidth <= 16)],
+                         dtype=t.int32, device=_lib.device())
+        self.comm.all_reduce(flags, "min")
+        self._agreed = tuple(bool(v) for v in flags.cpu().tolist())
+
+    def _canonical(self) -> bool:
+        a = getattr(self, "_agreed", None)
+        return a[0] if a is not None else bool(self.ds.desc.canonical)
+
+    def _narrow_bw(self) -> bool:
+        a = getattr(self, "_agreed", None)
+        return a[1] if a is not None else self.ds.desc.max_bitwidth <= 16
 
     # The three phases below are split so a multi-rank run can also be emulated rank by rank
     # in one process (tests/test_gpu_pipeline.py); prepare() runs them around the collectives.
@@ -379,7 +434,7 @@ class WindowPipeline:
         """The fused window kernels need rows of whole chunks (HSZP_ND), 16-B rows and fp32 outputs."""
         t = _lib.torch()
         n2 = self.sf.global_dims[2]
-        if n2 % 4 or outs[0].dtype != t.float32 or not self.ds.desc.canonical:
+        if n2 % 4 or outs[0].dtype != t.float32 or not self._canonical():
             return False
         if self.sf.kind == HSZP_ND:
             return n2 % 32 == 0 and n2 <= 4096
@@ -479,7 +534,8 @@ class WindowPipeline:
     def _persistent(self):
         """Buffers whose addresses stay fixed across runs (graph-capture safe)."""
         t = _lib.torch()
-        if getattr(self, "_pers_W", None) == self.W:
+        key = (self.W, self.band_rows_req, self.one_pass, self.lorenzo_one_pass, self.l16, self.l8)
+        if getattr(self, "_pers_W", None) == self.W and getattr(self, "_pers_key", None) == key:
             return
         n1, n2 = self.sf.global_dims[1], self.sf.global_dims[2]
         dev = _lib.device()
@@ -500,6 +556,7 @@ class WindowPipeline:
             self.bands = [t.empty((self.W, nb, n2), dtype=t.int32, device=dev) for _ in range(nslots)]
             self.l16_ovf = t.zeros(1, dtype=t.int32, device=dev)
         self._pers_W = self.W
+        self._pers_key = key
         self._graph = None
 
     def _band_rows(self) -> int:
@@ -538,7 +595,8 @@ class WindowPipeline:
 
     def _replay(self, outs):
         t = _lib.torch()
-        key = tuple(_lib.ptr(o) for o in outs) + (self.halo_lo is not None, self.halo_hi is not None)
+        key = tuple(_lib.ptr(o) for o in outs) + (self.halo_lo is not None, self.halo_hi is not None,
+                                                  self.exact_fp32, self.overlap, self.fused_layers, self.side_priority)
         if self._graph is None or self._graph_key != key:
             self._fused_loop(outs)                        # warm-up: workspaces, smem attributes
             t.cuda.synchronize()
@@ -569,7 +627,7 @@ class WindowPipeline:
     def _one_pass_ok(self) -> bool:
         sf, ds = self.sf, self.ds
         n = sf.global_dims
-        if not self.one_pass or ds.desc.max_bitwidth > 16:
+        if not self.one_pass or not self._narrow_bw():
             return False
         if sf.kind == HSZP_ND:
             return self.lorenzo_one_pass and n[2] % 64 == 0 and n[2] <= 4096
@@ -765,7 +823,12 @@ class WindowPipeline:
         self.local_sums = self.acc
         if _prepared:
             return acc_to_ints(self.acc)
+        ct = self.comm_timer if self.comm.world > 1 else None
+        if ct:
+            ct.begin("stats_allgather")
         parts = self.comm.all_gather(self.acc)
+        if ct:
+            ct.end("stats_allgather", 0)
         tot = dict(s1=0, s2=0, count=0, vmin=2**31, vmax=-(2**31))
         for p in parts:
             d = acc_to_ints(p)
