@@ -66,6 +66,8 @@ def parse():
     ap.add_argument("--no-parity", action="store_true", help="skip the post-timed oracle parity probe")
     ap.add_argument("--no-exact", action="store_true", help="skip the exact-fp32 timing after the headline")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline: seconds of all-core work")
+    ap.add_argument("--rows", type=int, nargs="*", default=[4],
+                    help="BASELINE configs whose per-row SURVEY §8(a) table goes into the line's `rows` (N = 1)")
     return ap.parse_args()
 
 
@@ -376,6 +378,16 @@ def run_ours(args):
     # ---- CPU baseline (rank 0, N = 1) ---------------------------------------------------------------
     cpu = cpu_baseline(cpu_blobs, args.cpu_seconds) if cpu_blobs else None
 
+    # ---- per-row table (SURVEY §8(a) rows on configs 1-4; N = 1, after the headline's buffers are freed) --
+    rows = None
+    if world == 1 and args.rows:
+        import bench_rows
+
+        del outs, pipes, shards
+        torch.cuda.empty_cache()
+        rows = bench_rows.measure(args.rows, cpu=not args.no_cpu, peak=peak,
+                                  log=lambda m: print(m, file=sys.stderr, flush=True))
+
     if rank == 0:
         s = results
         line = {
@@ -395,7 +407,7 @@ def run_ours(args):
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks.summary(),
             "stats_check": {KIND_NAMES[k]: {"mean": s[k]["mean"], "var": s[k]["var"]} for k in KINDS},
-            "exact_fp32": exact, "parity": parity,
+            "exact_fp32": exact, "parity": parity, "rows": rows,
         }
         if world > 1:
             line["comm_ms_per_step"] = comm_ms

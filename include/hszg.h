@@ -172,7 +172,9 @@ int hszg_metadata_grid(const HszgGeom* g, const int32_t* metadata, int64_t* out,
  *       2 = HSZP_ND weighted   sum(prod(n_k-i_k) p)      (stats.py:95-112)
  *       3 = HSZX* stage-2 sums of q = p + M_b in stream order (no scatter)
  *       4 = stage-1 sum(M_b * S_b)                          (stats.py:69-77)
- * mode 1-4 read the compressed stream; mode 0 reads an int32 array (src). */
+ * mode 1-4 read the compressed stream; mode 0 reads an int32 array (src).
+ * mode | HSZG_REDUCE_NO_EXTREMA: vmin / vmax are not wanted (statistics only; leaner decode). */
+#define HSZG_REDUCE_NO_EXTREMA 0x100
 int hszg_reduce_stream(const HszgGeom* g, const HszgStream* s, int mode, HszgSums* out_dev, void* ws,
                        size_t ws_bytes, void* stream, HszgErr* err);
 /* modes 1-3 over an already-decoded stream-order residual array p (DecorrelatedStream.values) */
@@ -195,6 +197,13 @@ int hszg_region_reduce(const int32_t* q, int32_t ndims, const int64_t* dims, con
 
 /* Per-region finalisation: mean = S1/size*2eps, var = (size*S2 - S1^2)/(size(size-1))*(2eps)^2 (NaN
  * below 2 points), fmin/fmax = q{min,max}*2eps, *count_dev = #regions with fmin < tau <= fmax. */
+/* N2-N4 fused from an HSZX* stream (q = p + M_b, stage 2 / 3 alike; no reconstruction): per-region
+ * S1, S2 (lo / hi), qmin, qmax, size as hszg_region_reduce.  Regions (original dims) must be multiples
+ * of the block extents (or reach the grid end) and every chunk full; else HSZG_UNSUPPORTED_STAGE and
+ * the caller reconstructs q.  ws >= 64 bytes per region.  (new, SURVEY section 8, N2-N4 / K-REG) */
+int hszg_region_stream(const HszgGeom* g, const HszgStream* s, const int64_t* region, int64_t* s1, uint64_t* s2_lo,
+                       int64_t* s2_hi, int32_t* qmin, int32_t* qmax, int64_t* size, void* ws, size_t ws_bytes,
+                       void* stream, HszgErr* err);
 int hszg_region_finalize(const int64_t* s1, const uint64_t* s2_lo, const int64_t* s2_hi, const int32_t* qmin,
                          const int32_t* qmax, const int64_t* size, int64_t n_regions, double two_eps, double tau,
                          double* mean, double* var, double* fmin, double* fmax, unsigned long long* count_dev,

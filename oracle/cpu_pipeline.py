@@ -119,9 +119,9 @@ def ref_stage2(c):
     """Stage 2 through the reference decoder when present (_bitpack.decode_stream, _bitpack.pyx:90-144;
     called as codec.decode_stream does, codec.py:114-121), else the oracle's C restatement."""
     bp = ref_codec()
-    if bp is None:
-        return O.stage2(c)
     sp = c.spans
+    if bp is None:
+        return O.decode_stream(c.payload, sp, c.offsets)
     return bp.decode_stream(c.payload, np.ascontiguousarray(sp[:, 0], dtype=np.int64),
                             np.ascontiguousarray(sp[:, 1], dtype=np.int64),
                             np.ascontiguousarray(c.offsets, dtype=np.uint64))

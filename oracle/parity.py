@@ -72,3 +72,25 @@ def sub_stream(kind, dims, block_dims, eps, payload: bytes, offsets, metadata, c
     bd = tuple(min(b, n) for b, n in zip(block_dims, sub_dims))
     meta = None if metadata is None else np.asarray(metadata)[m0:m1].copy()
     return O.Stream(kind, sub_dims, bd, eps, meta, sub_offs, bytes(payload[b0:b1]))
+
+
+def leading_planes(c, nz: int):
+    """The oracle Stream of the first nz planes (axis 0) of a 3-D container: a prefix of the chunk list
+    (every kind's stream order covers whole leading planes: flat 1-D blocks, HSZP_ND planes, HSZX_ND
+    block layers when nz is a multiple of the block depth) and of the block means.  Stage 2/3 of it
+    equal the container's first nz planes (no carry: the prefixes start at plane 0)."""
+    dims = tuple(c.dims)
+    sub = (nz,) + dims[1:]
+    n = int(np.prod(sub))
+    spans = c.spans
+    c1 = int(np.searchsorted(spans[:, 1], n)) + 1
+    assert int(spans[c1 - 1, 1]) == n, "plane boundary is not a chunk boundary"
+    offs = np.asarray(c.offsets, dtype=np.uint64)
+    b1 = int(offs[c1]) if c1 < len(offs) else len(c.payload)
+    bd = tuple(c.block_dims) if O.is_nd(c.kind) else (min(int(c.block_dims[0]), n),) + (1,) * (len(dims) - 1)
+    bd = tuple(min(b, s) for b, s in zip(bd, sub)) if O.is_nd(c.kind) else bd
+    meta = None
+    if c.metadata is not None:
+        gd, gb = O.effective_geometry(c.kind, sub, bd)
+        meta = np.asarray(c.metadata)[:int(np.prod(O.block_grid(gd, gb)))].copy()
+    return O.Stream(c.kind, sub, bd, c.eps, meta, offs[:c1].copy(), bytes(c.payload[:b1]))

@@ -139,6 +139,8 @@ _SIGS = {
     "hszg_reduce_dot": [_P, _P, _I64, _P, _P, _SZ, _P],
     "hszg_region_reduce": [_P, ctypes.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "hszg_region_finalize": [_P, _P, _P, _P, _P, _P, _I64, _D, _D, _P, _P, _P, _P, _P, _P],
+    "hszg_region_stream": [ctypes.POINTER(Geom), ctypes.POINTER(StreamDesc), _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P,
+                           ctypes.POINTER(Err)],
     "hszg_reduce_flt": [_P, _I64, _P, _P, _P, _SZ, _P],
     "hszg_stencil": [_I32, ctypes.c_int32, _P, ctypes.c_int32, _P, _P, _I32, ctypes.c_int32, _P, _P],
     "hszg_stencil_window": [_I32, _P, ctypes.c_int32, _P, _P, _I32, ctypes.c_int32, _P, _I64, _I64, _I64, _I64, _P],

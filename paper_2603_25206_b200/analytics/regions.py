@@ -20,6 +20,7 @@ finalises the floats and the count.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -75,6 +76,51 @@ def region_reduce_device(q_dev, eps: float, region, tau: float = float("nan")):
     return dict(grid=grid, region=tuple(min(r, n) for r, n in zip(reg, q_dev.shape)), buf=buf, **v)
 
 
+def _region_device(c: CompressedStream, stage: Stage, region, tau: float):
+    """Per-region outputs on the device: fused from the bytes for the block-mean kinds when the regions
+    align with the blocks (hszg_region_stream, K-REG), else over the reconstructed q."""
+    stage = Stage(stage)
+    if stage not in (Stage.DECORRELATED, Stage.QUANTIZED):
+        raise ValueError("regional statistics run on stage 2 or 3 integers")
+    _check_stage(c, stage)
+    count_stage_work(c, stage)
+    if c.kind.is_block_mean:
+        d = c.device().validate()
+        nd = len(c.shape.dims)
+        reg = _region_tuple(region, nd)
+        dims = tuple(int(n) for n in c.shape.dims)
+        regc = tuple(min(r, n) for r, n in zip(reg, dims))
+        grid = tuple(-(-n // r) for n, r in zip(dims, regc))
+        nr = int(np.prod(grid))
+        buf = devmod.region_buffer(nr)
+        v = devmod.region_views(buf, nr)
+        ws = _lib.workspace(64 * nr)
+        err = _lib.Err()
+        reg_arr = (ctypes.c_int64 * 3)(*(list(reg) + [1] * (3 - nd)))
+        st = _lib.lib().hszg_region_stream(ctypes.byref(d.geom), ctypes.byref(d.desc),
+                                            ctypes.cast(reg_arr, ctypes.c_void_p), _lib.ptr(v["s1"]),
+                                            _lib.ptr(v["s2lo"]), _lib.ptr(v["s2hi"]), _lib.ptr(v["qmin"]),
+                                            _lib.ptr(v["qmax"]), _lib.ptr(v["size"]), _lib.ptr(ws), ws.numel(),
+                                            _lib.stream_handle(), ctypes.byref(err))
+        if st == _lib.OK:
+            return _finalize(dict(grid=grid, region=regc, buf=buf, **v), c.eps, tau)
+        if st != _lib.UNSUPPORTED_STAGE:
+            _lib.raise_for(st, err, "hszg_region_stream")
+    t = _lib.torch()
+    q = c.device().reconstruct(t.int32)
+    return region_reduce_device(q, c.eps, region, tau)
+
+
+def _finalize(r, eps: float, tau: float):
+    v = r
+    nr = v["s1"].numel()
+    _lib.call("hszg_region_finalize", _lib.ptr(v["s1"]), _lib.ptr(v["s2lo"]), _lib.ptr(v["s2hi"]),
+              _lib.ptr(v["qmin"]), _lib.ptr(v["qmax"]), _lib.ptr(v["size"]), nr, 2.0 * eps, float(tau),
+              _lib.ptr(v["mean"]), _lib.ptr(v["var"]), _lib.ptr(v["vmin"]), _lib.ptr(v["vmax"]), _lib.ptr(v["count"]),
+              _lib.stream_handle())
+    return r
+
+
 def _quantized(c: CompressedStream, stage: Stage):
     stage = Stage(stage)
     if stage not in (Stage.DECORRELATED, Stage.QUANTIZED):
@@ -88,8 +134,7 @@ def _quantized(c: CompressedStream, stage: Stage):
 def region_stats(c: CompressedStream, region, stage: Stage = Stage.QUANTIZED,
                  tau: float | None = None) -> RegionStats:
     """Per-region mean/variance/min/max (N2, N3) and optionally the tau crossing count (N4)."""
-    q = _quantized(c, stage)
-    r = region_reduce_device(q, c.eps, region, float("nan") if tau is None else tau)
+    r = _region_device(c, stage, region, float("nan") if tau is None else tau)
     g = r["grid"]
     nr = int(np.prod(g))
     host = r["buf"].cpu().numpy()                 # every output in one device -> host copy
@@ -113,8 +158,7 @@ def region_minmax(c: CompressedStream, region, stage: Stage = Stage.QUANTIZED):
 
 def threshold_count(c: CompressedStream, region, tau: float, stage: Stage = Stage.QUANTIZED) -> int:
     """N4: number of regions with min_r < tau <= max_r (only the count leaves the device)."""
-    q = _quantized(c, stage)
-    return int(region_reduce_device(q, c.eps, region, float(tau))["count"].item())
+    return int(_region_device(c, stage, region, float(tau))["count"].item())
 
 
 def gradient_magnitude(c: CompressedStream, stage: Stage = Stage.QUANTIZED, out: str = "numpy", out_dtype=None):

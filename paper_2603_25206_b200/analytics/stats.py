@@ -28,6 +28,7 @@ MODE_HSZP_WEIGHTED = 1
 MODE_LORENZO_WEIGHTED = 2
 MODE_BLOCK_MEAN_Q = 3
 MODE_META = 4
+NO_EXTREMA = 0x100          # HSZG_REDUCE_NO_EXTREMA: min / max not computed (leaner decode)
 
 
 @dataclass(frozen=True)
@@ -254,7 +255,7 @@ def stream_sums(c: CompressedStream, stage: Stage):
     if stage == Stage.META:
         return _lib.read_sums(d.reduce(MODE_META))
     if c.kind.is_block_mean:
-        return _lib.read_sums(d.reduce(MODE_BLOCK_MEAN_Q))
+        return _lib.read_sums(d.reduce(MODE_BLOCK_MEAN_Q | NO_EXTREMA))
     fused = d.quantized_sums()          # q reduced where it is formed, never written (HSZP, 3-D HSZP_ND)
     if fused is not None:
         return _lib.read_sums(fused)
@@ -286,10 +287,9 @@ def compute_stat(c: CompressedStream, op: str, stage: Stage) -> StatResult:
         var = m2 / (n - 1)
         return StatResult(math.sqrt(var) if op == "std" else var, stage, op)
     if op == "mean":
-        if stage == Stage.DECORRELATED:
-            total = _lib.read_sums(d.reduce(_weighted_mode(c.kind))).s1   # no reconstruction
-        else:
-            total = stream_sums(c, stage).s1
+        # sum q is the same exact integer at stages 2 and 3: the weighted residual sum (prefix kinds,
+        # stats.py:88/95-112) or the block-mean sum (HSZX*) straight from the bytes — no reconstruction
+        total = _lib.read_sums(d.reduce(_weighted_mode(c.kind) | NO_EXTREMA)).s1
         return StatResult(total / n * (2.0 * eps), stage, op)
     s = stream_sums(c, stage)
     if stage == Stage.DECORRELATED and c.kind.is_block_mean:

@@ -1,0 +1,151 @@
+// moments.cuh — lean per-chunk moments of a validated FULL chunk (32 values) straight from its
+// staged bytes: the decode core of the fused statistics / regional reductions (K-STAT, K-REG).
+//
+// The layout is the reference chunk (_fallback.py:1-8, _bitpack.pyx:124-143): 1 bit-width byte,
+// 4 sign bytes (value j <-> bit j), then 32 magnitudes of bw bits LSB-first.  Statistics never
+// need the signed values one by one:
+//     sum p   = sum |p| - 2 sum_{sign set} |p|      (a predicated add per value)
+//     sum p^2 = sum |p|^2                            (sign-free: one IMAD per value)
+//     sum j p = sum j|p| - 2 sum_{sign set} j|p|     (weighted means, stats.py:88/95-112)
+// so a value costs a field extract, one add into |p|, a predicated add, one IMAD (+ two for the
+// index-weighted sum, + a negate and a 3-input min/max when extrema are wanted).
+//
+// Field extraction reads G values per 32-bit funnel window (G = 4 for bw <= 8, G = 2 for bw <= 16):
+// the bit cursor advances once per window.  The window width is chosen per WARP (all lanes <= 8:
+// G = 4, all <= 16: G = 2), so lanes never diverge on it; chunks wider than 16 bits (rare: the
+// reference encoder produces them only for |p| >= 2^16) take an exact 128-bit path.
+#pragma once
+#include "common.cuh"
+
+namespace hszg {
+
+struct ChunkMoments {
+    int64_t sp;      // sum p
+    u128 sq;         // sum p^2
+    int64_t tp;      // sum j p (TSUM)
+    int32_t mn, mx;  // min / max p (MINMAX)
+};
+
+// acc += v when (word & bit) != 0 (a predicated add: LOP3 -> P, @P IADD; bit is a constant after
+// unrolling)
+__device__ __forceinline__ void add_if_bit(uint32_t& acc, uint32_t word, uint32_t bit, uint32_t v) {
+    asm("{\n .reg .pred p;\n .reg .b32 t;\n and.b32 t, %1, %2;\n setp.ne.b32 p, t, 0;\n @p add.u32 %0, %0, %3;\n}"
+        : "+r"(acc)
+        : "r"(word), "r"(bit), "r"(v));
+}
+
+template <int G, bool TSUM, bool MINMAX>
+__device__ __forceinline__ void chunk_moments_g(const uint32_t* w, uint32_t rel, uint32_t bw, uint32_t smask,
+                                                ChunkMoments& r) {
+    const uint32_t bitpos = (rel + 5) * 8;
+    uint32_t wi = bitpos >> 5, sh = bitpos & 31;
+    uint32_t cur = w[wi], nxt = w[wi + 1];
+    const uint32_t mask = (1u << bw) - 1u;          // bw <= 16 here
+    const uint32_t adv = (uint32_t)G * bw;
+    uint32_t sa = 0, sn = 0, ta = 0, tn = 0;
+    uint32_t sq32 = 0;                               // G = 4: 32 squares of < 2^8 fit 21 bits
+    uint64_t sq64 = 0;
+    int32_t mn = INT32_MAX, mx = INT32_MIN;
+#pragma unroll
+    for (int k = 0; k < 32 / G; k++) {
+        const uint32_t grp = __funnelshift_r(cur, nxt, sh);
+#pragma unroll
+        for (int i = 0; i < G; i++) {
+            const int j = k * G + i;
+            const uint32_t m = i == 0 ? (grp & mask) : ((grp >> (i * bw)) & mask);
+            sa += m;
+            add_if_bit(sn, smask, 1u << j, m);
+            if (G == 4) sq32 += m * m;
+            else sq64 += (uint64_t)m * m;
+            if (TSUM) {
+                ta += (uint32_t)j * m;
+                add_if_bit(tn, smask, 1u << j, (uint32_t)j * m);
+            }
+            if (MINMAX) {
+                const bool neg = (smask >> j) & 1u;
+                const int32_t v = neg ? -(int32_t)m : (int32_t)m;
+                mn = min(mn, v);
+                mx = max(mx, v);
+            }
+        }
+        if (k + 1 < 32 / G) {
+            sh += adv;
+            if (sh >= 32) {
+                sh -= 32;
+                cur = nxt;
+                wi++;
+                nxt = w[wi + 1];
+            }
+        }
+    }
+    r.sp = (int64_t)sa - 2 * (int64_t)sn;
+    r.sq = G == 4 ? (u128)sq32 : (u128)sq64;
+    r.tp = (int64_t)ta - 2 * (int64_t)tn;
+    r.mn = mn;
+    r.mx = mx;
+}
+
+// bw 17..32: exact, value by value (int64 / u128)
+template <bool TSUM, bool MINMAX>
+__device__ __forceinline__ void chunk_moments_wide(const uint32_t* w, uint32_t rel, uint32_t bw, uint32_t smask,
+                                                   ChunkMoments& r) {
+    const uint32_t bitpos = (rel + 5) * 8;
+    uint32_t wi = bitpos >> 5, sh = bitpos & 31;
+    uint32_t cur = w[wi], nxt = w[wi + 1];
+    const uint32_t mask = bw >= 32 ? 0xffffffffu : (1u << bw) - 1u;
+    int64_t sp = 0, tp = 0;
+    u128 sq = 0;
+    int32_t mn = INT32_MAX, mx = INT32_MIN;
+    for (int j = 0; j < 32; j++) {
+        const uint32_t m = __funnelshift_r(cur, nxt, sh) & mask;    // <= 2^31 - 1 (validated)
+        sh += bw;
+        if (sh >= 32) {
+            sh -= 32;
+            cur = nxt;
+            wi++;
+            nxt = w[wi + 1];
+        }
+        const int64_t v = ((smask >> j) & 1u) ? -(int64_t)m : (int64_t)m;
+        sp += v;
+        sq += (u128)((uint64_t)m * m);
+        if (TSUM) tp += (int64_t)j * v;
+        if (MINMAX) {
+            mn = min(mn, (int32_t)v);
+            mx = max(mx, (int32_t)v);
+        }
+    }
+    r.sp = sp;
+    r.sq = sq;
+    r.tp = tp;
+    r.mn = mn;
+    r.mx = mx;
+}
+
+// Moments of the full chunk whose bytes start at byte `rel` of the staged words.  All 32 lanes of
+// the warp must call it (valid = false for lanes without a chunk); the window width is warp-uniform.
+template <bool TSUM, bool MINMAX>
+__device__ __forceinline__ ChunkMoments chunk_moments(const uint32_t* w, uint32_t rel, bool valid) {
+    ChunkMoments r;
+    uint32_t bw = valid ? smem_byte(w, rel) : 0u;
+    const uint32_t smask = bw ? smem_u32(w, rel + 1) : 0u;
+    const unsigned act = __activemask();
+    if (__all_sync(act, bw <= 8)) {
+        chunk_moments_g<4, TSUM, MINMAX>(w, rel, bw, smask, r);
+    } else if (__all_sync(act, bw <= 16)) {
+        chunk_moments_g<2, TSUM, MINMAX>(w, rel, bw, smask, r);
+    } else if (bw <= 16) {
+        chunk_moments_g<2, TSUM, MINMAX>(w, rel, bw, smask, r);
+    } else {
+        chunk_moments_wide<TSUM, MINMAX>(w, rel, bw, smask, r);
+    }
+    if (!valid) {
+        r.sp = 0;
+        r.sq = 0;
+        r.tp = 0;
+        r.mn = INT32_MAX;
+        r.mx = INT32_MIN;
+    }
+    return r;
+}
+
+}  // namespace hszg

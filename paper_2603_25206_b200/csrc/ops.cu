@@ -13,6 +13,9 @@
 #include <cstdlib>
 #include "tile.cuh"
 #include "async.cuh"
+#include "moments.cuh"
+#include "wtiles.cuh"
+#include "stencil.cuh"
 
 namespace hszg {
 
@@ -88,28 +91,41 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_reduce_tiles(SegGeo sg, const u
 
 // Grid-strided 256-chunk tiles with double-buffered staging: the byte range of the CTA's next tile is
 // copied with 16-B cp.async into the other buffer while the current one decodes (two barriers per
-// tile).  body(c, words, rel) handles chunk c (words: the staged bytes, rel: its byte offset there).
-template <typename Body>
+// tile).  Each thread's index entries (chunk start / end bytes) and one auxiliary word per chunk
+// (aux(c), e.g. its block mean) are loaded two tiles ahead, so no global-load latency sits between a
+// tile's barriers.  body(c, words, rel, valid, aux) handles chunk c (words: the staged bytes, rel: its
+// byte offset there); every thread of the CTA calls it each tile (valid = false past the last chunk),
+// so warps stay converged for warp-uniform decode decisions.
+struct NoAux {
+    __device__ __forceinline__ int32_t operator()(int64_t) const { return 0; }
+};
+
+template <typename Body, typename Aux = NoAux>
 __device__ __forceinline__ void staged_tiles(const uint8_t* __restrict__ payload, uint64_t len,
                                              const uint64_t* __restrict__ offsets, int64_t n_chunks, uint8_t* smem,
-                                             uint32_t buf_bytes, Body body) {
+                                             uint32_t buf_bytes, Body body, Aux aux = Aux()) {
     // byte ranges of the CTA's i-th tile in slot i % 3: a thread one iteration ahead writes a slot no
     // thread still reads (barrier A of the next iteration separates the third)
     __shared__ uint64_t s_lo[3], s_hi[3];
     const int64_t tiles = (n_chunks + TILE_CHUNKS - 1) / TILE_CHUNKS;
-    uint64_t off = 0, end = 0;
-    auto fetch = [&](int64_t t) {                  // this thread's chunk of tile t: start / end bytes
+    const int64_t G = gridDim.x;
+    struct Ent {
+        uint64_t off, end;
+        int32_t aux;
+    };
+    auto fetch = [&](int64_t t, Ent& e) {          // this thread's chunk of tile t: start / end bytes, aux
         const int64_t c = t * TILE_CHUNKS + threadIdx.x;
         if (t < tiles && c < n_chunks) {
-            off = __ldg(offsets + c);
-            end = c + 1 < n_chunks ? __ldg(offsets + c + 1) : payload_end(offsets, n_chunks, len);
+            e.off = __ldg(offsets + c);
+            e.end = c + 1 < n_chunks ? __ldg(offsets + c + 1) : payload_end(offsets, n_chunks, len);
+            e.aux = aux(c);
         }
     };
-    auto publish = [&](int64_t t, int r) {         // the tile's byte range, from its first / last chunk
+    auto publish = [&](int64_t t, int r, const Ent& e) {   // the tile's byte range, from its first / last chunk
         const int64_t c0 = t * TILE_CHUNKS;
         const int nch = (int)(n_chunks - c0 < TILE_CHUNKS ? n_chunks - c0 : TILE_CHUNKS);
-        if (threadIdx.x == 0) s_lo[r] = off;
-        if ((int)threadIdx.x == nch - 1) s_hi[r] = end;
+        if (threadIdx.x == 0) s_lo[r] = e.off;
+        if ((int)threadIdx.x == nch - 1) s_hi[r] = e.end;
     };
     auto issue = [&](int b, int r) {
         uint4* sb = reinterpret_cast<uint4*>(smem + (size_t)b * buf_bytes);
@@ -122,79 +138,102 @@ __device__ __forceinline__ void staged_tiles(const uint8_t* __restrict__ payload
     };
     int64_t t = blockIdx.x;
     if (t >= tiles) return;
-    fetch(t);
-    publish(t, 0);
+    Ent A = {0, 0, 0}, B = {0, 0, 0};
+    fetch(t, A);
+    publish(t, 0, A);
+    fetch(t + G, B);
     __syncthreads();
     issue(0, 0);
-    uint64_t cur = off;
-    for (int i = 0; t < tiles; t += gridDim.x, i++) {
+    for (int i = 0; t < tiles; t += G, i++) {
         const int b = i & 1, r = i % 3, rn = (i + 1) % 3;
-        const int64_t tn = t + gridDim.x;
-        fetch(tn);
-        if (tn < tiles) publish(tn, rn);
+        const int64_t tn = t + G;
+        const Ent cur = A;
+        if (tn < tiles) publish(tn, rn, B);         // B was loaded an iteration ago
+        A = B;
+        fetch(tn + G, B);                           // two tiles ahead: consumed next iteration
         __syncthreads();                            // (A) next range visible; buffer b^1 no longer read
         if (tn < tiles) issue(b ^ 1, rn);
         else cp_async_commit();                     // keep one group per iteration
         cp_async_wait<1>();                         // this thread's copies of tile t landed
         __syncthreads();                            // (B) everyone's
         const int64_t c = t * TILE_CHUNKS + threadIdx.x;
-        if (c < n_chunks) {
-            const uint64_t base = s_lo[r] & ~(uint64_t)15;
-            body(c, reinterpret_cast<const uint32_t*>(smem + (size_t)b * buf_bytes), (uint32_t)(cur - base));
-        }
-        cur = off;
+        const uint64_t base = s_lo[r] & ~(uint64_t)15;
+        const bool valid = c < n_chunks;
+        body(c, reinterpret_cast<const uint32_t*>(smem + (size_t)b * buf_bytes), valid ? (uint32_t)(cur.off - base) : 0u,
+             valid, cur.aux);
     }
     cp_async_wait<0>();
 }
 
+// Exact per-thread accumulation of q = p + m moments from chunk moments of p (32 full values):
+//   sum q = sum p + 32 m,  sum q^2 = sum p^2 + 2 m sum p + 32 m^2.
+// Narrow chunks (|sum p| < 2^24, sum p^2 < 2^40, |m| < 2^25) accumulate the three terms in 64-bit
+// registers, folded into int128 every 2048 chunks (bounds: 2^51, 2^60, 2^61); the rest take the
+// 128-bit algebra directly.
+struct QMomAcc {
+    int64_t s1 = 0;
+    i128 s2 = 0;
+    uint64_t sq = 0;
+    int64_t msp = 0;
+    uint64_t mm = 0;
+    int n = 0;
+    __device__ __forceinline__ void fold() {
+        s2 += (i128)sq + 2 * (i128)msp + 32 * (i128)mm;
+        sq = 0;
+        msp = 0;
+        mm = 0;
+        n = 0;
+    }
+    __device__ __forceinline__ void add(const ChunkMoments& r, int64_t m) {
+        s1 += r.sp + 32 * m;
+        if (r.sq >> 40 == 0 && r.sp > -(1ll << 24) && r.sp < (1ll << 24) && m > -(1ll << 25) && m < (1ll << 25)) {
+            sq += (uint64_t)r.sq;
+            msp += m * r.sp;
+            mm += (uint64_t)(m * m);
+            if (++n == 2048) fold();
+        } else {
+            s2 += (i128)r.sq + (i128)(2 * m) * (i128)r.sp + (i128)(32 * m) * (i128)m;
+        }
+    }
+    __device__ __forceinline__ i128 total() {
+        fold();
+        return s2;
+    }
+};
+
+struct MetaAux {       // block mean of chunk c (every segment full: c / cps; cps a power of two: shift)
+    const int32_t* meta;
+    int64_t cps;
+    int shift;         // >= 0: cps == 1 << shift
+    __device__ __forceinline__ int32_t operator()(int64_t c) const {
+        return __ldg(meta + (shift >= 0 ? (c >> shift) : c / cps));
+    }
+};
+
 // MetaChunk fast path: every chunk full and every segment full-size (chunk c belongs to segment
-// c / cps), so a chunk decodes with decode32s into int4 groups; sums in int64 / u128 per thread.
-// Grid-strided over tiles: 8 CTAs per SM, one partial per CTA.
+// c / cps): per chunk the lean moments of p (moments.cuh), then the q algebra above; the block mean
+// comes with the index entries (warp_tiles, wtiles.cuh).  One partial per CTA.
+template <bool MINMAX>
 __global__ void __launch_bounds__(TILE_CHUNKS) k_reduce_meta_fast(const uint8_t* __restrict__ payload, uint64_t len,
                                                                   const uint64_t* __restrict__ offsets, int64_t n_chunks,
-                                                                  const int32_t* __restrict__ meta, int64_t cps,
-                                                                  int64_t n, HszgSums* partials, uint32_t buf_bytes) {
+                                                                  MetaAux aux, int64_t n, HszgSums* partials,
+                                                                  uint32_t buf_bytes) {
     extern __shared__ __align__(16) uint8_t smem[];
     Acc a;
     a.init();
-    u128 s2 = 0;
-    staged_tiles(payload, len, offsets, n_chunks, smem, buf_bytes, [&](int64_t c, const uint32_t* words, uint32_t rel) {
-        const int32_t mm = __ldg(meta + c / cps);
-        if (smem_byte(words, rel) <= 27) {
-            // |p| < 2^27: sums of the residuals p (q = p + m per chunk), 64-bit sum of squares chained
-            // through IMAD.WIDE, then sum q = sum p + 32m, sum q^2 = sum p^2 + 2m sum p + 32m^2
-            int64_t sp = 0, sq = 0;
-            int mnp = INT32_MAX, mxp = INT32_MIN;
-            decode32s<false>(words, rel, 0, [&](int, int4 v) {
-                sp += (int64_t)(v.x + v.y + v.z + v.w);
-                sq += (int64_t)v.x * v.x;
-                sq += (int64_t)v.y * v.y;
-                sq += (int64_t)v.z * v.z;
-                sq += (int64_t)v.w * v.w;
-                mnp = min(mnp, min(min(v.x, v.y), min(v.z, v.w)));
-                mxp = max(mxp, max(max(v.x, v.y), max(v.z, v.w)));
-            });
-            const int64_t m64 = mm;
-            a.s1 += (i128)(sp + 32 * m64);
-            a.s2 += (i128)sq + (i128)(2 * m64) * (i128)sp + (i128)(32 * m64) * (i128)m64;
-            a.vmin = min(a.vmin, mnp + mm);
-            a.vmax = max(a.vmax, mxp + mm);
-        } else {
-            int64_t s1 = 0;
-            int mn = a.vmin, mx = a.vmax;
-            decode32s<false>(words, rel, mm, [&](int, int4 v) {
-                s1 += (int64_t)v.x + v.y + v.z + v.w;
-                s2 += (u128)(sq64(v.x) + sq64(v.y));
-                s2 += (u128)(sq64(v.z) + sq64(v.w));
-                mn = min(mn, min(min(v.x, v.y), min(v.z, v.w)));
-                mx = max(mx, max(max(v.x, v.y), max(v.z, v.w)));
-            });
-            a.s1 += s1;
-            a.vmin = mn;
-            a.vmax = mx;
+    QMomAcc q;
+    warp_tiles(payload, len, offsets, n_chunks, smem + (threadIdx.x >> 5) * WT_NS * buf_bytes, buf_bytes,
+               wt_bars(smem, buf_bytes), [&](int64_t, const uint32_t* words, uint32_t rel, bool valid, int32_t m) {
+        const ChunkMoments r = chunk_moments<false, MINMAX>(words, rel, valid);
+        if (!valid) return;
+        q.add(r, m);
+        if (MINMAX) {
+            a.vmin = min(a.vmin, r.mn + m);
+            a.vmax = max(a.vmax, r.mx + m);
         }
-    });
-    a.s2 += (i128)s2;
+    }, aux);
+    a.s1 = q.s1;
+    a.s2 = q.total();
     block_reduce(a);
     if (threadIdx.x == 0) {
         a.count = blockIdx.x ? 0 : n;
@@ -204,8 +243,8 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_reduce_meta_fast(const uint8_t*
 
 // WeightedChunk fast path (stats.py:80-112: sum of (N0-i0)(N1-i1)(N2-i2) p over the box): every chunk
 // full and inside one row (n2 % 32 == 0), so a chunk starting at (i0, i1, x0) contributes
-// (N0-i0)(N1-i1)[(N2-x0) S - T] with S = sum p_j, T = sum j p_j — two integer sums per value, decoded
-// with decode32s; grid-strided tiles as k_reduce_meta_fast.
+// (N0-i0)(N1-i1)[(N2-x0) S - T] with S = sum p_j, T = sum j p_j — the lean moments with TSUM;
+// warp-private tiles as k_reduce_meta_fast.
 __global__ void __launch_bounds__(TILE_CHUNKS) k_reduce_weighted_fast(const uint8_t* __restrict__ payload,
                                                                       uint64_t len,
                                                                       const uint64_t* __restrict__ offsets,
@@ -216,21 +255,136 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_reduce_weighted_fast(const uint
     Acc a;
     a.init();
     const int64_t cpr = N2 / kChunkCap;
-    staged_tiles(payload, len, offsets, n_chunks, smem, buf_bytes, [&](int64_t c, const uint32_t* words, uint32_t rel) {
-        int64_t S = 0, T = 0;
-        decode32s<false>(words, rel, 0, [&](int q, int4 v) {
-            S += (int64_t)v.x + v.y + v.z + v.w;
-            T += (int64_t)(4 * q) * v.x + (int64_t)(4 * q + 1) * v.y + (int64_t)(4 * q + 2) * v.z +
-                 (int64_t)(4 * q + 3) * v.w;
-        });
+    i128 s1 = 0;
+    warp_tiles(payload, len, offsets, n_chunks, smem + (threadIdx.x >> 5) * WT_NS * buf_bytes, buf_bytes,
+               wt_bars(smem, buf_bytes), [&](int64_t c, const uint32_t* words, uint32_t rel, bool valid, int32_t) {
+        const ChunkMoments r = chunk_moments<true, false>(words, rel, valid);
+        if (!valid) return;
         const int64_t row = c / cpr, x0 = (c - row * cpr) * kChunkCap;
         const int64_t i0 = row / N1, i1 = row - i0 * N1;
-        a.s1 += (i128)((N0 - i0) * (N1 - i1)) * ((i128)(N2 - x0) * S - T);
+        const i128 inner = (i128)(N2 - x0) * r.sp - r.tp;
+        s1 += (i128)((N0 - i0) * (N1 - i1)) * inner;
     });
+    a.s1 = s1;
     block_reduce(a);
     if (threadIdx.x == 0) {
         a.count = blockIdx.x ? 0 : n;
         store_sums(partials + blockIdx.x, a);
+    }
+}
+
+// ---- K-REG fused from the bytes (HSZX*: regions of q = p + M_b, no reconstruction) -------------
+// Regions tile the box like grid.partition with extents R (a multiple of the block extents B on every
+// axis, so each block lies in exactly one region).  Per chunk: the lean moments of p plus the block
+// mean (exact q moments), keyed by region; a warp-segmented inclusive scan over the 32 lanes (consecutive
+// chunks share a block, hence a region) leaves each run's total on its last lane, which adds it into
+// the region's accumulator (int64 S1, S2 as four 32-bit limbs in u64 words, int32 min / max atomics).
+// k_region_accum_finish turns the accumulators into the region_buffer layout (s1, s2 lo / hi, size,
+// qmin, qmax) for k_region_finalize.
+struct RegAccum {
+    unsigned long long s1;      // two's complement int64
+    unsigned long long l[4];    // S2 limbs (32-bit parts, limb 3 signed)
+    int qmin, qmax;
+    unsigned long long pad[2];
+};
+static_assert(sizeof(RegAccum) == 64, "RegAccum layout");
+
+__global__ void k_region_accum_init(RegAccum* acc, int64_t nr) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nr; r += (int64_t)gridDim.x * blockDim.x) {
+        RegAccum a;
+        a.s1 = 0;
+        a.l[0] = a.l[1] = a.l[2] = a.l[3] = 0;
+        a.qmin = INT32_MAX;
+        a.qmax = INT32_MIN;
+        a.pad[0] = a.pad[1] = 0;
+        acc[r] = a;
+    }
+}
+
+struct RegionMap {
+    int64_t rg[3];      // region grid
+    int64_t bpr[3];     // blocks per region extent (R / B)
+};
+
+__global__ void __launch_bounds__(TILE_CHUNKS) k_region_fused(SegGeo sg, RegionMap rm, const uint8_t* __restrict__ payload,
+                                                              uint64_t len, const uint64_t* __restrict__ offsets,
+                                                              const int32_t* __restrict__ meta, bool full_segs,
+                                                              int64_t cps, RegAccum* acc, uint32_t buf_bytes) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int lane = threadIdx.x & 31;
+    warp_tiles(payload, len, offsets, sg.n_chunks, smem + (threadIdx.x >> 5) * WT_NS * buf_bytes, buf_bytes,
+               wt_bars(smem, buf_bytes), [&](int64_t c, const uint32_t* words, uint32_t rel, bool valid, int32_t) {
+        const ChunkMoments r = chunk_moments<false, true>(words, rel, valid);
+        int64_t key = -1 - lane;                  // lanes without a chunk: unique keys, zero moments
+        int64_t s1 = 0;
+        i128 s2 = 0;
+        int mn = INT32_MAX, mx = INT32_MIN;
+        if (valid) {
+            int64_t seg;
+            if (full_segs) seg = c / cps;
+            else seg = locate_chunk(sg, c).seg;
+            const int64_t b2 = seg % sg.G[2];
+            const int64_t t = seg / sg.G[2];
+            const int64_t b1 = t % sg.G[1];
+            const int64_t b0 = t / sg.G[1];
+            key = ((b0 / rm.bpr[0]) * rm.rg[1] + b1 / rm.bpr[1]) * rm.rg[2] + b2 / rm.bpr[2];
+            const int64_t m = __ldg(meta + seg);
+            s1 = r.sp + 32 * m;
+            s2 = (i128)r.sq + (i128)(2 * m) * (i128)r.sp + (i128)(32 * m) * (i128)m;
+            mn = r.mn + (int32_t)m;
+            mx = r.mx + (int32_t)m;
+        }
+        // inclusive segmented scan over runs of equal keys (a key may recur after another run: runs,
+        // not keys, are the segments — each run's last lane adds its run into the region)
+        const int64_t prev = __shfl_up_sync(0xffffffffu, key, 1);
+        const unsigned heads = __ballot_sync(0xffffffffu, lane == 0 || prev != key);
+        const int run = __popc(heads & (0xffffffffu >> (31 - lane)));
+        uint64_t lo = (uint64_t)(u128)s2, hi = (uint64_t)((u128)s2 >> 64);
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int ok = __shfl_up_sync(0xffffffffu, run, d);
+            const int64_t o1 = __shfl_up_sync(0xffffffffu, s1, d);
+            const uint64_t olo = __shfl_up_sync(0xffffffffu, lo, d);
+            const uint64_t ohi = __shfl_up_sync(0xffffffffu, hi, d);
+            const int omn = __shfl_up_sync(0xffffffffu, mn, d);
+            const int omx = __shfl_up_sync(0xffffffffu, mx, d);
+            if (lane >= d && ok == run) {
+                s1 += o1;
+                const u128 tt = (((u128)hi << 64) | lo) + (((u128)ohi << 64) | olo);
+                lo = (uint64_t)tt;
+                hi = (uint64_t)(tt >> 64);
+                mn = min(mn, omn);
+                mx = max(mx, omx);
+            }
+        }
+        const int64_t next = __shfl_down_sync(0xffffffffu, key, 1);
+        if (valid && (lane == 31 || next != key)) {
+            RegAccum* a = acc + key;
+            atomicAdd(&a->s1, (unsigned long long)s1);
+            acc_add_i128(a->l, (i128)(((u128)hi << 64) | lo));
+            atomicMin(&a->qmin, mn);
+            atomicMax(&a->qmax, mx);
+        }
+    });
+}
+
+// accumulators -> region_buffer words (s1, s2 lo / hi, size, qmin, qmax); sizes in closed form
+__global__ void k_region_accum_finish(const RegAccum* acc, int64_t n0, int64_t n1, int64_t n2, int64_t R0, int64_t R1,
+                                      int64_t R2, int64_t g1, int64_t g2, int64_t nr, int64_t* s1, uint64_t* s2lo,
+                                      int64_t* s2hi, int32_t* qmin, int32_t* qmax, int64_t* size) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nr; r += (int64_t)gridDim.x * blockDim.x) {
+        const RegAccum a = acc[r];
+        s1[r] = (int64_t)a.s1;
+        const u128 v = (u128)a.l[0] + ((u128)a.l[1] << 32) + ((u128)a.l[2] << 64) + ((u128)(int64_t)a.l[3] << 96);
+        s2lo[r] = (uint64_t)v;
+        s2hi[r] = (int64_t)(uint64_t)(v >> 64);
+        qmin[r] = a.qmin;
+        qmax[r] = a.qmax;
+        const int64_t r2 = r % g2, t = r / g2, r1 = t % g1, r0 = t / g1;
+        const int64_t e0 = (r0 + 1) * R0 <= n0 ? R0 : n0 - r0 * R0;
+        const int64_t e1 = (r1 + 1) * R1 <= n1 ? R1 : n1 - r1 * R1;
+        const int64_t e2 = (r2 + 1) * R2 <= n2 ? R2 : n2 - r2 * R2;
+        size[r] = e0 * e1 * e2;
     }
 }
 
@@ -671,12 +825,33 @@ int hszg_finalize_sums(HszgSums* partials, int64_t nparts, HszgSums* out, cudaSt
     return finalize(partials, nparts, out, st);
 }
 
+// warp_tiles launches: 256 threads, WT_NS stages per warp, as many CTAs per SM as fit
+template <typename K>
+static unsigned wtile_grid(K kernel, int max_bw, int64_t n_chunks, size_t* smem_out, uint32_t* stage_out) {
+    const uint32_t sb = wtile_stage_bytes(max_bw);
+    const size_t smem = (size_t)8 * WT_NS * sb + 8 * WT_NS * 8;
+    allow_smem(kernel, smem);
+    int per_sm = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, smem) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    cudaGetLastError();
+    const int64_t warps = (n_chunks + 31) / 32;
+    int64_t grid = (int64_t)148 * per_sm;
+    const int64_t need = (warps + 7) / 8;
+    if (need < grid) grid = need > 0 ? need : 1;
+    *smem_out = smem;
+    *stage_out = sb;
+    return (unsigned)grid;
+}
+
 extern "C" int hszg_reduce_stream(const HszgGeom* g, const HszgStream* s, int mode, HszgSums* out_dev, void* ws,
                                   size_t ws_bytes, void* stream, HszgErr* err) {
     err->status = HSZG_OK;
     cudaStream_t st = as_stream(stream);
     const SegGeo sg = make_seggeo(*g);
     HszgSums* partials = reinterpret_cast<HszgSums*>(ws);
+    const bool no_extrema = (mode & HSZG_REDUCE_NO_EXTREMA) != 0;   // vmin / vmax not wanted (statistics)
+    mode &= ~HSZG_REDUCE_NO_EXTREMA;
     if (mode == 4) {
         if (!s->metadata) {
             err->status = HSZG_INVALID_ARG;
@@ -709,21 +884,31 @@ extern "C" int hszg_reduce_stream(const HszgGeom* g, const HszgStream* s, int mo
         bool full_segs = g->n_chunks * kChunkCap == g->n && (sg.B[0] * sg.B[1] * sg.B[2]) % kChunkCap == 0;
         for (int a = 0; a < 3; a++) full_segs = full_segs && sg.E[a] == sg.B[a];
         if (mode != 3 && g->n_chunks * kChunkCap == g->n && sg.n[2] % kChunkCap == 0) {
-            const uint32_t bb = (uint32_t)((stage_bytes(s->max_bitwidth) + 15) / 16 * 16);
-            allow_smem(k_reduce_weighted_fast, 2 * (size_t)bb);
-            const int64_t grid = tiles < 148 * 6 ? tiles : 148 * 6;
-            k_reduce_weighted_fast<<<(unsigned)grid, TILE_CHUNKS, 2 * (size_t)bb, st>>>(
-                s->payload, s->payload_len, s->offsets, g->n_chunks, sg.n[0], sg.n[1], sg.n[2], g->n, partials, bb);
+            size_t sm;
+            uint32_t bb;
+            const unsigned grid = wtile_grid(k_reduce_weighted_fast, s->max_bitwidth, g->n_chunks, &sm, &bb);
+            k_reduce_weighted_fast<<<grid, 256, sm, st>>>(s->payload, s->payload_len, s->offsets, g->n_chunks,
+                                                         sg.n[0], sg.n[1], sg.n[2], g->n, partials, bb);
             { const cudaError_t e_ = cudaGetLastError(); if (e_ != cudaSuccess) return hszg_set_cuda_error(err, e_, "reduce tiles"); }
             return finalize(partials, grid, out_dev, st);
         }
         if (mode == 3 && full_segs) {
-            const uint32_t bb = (uint32_t)((stage_bytes(s->max_bitwidth) + 15) / 16 * 16);
-            allow_smem(k_reduce_meta_fast, 2 * (size_t)bb);
-            const int64_t grid = tiles < 148 * 6 ? tiles : 148 * 6;
-            k_reduce_meta_fast<<<(unsigned)grid, TILE_CHUNKS, 2 * (size_t)bb, st>>>(
-                s->payload, s->payload_len, s->offsets, g->n_chunks, s->metadata,
-                (sg.B[0] * sg.B[1] * sg.B[2]) / kChunkCap, g->n, partials, bb);
+            const int64_t cps = (sg.B[0] * sg.B[1] * sg.B[2]) / kChunkCap;
+            MetaAux aux{s->metadata, cps, -1};
+            for (int k = 0; k < 40; k++)
+                if (cps == (int64_t)1 << k) aux.shift = k;
+            size_t sm;
+            uint32_t bb;
+            unsigned grid;
+            if (no_extrema) {
+                grid = wtile_grid(k_reduce_meta_fast<false>, s->max_bitwidth, g->n_chunks, &sm, &bb);
+                k_reduce_meta_fast<false><<<grid, 256, sm, st>>>(s->payload, s->payload_len, s->offsets,
+                                                                g->n_chunks, aux, g->n, partials, bb);
+            } else {
+                grid = wtile_grid(k_reduce_meta_fast<true>, s->max_bitwidth, g->n_chunks, &sm, &bb);
+                k_reduce_meta_fast<true><<<grid, 256, sm, st>>>(s->payload, s->payload_len, s->offsets,
+                                                               g->n_chunks, aux, g->n, partials, bb);
+            }
             { const cudaError_t e_ = cudaGetLastError(); if (e_ != cudaSuccess) return hszg_set_cuda_error(err, e_, "reduce tiles"); }
             return finalize(partials, grid, out_dev, st);
         }
@@ -830,6 +1015,55 @@ extern "C" int hszg_region_reduce(const int32_t* q, int32_t ndims, const int64_t
     const int threads = rs >= 1024 ? 256 : (rs >= 256 ? 128 : 64);
     k_region_reduce<<<(unsigned)nr, threads, 0, as_stream(stream)>>>(q, n[0], n[1], n[2], R[0], R[1], R[2], g1, g2,
                                                                      s1, s2_lo, s2_hi, qmin, qmax, size);
+    return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
+}
+
+// Region reduction straight from an HSZX* stream (stage 2 / 3 integers q = p + M_b): see k_region_fused.
+// region[] in the ORIGINAL dims (clipped to them); every extent must be a multiple of the block extent
+// (or reach the grid end) and every chunk must be full.  Returns HSZG_UNSUPPORTED_STAGE when not
+// applicable (the caller reconstructs q and runs hszg_region_reduce).  ws: >= nr * 64 bytes.
+extern "C" int hszg_region_stream(const HszgGeom* g, const HszgStream* s, const int64_t* region, int64_t* s1,
+                                  uint64_t* s2_lo, int64_t* s2_hi, int32_t* qmin, int32_t* qmax, int64_t* size,
+                                  void* ws, size_t ws_bytes, void* stream, HszgErr* err) {
+    err->status = HSZG_OK;
+    cudaStream_t st = as_stream(stream);
+    if ((g->kind != 2 && g->kind != 3) || !s->canonical || !s->metadata || g->n_chunks * kChunkCap != g->n)
+        return HSZG_UNSUPPORTED_STAGE;
+    const SegGeo sg = make_seggeo(*g);
+    // regions in box coordinates (the box is the original dims, leading 1s for 2-D / 1-D)
+    const int nd = g->ndims;
+    int64_t R[3] = {1, 1, 1};
+    for (int k = 0; k < nd; k++) {
+        const int64_t r = region[k] < g->dims[k] ? region[k] : g->dims[k];
+        if (r < 1) return HSZG_INVALID_ARG;
+        R[3 - nd + k] = r;
+    }
+    if (g->kind == 2 && !(sg.n[0] == 1 && sg.n[1] == 1 && R[0] == 1 && R[1] == 1)) {
+        // HSZX: 1-D blocks of the flat stream; regions must be 1-D too
+        return HSZG_UNSUPPORTED_STAGE;
+    }
+    RegionMap rm;
+    for (int a = 0; a < 3; a++) {
+        rm.rg[a] = (sg.n[a] + R[a] - 1) / R[a];
+        if (R[a] % sg.B[a] != 0 && R[a] < sg.n[a]) return HSZG_UNSUPPORTED_STAGE;
+        rm.bpr[a] = R[a] >= sg.n[a] ? sg.G[a] : R[a] / sg.B[a];
+    }
+    const int64_t nr = rm.rg[0] * rm.rg[1] * rm.rg[2];
+    if (ws_bytes < (size_t)nr * sizeof(RegAccum)) return HSZG_INVALID_ARG;
+    RegAccum* acc = reinterpret_cast<RegAccum*>(ws);
+    bool full_segs = (sg.B[0] * sg.B[1] * sg.B[2]) % kChunkCap == 0;
+    for (int a = 0; a < 3; a++) full_segs = full_segs && sg.E[a] == sg.B[a];
+    const int64_t cps = (sg.B[0] * sg.B[1] * sg.B[2]) / kChunkCap;
+    k_region_accum_init<<<grid_for(nr, 256, 148 * 8), 256, 0, st>>>(acc, nr);
+    size_t sm;
+    uint32_t bb;
+    const unsigned grid = wtile_grid(k_region_fused, s->max_bitwidth, g->n_chunks, &sm, &bb);
+    k_region_fused<<<grid, 256, sm, st>>>(sg, rm, s->payload, s->payload_len, s->offsets, s->metadata, full_segs, cps,
+                                          acc, bb);
+    { const cudaError_t e_ = cudaGetLastError(); if (e_ != cudaSuccess) return hszg_set_cuda_error(err, e_, "region fused"); }
+    k_region_accum_finish<<<grid_for(nr, 256, 148 * 8), 256, 0, st>>>(acc, sg.n[0], sg.n[1], sg.n[2], R[0], R[1], R[2],
+                                                                     rm.rg[1], rm.rg[2], nr, s1, s2_lo, s2_hi, qmin,
+                                                                     qmax, size);
     return cudaGetLastError() == cudaSuccess ? HSZG_OK : HSZG_CUDA;
 }
 

@@ -449,3 +449,56 @@ def test_stats_wide_bitwidths(H, kind):
         want = O.var_from_dq(O.stage3(oc), c.eps) if st == H.h.Stage.QUANTIZED or not c.kind.is_block_mean else None
         if want is not None:
             assert got == want, (kind, st)
+
+
+# fused K-REG from the bytes (hszg_region_stream): HSZX* regions aligned with the blocks, every chunk full
+@pytest.mark.parametrize("dims,region,bd", [((48, 40, 64), 8, (8, 8, 8)), ((48, 40, 64), (16, 8, 32), (8, 8, 8)),
+                                            ((40, 50, 60), 16, (8, 8, 8)), ((64, 64), 16, (8, 8)),
+                                            ((24, 32, 96), (8, 16, 48), (4, 8, 8)), ((4096,), 256, (32,)),
+                                            ((48, 40, 64), 1000, (8, 8, 8))])
+@pytest.mark.parametrize("scale", ["smooth", "wide"])
+def test_regions_fused_from_bytes(H, rng, dims, region, bd, scale):
+    kind = 2 if len(dims) == 1 else 3
+    field = O.random_field(rng, dims, "smooth")
+    eps = 1e-3 * float(field.max() - field.min()) if scale == "smooth" else 1e-8 * float(np.abs(field).max())
+    c = H.h.compress(field, H.h.CompressorKind(kind), H.h.ErrorBound("abs", eps), bd if kind == 3 else bd[0])
+    oc = _oracle_of(c)
+    q = O.stage3(oc)
+    for stage in (H.h.Stage.DECORRELATED, H.h.Stage.QUANTIZED):
+        rs = H.regions.region_stats(c, region, stage, tau=float(np.median(field)))
+        s1, s2, qmin, qmax, size = O.region_reduce(q, region)
+        assert np.array_equal(rs.s1, s1.astype(np.int64)) and np.array_equal(rs.size, size)
+        assert all(int(a) == int(b) for a, b in zip(rs.s2.ravel(), s2.ravel()))
+        assert np.array_equal(rs.qmin, qmin) and np.array_equal(rs.qmax, qmax)
+        mean, var = O.region_stats(q, c.eps, region)
+        np.testing.assert_allclose(rs.mean, mean, rtol=1e-15, atol=0)
+        np.testing.assert_allclose(rs.var, var, rtol=1e-12, atol=0)
+        assert rs.crossing_count == O.threshold_count(q, c.eps, region, float(np.median(field)))
+        assert H.regions.threshold_count(c, region, 0.0, stage) == O.threshold_count(q, c.eps, region, 0.0)
+
+
+@pytest.mark.parametrize("kind", ALL)
+@pytest.mark.parametrize("scale", ["smooth", "wide", "zero"])
+def test_stats_lean_decode_vs_oracle(H, rng, kind, scale):
+    """K-STAT lean moments (moments.cuh): bit widths 0 (constant), <= 8, 9..16 and > 16 (exact 128-bit
+    path) in one stream; mean / var / std at stages 2 and 3 bit-identical to the oracle."""
+    dims = (24, 32, 64)
+    f = _wide_bitwidth_field(rng, dims) if scale == "wide" else O.random_field(rng, dims, "smooth")
+    if scale == "zero":
+        f = np.full(dims, 0.25, dtype=np.float32)
+        f[3, 4, 5] = 1.0
+    eps = 1e-3 if scale != "smooth" else 1e-4 * float(f.max() - f.min())
+    c = H.h.compress(f, H.h.CompressorKind(kind), H.h.ErrorBound("abs", eps))
+    oc = _oracle_of(c)
+    for st in (2, 3):
+        for op in ("mean", "var", "std"):
+            assert H.stats.compute_stat(c, op, H.h.Stage(st)).value == O.compute_stat(oc, op, st), (kind, st, op)
+
+
+def _wide_bitwidth_field(rng, dims):
+    """Noise whose amplitude changes every 8 x-values (bit widths 0 .. ~22), plus a constant region."""
+    n2 = dims[2]
+    scale = 10.0 ** rng.uniform(-4, 3, size=n2 // 8).repeat(8)
+    f = rng.normal(size=dims) * scale[None, None, :]
+    f[:, :, :16] = 0.5
+    return f.astype(np.float32)

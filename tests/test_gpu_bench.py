@@ -13,7 +13,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-ARGS = ["--dims", "96", "512", "512", "--steps", "1", "--warmup", "3", "--no-e2e", "--no-cpu", "--window", "32"]
+ARGS = ["--dims", "96", "512", "512", "--steps", "1", "--warmup", "3", "--no-e2e", "--no-cpu", "--window", "32", "--rows"]
 
 
 def _line(out: str) -> dict:
