@@ -19,6 +19,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from .._nvtx import ranged
 from .. import _lib, device as devmod
 from ..compressors import CompressedStream, CompressorKind, DecorrelatedStream, _as_device, recorrelate
 from ..errors import UnsupportedStageError
@@ -143,6 +144,7 @@ def _stage_q(c: CompressedStream, stage: Stage):
 _OPS = {"derivative": _lib.OP_DERIV, "laplacian": _lib.OP_LAPLACIAN, "gradient_magnitude": _lib.OP_GRADMAG}
 
 
+@ranged("hsz/compute_field_op")
 def compute_field_op(c: CompressedStream, op: str, stage: Stage, out: str = "numpy", out_dtype=None) -> DerivedField:
     """Derivative / Laplacian (and gradient magnitude, N5) of one compressed field (fields.py:181-196)."""
     stage = Stage(stage)
@@ -181,11 +183,13 @@ def _vector_op(sources, stage, opcode, name, names, out, out_dtype):
     return DerivedField(name, _host(outs, out), names[: len(outs)])
 
 
+@ranged("hsz/divergence")
 def divergence(sources, stage: Stage, out: str = "numpy", out_dtype=None) -> DerivedField:
     """sum_k D_k(u_k) in float64 in component order (fields.py:216-222), one fused launch."""
     return _vector_op(sources, stage, _lib.OP_DIVERGENCE, "divergence", ("div",), out, out_dtype)
 
 
+@ranged("hsz/curl")
 def curl(sources, stage: Stage, out: str = "numpy", out_dtype=None) -> DerivedField:
     """2-D scalar curl dy(u)-dx(v); 3-D right-handed curl (fields.py:225-236)."""
     names = ("curl",) if len(sources) == 2 else ("cx", "cy", "cz")
@@ -196,6 +200,7 @@ def curl(sources, stage: Stage, out: str = "numpy", out_dtype=None) -> DerivedFi
 # Out-of-core streaming (Algorithm 3)
 
 
+@ranged("hsz/streamed_derivative")
 def streamed_derivative(c: CompressedStream, out: str = "numpy", out_dtype=None, from_host=None) -> DerivedField:
     """Slab-streamed derivative holding at most three quantized slabs (fields.py:243-272).
 

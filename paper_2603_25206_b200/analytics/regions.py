@@ -25,6 +25,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from .._nvtx import ranged
 from .. import _lib, device as devmod
 from ..compressors import CompressedStream
 from ..stages import Stage, _check_stage, count_stage_work
@@ -131,6 +132,7 @@ def _quantized(c: CompressedStream, stage: Stage):
     return c.device().reconstruct(t.int32)
 
 
+@ranged("hsz/region_stats")
 def region_stats(c: CompressedStream, region, stage: Stage = Stage.QUANTIZED,
                  tau: float | None = None) -> RegionStats:
     """Per-region mean/variance/min/max (N2, N3) and optionally the tau crossing count (N4)."""
@@ -156,6 +158,7 @@ def region_minmax(c: CompressedStream, region, stage: Stage = Stage.QUANTIZED):
     return s.qmin, s.qmax, s.vmin, s.vmax
 
 
+@ranged("hsz/threshold_count")
 def threshold_count(c: CompressedStream, region, tau: float, stage: Stage = Stage.QUANTIZED) -> int:
     """N4: number of regions with min_r < tau <= max_r (only the count leaves the device)."""
     return int(_region_device(c, stage, region, float(tau))["count"].item())

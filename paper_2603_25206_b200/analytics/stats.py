@@ -17,6 +17,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from .._nvtx import ranged
 from .. import _lib, device as devmod
 from ..compressors import CompressedStream, CompressorKind, DecorrelatedStream, _as_device, _stored_block_dims
 from ..errors import UnsupportedStageError
@@ -263,6 +264,7 @@ def stream_sums(c: CompressedStream, stage: Stage):
     return _lib.read_sums(devmod.reduce_i32(q))
 
 
+@ranged("hsz/compute_stat")
 def compute_stat(c: CompressedStream, op: str, stage: Stage) -> StatResult:
     """Run mean / std / var at the given stage of a compressed stream (stats.py:195-212)."""
     stage = Stage(stage)

@@ -22,6 +22,7 @@ from functools import cached_property
 
 import numpy as np
 
+from ._nvtx import ranged
 from . import _lib, codec
 from .device import DeviceStream
 from .errors import EpsTooSmallError, MissingContextError
@@ -437,6 +438,7 @@ def compress_device(field_dev, kind: CompressorKind, eps: float, block_dims) -> 
     return ds
 
 
+@ranged("hsz/compress")
 def compress(field, kind: CompressorKind, bound: ErrorBound, block_dims=None) -> CompressedStream:
     """Quantize, partition, decorrelate and encode a floating-point field (compressors.py:313-339)."""
     kind = CompressorKind(kind)

@@ -31,6 +31,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
+from ._nvtx import ranged
 
 _SMS = 148          # B200 SM count (grid sizing only)
 FUSED_LAYERS = 16   # block layers (8 planes each) per CTA of the one-pass kernels
@@ -440,6 +441,7 @@ class WindowPipeline:
             return n2 % 32 == 0 and n2 <= 4096
         return True
 
+    @ranged("hsz/pipeline_run")
     def run(self, outs, stats: bool = True, _prepared: bool = False):
         """Fill outs = [dz, dy, dx, laplacian] (float tensors of shape (nz, n1, n2)); return global stats.
 

@@ -22,6 +22,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from ._nvtx import ranged
 from . import _lib
 from .compressors import CompressedStream, CompressorKind, DecorrelatedStream
 from .counters import decode_counters
@@ -82,6 +83,7 @@ def _check_stage(c: CompressedStream, stage: Stage):
         raise UnsupportedStageError(f"stage {stage.cli_name} is not supported by {c.kind.cli_name}")
 
 
+@ranged("hsz/partial_decompress")
 def partial_decompress(c: CompressedStream, stage: Stage, out: str = "numpy", dtype=None):
     """Decompress to ``stage`` (stages.py:63-88).
 
