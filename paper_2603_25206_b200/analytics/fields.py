@@ -143,7 +143,6 @@ def _stage_q(c: CompressedStream, stage: Stage):
 
 _OPS = {"derivative": _lib.OP_DERIV, "laplacian": _lib.OP_LAPLACIAN, "gradient_magnitude": _lib.OP_GRADMAG}
 
-
 @ranged("hsz/compute_field_op")
 def compute_field_op(c: CompressedStream, op: str, stage: Stage, out: str = "numpy", out_dtype=None) -> DerivedField:
     """Derivative / Laplacian (and gradient magnitude, N5) of one compressed field (fields.py:181-196)."""

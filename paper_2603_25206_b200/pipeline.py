@@ -65,6 +65,13 @@ def apply_settings(pipe, **kw):
 class Comm:
     """Rank/world and the few collectives the pipeline needs (no-ops at world size 1)."""
 
+    @classmethod
+    def local(cls):
+        """A world-1 communicator regardless of any initialised process group (single-GPU API calls)."""
+        c = cls.__new__(cls)
+        c.dist, c.group, c.rank, c.world, c.host_staged = None, None, 0, 1, False
+        return c
+
     def __init__(self, group=None):
         try:
             import torch.distributed as dist
@@ -435,7 +442,8 @@ class WindowPipeline:
         """The fused window kernels need rows of whole chunks (HSZP_ND), 16-B rows and fp32 outputs."""
         t = _lib.torch()
         n2 = self.sf.global_dims[2]
-        if n2 % 4 or outs[0].dtype != t.float32 or not self._canonical():
+        o = next(x for x in outs if x is not None)
+        if n2 % 4 or o.dtype != t.float32 or not self._canonical():
             return False
         if self.sf.kind == HSZP_ND:
             return n2 % 32 == 0 and n2 <= 4096
@@ -457,7 +465,7 @@ class WindowPipeline:
                 self._replay(outs)
             else:
                 self._fused_loop(outs)
-            res = self._finish_stats(_prepared)
+            res = self._finish_stats(_prepared) if stats else None
             ovf = self._l_overflow(_prepared)
             if ovf:
                 # a narrow band-local prefix did not fit: widen (int8 -> int16, int16 -> int32; kept from
@@ -468,14 +476,15 @@ class WindowPipeline:
                 self._pers_W = None
                 self._stage_boundary()
                 self._fused_loop(outs)
-                res = self._finish_stats(_prepared)
+                res = self._finish_stats(_prepared) if stats else None
                 if self._l_overflow(_prepared):
                     self.l16 = False
                     self._pers_W = None
                     self._stage_boundary()
                     self._fused_loop(outs)
-                    res = self._finish_stats(_prepared)
-            if not self.exact_fp32 and not self._fast_valid(res, _prepared):
+                    res = self._finish_stats(_prepared) if stats else None
+            if not self.exact_fp32 and not self._fast_valid(res if stats else self._finish_stats(_prepared),
+                                                            _prepared):
                 # the fast emitter needs |q| < 2^27 (FAST_QLIM, stencil.cuh): every q is some point's
                 # centre, so the exact min / max decide it; redo the pass with the exact emitter
                 self.exact_fp32 = True
@@ -597,7 +606,7 @@ class WindowPipeline:
 
     def _replay(self, outs):
         t = _lib.torch()
-        key = tuple(_lib.ptr(o) for o in outs) + (self.halo_lo is not None, self.halo_hi is not None,
+        key = tuple(0 if o is None else _lib.ptr(o) for o in outs) + (self.halo_lo is not None, self.halo_hi is not None,
                                                   self.exact_fp32, self.overlap, self.fused_layers, self.side_priority)
         if self._graph is None or self._graph_key != key:
             self._fused_loop(outs)                        # warm-up: workspaces, smem attributes
@@ -651,7 +660,7 @@ class WindowPipeline:
             self.timer.begin("fused")
         carry = self.carry_buf[0] if sf.z0 > 0 else None
         upper = self.halo_buf[1] if self.halo_hi is not None else None
-        outs_arr = (ctypes.c_void_p * 4)(*[_lib.ptr(o) for o in outs])
+        outs_arr = self._outs_arr(outs, 0, self.sf.nz)
         _lib.call("hszg_lorenzo_onepass", ctypes.byref(self.ds.geom), ctypes.byref(self.ds.desc),
                   _lib.ptr(self.lz_bands), _lib.ptr(self.lz_edges), _lib.ptr(carry) if carry is not None else None,
                   _lib.ptr(upper) if upper is not None else None, sf.z0, sf.global_dims[0], outs_arr,
@@ -667,7 +676,7 @@ class WindowPipeline:
         if self.timer:
             self.timer.begin("fused")
         err = _lib.Err()
-        outs_arr = (ctypes.c_void_p * 4)(*[_lib.ptr(o) for o in outs])
+        outs_arr = self._outs_arr(outs, 0, self.sf.nz)
         _lib.call("hszg_fused_blocks", ctypes.byref(self.ds.geom), ctypes.byref(self.ds.desc), sf.z0,
                   sf.global_dims[0], _lib.ptr(self.halo_buf[0]) if self.halo_lo is not None else None,
                   _lib.ptr(self.halo_buf[1]) if self.halo_hi is not None else None, outs_arr, _lib.ptr(self.acc),
@@ -677,7 +686,8 @@ class WindowPipeline:
             self.timer.end("fused", self._range_bytes(0, sf.nz) + 16 * sf.nz * self.plane)
 
     def _outs_arr(self, outs, a, b):
-        return (ctypes.c_void_p * 4)(*[_lib.ptr(o[a:b]) for o in outs])
+        """Output pointers of planes [a, b); None outputs stay null (the kernels skip them)."""
+        return (ctypes.c_void_p * 4)(*[None if o is None else _lib.ptr(o[a:b]) for o in outs])
 
     def _windows(self):
         nz = self.sf.nz
