@@ -201,15 +201,6 @@ struct QMomAcc {
     }
 };
 
-struct MetaAux {       // block mean of chunk c (every segment full: c / cps; cps a power of two: shift)
-    const int32_t* meta;
-    int64_t cps;
-    int shift;         // >= 0: cps == 1 << shift
-    __device__ __forceinline__ int32_t operator()(int64_t c) const {
-        return __ldg(meta + (shift >= 0 ? (c >> shift) : c / cps));
-    }
-};
-
 // MetaChunk fast path: every chunk full and every segment full-size (chunk c belongs to segment
 // c / cps): per chunk the lean moments of p (moments.cuh), then the q algebra above; the block mean
 // comes with the index entries (warp_tiles, wtiles.cuh).  One partial per CTA.
@@ -823,25 +814,6 @@ static int finalize(HszgSums* partials, int64_t nparts, HszgSums* out, cudaStrea
 
 int hszg_finalize_sums(HszgSums* partials, int64_t nparts, HszgSums* out, cudaStream_t st) {
     return finalize(partials, nparts, out, st);
-}
-
-// warp_tiles launches: 256 threads, WT_NS stages per warp, as many CTAs per SM as fit
-template <typename K>
-static unsigned wtile_grid(K kernel, int max_bw, int64_t n_chunks, size_t* smem_out, uint32_t* stage_out) {
-    const uint32_t sb = wtile_stage_bytes(max_bw);
-    const size_t smem = (size_t)8 * WT_NS * sb + 8 * WT_NS * 8;
-    allow_smem(kernel, smem);
-    int per_sm = 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, smem) != cudaSuccess || per_sm < 1)
-        per_sm = 1;
-    cudaGetLastError();
-    const int64_t warps = (n_chunks + 31) / 32;
-    int64_t grid = (int64_t)148 * per_sm;
-    const int64_t need = (warps + 7) / 8;
-    if (need < grid) grid = need > 0 ? need : 1;
-    *smem_out = smem;
-    *stage_out = sb;
-    return (unsigned)grid;
 }
 
 extern "C" int hszg_reduce_stream(const HszgGeom* g, const HszgStream* s, int mode, HszgSums* out_dev, void* ws,

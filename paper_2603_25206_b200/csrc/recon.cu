@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include "tile.cuh"
 #include "lookback.cuh"
+#include "wtiles.cuh"
 
 extern "C" int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t band_rows, void* L, int32_t* A,
                               int32_t* strip_edges, int l_int16, int32_t* l_overflow, int ctas_per_sm, void* stream,
@@ -487,8 +488,129 @@ static bool stream_full_ok(const HszgGeom* g, const SegGeo& sg, const void* out)
     return ok;
 }
 
+// Stream-order outputs (stage 2 p; HSZX stage 3/4 q = p + M_b, whose stream order is row-major) from
+// warp-private 32-chunk tiles (wtiles.cuh): each lane decodes its chunk into the warp's shared tile
+// (36-word chunk stride, 16-B stores), then the warp writes the tile's 1024 contiguous values with
+// coalesced 16-B stores (512 B per warp instruction instead of 32 scattered 16-B pieces).
+constexpr size_t WS_TILE_BYTES = (size_t)32 * kChunkStride * 4;
+
+template <int Mode, typename OutT>
+__global__ void __launch_bounds__(256) k_wt_stream(const uint8_t* __restrict__ payload, uint64_t len,
+                                                   const uint64_t* __restrict__ offsets, int64_t n_chunks, MetaAux aux,
+                                                   double two_eps, OutT* __restrict__ out, uint32_t sb_bytes) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int lane = threadIdx.x & 31;
+    int32_t* tile = reinterpret_cast<int32_t*>(wt_scratch(smem, sb_bytes, WS_TILE_BYTES));
+    auto body = [&](int64_t c, const uint32_t* words, uint32_t rel, bool valid, int32_t m) {
+        if (valid) decode32<false>(words, rel, tile + lane * kChunkStride, Mode ? m : 0);
+        __syncwarp();
+        const int64_t c0 = c - lane;
+        const int nv = n_chunks - c0 < 32 ? (int)(n_chunks - c0) : 32;
+        OutT* o = out + c0 * kChunkCap;
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const int idx = 128 * i + 4 * lane;
+            if ((idx >> 5) < nv)
+                store4<OutT>(o + idx, *reinterpret_cast<const int4*>(tile + (idx >> 5) * kChunkStride + (idx & 31)),
+                             two_eps);
+        }
+        __syncwarp();
+    };
+    if (Mode) warp_tiles(payload, len, offsets, n_chunks, smem + (threadIdx.x >> 5) * WT_NS * sb_bytes, sb_bytes,
+                         wt_bars(smem, sb_bytes), body, aux);
+    else warp_tiles(payload, len, offsets, n_chunks, smem + (threadIdx.x >> 5) * WT_NS * sb_bytes, sb_bytes,
+                    wt_bars(smem, sb_bytes), body);
+}
+
+// HSZX_ND stage 3 / 4 with power-of-two block extents (B2 >= 4) and full blocks: the warp's tile
+// (32 chunks, 1024 block-contiguous values: whole blocks or a part of one) is written to the row-major
+// grid a float4 at a time — lane pairs write whole 32-B rows of 8^3 blocks, every sector full.  Block
+// origins are computed once per tile (one lane per block) and shuffled to the writers.
+struct BlkGeo {
+    int lb0, lb1, lb2, lbs;           // log2 of the block extents, of the block size
+    int64_t G1, G2, n1, n2;
+};
+
+template <typename OutT>
+__global__ void __launch_bounds__(256) k_wt_blocks(const uint8_t* __restrict__ payload, uint64_t len,
+                                                   const uint64_t* __restrict__ offsets, int64_t n_chunks, MetaAux aux,
+                                                   BlkGeo bg, double two_eps, OutT* __restrict__ out, uint32_t sb_bytes) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int lane = threadIdx.x & 31;
+    int32_t* tile = reinterpret_cast<int32_t*>(wt_scratch(smem, sb_bytes, WS_TILE_BYTES));
+    const int nblk = bg.lbs >= 10 ? 1 : 1 << (10 - bg.lbs);          // blocks per full tile (<= 32)
+    warp_tiles(payload, len, offsets, n_chunks, smem + (threadIdx.x >> 5) * WT_NS * sb_bytes, sb_bytes,
+               wt_bars(smem, sb_bytes), [&](int64_t c, const uint32_t* words, uint32_t rel, bool valid, int32_t m) {
+        if (valid) decode32<false>(words, rel, tile + lane * kChunkStride, m);
+        const int64_t c0 = c - lane;
+        const int nv = n_chunks - c0 < 32 ? (int)(n_chunks - c0) : 32;
+        const int64_t v0 = c0 * kChunkCap;
+        const int64_t bfirst = v0 >> bg.lbs;
+        int64_t org = 0;
+        if (lane < nblk) {
+            const int64_t b = bfirst + lane;
+            const int64_t b2 = b % bg.G2, r = b / bg.G2;
+            const int64_t b1 = r % bg.G1, b0 = r / bg.G1;
+            org = (((b0 << bg.lb0) * bg.n1) + (b1 << bg.lb1)) * bg.n2 + (b2 << bg.lb2);
+        }
+        __syncwarp();
+        const int64_t bmask = ((int64_t)1 << bg.lbs) - 1;
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const int idx = 128 * i + 4 * lane;
+            const int64_t v = v0 + idx;
+            const int bl = (int)((v >> bg.lbs) - bfirst);
+            const int64_t ob = __shfl_sync(0xffffffffu, org, bl & 31);
+            if ((idx >> 5) < nv) {
+                const int64_t l = v & bmask;
+                const int64_t xl = l & ((1 << bg.lb2) - 1);
+                const int64_t yl = (l >> bg.lb2) & ((1 << bg.lb1) - 1);
+                const int64_t zl = l >> (bg.lb1 + bg.lb2);
+                store4<OutT>(out + ob + (zl * bg.n1 + yl) * bg.n2 + xl,
+                             *reinterpret_cast<const int4*>(tile + (idx >> 5) * kChunkStride + (idx & 31)), two_eps);
+            }
+        }
+        __syncwarp();
+    }, aux);
+}
+
+static int ilog2_exact(int64_t v) {
+    for (int k = 0; k < 62; k++)
+        if (v == (int64_t)1 << k) return k;
+    return -1;
+}
+
 template <int Mode, typename OutT>
 static void launch_stream_full(const HszgGeom* g, const HszgStream* s, const SegGeo& sg, OutT* out, cudaStream_t st) {
+    static const char* wtb = getenv("HSZG_STREAM");
+    if (Mode == 2 && !(wtb && wtb[0] == 'c')) {
+        BlkGeo bg{ilog2_exact(sg.B[0]), ilog2_exact(sg.B[1]), ilog2_exact(sg.B[2]), 0, sg.G[1], sg.G[2], sg.n[1], sg.n[2]};
+        if (bg.lb0 >= 0 && bg.lb1 >= 0 && bg.lb2 >= 2) {
+            bg.lbs = bg.lb0 + bg.lb1 + bg.lb2;
+            const int64_t cps = (sg.B[0] * sg.B[1] * sg.B[2]) / kChunkCap;
+            MetaAux aux{s->metadata, cps, ilog2_exact(cps)};
+            size_t sm;
+            uint32_t sb;
+            const unsigned grid = wtile_grid(k_wt_blocks<OutT>, s->max_bitwidth, g->n_chunks, &sm, &sb, WS_TILE_BYTES);
+            k_wt_blocks<OutT><<<grid, 256, sm, st>>>(s->payload, s->payload_len, s->offsets, g->n_chunks, aux, bg,
+                                                    2.0 * g->eps, out, sb);
+            return;
+        }
+    }
+    static const char* wt = getenv("HSZG_STREAM");           // 'c': the CTA-tile kernel below (A/B runs)
+    if (Mode != 2 && !(wt && wt[0] == 'c')) {
+        const int64_t cps = (sg.B[0] * sg.B[1] * sg.B[2]) / kChunkCap;
+        MetaAux aux{s->metadata, cps > 0 ? cps : 1, -1};
+        for (int k = 0; k < 40; k++)
+            if (aux.cps == (int64_t)1 << k) aux.shift = k;
+        size_t sm;
+        uint32_t sb;
+        const unsigned grid = wtile_grid(k_wt_stream<Mode, OutT>, s->max_bitwidth, g->n_chunks, &sm, &sb,
+                                         WS_TILE_BYTES);
+        k_wt_stream<Mode, OutT><<<grid, 256, sm, st>>>(s->payload, s->payload_len, s->offsets, g->n_chunks, aux,
+                                                       2.0 * g->eps, out, sb);
+        return;
+    }
     const size_t smem = stage_bytes(s->max_bitwidth);
     allow_smem(k_stream_full<Mode, OutT>, smem);
     const int64_t tiles = (g->n_chunks + SF_THREADS - 1) / SF_THREADS;

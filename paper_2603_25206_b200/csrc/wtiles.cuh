@@ -9,6 +9,7 @@
 #pragma once
 #include "async.cuh"
 #include "common.cuh"
+#include "tile.cuh"
 
 namespace hszg {
 
@@ -102,6 +103,41 @@ __device__ __forceinline__ void warp_tiles(const uint8_t* __restrict__ payload, 
              valid ? (uint32_t)(cur.off - base) : 0u, valid, cur.aux);
         __syncwarp();                             // the stage may be refilled next iteration
     }
+}
+
+struct MetaAux {       // block mean of chunk c (every segment full: c / cps; cps a power of two: shift)
+    const int32_t* meta;
+    int64_t cps;
+    int shift;         // >= 0: cps == 1 << shift
+    __device__ __forceinline__ int32_t operator()(int64_t c) const {
+        return __ldg(meta + (shift >= 0 ? (c >> shift) : c / cps));
+    }
+};
+
+// warp_tiles launches: 256 threads, WT_NS stages per warp, as many CTAs per SM as fit
+// (+ extra_per_warp bytes of per-warp scratch after the barriers)
+template <typename K>
+inline unsigned wtile_grid(K kernel, int max_bw, int64_t n_chunks, size_t* smem_out, uint32_t* stage_out,
+                           size_t extra_per_warp = 0) {
+    const uint32_t sb = wtile_stage_bytes(max_bw);
+    const size_t smem = (size_t)8 * WT_NS * sb + 8 * WT_NS * 8 + 8 * extra_per_warp;
+    allow_smem(kernel, smem);
+    int per_sm = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, smem) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    cudaGetLastError();
+    const int64_t warps = (n_chunks + 31) / 32;
+    int64_t grid = (int64_t)148 * per_sm;
+    const int64_t need = (warps + 7) / 8;
+    if (need < grid) grid = need > 0 ? need : 1;
+    *smem_out = smem;
+    *stage_out = sb;
+    return (unsigned)grid;
+}
+
+// this warp's scratch (extra_per_warp bytes, 16-B aligned) after the rings and the barriers
+__device__ __forceinline__ uint8_t* wt_scratch(uint8_t* smem, uint32_t stage_bytes, size_t extra_per_warp) {
+    return smem + (size_t)8 * WT_NS * stage_bytes + 8 * WT_NS * 8 + (threadIdx.x >> 5) * extra_per_warp;
 }
 
 }  // namespace hszg
