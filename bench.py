@@ -179,6 +179,9 @@ def count_kernel_launches(fn):
     from torch.profiler import ProfilerActivity, profile
 
     torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]):      # CUPTI warm-up: a fresh session can miss
+        fn()                                                # the first launches (bench_rows._kernel_ms)
+        torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         fn()
         torch.cuda.synchronize()
