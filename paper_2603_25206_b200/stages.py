@@ -272,54 +272,94 @@ def slab_iter(c: CompressedStream, stage: Stage, out: str = "numpy", from_host=N
     stage = Stage(stage)
     if stage not in supported_stages(c.kind) or stage == Stage.META:
         raise UnsupportedStageError(f"stage {stage.cli_name} is not slab-iterable for {c.kind.cli_name}")
-    t = _lib.torch()
-    carry = None
     bounds = slab_bounds(c)
     src = None
     if streaming.should_stream(c, from_host):
         src = streaming.HostSlabSource(c, bounds, lambda lo, hi: _slab_layout(c, lo, hi),
                                        budget or streaming.DEFAULT_BUDGET)
+    yield from _slab_iter_batched(c, stage, out, bounds, src)
+
+
+SLAB_BATCH_BYTES = 64 << 20     # device bytes of int32 values decoded per launch group by slab_iter
+
+
+def _slab_iter_batched(c: CompressedStream, stage: Stage, out: str, bounds: list, src=None):
+    """slab_iter with consecutive slabs decoded together — up to SLAB_BATCH_BYTES of values per reconstruct
+    launch and, when streaming from host memory, inside one fetch unit (HSZP_ND: one plane per slab would
+    otherwise be one band-scan launch per plane) — and yielded as views of the batch: the same arrays,
+    counters and slab-tracker events per slab as one-slab decoding (stages.py:173-225)."""
+    t = _lib.torch()
+    per_row = int(np.prod(c.shape.dims[1:])) if c.kind.is_nd else 1
+    if src is None:
+        host = c.chunk_offsets
+        d = c.device().validate()
+        nc, plen = d.n_chunks, d.payload_len
+
+    def slab_bytes(k, lo, hi):
+        if src is not None:                          # from the fetch units' slab table
+            first, last, b0, b1 = src.slabs[k][:4]
+            return last - first, b1 - b0
+        first, last = _slab_chunk_range(c, lo, hi)
+        a = int(host[first]) if first < nc else plen
+        b = int(host[last]) if last < nc else plen
+        return last - first, b - a
+
+    carry = None
     cur_unit = -1
-    for k, (lo, hi) in enumerate(bounds):
+    k = 0
+    while k < len(bounds):
+        j = k + 1
+        while (j < len(bounds) and (bounds[j][1] - bounds[k][0]) * per_row * 4 <= SLAB_BATCH_BYTES
+               and (src is None or src.unit_of[j] == src.unit_of[k])):
+            j += 1
+        blo, bhi = bounds[k][0], bounds[j - 1][1]
         if src is None:
-            sub, nch, nbytes = _slab_view(c, lo, hi)
+            sub, _, _ = _slab_view(c, blo, bhi)
         else:
             u = int(src.unit_of[k])
             if u != cur_unit and cur_unit >= 0:
-                src.release(cur_unit)          # its slabs' kernels are queued: the slot may refill
+                src.release(cur_unit)                # its slabs' kernels are queued: the slot may refill
             cur_unit = u
-            sub, nch, nbytes, _ = src.slab(k)
-        decode_counters.chunks_decoded += nch
-        decode_counters.bytes_read += nbytes
+            sub = src.span(k, j)
         if stage == Stage.DECORRELATED:
-            p = sub.decode()
-            slab_tracker.alloc()
-            yield p.cpu().numpy() if out == "numpy" else p
-            continue
-        if c.kind.is_block_mean:
-            decode_counters.bytes_read += 4 * (sub.metadata.numel())
-        q = sub.reconstruct(t.int32)
-        if c.kind == CompressorKind.HSZP:
-            q = q.reshape(-1)
-            if carry is not None:
-                _lib.call("hszg_add_plane", _lib.ptr(q), _lib.ptr(carry), 1, q.numel(), _lib.stream_handle())
-            carry = q[-1:].clone()
-        elif c.kind == CompressorKind.HSZP_ND:
-            plane = int(np.prod(c.shape.dims[1:]))
-            if carry is not None:
-                _lib.call("hszg_add_plane", _lib.ptr(q), _lib.ptr(carry), plane, q.numel(), _lib.stream_handle())
-            carry = q.reshape(hi - lo, -1)[-1].clone()
-        decode_counters.recorrelated_elements += q.numel()
-        if stage == Stage.QUANTIZED:
-            slab_tracker.alloc()
-            yield q.cpu().numpy() if out == "numpy" else q
+            vals = sub.decode()
         else:
-            decode_counters.dequantized_elements += q.numel()
-            from .quant import dequantize_device
+            vals = sub.reconstruct(t.int32)
+            if c.kind == CompressorKind.HSZP:
+                vals = vals.reshape(-1)
+                if carry is not None:
+                    _lib.call("hszg_add_plane", _lib.ptr(vals), _lib.ptr(carry), 1, vals.numel(), _lib.stream_handle())
+                carry = vals[-1:].clone()
+            elif c.kind == CompressorKind.HSZP_ND:
+                if carry is not None:
+                    _lib.call("hszg_add_plane", _lib.ptr(vals), _lib.ptr(carry), per_row, vals.numel(),
+                              _lib.stream_handle())
+                carry = vals.reshape(bhi - blo, -1)[-1].clone()
+            if stage == Stage.FULL:
+                from .quant import dequantize_device
 
-            f = dequantize_device(q, c.eps)
+                vals = dequantize_device(vals, c.eps)
+        flat = vals.reshape(-1)
+        host_vals = flat.cpu().numpy() if out == "numpy" else None
+        for i, (lo, hi) in enumerate(bounds[k:j], start=k):
+            nch, nbytes = slab_bytes(i, lo, hi)
+            decode_counters.chunks_decoded += nch
+            decode_counters.bytes_read += nbytes
+            a, b = (lo - blo) * per_row, (hi - blo) * per_row
+            shape = ((hi - lo),) + tuple(c.shape.dims[1:]) if c.kind.is_nd else (hi - lo,)
+            if stage != Stage.DECORRELATED:
+                if c.kind.is_block_mean:
+                    _, _, mlo, mhi, _, _ = _slab_layout(c, lo, hi)
+                    decode_counters.bytes_read += 4 * (mhi - mlo)
+                decode_counters.recorrelated_elements += b - a
+                if stage == Stage.FULL:
+                    decode_counters.dequantized_elements += b - a
             slab_tracker.alloc()
-            yield f.cpu().numpy() if out == "numpy" else f
+            if stage == Stage.DECORRELATED:                  # stage 2: stream order, flat (sub.decode())
+                yield host_vals[a:b] if out == "numpy" else flat[a:b]
+            else:
+                yield host_vals[a:b].reshape(shape) if out == "numpy" else flat[a:b].reshape(shape)
+        k = j
 
 
 def sliding_window(c: CompressedStream, stage: Stage, out: str = "numpy", from_host=None):

@@ -163,6 +163,20 @@ class HostSlabSource:
         sub.validated = True
         return sub, last - first, b1 - b0, u
 
+    def span(self, k0: int, k1: int) -> DeviceStream:
+        """Validated DeviceStream view of slabs [k0, k1) of one unit (slab_iter decodes them together)."""
+        sub0, _, _, u = self.slab(k0)
+        if k1 == k0 + 1:
+            return sub0
+        assert int(self.unit_of[k1 - 1]) == u, "a span must stay inside one fetch unit"
+        s = self.fetched[u]
+        _, _, _, _, _, _, dims, bd = self.slabs[k0]
+        sdims, sbd = self.unit_dims(self.bounds[k0][0], self.bounds[k1 - 1][1], dims, bd)
+        sub = self._view(s, u, k0, k1, sdims, sbd)
+        sub.desc.canonical, sub.desc.max_bitwidth = self.validated[u]
+        sub.validated = True
+        return sub
+
     def unit_dims(self, lo, hi, dims, bd):
         if self.c.kind.is_nd:
             return (hi - lo,) + tuple(self.c.shape.dims[1:]), tuple(

@@ -31,12 +31,21 @@ def test_streamed_slabs_match_resident(kind, dims, budget):
     f = O.random_field(rng, dims, "smooth")
     c = h.compress(f, h.CompressorKind(kind), h.ErrorBound("rel", 1e-3))
     hc = _host_only(c)
+    from paper_2603_25206_b200.counters import decode_counters
+
     for st in (h.Stage.DECORRELATED, h.Stage.QUANTIZED, h.Stage.FULL):
-        want = list(h.slab_iter(c, st))
+        decode_counters.reset()
+        want = list(h.slab_iter(c, st))                 # resident: batched decode, per-slab views
+        cw = (decode_counters.chunks_decoded, decode_counters.bytes_read, decode_counters.recorrelated_elements,
+              decode_counters.dequantized_elements)
+        decode_counters.reset()
         got = list(h.slab_iter(hc, st, from_host=True, budget=budget))
+        cg = (decode_counters.chunks_decoded, decode_counters.bytes_read, decode_counters.recorrelated_elements,
+              decode_counters.dequantized_elements)
+        assert cw == cg, (st, cw, cg)                   # the reference's per-slab work counters
         assert len(got) == len(want)
         for a, b in zip(got, want):
-            assert np.array_equal(a, b), (st, budget)
+            assert a.shape == b.shape and np.array_equal(a, b), (st, budget)
     assert hc._device is None                      # nothing uploaded whole
 
 
