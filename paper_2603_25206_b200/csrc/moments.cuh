@@ -148,4 +148,91 @@ __device__ __forceinline__ ChunkMoments chunk_moments(const uint32_t* w, uint32_
     return r;
 }
 
+// Running-prefix moments of one full chunk (HSZP variance by tile algebra, ops.cu): with l_k the
+// chunk-local inclusive prefix of p (l_31 = T, the chunk total), returns T, S1 = sum_k l_k and
+// S2 = sum_k l_k^2.  Narrow chunks (bw <= 16: |l_k| < 2^21) run in int32 / one IMAD.WIDE per value; the
+// window width is warp-uniform as in chunk_moments; wider chunks take int64 / u128.
+struct PrefixMoments {
+    int64_t T, S1;
+    u128 S2;
+};
+
+template <int G>
+__device__ __forceinline__ void prefix_moments_g(const uint32_t* w, uint32_t rel, uint32_t bw, uint32_t smask,
+                                                 PrefixMoments& r) {
+    const uint32_t bitpos = (rel + 5) * 8;
+    uint32_t wi = bitpos >> 5, sh = bitpos & 31;
+    uint32_t cur = w[wi], nxt = w[wi + 1];
+    const uint32_t mask = (1u << bw) - 1u;
+    const uint32_t adv = (uint32_t)G * bw;
+    int32_t run = 0, s1 = 0;
+    uint64_t s2 = 0;
+#pragma unroll
+    for (int k = 0; k < 32 / G; k++) {
+        const uint32_t grp = __funnelshift_r(cur, nxt, sh);
+#pragma unroll
+        for (int i = 0; i < G; i++) {
+            const int j = k * G + i;
+            const int32_t m = (int32_t)(i == 0 ? (grp & mask) : ((grp >> (i * bw)) & mask));
+            run += ((smask >> j) & 1u) ? -m : m;
+            s1 += run;
+            s2 += (uint64_t)((int64_t)run * run);
+        }
+        if (k + 1 < 32 / G) {
+            sh += adv;
+            if (sh >= 32) {
+                sh -= 32;
+                cur = nxt;
+                wi++;
+                nxt = w[wi + 1];
+            }
+        }
+    }
+    r.T = run;
+    r.S1 = s1;
+    r.S2 = s2;
+}
+
+__device__ __forceinline__ void prefix_moments_wide(const uint32_t* w, uint32_t rel, uint32_t bw, uint32_t smask,
+                                                    PrefixMoments& r) {
+    const uint32_t bitpos = (rel + 5) * 8;
+    uint32_t wi = bitpos >> 5, sh = bitpos & 31;
+    uint32_t cur = w[wi], nxt = w[wi + 1];
+    const uint32_t mask = bw >= 32 ? 0xffffffffu : (1u << bw) - 1u;
+    int64_t run = 0, s1 = 0;
+    u128 s2 = 0;
+    for (int j = 0; j < 32; j++) {
+        const int64_t m = (int64_t)(__funnelshift_r(cur, nxt, sh) & mask);
+        sh += bw;
+        if (sh >= 32) {
+            sh -= 32;
+            cur = nxt;
+            wi++;
+            nxt = w[wi + 1];
+        }
+        run += ((smask >> j) & 1u) ? -m : m;
+        s1 += run;
+        s2 += (u128)(uint64_t)(run < 0 ? -run : run) * (u128)(uint64_t)(run < 0 ? -run : run);
+    }
+    r.T = run;
+    r.S1 = s1;
+    r.S2 = s2;
+}
+
+__device__ __forceinline__ PrefixMoments prefix_moments(const uint32_t* w, uint32_t rel, bool valid) {
+    PrefixMoments r;
+    const uint32_t bw = valid ? smem_byte(w, rel) : 0u;
+    const uint32_t smask = bw ? smem_u32(w, rel + 1) : 0u;
+    const unsigned act = __activemask();
+    if (__all_sync(act, bw <= 8)) prefix_moments_g<4>(w, rel, bw, smask, r);
+    else if (bw <= 16) prefix_moments_g<2>(w, rel, bw, smask, r);
+    else prefix_moments_wide(w, rel, bw, smask, r);
+    if (!valid) {
+        r.T = 0;
+        r.S1 = 0;
+        r.S2 = 0;
+    }
+    return r;
+}
+
 }  // namespace hszg

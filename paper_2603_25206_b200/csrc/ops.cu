@@ -264,6 +264,165 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_reduce_weighted_fast(const uint
     }
 }
 
+// ---- HSZP variance by tile algebra (stats.py:168-173 sums of q = cumsum(p), compressors.py:212) ----
+// q_i = C_t + L_i inside a 32-chunk warp tile t, C_t = q just before the tile (the exclusive prefix of
+// the tile totals, exact in int32 wrap-around because every q fits int32) and L_i the tile-local prefix.
+//   sum q = sum_t (n_t C_t + sum L),   sum q^2 = sum_t (sum L^2 + 2 C_t sum L + n_t C_t^2)
+// k_hszp_tile_sums decodes each tile once (warp-private TMA tiles, running-prefix chunk moments, a warp
+// scan of the chunk totals) and writes (T_t, sum L, sum L^2); k_hszp_tile_combine scans T_t and folds
+// the algebra in int128.  No look-back chain, q never stored.
+struct HszpTileRec {
+    int64_t T;         // tile total of p
+    int64_t s1;        // sum of the tile-local prefixes L
+    uint64_t s2lo;     // sum L^2 (u128)
+    uint64_t s2hi;
+};
+
+__global__ void __launch_bounds__(256) k_hszp_tile_sums(const uint8_t* __restrict__ payload, uint64_t len,
+                                                        const uint64_t* __restrict__ offsets, int64_t n_chunks,
+                                                        HszpTileRec* rec, uint32_t buf_bytes) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int lane = threadIdx.x & 31;
+    warp_tiles(payload, len, offsets, n_chunks, smem + (threadIdx.x >> 5) * WT_NS * buf_bytes, buf_bytes,
+               wt_bars(smem, buf_bytes), [&](int64_t c, const uint32_t* words, uint32_t rel, bool valid, int32_t) {
+        const PrefixMoments r = prefix_moments(words, rel, valid);
+        int64_t inc = r.T;                                   // warp inclusive scan of the chunk totals
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int64_t o = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += o;
+        }
+        const int64_t E = inc - r.T;                          // chunk offset inside the tile
+        int64_t s1 = 32 * E + r.S1;
+        i128 s2 = (i128)r.S2 + (i128)(2 * E) * (i128)r.S1 + (i128)(32 * E) * (i128)E;
+        if (!valid) {
+            s1 = 0;
+            s2 = 0;
+        }
+        uint64_t lo = (uint64_t)(u128)s2, hi = (uint64_t)((u128)s2 >> 64);
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            s1 += (int64_t)__shfl_down_sync(0xffffffffu, (unsigned long long)s1, d);
+            const uint64_t olo = __shfl_down_sync(0xffffffffu, lo, d), ohi = __shfl_down_sync(0xffffffffu, hi, d);
+            const u128 t = (((u128)hi << 64) | lo) + (((u128)ohi << 64) | olo);
+            lo = (uint64_t)t;
+            hi = (uint64_t)(t >> 64);
+        }
+        const int64_t total = __shfl_sync(0xffffffffu, inc, 31);
+        if (lane == 0) rec[c >> 5] = HszpTileRec{total, s1, lo, hi};
+    });
+}
+
+// Tile combine over NB CTAs: CTA b owns tiles [b*per, (b+1)*per), each thread a contiguous run of them.
+constexpr int HC_THREADS = 256;
+
+__device__ __forceinline__ void hc_range(int64_t tiles, int64_t& t0, int64_t& t1) {
+    const int64_t per = (tiles + gridDim.x - 1) / gridDim.x;
+    const int64_t b0 = blockIdx.x * per, b1 = b0 + per < tiles ? b0 + per : tiles;
+    const int64_t tp = (per + HC_THREADS - 1) / HC_THREADS;
+    t0 = b0 + threadIdx.x * tp;
+    t1 = t0 + tp < b1 ? t0 + tp : b1;
+    if (t0 > b1) t0 = b1;
+}
+
+// phase 1: each CTA's wrap-around sum of its tile totals
+__global__ void __launch_bounds__(HC_THREADS) k_hszp_block_totals(const HszpTileRec* __restrict__ rec, int64_t tiles,
+                                                                  uint32_t* __restrict__ bt) {
+    int64_t t0, t1;
+    hc_range(tiles, t0, t1);
+    uint32_t sum = 0;
+    for (int64_t t = t0; t < t1; t++) sum += (uint32_t)rec[t].T;
+    for (int d = 16; d > 0; d >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, d);
+    __shared__ uint32_t ws[HC_THREADS / 32];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t v = 0;
+        for (int i = 0; i < HC_THREADS / 32; i++) v += ws[i];
+        bt[blockIdx.x] = v;
+    }
+}
+
+// phase 2: carries (exclusive prefix of the CTA totals, then of the threads' runs) and the int128 algebra
+__global__ void __launch_bounds__(HC_THREADS) k_hszp_tile_combine(const HszpTileRec* __restrict__ rec, int64_t tiles,
+                                                                  int64_t n, const uint32_t* __restrict__ bt,
+                                                                  HszgSums* partials) {
+    __shared__ uint32_t s_run[HC_THREADS];
+    __shared__ uint32_t s_base;
+    uint32_t base = 0;
+    for (int i = threadIdx.x; i < (int)blockIdx.x; i += HC_THREADS) base += bt[i];
+    for (int d = 16; d > 0; d >>= 1) base += __shfl_down_sync(0xffffffffu, base, d);
+    if (threadIdx.x == 0) s_base = 0;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) atomicAdd(&s_base, base);
+    int64_t t0, t1;
+    hc_range(tiles, t0, t1);
+    uint32_t sum = 0;
+    for (int64_t t = t0; t < t1; t++) sum += (uint32_t)rec[t].T;
+    s_run[threadIdx.x] = sum;
+    __syncthreads();
+    for (int d = 1; d < HC_THREADS; d <<= 1) {              // inclusive scan (uint32 wrap)
+        const uint32_t v = threadIdx.x >= (unsigned)d ? s_run[threadIdx.x - d] : 0u;
+        __syncthreads();
+        s_run[threadIdx.x] += v;
+        __syncthreads();
+    }
+    uint32_t carry = s_base + s_run[threadIdx.x] - sum;    // q just before this thread's first tile
+    Acc a;
+    a.init();
+    for (int64_t t = t0; t < t1; t++) {
+        const HszpTileRec r = rec[t];
+        const int64_t C = (int32_t)carry;
+        const int64_t nt = (t + 1) * 1024 <= n ? 1024 : n - t * 1024;
+        const i128 L2 = (i128)(((u128)r.s2hi << 64) | r.s2lo);
+        a.s1 += (i128)nt * C + r.s1;
+        a.s2 += L2 + (i128)(2 * C) * (i128)r.s1 + (i128)(nt * C) * (i128)C;
+        carry += (uint32_t)r.T;
+    }
+    block_reduce(a);
+    if (threadIdx.x == 0) {
+        a.count = blockIdx.x ? 0 : n;
+        a.vmin = INT32_MIN;                                   // extrema not computed by this path
+        a.vmax = INT32_MAX;
+        store_sums(partials + blockIdx.x, a);
+    }
+}
+
+// HSZP (full chunks, canonical) sums of q without the scan: 0 = done, 1 = not applicable
+constexpr int HC_BLOCKS = 148 * 4;
+
+size_t hszp_tile_sums_ws(const HszgGeom* g, const HszgStream* s) {
+    if (g->kind != HSZG_HSZP || !s->canonical || g->n_chunks * kChunkCap != g->n) return 0;
+    const int64_t tiles = (g->n_chunks + 31) / 32;
+    return (((size_t)tiles * sizeof(HszpTileRec) + 255) & ~(size_t)255) + HC_BLOCKS * 4 +
+           (size_t)(HC_BLOCKS + 1) * sizeof(HszgSums) + 512;
+}
+
+}  // namespace hszg
+int hszg_finalize_sums(HszgSums* partials, int64_t nparts, HszgSums* out, cudaStream_t st);
+namespace hszg {
+
+int hszp_tile_sums(const HszgGeom* g, const HszgStream* s, HszgSums* out_dev, void* ws, size_t ws_bytes,
+                   cudaStream_t st) {
+    const size_t need = hszp_tile_sums_ws(g, s);
+    if (need == 0 || ws_bytes < need) return 1;
+    const int64_t tiles = (g->n_chunks + 31) / 32;
+    char* w = reinterpret_cast<char*>(ws);
+    HszpTileRec* rec = reinterpret_cast<HszpTileRec*>(w);
+    const size_t ro = ((size_t)tiles * sizeof(HszpTileRec) + 255) & ~(size_t)255;
+    uint32_t* bt = reinterpret_cast<uint32_t*>(w + ro);
+    HszgSums* partials = reinterpret_cast<HszgSums*>(w + ro + ((HC_BLOCKS * 4 + 255) & ~255));
+    size_t sm;
+    uint32_t sb;
+    const unsigned grid = wtile_grid(k_hszp_tile_sums, s->max_bitwidth, g->n_chunks, &sm, &sb);
+    k_hszp_tile_sums<<<grid, 256, sm, st>>>(s->payload, s->payload_len, s->offsets, g->n_chunks, rec, sb);
+    const int nb = (int)(tiles < HC_BLOCKS ? tiles : HC_BLOCKS);
+    k_hszp_block_totals<<<nb, HC_THREADS, 0, st>>>(rec, tiles, bt);
+    k_hszp_tile_combine<<<nb, HC_THREADS, 0, st>>>(rec, tiles, g->n, bt, partials);
+    if (cudaGetLastError() != cudaSuccess) return -1;
+    return ::hszg_finalize_sums(partials, nb, out_dev, st) == HSZG_OK ? 0 : -1;
+}
+
 // ---- K-REG fused from the bytes (HSZX*: regions of q = p + M_b, no reconstruction) -------------
 // Regions tile the box like grid.partition with extents R (a multiple of the block extents B on every
 // axis, so each block lies in exactly one region).  Per chunk: the lean moments of p plus the block

@@ -1235,13 +1235,16 @@ size_t hszg_reduce_ws_bytes(int64_t tiles);
 int hszg_finalize_sums(HszgSums* partials, int64_t nparts, HszgSums* out, cudaStream_t st);
 
 // 0 when the stream has no fused path (see include/hszg.h)
+namespace hszg {
+size_t hszp_tile_sums_ws(const HszgGeom* g, const HszgStream* s);
+int hszp_tile_sums(const HszgGeom* g, const HszgStream* s, HszgSums* out_dev, void* ws, size_t ws_bytes,
+                   cudaStream_t st);
+}  // namespace hszg
+
 size_t hszg_quantized_sums_ws(const HszgGeom* g, const HszgStream* s) {
     if (!s || !s->canonical || g->n == 0) return 0;
+    if (const size_t t = hszg::hszp_tile_sums_ws(g, s)) return t;          // HSZP: tile algebra (ops.cu)
     const SegGeo sg = make_seggeo(*g);
-    if (g->kind == HSZG_HSZP && g->n_chunks * kChunkCap == g->n) {
-        const int64_t tiles = (g->n_chunks + TILE_CHUNKS - 1) / TILE_CHUNKS;
-        return lookback_ws_bytes(g->n_chunks) + hszg_reduce_ws_bytes(tiles) + 256;
-    }
     if (g->kind == HSZG_HSZP_ND && g->ndims == 3 && sg.n[2] % 32 == 0 && sg.n[2] <= 4096 && sg.n[0] <= 65535 &&
         recon_band_rows(sg.n[0], sg.n[1], sg.n[2]) >= sg.n[1]) {
         const int64_t Lc = sg.n[1] * sg.n[2];
@@ -1262,17 +1265,13 @@ extern "C" int hszg_quantized_sums(const HszgGeom* g, const HszgStream* s, HszgS
     }
     const SegGeo sg = make_seggeo(*g);
     char* w = reinterpret_cast<char*>(ws);
-    if (g->kind == HSZG_HSZP) {
-        const int64_t tiles = (g->n_chunks + TILE_CHUNKS - 1) / TILE_CHUNKS;
-        LBState lb = lookback_carve(ws, tiles);
-        HszgSums* partials = reinterpret_cast<HszgSums*>(w + ((lookback_ws_bytes(g->n_chunks) + 255) & ~(size_t)255));
-        cudaMemsetAsync(ws, 0, lookback_clear_bytes(tiles), st);
-        const size_t fsmem = kFastTileBytes + stage_bytes(s->max_bitwidth);
-        allow_smem(k_tile_scan_fast<int32_t>, fsmem);
-        k_tile_scan_fast<int32_t><<<(unsigned)tiles, TILE_CHUNKS, fsmem, st>>>(
-            s->payload, s->payload_len, s->offsets, g->n_chunks, lb, 0.0, nullptr, partials);
-        HSZG_CHECK_LAUNCH("quantized sums hszp");
-        return hszg_finalize_sums(partials, tiles, out_dev, st);
+    if (g->kind == HSZG_HSZP && hszg::hszp_tile_sums_ws(g, s)) {
+        if (hszg::hszp_tile_sums(g, s, out_dev, ws, ws_bytes, st)) {
+            err->status = HSZG_CUDA;
+            snprintf(err->message, sizeof(err->message), "quantized sums hszp: launch failed");
+            return HSZG_CUDA;
+        }
+        return HSZG_OK;
     }
     // HSZP_ND 3-D, one band per plane
     int32_t* L = reinterpret_cast<int32_t*>(w);

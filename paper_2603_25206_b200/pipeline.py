@@ -165,7 +165,12 @@ def exclusive_plane_prefix(planes, rank: int):
     import torch
 
     acc = torch.zeros_like(planes[0])
-    for g in range(rank):
+    if acc.is_cuda:                          # one wrap-around int32 add kernel per lower rank (hszg_add_plane)
+        for g in range(rank):
+            src = planes[g].contiguous()
+            _lib.call("hszg_add_plane", _lib.ptr(acc), _lib.ptr(src), acc.numel(), acc.numel(), _lib.stream_handle())
+        return acc
+    for g in range(rank):                    # host tensors (gloo CPU tests): the same arithmetic in int64
         acc = (acc.to(torch.int64) + planes[g].to(torch.int64)).remainder(2**32)
         acc = torch.where(acc >= 2**31, acc - 2**32, acc).to(planes[0].dtype)
     return acc
