@@ -78,7 +78,13 @@ extern "C" size_t hszg_workspace_bytes(const HszgGeom* g, const HszgStream* s, i
             const SegGeo sg = make_seggeo(*g);
             const bool fused = canonical && (g->kind == HSZG_HSZX || g->kind == HSZG_HSZP ||
                                              (g->kind == HSZG_HSZX_ND && sg.cpb[0] <= TILE_CHUNKS));
-            if (fused) return lookback_ws_bytes(g->n_chunks) + 256;
+            if (fused) {
+                // HSZP: the tile carries of the three-pass scan (recon.cu) or the look-back state
+                const int64_t tiles = (g->n_chunks + 31) / 32;
+                const size_t a = lookback_ws_bytes(g->n_chunks);
+                const size_t b = (((size_t)tiles * 4 + 255) & ~(size_t)255) + 148 * 4 * 4 + 256;
+                return (a > b ? a : b) + 256;
+            }
             if (canonical && g->kind == HSZG_HSZP_ND && g->ndims == 3)   // band-scan path: band totals
             {
                 const int64_t br = recon_band_rows(g->dims[0], g->dims[1], g->dims[2]);

@@ -18,6 +18,7 @@
 #include "tile.cuh"
 #include "lookback.cuh"
 #include "wtiles.cuh"
+#include "moments.cuh"
 
 extern "C" int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t band_rows, void* L, int32_t* A,
                               int32_t* strip_edges, int l_int16, int32_t* l_overflow, int ctas_per_sm, void* stream,
@@ -580,6 +581,153 @@ static int ilog2_exact(int64_t v) {
     return -1;
 }
 
+// ---- HSZP stage 3 / 4 in three passes over warp tiles (compressors.py:212, the flat inclusive cumsum) ----
+// (1) k_hszp_tile_totals: the wrap-around total of p over each 32-chunk tile (lean chunk sums);
+// (2) k_hszp_carries: C_t = exclusive prefix of the tile totals (uint32 wrap-around is exact: every q
+//     fits int32), two multi-CTA passes; (3) k_wt_prefix_stream: decode with the in-chunk prefix into the
+// warp's shared tile, add C_t + the chunk's offset in the tile (warp scan), coalesced 16-B stores.  No
+// look-back chain: every tile is independent once the carries are known.
+__global__ void __launch_bounds__(256) k_hszp_tile_totals(const uint8_t* __restrict__ payload, uint64_t len,
+                                                          const uint64_t* __restrict__ offsets, int64_t n_chunks,
+                                                          uint32_t* __restrict__ tot, uint32_t sb) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int lane = threadIdx.x & 31;
+    warp_tiles(payload, len, offsets, n_chunks, smem + (threadIdx.x >> 5) * WT_NS * sb, sb, wt_bars(smem, sb),
+               [&](int64_t c, const uint32_t* words, uint32_t rel, bool valid, int32_t) {
+        uint32_t t = (uint32_t)chunk_moments<false, false>(words, rel, valid).sp;
+        for (int d = 16; d > 0; d >>= 1) t += __shfl_down_sync(0xffffffffu, t, d);
+        if (lane == 0) tot[c >> 5] = t;
+    });
+}
+
+constexpr int HCS_THREADS = 256;
+constexpr int HCS_BLOCKS = 148 * 4;
+
+__device__ __forceinline__ void hcs_range(int64_t tiles, int64_t& t0, int64_t& t1) {
+    const int64_t per = (tiles + gridDim.x - 1) / gridDim.x;
+    const int64_t b0 = blockIdx.x * per, b1 = b0 + per < tiles ? b0 + per : tiles;
+    const int64_t tp = (per + HCS_THREADS - 1) / HCS_THREADS;
+    t0 = b0 + threadIdx.x * tp;
+    t1 = t0 + tp < b1 ? t0 + tp : b1;
+    if (t0 > b1) t0 = b1;
+}
+
+__global__ void __launch_bounds__(HCS_THREADS) k_hszp_carry_blocks(const uint32_t* __restrict__ tot, int64_t tiles,
+                                                                   uint32_t* __restrict__ bt) {
+    int64_t t0, t1;
+    hcs_range(tiles, t0, t1);
+    uint32_t sum = 0;
+    for (int64_t t = t0; t < t1; t++) sum += tot[t];
+    for (int d = 16; d > 0; d >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, d);
+    __shared__ uint32_t ws[HCS_THREADS / 32];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t v = 0;
+        for (int i = 0; i < HCS_THREADS / 32; i++) v += ws[i];
+        bt[blockIdx.x] = v;
+    }
+}
+
+// in place: tot[t] -> C_t (exclusive prefix)
+__global__ void __launch_bounds__(HCS_THREADS) k_hszp_carries(uint32_t* __restrict__ tot, int64_t tiles,
+                                                              const uint32_t* __restrict__ bt) {
+    __shared__ uint32_t s_run[HCS_THREADS];
+    __shared__ uint32_t s_base;
+    uint32_t base = 0;
+    for (int i = threadIdx.x; i < (int)blockIdx.x; i += HCS_THREADS) base += bt[i];
+    for (int d = 16; d > 0; d >>= 1) base += __shfl_down_sync(0xffffffffu, base, d);
+    if (threadIdx.x == 0) s_base = 0;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) atomicAdd(&s_base, base);
+    int64_t t0, t1;
+    hcs_range(tiles, t0, t1);
+    uint32_t sum = 0;
+    for (int64_t t = t0; t < t1; t++) sum += tot[t];
+    s_run[threadIdx.x] = sum;
+    __syncthreads();
+    for (int d = 1; d < HCS_THREADS; d <<= 1) {
+        const uint32_t v = threadIdx.x >= (unsigned)d ? s_run[threadIdx.x - d] : 0u;
+        __syncthreads();
+        s_run[threadIdx.x] += v;
+        __syncthreads();
+    }
+    uint32_t carry = s_base + s_run[threadIdx.x] - sum;
+    for (int64_t t = t0; t < t1; t++) {
+        const uint32_t v = tot[t];
+        tot[t] = carry;
+        carry += v;
+    }
+}
+
+struct CarryAux {      // the tile carry of chunk c (tile = 32 chunks)
+    const uint32_t* C;
+    __device__ __forceinline__ int32_t operator()(int64_t c) const { return (int32_t)__ldg(C + (c >> 5)); }
+};
+
+template <typename OutT>
+__global__ void __launch_bounds__(256) k_wt_prefix_stream(const uint8_t* __restrict__ payload, uint64_t len,
+                                                          const uint64_t* __restrict__ offsets, int64_t n_chunks,
+                                                          CarryAux aux, double two_eps, OutT* __restrict__ out,
+                                                          uint32_t sb) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int lane = threadIdx.x & 31;
+    int32_t* tile = reinterpret_cast<int32_t*>(wt_scratch(smem, sb, WS_TILE_BYTES));
+    warp_tiles(payload, len, offsets, n_chunks, smem + (threadIdx.x >> 5) * WT_NS * sb, sb, wt_bars(smem, sb),
+               [&](int64_t c, const uint32_t* words, uint32_t rel, bool valid, int32_t C) {
+        uint32_t run = 0;
+        if (valid) run = decode32<true>(words, rel, tile + lane * kChunkStride, 0);
+        uint32_t inc = run;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += o;
+        }
+        const uint32_t add = (uint32_t)C + inc - run;
+        const int64_t c0 = c - lane;
+        const int nv = n_chunks - c0 < 32 ? (int)(n_chunks - c0) : 32;
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const int idx = 128 * i + 4 * lane;
+            const uint32_t a = __shfl_sync(0xffffffffu, add, idx >> 5);
+            if ((idx >> 5) < nv) {
+                const int4 v = *reinterpret_cast<const int4*>(tile + (idx >> 5) * kChunkStride + (idx & 31));
+                store4<OutT>(out + c0 * kChunkCap + idx,
+                             make_int4((int)((uint32_t)v.x + a), (int)((uint32_t)v.y + a), (int)((uint32_t)v.z + a),
+                                       (int)((uint32_t)v.w + a)),
+                             two_eps);
+            }
+        }
+        __syncwarp();
+    }, aux);
+}
+
+inline size_t hszp_prefix_ws(int64_t n_chunks) {
+    const int64_t tiles = (n_chunks + 31) / 32;
+    return (((size_t)tiles * 4 + 255) & ~(size_t)255) + HCS_BLOCKS * 4 + 256;
+}
+
+template <typename OutT>
+static bool launch_hszp_prefix(const HszgGeom* g, const HszgStream* s, OutT* out, void* ws, size_t ws_bytes,
+                               cudaStream_t st) {
+    if (ws_bytes < hszp_prefix_ws(g->n_chunks)) return false;
+    const int64_t tiles = (g->n_chunks + 31) / 32;
+    uint32_t* tot = reinterpret_cast<uint32_t*>(ws);
+    uint32_t* bt = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(ws) + (((size_t)tiles * 4 + 255) & ~(size_t)255));
+    size_t sm;
+    uint32_t sb;
+    unsigned grid = wtile_grid(k_hszp_tile_totals, s->max_bitwidth, g->n_chunks, &sm, &sb);
+    k_hszp_tile_totals<<<grid, 256, sm, st>>>(s->payload, s->payload_len, s->offsets, g->n_chunks, tot, sb);
+    const int nb = (int)(tiles < HCS_BLOCKS ? tiles : HCS_BLOCKS);
+    k_hszp_carry_blocks<<<nb, HCS_THREADS, 0, st>>>(tot, tiles, bt);
+    k_hszp_carries<<<nb, HCS_THREADS, 0, st>>>(tot, tiles, bt);
+    grid = wtile_grid(k_wt_prefix_stream<OutT>, s->max_bitwidth, g->n_chunks, &sm, &sb, WS_TILE_BYTES);
+    k_wt_prefix_stream<OutT><<<grid, 256, sm, st>>>(s->payload, s->payload_len, s->offsets, g->n_chunks,
+                                                    CarryAux{tot}, 2.0 * g->eps, out, sb);
+    return true;
+}
+
 template <int Mode, typename OutT>
 static void launch_stream_full(const HszgGeom* g, const HszgStream* s, const SegGeo& sg, OutT* out, cudaStream_t st) {
     static const char* wtb = getenv("HSZG_STREAM");
@@ -1042,6 +1190,11 @@ static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, 
             }
             break;
         case HSZG_HSZP:
+            if (fast && g->n_chunks * kChunkCap == g->n && (reinterpret_cast<uintptr_t>(out) & 15) == 0 && !sf_off() &&
+                launch_hszp_prefix<OutT>(g, s, out, ws, ws_bytes, st)) {
+                HSZG_CHECK_LAUNCH("reconstruct hszp");
+                return HSZG_OK;
+            }
             if (fast) {
                 if (ws_bytes < lookback_ws_bytes(g->n_chunks)) break;
                 LBState lb = lookback_carve(ws, tiles);
