@@ -155,6 +155,7 @@ __device__ __forceinline__ ChunkMoments chunk_moments(const uint32_t* w, uint32_
 struct PrefixMoments {
     int64_t T, S1;
     u128 S2;
+    int64_t mn, mx;      // min / max of the l_k
 };
 
 template <int G>
@@ -165,7 +166,7 @@ __device__ __forceinline__ void prefix_moments_g(const uint32_t* w, uint32_t rel
     uint32_t cur = w[wi], nxt = w[wi + 1];
     const uint32_t mask = (1u << bw) - 1u;
     const uint32_t adv = (uint32_t)G * bw;
-    int32_t run = 0, s1 = 0;
+    int32_t run = 0, s1 = 0, mn = INT32_MAX, mx = INT32_MIN;
     uint64_t s2 = 0;
 #pragma unroll
     for (int k = 0; k < 32 / G; k++) {
@@ -177,6 +178,8 @@ __device__ __forceinline__ void prefix_moments_g(const uint32_t* w, uint32_t rel
             run += ((smask >> j) & 1u) ? -m : m;
             s1 += run;
             s2 += (uint64_t)((int64_t)run * run);
+            mn = min(mn, run);
+            mx = max(mx, run);
         }
         if (k + 1 < 32 / G) {
             sh += adv;
@@ -191,6 +194,8 @@ __device__ __forceinline__ void prefix_moments_g(const uint32_t* w, uint32_t rel
     r.T = run;
     r.S1 = s1;
     r.S2 = s2;
+    r.mn = mn;
+    r.mx = mx;
 }
 
 __device__ __forceinline__ void prefix_moments_wide(const uint32_t* w, uint32_t rel, uint32_t bw, uint32_t smask,
@@ -199,7 +204,7 @@ __device__ __forceinline__ void prefix_moments_wide(const uint32_t* w, uint32_t 
     uint32_t wi = bitpos >> 5, sh = bitpos & 31;
     uint32_t cur = w[wi], nxt = w[wi + 1];
     const uint32_t mask = bw >= 32 ? 0xffffffffu : (1u << bw) - 1u;
-    int64_t run = 0, s1 = 0;
+    int64_t run = 0, s1 = 0, mn = INT64_MAX, mx = INT64_MIN;
     u128 s2 = 0;
     for (int j = 0; j < 32; j++) {
         const int64_t m = (int64_t)(__funnelshift_r(cur, nxt, sh) & mask);
@@ -213,10 +218,14 @@ __device__ __forceinline__ void prefix_moments_wide(const uint32_t* w, uint32_t 
         run += ((smask >> j) & 1u) ? -m : m;
         s1 += run;
         s2 += (u128)(uint64_t)(run < 0 ? -run : run) * (u128)(uint64_t)(run < 0 ? -run : run);
+        mn = min(mn, run);
+        mx = max(mx, run);
     }
     r.T = run;
     r.S1 = s1;
     r.S2 = s2;
+    r.mn = mn;
+    r.mx = mx;
 }
 
 __device__ __forceinline__ PrefixMoments prefix_moments(const uint32_t* w, uint32_t rel, bool valid) {
@@ -231,6 +240,8 @@ __device__ __forceinline__ PrefixMoments prefix_moments(const uint32_t* w, uint3
         r.T = 0;
         r.S1 = 0;
         r.S2 = 0;
+        r.mn = INT64_MAX;
+        r.mx = INT64_MIN;
     }
     return r;
 }

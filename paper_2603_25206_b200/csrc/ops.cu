@@ -276,6 +276,7 @@ struct HszpTileRec {
     int64_t s1;        // sum of the tile-local prefixes L
     uint64_t s2lo;     // sum L^2 (u128)
     uint64_t s2hi;
+    int64_t mn, mx;    // min / max of L (q = C_t + L: the extrema of q follow in the combine)
 };
 
 __global__ void __launch_bounds__(256) k_hszp_tile_sums(const uint8_t* __restrict__ payload, uint64_t len,
@@ -295,9 +296,12 @@ __global__ void __launch_bounds__(256) k_hszp_tile_sums(const uint8_t* __restric
         const int64_t E = inc - r.T;                          // chunk offset inside the tile
         int64_t s1 = 32 * E + r.S1;
         i128 s2 = (i128)r.S2 + (i128)(2 * E) * (i128)r.S1 + (i128)(32 * E) * (i128)E;
+        int64_t mn = E + r.mn, mx = E + r.mx;
         if (!valid) {
             s1 = 0;
             s2 = 0;
+            mn = INT64_MAX;
+            mx = INT64_MIN;
         }
         uint64_t lo = (uint64_t)(u128)s2, hi = (uint64_t)((u128)s2 >> 64);
 #pragma unroll
@@ -307,9 +311,11 @@ __global__ void __launch_bounds__(256) k_hszp_tile_sums(const uint8_t* __restric
             const u128 t = (((u128)hi << 64) | lo) + (((u128)ohi << 64) | olo);
             lo = (uint64_t)t;
             hi = (uint64_t)(t >> 64);
+            mn = min(mn, (int64_t)__shfl_down_sync(0xffffffffu, (unsigned long long)mn, d));
+            mx = max(mx, (int64_t)__shfl_down_sync(0xffffffffu, (unsigned long long)mx, d));
         }
         const int64_t total = __shfl_sync(0xffffffffu, inc, 31);
-        if (lane == 0) rec[c >> 5] = HszpTileRec{total, s1, lo, hi};
+        if (lane == 0) rec[c >> 5] = HszpTileRec{total, s1, lo, hi, mn, mx};
     });
 }
 
@@ -377,13 +383,13 @@ __global__ void __launch_bounds__(HC_THREADS) k_hszp_tile_combine(const HszpTile
         const i128 L2 = (i128)(((u128)r.s2hi << 64) | r.s2lo);
         a.s1 += (i128)nt * C + r.s1;
         a.s2 += L2 + (i128)(2 * C) * (i128)r.s1 + (i128)(nt * C) * (i128)C;
+        a.vmin = min(a.vmin, (int32_t)(C + r.mn));            // every q fits int32
+        a.vmax = max(a.vmax, (int32_t)(C + r.mx));
         carry += (uint32_t)r.T;
     }
     block_reduce(a);
     if (threadIdx.x == 0) {
         a.count = blockIdx.x ? 0 : n;
-        a.vmin = INT32_MIN;                                   // extrema not computed by this path
-        a.vmax = INT32_MAX;
         store_sums(partials + blockIdx.x, a);
     }
 }
@@ -1381,7 +1387,9 @@ __device__ __forceinline__ void st4(double* o, int64_t i, const double* v) {
     __stcs(reinterpret_cast<double2*>(o + i + 2), make_double2(v[2], v[3]));
 }
 
-template <int OP, int ND, typename OutT>
+// FD: float-domain input (stage 4: q read as fl(q * 2eps)) — a template parameter so the integer
+// (stage 2/3) kernels carry no float-domain code (they were issue-bound on it: 81% issue slots)
+template <int OP, int ND, typename OutT, bool FD>
 __global__ void __launch_bounds__(SV_THREADS) k_stencil_v4(StencilArgs A, int zc, int64_t zend) {
     const int lane = threadIdx.x & 31;
     const int64_t xi0 = ((int64_t)blockIdx.x * SV_THREADS + threadIdx.x) * 4;
@@ -1395,7 +1403,7 @@ __global__ void __launch_bounds__(SV_THREADS) k_stencil_v4(StencilArgs A, int zc
     p.yin = y > 0 && y < n1 - 1;
     p.x0 = xi == 0;
     p.xl = xi + 3 >= n2 - 1;
-    const bool fd = A.float_domain == 1;
+    constexpr bool fd = FD;
     constexpr int a0 = 3 - ND;                        // box axis of original axis 0
     constexpr int NC = (OP == HSZG_OP_DIVERGENCE || OP == HSZG_OP_CURL) ? ND : 1;
     const int4 z4 = make_int4(0, 0, 0, 0);
@@ -1520,23 +1528,31 @@ __global__ void __launch_bounds__(SV_THREADS) k_stencil_v4(StencilArgs A, int zc
     }   // z
 }
 
-template <int ND, typename OutT>
-static void launch_sv4(const StencilArgs& A, dim3 grid, int zc, int64_t zend, cudaStream_t st) {
+template <int ND, typename OutT, bool FD>
+static void launch_sv4_fd(const StencilArgs& A, dim3 grid, int zc, int64_t zend, cudaStream_t st) {
     switch (A.op) {
-        case HSZG_OP_DERIV: k_stencil_v4<HSZG_OP_DERIV, ND, OutT><<<grid, SV_THREADS, 0, st>>>(A, zc, zend); break;
+        case HSZG_OP_DERIV: k_stencil_v4<HSZG_OP_DERIV, ND, OutT, FD><<<grid, SV_THREADS, 0, st>>>(A, zc, zend); break;
         case HSZG_OP_LAPLACIAN:
-            k_stencil_v4<HSZG_OP_LAPLACIAN, ND, OutT><<<grid, SV_THREADS, 0, st>>>(A, zc, zend);
+            k_stencil_v4<HSZG_OP_LAPLACIAN, ND, OutT, FD><<<grid, SV_THREADS, 0, st>>>(A, zc, zend);
             break;
         case HSZG_OP_GRAD_LAP:
-            k_stencil_v4<HSZG_OP_GRAD_LAP, ND, OutT><<<grid, SV_THREADS, 0, st>>>(A, zc, zend);
+            k_stencil_v4<HSZG_OP_GRAD_LAP, ND, OutT, FD><<<grid, SV_THREADS, 0, st>>>(A, zc, zend);
             break;
-        case HSZG_OP_GRADMAG: k_stencil_v4<HSZG_OP_GRADMAG, ND, OutT><<<grid, SV_THREADS, 0, st>>>(A, zc, zend); break;
+        case HSZG_OP_GRADMAG:
+            k_stencil_v4<HSZG_OP_GRADMAG, ND, OutT, FD><<<grid, SV_THREADS, 0, st>>>(A, zc, zend);
+            break;
         case HSZG_OP_DIVERGENCE:
-            k_stencil_v4<HSZG_OP_DIVERGENCE, ND, OutT><<<grid, SV_THREADS, 0, st>>>(A, zc, zend);
+            k_stencil_v4<HSZG_OP_DIVERGENCE, ND, OutT, FD><<<grid, SV_THREADS, 0, st>>>(A, zc, zend);
             break;
-        case HSZG_OP_CURL: k_stencil_v4<HSZG_OP_CURL, ND, OutT><<<grid, SV_THREADS, 0, st>>>(A, zc, zend); break;
+        case HSZG_OP_CURL: k_stencil_v4<HSZG_OP_CURL, ND, OutT, FD><<<grid, SV_THREADS, 0, st>>>(A, zc, zend); break;
         default: break;
     }
+}
+
+template <int ND, typename OutT>
+static void launch_sv4(const StencilArgs& A, dim3 grid, int zc, int64_t zend, cudaStream_t st) {
+    if (A.float_domain == 1) launch_sv4_fd<ND, OutT, true>(A, grid, zc, zend, st);
+    else launch_sv4_fd<ND, OutT, false>(A, grid, zc, zend, st);
 }
 
 }  // namespace hszg
