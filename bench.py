@@ -384,12 +384,21 @@ def run_ours(args):
     # ---- per-row table (SURVEY §8(a) rows on configs 1-4; N = 1, after the headline's buffers are freed) --
     rows = None
     if world == 1 and args.rows:
-        import bench_rows
+        # in a child process: a CUPTI session there starts clean (this process's earlier profiler sessions
+        # and graph replays made later sessions drop kernel records)
+        import tempfile
 
         del outs, pipes, shards
         torch.cuda.empty_cache()
-        rows = bench_rows.measure(args.rows, cpu=not args.no_cpu, peak=peak,
-                                  log=lambda m: print(m, file=sys.stderr, flush=True))
+        with tempfile.NamedTemporaryFile(suffix=".json") as tf:
+            cmd = [sys.executable, os.path.join(ROOT, "bench_rows.py"), "--configs", *map(str, args.rows),
+                   "--out", tf.name] + (["--no-cpu"] if args.no_cpu else [])
+            r = subprocess.run(cmd, stdout=sys.stderr, stderr=sys.stderr)
+            if r.returncode == 0:
+                with open(tf.name) as fh:
+                    rows = json.load(fh)
+            else:
+                rows = {"error": f"bench_rows.py exited {r.returncode}"}
 
     if rank == 0:
         s = results
