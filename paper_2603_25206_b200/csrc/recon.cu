@@ -15,6 +15,7 @@
 // result back to int32, compressors.py:226).
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 #include "tile.cuh"
 #include "lookback.cuh"
 #include "wtiles.cuh"
@@ -868,10 +869,98 @@ __global__ void k_col_scan_bands(const int32_t* src, const int32_t* __restrict__
     const int64_t y = l / n2, x = l - y * n2;
     const int32_t* a = A + (y / BR) * n2 + x;
     const int64_t as = nb * n2;
+    const int32_t* s = src + l;
+    OutT* d = dst + l;
     uint32_t acc = 0;
-    for (int64_t m = 0; m < M; m++) {      // src may be dst: each element is read before it is written
-        acc += (uint32_t)src[m * Lc + l] + (uint32_t)__ldg(a + m * as);
-        dst[m * Lc + l] = Conv<OutT>::go((int32_t)acc, two_eps);
+    int64_t m = 0;
+    // src may be dst, but every element is read once, by the thread that later overwrites it, so the
+    // non-coherent path is safe and frees the compiler to batch the loads across the stores
+    for (; m + 8 <= M; m += 8) {
+        uint32_t v[8], o[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            v[k] = (uint32_t)__ldg(s + (m + k) * Lc);
+            o[k] = (uint32_t)__ldg(a + (m + k) * as);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            acc += v[k] + o[k];
+            d[(m + k) * Lc] = Conv<OutT>::go((int32_t)acc, two_eps);
+        }
+    }
+    for (; m < M; m++) {
+        acc += (uint32_t)s[m * Lc] + (uint32_t)__ldg(a + m * as);
+        d[m * Lc] = Conv<OutT>::go((int32_t)acc, two_eps);
+    }
+}
+
+// Vectorised z prefix (Lc % 4 == 0, 16-byte aligned planes): four adjacent columns per thread, so a
+// warp reads 512 contiguous bytes per plane instead of 128 — fewer, longer DRAM bursts for the
+// plane-strided walk.  A (optional) = the band offsets of k_col_scan_bands.  src may be dst: every
+// element is read once, by the thread that later overwrites it, so the non-coherent path is safe.
+template <typename OutT>
+__device__ __forceinline__ void store4(OutT* d, const uint32_t (&v)[4], double two_eps) {
+    if constexpr (sizeof(OutT) == 4) {
+        typedef typename std::conditional<std::is_same<OutT, float>::value, float4, int4>::type V4;
+        V4 o;
+        o.x = Conv<OutT>::go((int32_t)v[0], two_eps);
+        o.y = Conv<OutT>::go((int32_t)v[1], two_eps);
+        o.z = Conv<OutT>::go((int32_t)v[2], two_eps);
+        o.w = Conv<OutT>::go((int32_t)v[3], two_eps);
+        *reinterpret_cast<V4*>(d) = o;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; j += 2)
+            *reinterpret_cast<double2*>(d + j) =
+                make_double2(Conv<OutT>::go((int32_t)v[j], two_eps), Conv<OutT>::go((int32_t)v[j + 1], two_eps));
+    }
+}
+
+template <typename OutT, bool BANDS>
+__global__ void __launch_bounds__(256) k_col_scan_v4(const int32_t* src, const int32_t* __restrict__ A, int64_t M,
+                                                     int64_t n1, int64_t n2, int64_t BR, int64_t nb, double two_eps,
+                                                     OutT* dst) {
+    const int64_t Lc = n1 * n2;
+    const int64_t l = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+    if (l >= Lc) return;
+    const int32_t* s = src + l;
+    OutT* d = dst + l;
+    const int32_t* a = A;
+    int64_t as = 0;
+    if constexpr (BANDS) {
+        const int64_t y = l / n2, x = l - y * n2;
+        a = A + (y / BR) * n2 + x;
+        as = nb * n2;
+    }
+    uint32_t acc[4] = {0, 0, 0, 0};
+    constexpr int U = 4;
+    int64_t m = 0;
+    for (; m + U <= M; m += U) {
+        int4 v[U], o[U];
+#pragma unroll
+        for (int k = 0; k < U; k++) {
+            v[k] = __ldg(reinterpret_cast<const int4*>(s + (m + k) * Lc));
+            if constexpr (BANDS) o[k] = __ldg(reinterpret_cast<const int4*>(a + (m + k) * as));
+            else o[k] = make_int4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int k = 0; k < U; k++) {
+            acc[0] += (uint32_t)v[k].x + (uint32_t)o[k].x;
+            acc[1] += (uint32_t)v[k].y + (uint32_t)o[k].y;
+            acc[2] += (uint32_t)v[k].z + (uint32_t)o[k].z;
+            acc[3] += (uint32_t)v[k].w + (uint32_t)o[k].w;
+            store4<OutT>(d + (m + k) * Lc, acc, two_eps);
+        }
+    }
+    for (; m < M; m++) {
+        const int4 v = __ldg(reinterpret_cast<const int4*>(s + m * Lc));
+        int4 o = make_int4(0, 0, 0, 0);
+        if constexpr (BANDS) o = __ldg(reinterpret_cast<const int4*>(a + m * as));
+        acc[0] += (uint32_t)v.x + (uint32_t)o.x;
+        acc[1] += (uint32_t)v.y + (uint32_t)o.y;
+        acc[2] += (uint32_t)v.z + (uint32_t)o.z;
+        acc[3] += (uint32_t)v.w + (uint32_t)o.w;
+        store4<OutT>(d + m * Lc, acc, two_eps);
     }
 }
 
@@ -1146,10 +1235,19 @@ static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, 
                     int32_t* A = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ws) + (sizeof(OutT) == 4 ? 0 : n4));
                     const int rr = hszg_band_scan(g, s, br, buf, A, nullptr, 0, nullptr, 0, st, err);
                     if (rr) return rr;
-                    if (nb == 1) {          // one band per plane: A holds zeros, the plain z prefix
+                    const int64_t Lc = sg.n[1] * sg.n[2];
+                    static const int v4 = getenv("HSZG_COLSCAN_V4") ? atoi(getenv("HSZG_COLSCAN_V4")) : 1;
+                    if (v4) {               // n2 % 32 == 0: whole int4 groups, 16-byte aligned planes
+                        const unsigned blocks = (unsigned)((Lc / 4 + 255) / 256);
+                        if (nb == 1)
+                            k_col_scan_v4<OutT, false><<<blocks, 256, 0, st>>>(buf, nullptr, sg.n[0], sg.n[1], sg.n[2],
+                                                                               br, nb, two_eps, out);
+                        else
+                            k_col_scan_v4<OutT, true><<<blocks, 256, 0, st>>>(buf, A, sg.n[0], sg.n[1], sg.n[2], br,
+                                                                              nb, two_eps, out);
+                    } else if (nb == 1) {   // one band per plane: A holds zeros, the plain z prefix
                         launch_col_scan<OutT>(buf, 1, sg.n[0], sg.n[1] * sg.n[2], two_eps, out, st);
                     } else {
-                        const int64_t Lc = sg.n[1] * sg.n[2];
                         k_col_scan_bands<OutT><<<(unsigned)((Lc + 255) / 256), 256, 0, st>>>(
                             buf, A, sg.n[0], sg.n[1], sg.n[2], br, nb, two_eps, out);
                     }

@@ -11,6 +11,7 @@
 // with coalesced stores.
 #pragma once
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 #include "common.cuh"
@@ -62,6 +63,10 @@ inline void allow_smem(K kernel, size_t bytes) {
 // enough for two waves of band-scan CTAs (then the z prefix needs no band offsets, which cost it
 // ~60% more time); otherwise whole 256-chunk tiles and >= 16 bands-x-planes per SM.
 inline int64_t recon_band_rows(int64_t n0, int64_t n1, int64_t n2) {
+    if (const char* e = getenv("HSZG_RECON_BR")) {       // A/B runs: force the band height
+        const int64_t v = atoll(e);
+        if (v > 0) return v < n1 ? v : n1;
+    }
     if (n0 >= 2 * 148) return n1 > 0 ? n1 : 1;
     const int64_t cpr = n2 / 32 > 0 ? n2 / 32 : 1;
     const int64_t rpt = TILE_CHUNKS / cpr > 0 ? TILE_CHUNKS / cpr : 1;
