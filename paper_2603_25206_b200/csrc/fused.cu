@@ -280,7 +280,13 @@ __global__ void __launch_bounds__(FX_T, 1) k_fused_blocks(FxArgs a, uint32_t buf
     };
     wait_full(zb - 1);
     wait_full(zb);
-    for (int64_t z = zb; z < ze; z++) {
+    // loop-invariant parts hoisted: output offset = z * plane + (y * n2 + x)
+    const int64_t ybase = y0 + FX_RPW * cw;
+    const int64_t rowoff = ybase * a.n2 + x;
+    const int so0 = (FX_RPW * cw + 1) * FX_RW + FX_X0 + 4 * lane;
+    const int eo = lane == 0 ? -1 : 4;                            // lane 0: column x0-1; lane 31: x0+128
+    int64_t zoff = zb * plane;
+    for (int64_t z = zb; z < ze; z++, zoff += plane) {
         wait_full(z + 1);
         const int32_t* Pm = Q + (int)((z - 1) & (NPL - 1)) * FX_PLANE;
         const int32_t* Pc = Q + (int)(z & (NPL - 1)) * FX_PLANE;
@@ -290,20 +296,21 @@ __global__ void __launch_bounds__(FX_T, 1) k_fused_blocks(FxArgs a, uint32_t buf
 #pragma unroll
         for (int k = 0; k < FX_RPW; k++) {
             const int r = FX_RPW * cw + k;                        // output row within the CTA
-            const int64_t y = y0 + r;
-            const int so = (r + 1) * FX_RW + FX_X0 + 4 * lane;
+            const int64_t y = ybase + k;
+            const int so = so0 + k * FX_RW;
             const int4 c = *reinterpret_cast<const int4*>(Pc + so);
+            const int e = Pc[so + eo];                            // every lane loads: no branch
             int left = __shfl_up_sync(0xffffffffu, c.w, 1);
             int right = __shfl_down_sync(0xffffffffu, c.x, 1);
-            if (lane == 0) left = Pc[so - 1];
-            if (lane == 31) right = Pc[so + 4];
+            left = lane == 0 ? e : left;
+            right = lane == 31 ? e : right;
             if (r < 8 * nby && x < a.n2) {
                 const bool yin = y > 0 && y < a.n1 - 1;
                 const int4 ym = *reinterpret_cast<const int4*>(Pc + so - FX_RW);
                 const int4 yp = *reinterpret_cast<const int4*>(Pc + so + FX_RW);
                 const int4 zm = *reinterpret_cast<const int4*>(Pm + so);
                 const int4 zp = *reinterpret_cast<const int4*>(Pp + so);
-                const int64_t o = z * plane + y * a.n2 + x;
+                const int64_t o = zoff + rowoff + k * a.n2;
                 if (Exact)
                     emit4(a.o0, a.o1, a.o2, a.o3, o, zin, yin, x, a.n2, zm, c, zp, ym, yp, left, right, a.eps,
                           two_eps);
