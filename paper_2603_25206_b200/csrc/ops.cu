@@ -205,7 +205,7 @@ struct QMomAcc {
 // c / cps): per chunk the lean moments of p (moments.cuh), then the q algebra above; the block mean
 // comes with the index entries (warp_tiles, wtiles.cuh).  One partial per CTA.
 template <bool MINMAX>
-__global__ void __launch_bounds__(TILE_CHUNKS) k_reduce_meta_fast(const uint8_t* __restrict__ payload, uint64_t len,
+__global__ void __launch_bounds__(256, HSZG_WT_MINB_S) k_reduce_meta_fast(const uint8_t* __restrict__ payload, uint64_t len,
                                                                   const uint64_t* __restrict__ offsets, int64_t n_chunks,
                                                                   MetaAux aux, int64_t n, HszgSums* partials,
                                                                   uint32_t buf_bytes) {
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_reduce_meta_fast(const uint8_t*
 // full and inside one row (n2 % 32 == 0), so a chunk starting at (i0, i1, x0) contributes
 // (N0-i0)(N1-i1)[(N2-x0) S - T] with S = sum p_j, T = sum j p_j — the lean moments with TSUM;
 // warp-private tiles as k_reduce_meta_fast.
-__global__ void __launch_bounds__(TILE_CHUNKS) k_reduce_weighted_fast(const uint8_t* __restrict__ payload,
+__global__ void __launch_bounds__(256, HSZG_WT_MINB_S) k_reduce_weighted_fast(const uint8_t* __restrict__ payload,
                                                                       uint64_t len,
                                                                       const uint64_t* __restrict__ offsets,
                                                                       int64_t n_chunks, int64_t N0, int64_t N1,
@@ -279,7 +279,7 @@ struct HszpTileRec {
     int64_t mn, mx;    // min / max of L (q = C_t + L: the extrema of q follow in the combine)
 };
 
-__global__ void __launch_bounds__(256) k_hszp_tile_sums(const uint8_t* __restrict__ payload, uint64_t len,
+__global__ void __launch_bounds__(256, HSZG_WT_MINB_S) k_hszp_tile_sums(const uint8_t* __restrict__ payload, uint64_t len,
                                                         const uint64_t* __restrict__ offsets, int64_t n_chunks,
                                                         HszpTileRec* rec, uint32_t buf_bytes) {
     extern __shared__ __align__(16) uint8_t smem[];
@@ -462,7 +462,7 @@ struct RegionMap {
     int64_t bpr[3];     // blocks per region extent (R / B)
 };
 
-__global__ void __launch_bounds__(TILE_CHUNKS) k_region_fused(SegGeo sg, RegionMap rm, const uint8_t* __restrict__ payload,
+__global__ void __launch_bounds__(256, HSZG_WT_MINB_S) k_region_fused(SegGeo sg, RegionMap rm, const uint8_t* __restrict__ payload,
                                                               uint64_t len, const uint64_t* __restrict__ offsets,
                                                               const int32_t* __restrict__ meta, bool full_segs,
                                                               int64_t cps, RegAccum* acc, uint32_t buf_bytes) {

@@ -497,7 +497,7 @@ static bool stream_full_ok(const HszgGeom* g, const SegGeo& sg, const void* out)
 constexpr size_t WS_TILE_BYTES = (size_t)32 * kChunkStride * 4;
 
 template <int Mode, typename OutT>
-__global__ void __launch_bounds__(256) k_wt_stream(const uint8_t* __restrict__ payload, uint64_t len,
+__global__ void __launch_bounds__(256, HSZG_WT_MINB_R) k_wt_stream(const uint8_t* __restrict__ payload, uint64_t len,
                                                    const uint64_t* __restrict__ offsets, int64_t n_chunks, MetaAux aux,
                                                    double two_eps, OutT* __restrict__ out, uint32_t sb_bytes) {
     extern __shared__ __align__(16) uint8_t smem[];
@@ -531,16 +531,30 @@ __global__ void __launch_bounds__(256) k_wt_stream(const uint8_t* __restrict__ p
 struct BlkGeo {
     int lb0, lb1, lb2, lbs;           // log2 of the block extents, of the block size
     int64_t G1, G2, n1, n2;
+    int pre;                          // lbs <= 10 and block-local offsets fit int32: per-lane offsets precomputed
 };
 
 template <typename OutT>
-__global__ void __launch_bounds__(256) k_wt_blocks(const uint8_t* __restrict__ payload, uint64_t len,
+__global__ void __launch_bounds__(256, HSZG_WT_MINB_R) k_wt_blocks(const uint8_t* __restrict__ payload, uint64_t len,
                                                    const uint64_t* __restrict__ offsets, int64_t n_chunks, MetaAux aux,
                                                    BlkGeo bg, double two_eps, OutT* __restrict__ out, uint32_t sb_bytes) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31;
     int32_t* tile = reinterpret_cast<int32_t*>(wt_scratch(smem, sb_bytes, WS_TILE_BYTES));
     const int nblk = bg.lbs >= 10 ? 1 : 1 << (10 - bg.lbs);          // blocks per full tile (<= 32)
+    // Blocks of <= 1024 values tile a 1024-value warp tile exactly, so store i of this lane always lands
+    // in the same block of the tile at the same block-local offset: both are computed once here
+    // (bg.pre: the host checked that the local offsets fit int32) instead of per store.
+    int32_t loff[8];
+    int lblk[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        const int idx = 128 * i + 4 * lane;
+        lblk[i] = bg.pre ? idx >> bg.lbs : 0;
+        const int l = bg.pre ? idx & ((1 << bg.lbs) - 1) : 0;
+        const int xl = l & ((1 << bg.lb2) - 1), yl = (l >> bg.lb2) & ((1 << bg.lb1) - 1), zl = l >> (bg.lb1 + bg.lb2);
+        loff[i] = bg.pre ? (int32_t)(((int64_t)zl * bg.n1 + yl) * bg.n2 + xl) : 0;
+    }
     warp_tiles(payload, len, offsets, n_chunks, smem + (threadIdx.x >> 5) * WT_NS * sb_bytes, sb_bytes,
                wt_bars(smem, sb_bytes), [&](int64_t c, const uint32_t* words, uint32_t rel, bool valid, int32_t m) {
         if (valid) decode32<false>(words, rel, tile + lane * kChunkStride, m);
@@ -556,6 +570,18 @@ __global__ void __launch_bounds__(256) k_wt_blocks(const uint8_t* __restrict__ p
             org = (((b0 << bg.lb0) * bg.n1) + (b1 << bg.lb1)) * bg.n2 + (b2 << bg.lb2);
         }
         __syncwarp();
+        if (bg.pre) {
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                const int64_t ob = __shfl_sync(0xffffffffu, org, lblk[i]);
+                const int idx = 128 * i + 4 * lane;
+                if ((idx >> 5) < nv)
+                    store4<OutT>(out + ob + loff[i],
+                                 *reinterpret_cast<const int4*>(tile + (idx >> 5) * kChunkStride + (idx & 31)), two_eps);
+            }
+            __syncwarp();
+            return;
+        }
         const int64_t bmask = ((int64_t)1 << bg.lbs) - 1;
 #pragma unroll
         for (int i = 0; i < 8; i++) {
@@ -588,7 +614,7 @@ static int ilog2_exact(int64_t v) {
 //     fits int32), two multi-CTA passes; (3) k_wt_prefix_stream: decode with the in-chunk prefix into the
 // warp's shared tile, add C_t + the chunk's offset in the tile (warp scan), coalesced 16-B stores.  No
 // look-back chain: every tile is independent once the carries are known.
-__global__ void __launch_bounds__(256) k_hszp_tile_totals(const uint8_t* __restrict__ payload, uint64_t len,
+__global__ void __launch_bounds__(256, HSZG_WT_MINB_R) k_hszp_tile_totals(const uint8_t* __restrict__ payload, uint64_t len,
                                                           const uint64_t* __restrict__ offsets, int64_t n_chunks,
                                                           uint32_t* __restrict__ tot, uint32_t sb) {
     extern __shared__ __align__(16) uint8_t smem[];
@@ -667,7 +693,7 @@ struct CarryAux {      // the tile carry of chunk c (tile = 32 chunks)
 };
 
 template <typename OutT>
-__global__ void __launch_bounds__(256) k_wt_prefix_stream(const uint8_t* __restrict__ payload, uint64_t len,
+__global__ void __launch_bounds__(256, HSZG_WT_MINB_R) k_wt_prefix_stream(const uint8_t* __restrict__ payload, uint64_t len,
                                                           const uint64_t* __restrict__ offsets, int64_t n_chunks,
                                                           CarryAux aux, double two_eps, OutT* __restrict__ out,
                                                           uint32_t sb) {
@@ -736,6 +762,7 @@ static void launch_stream_full(const HszgGeom* g, const HszgStream* s, const Seg
         BlkGeo bg{ilog2_exact(sg.B[0]), ilog2_exact(sg.B[1]), ilog2_exact(sg.B[2]), 0, sg.G[1], sg.G[2], sg.n[1], sg.n[2]};
         if (bg.lb0 >= 0 && bg.lb1 >= 0 && bg.lb2 >= 2) {
             bg.lbs = bg.lb0 + bg.lb1 + bg.lb2;
+            bg.pre = bg.lbs <= 10 && ((sg.B[0] - 1) * sg.n[1] + sg.B[1]) * sg.n[2] < ((int64_t)1 << 31);
             const int64_t cps = (sg.B[0] * sg.B[1] * sg.B[2]) / kChunkCap;
             MetaAux aux{s->metadata, cps, ilog2_exact(cps)};
             size_t sm;

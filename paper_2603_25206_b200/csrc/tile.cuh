@@ -126,16 +126,21 @@ __device__ __forceinline__ uint32_t decode32_g(const uint32_t* w, uint32_t rel, 
 // Decode one validated FULL chunk (32 values) whose bytes start at byte `rel` of the staged words:
 // store(g, int4) receives values 4g..4g+3 — the inclusive running sum (Prefix) or value + add.
 // Returns the chunk sum mod 2^32.  Same bit layout as decode_chunk_words (_bitpack.pyx:124-143).
+// The window width G is chosen per WARP (the widest chunk of the lanes calling it), so lanes with
+// different bit-width classes never run two unrolled decodes one after the other; bw = 0 chunks go
+// through the G = 4 decode (mask 0) unless the whole warp is zero.
 template <bool Prefix, typename Store>
 __device__ __forceinline__ uint32_t decode32s(const uint32_t* w, uint32_t rel, int32_t add, Store store) {
     const int bw = (int)smem_byte(w, rel);
-    if (bw == 0) {
+    const unsigned act = __activemask();
+    if (__all_sync(act, bw == 0)) {
         const int4 c = Prefix ? make_int4(0, 0, 0, 0) : make_int4(add, add, add, add);
 #pragma unroll
         for (int q = 0; q < 8; q++) store(q, c);
         return 0;
     }
-    if (bw <= 8) return decode32_g<4, Prefix>(w, rel, bw, add, store);
+    if (__all_sync(act, bw <= 8)) return decode32_g<4, Prefix>(w, rel, bw, add, store);
+    if (__all_sync(act, bw <= 16)) return decode32_g<2, Prefix>(w, rel, bw, add, store);
     if (bw <= 16) return decode32_g<2, Prefix>(w, rel, bw, add, store);
     return decode32_g<1, Prefix>(w, rel, bw, add, store);
 }
@@ -176,11 +181,13 @@ __device__ __forceinline__ void decode8_g(const uint32_t* w, uint32_t rel, int b
 
 __device__ __forceinline__ void decode8(const uint32_t* w, uint32_t rel, int k, int32_t add, int4& lo, int4& hi) {
     const int bw = (int)smem_byte(w, rel);
-    if (bw == 0) {
+    const unsigned act = __activemask();                 // warp-uniform window width, as decode32s
+    if (__all_sync(act, bw == 0)) {
         lo = hi = make_int4(add, add, add, add);
         return;
     }
-    if (bw <= 8) return decode8_g<4>(w, rel, bw, k, add, lo, hi);
+    if (__all_sync(act, bw <= 8)) return decode8_g<4>(w, rel, bw, k, add, lo, hi);
+    if (__all_sync(act, bw <= 16)) return decode8_g<2>(w, rel, bw, k, add, lo, hi);
     if (bw <= 16) return decode8_g<2>(w, rel, bw, k, add, lo, hi);
     return decode8_g<1>(w, rel, bw, k, add, lo, hi);
 }

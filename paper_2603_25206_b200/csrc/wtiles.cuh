@@ -13,7 +13,16 @@
 
 namespace hszg {
 
-constexpr int WT_NS = 3;                  // ring stages per warp
+#ifndef HSZG_WT_NS
+#define HSZG_WT_NS 3
+#endif
+#ifndef HSZG_WT_MINB_R                    // min resident CTAs for the launch bounds of the warp-tile kernels
+#define HSZG_WT_MINB_R 1                  // that stage a shared output tile (recon.cu) ...
+#endif
+#ifndef HSZG_WT_MINB_S
+#define HSZG_WT_MINB_S 4                  // ... and of the reductions (ops.cu): 64 registers, 4 CTAs per SM
+#endif
+constexpr int WT_NS = HSZG_WT_NS;         // ring stages per warp
 
 // per-warp stage bytes for a stream whose widest chunk has max_bw bits (32 full chunks + alignment
 // slack + the bit cursor's zero look-ahead vector)
