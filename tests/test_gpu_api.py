@@ -502,3 +502,39 @@ def _wide_bitwidth_field(rng, dims):
     f = rng.normal(size=dims) * scale[None, None, :]
     f[:, :, :16] = 0.5
     return f.astype(np.float32)
+
+
+# ---- HSZP_ND int16 band-local prefixes with the exact redo of overflowing planes (recon.cu) -------
+
+
+def _hszpnd_overflow_field(rng, dims, case):
+    f = O.random_field(rng, dims, "smooth").astype(np.float64)
+    if case == "first_plane":        # q ~ 5e5 everywhere: plane 0's prefix (= q itself) overflows int16
+        return (f + 100.0).astype(np.float32), 1e-4
+    if case == "all_planes":         # z differences of q ~ 1e5: every plane overflows
+        return O.random_field(rng, dims, "noise"), 1e-5
+    return f.astype(np.float32), 1e-2  # fits int16 everywhere
+
+
+@pytest.mark.parametrize("case", ["fits", "first_plane", "all_planes"])
+@pytest.mark.parametrize("dims", [(300, 16, 64), (40, 33, 96)], ids=["one-band", "bands"])
+def test_hszpnd_l16_redo(H, rng, dims, case):
+    """Stage 3 / 4 and the stage-3 variance of HSZP_ND through the int16 band scan: planes whose
+    band-local prefixes do not fit int16 are redone at int32 — results identical to the oracle."""
+    import torch
+
+    field, eps = _hszpnd_overflow_field(rng, dims, case)
+    c = H.h.compress(field, H.h.CompressorKind.HSZP_ND, H.h.ErrorBound("abs", eps))
+    ref = _oracle_of(c)
+    q = O.stage3(ref)
+    if case == "all_planes":
+        assert np.abs(np.diff(q.astype(np.int64), axis=0)).max() > 2**15
+    if case == "first_plane":
+        assert np.abs(q[0].astype(np.int64)).max() > 2**15
+    assert np.array_equal(H.h.partial_decompress(c, H.h.Stage.QUANTIZED).values, q)
+    full = H.h.partial_decompress(c, H.h.Stage.FULL)
+    assert np.array_equal(full, O.dequantize(q, c.eps))
+    f32 = H.h.partial_decompress(c, H.h.Stage.FULL, dtype=torch.float32)
+    assert np.array_equal(np.asarray(f32), O.dequantize(q, c.eps).astype(np.float32))
+    for op in ("mean", "var"):
+        assert H.stats.compute_stat(c, op, H.h.Stage.QUANTIZED).value == O.compute_stat(ref, op, 3), op
