@@ -291,9 +291,17 @@ def raise_for(status: int, err: Err | None = None, what: str = ""):
     raise cls(msg)
 
 
+_SYNC = os.environ.get("HSZG_SYNC") == "1"     # debugging: synchronise after every entry point
+
+
 def call(fn_name: str, *args, err: Err | None = None):
     status = getattr(lib(), fn_name)(*args)
     raise_for(status, err, fn_name)
+    if _SYNC and not torch().cuda.is_current_stream_capturing():
+        try:
+            torch().cuda.synchronize()
+        except Exception as e:  # noqa: BLE001
+            raise RuntimeError(f"{fn_name}: device fault after the call: {e}") from e
 
 
 # ---------------------------------------------------------------------------

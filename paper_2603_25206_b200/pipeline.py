@@ -443,11 +443,25 @@ class WindowPipeline:
         return self.run(outs, stats, _prepared=True)
 
     # -- the windowed pass ---------------------------------------------------------------
+    def _check_outs(self, outs):
+        """outs must be four distinct contiguous float32 / float64 CUDA tensors of the slab's shape (the
+        kernels write every output; a null or short output would be written out of bounds)."""
+        t = _lib.torch()
+        shape = (self.sf.nz,) + tuple(self.sf.global_dims[1:])
+        if len(outs) != 4 or any(o is None for o in outs):
+            raise ValueError("WindowPipeline.run needs four output tensors [dz, dy, dx, laplacian]")
+        for o in outs:
+            if (tuple(o.shape) != shape or o.dtype not in (t.float32, t.float64) or not o.is_cuda
+                    or not o.is_contiguous()):
+                raise ValueError(f"pipeline outputs must be contiguous float CUDA tensors of shape {shape}")
+        if len({o.data_ptr() for o in outs}) != 4:
+            raise ValueError("pipeline outputs must not alias")
+
     def _fast_ok(self, outs) -> bool:
         """The fused window kernels need rows of whole chunks (HSZP_ND), 16-B rows and fp32 outputs."""
         t = _lib.torch()
         n2 = self.sf.global_dims[2]
-        o = next(x for x in outs if x is not None)
+        o = outs[0]
         if n2 % 4 or o.dtype != t.float32 or not self._canonical():
             return False
         if self.sf.kind == HSZP_ND:
@@ -462,6 +476,7 @@ class WindowPipeline:
         graph and replayed; the per-container boundary phase (halos / carry, collectives) and the
         final stats read-back stay outside it.
         """
+        self._check_outs(outs)
         if not _prepared:
             self.prepare()
         if self._fast_ok(outs):
@@ -691,8 +706,8 @@ class WindowPipeline:
             self.timer.end("fused", self._range_bytes(0, sf.nz) + 16 * sf.nz * self.plane)
 
     def _outs_arr(self, outs, a, b):
-        """Output pointers of planes [a, b); None outputs stay null (the kernels skip them)."""
-        return (ctypes.c_void_p * 4)(*[None if o is None else _lib.ptr(o[a:b]) for o in outs])
+        """Output pointers of planes [a, b) (run() checked that all four exist)."""
+        return (ctypes.c_void_p * 4)(*[_lib.ptr(o[a:b]) for o in outs])
 
     def _windows(self):
         nz = self.sf.nz
