@@ -142,6 +142,47 @@ def _stage_q(c: CompressedStream, stage: Stage):
 
 
 _OPS = {"derivative": _lib.OP_DERIV, "laplacian": _lib.OP_LAPLACIAN, "gradient_magnitude": _lib.OP_GRADMAG}
+_FAST_QLIM = 1 << 27        # int32 stencils (table emitter) are exact while |q| < 2^27 (stencil.cuh)
+_SMS = 148
+
+
+def _fused_layers(dims) -> int:
+    """Block layers per CTA of hszg_fused_blocks for a whole field: fewest (CTA waves x layers per CTA,
+    plus ~2 layers of pipeline fill per CTA) on one CTA per SM."""
+    n0, n1, n2 = dims
+    xy = -(-(n2 // 8) // 16) * -(-(n1 // 8) // 2)
+    nlay = n0 // 8
+    best = None
+    for zl in range(1, nlay + 1):
+        cost = -(-(xy * -(-nlay // zl)) // _SMS) * (zl + 2)
+        if best is None or cost < best[0]:
+            best = (cost, zl)
+    return best[1]
+
+
+def _fused_stencil(c: CompressedStream, op: str, dtype):
+    """HSZX_ND (8^3 blocks, 3-D) derivative / Laplacian with fp32 outputs in one pass from the compressed
+    bytes (hszg_fused_blocks with only the requested outputs: q never reaches HBM), bit-identical to
+    reconstruct + K-STEN: fl32 of the reference float64 by the table emitter while |q| < 2^27 (bounded here
+    by the block means and the bit width), else the fp64-conversion emitter.  None when not eligible."""
+    t = _lib.torch()
+    dims = tuple(c.shape.dims)
+    if (dtype != t.float32 or c.kind != CompressorKind.HSZX_ND or len(dims) != 3 or tuple(c.block_dims) != (8, 8, 8)
+            or any(n % 8 for n in dims) or op not in ("derivative", "laplacian")):
+        return None
+    ds = c.device().validate()
+    if not ds.desc.canonical or ds.desc.max_bitwidth > 16:
+        return None
+    qmax = ds.mean_absmax() + (1 << ds.desc.max_bitwidth)
+    mode = 2 if (qmax < _FAST_QLIM and 2.0 ** -125 <= float(c.eps) <= 2.0 ** 90) else 1
+    outs = [t.empty(dims, dtype=t.float32, device=_lib.device()) for _ in range(3 if op == "derivative" else 1)]
+    ptrs = [_lib.ptr(o) for o in outs] + [None] if op == "derivative" else [None, None, None, _lib.ptr(outs[0])]
+    import ctypes
+    err = _lib.Err()
+    _lib.call("hszg_fused_blocks", ctypes.byref(ds.geom), ctypes.byref(ds.desc), 0, dims[0], None, None,
+              (ctypes.c_void_p * 4)(*ptrs), None, _fused_layers(dims), mode, _lib.stream_handle(),
+              ctypes.byref(err), err=err)
+    return outs
 
 @ranged("hsz/compute_field_op")
 def compute_field_op(c: CompressedStream, op: str, stage: Stage, out: str = "numpy", out_dtype=None) -> DerivedField:
@@ -151,12 +192,21 @@ def compute_field_op(c: CompressedStream, op: str, stage: Stage, out: str = "num
         if stage == Stage.META:
             raise UnsupportedStageError("stencil operations need stage >= decorrelated")
         raise ValueError(f"unknown field operation {op!r}")
-    q = _stage_q(c, stage)
-    if op == "laplacian" and q.dim() < 2:
-        raise ValueError("Laplacian requires 2D or 3D data")
-    outs = devmod.stencil(_OPS[op], [q], [c.eps], stage == Stage.FULL, _dtype(out_dtype))
+    outs = None
+    if stage in (Stage.DECORRELATED, Stage.QUANTIZED):
+        _check_stage(c, stage)
+        outs = _fused_stencil(c, op, _dtype(out_dtype))
+    if outs is not None:
+        count_stage_work(c, stage)
+        ndim = 3
+    else:
+        q = _stage_q(c, stage)
+        ndim = q.dim()
+        if op == "laplacian" and q.dim() < 2:
+            raise ValueError("Laplacian requires 2D or 3D data")
+        outs = devmod.stencil(_OPS[op], [q], [c.eps], stage == Stage.FULL, _dtype(out_dtype))
     if op == "derivative":
-        return DerivedField("derivative", _host(outs, out), AXIS_NAMES[: q.dim()])
+        return DerivedField("derivative", _host(outs, out), AXIS_NAMES[:ndim])
     if op == "laplacian":
         return DerivedField("laplacian", _host(outs, out), ("lap",))
     return DerivedField("gradient_magnitude", _host(outs, out), ("gradmag",))

@@ -69,12 +69,13 @@ inline size_t fx_payload_bytes(int max_bw) {
 inline size_t fx_buffer_bytes(int max_bw) {
     return (size_t)FX_RANGES * (FX_OSTR * 8 + FX_MSTR * 4) + fx_payload_bytes(max_bw);
 }
-inline size_t fx_smem_bytes(int max_bw, int npl) {
-    return (size_t)npl * FX_PLANE * 4 + 2 * fx_buffer_bytes(max_bw);
+inline size_t fx_smem_bytes(int max_bw, int npl, int em = EM_FAST) {
+    return (size_t)npl * FX_PLANE * 4 + 2 * fx_buffer_bytes(max_bw) + (em == EM_TABLE ? XT_BYTES : 0);
 }
 
-template <bool Exact, int NPL>
+template <int EM, int NPL, int OM>
 __global__ void __launch_bounds__(FX_T, 1) k_fused_blocks(FxArgs a, uint32_t buf_bytes) {
+    constexpr bool Exact = EM == EM_EXACT;
     extern __shared__ __align__(128) uint8_t smem[];
     int32_t* Q = reinterpret_cast<int32_t*>(smem);
     uint8_t* BUF = smem + (size_t)NPL * FX_PLANE * 4;      // 2 layer buffers: [offsets | means | payload]
@@ -98,6 +99,8 @@ __global__ void __launch_bounds__(FX_T, 1) k_fused_blocks(FxArgs a, uint32_t buf
     const int nblk = (int)(lbx - fbx + 1);
 
     for (int i = threadIdx.x; i < NPL * FX_PLANE / 4; i += FX_T) reinterpret_cast<int4*>(Q)[i] = make_int4(0, 0, 0, 0);
+    float* XT = reinterpret_cast<float*>(BUF + 2 * (size_t)buf_bytes);      // EM_TABLE: after the layer buffers
+    if (EM == EM_TABLE) xtable_fill(XT, a.eps, threadIdx.x, FX_T);
     if (threadIdx.x == 0) {
         for (int i = 0; i < NPL; i++) {
             mbar_init(&bar_full[i], FX_DT);
@@ -311,9 +314,12 @@ __global__ void __launch_bounds__(FX_T, 1) k_fused_blocks(FxArgs a, uint32_t buf
                 const int4 zm = *reinterpret_cast<const int4*>(Pm + so);
                 const int4 zp = *reinterpret_cast<const int4*>(Pp + so);
                 const int64_t o = zoff + rowoff + k * a.n2;
-                if (Exact)
-                    emit4(a.o0, a.o1, a.o2, a.o3, o, zin, yin, x, a.n2, zm, c, zp, ym, yp, left, right, a.eps,
-                          two_eps);
+                if (EM == EM_EXACT)
+                    emit4<OM>(a.o0, a.o1, a.o2, a.o3, o, zin, yin, x, a.n2, zm, c, zp, ym, yp, left, right, a.eps,
+                              two_eps);
+                else if (EM == EM_TABLE)
+                    emit4x<OM>(a.o0, a.o1, a.o2, a.o3, o, zin, yin, x, a.n2, zm, c, zp, ym, yp, left, right, a.eps,
+                           XT + XT_R);
                 else if (zin && yin)                          // interior rows: no boundary branches
                     emit4f(a.o0, a.o1, a.o2, a.o3, o, true, true, x, a.n2, zm, c, zp, ym, yp, left, right, a.eps,
                            two_eps, epsf, two_epsf);
@@ -339,10 +345,16 @@ int hszg_set_cuda_error(HszgErr* err, cudaError_t e, const char* where);
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 static bool al16f(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-template <bool Exact, int NPL>
+template <int EM, int NPL, int OM>
 static void launch_fused_blocks(const FxArgs& a, dim3 grid, size_t smem, uint32_t buf_bytes, cudaStream_t st) {
-    allow_smem(k_fused_blocks<Exact, NPL>, smem);
-    k_fused_blocks<Exact, NPL><<<grid, FX_T, smem, st>>>(a, buf_bytes);
+    allow_smem(k_fused_blocks<EM, NPL, OM>, smem);
+    k_fused_blocks<EM, NPL, OM><<<grid, FX_T, smem, st>>>(a, buf_bytes);
+}
+template <int EM, int NPL>
+static void launch_fused_om(int om, const FxArgs& a, dim3 grid, size_t smem, uint32_t bb, cudaStream_t st) {
+    if (om == OM_ALL) launch_fused_blocks<EM, NPL, OM_ALL>(a, grid, smem, bb, st);
+    else if (om == OM_GRAD) launch_fused_blocks<EM, NPL, OM_GRAD>(a, grid, smem, bb, st);
+    else launch_fused_blocks<EM, NPL, OM_LAP>(a, grid, smem, bb, st);
 }
 
 static constexpr size_t kSmemLimit = 227 * 1024 - 2048;   // dynamic part (static barriers etc. aside)
@@ -352,17 +364,25 @@ extern "C" int hszg_fused_blocks(const HszgGeom* g, const HszgStream* s, int64_t
                                  int64_t zlayers, int exact, void* stream, HszgErr* err) {
     err->status = HSZG_OK;
     const int64_t nz = g->dims[0], n1 = g->dims[1], n2 = g->dims[2];
-    const int npl = fx_smem_bytes(s->max_bitwidth, 8) <= kSmemLimit ? 8 : 4;
-    const size_t smem = fx_smem_bytes(s->max_bitwidth, npl);
+    // exact: 0 fast fp32, 1 exact (fp64 conversions), 2 exact by table (int32 stencils: |q| < 2^27)
+    int em = exact == 2 ? EM_TABLE : (exact ? EM_EXACT : EM_FAST);
+    if (em == EM_TABLE && fx_smem_bytes(s->max_bitwidth, 4, em) > kSmemLimit) em = EM_EXACT;   // wide bit widths
+    // outputs: all four, the gradient only (laplacian null: the API's derivative) or the Laplacian only
+    const bool has[4] = {out[0] != nullptr, out[1] != nullptr, out[2] != nullptr, out[3] != nullptr};
+    const int om = (has[0] && has[1] && has[2]) ? (has[3] ? OM_ALL : OM_GRAD)
+                                                : ((!has[0] && !has[1] && !has[2] && has[3]) ? OM_LAP : 0);
+    const int npl = fx_smem_bytes(s->max_bitwidth, 8, em) <= kSmemLimit ? 8 : 4;
+    const size_t smem = fx_smem_bytes(s->max_bitwidth, npl, em);
     if (g->kind != HSZG_HSZX_ND || g->ndims != 3 || g->block_dims[0] != 8 || g->block_dims[1] != 8 ||
         g->block_dims[2] != 8 || nz % 8 || n1 % 8 || n2 % 8 || !s->canonical || !s->metadata || zlayers < 1 ||
-        smem > kSmemLimit || !al16f(out[0]) || !al16f(out[1]) || !al16f(out[2]) || !al16f(out[3]) ||
+        smem > kSmemLimit || !om || !al16f(out[0]) || !al16f(out[1]) || !al16f(out[2]) || !al16f(out[3]) ||
         (halo_lo && !al16f(halo_lo)) || (halo_hi && !al16f(halo_hi)) || !al16f(s->offsets) ||
         !al16f(s->metadata) || !al16f(s->payload)) {
         err->status = HSZG_INVALID_ARG;
         snprintf(err->message, sizeof(err->message),
                  "fused_blocks needs a canonical 3-D HSZX_ND stream with 8x8x8 blocks dividing the box, 16-B "
-                 "aligned buffers and staging that fits shared memory (max bit width %d)", s->max_bitwidth);
+                 "aligned buffers, outputs {dz, dy, dx, lap}, {dz, dy, dx} or {lap} and staging that fits shared "
+                 "memory (max bit width %d)", s->max_bitwidth);
         return HSZG_INVALID_ARG;
     }
     if (g->n == 0) return HSZG_OK;
@@ -393,12 +413,20 @@ extern "C" int hszg_fused_blocks(const HszgGeom* g, const HszgStream* s, int64_t
               (unsigned)((nlay + zlayers - 1) / zlayers));
     const uint32_t bb = (uint32_t)fx_buffer_bytes(s->max_bitwidth);
     cudaStream_t st = as_stream(stream);
-    if (exact) {
-        if (npl == 8) launch_fused_blocks<true, 8>(a, grid, smem, bb, st);
-        else launch_fused_blocks<true, 4>(a, grid, smem, bb, st);
-    } else {
-        if (npl == 8) launch_fused_blocks<false, 8>(a, grid, smem, bb, st);
-        else launch_fused_blocks<false, 4>(a, grid, smem, bb, st);
+    if (em == EM_EXACT) {
+        if (npl == 8) launch_fused_om<EM_EXACT, 8>(om, a, grid, smem, bb, st);
+        else launch_fused_om<EM_EXACT, 4>(om, a, grid, smem, bb, st);
+    } else if (em == EM_TABLE) {
+        if (npl == 8) launch_fused_om<EM_TABLE, 8>(om, a, grid, smem, bb, st);
+        else launch_fused_om<EM_TABLE, 4>(om, a, grid, smem, bb, st);
+    } else {                                   // fast: all four outputs (the pipeline)
+        if (om != OM_ALL) {
+            err->status = HSZG_INVALID_ARG;
+            snprintf(err->message, sizeof(err->message), "fused_blocks: output subsets need an exact emitter");
+            return HSZG_INVALID_ARG;
+        }
+        if (npl == 8) launch_fused_blocks<EM_FAST, 8, OM_ALL>(a, grid, smem, bb, st);
+        else launch_fused_blocks<EM_FAST, 4, OM_ALL>(a, grid, smem, bb, st);
     }
     { const cudaError_t e_ = cudaGetLastError(); if (e_ != cudaSuccess) return hszg_set_cuda_error(err, e_, "fused_blocks"); }
     return HSZG_OK;

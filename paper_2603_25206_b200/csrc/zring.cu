@@ -40,8 +40,8 @@ __host__ __device__ constexpr int zr_max(int a, int b) { return a > b ? a : b; }
 // staging slot: 18 L rows (row stride = the wider of the L and lookahead rows) + 3 int32 band-offset rows
 __host__ __device__ constexpr int zr_lb(int lw, int law) { return zr_max(zr_lrow_bytes(lw), zr_lrow_bytes(law)); }
 __host__ __device__ constexpr int zr_slot_bytes(int lw, int law) { return ZR_ROWS * zr_lb(lw, law) + 3 * ZR_SW * 4; }
-constexpr size_t zr_smem(int lw, int law) {
-    return (size_t)ZR_NPL * ZR_PLANE * 4 + (size_t)ZR_D * zr_slot_bytes(lw, law);
+constexpr size_t zr_smem(int lw, int law, int em = EM_FAST) {
+    return (size_t)ZR_NPL * ZR_PLANE * 4 + (size_t)ZR_D * zr_slot_bytes(lw, law) + (em == EM_TABLE ? XT_BYTES : 0);
 }
 
 struct ZrArgs {
@@ -66,8 +66,9 @@ struct ZrArgs {
 // 64 registers (no spills): two sweep CTAs (2 x 12 warps x 2048 regs) leave exactly one k_band_scan
 // CTA's 16 K registers free, so the side stream's band scans co-reside with the sweeps instead of
 // waiting for a whole SM slot (at 72 registers they could not).
-template <bool Exact, int LW, int LAW>
+template <int EM, int LW, int LAW>
 __global__ void __maxnreg__(64) k_zsweep_ring(ZrArgs a) {
+    constexpr bool Exact = EM == EM_EXACT;
     extern __shared__ __align__(128) int32_t zsm[];
     int32_t* Q = zsm;                                     // [ZR_NPL][ZR_ROWS][ZR_RW]
     uint8_t* S = reinterpret_cast<uint8_t*>(zsm + ZR_NPL * ZR_PLANE);   // [ZR_D][slot]
@@ -86,6 +87,8 @@ __global__ void __maxnreg__(64) k_zsweep_ring(ZrArgs a) {
     const int64_t nst = nout + (has_look ? 1 : 0);         // staged planes
 
     for (int i = threadIdx.x; i < (int)(zr_smem(LW, LAW) / 16); i += ZR_T) reinterpret_cast<int4*>(zsm)[i] = make_int4(0, 0, 0, 0);
+    float* XT = reinterpret_cast<float*>(S + (size_t)ZR_D * SLOT);        // EM_TABLE: after the staging slots
+    if (EM == EM_TABLE) xtable_fill(XT, a.eps, threadIdx.x, ZR_T);
     if (threadIdx.x == 0) {
         for (int i = 0; i < ZR_D; i++) {
             mbar_init(&s_full[i], 1);
@@ -262,9 +265,12 @@ __global__ void __maxnreg__(64) k_zsweep_ring(ZrArgs a) {
                 const int4 zm = *reinterpret_cast<const int4*>(Pm + so);
                 const int4 zp = *reinterpret_cast<const int4*>(Pp + so);
                 const int64_t o = z * plane + y * n2 + x;
-                if (Exact)
+                if (EM == EM_EXACT)
                     emit4(a.o0, a.o1, a.o2, a.o3, o, zin, yin, x, n2, zm, c, zp, ym, yp, left, right, a.eps,
                           two_eps);
+                else if (EM == EM_TABLE)
+                    emit4x<OM_ALL>(a.o0, a.o1, a.o2, a.o3, o, zin, yin, x, n2, zm, c, zp, ym, yp, left, right, a.eps,
+                           XT + XT_R);
                 else if (zin && yin)
                     emit4f(a.o0, a.o1, a.o2, a.o3, o, true, true, x, n2, zm, c, zp, ym, yp, left, right, a.eps,
                            two_eps, epsf, two_epsf);
@@ -312,24 +318,24 @@ int launch_zsweep_ring(const int32_t* L, int64_t n1, int64_t n2, int64_t nout, c
     dim3 grid((unsigned)((n2 + ZR_TX - 1) / ZR_TX), (unsigned)((n1 + ZR_TY - 1) / ZR_TY));
 #define ZR_LAUNCH(E, W, WA)                                                           \
     do {                                                                              \
-        allow_smem(k_zsweep_ring<E, W, WA>, zr_smem(W, WA));                          \
-        k_zsweep_ring<E, W, WA><<<grid, ZR_T, zr_smem(W, WA), st>>>(a);               \
+        allow_smem(k_zsweep_ring<E, W, WA>, zr_smem(W, WA, E));                       \
+        k_zsweep_ring<E, W, WA><<<grid, ZR_T, zr_smem(W, WA, E), st>>>(a);            \
+    } while (0)
+#define ZR_WIDTHS(E)                                                                  \
+    do {                                                                              \
+        if (key == 0) ZR_LAUNCH(E, 4, 4);                                             \
+        else if (key == 4) ZR_LAUNCH(E, 2, 2);                                        \
+        else if (key == 8) ZR_LAUNCH(E, 1, 1);                                        \
+        else if (key == 5) ZR_LAUNCH(E, 2, 1);                                        \
+        else return 1;                                                                \
     } while (0)
     // width codes 0/1/2 = int32/int16/int8; supported pairs: equal, or int16 window + int8 lookahead
     const int key = lmode * 3 + lamode;
-    if (exact) {
-        if (key == 0) ZR_LAUNCH(true, 4, 4);
-        else if (key == 4) ZR_LAUNCH(true, 2, 2);
-        else if (key == 8) ZR_LAUNCH(true, 1, 1);
-        else if (key == 5) ZR_LAUNCH(true, 2, 1);
-        else return 1;
-    } else {
-        if (key == 0) ZR_LAUNCH(false, 4, 4);
-        else if (key == 4) ZR_LAUNCH(false, 2, 2);
-        else if (key == 8) ZR_LAUNCH(false, 1, 1);
-        else if (key == 5) ZR_LAUNCH(false, 2, 1);
-        else return 1;
-    }
+    // exact: 0 fast fp32, 1 exact (fp64 conversions), 2 exact by table (int32 stencils: |q| < 2^27)
+    if (exact == 2) ZR_WIDTHS(EM_TABLE);
+    else if (exact) ZR_WIDTHS(EM_EXACT);
+    else ZR_WIDTHS(EM_FAST);
+#undef ZR_WIDTHS
 #undef ZR_LAUNCH
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }

@@ -127,6 +127,14 @@ class DeviceStream:
         sub.validated = self.validated
         return sub
 
+    def mean_absmax(self) -> int:
+        """max |M_b| over the block means (cached; 0 without metadata): with the max bit width it bounds
+        |q| = |p + M_b| for the int32 stencil kernels (fused, table emitter)."""
+        if getattr(self, "_mean_absmax", None) is None:
+            m = self.metadata
+            self._mean_absmax = 0 if m is None or m.numel() == 0 else int(m.to(_lib.torch().int64).abs().max())
+        return self._mean_absmax
+
     # ---- validation -----------------------------------------------------------------
 
     def validate(self):

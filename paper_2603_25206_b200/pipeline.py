@@ -36,6 +36,7 @@ from ._nvtx import ranged
 _SMS = 148          # B200 SM count (grid sizing only)
 FUSED_LAYERS = 16   # block layers (8 planes each) per CTA of the one-pass kernels
 FAST_QLIM = 1 << 27  # fast fp32 emitter validity bound on |q| (stencil.cuh)
+EM_FAST, EM_EXACT, EM_TABLE = 0, 1, 2   # emitter modes of the fused kernels (stencil.cuh EmitMode)
 
 HSZP_ND, HSZX_ND = 1, 3
 SUMS_BYTES = 64
@@ -45,7 +46,7 @@ SUMS_BYTES = 64
 # sized by _band_rows: 256 rows at 2048^2 planes) under the ring z-sweeps, fast fp32 emitter.
 HEADLINE_SETTINGS = dict(use_graph=True, exact_fp32=False, one_pass=True, lorenzo_one_pass=False, overlap=True,
                          band_rows_req=None)
-SETTINGS = ("use_graph", "exact_fp32", "one_pass", "lorenzo_one_pass", "overlap", "band_rows_req", "fused_layers")
+SETTINGS = ("use_graph", "exact_fp32", "exact_table", "one_pass", "lorenzo_one_pass", "overlap", "band_rows_req", "fused_layers")
 
 
 def apply_settings(pipe, **kw):
@@ -503,16 +504,17 @@ class WindowPipeline:
                     self._stage_boundary()
                     self._fused_loop(outs)
                     res = self._finish_stats(_prepared) if stats else None
-            if not self.exact_fp32 and not self._fast_valid(res if stats else self._finish_stats(_prepared),
-                                                            _prepared):
-                # the fast emitter needs |q| < 2^27 (FAST_QLIM, stencil.cuh): every q is some point's
-                # centre, so the exact min / max decide it; redo the pass with the exact emitter
-                self.exact_fp32 = True
+            if self._emit_mode() != EM_EXACT and not self._fast_valid(
+                    res if stats else self._finish_stats(_prepared), _prepared):
+                # the fast and table emitters compute the stencils in int32, valid while |q| < 2^27
+                # (FAST_QLIM, stencil.cuh): every q is some point's centre, so the exact min / max decide
+                # it; redo the pass with the fp64-conversion exact emitter
+                self._force_exact64 = True
                 try:
                     self._fused_loop(outs)
                     res = self._finish_stats(_prepared)
                 finally:
-                    self.exact_fp32 = False
+                    self._force_exact64 = False
             return res if stats else None
         return self._run_generic(outs, stats, _prepared)
 
@@ -559,6 +561,19 @@ class WindowPipeline:
     # fp32 outputs of the fused loop: True = fl32 of the reference float64 (bit-exact vs the oracle);
     # False = int32 stencil x fl32(eps) in fp32 (<= 2^-23 relative, no fp64 conversions: faster).
     exact_fp32 = False
+    # exact mode by table (EM_TABLE, stencil.cuh): bit-identical to the fp64-conversion emitter; off = always
+    # the conversion chain (tests compare the two)
+    exact_table = True
+    _force_exact64 = False
+
+    def _emit_mode(self) -> int:
+        """Emitter mode of the fused kernels: EM_FAST, EM_EXACT (fp64 conversions) or EM_TABLE."""
+        if self._force_exact64:
+            return EM_EXACT
+        if not self.exact_fp32:
+            return EM_FAST
+        eps = float(self.sf.eps)
+        return EM_TABLE if (self.exact_table and 2.0 ** -125 <= eps <= 2.0 ** 90) else EM_EXACT
     band_rows_req = None        # force a band height for hszg_band_scan (tests); None: sized for the grid
 
     # -- fused loops (window.cu) ---------------------------------------------------------------
@@ -627,7 +642,7 @@ class WindowPipeline:
     def _replay(self, outs):
         t = _lib.torch()
         key = tuple(0 if o is None else _lib.ptr(o) for o in outs) + (self.halo_lo is not None, self.halo_hi is not None,
-                                                  self.exact_fp32, self.overlap, self.fused_layers, self.side_priority)
+                                                  self._emit_mode(), self.overlap, self.fused_layers, self.side_priority)
         if self._graph is None or self._graph_key != key:
             self._fused_loop(outs)                        # warm-up: workspaces, smem attributes
             t.cuda.synchronize()
@@ -684,7 +699,7 @@ class WindowPipeline:
         _lib.call("hszg_lorenzo_onepass", ctypes.byref(self.ds.geom), ctypes.byref(self.ds.desc),
                   _lib.ptr(self.lz_bands), _lib.ptr(self.lz_edges), _lib.ptr(carry) if carry is not None else None,
                   _lib.ptr(upper) if upper is not None else None, sf.z0, sf.global_dims[0], outs_arr,
-                  _lib.ptr(self.acc), int(self.exact_fp32), _lib.stream_handle(), ctypes.byref(err), err=err)
+                  _lib.ptr(self.acc), self._emit_mode(), _lib.stream_handle(), ctypes.byref(err), err=err)
         if self.timer:
             self.timer.end("fused", self._range_bytes(0, sf.nz) + 16 * sf.nz * self.plane)
 
@@ -700,7 +715,7 @@ class WindowPipeline:
         _lib.call("hszg_fused_blocks", ctypes.byref(self.ds.geom), ctypes.byref(self.ds.desc), sf.z0,
                   sf.global_dims[0], _lib.ptr(self.halo_buf[0]) if self.halo_lo is not None else None,
                   _lib.ptr(self.halo_buf[1]) if self.halo_hi is not None else None, outs_arr, _lib.ptr(self.acc),
-                  max(1, min(nlay, self.fused_layers)), int(self.exact_fp32), _lib.stream_handle(), ctypes.byref(err),
+                  max(1, min(nlay, self.fused_layers)), self._emit_mode(), _lib.stream_handle(), ctypes.byref(err),
                   err=err)
         if self.timer:
             self.timer.end("fused", self._range_bytes(0, sf.nz) + 16 * sf.nz * self.plane)
@@ -747,7 +762,7 @@ class WindowPipeline:
             _lib.call("hszg_zgrad_lap", _lib.ptr(ring[k % 3]), n1, n2, 0, b - a, sf.z0 + a, sf.global_dims[0],
                       ctypes.c_double(sf.eps), self._outs_arr(outs, a, b), _lib.ptr(self.acc),
                       _lib.ptr(prev) if prev is not None else None, _lib.ptr(nxt) if nxt is not None else None,
-                      int(self.exact_fp32), _lib.stream_handle())
+                      self._emit_mode(), _lib.stream_handle())
             if self.timer:
                 self.timer.end("stencil", (4 + 16) * (b - a) * self.plane)
             if k + 2 < nw:
@@ -834,7 +849,7 @@ class WindowPipeline:
                       sf.global_dims[0], ctypes.c_double(sf.eps), self._outs_arr(outs, a, b), _lib.ptr(self.acc),
                       _lib.ptr(self.bands[k % ns]) if br else None,
                       _lib.ptr(self.bands[(k + 1) % ns]) if (br and look is not None) else None, br,
-                      modes[k] | ((modes[k + 1] if k + 1 < nw else modes[k]) << 4), int(self.exact_fp32),
+                      modes[k] | ((modes[k + 1] if k + 1 < nw else modes[k]) << 4), self._emit_mode(),
                       _lib.stream_handle())
             if self.timer:
                 self.timer.end("stencil", ((4, 2, 1)[modes[k]] + 16) * (b - a) * self.plane)
