@@ -85,6 +85,63 @@ __device__ __forceinline__ void chunk_moments_g(const uint32_t* w, uint32_t rel,
     r.mx = mx;
 }
 
+// bw <= 8 without extrema, four values per IDP4A (SWAR): the four bw-bit fields of a 32-bit funnel window are
+// spread into the bytes of a word (a shift + LOP3 each), the four sign bits into bytes of +1 / -1 (one
+// magic multiply spreads bits 0-3 to bits 0, 8, 16, 24), and one dp4a each gives sum p, sum |p|^2 (and
+// sum j p with per-byte signed indices): ~4 instructions per value instead of ~7.
+__device__ __forceinline__ int32_t dp4a_us(uint32_t a, uint32_t b, int32_t c) {      // u8 x s8
+    int32_t d;
+    asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ uint32_t dp4a_uu(uint32_t a, uint32_t b, uint32_t c) {    // u8 x u8
+    uint32_t d;
+    asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+template <bool TSUM>
+__device__ __forceinline__ void chunk_moments_b8(const uint32_t* w, uint32_t rel, uint32_t bw, uint32_t smask,
+                                                 ChunkMoments& r) {
+    const uint32_t bitpos = (rel + 5) * 8;
+    uint32_t wi = bitpos >> 5, sh = bitpos & 31;
+    uint32_t cur = w[wi], nxt = w[wi + 1];
+    const uint32_t mask = (1u << bw) - 1u;          // bw <= 8
+    const uint32_t adv = 4 * bw;
+    const uint32_t s1 = 8 - bw, s2 = 16 - 2 * bw, s3 = 24 - 3 * bw;
+    const uint32_t m1 = mask << 8, m2 = mask << 16, m3 = mask << 24;
+    int32_t sp = 0, tp = 0;                          // |sum| <= 32 * 255, |sum j p| <= 31 * 32 * 255
+    uint32_t sq = 0;                                 // <= 32 * 255^2
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        const uint32_t grp = __funnelshift_r(cur, nxt, sh);
+        const uint32_t b = (grp & mask) | ((grp << s1) & m1) | ((grp << s2) & m2) | ((grp << s3) & m3);
+        const uint32_t sb = (((smask >> (4 * k)) & 15u) * 0x00204081u) & 0x01010101u;   // sign bits -> bytes
+        sp = dp4a_us(b, sb * 0xFEu + 0x01010101u, sp);                                  // bytes +1 / -1
+        sq = dp4a_uu(b, b, sq);
+        if (TSUM) {
+            // signed byte indices j = 4k + i (negated where the sign is set; byte 0 of k = 0 is j = 0)
+            const uint32_t sbt = k == 0 ? (sb & 0x01010100u) : sb;
+            const uint32_t idx = 0x03020100u + 0x04040404u * (uint32_t)k;
+            tp = dp4a_us(b, (idx ^ (sbt * 0xFFu)) + sbt, tp);
+        }
+        if (k + 1 < 8) {
+            sh += adv;
+            if (sh >= 32) {
+                sh -= 32;
+                cur = nxt;
+                wi++;
+                nxt = w[wi + 1];
+            }
+        }
+    }
+    r.sp = sp;
+    r.sq = (u128)sq;
+    r.tp = tp;
+    r.mn = INT32_MAX;
+    r.mx = INT32_MIN;
+}
+
 // bw 17..32: exact, value by value (int64 / u128)
 template <bool TSUM, bool MINMAX>
 __device__ __forceinline__ void chunk_moments_wide(const uint32_t* w, uint32_t rel, uint32_t bw, uint32_t smask,
@@ -130,7 +187,8 @@ __device__ __forceinline__ ChunkMoments chunk_moments(const uint32_t* w, uint32_
     const uint32_t smask = bw ? smem_u32(w, rel + 1) : 0u;
     const unsigned act = __activemask();
     if (__all_sync(act, bw <= 8)) {
-        chunk_moments_g<4, TSUM, MINMAX>(w, rel, bw, smask, r);
+        if (MINMAX) chunk_moments_g<4, TSUM, MINMAX>(w, rel, bw, smask, r);
+        else chunk_moments_b8<TSUM>(w, rel, bw, smask, r);
     } else if (__all_sync(act, bw <= 16)) {
         chunk_moments_g<2, TSUM, MINMAX>(w, rel, bw, smask, r);
     } else if (bw <= 16) {
