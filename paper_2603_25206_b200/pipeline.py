@@ -580,7 +580,7 @@ class WindowPipeline:
     def _persistent(self):
         """Buffers whose addresses stay fixed across runs (graph-capture safe)."""
         t = _lib.torch()
-        key = (self.W, self.band_rows_req, self.one_pass, self.lorenzo_one_pass, self.l16, self.l8)
+        key = (self.W, self.band_rows_req, self.one_pass, self.lorenzo_one_pass, self.l16, self.l8, self.overlap)
         if getattr(self, "_pers_W", None) == self.W and getattr(self, "_pers_key", None) == key:
             return
         n1, n2 = self.sf.global_dims[1], self.sf.global_dims[2]
