@@ -302,7 +302,11 @@ int hszg_quantized_sums(const HszgGeom* g, const HszgStream* s, HszgSums* out_de
  * max bit width <= 16): q never reaches memory.  The stream is a z-slab of a gN0-plane field whose
  * first plane is global plane gz0; halo_lo / halo_hi (optional, n1*n2 int32) are q of the planes just
  * below / above the slab.  zlayers = 8-plane block layers per CTA (z segment of the grid).
- * out[4] = dz, dy, dx, Laplacian (fp32, slab-sized); acc (optional) accumulates the slab's stats. */
+ * out[4] = dz, dy, dx, Laplacian (fp32, slab-sized); acc (optional) accumulates the slab's stats.
+ * exact: 0 fast fp32 (int32 stencil x fl32(eps), |q| < 2^27), 1 fl32 of the reference float64 by fp64
+ * conversions, 2 the same values by a shared-memory table (int32 stencils: the caller guarantees
+ * |q| < 2^27).  In the exact modes out may hold only {dz, dy, dx} (Laplacian NULL) or only the
+ * Laplacian (the API's derivative / laplacian calls, fields.py:34-93); other subsets: HSZG_INVALID_ARG. */
 int hszg_fused_blocks(const HszgGeom* g, const HszgStream* s, int64_t gz0, int64_t gN0, const int32_t* halo_lo,
                       const int32_t* halo_hi, float* const* out, HszgAcc* acc, int64_t zlayers, int exact,
                       void* stream, HszgErr* err);
