@@ -286,7 +286,9 @@ int hszg_zgrad_lap(const int32_t* q, int64_t n1, int64_t n2, int64_t zlo, int64_
  * q[a+nout-1] to carry_out — q itself is never stored.  With band_off (hszg_band_scan output) P2 is
  * band-local: row y of plane z adds band_off[z][y / band_rows][:] (look_band_off: the lookahead's);
  * p2_mode: width codes of those band-local prefixes (hszg_band_scan l_mode) — bits 0-3 for P2, bits 4-7
- * for the lookahead plane: 0 int32, 1 int16, 2 int8; pairs equal, or int16 P2 with an int8 lookahead. */
+ * for the lookahead plane: 0 int32, 1 int16, 2 int8; pairs equal, or int16 P2 with an int8 lookahead.
+ * exact: as hszg_fused_blocks (0 fast, 1 fp64 conversions, 2 table; 2 only on the ring sweep, band_rows % 16
+ * == 0, else treated as 1). */
 int hszg_zsweep_grad_lap(const int32_t* P2, int64_t n1, int64_t n2, int64_t nout, const int32_t* lookahead,
                          const int32_t* carry, const int32_t* q_upper, int32_t* carry_out, int64_t gz0, int64_t gN0,
                          double eps, float* const* out, HszgAcc* acc, const int32_t* band_off,
