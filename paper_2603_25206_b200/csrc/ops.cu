@@ -525,6 +525,49 @@ __global__ void __launch_bounds__(256, HSZG_WT_MINB_S) k_region_fused(SegGeo sg,
 }
 
 // accumulators -> region_buffer words (s1, s2 lo / hi, size, qmin, qmax); sizes in closed form
+// Regions that are exactly the stream's blocks (region extent = block extent on every axis, every block full,
+// CPS = chunks per block dividing 32): a block's chunks sit in CPS consecutive lanes of one warp tile, so the
+// region is reduced by log2(CPS) xor-shuffle steps and its group leader writes the region_buffer entry itself
+// (one writer per region: no accumulator, no atomics, no init / finish kernels; key = chunk / CPS).
+template <int CPS>
+__global__ void __launch_bounds__(256, HSZG_WT_MINB_S) k_region_blocks(const uint8_t* __restrict__ payload, uint64_t len,
+                                                               const uint64_t* __restrict__ offsets, int64_t n_chunks,
+                                                               const int32_t* __restrict__ meta, int64_t bsize,
+                                                               int64_t* s1o, uint64_t* s2lo, int64_t* s2hi,
+                                                               int32_t* qmin, int32_t* qmax, int64_t* size,
+                                                               uint32_t buf_bytes) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int lane = threadIdx.x & 31;
+    warp_tiles(payload, len, offsets, n_chunks, smem + (threadIdx.x >> 5) * WT_NS * buf_bytes, buf_bytes,
+               wt_bars(smem, buf_bytes), [&](int64_t c, const uint32_t* words, uint32_t rel, bool valid, int32_t) {
+        const ChunkMoments r = chunk_moments<false, true>(words, rel, valid);
+        const int64_t seg = c / CPS;
+        const int64_t m = valid ? (int64_t)__ldg(meta + seg) : 0;
+        int64_t s1 = valid ? r.sp + 32 * m : 0;
+        const u128 s2 = valid ? (u128)((i128)r.sq + (i128)(2 * m) * (i128)r.sp + (i128)(32 * m) * (i128)m) : (u128)0;
+        uint64_t lo = (uint64_t)s2, hi = (uint64_t)(s2 >> 64);
+        int mn = valid ? r.mn + (int32_t)m : INT32_MAX, mx = valid ? r.mx + (int32_t)m : INT32_MIN;
+#pragma unroll
+        for (int d = 1; d < CPS; d <<= 1) {
+            s1 += __shfl_xor_sync(0xffffffffu, s1, d);
+            const uint64_t olo = __shfl_xor_sync(0xffffffffu, lo, d), ohi = __shfl_xor_sync(0xffffffffu, hi, d);
+            const u128 t = (((u128)hi << 64) | lo) + (((u128)ohi << 64) | olo);
+            lo = (uint64_t)t;
+            hi = (uint64_t)(t >> 64);
+            mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, d));
+            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+        }
+        if (valid && (lane & (CPS - 1)) == 0) {
+            s1o[seg] = s1;
+            s2lo[seg] = lo;
+            s2hi[seg] = (int64_t)hi;
+            qmin[seg] = mn;
+            qmax[seg] = mx;
+            size[seg] = bsize;
+        }
+    });
+}
+
 __global__ void k_region_accum_finish(const RegAccum* acc, int64_t n0, int64_t n1, int64_t n2, int64_t R0, int64_t R1,
                                       int64_t R2, int64_t g1, int64_t g2, int64_t nr, int64_t* s1, uint64_t* s2lo,
                                       int64_t* s2hi, int32_t* qmin, int32_t* qmax, int64_t* size) {
@@ -1191,6 +1234,30 @@ extern "C" int hszg_region_stream(const HszgGeom* g, const HszgStream* s, const 
     bool full_segs = (sg.B[0] * sg.B[1] * sg.B[2]) % kChunkCap == 0;
     for (int a = 0; a < 3; a++) full_segs = full_segs && sg.E[a] == sg.B[a];
     const int64_t cps = (sg.B[0] * sg.B[1] * sg.B[2]) / kChunkCap;
+    if (full_segs && rm.bpr[0] == 1 && rm.bpr[1] == 1 && rm.bpr[2] == 1 && cps >= 1 && cps <= 32 &&
+        (cps & (cps - 1)) == 0 && nr == g->n_chunks / cps) {
+        // region = block: the one-writer kernel (no accumulator)
+        size_t sm;
+        uint32_t bb;
+        const int64_t bs = sg.B[0] * sg.B[1] * sg.B[2];
+#define HSZG_RB(C)                                                                                              \
+        do {                                                                                                    \
+            const unsigned grid = wtile_grid(k_region_blocks<C>, s->max_bitwidth, g->n_chunks, &sm, &bb);      \
+            k_region_blocks<C><<<grid, 256, sm, st>>>(s->payload, s->payload_len, s->offsets, g->n_chunks,      \
+                                                      s->metadata, bs, s1, s2_lo, s2_hi, qmin, qmax, size, bb); \
+        } while (0)
+        switch (cps) {
+            case 1: HSZG_RB(1); break;
+            case 2: HSZG_RB(2); break;
+            case 4: HSZG_RB(4); break;
+            case 8: HSZG_RB(8); break;
+            case 16: HSZG_RB(16); break;
+            default: HSZG_RB(32); break;
+        }
+#undef HSZG_RB
+        { const cudaError_t e_ = cudaGetLastError(); if (e_ != cudaSuccess) return hszg_set_cuda_error(err, e_, "region blocks"); }
+        return HSZG_OK;
+    }
     k_region_accum_init<<<grid_for(nr, 256, 148 * 8), 256, 0, st>>>(acc, nr);
     size_t sm;
     uint32_t bb;

@@ -389,6 +389,28 @@ def test_regions_vs_oracle(H, rng, kind, dims, region):
     np.testing.assert_array_equal(g, O.gradient_magnitude(q, c.eps))
 
 
+@pytest.mark.parametrize("case", ["nd8", "nd4", "nd2x4x8", "x1d"])
+def test_regions_equal_blocks_vs_oracle(H, rng, monkeypatch, case):
+    """Regions that are exactly the stream's blocks (HSZX_ND 8^3: 16 chunks per block; 4^3: 2; 2x4x8: 2; HSZX 1-D
+    blocks of 128: 4) take the one-writer k_region_blocks path (no accumulator); results equal the oracle's,
+    including a wide-residual field (int128 S2 per block) and the min / max."""
+    from paper_2603_25206_b200 import _lib
+
+    dims, kind, bd, region = {"nd8": ((16, 24, 40), 3, (8, 8, 8), 8), "nd4": ((8, 12, 16), 3, (4, 4, 4), 4),
+                              "nd2x4x8": ((6, 8, 32), 3, (2, 4, 8), (2, 4, 8)),
+                              "x1d": ((64 * 128,), 2, (128,), 128)}[case]
+    field = O.random_field(rng, dims, "mixed") * np.float32(50.0)
+    c = H.h.compress(field, H.h.CompressorKind(kind), H.h.ErrorBound("rel", 1e-6), block_dims=bd)
+    oc = _oracle_of(c)
+    q = O.stage3(oc)
+    rs = H.regions.region_stats(c, region, tau=float(np.median(field)))
+    s1, s2, qmin, qmax, size = O.region_reduce(q, region)
+    assert np.array_equal(rs.s1, s1.astype(np.int64)) and np.array_equal(rs.size, size)
+    assert all(int(a) == int(b) for a, b in zip(rs.s2.ravel(), s2.ravel()))
+    assert np.array_equal(rs.qmin, qmin) and np.array_equal(rs.qmax, qmax)
+    assert rs.crossing_count == O.threshold_count(q, c.eps, region, float(np.median(field)))
+
+
 @pytest.mark.parametrize("dims,region", [((6, 10, 256), (3, 4, 128)), ((5, 9, 20), 8), ((7, 9, 11), 4)])
 def test_region_reduce_extreme_values(H, rng, dims, region):
     """|q| near 2^31: per-region S2 beyond 2^64 (int128 path) in both K-REG kernels."""
