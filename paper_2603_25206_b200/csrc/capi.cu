@@ -89,7 +89,9 @@ extern "C" size_t hszg_workspace_bytes(const HszgGeom* g, const HszgStream* s, i
             {
                 const int64_t br = recon_band_rows(g->dims[0], g->dims[1], g->dims[2]);
                 const int64_t nb = (g->dims[1] + br - 1) / br;
-                return (out_type == HSZG_F64 ? n4 : 0) + (size_t)g->dims[0] * nb * g->dims[2] * 4 + 512;
+                // + the int16 band-local prefixes of the narrow path (recon.cu band_scan_narrow) and its flag
+                const size_t p2b = out_type == HSZG_F64 ? n4 : (((size_t)g->n * 2 + 255) & ~(size_t)255);
+                return p2b + (size_t)g->dims[0] * nb * g->dims[2] * 4 + 512;
             }
             // generic: decode buffer (fp64 output only) + per-kind transform scratch
             size_t b = out_type == HSZG_F64 ? n4 : 0;

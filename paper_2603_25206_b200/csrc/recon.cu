@@ -383,7 +383,8 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_tile_scan_fast(const uint8_t* _
 }
 
 // z prefix (one band per plane: L is the plane's 2-D prefix) reduced instead of stored
-__global__ void __launch_bounds__(256) k_col_scan_sums(const int32_t* __restrict__ src, int64_t M, int64_t Lc,
+template <typename SrcT = int32_t>
+__global__ void __launch_bounds__(256) k_col_scan_sums(const SrcT* __restrict__ src, int64_t M, int64_t Lc,
                                                        HszgSums* partials) {
     const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     int64_t s1 = 0;
@@ -401,14 +402,14 @@ __global__ void __launch_bounds__(256) k_col_scan_sums(const int32_t* __restrict
             mx = max(mx, q);
         };
         for (; m + 4 <= M; m += 4) {
-            const uint32_t v0 = (uint32_t)__ldg(src + m * Lc + l), v1 = (uint32_t)__ldg(src + (m + 1) * Lc + l);
-            const uint32_t v2 = (uint32_t)__ldg(src + (m + 2) * Lc + l), v3 = (uint32_t)__ldg(src + (m + 3) * Lc + l);
+            const uint32_t v0 = (uint32_t)(int32_t)__ldg(src + m * Lc + l), v1 = (uint32_t)(int32_t)__ldg(src + (m + 1) * Lc + l);
+            const uint32_t v2 = (uint32_t)(int32_t)__ldg(src + (m + 2) * Lc + l), v3 = (uint32_t)(int32_t)__ldg(src + (m + 3) * Lc + l);
             take(v0);
             take(v1);
             take(v2);
             take(v3);
         }
-        for (; m < M; m++) take((uint32_t)__ldg(src + m * Lc + l));
+        for (; m < M; m++) take((uint32_t)(int32_t)__ldg(src + m * Lc + l));
     }
     Acc a;
     a.init();
@@ -943,14 +944,22 @@ __device__ __forceinline__ void store4(OutT* d, const uint32_t (&v)[4], double t
     }
 }
 
-template <typename OutT, bool BANDS>
-__global__ void __launch_bounds__(256) k_col_scan_v4(const int32_t* src, const int32_t* __restrict__ A, int64_t M,
+// 4 values of a P2 row: int32 (16 B) or int16 (8 B, the narrow band-local prefixes)
+__device__ __forceinline__ int4 ld_p2x4(const int32_t* p) { return __ldg(reinterpret_cast<const int4*>(p)); }
+__device__ __forceinline__ int4 ld_p2x4(const int16_t* p) {
+    const uint2 h = __ldg(reinterpret_cast<const uint2*>(p));
+    return make_int4((int32_t)(int16_t)(h.x & 0xffffu), (int32_t)h.x >> 16, (int32_t)(int16_t)(h.y & 0xffffu),
+                     (int32_t)h.y >> 16);
+}
+
+template <typename OutT, bool BANDS, typename SrcT = int32_t>
+__global__ void __launch_bounds__(256) k_col_scan_v4(const SrcT* src, const int32_t* __restrict__ A, int64_t M,
                                                      int64_t n1, int64_t n2, int64_t BR, int64_t nb, double two_eps,
                                                      OutT* dst) {
     const int64_t Lc = n1 * n2;
     const int64_t l = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
     if (l >= Lc) return;
-    const int32_t* s = src + l;
+    const SrcT* s = src + l;
     OutT* d = dst + l;
     const int32_t* a = A;
     int64_t as = 0;
@@ -966,7 +975,7 @@ __global__ void __launch_bounds__(256) k_col_scan_v4(const int32_t* src, const i
         int4 v[U], o[U];
 #pragma unroll
         for (int k = 0; k < U; k++) {
-            v[k] = __ldg(reinterpret_cast<const int4*>(s + (m + k) * Lc));
+            v[k] = ld_p2x4(s + (m + k) * Lc);
             if constexpr (BANDS) o[k] = __ldg(reinterpret_cast<const int4*>(a + (m + k) * as));
             else o[k] = make_int4(0, 0, 0, 0);
         }
@@ -980,7 +989,7 @@ __global__ void __launch_bounds__(256) k_col_scan_v4(const int32_t* src, const i
         }
     }
     for (; m < M; m++) {
-        const int4 v = __ldg(reinterpret_cast<const int4*>(s + m * Lc));
+        const int4 v = ld_p2x4(s + m * Lc);
         int4 o = make_int4(0, 0, 0, 0);
         if constexpr (BANDS) o = __ldg(reinterpret_cast<const int4*>(a + m * as));
         acc[0] += (uint32_t)v.x + (uint32_t)o.x;
@@ -1224,6 +1233,30 @@ static int transform_decoded(const HszgGeom* g, const SegGeo& sg, const int32_t*
     return HSZG_OK;
 }
 
+
+// Narrow band-local prefixes for the API's 3-D HSZP_ND passes (stage 3 / 4, quantized sums): with one band per
+// plane the band scan's L is P2 = q[z] - q[z-1], small for the reference's fields, so it is stored as int16 (half
+// the write and the z scan's read of int32; hszg_band_scan l_mode 1) and its overflow flag is read back (a host
+// sync, skipped under stream capture).  1: p16 holds every P2 value; 0: the caller runs the int32 path; < 0: error.
+static int band_scan_narrow(const HszgGeom* g, const HszgStream* s, int64_t br, int16_t* p16, int32_t* A,
+                            int32_t* flag, cudaStream_t st, HszgErr* err) {
+    static const char* off = getenv("HSZG_P2_NARROW");       // "0": always int32 (A/B runs)
+    if ((off && off[0] == '0') || g->dims[2] % 8) return 0;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+        cudaGetLastError();
+        return 0;
+    }
+    if (cudaMemsetAsync(flag, 0, sizeof(int32_t), st) != cudaSuccess) return -HSZG_CUDA;
+    const int rr = hszg_band_scan(g, s, br, p16, A, nullptr, 1, flag, 0, st, err);
+    if (rr) return -rr;
+    int32_t h = 0;
+    if (cudaMemcpyAsync(&h, flag, sizeof(h), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return -HSZG_CUDA;
+    return h == 0 ? 1 : 0;
+}
+
 template <typename OutT>
 static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, void* ws, size_t ws_bytes,
                              cudaStream_t st, HszgErr* err) {
@@ -1257,6 +1290,27 @@ static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, 
                 const int64_t br = recon_band_rows(sg.n[0], sg.n[1], sg.n[2]);
                 const int64_t nb = (sg.n[1] + br - 1) / br;
                 const size_t need = (sizeof(OutT) == 4 ? 0 : n4) + (size_t)sg.n[0] * nb * sg.n[2] * 4;
+                // narrow first: int16 P2 in the workspace (n4 bytes for fp64 outputs, else n * 2), then A, flag
+                const size_t p2b = sizeof(OutT) == 4 ? (((size_t)g->n * 2 + 255) & ~(size_t)255) : n4;
+                const size_t abytes = (size_t)sg.n[0] * nb * sg.n[2] * 4;
+                if (ws_bytes >= p2b + abytes + 256) {
+                    int16_t* p16 = reinterpret_cast<int16_t*>(ws);
+                    int32_t* A16 = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ws) + p2b);
+                    int32_t* flag = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ws) + p2b + abytes);
+                    const int nr_ = band_scan_narrow(g, s, br, p16, A16, flag, st, err);
+                    if (nr_ < 0) return -nr_;
+                    if (nr_ == 1) {
+                        const unsigned blocks = (unsigned)((sg.n[1] * sg.n[2] / 4 + 255) / 256);
+                        if (nb == 1)
+                            k_col_scan_v4<OutT, false, int16_t><<<blocks, 256, 0, st>>>(
+                                p16, nullptr, sg.n[0], sg.n[1], sg.n[2], br, nb, two_eps, out);
+                        else
+                            k_col_scan_v4<OutT, true, int16_t><<<blocks, 256, 0, st>>>(
+                                p16, A16, sg.n[0], sg.n[1], sg.n[2], br, nb, two_eps, out);
+                        HSZG_CHECK_LAUNCH("z scan (int16)");
+                        return HSZG_OK;
+                    }
+                }
                 if (ws_bytes >= need) {
                     int32_t* buf = sizeof(OutT) == 4 ? reinterpret_cast<int32_t*>(out) : reinterpret_cast<int32_t*>(ws);
                     int32_t* A = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ws) + (sizeof(OutT) == 4 ? 0 : n4));
@@ -1556,10 +1610,21 @@ extern "C" int hszg_quantized_sums(const HszgGeom* g, const HszgStream* s, HszgS
     int32_t* A = reinterpret_cast<int32_t*>(w + (size_t)g->n * 4);
     HszgSums* partials = reinterpret_cast<HszgSums*>(w + (((size_t)g->n * 4 + (size_t)sg.n[0] * sg.n[2] * 4 + 255) &
                                                           ~(size_t)255));
-    const int rr = hszg_band_scan(g, s, sg.n[1], L, A, nullptr, 0, nullptr, 0, st, err);
-    if (rr) return rr;
     const int64_t Lc = sg.n[1] * sg.n[2];
     const int64_t nblk = (Lc + 255) / 256;
+    if ((size_t)g->n >= 256) {   // int16 P2 in the first half of L's space, the flag after it (band_scan_narrow)
+        int16_t* p16 = reinterpret_cast<int16_t*>(w);
+        int32_t* flag = reinterpret_cast<int32_t*>(w + (((size_t)g->n * 2 + 255) & ~(size_t)255));
+        const int nr_ = band_scan_narrow(g, s, sg.n[1], p16, A, flag, st, err);
+        if (nr_ < 0) return -nr_;
+        if (nr_ == 1) {
+            k_col_scan_sums<int16_t><<<(unsigned)nblk, 256, 0, st>>>(p16, sg.n[0], Lc, partials);
+            HSZG_CHECK_LAUNCH("quantized sums hszp-nd (int16)");
+            return hszg_finalize_sums(partials, nblk, out_dev, st);
+        }
+    }
+    const int rr = hszg_band_scan(g, s, sg.n[1], L, A, nullptr, 0, nullptr, 0, st, err);
+    if (rr) return rr;
     k_col_scan_sums<<<(unsigned)nblk, 256, 0, st>>>(L, sg.n[0], Lc, partials);
     HSZG_CHECK_LAUNCH("quantized sums hszp-nd");
     return hszg_finalize_sums(partials, nblk, out_dev, st);

@@ -389,6 +389,26 @@ def test_regions_vs_oracle(H, rng, kind, dims, region):
     np.testing.assert_array_equal(g, O.gradient_magnitude(q, c.eps))
 
 
+@pytest.mark.parametrize("case", ["smooth", "noise"])
+@pytest.mark.parametrize("dims", [(12, 20, 64), (40, 16, 32)])
+def test_hszp_nd_narrow_prefix_and_fallback(H, rng, case, dims):
+    """3-D HSZP_ND stage 3 / 4 and variance run the band scan with int16 band-local prefixes (P2 = q[z] - q[z-1])
+    and fall back to int32 when one does not fit (the noisy field at a tight bound: |P2| >> 2^15); both equal the
+    oracle bit for bit."""
+    field = O.random_field(rng, dims, case) * (np.float32(1.0) if case == "smooth" else np.float32(1e4))
+    bound = H.h.ErrorBound("rel", 1e-3 if case == "smooth" else 1e-7)
+    c = H.h.compress(field, H.h.CompressorKind.HSZP_ND, bound)
+    oc = _oracle_of(c)
+    q = O.stage3(oc)
+    if case == "noise":
+        assert np.abs(np.diff(q.astype(np.int64), axis=0)).max() > 2**15       # the int32 fallback runs
+    got = H.h.partial_decompress(c, H.h.Stage.QUANTIZED).values
+    assert np.array_equal(got, q)
+    f4 = H.h.partial_decompress(c, H.h.Stage.FULL)
+    assert np.array_equal(getattr(f4, "values", f4), O.stage4(oc, q))
+    assert H.stats.compute_stat(c, "var", H.h.Stage.QUANTIZED).value == O.compute_stat(oc, "var", 3)
+
+
 @pytest.mark.parametrize("case", ["nd8", "nd4", "nd2x4x8", "x1d"])
 def test_regions_equal_blocks_vs_oracle(H, rng, monkeypatch, case):
     """Regions that are exactly the stream's blocks (HSZX_ND 8^3: 16 chunks per block; 4^3: 2; 2x4x8: 2; HSZX 1-D
