@@ -382,34 +382,50 @@ __global__ void __launch_bounds__(TILE_CHUNKS) k_tile_scan_fast(const uint8_t* _
     }
 }
 
+// 4 values of a P2 row: int32 (16 B) or int16 (8 B, the narrow band-local prefixes)
+__device__ __forceinline__ int4 ld_p2x4(const int32_t* p) { return __ldg(reinterpret_cast<const int4*>(p)); }
+__device__ __forceinline__ int4 ld_p2x4(const int16_t* p) {
+    const uint2 h = __ldg(reinterpret_cast<const uint2*>(p));
+    return make_int4((int32_t)(int16_t)(h.x & 0xffffu), (int32_t)h.x >> 16, (int32_t)(int16_t)(h.y & 0xffffu),
+                     (int32_t)h.y >> 16);
+}
+
 // z prefix (one band per plane: L is the plane's 2-D prefix) reduced instead of stored
-template <typename SrcT = int32_t>
-__global__ void __launch_bounds__(256) k_col_scan_sums(const SrcT* __restrict__ src, int64_t M, int64_t Lc,
-                                                       HszgSums* partials) {
-    const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+// (four columns per thread: one 16-B / 8-B load per plane; Lc % 4 == 0 and a 16-B aligned src)
+template <typename SrcT>
+__global__ void __launch_bounds__(256) k_col_scan_sums_v4(const SrcT* __restrict__ src, int64_t M, int64_t Lc,
+                                                          HszgSums* partials) {
+    const int64_t l = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
     int64_t s1 = 0;
     u128 s2 = 0;
     int mn = INT32_MAX, mx = INT32_MIN;
     if (l < Lc) {
-        uint32_t acc = 0;
-        int64_t m = 0;
-        auto take = [&](uint32_t v) {
-            acc += v;
-            const int q = (int)acc;
-            s1 += q;
-            s2 += (u128)(uint64_t)((int64_t)q * q);
-            mn = min(mn, q);
-            mx = max(mx, q);
+        uint32_t acc[4] = {0, 0, 0, 0};
+        const SrcT* c = src + l;
+        auto take = [&](int4 v) {
+            const uint32_t w[4] = {(uint32_t)v.x, (uint32_t)v.y, (uint32_t)v.z, (uint32_t)v.w};
+            uint64_t sq = 0;                    // four squares < 2^64 (|q| <= 2^31)
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                acc[j] += w[j];
+                const int q = (int)acc[j];
+                s1 += q;
+                sq += (uint64_t)((int64_t)q * q);
+                mn = min(mn, q);
+                mx = max(mx, q);
+            }
+            s2 += (u128)sq;
         };
+        int64_t m = 0;
         for (; m + 4 <= M; m += 4) {
-            const uint32_t v0 = (uint32_t)(int32_t)__ldg(src + m * Lc + l), v1 = (uint32_t)(int32_t)__ldg(src + (m + 1) * Lc + l);
-            const uint32_t v2 = (uint32_t)(int32_t)__ldg(src + (m + 2) * Lc + l), v3 = (uint32_t)(int32_t)__ldg(src + (m + 3) * Lc + l);
+            const int4 v0 = ld_p2x4(c + m * Lc), v1 = ld_p2x4(c + (m + 1) * Lc);
+            const int4 v2 = ld_p2x4(c + (m + 2) * Lc), v3 = ld_p2x4(c + (m + 3) * Lc);
             take(v0);
             take(v1);
             take(v2);
             take(v3);
         }
-        for (; m < M; m++) take((uint32_t)(int32_t)__ldg(src + m * Lc + l));
+        for (; m < M; m++) take(ld_p2x4(c + m * Lc));
     }
     Acc a;
     a.init();
@@ -418,9 +434,8 @@ __global__ void __launch_bounds__(256) k_col_scan_sums(const SrcT* __restrict__ 
     a.vmin = mn;
     a.vmax = mx;
     block_reduce(a);
-    // counts are summed by the finalizer: each CTA contributes its active columns x M
-    const int64_t active = (Lc - blockIdx.x * (int64_t)blockDim.x) < blockDim.x ? (Lc - blockIdx.x * (int64_t)blockDim.x)
-                                                                              : blockDim.x;
+    const int64_t cols = Lc - 4 * blockIdx.x * (int64_t)blockDim.x;
+    const int64_t active = cols < 4 * (int64_t)blockDim.x ? cols : 4 * (int64_t)blockDim.x;
     if (threadIdx.x == 0) {
         a.count = active * M;
         store_sums(partials + blockIdx.x, a);
@@ -942,14 +957,6 @@ __device__ __forceinline__ void store4(OutT* d, const uint32_t (&v)[4], double t
             *reinterpret_cast<double2*>(d + j) =
                 make_double2(Conv<OutT>::go((int32_t)v[j], two_eps), Conv<OutT>::go((int32_t)v[j + 1], two_eps));
     }
-}
-
-// 4 values of a P2 row: int32 (16 B) or int16 (8 B, the narrow band-local prefixes)
-__device__ __forceinline__ int4 ld_p2x4(const int32_t* p) { return __ldg(reinterpret_cast<const int4*>(p)); }
-__device__ __forceinline__ int4 ld_p2x4(const int16_t* p) {
-    const uint2 h = __ldg(reinterpret_cast<const uint2*>(p));
-    return make_int4((int32_t)(int16_t)(h.x & 0xffffu), (int32_t)h.x >> 16, (int32_t)(int16_t)(h.y & 0xffffu),
-                     (int32_t)h.y >> 16);
 }
 
 template <typename OutT, bool BANDS, typename SrcT = int32_t>
@@ -1611,21 +1618,22 @@ extern "C" int hszg_quantized_sums(const HszgGeom* g, const HszgStream* s, HszgS
     HszgSums* partials = reinterpret_cast<HszgSums*>(w + (((size_t)g->n * 4 + (size_t)sg.n[0] * sg.n[2] * 4 + 255) &
                                                           ~(size_t)255));
     const int64_t Lc = sg.n[1] * sg.n[2];
-    const int64_t nblk = (Lc + 255) / 256;
     if ((size_t)g->n >= 256) {   // int16 P2 in the first half of L's space, the flag after it (band_scan_narrow)
         int16_t* p16 = reinterpret_cast<int16_t*>(w);
         int32_t* flag = reinterpret_cast<int32_t*>(w + (((size_t)g->n * 2 + 255) & ~(size_t)255));
         const int nr_ = band_scan_narrow(g, s, sg.n[1], p16, A, flag, st, err);
         if (nr_ < 0) return -nr_;
         if (nr_ == 1) {
-            k_col_scan_sums<int16_t><<<(unsigned)nblk, 256, 0, st>>>(p16, sg.n[0], Lc, partials);
+            const int64_t nb4 = (Lc / 4 + 255) / 256;           // n2 % 32 == 0: Lc % 4 == 0
+            k_col_scan_sums_v4<int16_t><<<(unsigned)nb4, 256, 0, st>>>(p16, sg.n[0], Lc, partials);
             HSZG_CHECK_LAUNCH("quantized sums hszp-nd (int16)");
-            return hszg_finalize_sums(partials, nblk, out_dev, st);
+            return hszg_finalize_sums(partials, nb4, out_dev, st);
         }
     }
     const int rr = hszg_band_scan(g, s, sg.n[1], L, A, nullptr, 0, nullptr, 0, st, err);
     if (rr) return rr;
-    k_col_scan_sums<<<(unsigned)nblk, 256, 0, st>>>(L, sg.n[0], Lc, partials);
+    const int64_t nb4 = (Lc / 4 + 255) / 256;
+    k_col_scan_sums_v4<int32_t><<<(unsigned)nb4, 256, 0, st>>>(L, sg.n[0], Lc, partials);
     HSZG_CHECK_LAUNCH("quantized sums hszp-nd");
-    return hszg_finalize_sums(partials, nblk, out_dev, st);
+    return hszg_finalize_sums(partials, nb4, out_dev, st);
 }
