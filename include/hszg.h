@@ -146,6 +146,11 @@ int hszg_encode_pack(const HszgGeom* g, const int32_t* p, const uint64_t* offset
 /* Stage 3 (out_type HSZG_I32, q row-major) or stage 4 (HSZG_F32/F64 = q*(2*eps)). */
 int hszg_reconstruct(const HszgGeom* g, const HszgStream* s, void* out, int out_type, void* ws,
                      size_t ws_bytes, void* stream, HszgErr* err);
+/* hszg_reconstruct of a z-slab sub-stream of a 3-D HSZP_ND field (canonical, n2 % 32 == 0) with the slab's carry
+ * q[z0-1] (n1*n2 int32, 16-B aligned) folded into the z prefix: the slab's global q without a separate
+ * add pass (stages.py:193-204 slab iteration).  HSZG_UNSUPPORTED_STAGE for other streams. */
+int hszg_reconstruct_carry(const HszgGeom* g, const HszgStream* s, void* out, int out_type, const int32_t* carry,
+                           void* ws, size_t ws_bytes, void* stream, HszgErr* err);
 /* recorrelate (compressors.py:201-226) of a decoded stream-order residual array p (not overwritten). */
 int hszg_recorrelate(const HszgGeom* g, const int32_t* p, const int32_t* metadata, void* out, int out_type, void* ws,
                      size_t ws_bytes, void* stream, HszgErr* err);

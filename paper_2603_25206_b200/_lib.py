@@ -122,6 +122,8 @@ _SIGS = {
     "hszg_encode_pack": [ctypes.POINTER(Geom), _P, _P, _P, _P, _P, ctypes.POINTER(Err)],
     "hszg_reconstruct": [ctypes.POINTER(Geom), ctypes.POINTER(StreamDesc), _P, _I32, _P, _SZ, _P,
                          ctypes.POINTER(Err)],
+    "hszg_reconstruct_carry": [ctypes.POINTER(Geom), ctypes.POINTER(StreamDesc), _P, _I32, _P, _P, _SZ, _P,
+                               ctypes.POINTER(Err)],
     "hszg_dequantize": [_P, _I64, _D, _P, _I32, _P],
     "hszg_recorrelate": [ctypes.POINTER(Geom), _P, _P, _P, _I32, _P, _SZ, _P, ctypes.POINTER(Err)],
     "hszg_add_plane": [_P, _P, _I64, _I64, _P],

@@ -962,7 +962,7 @@ __device__ __forceinline__ void store4(OutT* d, const uint32_t (&v)[4], double t
 template <typename OutT, bool BANDS, typename SrcT = int32_t>
 __global__ void __launch_bounds__(256) k_col_scan_v4(const SrcT* src, const int32_t* __restrict__ A, int64_t M,
                                                      int64_t n1, int64_t n2, int64_t BR, int64_t nb, double two_eps,
-                                                     OutT* dst) {
+                                                     OutT* dst, const int32_t* __restrict__ carry = nullptr) {
     const int64_t Lc = n1 * n2;
     const int64_t l = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
     if (l >= Lc) return;
@@ -976,6 +976,13 @@ __global__ void __launch_bounds__(256) k_col_scan_v4(const SrcT* src, const int3
         as = nb * n2;
     }
     uint32_t acc[4] = {0, 0, 0, 0};
+    if (carry) {                                 // q of the plane before the stream's first (a slab's carry)
+        const int4 c = __ldg(reinterpret_cast<const int4*>(carry + l));
+        acc[0] = (uint32_t)c.x;
+        acc[1] = (uint32_t)c.y;
+        acc[2] = (uint32_t)c.z;
+        acc[3] = (uint32_t)c.w;
+    }
     constexpr int U = 4;
     int64_t m = 0;
     for (; m + U <= M; m += U) {
@@ -1266,13 +1273,17 @@ static int band_scan_narrow(const HszgGeom* g, const HszgStream* s, int64_t br, 
 
 template <typename OutT>
 static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, void* ws, size_t ws_bytes,
-                             cudaStream_t st, HszgErr* err) {
+                             cudaStream_t st, HszgErr* err, const int32_t* carry = nullptr) {
     const SegGeo sg = make_seggeo(*g);
     const double two_eps = 2.0 * g->eps;
     if (g->n == 0) return HSZG_OK;
     const size_t smem = tile_smem_bytes(s->max_bitwidth);
     const int64_t tiles = (g->n_chunks + TILE_CHUNKS - 1) / TILE_CHUNKS;
     const bool fast = s->canonical != 0;
+    // a carry plane (hszg_reconstruct_carry) is folded into the HSZP_ND band-scan z prefix only
+    const bool band_path = fast && g->kind == HSZG_HSZP_ND && g->ndims == 3 && sg.n[2] % 32 == 0 &&
+                           sg.n[2] <= 4096 && sg.n[0] <= 65535;
+    if (carry && (!band_path || (reinterpret_cast<uintptr_t>(carry) & 15))) return HSZG_UNSUPPORTED_STAGE;
     switch (g->kind) {
         case HSZG_HSZX:
             if (fast && stream_full_ok(g, sg, out) && !sf_off()) {
@@ -1310,10 +1321,10 @@ static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, 
                         const unsigned blocks = (unsigned)((sg.n[1] * sg.n[2] / 4 + 255) / 256);
                         if (nb == 1)
                             k_col_scan_v4<OutT, false, int16_t><<<blocks, 256, 0, st>>>(
-                                p16, nullptr, sg.n[0], sg.n[1], sg.n[2], br, nb, two_eps, out);
+                                p16, nullptr, sg.n[0], sg.n[1], sg.n[2], br, nb, two_eps, out, carry);
                         else
                             k_col_scan_v4<OutT, true, int16_t><<<blocks, 256, 0, st>>>(
-                                p16, A16, sg.n[0], sg.n[1], sg.n[2], br, nb, two_eps, out);
+                                p16, A16, sg.n[0], sg.n[1], sg.n[2], br, nb, two_eps, out, carry);
                         HSZG_CHECK_LAUNCH("z scan (int16)");
                         return HSZG_OK;
                     }
@@ -1325,14 +1336,14 @@ static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, 
                     if (rr) return rr;
                     const int64_t Lc = sg.n[1] * sg.n[2];
                     static const int v4 = getenv("HSZG_COLSCAN_V4") ? atoi(getenv("HSZG_COLSCAN_V4")) : 1;
-                    if (v4) {               // n2 % 32 == 0: whole int4 groups, 16-byte aligned planes
+                    if (v4 || carry) {      // n2 % 32 == 0: whole int4 groups, 16-byte aligned planes
                         const unsigned blocks = (unsigned)((Lc / 4 + 255) / 256);
                         if (nb == 1)
                             k_col_scan_v4<OutT, false><<<blocks, 256, 0, st>>>(buf, nullptr, sg.n[0], sg.n[1], sg.n[2],
-                                                                               br, nb, two_eps, out);
+                                                                               br, nb, two_eps, out, carry);
                         else
                             k_col_scan_v4<OutT, true><<<blocks, 256, 0, st>>>(buf, A, sg.n[0], sg.n[1], sg.n[2], br,
-                                                                              nb, two_eps, out);
+                                                                              nb, two_eps, out, carry);
                     } else if (nb == 1) {   // one band per plane: A holds zeros, the plain z prefix
                         launch_col_scan<OutT>(buf, 1, sg.n[0], sg.n[1] * sg.n[2], two_eps, out, st);
                     } else {
@@ -1343,6 +1354,7 @@ static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, 
                     return HSZG_OK;
                 }
             }
+            if (carry) return HSZG_UNSUPPORTED_STAGE;     // workspace too small for the band path
             break;
         case HSZG_HSZX_ND:
             if (fast && stream_full_ok(g, sg, out) && sg.B[2] % 4 == 0 && 32 % sg.B[2] == 0 && !sf_off()) {
@@ -1432,6 +1444,22 @@ extern "C" int hszg_reconstruct(const HszgGeom* g, const HszgStream* s, void* ou
         case HSZG_I32: return reconstruct_typed<int32_t>(g, s, reinterpret_cast<int32_t*>(out), ws, ws_bytes, st, err);
         case HSZG_F32: return reconstruct_typed<float>(g, s, reinterpret_cast<float*>(out), ws, ws_bytes, st, err);
         case HSZG_F64: return reconstruct_typed<double>(g, s, reinterpret_cast<double*>(out), ws, ws_bytes, st, err);
+        default:
+            err->status = HSZG_INVALID_ARG;
+            snprintf(err->message, sizeof(err->message), "unknown output type %d", out_type);
+            return HSZG_INVALID_ARG;
+    }
+}
+
+extern "C" int hszg_reconstruct_carry(const HszgGeom* g, const HszgStream* s, void* out, int out_type,
+                                      const int32_t* carry, void* ws, size_t ws_bytes, void* stream, HszgErr* err) {
+    err->status = HSZG_OK;
+    cudaStream_t st = as_stream(stream);
+    if (!carry) return hszg_reconstruct(g, s, out, out_type, ws, ws_bytes, stream, err);
+    switch (out_type) {
+        case HSZG_I32: return reconstruct_typed<int32_t>(g, s, reinterpret_cast<int32_t*>(out), ws, ws_bytes, st, err, carry);
+        case HSZG_F32: return reconstruct_typed<float>(g, s, reinterpret_cast<float*>(out), ws, ws_bytes, st, err, carry);
+        case HSZG_F64: return reconstruct_typed<double>(g, s, reinterpret_cast<double*>(out), ws, ws_bytes, st, err, carry);
         default:
             err->status = HSZG_INVALID_ARG;
             snprintf(err->message, sizeof(err->message), "unknown output type %d", out_type);

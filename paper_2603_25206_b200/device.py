@@ -160,8 +160,9 @@ class DeviceStream:
                   _lib.stream_handle(), ctypes.byref(err), err=err)
         return out
 
-    def reconstruct(self, dtype=None, out=None):
-        """Stage 3 (int32 q, row-major grid) or stage 4 (float32/float64 q*2eps)."""
+    def reconstruct(self, dtype=None, out=None, carry=None):
+        """Stage 3 (int32 q, row-major grid) or stage 4 (float32/float64 q*2eps).  carry: q of the plane before
+        this sub-stream's first (3-D HSZP_ND slabs, `carry_ok`), folded into the z prefix."""
         t = _t()
         self.validate()
         dtype = dtype or t.int32
@@ -170,9 +171,19 @@ class DeviceStream:
             out = t.empty(self.dims, dtype=dtype, device=_lib.device())
         ws = _lib.workspace(_lib.ws_bytes(self.geom, self.desc, _lib.WS_RECONSTRUCT, code))
         err = _lib.Err()
-        _lib.call("hszg_reconstruct", ctypes.byref(self.geom), ctypes.byref(self.desc), _lib.ptr(out), code,
-                  _lib.ptr(ws), ws.numel(), _lib.stream_handle(), ctypes.byref(err), err=err)
+        if carry is None:
+            _lib.call("hszg_reconstruct", ctypes.byref(self.geom), ctypes.byref(self.desc), _lib.ptr(out), code,
+                      _lib.ptr(ws), ws.numel(), _lib.stream_handle(), ctypes.byref(err), err=err)
+        else:
+            _lib.call("hszg_reconstruct_carry", ctypes.byref(self.geom), ctypes.byref(self.desc), _lib.ptr(out), code,
+                      _lib.ptr(carry), _lib.ptr(ws), ws.numel(), _lib.stream_handle(), ctypes.byref(err), err=err)
         return out
+
+    def carry_ok(self) -> bool:
+        """reconstruct(carry=...) applies: a canonical 3-D HSZP_ND stream whose rows are whole chunks."""
+        self.validate()
+        return (self.kind == 1 and len(self.dims) == 3 and bool(self.desc.canonical) and self.dims[2] % 32 == 0
+                and self.dims[2] <= 4096 and self.dims[0] <= 65535)
 
     # ---- reductions --------------------------------------------------------------
 

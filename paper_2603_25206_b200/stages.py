@@ -323,6 +323,14 @@ def _slab_iter_batched(c: CompressedStream, stage: Stage, out: str, bounds: list
             sub = src.span(k, j)
         if stage == Stage.DECORRELATED:
             vals = sub.decode()
+        elif c.kind == CompressorKind.HSZP_ND and carry is not None and sub.carry_ok():
+            # the previous batch's last plane folded into this batch's z prefix (no separate add pass)
+            vals = sub.reconstruct(t.int32, carry=carry)
+            carry = vals.reshape(bhi - blo, -1)[-1].clone()
+            if stage == Stage.FULL:
+                from .quant import dequantize_device
+
+                vals = dequantize_device(vals, c.eps)
         else:
             vals = sub.reconstruct(t.int32)
             if c.kind == CompressorKind.HSZP:

@@ -119,3 +119,34 @@ def test_pinned_file_io_roundtrip(tmp_path, kind):
     assert pc2._device is None
     bc = io.read_compressed(path, pinned=False)
     assert isinstance(bc.payload, bytes) and bc.pinned_payload() is None
+
+
+@pytest.mark.parametrize("stage", [3, 4])
+def test_slab_batches_fold_the_carry(monkeypatch, stage):
+    """3-D HSZP_ND slab iteration in several launch groups: every group after the first reconstructs with the
+    previous group's last plane folded into its z prefix (hszg_reconstruct_carry); the slabs equal the oracle's."""
+    import paper_2603_25206_b200 as h
+    from paper_2603_25206_b200 import _lib, io as hio, stages
+
+    rng = np.random.default_rng(31)
+    dims = (21, 12, 64)
+    f = O.random_field(rng, dims, "smooth")
+    c = h.compress(f, h.CompressorKind.HSZP_ND, h.ErrorBound("rel", 1e-3))
+    monkeypatch.setattr(stages, "SLAB_BATCH_BYTES", 4 * 12 * 64 * 3)       # three planes per launch group
+    calls = []
+    real = _lib.call
+
+    def spy(name, *a, **k):
+        calls.append(name)
+        return real(name, *a, **k)
+
+    monkeypatch.setattr(_lib, "call", spy)
+    oc = O.stream_from_bytes(hio.stream_to_bytes(c))
+    q = O.stage3(oc)
+    want = q if stage == 3 else O.stage4(oc, q)
+    got = np.concatenate([np.asarray(s) for s in h.slab_iter(c, h.Stage(stage))])
+    assert calls.count("hszg_reconstruct_carry") >= 6
+    if stage == 3:
+        assert np.array_equal(got.reshape(dims), want)
+    else:
+        assert np.array_equal(got.reshape(dims), want.astype(got.dtype))
