@@ -105,6 +105,17 @@ struct GeoSpans {
     SegGeo sg;
     __device__ __forceinline__ ChunkLoc get(int64_t c) const { return locate_chunk(sg, c); }
 };
+// every chunk full (every segment size a multiple of 32): chunk c = values 32c .. 32c+31, no geometry math
+struct FullSpans {
+    __device__ __forceinline__ ChunkLoc get(int64_t c) const {
+        ChunkLoc L;
+        L.start = c * kChunkCap;
+        L.count = kChunkCap;
+        L.seg = 0;
+        L.j = 0;
+        return L;
+    }
+};
 struct ArrSpans {
     const int64_t* st;
     const int64_t* en;
@@ -523,8 +534,14 @@ extern "C" int hszg_validate(const HszgGeom* g, HszgStream* s, void* ws, size_t 
     err->status = HSZG_OK;
     GeoSpans sp{make_seggeo(*g)};
     int canonical = 0, max_bw = 0;
-    int r = validate_impl(sp, g->n_chunks, s->payload, s->payload_len, s->offsets, ws, ws_bytes,
-                          as_stream(stream), err, &canonical, &max_bw);
+    bool full = g->n_chunks * kChunkCap == g->n;
+    for (int k = 0; k < 8 && full; k++) full = sp.sg.cpb[k] * kChunkCap == (((k >> 2) & 1 ? sp.sg.E[0] : sp.sg.B[0]) *
+                                                                      ((k >> 1) & 1 ? sp.sg.E[1] : sp.sg.B[1]) *
+                                                                      (k & 1 ? sp.sg.E[2] : sp.sg.B[2]));
+    int r = full ? validate_impl(FullSpans{}, g->n_chunks, s->payload, s->payload_len, s->offsets, ws, ws_bytes,
+                                 as_stream(stream), err, &canonical, &max_bw)
+                 : validate_impl(sp, g->n_chunks, s->payload, s->payload_len, s->offsets, ws, ws_bytes,
+                                 as_stream(stream), err, &canonical, &max_bw);
     s->canonical = canonical;
     s->max_bitwidth = max_bw;
     return r;
