@@ -636,8 +636,10 @@ CPU_SECONDS = 10.0
 
 def measured_traffic(op, dims, world, window):
     """DRAM bytes per step of an op from the committed ncu `--set full` captures of its kernels
-    (profiles/r01_traffic.json), when they were taken on this exact shape (config 5, 1 GPU, W = 64)."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")
+    (profiles/r02_traffic.json; r01_traffic.json as a fallback), when they were taken on this exact shape (config 5, 1 GPU, W = 64)."""
+    prof = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles")
+    name = "r02_traffic.json" if os.path.exists(os.path.join(prof, "r02_traffic.json")) else "r01_traffic.json"
+    path = os.path.join(prof, name)
     try:
         with open(path) as f:
             rec = json.load(f)["ops"].get(op)
@@ -646,7 +648,7 @@ def measured_traffic(op, dims, world, window):
     if rec is None or tuple(dims) != (2048, 2048, 2048) or world != 1 or window != 64:
         return None
     return {"traffic_bytes_per_step": int(rec["traffic_bytes_per_step"]),
-            "source": "profiles/r01_traffic.json: ncu --set full of " + ", ".join(rec["kernels"])}
+            "source": f"profiles/{name}: ncu --set full of " + ", ".join(rec["kernels"])}
 
 
 def build_cpu_sample(field_dev, eps):
