@@ -380,9 +380,8 @@ extern "C" int hszg_fused_blocks(const HszgGeom* g, const HszgStream* s, int64_t
         !al16f(s->metadata) || !al16f(s->payload)) {
         err->status = HSZG_INVALID_ARG;
         snprintf(err->message, sizeof(err->message),
-                 "fused_blocks needs a canonical 3-D HSZX_ND stream with 8x8x8 blocks dividing the box, 16-B "
-                 "aligned buffers, outputs {dz, dy, dx, lap}, {dz, dy, dx} or {lap} and staging that fits shared "
-                 "memory (max bit width %d)", s->max_bitwidth);
+                 "fused_blocks: needs canonical 3-D HSZX_ND, 8^3 blocks dividing the box, 16-B aligned buffers, "
+                 "outputs all / {dz,dy,dx} / {lap}, staging in smem (max bw %d)", s->max_bitwidth);
         return HSZG_INVALID_ARG;
     }
     if (g->n == 0) return HSZG_OK;
