@@ -326,9 +326,11 @@ __global__ void __launch_bounds__(FX_T, 1) k_fused_blocks(FxArgs a, uint32_t buf
                 else
                     emit4f(a.o0, a.o1, a.o2, a.o3, o, zin, yin, x, a.n2, zm, c, zp, ym, yp, left, right, a.eps,
                            two_eps, epsf, two_epsf);
-                if (Exact) st.add4(c);                    // stats always kept (acc may be null)
-                else st.add4f(c);
-                count += 4;
+                if (OM == OM_ALL || a.acc) {              // the API's subsets pass no accumulator: no statistics
+                    if (Exact) st.add4(c);
+                    else st.add4f(c);
+                    count += 4;
+                }
             }
         }
         if (!Exact && (z & 15) == 15) st.fold();   // <= 32 add4f between folds
