@@ -265,6 +265,19 @@ int hszg_decorrelate_sized(const HszgGeom* g, const int32_t* q, int32_t* p, int3
 /* Exclusive scan of precomputed chunk sizes (in place: sizes -> offsets) and the payload total. */
 int hszg_encode_offsets(const HszgGeom* g, uint64_t* offsets, uint64_t* total_host, void* ws, size_t ws_bytes,
                         void* stream, HszgErr* err);
+/* One-pass compress (csrc/compress.cu) of a float32 field: quantize (quant.py:69-82) + decorrelate
+ * (compressors.py:149-198) + encode_stream (codec.py:84-106, _bitpack.pyx:24-87) in one kernel, replacing
+ * the chain hszg_quantize_f32 -> hszg_decorrelate_sized -> hszg_encode_offsets -> hszg_encode_pack.
+ * hszg_compress_plan returns 1 when the geometry has a one-pass front (every chunk 32 values; HSZP,
+ * HSZP_ND with n2 % 32 == 0 and n2 <= 8192, HSZX / HSZX_ND with full blocks of 32k <= 8192 values,
+ * B2 % 4 == 0) and the workspace / payload capacity it needs (n_chunks * 133 + HSZG_PAYLOAD_PAD: the
+ * worst case, the payload length is known only after the pass), else 0.  hszg_compress_fused writes
+ * the payload (its length to *total_host, the pad zeroed), the chunk offsets and the block means;
+ * synchronous status with the messages of the chain (EpsTooSmallError / ValueError). */
+int hszg_compress_plan(const HszgGeom* g, uint64_t* ws_bytes, uint64_t* payload_capacity);
+int hszg_compress_fused(const HszgGeom* g, const float* field, double recip, uint8_t* payload, uint64_t capacity,
+                        uint64_t* offsets, int32_t* metadata, uint64_t* total_host, void* ws, size_t ws_bytes,
+                        void* stream, HszgErr* err);
 
 /* ---- windowed 3-D pipeline (pipeline.py; Algorithm 3 on the device) -------------------------- */
 /* fp32 outputs: exact != 0 gives fl32(fl64(D*eps)) (one rounding of the reference float64); exact == 0

@@ -156,6 +156,9 @@ _SIGS = {
                                ctypes.POINTER(Err)],
     "hszg_encode_offsets": [ctypes.POINTER(Geom), _P, ctypes.POINTER(ctypes.c_uint64), _P, _SZ, _P,
                             ctypes.POINTER(Err)],
+    "hszg_compress_plan": [ctypes.POINTER(Geom), ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)],
+    "hszg_compress_fused": [ctypes.POINTER(Geom), _P, _D, _P, ctypes.c_uint64, _P, _P, ctypes.POINTER(ctypes.c_uint64),
+                            _P, _SZ, _P, ctypes.POINTER(Err)],
     "hszg_acc_reset": [_P, _P],
     "hszg_zgrad_lap": [_P, _I64, _I64, _I64, _I64, _I64, _I64, _D, _P, _P, _P, _P, _I32, _P],
     "hszg_zsweep_grad_lap": [_P, _I64, _I64, _I64, _P, _P, _P, _P, _I64, _I64, _D, _P, _P, _P, _P, _I64, _I32, _I32,

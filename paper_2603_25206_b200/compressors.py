@@ -16,6 +16,7 @@ and one read from bytes is uploaded once on first use.
 from __future__ import annotations
 
 import ctypes
+import os
 import enum
 from dataclasses import dataclass, field
 from functools import cached_property
@@ -398,6 +399,43 @@ class CompressedStream:
         return 4.0 * self.shape.total / self.byte_size()
 
 
+_ONE_PASS = os.environ.get("HSZG_COMPRESS", "") != "chain"      # "chain": the multi-kernel path (A/B, tests)
+_TRIM_BYTES = 1 << 30                    # a worst-case payload buffer wasting more than this is trimmed
+
+
+def _compress_one_pass(field_dev, kind: CompressorKind, shape: GridShape, eps: float, block_dims):
+    """One kernel from the float32 field to the container (csrc/compress.cu, hszg_compress_fused), or None
+    when the geometry has no one-pass front.  The payload is written into a worst-case buffer (its length
+    is known only after the pass) that is trimmed to size when that wastes more than _TRIM_BYTES."""
+    t = _lib.torch()
+    if not eps > 0:
+        raise ValueError(f"eps must be positive, got {eps}")
+    g = _lib.make_geom(int(kind), shape.dims, block_dims, eps)
+    wsb, cap = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    if not _lib.lib().hszg_compress_plan(ctypes.byref(g), ctypes.byref(wsb), ctypes.byref(cap)):
+        return None
+    flat = field_dev.reshape(-1)
+    if int(flat.data_ptr()) % 16:
+        return None
+    dev = _lib.device()
+    n_chunks = int(g.n_chunks)
+    offs = t.empty(max(n_chunks, 1), dtype=t.int64, device=dev)[:n_chunks]
+    meta = t.empty(max(int(g.n_blocks), 1), dtype=t.int32, device=dev) if kind.is_block_mean else None
+    payload = t.empty(int(cap.value), dtype=t.uint8, device=dev)
+    ws = _lib.workspace(int(wsb.value))
+    total = ctypes.c_uint64(0)
+    err = _lib.Err()
+    _lib.call("hszg_compress_fused", ctypes.byref(g), _lib.ptr(flat), 1.0 / (2.0 * eps), _lib.ptr(payload),
+              int(cap.value), _lib.ptr(offs), _lib.ptr(meta) if meta is not None else None, ctypes.byref(total),
+              _lib.ptr(ws), ws.numel(), _lib.stream_handle(), ctypes.byref(err), err=err)
+    plen = int(total.value)
+    if payload.numel() - (plen + _lib.PAYLOAD_PAD) > _TRIM_BYTES:
+        payload = payload[: plen + _lib.PAYLOAD_PAD].clone()
+    if meta is not None:
+        meta = meta[: int(g.n_blocks)]
+    return DeviceStream(int(kind), shape.dims, block_dims, eps, payload, plen, offs, meta)
+
+
 def compress_device(field_dev, kind: CompressorKind, eps: float, block_dims) -> DeviceStream:
     """Quantize + decorrelate + encode a CUDA float field into a DeviceStream (no host copies).  The
     decorrelation kernel also emits the chunk bit widths / sizes when every chunk is full
@@ -405,6 +443,10 @@ def compress_device(field_dev, kind: CompressorKind, eps: float, block_dims) -> 
     t = _lib.torch()
     kind = CompressorKind(kind)
     shape = GridShape(tuple(field_dev.shape))
+    if field_dev.dtype == t.float32 and _ONE_PASS:
+        ds = _compress_one_pass(field_dev, kind, shape, eps, block_dims)
+        if ds is not None:
+            return ds
     q = quantize_device(field_dev, eps)
     g = _lib.make_geom(int(kind), shape.dims, block_dims, eps)
     n_chunks = int(g.n_chunks)

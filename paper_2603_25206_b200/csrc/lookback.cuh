@@ -153,6 +153,37 @@ __device__ __forceinline__ uint32_t lookback_exclusive_warp32(const LBState& st,
     return excl;
 }
 
+// 62-bit variant (byte offsets): flag in bits 62-63, value in the low 62 bits, one 64-bit store per
+// publication and no fences (the single-copy atomic word carries flag and value together).
+__device__ __forceinline__ unsigned long long lookback_exclusive_warp62(const LBState& st, int64_t tile,
+                                                                        unsigned long long agg) {
+    const int lane = threadIdx.x & 31;
+    volatile unsigned long long* w = st.agg;
+    const unsigned long long AGG = 1ull << 62, INCL = 2ull << 62, VAL = (1ull << 62) - 1;
+    if (lane == 0) w[tile] = (tile == 0 ? INCL : AGG) | agg;
+    if (tile == 0) return 0ull;
+    unsigned long long excl = 0;
+    int64_t p = tile - 1;
+    while (true) {
+        const int64_t idx = p - lane;
+        const unsigned long long v = idx >= 0 ? w[idx] : INCL;   // before tile 0: inclusive 0
+        const unsigned f = (unsigned)(v >> 62);
+        const unsigned incl = __ballot_sync(0xffffffffu, f == 2);
+        const unsigned zero = __ballot_sync(0xffffffffu, f == 0);
+        const int k = incl ? __ffs(incl) - 1 : 31;
+        const unsigned need = (2u << k) - 1u;
+        if (zero & need) continue;
+        unsigned long long x = lane <= k ? (v & VAL) : 0ull;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) x += __shfl_xor_sync(0xffffffffu, x, d);
+        excl += x;
+        if (incl) break;
+        p -= 32;
+    }
+    if (lane == 0) w[tile] = INCL | (excl + agg);
+    return excl;
+}
+
 // block-wide exclusive scan of one u64 per thread; returns exclusive value, *total = block sum
 __device__ __forceinline__ unsigned long long block_exclusive_u64(unsigned long long v, unsigned long long* total) {
     __shared__ unsigned long long warp_tot[32];
