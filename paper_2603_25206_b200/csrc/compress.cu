@@ -310,8 +310,10 @@ __global__ void __launch_bounds__(CF_T, 768 / CF_T) k_compress_tiles(CfArgs a) {
                 const int xx = 4 * g, t = xx / B2, xl = xx - t * B2;
                 const bool bg = cf_big(vv[j], vlim);
                 big |= bg;
-                *reinterpret_cast<int4*>(cf_slot(P, (int64_t)t * segsz + zy * B2 + xl)) =
-                    bg ? cf_q4(vv[j], recip, f) : cf_qf4(vv[j], recip);
+                int4 q;
+                if (__any_sync(__activemask(), bg)) q = cf_q4(vv[j], recip, f);   // exact (range checks)
+                else q = cf_qf4(vv[j], recip);
+                *reinterpret_cast<int4*>(cf_slot(P, (int64_t)t * segsz + zy * B2 + xl)) = q;
             }
         }
         const bool exact = __syncthreads_or(big);                    // some |q| >= 2^28: int64 residual checks
@@ -330,7 +332,14 @@ __global__ void __launch_bounds__(CF_T, 768 / CF_T) k_compress_tiles(CfArgs a) {
         __syncthreads();
         if (c < nch) {
             const int blk = cpb == 1 ? c : c / cpb;
-            const int64_t mean = s_bsum[blk] / segsz;                // C division: truncation toward zero
+            const int64_t bs = s_bsum[blk];
+            int64_t mean;                                            // truncation toward zero (C division)
+            if ((segsz & (segsz - 1)) == 0) {
+                const int lg = __ffs(segsz) - 1;
+                mean = bs >= 0 ? (bs >> lg) : -((-bs) >> lg);
+            } else {
+                mean = bs / segsz;
+            }
             if (c == blk * cpb) a.meta[seg0 + blk] = (int32_t)mean;
             if (!exact) {
                 const int32_t m32 = (int32_t)mean;
@@ -385,7 +394,11 @@ __global__ void __launch_bounds__(CF_T, 768 / CF_T) k_compress_tiles(CfArgs a) {
     // warp 0 looks back for the tile's byte base while the other warps pack (the packed bytes do not depend
     // on the base: the staging copy starts at tile byte 0, the copy-out shifts it to the base's alignment)
     if (warp == 0) {
+#ifdef CF_NO_LOOKBACK                                                 // timing probe only (wrong offsets)
+        const unsigned long long base = (unsigned long long)tile * 20000ull;
+#else
         const unsigned long long base = lookback_exclusive_warp62(a.lb, tile, (unsigned long long)tot);
+#endif
         if (lane == 0) {
             s_base = base;
             if (tile == a.n_tiles - 1) *a.total = base + tot;
