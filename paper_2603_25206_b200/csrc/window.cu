@@ -300,7 +300,7 @@ constexpr int BS_MAXG = 4;   // int4 column groups per thread: n2 <= 4 * 4 * TIL
 constexpr int SE_W = 128;    // strip width of the strip-edge table (the one-pass HSZP_ND kernel's x tile)
 
 
-template <bool Edges, int LW, bool Full>
+template <bool Edges, int LW, bool Full, int KM>
 __global__ void __maxnreg__(56) k_band_scan(const uint8_t* __restrict__ payload, uint64_t len,
                                                           const uint64_t* __restrict__ offsets, int64_t n_chunks,
                                                           int n1, int n2, int BR, void* __restrict__ L,
@@ -316,7 +316,10 @@ __global__ void __maxnreg__(56) k_band_scan(const uint8_t* __restrict__ payload,
     const int cpr = n2 >> 5;                 // chunks per row (<= 128)
     const int rpt = TILE_CHUNKS / cpr;       // rows per tile (whole rows: rpt * cpr <= 256 chunks)
     const int ng = n2 >> 2;
-    const int kmax = (ng + TILE_CHUNKS - 1) / TILE_CHUNKS;   // column groups per thread (uniform)
+    // column groups per thread: KM = ceil(ng / 256) (launcher); this thread owns nk <= KM of them
+    int nk = KM;
+    if (!Full) nk = max(0, min(KM, (ng - (int)threadIdx.x + TILE_CHUNKS - 1) / TILE_CHUNKS));
+    const int toff0 = (int)(threadIdx.x >> 3) * kChunkStride + (int)((threadIdx.x & 7) << 2);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int32_t* tile = reinterpret_cast<int32_t*>(smem);
     uint8_t* SB = smem + kFastTileBytes;     // two staging buffers of sbytes: tile u in buffer u & 1
@@ -362,9 +365,9 @@ __global__ void __maxnreg__(56) k_band_scan(const uint8_t* __restrict__ payload,
         }
         uint64_t my_off = (int)threadIdx.x < tile_nch(0) ? __ldg(offsets + tile_c0(0) + threadIdx.x) : 0;
         __syncthreads();
-        int4 ysum[BS_MAXG];
+        int4 ysum[KM];
     #pragma unroll
-        for (int k = 0; k < BS_MAXG; k++) ysum[k] = make_int4(0, 0, 0, 0);
+        for (int k = 0; k < KM; k++) ysum[k] = make_int4(0, 0, 0, 0);
         for (int t = 0; t < ntiles; t++) {
             const int r0 = y0 + t * rpt;
             const int nr = min(rpt, y1 - r0);
@@ -421,52 +424,55 @@ __global__ void __maxnreg__(56) k_band_scan(const uint8_t* __restrict__ payload,
             }
             __syncthreads();
             const int nstrips = (n2 + SE_W - 1) / SE_W;
-            // rows of the tile: incremental row offsets, uniform k bound (no divergent skips when every
-            // thread owns kmax column groups: Full), narrow-range check by OR of v + 2^15 / 2^7 (bits >= 16 / 8
-            // flag it)
-            int64_t rowoff = (z * n1 + r0) * (int64_t)n2;
-            const int32_t* trow = tile;                   // tile row rr: chunks rr*cpr ..
-            const uint32_t* orow = s_off;
-            for (int rr = 0; rr < nr; rr++, rowoff += n2, trow += cpr * kChunkStride, orow += cpr) {
-                const int y = r0 + rr;
+            // rows of the tile.  Column group k of this thread is gi = tid + 256 k, i.e. chunk (tid >> 3) + 32 k,
+            // words 4 (tid & 7) ..: a per-thread base plus compile-time offsets, advanced by uniform row
+            // strides (the loop is unrolled over rows; threads without a column group skip it — there is
+            // no barrier inside).  Narrow-range check by OR of v + 2^15 / 2^7 (bits >= 16 / 8 flag it).
+            if (Full || nk > 0) {
+                const int32_t* tp = tile + toff0;              // tile row rr: chunks rr*cpr ..
+                const uint32_t* op = s_off + (threadIdx.x >> 3);
+                uint8_t* Lp = static_cast<uint8_t*>(L) + ((z * n1 + r0) * (int64_t)n2 + 4 * (int)threadIdx.x) * LW;
+    #pragma unroll 4
+                for (int rr = 0; rr < nr; rr++, tp += cpr * kChunkStride, op += cpr, Lp += (int64_t)n2 * LW) {
     #pragma unroll
-                for (int k = 0; k < BS_MAXG; k++) {
-                    if (k >= kmax) break;
-                    const int gi = threadIdx.x + k * TILE_CHUNKS;
-                    if (Full || gi < ng) {
-                        const int4 v = *reinterpret_cast<const int4*>(trow + (gi >> 3) * kChunkStride + ((gi & 7) << 2));
-                        const int4 rv = add4u(v, orow[gi >> 3]);      // row prefix R at x = 4gi .. 4gi+3
-                        ysum[k] = add4(ysum[k], rv);
-                        if (L && LW == 4) *reinterpret_cast<int4*>(static_cast<int32_t*>(L) + rowoff + 4 * gi) = ysum[k];
-                        if (L && LW == 2) {
-                            const int4 v4 = ysum[k];
-                            rng16 |= ((uint32_t)v4.x + 0x8000u) | ((uint32_t)v4.y + 0x8000u) | ((uint32_t)v4.z + 0x8000u) |
-                                     ((uint32_t)v4.w + 0x8000u);
-                            uint2 pk;                                                  // low halves, 2 PRMTs
-                            pk.x = __byte_perm((uint32_t)v4.x, (uint32_t)v4.y, 0x5410);
-                            pk.y = __byte_perm((uint32_t)v4.z, (uint32_t)v4.w, 0x5410);
-                            *reinterpret_cast<uint2*>(static_cast<int16_t*>(L) + rowoff + 4 * gi) = pk;
-                        }
-                        if (L && LW == 1) {
-                            const int4 v4 = ysum[k];
-                            rng16 |= ((uint32_t)v4.x + 0x80u) | ((uint32_t)v4.y + 0x80u) | ((uint32_t)v4.z + 0x80u) |
-                                     ((uint32_t)v4.w + 0x80u);
-                            const uint32_t lo = __byte_perm((uint32_t)v4.x, (uint32_t)v4.y, 0x0040);   // low bytes
-                            const uint32_t hi = __byte_perm((uint32_t)v4.z, (uint32_t)v4.w, 0x0040);
-                            *reinterpret_cast<uint32_t*>(static_cast<int8_t*>(L) + rowoff + 4 * gi) = __byte_perm(lo, hi, 0x5410);
-                        }
-                        if (Edges) {                                  // strip edges: E[s] = R(128s-1), F[s] = R(128s+128)
-                            const int xg = 4 * gi;
-                            const int64_t n1e = ((int64_t)n1 + 1) & ~(int64_t)1;   // even rows per strip block
-                            int32_t* ef = EF + ((z * nstrips) * n1e + y) * 2;
-                            if ((xg & (SE_W - 1)) == SE_W - 4 && (xg + 4) / SE_W < nstrips)
-                                ef[(int64_t)((xg + 4) / SE_W) * n1e * 2] = rv.w;
-                            if ((xg & (SE_W - 1)) == 0) {
-                                const int s2 = xg / SE_W;
-                                if (s2 > 0) ef[(int64_t)(s2 - 1) * n1e * 2 + 1] = rv.x;
-                                else {
-                                    ef[0] = 0;
-                                    ef[(int64_t)(nstrips - 1) * n1e * 2 + 1] = 0;
+                    for (int k = 0; k < KM; k++) {
+                        if (Full || k < nk) {
+                            const int4 v = *reinterpret_cast<const int4*>(tp + 32 * k * kChunkStride);
+                            const int4 rv = add4u(v, op[32 * k]);         // row prefix R at x = 4gi .. 4gi+3
+                            ysum[k] = add4(ysum[k], rv);
+                            uint8_t* Lk = Lp + (size_t)k * 4 * TILE_CHUNKS * LW;
+                            if (L && LW == 4) *reinterpret_cast<int4*>(Lk) = ysum[k];
+                            if (L && LW == 2) {
+                                const int4 v4 = ysum[k];
+                                rng16 |= ((uint32_t)v4.x + 0x8000u) | ((uint32_t)v4.y + 0x8000u) | ((uint32_t)v4.z + 0x8000u) |
+                                         ((uint32_t)v4.w + 0x8000u);
+                                uint2 pk;                                                  // low halves, 2 PRMTs
+                                pk.x = __byte_perm((uint32_t)v4.x, (uint32_t)v4.y, 0x5410);
+                                pk.y = __byte_perm((uint32_t)v4.z, (uint32_t)v4.w, 0x5410);
+                                *reinterpret_cast<uint2*>(Lk) = pk;
+                            }
+                            if (L && LW == 1) {
+                                const int4 v4 = ysum[k];
+                                rng16 |= ((uint32_t)v4.x + 0x80u) | ((uint32_t)v4.y + 0x80u) | ((uint32_t)v4.z + 0x80u) |
+                                         ((uint32_t)v4.w + 0x80u);
+                                const uint32_t lo = __byte_perm((uint32_t)v4.x, (uint32_t)v4.y, 0x0040);   // low bytes
+                                const uint32_t hi = __byte_perm((uint32_t)v4.z, (uint32_t)v4.w, 0x0040);
+                                *reinterpret_cast<uint32_t*>(Lk) = __byte_perm(lo, hi, 0x5410);
+                            }
+                            if (Edges) {                                  // strip edges: E[s] = R(128s-1), F[s] = R(128s+128)
+                                const int y = r0 + rr;
+                                const int xg = 4 * ((int)threadIdx.x + k * TILE_CHUNKS);
+                                const int64_t n1e = ((int64_t)n1 + 1) & ~(int64_t)1;   // even rows per strip block
+                                int32_t* ef = EF + ((z * nstrips) * n1e + y) * 2;
+                                if ((xg & (SE_W - 1)) == SE_W - 4 && (xg + 4) / SE_W < nstrips)
+                                    ef[(int64_t)((xg + 4) / SE_W) * n1e * 2] = rv.w;
+                                if ((xg & (SE_W - 1)) == 0) {
+                                    const int s2 = xg / SE_W;
+                                    if (s2 > 0) ef[(int64_t)(s2 - 1) * n1e * 2 + 1] = rv.x;
+                                    else {
+                                        ef[0] = 0;
+                                        ef[(int64_t)(nstrips - 1) * n1e * 2 + 1] = 0;
+                                    }
                                 }
                             }
                         }
@@ -477,7 +483,7 @@ __global__ void __maxnreg__(56) k_band_scan(const uint8_t* __restrict__ payload,
         }
         int32_t* arow = A + (z * nb + b) * (int64_t)n2;
     #pragma unroll
-        for (int k = 0; k < BS_MAXG; k++) {
+        for (int k = 0; k < KM; k++) {
             const int gi = threadIdx.x + k * TILE_CHUNKS;
             if (gi < ng) *reinterpret_cast<int4*>(arow + 4 * gi) = ysum[k];
         }
@@ -621,14 +627,22 @@ extern "C" int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t ba
     }
     const dim3 grid((unsigned)nct);
     cudaStream_t st = as_stream(stream);
-    const bool full = (n2 / 4) % TILE_CHUNKS == 0;
+    const int kmax = (int)((n2 / 4 + TILE_CHUNKS - 1) / TILE_CHUNKS);   // column groups per thread: 1, 2 or 4 (3 runs as 4)
+    const bool full = n2 / 4 == (int64_t)(kmax == 3 ? 4 : kmax) * TILE_CHUNKS;   // every thread owns all its groups
+#define HSZG_BS_K(E, LS, F, K)                                                                               \
+    do {                                                                                                     \
+        allow_smem(k_band_scan<E, LS, F, K>, smem);                                                          \
+        k_band_scan<E, LS, F, K><<<grid, TILE_CHUNKS, smem, st>>>(s->payload, s->payload_len, s->offsets,     \
+                                                                 g->n_chunks, (int)n1, (int)n2,              \
+                                                                 (int)band_rows, L_, A,                      \
+                                                                 E ? strip_edges : nullptr, l_overflow,      \
+                                                                 sbytes, (int)nb, np);                       \
+    } while (0)
 #define HSZG_BS(E, LS, F)                                                                                    \
     do {                                                                                                     \
-        allow_smem(k_band_scan<E, LS, F>, smem);                                                             \
-        k_band_scan<E, LS, F><<<grid, TILE_CHUNKS, smem, st>>>(s->payload, s->payload_len, s->offsets,        \
-                                                              g->n_chunks, (int)n1, (int)n2, (int)band_rows, \
-                                                              L_, A, E ? strip_edges : nullptr,              \
-                                                              l_overflow, sbytes, (int)nb, np);                           \
+        if (kmax == 1) HSZG_BS_K(E, LS, F, 1);                                                               \
+        else if (kmax == 2) HSZG_BS_K(E, LS, F, 2);                                                          \
+        else HSZG_BS_K(E, LS, F, 4);                                                                         \
     } while (0)
     void* L_ = L;
     if (strip_edges) {
@@ -645,6 +659,7 @@ extern "C" int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t ba
         else HSZG_BS(false, 4, false);
     }
 #undef HSZG_BS
+#undef HSZG_BS_K
     const int64_t threads = np * (n2 / 4);
     k_band_prefix<<<(unsigned)((threads + 255) / 256), 256, 0, as_stream(stream)>>>(A, (int)nb, n2, np);
     { const cudaError_t e_ = cudaGetLastError(); if (e_ != cudaSuccess) return hszg_set_cuda_error(err, e_, "band_scan"); }
