@@ -306,7 +306,7 @@ __global__ void __maxnreg__(56) k_band_scan(const uint8_t* __restrict__ payload,
                                                           int n1, int n2, int BR, void* __restrict__ L,
                                                           int32_t* __restrict__ A, int32_t* __restrict__ EF,
                                                           int32_t* __restrict__ l_ovf, uint32_t sbytes, int nb,
-                                                          int64_t np) {
+                                                          int64_t np, int nbuf) {
     uint32_t rng16 = 0;                      // OR of (value + 2^15 / 2^7) over the values stored narrow
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint32_t s_off[TILE_CHUNKS];
@@ -322,7 +322,11 @@ __global__ void __maxnreg__(56) k_band_scan(const uint8_t* __restrict__ payload,
     const int toff0 = (int)(threadIdx.x >> 3) * kChunkStride + (int)((threadIdx.x & 7) << 2);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int32_t* tile = reinterpret_cast<int32_t*>(smem);
-    uint8_t* SB = smem + kFastTileBytes;     // two staging buffers of sbytes: tile u in buffer u & 1
+    // nbuf = 2: two staging buffers of sbytes, tile u in buffer u & 1, loaded a tile ahead of the decode;
+    // nbuf = 1: one buffer (a CTA more per SM for the one-CTA-per-item grid), tile u + 1 loaded as soon as
+    // tile u is decoded, under its row scan and write-out
+    uint8_t* SB = smem + kFastTileBytes;
+    const uint32_t bmask = nbuf == 2 ? 1u : 0u, pshift = nbuf == 2 ? 1u : 0u;
     const uint32_t* words = reinterpret_cast<const uint32_t*>(SB);
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
@@ -350,7 +354,7 @@ __global__ void __maxnreg__(56) k_band_scan(const uint8_t* __restrict__ payload,
             n_hi = c1 < n_chunks ? __ldg(offsets + c1) : payload_end(offsets, n_chunks, len);
         };
         auto issue = [&](int t) {
-            const uint32_t u = (gt + (uint32_t)t) & 1;
+            const uint32_t u = (gt + (uint32_t)t) & bmask;
             const uint64_t base = n_lo & ~(uint64_t)15;
             const uint32_t bytes = (uint32_t)(((n_hi - base + 15) >> 4) << 4);
             s_base[u] = base;
@@ -373,8 +377,8 @@ __global__ void __maxnreg__(56) k_band_scan(const uint8_t* __restrict__ payload,
             const int nr = min(rpt, y1 - r0);
             const int nch = nr * cpr;
             const uint32_t u = gt + (uint32_t)t;
-            mbar_wait(&bar[u & 1], (u >> 1) & 1);
-            if (threadIdx.x == 0 && t + 1 < ntiles) {        // buffer (t+1)&1 was released at the end of t-1
+            mbar_wait(&bar[u & bmask], (u >> pshift) & 1);
+            if (nbuf == 2 && threadIdx.x == 0 && t + 1 < ntiles) {   // buffer (t+1)&1 was released at the end of t-1
                 issue(t + 1);
                 if (t + 2 < ntiles) range(t + 2);
             }
@@ -382,7 +386,7 @@ __global__ void __maxnreg__(56) k_band_scan(const uint8_t* __restrict__ payload,
             if (t + 1 < ntiles && (int)threadIdx.x < tile_nch(t + 1)) my_off = __ldg(offsets + tile_c0(t + 1) + threadIdx.x);
             uint32_t tot = 0;
             if ((int)threadIdx.x < nch) {
-                const uint32_t rel = (uint32_t)(cur_off - s_base[u & 1]) + (u & 1) * sbytes;
+                const uint32_t rel = (uint32_t)(cur_off - s_base[u & bmask]) + (u & bmask) * sbytes;
                 tot = decode32<true>(words, rel, tile + threadIdx.x * kChunkStride, 0);
             }
             // exclusive prefix of the chunk sums along each row
@@ -423,6 +427,10 @@ __global__ void __maxnreg__(56) k_band_scan(const uint8_t* __restrict__ payload,
                 s_off[threadIdx.x] = inc - tot - before;
             }
             __syncthreads();
+            if (nbuf == 1 && threadIdx.x == 0 && t + 1 < ntiles) {   // every chunk of tile t is decoded
+                issue(t + 1);
+                if (t + 2 < ntiles) range(t + 2);
+            }
             const int nstrips = (n2 + SE_W - 1) / SE_W;
             // rows of the tile.  Column group k of this thread is gi = tid + 256 k, i.e. chunk (tid >> 3) + 32 k,
             // words 4 (tid & 7) ..: a per-thread base plus compile-time offsets, advanced by uniform row
@@ -613,7 +621,15 @@ extern "C" int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t ba
     if (g->n_chunks == 0) return HSZG_OK;
     const int64_t nb = (n1 + band_rows - 1) / band_rows;
     const uint32_t sbytes = (uint32_t)((stage_bytes(s->max_bitwidth) + 15) / 16 * 16);
-    const size_t smem = kFastTileBytes + 2 * (size_t)sbytes + 16;
+    // one staging buffer when that fits one more CTA per SM for the one-CTA-per-item grid (HSZG_BS_NBUF forces it)
+    int nbuf = 2;
+    if (ctas_per_sm == 0) {
+        static const int force = getenv("HSZG_BS_NBUF") ? atoi(getenv("HSZG_BS_NBUF")) : 0;
+        const size_t per_sm = 227 * 1024;
+        const size_t s1 = kFastTileBytes + (size_t)sbytes + 16 + 2048, s2 = s1 + sbytes;   // + static and reserved
+        if (force == 1 || (force == 0 && per_sm / s1 > per_sm / s2 && per_sm / s1 <= 4)) nbuf = 1;
+    }
+    const size_t smem = kFastTileBytes + (size_t)nbuf * sbytes + 16;
     // ctas_per_sm = 0: one CTA per (band, plane), the fastest grid alone; k > 0: a persistent grid of
     // k CTAs per SM, which leaves the z-sweep beside it its SM slots (pipeline.py runs the scans of
     // later windows on a high-priority side stream under the sweeps: config-5 HSZP_ND 32.5 -> 30.9 ms)
@@ -636,7 +652,7 @@ extern "C" int hszg_band_scan(const HszgGeom* g, const HszgStream* s, int64_t ba
                                                                  g->n_chunks, (int)n1, (int)n2,              \
                                                                  (int)band_rows, L_, A,                      \
                                                                  E ? strip_edges : nullptr, l_overflow,      \
-                                                                 sbytes, (int)nb, np);                       \
+                                                                 sbytes, (int)nb, np, nbuf);                 \
     } while (0)
 #define HSZG_BS(E, LS, F)                                                                                    \
     do {                                                                                                     \
