@@ -390,24 +390,47 @@ __device__ __forceinline__ int4 ld_p2x4(const int16_t* p) {
                      (int32_t)h.y >> 16);
 }
 
-// z prefix (one band per plane: L is the plane's 2-D prefix) reduced instead of stored
-// (four columns per thread: one 16-B / 8-B load per plane; Lc % 4 == 0 and a 16-B aligned src)
-template <typename SrcT>
+// V values of a P2 row (V = 4 or 2)
+template <int V> struct P2Vec;
+template <> struct P2Vec<4> {
+    template <typename T> static __device__ __forceinline__ void ld(const T* p, int32_t* v) {
+        const int4 t = ld_p2x4(p);
+        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+    }
+};
+template <> struct P2Vec<2> {
+    static __device__ __forceinline__ void ld(const int32_t* p, int32_t* v) {
+        const int2 t = __ldg(reinterpret_cast<const int2*>(p));
+        v[0] = t.x; v[1] = t.y;
+    }
+    static __device__ __forceinline__ void ld(const int16_t* p, int32_t* v) {
+        const uint32_t h = __ldg(reinterpret_cast<const uint32_t*>(p));
+        v[0] = (int32_t)(int16_t)(h & 0xffffu); v[1] = (int32_t)h >> 16;
+    }
+};
+
+// z prefix (one band per plane: L is the plane's 2-D prefix) reduced instead of stored: V columns per
+// thread (one 16-B / 8-B / 4-B load per plane; Lc % 4 == 0 and a 16-B aligned src), U planes in flight.
+// Planes with few column groups (512^2: 65536 int4 groups = 14 warps per SM) take V = 2 in 128-thread
+// CTAs: the per-column chains (prefix, 64-bit sum, 128-bit sum of squares) are latency-bound, so twice
+// the threads with half the work each run faster (512^3: 107 -> 87 us; one column per thread: 108 us).
+template <typename SrcT, int V, int U>
 __global__ void __launch_bounds__(256) k_col_scan_sums_v4(const SrcT* __restrict__ src, int64_t M, int64_t Lc,
                                                           HszgSums* partials) {
-    const int64_t l = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+    const int64_t l = V * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
     int64_t s1 = 0;
     u128 s2 = 0;
     int mn = INT32_MAX, mx = INT32_MIN;
     if (l < Lc) {
-        uint32_t acc[4] = {0, 0, 0, 0};
-        const SrcT* c = src + l;
-        auto take = [&](int4 v) {
-            const uint32_t w[4] = {(uint32_t)v.x, (uint32_t)v.y, (uint32_t)v.z, (uint32_t)v.w};
-            uint64_t sq = 0;                    // four squares < 2^64 (|q| <= 2^31)
+        uint32_t acc[V];
 #pragma unroll
-            for (int j = 0; j < 4; j++) {
-                acc[j] += w[j];
+        for (int j = 0; j < V; j++) acc[j] = 0;
+        const SrcT* c = src + l;
+        auto take = [&](const int32_t* w) {
+            uint64_t sq = 0;                    // V squares < 2^64 (|q| <= 2^31)
+#pragma unroll
+            for (int j = 0; j < V; j++) {
+                acc[j] += (uint32_t)w[j];
                 const int q = (int)acc[j];
                 s1 += q;
                 sq += (uint64_t)((int64_t)q * q);
@@ -417,15 +440,18 @@ __global__ void __launch_bounds__(256) k_col_scan_sums_v4(const SrcT* __restrict
             s2 += (u128)sq;
         };
         int64_t m = 0;
-        for (; m + 4 <= M; m += 4) {
-            const int4 v0 = ld_p2x4(c + m * Lc), v1 = ld_p2x4(c + (m + 1) * Lc);
-            const int4 v2 = ld_p2x4(c + (m + 2) * Lc), v3 = ld_p2x4(c + (m + 3) * Lc);
-            take(v0);
-            take(v1);
-            take(v2);
-            take(v3);
+        for (; m + U <= M; m += U) {
+            int32_t v[U][V];
+#pragma unroll
+            for (int k = 0; k < U; k++) P2Vec<V>::ld(c + (m + k) * Lc, v[k]);
+#pragma unroll
+            for (int k = 0; k < U; k++) take(v[k]);
         }
-        for (; m < M; m++) take(ld_p2x4(c + m * Lc));
+        for (; m < M; m++) {
+            int32_t v[V];
+            P2Vec<V>::ld(c + m * Lc, v);
+            take(v);
+        }
     }
     Acc a;
     a.init();
@@ -434,12 +460,27 @@ __global__ void __launch_bounds__(256) k_col_scan_sums_v4(const SrcT* __restrict
     a.vmin = mn;
     a.vmax = mx;
     block_reduce(a);
-    const int64_t cols = Lc - 4 * blockIdx.x * (int64_t)blockDim.x;
-    const int64_t active = cols < 4 * (int64_t)blockDim.x ? cols : 4 * (int64_t)blockDim.x;
+    const int64_t cols = Lc - V * blockIdx.x * (int64_t)blockDim.x;
+    const int64_t active = cols < V * (int64_t)blockDim.x ? cols : V * (int64_t)blockDim.x;
     if (threadIdx.x == 0) {
         a.count = active * M;
         store_sums(partials + blockIdx.x, a);
     }
+}
+
+// launch: four columns per thread in 256-thread CTAs, or two in 128-thread CTAs for small planes
+template <typename SrcT>
+static int64_t launch_col_scan_sums(const SrcT* src, int64_t M, int64_t Lc, HszgSums* partials, cudaStream_t st) {
+    static const int force = getenv("HSZG_CSS_V") ? atoi(getenv("HSZG_CSS_V")) : 0;     // A/B runs: 2 or 4
+    const bool narrow = force ? force == 2 : Lc / 4 < (int64_t)148 * 1024;
+    if (narrow) {
+        const int64_t nb = (Lc / 2 + 127) / 128;
+        k_col_scan_sums_v4<SrcT, 2, 8><<<(unsigned)nb, 128, 0, st>>>(src, M, Lc, partials);
+        return nb;
+    }
+    const int64_t nb = (Lc / 4 + 255) / 256;
+    k_col_scan_sums_v4<SrcT, 4, 4><<<(unsigned)nb, 256, 0, st>>>(src, M, Lc, partials);
+    return nb;
 }
 
 // ---- full-chunk streams without a shared value tile (register-resident chunks) ----------------
@@ -1318,12 +1359,13 @@ static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, 
                     const int nr_ = band_scan_narrow(g, s, br, p16, A16, flag, st, err);
                     if (nr_ < 0) return -nr_;
                     if (nr_ == 1) {
+                        const unsigned cst = 256u;
                         const unsigned blocks = (unsigned)((sg.n[1] * sg.n[2] / 4 + 255) / 256);
                         if (nb == 1)
-                            k_col_scan_v4<OutT, false, int16_t><<<blocks, 256, 0, st>>>(
+                            k_col_scan_v4<OutT, false, int16_t><<<blocks, cst, 0, st>>>(
                                 p16, nullptr, sg.n[0], sg.n[1], sg.n[2], br, nb, two_eps, out, carry);
                         else
-                            k_col_scan_v4<OutT, true, int16_t><<<blocks, 256, 0, st>>>(
+                            k_col_scan_v4<OutT, true, int16_t><<<blocks, cst, 0, st>>>(
                                 p16, A16, sg.n[0], sg.n[1], sg.n[2], br, nb, two_eps, out, carry);
                         HSZG_CHECK_LAUNCH("z scan (int16)");
                         return HSZG_OK;
@@ -1337,12 +1379,13 @@ static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, 
                     const int64_t Lc = sg.n[1] * sg.n[2];
                     static const int v4 = getenv("HSZG_COLSCAN_V4") ? atoi(getenv("HSZG_COLSCAN_V4")) : 1;
                     if (v4 || carry) {      // n2 % 32 == 0: whole int4 groups, 16-byte aligned planes
+                        const unsigned cst = 256u;
                         const unsigned blocks = (unsigned)((Lc / 4 + 255) / 256);
                         if (nb == 1)
-                            k_col_scan_v4<OutT, false><<<blocks, 256, 0, st>>>(buf, nullptr, sg.n[0], sg.n[1], sg.n[2],
+                            k_col_scan_v4<OutT, false><<<blocks, cst, 0, st>>>(buf, nullptr, sg.n[0], sg.n[1], sg.n[2],
                                                                                br, nb, two_eps, out, carry);
                         else
-                            k_col_scan_v4<OutT, true><<<blocks, 256, 0, st>>>(buf, A, sg.n[0], sg.n[1], sg.n[2], br,
+                            k_col_scan_v4<OutT, true><<<blocks, cst, 0, st>>>(buf, A, sg.n[0], sg.n[1], sg.n[2], br,
                                                                               nb, two_eps, out, carry);
                     } else if (nb == 1) {   // one band per plane: A holds zeros, the plain z prefix
                         launch_col_scan<OutT>(buf, 1, sg.n[0], sg.n[1] * sg.n[2], two_eps, out, st);
@@ -1652,16 +1695,14 @@ extern "C" int hszg_quantized_sums(const HszgGeom* g, const HszgStream* s, HszgS
         const int nr_ = band_scan_narrow(g, s, sg.n[1], p16, A, flag, st, err);
         if (nr_ < 0) return -nr_;
         if (nr_ == 1) {
-            const int64_t nb4 = (Lc / 4 + 255) / 256;           // n2 % 32 == 0: Lc % 4 == 0
-            k_col_scan_sums_v4<int16_t><<<(unsigned)nb4, 256, 0, st>>>(p16, sg.n[0], Lc, partials);
+            const int64_t nb4 = launch_col_scan_sums(p16, sg.n[0], Lc, partials, st);   // n2 % 32 == 0: Lc % 4 == 0
             HSZG_CHECK_LAUNCH("quantized sums hszp-nd (int16)");
             return hszg_finalize_sums(partials, nb4, out_dev, st);
         }
     }
     const int rr = hszg_band_scan(g, s, sg.n[1], L, A, nullptr, 0, nullptr, 0, st, err);
     if (rr) return rr;
-    const int64_t nb4 = (Lc / 4 + 255) / 256;
-    k_col_scan_sums_v4<int32_t><<<(unsigned)nb4, 256, 0, st>>>(L, sg.n[0], Lc, partials);
+    const int64_t nb4 = launch_col_scan_sums(L, sg.n[0], Lc, partials, st);
     HSZG_CHECK_LAUNCH("quantized sums hszp-nd");
     return hszg_finalize_sums(partials, nb4, out_dev, st);
 }
