@@ -1055,6 +1055,59 @@ __global__ void __launch_bounds__(256) k_col_scan_v4(const SrcT* src, const int3
     }
 }
 
+// The same z prefix (no band offsets) with two columns per thread in 128-thread CTAs, eight planes in flight:
+// planes with few int4 column groups (512^2: 65536 = 13 warps per SM) leave k_col_scan_v4 latency-bound
+// (4.9 TB/s); twice the threads with half the columns each hide the load latency.
+template <typename OutT, typename SrcT>
+__global__ void __launch_bounds__(128) k_col_scan_v2(const SrcT* src, int64_t M, int64_t Lc, double two_eps, OutT* dst,
+                                                     const int32_t* __restrict__ carry) {
+    const int64_t l = 2 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+    if (l >= Lc) return;
+    const SrcT* s = src + l;
+    OutT* d = dst + l;
+    uint32_t acc[2] = {0, 0};
+    if (carry) {
+        const int2 c = __ldg(reinterpret_cast<const int2*>(carry + l));
+        acc[0] = (uint32_t)c.x;
+        acc[1] = (uint32_t)c.y;
+    }
+    auto put = [&](OutT* o) {
+        if constexpr (sizeof(OutT) == 4) {
+            OutT t[2] = {Conv<OutT>::go((int32_t)acc[0], two_eps), Conv<OutT>::go((int32_t)acc[1], two_eps)};
+            *reinterpret_cast<uint2*>(o) = *reinterpret_cast<const uint2*>(t);
+        } else {
+            *reinterpret_cast<double2*>(o) =
+                make_double2(Conv<OutT>::go((int32_t)acc[0], two_eps), Conv<OutT>::go((int32_t)acc[1], two_eps));
+        }
+    };
+    constexpr int U = 8;
+    int64_t m = 0;
+    for (; m + U <= M; m += U) {
+        int32_t v[U][2];
+#pragma unroll
+        for (int k = 0; k < U; k++) P2Vec<2>::ld(s + (m + k) * Lc, v[k]);
+#pragma unroll
+        for (int k = 0; k < U; k++) {
+            acc[0] += (uint32_t)v[k][0];
+            acc[1] += (uint32_t)v[k][1];
+            put(d + (m + k) * Lc);
+        }
+    }
+    for (; m < M; m++) {
+        int32_t v[2];
+        P2Vec<2>::ld(s + m * Lc, v);
+        acc[0] += (uint32_t)v[0];
+        acc[1] += (uint32_t)v[1];
+        put(d + m * Lc);
+    }
+}
+
+// small planes take the two-column kernel (HSZG_CS_V=4 forces the four-column one for A/B runs)
+inline bool col_scan_narrow(int64_t Lc) {
+    static const int force = getenv("HSZG_CS_V") ? atoi(getenv("HSZG_CS_V")) : 0;
+    return force ? force == 2 : Lc / 4 < (int64_t)148 * 1024;
+}
+
 // Few, long columns (e.g. the y pass of a 2-D field: 3600 columns of 1800): S threads per column
 // scan S segments — sums, an exclusive prefix across the segments in shared memory, then the
 // segment rescans (re-read from L2) — so the launch has ~150k threads instead of one per column.
@@ -1361,7 +1414,10 @@ static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, 
                     if (nr_ == 1) {
                         const unsigned cst = 256u;
                         const unsigned blocks = (unsigned)((sg.n[1] * sg.n[2] / 4 + 255) / 256);
-                        if (nb == 1)
+                        if (nb == 1 && col_scan_narrow(sg.n[1] * sg.n[2]))
+                            k_col_scan_v2<OutT, int16_t><<<(unsigned)((sg.n[1] * sg.n[2] / 2 + 127) / 128), 128, 0, st>>>(
+                                p16, sg.n[0], sg.n[1] * sg.n[2], two_eps, out, carry);
+                        else if (nb == 1)
                             k_col_scan_v4<OutT, false, int16_t><<<blocks, cst, 0, st>>>(
                                 p16, nullptr, sg.n[0], sg.n[1], sg.n[2], br, nb, two_eps, out, carry);
                         else
@@ -1381,7 +1437,10 @@ static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, 
                     if (v4 || carry) {      // n2 % 32 == 0: whole int4 groups, 16-byte aligned planes
                         const unsigned cst = 256u;
                         const unsigned blocks = (unsigned)((Lc / 4 + 255) / 256);
-                        if (nb == 1)
+                        if (nb == 1 && col_scan_narrow(Lc))
+                            k_col_scan_v2<OutT, int32_t><<<(unsigned)((Lc / 2 + 127) / 128), 128, 0, st>>>(
+                                buf, sg.n[0], Lc, two_eps, out, carry);
+                        else if (nb == 1)
                             k_col_scan_v4<OutT, false><<<blocks, cst, 0, st>>>(buf, nullptr, sg.n[0], sg.n[1], sg.n[2],
                                                                                br, nb, two_eps, out, carry);
                         else
