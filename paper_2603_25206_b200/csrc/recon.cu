@@ -1058,13 +1058,22 @@ __global__ void __launch_bounds__(256) k_col_scan_v4(const SrcT* src, const int3
 // The same z prefix (no band offsets) with two columns per thread in 128-thread CTAs, eight planes in flight:
 // planes with few int4 column groups (512^2: 65536 = 13 warps per SM) leave k_col_scan_v4 latency-bound
 // (4.9 TB/s); twice the threads with half the columns each hide the load latency.
-template <typename OutT, typename SrcT>
+template <typename OutT, typename SrcT, bool BANDS = false>
 __global__ void __launch_bounds__(128) k_col_scan_v2(const SrcT* src, int64_t M, int64_t Lc, double two_eps, OutT* dst,
-                                                     const int32_t* __restrict__ carry) {
+                                                     const int32_t* __restrict__ carry,
+                                                     const int32_t* __restrict__ A = nullptr, int64_t n2 = 1,
+                                                     int64_t BR = 1, int64_t nb = 1) {
     const int64_t l = 2 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
     if (l >= Lc) return;
     const SrcT* s = src + l;
     OutT* d = dst + l;
+    const int32_t* a = A;                        // BANDS: + the exclusive band offsets A[z][y / BR][x] per plane
+    int64_t as = 0;
+    if constexpr (BANDS) {
+        const int64_t y = l / n2, x = l - y * n2;
+        a = A + (y / BR) * n2 + x;
+        as = nb * n2;
+    }
     uint32_t acc[2] = {0, 0};
     if (carry) {
         const int2 c = __ldg(reinterpret_cast<const int2*>(carry + l));
@@ -1085,7 +1094,14 @@ __global__ void __launch_bounds__(128) k_col_scan_v2(const SrcT* src, int64_t M,
     for (; m + U <= M; m += U) {
         int32_t v[U][2];
 #pragma unroll
-        for (int k = 0; k < U; k++) P2Vec<2>::ld(s + (m + k) * Lc, v[k]);
+        for (int k = 0; k < U; k++) {
+            P2Vec<2>::ld(s + (m + k) * Lc, v[k]);
+            if constexpr (BANDS) {
+                const int2 o = __ldg(reinterpret_cast<const int2*>(a + (m + k) * as));
+                v[k][0] += o.x;
+                v[k][1] += o.y;
+            }
+        }
 #pragma unroll
         for (int k = 0; k < U; k++) {
             acc[0] += (uint32_t)v[k][0];
@@ -1096,6 +1112,11 @@ __global__ void __launch_bounds__(128) k_col_scan_v2(const SrcT* src, int64_t M,
     for (; m < M; m++) {
         int32_t v[2];
         P2Vec<2>::ld(s + m * Lc, v);
+        if constexpr (BANDS) {
+            const int2 o = __ldg(reinterpret_cast<const int2*>(a + m * as));
+            v[0] += o.x;
+            v[1] += o.y;
+        }
         acc[0] += (uint32_t)v[0];
         acc[1] += (uint32_t)v[1];
         put(d + m * Lc);
@@ -1420,6 +1441,9 @@ static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, 
                         else if (nb == 1)
                             k_col_scan_v4<OutT, false, int16_t><<<blocks, cst, 0, st>>>(
                                 p16, nullptr, sg.n[0], sg.n[1], sg.n[2], br, nb, two_eps, out, carry);
+                        else if (col_scan_narrow(sg.n[1] * sg.n[2]))
+                            k_col_scan_v2<OutT, int16_t, true><<<(unsigned)((sg.n[1] * sg.n[2] / 2 + 127) / 128), 128, 0, st>>>(
+                                p16, sg.n[0], sg.n[1] * sg.n[2], two_eps, out, carry, A16, sg.n[2], br, nb);
                         else
                             k_col_scan_v4<OutT, true, int16_t><<<blocks, cst, 0, st>>>(
                                 p16, A16, sg.n[0], sg.n[1], sg.n[2], br, nb, two_eps, out, carry);
@@ -1443,6 +1467,9 @@ static int reconstruct_typed(const HszgGeom* g, const HszgStream* s, OutT* out, 
                         else if (nb == 1)
                             k_col_scan_v4<OutT, false><<<blocks, cst, 0, st>>>(buf, nullptr, sg.n[0], sg.n[1], sg.n[2],
                                                                                br, nb, two_eps, out, carry);
+                        else if (col_scan_narrow(Lc))
+                            k_col_scan_v2<OutT, int32_t, true><<<(unsigned)((Lc / 2 + 127) / 128), 128, 0, st>>>(
+                                buf, sg.n[0], Lc, two_eps, out, carry, A, sg.n[2], br, nb);
                         else
                             k_col_scan_v4<OutT, true><<<blocks, cst, 0, st>>>(buf, A, sg.n[0], sg.n[1], sg.n[2], br,
                                                                               nb, two_eps, out, carry);
